@@ -1,0 +1,192 @@
+/*
+ * riga_b200.h — C ABI of libriga_b200.so, the B200 (sm_100a) engine behind
+ * the drop-in Python API of paper_2009_08167_b200.
+ *
+ * The reference (rigaeig v0.1.0, /root/reference/pkg/src/rigaeig) has no FFI:
+ * its boundary is the set of Python functions in sparsela.py/eigensolver.py,
+ * one level above three numba kernels.  Each entry point below names the
+ * reference interface it replaces.  ctypes binds this header
+ * (paper_2009_08167_b200/_lib.py; INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - every call returns an int status (never throws across the ABI):
+ *      0 RIGA_OK, 1 RIGA_ZERO_PIVOT, 2 RIGA_BAD_ARG, 3 RIGA_CUDA_ERROR,
+ *      4 RIGA_OOM, 5 RIGA_BREAKDOWN (Lanczos invariant subspace), 6 RIGA_NO_DEVICE;
+ *    riga_last_error() gives the message of the last failure (thread-local).
+ *  - "host" pointers are plain CPU memory; "dev" pointers are device memory
+ *    on the handle's device (e.g. torch tensor data_ptr()).
+ *  - handles are opaque, owned by the library, freed by riga_*_destroy; each
+ *    handle is bound to one device and one CUDA stream and must not be used
+ *    from two host threads at once; different handles may run concurrently.
+ *  - indices: CSR row pointers int64, column indices int32; permutations
+ *    int64 with position k holding the original index eliminated k-th
+ *    (reference separator_ordering convention, sparsela.py:319-330).
+ */
+#ifndef RIGA_B200_H
+#define RIGA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  RIGA_OK = 0,
+  RIGA_ZERO_PIVOT = 1,
+  RIGA_BAD_ARG = 2,
+  RIGA_CUDA_ERROR = 3,
+  RIGA_OOM = 4,
+  RIGA_BREAKDOWN = 5,
+  RIGA_NO_DEVICE = 6
+};
+
+typedef struct riga_ctx riga_ctx;
+typedef struct riga_system riga_system;
+typedef struct riga_symbolic riga_symbolic;
+typedef struct riga_factor riga_factor;
+typedef struct riga_lanczos riga_lanczos;
+
+/* ---- library / context ------------------------------------------------ */
+const char* riga_last_error(void);
+int riga_version(void);
+/* Number of CUDA devices visible (0 on a CPU-only host). */
+int riga_device_count(int* count);
+/* Context = (device, stream).  stream_handle: 0 -> create a private
+ * non-blocking stream; otherwise a cudaStream_t owned by the caller. */
+int riga_ctx_create(int device, void* stream_handle, riga_ctx** out);
+int riga_ctx_destroy(riga_ctx* ctx);
+int riga_ctx_synchronize(riga_ctx* ctx);
+/* Raw cudaStream_t of the context (for torch.cuda.ExternalStream). */
+int riga_ctx_stream(riga_ctx* ctx, void** stream_out);
+
+/* ---- system: device CSR of K and M on one shared pattern ------------------
+ * Replaces the scipy CSR pair of DiscreteSystem (ref assembly.py:24-62).   */
+int riga_system_upload(riga_ctx* ctx, int64_t n, int64_t nnz, const int64_t* rowptr_host,
+                       const int32_t* colidx_host, const double* K_host, const double* M_host,
+                       riga_system** out);
+/* Device assembly of the Kronecker-composed Dirichlet-reduced pencil from
+ * 1D banded CSR matrices (ref assembly.py:139-192 kron_assemble).  dim in
+ * {1,2,3}; per direction t (x, y, z): n1[t], rowptr1[t], colidx1[t],
+ * k1[t], m1[t] (host).  Values are bit-identical to scipy's kron/+ (product
+ * and sum order fixed, no FMA contraction).                                 */
+int riga_system_assemble_kron(riga_ctx* ctx, int dim, const int64_t* n1,
+                              const int64_t* const* rowptr1, const int32_t* const* colidx1,
+                              const double* const* k1, const double* const* m1,
+                              riga_system** out);
+int riga_system_info(riga_system* sys, int64_t* n, int64_t* nnz);
+int riga_system_download(riga_system* sys, int64_t* rowptr_host, int32_t* colidx_host,
+                         double* K_host, double* M_host);
+/* Device pointers (for callers that keep data on the device). */
+int riga_system_device_ptrs(riga_system* sys, const int64_t** rowptr, const int32_t** colidx,
+                            const double** K, const double** M);
+int riga_system_destroy(riga_system* sys);
+
+/* y = A x on the device, A = K (which=0), M (which=1) or K - sigma M (2).
+ * Replaces mass_matvec (ref sparsela.py:280-290, scipy csr_matvec).        */
+int riga_spmv(riga_system* sys, int which, double sigma, const double* x_dev, double* y_dev);
+/* Generic device CSR SpMV on caller arrays (any square CSR, e.g. a plain
+ * scipy matrix handed to mass_matvec).                                     */
+int riga_csr_spmv(riga_ctx* ctx, int64_t n, const int64_t* rowptr_dev, const int32_t* colidx_dev,
+                  const double* val_dev, const double* x_dev, double* y_dev);
+
+/* ---- symbolic analysis (host C++, once per pattern + ordering) ----------
+ * Replaces the per-call permute/triu/_etree_counts of factor_ldl
+ * (ref sparsela.py:239-250, _etree_counts :100-115): elimination tree,
+ * postorder, column counts, fundamental + relaxed supernodes, frontal row
+ * structures, extend-add maps, tree levels.  fill_nnz and factor_flops
+ * are the reference's exact (unamalgamated) counts: nnz(L)+n and
+ * sum (colcount)^2 (ref sparsela.py:257-258).                              */
+int riga_symbolic_create(riga_system* sys, const int64_t* perm_host, riga_symbolic** out);
+/* Host-only analysis of a pattern (no device needed; used by CPU tests). */
+int riga_symbolic_analyze(int64_t n, const int64_t* rowptr_host, const int32_t* colidx_host,
+                          const int64_t* perm_host, riga_symbolic** out);
+/* stats[0..15]: fill_nnz, factor_flops, n_supernodes, max_front, n_levels,
+ * panel_entries, cb_entries, max_ncol, fundamental_supernodes,
+ * stored_L_entries, n_small_fronts, n_large_fronts, nnz_lower,
+ * tree_height, relaxed_flops (padded dense-front flop count), reserved. */
+int riga_symbolic_stats(riga_symbolic* sym, int64_t* stats16);
+/* Elimination order actually used (postordered copy of perm), int64[n]. */
+int riga_symbolic_order(riga_symbolic* sym, int64_t* order_host);
+/* Exact column counts of L (diagonal included) in the caller's perm order. */
+int riga_symbolic_colcounts(riga_symbolic* sym, int64_t* counts_host);
+int riga_symbolic_destroy(riga_symbolic* sym);
+
+/* ---- numeric multifrontal LDL^T of K - sigma M --------------------------
+ * Replaces factor_ldl + _ldl_numeric (ref sparsela.py:212-262, :118-159):
+ * unpivoted, zero_tol = rel_zero_tol * max|K - sigma M| computed on the
+ * device; inertia from the signs of D.  Status RIGA_ZERO_PIVOT when some
+ * |d_k| < zero_tol; *bad_pivot = the smallest such elimination position.
+ * The factor is allocated on the symbolic handle's device and stream.      */
+int riga_factor(riga_symbolic* sym, double sigma, double rel_zero_tol, riga_factor** out,
+                int64_t* n_negative, int64_t* bad_pivot);
+/* Same, for a caller-given symmetric matrix on the same pattern (values
+ * host, CSR order of the system) -- factor_ldl(A) for arbitrary A.       */
+int riga_factor_values(riga_symbolic* sym, const double* values_host, double rel_zero_tol,
+                       riga_factor** out, int64_t* n_negative, int64_t* bad_pivot);
+/* x = A^{-1} b, b and x device vectors in ORIGINAL numbering (may alias).
+ * Replaces solve_fb + _ldl_solve (ref sparsela.py:265-277, :162-175).      */
+int riga_factor_solve(riga_factor* f, const double* b_dev, double* x_dev);
+/* Timing of the last numeric factorization on the device (ms). */
+int riga_factor_time_ms(riga_factor* f, float* ms);
+/* D in elimination order (host double[n]). */
+int riga_factor_D(riga_factor* f, double* D_host);
+/* Supernodal L as CSC (unit diagonal excluded) in elimination order
+ * riga_symbolic_order(); Lp int64[n+1]; sizes from stats[9]
+ * (stored_L_entries).  For the reference's LDLFactorization.l_matrix()
+ * test hooks (ref sparsela.py:199-203).                                    */
+int riga_factor_export(riga_factor* f, int64_t* Lp_host, int32_t* Li_host, double* Lx_host);
+int riga_factor_destroy(riga_factor* f);
+
+/* ---- device Lanczos (shift-invert, CGS2 full reorthogonalisation) ------
+ * Replaces LanczosState / lanczos_extend / lift / thick_restart
+ * (ref eigensolver.py:140-357).  The basis V, its mass products MV
+ * (row-major, max_dim+1 rows of n) and the locked set live on the device;
+ * the host keeps T, coupling and all decisions.                            */
+int riga_lanczos_create(riga_system* sys, int64_t max_dim, riga_lanczos** out);
+int riga_lanczos_destroy(riga_lanczos* lz);
+/* Operator for the next extend: H = (K - shift M)^{-1} M via factor f.     */
+int riga_lanczos_set_operator(riga_lanczos* lz, riga_factor* f);
+/* Current basis size k (host view). */
+int riga_lanczos_k(riga_lanczos* lz, int64_t* k);
+/* Set the pending direction r from a host vector: Mr = M r, M-normalise.
+ * Status RIGA_BAD_ARG when the mass norm is zero (ref :188-195).          */
+int riga_lanczos_set_start(riga_lanczos* lz, const double* r_host);
+/* Fresh random direction (host-drawn r, ref _fresh_direction :214-227):
+ * ref_norm = sqrt(r M r); CGS2 against V[:k] and the locked set; accept if
+ * the new mass norm > 1e-8 max(ref_norm, 1e-300).  *accepted = 0/1.       */
+int riga_lanczos_fresh(riga_lanczos* lz, const double* r_host, int* accepted);
+/* Append a locked pair (device vectors x, Mx of length n). */
+int riga_lanczos_lock(riga_lanczos* lz, const double* x_dev, const double* mx_dev);
+int riga_lanczos_locked_count(riga_lanczos* lz, int64_t* count);
+/* Run Lanczos steps until k == limit or a breakdown (ref step :235-268).
+ * coupling_host: the arrowhead row coupling[:k] to apply on the first step
+ * (NULL = none).  Per executed step i: alpha[i], beta[i], wnorm[i] (host).
+ * *steps = steps executed; status RIGA_BREAKDOWN if the last step broke
+ * down (k already advanced, as in the reference).                          */
+int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_host,
+                        double breakdown_tol, double* alpha, double* beta, double* wnorm,
+                        int64_t* steps);
+/* X = V[:k]^T W, MX = MV[:k]^T W for c weight columns (W host, k x c,
+ * column-major), written as c rows of n into X_dev / MX_dev (ref lift
+ * :270-274, batched over the converged pairs of a cycle).                 */
+int riga_lanczos_lift(riga_lanczos* lz, const double* W_host, int64_t c, double* X_dev, double* MX_dev);
+/* Thick restart: V[:c] <- (V[:k]^T W)^T, MV likewise, k <- c; the pending
+ * residual direction is kept (ref thick_restart :326-357).                 */
+int riga_lanczos_restart(riga_lanczos* lz, const double* W_host, int64_t c);
+/* In-place projection of (x, mx) against the locked set, `passes` times:
+ * c = LM x; x -= L^T c; mx -= LM^T c (ref _sweep locking block :491-505).  */
+int riga_lanczos_project_locked(riga_lanczos* lz, double* x_dev, double* mx_dev, int passes);
+/* Gram matrix G = V[:k] MV[:k]^T to host (k x k row-major) for the
+ * DEBUG_INVARIANTS checks (ref check_invariants :276-282).                 */
+int riga_lanczos_gram(riga_lanczos* lz, double* G_host);
+/* Device pointers of V and MV (row-major, leading dimension *ld). */
+int riga_lanczos_basis(riga_lanczos* lz, double** V, double** MV, int64_t* ld);
+
+/* ---- dense vector helpers on the device (stream of ctx) ----------------- */
+int riga_dot(riga_ctx* ctx, int64_t n, const double* x_dev, const double* y_dev, double* out_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RIGA_B200_H */

@@ -1,0 +1,101 @@
+// Shared internals of libriga_b200.so (host + device).
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/riga_b200.h"
+
+namespace riga {
+
+// thread-local last error message (riga_last_error)
+void set_error(const std::string& msg);
+const char* last_error();
+
+#define RIGA_CHECK_ARG(cond, msg)          \
+  do {                                     \
+    if (!(cond)) {                         \
+      ::riga::set_error(msg);              \
+      return RIGA_BAD_ARG;                 \
+    }                                      \
+  } while (0)
+
+#define RIGA_CUDA(call)                                                                  \
+  do {                                                                                   \
+    cudaError_t _e = (call);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      ::riga::set_error(std::string("CUDA error ") + cudaGetErrorString(_e) + " at " +   \
+                        __FILE__ + ":" + std::to_string(__LINE__));                      \
+      return _e == cudaErrorMemoryAllocation ? RIGA_OOM : RIGA_CUDA_ERROR;               \
+    }                                                                                    \
+  } while (0)
+
+#define RIGA_TRY(call)              \
+  do {                              \
+    int _s = (call);                \
+    if (_s != RIGA_OK) return _s;   \
+  } while (0)
+
+// Device buffer with RAII release (allocated on the owner's device).
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  int alloc(size_t count) {
+    release();
+    if (count == 0) return RIGA_OK;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      set_error(std::string("cudaMalloc of ") + std::to_string(count * sizeof(T)) +
+                " bytes failed: " + cudaGetErrorString(e));
+      return e == cudaErrorMemoryAllocation ? RIGA_OOM : RIGA_CUDA_ERROR;
+    }
+    n = count;
+    return RIGA_OK;
+  }
+  int upload(const T* host, size_t count, cudaStream_t s) {
+    int st = alloc(count);
+    if (st) return st;
+    if (count) RIGA_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    return RIGA_OK;
+  }
+};
+
+}  // namespace riga
+
+struct riga_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double* scratch_host = nullptr;  // pinned scratch for small D2H reads
+  double* scratch_dev = nullptr;   // small device scratch (reductions)
+  size_t scratch_dev_n = 0;
+};
+
+// Device guard: sets the current device for the scope.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};

@@ -1,0 +1,78 @@
+// Handle definitions shared by the translation units of libriga_b200.so.
+#pragma once
+
+#include <memory>
+
+#include "common.h"
+#include "symbolic.h"
+
+struct riga_system {
+  riga_ctx* ctx = nullptr;
+  int64_t n = 0, nnz = 0;
+  riga::DevBuf<int64_t> rowptr;
+  riga::DevBuf<int32_t> colidx;
+  riga::DevBuf<double> K, M;
+};
+
+// Device copy of the symbolic analysis (read-only, shared by all factors).
+struct SymDev {
+  const int64_t *col0, *ncol, *front, *rows_off, *panel_off, *cb_off, *upd_off;
+  const int64_t *child_ptr, *asm_ptr;
+  const int32_t *sparent, *rows, *relpos, *child_list, *asm_slot, *asm_local;
+  const int32_t *level_nodes, *order;
+};
+
+struct LevelPlan {
+  int64_t begin = 0, nsmall = 0, nlarge = 0;  // offsets into level_nodes
+  // small fronts: contiguous classes [cls_begin[c], cls_begin[c+1]) with max front cls_f[c]
+  std::vector<int64_t> cls_begin;
+  std::vector<int32_t> cls_f;
+  int64_t max_np_large = 0, max_f_large = 0, max_nu_large = 0;
+  // extend-add rounds into large parents: ranges into ea_items (device)
+  std::vector<int64_t> ea_round_begin;  // size rounds+1
+  std::vector<int64_t> ea_round_maxnu;
+  int64_t max_f = 0, max_np = 0;
+};
+
+struct riga_symbolic {
+  riga_ctx* ctx = nullptr;
+  riga_system* sys = nullptr;  // may be null (host-only analysis)
+  riga::SymbolicHost h;
+  std::vector<LevelPlan> plan;
+  std::vector<int32_t> ea_items_host;  // child ids, grouped by (level, round)
+  bool on_device = false;
+  // device arrays
+  riga::DevBuf<int64_t> d_col0, d_ncol, d_front, d_rows_off, d_panel_off, d_cb_off, d_upd_off;
+  riga::DevBuf<int64_t> d_child_ptr, d_asm_ptr;
+  riga::DevBuf<int32_t> d_sparent, d_rows, d_relpos, d_child_list, d_asm_slot, d_asm_local;
+  riga::DevBuf<int32_t> d_level_nodes, d_order, d_ea_items, d_large_nodes;
+  int64_t n_large = 0;
+  SymDev dev() const {
+    return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,
+                  d_cb_off.p,   d_upd_off.p,   d_child_ptr.p,  d_asm_ptr.p,    d_sparent.p,
+                  d_rows.p,     d_relpos.p,    d_child_list.p, d_asm_slot.p,   d_asm_local.p,
+                  d_level_nodes.p, d_order.p};
+  }
+};
+
+struct riga_factor {
+  riga_ctx* ctx = nullptr;
+  riga_symbolic* sym = nullptr;
+  double sigma = 0.0;
+  riga::DevBuf<double> panel;  // all L panels (f x np, ld f)
+  riga::DevBuf<double> D;      // pivots in elimination order
+  riga::DevBuf<double> xperm;  // solve workspace (n)
+  riga::DevBuf<double> upd;    // solve contribution vectors (sum n_u)
+  riga::DevBuf<int64_t> stat;  // [0] n_negative, [1] first bad pivot (n if none)
+  riga::DevBuf<double> tol;    // [0] max|A|, [1] zero_tol
+  float factor_ms = 0.f;
+};
+
+namespace riga {
+// kernels shared between translation units
+int launch_dot(cudaStream_t s, int64_t n, const double* x, const double* y, double* out_dev);
+int system_spmv(riga_system* sys, cudaStream_t s, int which, double sigma, const double* x, double* y);
+int csr_spmv(cudaStream_t s, int64_t n, const int64_t* rowptr, const int32_t* colidx,
+             const double* val, const double* x, double* y);
+int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x);
+}  // namespace riga

@@ -1,0 +1,62 @@
+// FP64 peak probe: DMMA (mma.sync m8n8k4 f64) and DFMA register-only loops.
+// Used once to measure the roofline denominator for the LDL^T frontal updates.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void dmma_loop(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { c[i][0] = 0.0; c[i][1] = 0.0; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
+__global__ void dfma_loop(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i] = i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = fma(a, c[i], b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
+int main() {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  double* out; cudaMalloc(&out, 4096 * sizeof(double));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int warps = 4; warps <= 16; warps *= 2) {
+    int threads = warps * 32; int iters = 20000;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      dmma_loop<<<sms * 2, threads>>>(out, iters);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      double flops = 2.0 * sms * threads / 32 * iters * 8 * 512.0;
+      if (rep) printf("DMMA warps/CTA=%d: %.2f TFLOP/s (%.3f ms)\n", warps, flops / ms / 1e9, ms);
+      cudaEventRecord(e0);
+      dfma_loop<<<sms * 2, threads>>>(out, iters);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      flops = 2.0 * sms * threads * (double)iters * 8 * 2.0;
+      if (rep) printf("DFMA warps/CTA=%d: %.2f TFLOP/s (%.3f ms)\n", warps, flops / ms / 1e9, ms);
+    }
+  }
+  printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
