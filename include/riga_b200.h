@@ -117,12 +117,9 @@ int riga_symbolic_destroy(riga_symbolic* sym);
  * unpivoted, zero_tol = rel_zero_tol * max|K - sigma M| computed on the
  * device; inertia from the signs of D.  Status RIGA_ZERO_PIVOT when some
  * |d_k| < zero_tol; *bad_pivot = the smallest such elimination position.
- * The factor is allocated on the symbolic handle's device and stream.      */
-int riga_factor(riga_symbolic* sym, double sigma, double rel_zero_tol, riga_factor** out,
-                int64_t* n_negative, int64_t* bad_pivot);
-/* Same, for a caller-given symmetric matrix on the same pattern (values
- * host, CSR order of the system) -- factor_ldl(A) for arbitrary A.       */
-int riga_factor_values(riga_symbolic* sym, const double* values_host, double rel_zero_tol,
+ * ctx selects the stream (NULL = the symbolic handle's context); the
+ * factor stays bound to that context.                                      */
+int riga_factor_create(riga_ctx* ctx, riga_symbolic* sym, double sigma, double rel_zero_tol,
                        riga_factor** out, int64_t* n_negative, int64_t* bad_pivot);
 /* x = A^{-1} b, b and x device vectors in ORIGINAL numbering (may alias).
  * Replaces solve_fb + _ldl_solve (ref sparsela.py:265-277, :162-175).      */
@@ -142,8 +139,10 @@ int riga_factor_destroy(riga_factor* f);
  * Replaces LanczosState / lanczos_extend / lift / thick_restart
  * (ref eigensolver.py:140-357).  The basis V, its mass products MV
  * (row-major, max_dim+1 rows of n) and the locked set live on the device;
- * the host keeps T, coupling and all decisions.                            */
-int riga_lanczos_create(riga_system* sys, int64_t max_dim, riga_lanczos** out);
+ * the host keeps T, coupling and all decisions.  mass = NULL selects the
+ * Euclidean inner product (ref LanczosState(mass=None)).                   */
+int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max_dim,
+                        riga_lanczos** out);
 int riga_lanczos_destroy(riga_lanczos* lz);
 /* Operator for the next extend: H = (K - shift M)^{-1} M via factor f.     */
 int riga_lanczos_set_operator(riga_lanczos* lz, riga_factor* f);
@@ -167,6 +166,11 @@ int riga_lanczos_locked_count(riga_lanczos* lz, int64_t* count);
 int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_host,
                         double breakdown_tol, double* alpha, double* beta, double* wnorm,
                         int64_t* steps);
+/* One step with a caller-computed w = H v (device vector of length n), for
+ * operators that are not a device factor (ref LanczosState(apply_op=...)
+ * with an arbitrary callable).  Outputs as riga_lanczos_extend (1 step).   */
+int riga_lanczos_step_given(riga_lanczos* lz, const double* w_dev, const double* coupling_host,
+                            double breakdown_tol, double* alpha, double* beta, double* wnorm);
 /* X = V[:k]^T W, MX = MV[:k]^T W for c weight columns (W host, k x c,
  * column-major), written as c rows of n into X_dev / MX_dev (ref lift
  * :270-274, batched over the converged pairs of a cycle).                 */

@@ -1,0 +1,793 @@
+// Multifrontal supernodal LDL^T of K - sigma M and the supernodal solves.
+//
+//  riga_factor       <- factor_ldl + _ldl_numeric  ref sparsela.py:212-262, :118-159
+//  riga_factor_solve <- solve_fb + _ldl_solve      ref sparsela.py:265-277, :162-175
+//
+// Schedule (per factorization, all on one stream, level by level bottom-up):
+//   k_tol            zero_tol = rel * max|K - sigma M| (device reduction)
+//   k_asm_large      original entries -> panels of the large fronts
+//   per level:
+//     k_extend_add   child update blocks -> large parent fronts (rounds of
+//                    distinct parents, so no atomics and a fixed order)
+//     k_small_front  one CTA per front with f <= kSmallFront: the whole front
+//                    (originals + children) in shared memory, dense LDL^T of
+//                    the pivot block, Schur complement written back
+//     large fronts   right-looking blocked LDL^T in HBM: k_panel (diagonal
+//                    block + L21 rows), k_syrk<0> (trailing panel update)
+//                    and k_syrk<1> (update block -= L21 D L21^T, K = n_p),
+//                    both on FP64 tensor cores (mma.sync m8n8k4 -> DMMA)
+// Inertia = count of negative pivots (integer atomics, order independent).
+#include <algorithm>
+#include <cstring>
+
+#include "dmma.cuh"
+#include "internal.h"
+#include "kernels.cuh"
+
+namespace riga {
+
+constexpr int kNB = 32;         // panel block width of the large-front path
+constexpr int kPanelRows = 128;  // rows per CTA in k_panel
+
+// ---------------------------------------------------------------------------
+__global__ void k_tol(int64_t nnz, const double* __restrict__ K, const double* __restrict__ M,
+                      double sigma, double rel, double* __restrict__ partial,
+                      unsigned* __restrict__ ticket, double* __restrict__ tol,
+                      int64_t* __restrict__ stat, int64_t n) {
+  __shared__ double red[32];
+  __shared__ bool last;
+  double m = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+       q += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(__dsub_rn(K[q], __dmul_rn(sigma, M[q]))));
+  m = block_max(m, red);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = m;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+      t = fmax(t, ((volatile double*)partial)[i]);
+    t = block_max(t, red);
+    if (threadIdx.x == 0) {
+      tol[0] = t;
+      tol[1] = rel * t;
+      stat[0] = 0;
+      stat[1] = n;
+      *ticket = 0u;
+    }
+  }
+}
+
+__global__ void k_asm_large(SymDev S, const int32_t* __restrict__ nodes,
+                            const double* __restrict__ K, const double* __restrict__ M,
+                            double sigma, double* __restrict__ panel) {
+  int s = nodes[blockIdx.x];
+  double* P = panel + S.panel_off[s];
+  for (int64_t e = S.asm_ptr[s] + threadIdx.x; e < S.asm_ptr[s + 1]; e += blockDim.x) {
+    int32_t q = S.asm_slot[e];
+    P[S.asm_local[e]] = __dsub_rn(K[q], __dmul_rn(sigma, M[q]));
+  }
+}
+
+// child update block (lower triangle, ld nu_c) scatter-added into the parent
+__global__ void k_extend_add(SymDev S, const int32_t* __restrict__ items,
+                             double* __restrict__ panel, double* __restrict__ cb) {
+  int c = items[blockIdx.y];
+  int p = S.sparent[c];
+  int64_t nuc = S.front[c] - S.ncol[c];
+  int64_t fp = S.front[p], npp = S.ncol[p], nup = fp - npp;
+  const double* src = cb + S.cb_off[c];
+  const int32_t* rp = S.relpos + S.upd_off[c];
+  double* P = panel + S.panel_off[p];
+  double* C = cb + S.cb_off[p];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t b0 = (int64_t)blockIdx.x * 32;
+  for (int64_t b = b0 + w; b < min(b0 + 32, nuc); b += nw) {
+    int64_t rb = rp[b];
+    for (int64_t a = b + lane; a < nuc; a += 32) {
+      int64_t ra = rp[a];
+      double v = src[b * nuc + a];
+      if (rb < npp)
+        P[rb * fp + ra] += v;
+      else
+        C[(rb - npp) * nup + (ra - npp)] += v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Small fronts: whole front in shared memory (column-major, odd ld).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_small_front(SymDev S, const int32_t* __restrict__ nodes,
+                                                     const double* __restrict__ K,
+                                                     const double* __restrict__ M, double sigma,
+                                                     const double* __restrict__ tol,
+                                                     double* __restrict__ panel,
+                                                     double* __restrict__ cb,
+                                                     double* __restrict__ D,
+                                                     int64_t* __restrict__ stat) {
+  extern __shared__ double F[];
+  const int s = nodes[blockIdx.x];
+  const int f = (int)S.front[s], np = (int)S.ncol[s], nu = f - np;
+  const int ld = f | 1;
+  const int64_t col0 = S.col0[s];
+  double* lb0 = F + f * ld;
+  double* lb1 = lb0 + f;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  for (int i = tid; i < f * ld; i += blockDim.x) F[i] = 0.0;
+  __syncthreads();
+  for (int64_t e = S.asm_ptr[s] + tid; e < S.asm_ptr[s + 1]; e += blockDim.x) {
+    int loc = S.asm_local[e];
+    int col = loc / f, row = loc - col * f;
+    int32_t q = S.asm_slot[e];
+    F[col * ld + row] = __dsub_rn(K[q], __dmul_rn(sigma, M[q]));
+  }
+  __syncthreads();
+  for (int64_t t = S.child_ptr[s]; t < S.child_ptr[s + 1]; ++t) {
+    int c = S.child_list[t];
+    int nuc = (int)(S.front[c] - S.ncol[c]);
+    const double* src = cb + S.cb_off[c];
+    const int32_t* rp = S.relpos + S.upd_off[c];
+    for (int b = w; b < nuc; b += nw) {
+      int rb = rp[b];
+      for (int a = b + lane; a < nuc; a += 32) F[rb * ld + rp[a]] += src[b * nuc + a];
+    }
+    __syncthreads();
+  }
+  const double tv = tol[1];
+  int neg = 0;
+  int64_t bad = INT64_MAX;
+  for (int k = 0; k < np; ++k) {
+    double* lb = (k & 1) ? lb1 : lb0;
+    const double d = F[k * ld + k];
+    if (tid == 0) {
+      D[col0 + k] = d;
+      if (d < 0.0) neg++;
+      if (fabs(d) < tv && bad == INT64_MAX) bad = col0 + k;
+    }
+    for (int i = k + 1 + tid; i < f; i += blockDim.x) lb[i] = F[k * ld + i] / d;
+    __syncthreads();
+    for (int j = k + 1 + w; j < f; j += nw) {
+      const double cj = F[k * ld + j];
+      double* Fj = F + j * ld;
+      for (int i = j + lane; i < f; i += 32) Fj[i] -= lb[i] * cj;
+    }
+    __syncthreads();
+    for (int i = k + 1 + tid; i < f; i += blockDim.x) F[k * ld + i] = lb[i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (neg) atomicAdd((unsigned long long*)&stat[0], (unsigned long long)neg);
+    if (bad != INT64_MAX) atomicMin((long long*)&stat[1], (long long)bad);
+  }
+  double* P = panel + S.panel_off[s];
+  for (int c = w; c < np; c += nw)
+    for (int r = lane; r < f; r += 32) P[(int64_t)c * f + r] = F[c * ld + r];
+  if (nu > 0) {
+    double* C = cb + S.cb_off[s];
+    for (int b = w; b < nu; b += nw)
+      for (int a = b + lane; a < nu; a += 32) C[(int64_t)b * nu + a] = F[(np + b) * ld + np + a];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Large fronts, panel step kb: factor the diagonal block [kb, kb+nbk) (one
+// warp, redundantly per CTA) and turn the rows below it into L.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kPanelRows) k_panel(SymDev S, const int32_t* __restrict__ nodes,
+                                                      int kb, const double* __restrict__ tol,
+                                                      double* __restrict__ panel,
+                                                      double* __restrict__ D,
+                                                      int64_t* __restrict__ stat) {
+  __shared__ double Ld[kNB][kNB + 1];  // Ld[col][row]
+  __shared__ double dd[kNB];
+  const int s = nodes[blockIdx.y];
+  const int64_t f = S.front[s], np = S.ncol[s];
+  if (kb >= np) return;
+  const int nbk = (int)imin(kNB, np - kb);
+  const int64_t rbeg = kb + nbk + (int64_t)blockIdx.x * kPanelRows;
+  const bool writer = blockIdx.x == 0;
+  if (!writer && rbeg >= f) return;
+  double* P = panel + S.panel_off[s];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int idx = tid; idx < kNB * kNB; idx += blockDim.x) {
+    int c = idx / kNB, r = idx % kNB;
+    Ld[c][r] = (c < nbk && r < nbk && r >= c) ? P[(kb + c) * f + kb + r] : 0.0;
+  }
+  __syncthreads();
+  if (tid < 32) {  // unblocked LDL^T of the diagonal block by warp 0; lane = row
+    for (int k = 0; k < nbk; ++k) {
+      double d = Ld[k][k];
+      double ci = Ld[k][lane];
+      double li = ci / d;
+      __syncwarp();
+      if (lane > k && lane < nbk) {
+        for (int j = k + 1; j <= lane; ++j) Ld[j][lane] -= li * Ld[k][j];
+      }
+      __syncwarp();
+      if (lane > k && lane < nbk) Ld[k][lane] = li;
+      __syncwarp();
+    }
+    if (lane < nbk) dd[lane] = Ld[lane][lane];
+  }
+  __syncthreads();
+  if (writer) {
+    const int64_t col0 = S.col0[s];
+    for (int idx = tid; idx < nbk * nbk; idx += blockDim.x) {
+      int c = idx / nbk, r = idx % nbk;
+      if (r >= c) P[(kb + c) * f + kb + r] = Ld[c][r];
+    }
+    if (tid == 0) {
+      int neg = 0;
+      int64_t bad = INT64_MAX;
+      double tv = tol[1];
+      for (int k = 0; k < nbk; ++k) {
+        double d = dd[k];
+        D[col0 + kb + k] = d;
+        if (d < 0.0) neg++;
+        if (fabs(d) < tv && bad == INT64_MAX) bad = col0 + kb + k;
+      }
+      if (neg) atomicAdd((unsigned long long*)&stat[0], (unsigned long long)neg);
+      if (bad != INT64_MAX) atomicMin((long long*)&stat[1], (long long)bad);
+    }
+  }
+  const int64_t r = rbeg + tid;
+  if (r < f) {
+    double x[kNB];
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) x[c] = c < nbk ? P[(kb + c) * f + r] : 0.0;
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) {
+      if (c < nbk) {
+        double wv = x[c];
+#pragma unroll
+        for (int t = 0; t < c; ++t) wv -= x[t] * dd[t] * Ld[t][c];
+        x[c] = wv / dd[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kNB; ++c)
+      if (c < nbk) P[(kb + c) * f + r] = x[c];
+  }
+}
+
+// Trailing update on FP64 tensor cores:
+//   MODE 0: panel columns [kb+nbk, np), rows [kb+nbk, f), K = [kb, kb+nbk)
+//   MODE 1: update block rows/cols [np, f) (stored separately), K = [0, np)
+template <int MODE>
+__global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restrict__ nodes, int kb,
+                                              double* __restrict__ panel,
+                                              double* __restrict__ cb,
+                                              const double* __restrict__ D) {
+  const int s = nodes[blockIdx.y];
+  const int64_t f = S.front[s], np = S.ncol[s];
+  int64_t m0, nend, k0, k1;
+  if (MODE == 0) {
+    if (kb >= np) return;
+    int64_t nbk = imin(kNB, np - kb);
+    m0 = kb + nbk;
+    if (m0 >= np) return;
+    nend = np;
+    k0 = kb;
+    k1 = kb + nbk;
+  } else {
+    if (np >= f) return;
+    m0 = np;
+    nend = f;
+    k0 = 0;
+    k1 = np;
+  }
+  const int64_t ntj = (nend - m0 + 63) / 64, nti = (f - m0 + 63) / 64;
+  const int64_t ti = blockIdx.x / ntj, tj = blockIdx.x % ntj;
+  if (ti >= nti) return;
+  const int64_t i0 = m0 + ti * 64, j0 = m0 + tj * 64;
+  if (i0 + 63 < j0) return;  // strictly above the diagonal
+  const double* L = panel + S.panel_off[s];
+  const double* Dk = D + S.col0[s];
+  double* C;
+  int64_t ldc, coff;
+  if (MODE == 0) {
+    C = panel + S.panel_off[s];
+    ldc = f;
+    coff = 0;
+  } else {
+    C = cb + S.cb_off[s];
+    ldc = f - np;
+    coff = np;
+  }
+  dmma_syrk_tile(L, f, Dk, k0, k1, i0, j0, f, nend, C, ldc, coff);
+}
+
+// ---------------------------------------------------------------------------
+// Supernodal solves, one CTA per supernode of a level.
+// ---------------------------------------------------------------------------
+__global__ void k_perm_gather(int64_t n, const int32_t* __restrict__ order,
+                              const double* __restrict__ b, double* __restrict__ xp) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < n) xp[k] = b[order[k]];
+}
+__global__ void k_perm_scatter(int64_t n, const int32_t* __restrict__ order,
+                               const double* __restrict__ xp, double* __restrict__ x) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < n) x[order[k]] = xp[k];
+}
+
+__global__ void __launch_bounds__(256) k_fwd(SymDev S, const int32_t* __restrict__ nodes,
+                                             const double* __restrict__ panel,
+                                             double* __restrict__ xp, double* __restrict__ upd) {
+  extern __shared__ double y[];
+  const int s = nodes[blockIdx.x];
+  const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
+  const double* P = panel + S.panel_off[s];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int64_t i = tid; i < f; i += blockDim.x) y[i] = i < np ? xp[col0 + i] : 0.0;
+  __syncthreads();
+  for (int64_t t = S.child_ptr[s]; t < S.child_ptr[s + 1]; ++t) {
+    int c = S.child_list[t];
+    int64_t nuc = S.front[c] - S.ncol[c];
+    const int32_t* rp = S.relpos + S.upd_off[c];
+    const double* u = upd + S.upd_off[c];
+    for (int64_t a = tid; a < nuc; a += blockDim.x) y[rp[a]] += u[a];
+    __syncthreads();
+  }
+  for (int64_t kb = 0; kb < np; kb += 32) {
+    const int nbk = (int)imin(32, np - kb);
+    if (tid < 32) {
+      double yi = lane < nbk ? y[kb + lane] : 0.0;
+      for (int k = 0; k < nbk; ++k) {
+        double zk = __shfl_sync(0xffffffffu, yi, k);
+        if (lane > k && lane < nbk) yi -= P[(kb + k) * f + kb + lane] * zk;
+      }
+      if (lane < nbk) y[kb + lane] = yi;
+    }
+    __syncthreads();
+    for (int64_t i = kb + nbk + tid; i < f; i += blockDim.x) {
+      double acc = 0.0;
+      for (int k = 0; k < nbk; ++k) acc = fma(P[(kb + k) * f + i], y[kb + k], acc);
+      y[i] -= acc;
+    }
+    __syncthreads();
+  }
+  for (int64_t i = tid; i < np; i += blockDim.x) xp[col0 + i] = y[i];
+  double* u = upd + S.upd_off[s];
+  for (int64_t i = np + tid; i < f; i += blockDim.x) u[i - np] = y[i];
+}
+
+__global__ void __launch_bounds__(256) k_bwd(SymDev S, const int32_t* __restrict__ nodes,
+                                             const double* __restrict__ panel,
+                                             const double* __restrict__ D,
+                                             double* __restrict__ xp) {
+  extern __shared__ double y[];
+  const int s = nodes[blockIdx.x];
+  const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
+  const double* P = panel + S.panel_off[s];
+  const int32_t* rows = S.rows + S.rows_off[s];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  for (int64_t i = tid; i < f; i += blockDim.x)
+    y[i] = i < np ? xp[col0 + i] / D[col0 + i] : xp[rows[i]];
+  __syncthreads();
+  const int64_t nblk = (np + 31) / 32;
+  for (int64_t bi = nblk - 1; bi >= 0; --bi) {
+    const int64_t kb = bi * 32;
+    const int nbk = (int)imin(32, np - kb);
+    for (int c = w; c < nbk; c += nw) {
+      const double* Pc = P + (kb + c) * f;
+      double acc = 0.0;
+      for (int64_t i = kb + nbk + lane; i < f; i += 32) acc = fma(Pc[i], y[i], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) y[kb + c] -= acc;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double xc = lane < nbk ? y[kb + lane] : 0.0;
+      for (int k = nbk - 1; k >= 0; --k) {
+        double xk = __shfl_sync(0xffffffffu, xc, k);
+        if (lane < k) xc -= P[(kb + lane) * f + kb + k] * xk;
+      }
+      if (lane < nbk) y[kb + lane] = xc;
+    }
+    __syncthreads();
+  }
+  for (int64_t i = tid; i < np; i += blockDim.x) xp[col0 + i] = y[i];
+}
+
+// ---------------------------------------------------------------------------
+// host drivers
+// ---------------------------------------------------------------------------
+static int build_plan(riga_symbolic* sym) {
+  const SymbolicHost& h = sym->h;
+  sym->plan.assign(h.nlevels, LevelPlan());
+  sym->ea_items_host.clear();
+  std::vector<int32_t> large;
+  static const int bounds[] = {32, 64, 96, 128, kSmallFront};
+  for (int64_t l = 0; l < h.nlevels; ++l) {
+    LevelPlan& P = sym->plan[l];
+    P.begin = h.level_ptr[l];
+    int64_t end = h.level_ptr[l + 1];
+    P.nsmall = h.level_nsmall[l];
+    P.nlarge = end - P.begin - P.nsmall;
+    int64_t i = P.begin;
+    for (int b : bounds) {
+      int64_t j = i;
+      while (j < P.begin + P.nsmall && h.front[h.level_nodes[j]] <= b) ++j;
+      if (j > i) {
+        P.cls_begin.push_back(i);
+        P.cls_f.push_back(b);
+      }
+      i = j;
+    }
+    P.cls_begin.push_back(P.begin + P.nsmall);
+    for (int64_t q = P.begin; q < end; ++q) {
+      int32_t s = h.level_nodes[q];
+      P.max_f = std::max<int64_t>(P.max_f, h.front[s]);
+      P.max_np = std::max<int64_t>(P.max_np, h.ncol[s]);
+      if (q >= P.begin + P.nsmall) {
+        P.max_np_large = std::max<int64_t>(P.max_np_large, h.ncol[s]);
+        P.max_f_large = std::max<int64_t>(P.max_f_large, h.front[s]);
+        P.max_nu_large = std::max<int64_t>(P.max_nu_large, h.front[s] - h.ncol[s]);
+        large.push_back(s);
+      }
+    }
+    // extend-add rounds into the large parents of this level
+    int64_t maxch = 0;
+    for (int64_t q = P.begin + P.nsmall; q < end; ++q) {
+      int32_t s = h.level_nodes[q];
+      maxch = std::max<int64_t>(maxch, h.child_ptr[s + 1] - h.child_ptr[s]);
+    }
+    for (int64_t r = 0; r < maxch; ++r) {
+      P.ea_round_begin.push_back((int64_t)sym->ea_items_host.size());
+      int64_t mx = 0;
+      for (int64_t q = P.begin + P.nsmall; q < end; ++q) {
+        int32_t s = h.level_nodes[q];
+        if (h.child_ptr[s] + r < h.child_ptr[s + 1]) {
+          int32_t c = h.child_list[h.child_ptr[s] + r];
+          sym->ea_items_host.push_back(c);
+          mx = std::max<int64_t>(mx, h.front[c] - h.ncol[c]);
+        }
+      }
+      P.ea_round_maxnu.push_back(mx);
+    }
+    P.ea_round_begin.push_back((int64_t)sym->ea_items_host.size());
+  }
+  sym->n_large = (int64_t)large.size();
+  sym->large_host = large;
+  return RIGA_OK;
+}
+
+template <typename T>
+static int up(DevBuf<T>& d, const std::vector<T>& v, cudaStream_t s) {
+  return d.upload(v.data(), v.size(), s);
+}
+
+static int upload_symbolic(riga_symbolic* sym) {
+  cudaStream_t s = sym->ctx->stream;
+  const SymbolicHost& h = sym->h;
+  RIGA_TRY(up(sym->d_col0, h.col0, s));
+  RIGA_TRY(up(sym->d_ncol, h.ncol, s));
+  RIGA_TRY(up(sym->d_front, h.front, s));
+  RIGA_TRY(up(sym->d_rows_off, h.rows_off, s));
+  RIGA_TRY(up(sym->d_panel_off, h.panel_off, s));
+  RIGA_TRY(up(sym->d_cb_off, h.cb_off, s));
+  RIGA_TRY(up(sym->d_upd_off, h.upd_off, s));
+  RIGA_TRY(up(sym->d_child_ptr, h.child_ptr, s));
+  RIGA_TRY(up(sym->d_asm_ptr, h.asm_ptr, s));
+  RIGA_TRY(up(sym->d_sparent, h.sparent, s));
+  RIGA_TRY(up(sym->d_rows, h.rows, s));
+  RIGA_TRY(up(sym->d_relpos, h.relpos, s));
+  RIGA_TRY(up(sym->d_child_list, h.child_list, s));
+  std::vector<int32_t> slot32(h.asm_slot.begin(), h.asm_slot.end());
+  RIGA_TRY(up(sym->d_asm_slot, slot32, s));
+  RIGA_TRY(up(sym->d_asm_local, h.asm_local, s));
+  RIGA_TRY(up(sym->d_level_nodes, h.level_nodes, s));
+  std::vector<int32_t> ord32(h.order.begin(), h.order.end());
+  RIGA_TRY(up(sym->d_order, ord32, s));
+  RIGA_TRY(up(sym->d_ea_items, sym->ea_items_host, s));
+  RIGA_TRY(up(sym->d_large_nodes, sym->large_host, s));
+  RIGA_CUDA(cudaStreamSynchronize(s));
+  sym->on_device = true;
+  return RIGA_OK;
+}
+
+static int set_smem_attrs() {
+  static bool done = false;
+  if (done) return RIGA_OK;
+  int dev = 0, maxsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  RIGA_CUDA(cudaFuncSetAttribute(k_small_front, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  RIGA_CUDA(cudaFuncSetAttribute(k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  RIGA_CUDA(cudaFuncSetAttribute(k_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  done = true;
+  return RIGA_OK;
+}
+
+static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const double* Mv,
+                   double sigma, double rel) {
+  riga_symbolic* sym = F->sym;
+  const SymbolicHost& h = sym->h;
+  SymDev S = sym->dev();
+  RIGA_TRY(set_smem_attrs());
+  double* scratch = nullptr;
+  RIGA_CUDA(cudaMallocAsync(&scratch, 1024 * sizeof(double), st));
+  RIGA_CUDA(cudaMemsetAsync(scratch, 0, 1024 * sizeof(double), st));
+  int nb = (int)std::min<int64_t>(592, (sym->sys->nnz + 255) / 256);
+  k_tol<<<std::max(nb, 1), 256, 0, st>>>(sym->sys->nnz, Kv, Mv, sigma, rel, scratch,
+                                          reinterpret_cast<unsigned*>(scratch + 1000), F->tol.p,
+                                          F->stat.p, h.n);
+  RIGA_CUDA(cudaGetLastError());
+  double* cbuf = nullptr;
+  if (h.cb_total) RIGA_CUDA(cudaMallocAsync(&cbuf, h.cb_total * sizeof(double), st));
+  if (h.panel_large) RIGA_CUDA(cudaMemsetAsync(F->panel.p, 0, h.panel_large * 8, st));
+  if (h.cb_large) RIGA_CUDA(cudaMemsetAsync(cbuf, 0, h.cb_large * 8, st));
+  if (sym->n_large) {
+    k_asm_large<<<(unsigned)sym->n_large, 256, 0, st>>>(S, sym->d_large_nodes.p, Kv, Mv, sigma,
+                                                        F->panel.p);
+    RIGA_CUDA(cudaGetLastError());
+  }
+  for (int64_t l = 0; l < h.nlevels; ++l) {
+    const LevelPlan& P = sym->plan[l];
+    for (size_t r = 0; r + 1 < P.ea_round_begin.size(); ++r) {
+      int64_t cnt = P.ea_round_begin[r + 1] - P.ea_round_begin[r];
+      if (!cnt) continue;
+      dim3 g((unsigned)((P.ea_round_maxnu[r] + 31) / 32), (unsigned)cnt);
+      if (g.x == 0) continue;
+      k_extend_add<<<g, 256, 0, st>>>(S, sym->d_ea_items.p + P.ea_round_begin[r], F->panel.p, cbuf);
+      RIGA_CUDA(cudaGetLastError());
+    }
+    for (size_t c = 0; c + 1 < P.cls_begin.size(); ++c) {
+      int64_t cnt = P.cls_begin[c + 1] - P.cls_begin[c];
+      if (!cnt) continue;
+      int fm = P.cls_f[c];
+      size_t smem = (size_t)fm * (fm | 1) * 8 + 2 * (size_t)fm * 8;
+      k_small_front<<<(unsigned)cnt, 256, smem, st>>>(S, sym->d_level_nodes.p + P.cls_begin[c], Kv,
+                                                       Mv, sigma, F->tol.p, F->panel.p, cbuf,
+                                                       F->D.p, F->stat.p);
+      RIGA_CUDA(cudaGetLastError());
+    }
+    if (P.nlarge) {
+      const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
+      unsigned nl = (unsigned)P.nlarge;
+      for (int64_t kb = 0; kb < P.max_np_large; kb += kNB) {
+        unsigned rchunks = (unsigned)std::max<int64_t>(1, (P.max_f_large - kb + kPanelRows - 1) / kPanelRows);
+        k_panel<<<dim3(rchunks, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p,
+                                                          F->D.p, F->stat.p);
+        RIGA_CUDA(cudaGetLastError());
+        int64_t m0 = kb + kNB;
+        if (m0 < P.max_np_large) {
+          int64_t ntj = (P.max_np_large - m0 + 63) / 64, nti = (P.max_f_large - m0 + 63) / 64;
+          k_syrk<0><<<dim3((unsigned)(ntj * nti), nl), 128, 0, st>>>(S, ln, (int)kb, F->panel.p,
+                                                                    cbuf, F->D.p);
+          RIGA_CUDA(cudaGetLastError());
+        }
+      }
+      if (P.max_nu_large > 0) {
+        int64_t t = (P.max_nu_large + 63) / 64;
+        k_syrk<1><<<dim3((unsigned)(t * t), nl), 128, 0, st>>>(S, ln, 0, F->panel.p, cbuf, F->D.p);
+        RIGA_CUDA(cudaGetLastError());
+      }
+    }
+  }
+  if (cbuf) RIGA_CUDA(cudaFreeAsync(cbuf, st));
+  RIGA_CUDA(cudaFreeAsync(scratch, st));
+  return RIGA_OK;
+}
+
+int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x) {
+  riga_symbolic* sym = F->sym;
+  const SymbolicHost& h = sym->h;
+  SymDev S = sym->dev();
+  RIGA_TRY(set_smem_attrs());
+  unsigned g = (unsigned)((h.n + 255) / 256);
+  k_perm_gather<<<g, 256, 0, st>>>(h.n, sym->d_order.p, b, F->xperm.p);
+  for (int64_t l = 0; l < h.nlevels; ++l) {
+    const LevelPlan& P = sym->plan[l];
+    unsigned cnt = (unsigned)(h.level_ptr[l + 1] - h.level_ptr[l]);
+    k_fwd<<<cnt, 256, P.max_f * 8, st>>>(S, sym->d_level_nodes.p + P.begin, F->panel.p,
+                                          F->xperm.p, F->upd.p);
+  }
+  for (int64_t l = h.nlevels - 1; l >= 0; --l) {
+    const LevelPlan& P = sym->plan[l];
+    unsigned cnt = (unsigned)(h.level_ptr[l + 1] - h.level_ptr[l]);
+    k_bwd<<<cnt, 256, P.max_f * 8, st>>>(S, sym->d_level_nodes.p + P.begin, F->panel.p, F->D.p,
+                                          F->xperm.p);
+  }
+  k_perm_scatter<<<g, 256, 0, st>>>(h.n, sym->d_order.p, F->xperm.p, x);
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+}  // namespace riga
+
+using namespace riga;
+
+extern "C" {
+
+static int finish_symbolic(riga_symbolic* sym) { return build_plan(sym); }
+
+int riga_symbolic_analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                          const int64_t* perm, riga_symbolic** out) {
+  RIGA_CHECK_ARG(out && rowptr && colidx && perm && n > 0, "null arg");
+  auto sym = std::make_unique<riga_symbolic>();
+  std::string err;
+  if (analyze(n, rowptr, colidx, perm, sym->h, err)) {
+    set_error("symbolic analysis: " + err);
+    return RIGA_BAD_ARG;
+  }
+  RIGA_TRY(finish_symbolic(sym.get()));
+  *out = sym.release();
+  return RIGA_OK;
+}
+
+int riga_symbolic_create(riga_system* sys, const int64_t* perm, riga_symbolic** out) {
+  RIGA_CHECK_ARG(sys && perm && out, "null arg");
+  DeviceGuard g(sys->ctx->device);
+  std::vector<int64_t> rp(sys->n + 1);
+  std::vector<int32_t> ci(sys->nnz);
+  RIGA_TRY(riga_system_download(sys, rp.data(), ci.data(), nullptr, nullptr));
+  auto sym = std::make_unique<riga_symbolic>();
+  sym->ctx = sys->ctx;
+  sym->sys = sys;
+  std::string err;
+  if (analyze(sys->n, rp.data(), ci.data(), perm, sym->h, err)) {
+    set_error("symbolic analysis: " + err);
+    return RIGA_BAD_ARG;
+  }
+  RIGA_TRY(finish_symbolic(sym.get()));
+  RIGA_TRY(upload_symbolic(sym.get()));
+  *out = sym.release();
+  return RIGA_OK;
+}
+
+int riga_symbolic_stats(riga_symbolic* sym, int64_t* st) {
+  RIGA_CHECK_ARG(sym && st, "null arg");
+  const SymbolicHost& h = sym->h;
+  int64_t nsmall = 0;
+  for (int64_t s = 0; s < h.nsuper; ++s) nsmall += h.front[s] <= kSmallFront;
+  int64_t v[16] = {h.fill_nnz,    h.factor_flops, h.nsuper,         h.max_front,
+                   h.nlevels,     h.panel_total,  h.cb_total,       h.max_ncol,
+                   h.fundamental, h.stored_L,     nsmall,           h.nsuper - nsmall,
+                   h.nnz_lower,   h.tree_height,  h.relaxed_flops,  0};
+  std::memcpy(st, v, sizeof(v));
+  return RIGA_OK;
+}
+
+int riga_symbolic_order(riga_symbolic* sym, int64_t* order) {
+  RIGA_CHECK_ARG(sym && order, "null arg");
+  std::memcpy(order, sym->h.order.data(), sym->h.n * sizeof(int64_t));
+  return RIGA_OK;
+}
+
+int riga_symbolic_colcounts(riga_symbolic* sym, int64_t* counts) {
+  RIGA_CHECK_ARG(sym && counts, "null arg");
+  const SymbolicHost& h = sym->h;
+  for (int64_t k = 0; k < h.n; ++k) counts[h.post[k]] = h.colcount[k];
+  return RIGA_OK;
+}
+
+int riga_symbolic_destroy(riga_symbolic* sym) {
+  if (!sym) return RIGA_OK;
+  if (sym->ctx) {
+    DeviceGuard g(sym->ctx->device);
+    cudaStreamSynchronize(sym->ctx->stream);
+    delete sym;
+  } else {
+    delete sym;
+  }
+  return RIGA_OK;
+}
+
+int riga_factor_create(riga_ctx* ctx, riga_symbolic* sym, double sigma, double rel_zero_tol,
+                riga_factor** out, int64_t* n_negative, int64_t* bad_pivot) {
+  RIGA_CHECK_ARG(sym && out, "null arg");
+  RIGA_CHECK_ARG(sym->on_device && sym->sys, "symbolic handle has no device system");
+  if (!ctx) ctx = sym->ctx;
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const SymbolicHost& h = sym->h;
+  auto F = std::make_unique<riga_factor>();
+  F->ctx = ctx;
+  F->sym = sym;
+  F->sigma = sigma;
+  RIGA_TRY(F->panel.alloc(std::max<int64_t>(h.panel_total, 1)));
+  RIGA_TRY(F->D.alloc(h.n));
+  RIGA_TRY(F->xperm.alloc(h.n));
+  RIGA_TRY(F->upd.alloc(std::max<int64_t>(h.upd_total, 1)));
+  RIGA_TRY(F->stat.alloc(2));
+  RIGA_TRY(F->tol.alloc(2));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  int rc = numeric(F.get(), st, sym->sys->K.p, sym->sys->M.p, sigma, rel_zero_tol);
+  cudaEventRecord(e1, st);
+  if (rc) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+  }
+  int64_t stat[2];
+  double tol[2];
+  RIGA_CUDA(cudaMemcpyAsync(stat, F->stat.p, sizeof(stat), cudaMemcpyDeviceToHost, st));
+  RIGA_CUDA(cudaMemcpyAsync(tol, F->tol.p, sizeof(tol), cudaMemcpyDeviceToHost, st));
+  RIGA_CUDA(cudaStreamSynchronize(st));
+  cudaEventElapsedTime(&F->factor_ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (n_negative) *n_negative = stat[0];
+  if (bad_pivot) *bad_pivot = stat[1] < h.n ? stat[1] : -1;
+  if (tol[0] == 0.0) {
+    set_error("matrix is identically zero");
+    if (bad_pivot) *bad_pivot = -1;
+    return RIGA_ZERO_PIVOT;
+  }
+  if (stat[1] < h.n) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "pivot %lld below %.3e (shift at an eigenvalue?)",
+             (long long)stat[1], tol[1]);
+    set_error(buf);
+    *out = F.release();
+    return RIGA_ZERO_PIVOT;
+  }
+  *out = F.release();
+  return RIGA_OK;
+}
+
+int riga_factor_solve(riga_factor* f, const double* b, double* x) {
+  RIGA_CHECK_ARG(f && b && x, "null arg");
+  DeviceGuard g(f->ctx->device);
+  return factor_solve(f, f->ctx->stream, b, x);
+}
+
+int riga_factor_time_ms(riga_factor* f, float* ms) {
+  RIGA_CHECK_ARG(f && ms, "null arg");
+  *ms = f->factor_ms;
+  return RIGA_OK;
+}
+
+int riga_factor_D(riga_factor* f, double* D) {
+  RIGA_CHECK_ARG(f && D, "null arg");
+  DeviceGuard g(f->ctx->device);
+  RIGA_CUDA(cudaMemcpyAsync(D, f->D.p, f->sym->h.n * 8, cudaMemcpyDeviceToHost, f->ctx->stream));
+  RIGA_CUDA(cudaStreamSynchronize(f->ctx->stream));
+  return RIGA_OK;
+}
+
+int riga_factor_export(riga_factor* f, int64_t* Lp, int32_t* Li, double* Lx) {
+  RIGA_CHECK_ARG(f && Lp && Li && Lx, "null arg");
+  DeviceGuard g(f->ctx->device);
+  const SymbolicHost& h = f->sym->h;
+  std::vector<double> panel(h.panel_total);
+  RIGA_CUDA(cudaMemcpyAsync(panel.data(), f->panel.p, h.panel_total * 8, cudaMemcpyDeviceToHost,
+                            f->ctx->stream));
+  RIGA_CUDA(cudaStreamSynchronize(f->ctx->stream));
+  int64_t q = 0;
+  Lp[0] = 0;
+  for (int64_t s = 0; s < h.nsuper; ++s) {
+    int64_t fr = h.front[s], np = h.ncol[s];
+    const int32_t* rows = &h.rows[h.rows_off[s]];
+    const double* P = &panel[h.panel_off[s]];
+    for (int64_t c = 0; c < np; ++c) {
+      for (int64_t r = c + 1; r < fr; ++r) {
+        Li[q] = rows[r];
+        Lx[q] = P[c * fr + r];
+        ++q;
+      }
+      Lp[h.col0[s] + c + 1] = q;
+    }
+  }
+  return RIGA_OK;
+}
+
+int riga_factor_destroy(riga_factor* f) {
+  if (!f) return RIGA_OK;
+  DeviceGuard g(f->ctx->device);
+  cudaStreamSynchronize(f->ctx->stream);
+  delete f;
+  return RIGA_OK;
+}
+
+}  // extern "C"

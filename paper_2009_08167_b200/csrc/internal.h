@@ -40,6 +40,7 @@ struct riga_symbolic {
   riga::SymbolicHost h;
   std::vector<LevelPlan> plan;
   std::vector<int32_t> ea_items_host;  // child ids, grouped by (level, round)
+  std::vector<int32_t> large_host;     // all large fronts (for k_asm_large)
   bool on_device = false;
   // device arrays
   riga::DevBuf<int64_t> d_col0, d_ncol, d_front, d_rows_off, d_panel_off, d_cb_off, d_upd_off;

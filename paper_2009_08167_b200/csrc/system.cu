@@ -1,0 +1,428 @@
+// Context, device CSR system (upload / Kronecker assembly), SpMV, dots.
+//
+//  riga_system_assemble_kron  <- kron_assemble   ref assembly.py:139-186
+//  riga_spmv / riga_csr_spmv  <- mass_matvec     ref sparsela.py:280-290
+#include <cstring>
+#include <mutex>
+
+#include "internal.h"
+#include "kernels.cuh"
+
+namespace riga {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------------------
+// Kronecker assembly: one thread per nonzero of the d-dimensional pattern.
+// Row r = (iz, iy, ix) (x fastest); 1D rows have contiguous column ranges, so
+// the nnz of row r enumerate (jz, jy, jx) lexicographically = sorted columns.
+// Values reproduce scipy's evaluation order exactly (no FMA contraction):
+//   2D: K = my*kx + ky*mx                       M = my*mx
+//   3D: K = ((mz*my)*kx + (mz*ky)*mx) + (kz*my)*mx    M = (mz*my)*mx
+// ---------------------------------------------------------------------------
+struct Kron1D {
+  const int64_t* rp;
+  const int32_t* ci;
+  const double* k;
+  const double* m;
+  int64_t n;
+};
+
+__global__ void k_kron_rowptr(int dim, Kron1D x, Kron1D y, Kron1D z, int64_t n, int64_t* rowlen) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t ix = r % x.n, t = r / x.n;
+  int64_t len = x.rp[ix + 1] - x.rp[ix];
+  if (dim >= 2) {
+    int64_t iy = t % y.n;
+    t /= y.n;
+    len *= y.rp[iy + 1] - y.rp[iy];
+    if (dim == 3) len *= z.rp[t + 1] - z.rp[t];
+  }
+  rowlen[r] = len;
+}
+
+__global__ void k_kron_values(int dim, Kron1D x, Kron1D y, Kron1D z, int64_t n,
+                              const int64_t* __restrict__ rowptr, int32_t* __restrict__ colidx,
+                              double* __restrict__ K, double* __restrict__ M) {
+  // one warp per row; lanes stride over the row's entries
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  int64_t r = warp;
+  int64_t ix = r % x.n, t = r / x.n, iy = 0, iz = 0;
+  if (dim >= 2) {
+    iy = t % y.n;
+    iz = t / y.n;
+  }
+  int64_t lx = x.rp[ix + 1] - x.rp[ix];
+  int64_t ly = dim >= 2 ? y.rp[iy + 1] - y.rp[iy] : 1;
+  int64_t base = rowptr[r], len = rowptr[r + 1] - base;
+  for (int64_t e = lane; e < len; e += 32) {
+    int64_t ex = e % lx, et = e / lx;
+    int64_t qx = x.rp[ix] + ex;
+    double kx = x.k[qx], mx = x.m[qx];
+    int64_t col = x.ci[qx];
+    double kv, mv;
+    if (dim == 1) {
+      kv = kx;
+      mv = mx;
+    } else {
+      int64_t ey = et % ly, ez = et / ly;
+      int64_t qy = y.rp[iy] + ey;
+      double ky = y.k[qy], my = y.m[qy];
+      col += (int64_t)y.ci[qy] * x.n;
+      if (dim == 2) {
+        kv = __dadd_rn(__dmul_rn(my, kx), __dmul_rn(ky, mx));
+        mv = __dmul_rn(my, mx);
+      } else {
+        int64_t qz = z.rp[iz] + ez;
+        double kz = z.k[qz], mz = z.m[qz];
+        col += (int64_t)z.ci[qz] * x.n * y.n;
+        double mzmy = __dmul_rn(mz, my);
+        kv = __dadd_rn(__dadd_rn(__dmul_rn(mzmy, kx), __dmul_rn(__dmul_rn(mz, ky), mx)),
+                       __dmul_rn(__dmul_rn(kz, my), mx));
+        mv = __dmul_rn(mzmy, mx);
+      }
+    }
+    colidx[base + e] = (int32_t)col;
+    K[base + e] = kv;
+    M[base + e] = mv;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CSR SpMV, LANES threads per row, fixed reduction order (deterministic).
+// mode 0: y = A x;  mode 1: y = (K - sigma M) x with A = K, B = M.
+// ---------------------------------------------------------------------------
+template <int LANES, int MODE>
+__global__ void __launch_bounds__(256) k_spmv(int64_t n, const int64_t* __restrict__ rp,
+                                              const int32_t* __restrict__ ci,
+                                              const double* __restrict__ A,
+                                              const double* __restrict__ B, double sigma,
+                                              const double* __restrict__ x,
+                                              double* __restrict__ y) {
+  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LANES;
+  int sub = threadIdx.x % LANES;
+  if (row >= n) return;
+  int64_t b = rp[row], e = rp[row + 1];
+  double acc = 0.0;
+  for (int64_t q = b + sub; q < e; q += LANES) {
+    double a = __ldg(A + q);
+    if (MODE == 1) a = __dsub_rn(a, __dmul_rn(sigma, __ldg(B + q)));
+    acc = fma(a, __ldg(x + __ldg(ci + q)), acc);
+  }
+#pragma unroll
+  for (int o = LANES / 2; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o, LANES);
+  if (sub == 0) y[row] = acc;
+}
+
+int csr_spmv_impl(cudaStream_t s, int64_t n, const int64_t* rp, const int32_t* ci, const double* A,
+                  const double* B, double sigma, int mode, int64_t nnz, const double* x,
+                  double* y) {
+  if (n == 0) return RIGA_OK;
+  double avg = double(nnz) / double(n);
+  int lanes = avg >= 48 ? 32 : (avg >= 20 ? 16 : (avg >= 8 ? 8 : 4));
+  int64_t threads = n * lanes;
+  int blocks = (int)((threads + 255) / 256);
+#define RIGA_SPMV_CASE(L)                                                                  \
+  case L:                                                                                  \
+    if (mode == 0)                                                                         \
+      k_spmv<L, 0><<<blocks, 256, 0, s>>>(n, rp, ci, A, B, sigma, x, y);                   \
+    else                                                                                   \
+      k_spmv<L, 1><<<blocks, 256, 0, s>>>(n, rp, ci, A, B, sigma, x, y);                   \
+    break;
+  switch (lanes) {
+    RIGA_SPMV_CASE(4)
+    RIGA_SPMV_CASE(8)
+    RIGA_SPMV_CASE(16)
+    RIGA_SPMV_CASE(32)
+  }
+#undef RIGA_SPMV_CASE
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+int csr_spmv(cudaStream_t s, int64_t n, const int64_t* rowptr, const int32_t* colidx,
+             const double* val, const double* x, double* y) {
+  int64_t nnz = 0;
+  RIGA_CUDA(cudaMemcpyAsync(&nnz, rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  RIGA_CUDA(cudaStreamSynchronize(s));
+  return csr_spmv_impl(s, n, rowptr, colidx, val, nullptr, 0.0, 0, nnz, x, y);
+}
+
+int system_spmv(riga_system* sys, cudaStream_t s, int which, double sigma, const double* x,
+                double* y) {
+  switch (which) {
+    case 0:
+      return csr_spmv_impl(s, sys->n, sys->rowptr.p, sys->colidx.p, sys->K.p, nullptr, 0.0, 0,
+                           sys->nnz, x, y);
+    case 1:
+      return csr_spmv_impl(s, sys->n, sys->rowptr.p, sys->colidx.p, sys->M.p, nullptr, 0.0, 0,
+                           sys->nnz, x, y);
+    case 2:
+      return csr_spmv_impl(s, sys->n, sys->rowptr.p, sys->colidx.p, sys->K.p, sys->M.p, sigma, 1,
+                           sys->nnz, x, y);
+  }
+  set_error("spmv: which must be 0 (K), 1 (M) or 2 (K - sigma M)");
+  return RIGA_BAD_ARG;
+}
+
+// ---------------------------------------------------------------------------
+// Dot product, deterministic: per-block partials + last-block final sum.
+// ---------------------------------------------------------------------------
+__global__ void k_dot(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                      double* __restrict__ partial, unsigned* __restrict__ ticket,
+                      double* __restrict__ out) {
+  __shared__ double red[32];
+  __shared__ bool last;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc = fma(x[i], y[i], acc);
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = acc;
+    __threadfence();
+    unsigned t = atomicAdd(ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += ((volatile double*)partial)[i];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) {
+      *out = s;
+      *ticket = 0u;
+    }
+  }
+}
+
+int launch_dot(cudaStream_t s, int64_t n, const double* x, const double* y, double* out_dev) {
+  // scratch: partials (<= 592) + ticket live right after out_dev (caller
+  // provides a buffer of at least kDotScratch doubles)
+  int blocks = (int)std::min<int64_t>(592, std::max<int64_t>(1, (n + 255) / 256));
+  double* partial = out_dev + 1;
+  unsigned* ticket = reinterpret_cast<unsigned*>(out_dev + 1 + 592);
+  k_dot<<<blocks, 256, 0, s>>>(n, x, y, partial, ticket, out_dev);
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+}  // namespace riga
+
+using namespace riga;
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* riga_last_error(void) { return riga::last_error(); }
+int riga_version(void) { return 100; }
+
+int riga_device_count(int* count) {
+  RIGA_CHECK_ARG(count, "null count");
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *count = c;
+  return RIGA_OK;
+}
+
+int riga_ctx_create(int device, void* stream_handle, riga_ctx** out) {
+  RIGA_CHECK_ARG(out, "null out");
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess || c == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device visible: the B200 engine has no CPU fallback");
+    return RIGA_NO_DEVICE;
+  }
+  RIGA_CHECK_ARG(device >= 0 && device < c, "device index out of range");
+  DeviceGuard g(device);
+  auto* ctx = new riga_ctx();
+  ctx->device = device;
+  if (stream_handle) {
+    ctx->stream = (cudaStream_t)stream_handle;
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete ctx;
+      set_error(std::string("stream create: ") + cudaGetErrorString(e));
+      return RIGA_CUDA_ERROR;
+    }
+    ctx->own_stream = true;
+  }
+  cudaError_t e = cudaMallocHost(&ctx->scratch_host, 4096 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->scratch_dev, kDotScratch * 4 * sizeof(double));
+  if (e != cudaSuccess) {
+    set_error(std::string("ctx scratch: ") + cudaGetErrorString(e));
+    return RIGA_CUDA_ERROR;
+  }
+  cudaMemsetAsync(ctx->scratch_dev, 0, kDotScratch * 4 * sizeof(double), ctx->stream);
+  ctx->scratch_dev_n = kDotScratch * 4;
+  *out = ctx;
+  return RIGA_OK;
+}
+
+int riga_ctx_destroy(riga_ctx* ctx) {
+  if (!ctx) return RIGA_OK;
+  DeviceGuard g(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->scratch_host) cudaFreeHost(ctx->scratch_host);
+  if (ctx->scratch_dev) cudaFree(ctx->scratch_dev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return RIGA_OK;
+}
+
+int riga_ctx_synchronize(riga_ctx* ctx) {
+  RIGA_CHECK_ARG(ctx, "null ctx");
+  DeviceGuard g(ctx->device);
+  RIGA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return RIGA_OK;
+}
+
+int riga_ctx_stream(riga_ctx* ctx, void** stream_out) {
+  RIGA_CHECK_ARG(ctx && stream_out, "null arg");
+  *stream_out = (void*)ctx->stream;
+  return RIGA_OK;
+}
+
+int riga_system_upload(riga_ctx* ctx, int64_t n, int64_t nnz, const int64_t* rowptr,
+                       const int32_t* colidx, const double* K, const double* M,
+                       riga_system** out) {
+  RIGA_CHECK_ARG(ctx && out && rowptr && colidx && K && M, "null arg");
+  RIGA_CHECK_ARG(n > 0 && nnz >= 0 && rowptr[n] == nnz, "inconsistent CSR");
+  RIGA_CHECK_ARG(nnz < (int64_t(1) << 31), "nnz must fit int32 slots");
+  DeviceGuard g(ctx->device);
+  auto sys = std::make_unique<riga_system>();
+  sys->ctx = ctx;
+  sys->n = n;
+  sys->nnz = nnz;
+  RIGA_TRY(sys->rowptr.upload(rowptr, n + 1, ctx->stream));
+  RIGA_TRY(sys->colidx.upload(colidx, nnz, ctx->stream));
+  RIGA_TRY(sys->K.upload(K, nnz, ctx->stream));
+  RIGA_TRY(sys->M.upload(M, nnz, ctx->stream));
+  RIGA_CUDA(cudaStreamSynchronize(ctx->stream));
+  *out = sys.release();
+  return RIGA_OK;
+}
+
+int riga_system_assemble_kron(riga_ctx* ctx, int dim, const int64_t* n1,
+                              const int64_t* const* rowptr1, const int32_t* const* colidx1,
+                              const double* const* k1, const double* const* m1,
+                              riga_system** out) {
+  RIGA_CHECK_ARG(ctx && out && n1 && rowptr1 && colidx1 && k1 && m1, "null arg");
+  RIGA_CHECK_ARG(dim >= 1 && dim <= 3, "dim must be 1, 2 or 3");
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->stream;
+  DevBuf<int64_t> rp[3];
+  DevBuf<int32_t> ci[3];
+  DevBuf<double> kk[3], mm[3];
+  Kron1D ax[3] = {};
+  int64_t n = 1, nnz = 1;
+  for (int t = 0; t < dim; ++t) {
+    int64_t nt = n1[t], zt = rowptr1[t][nt];
+    RIGA_CHECK_ARG(nt > 0, "empty 1D matrix");
+    RIGA_TRY(rp[t].upload(rowptr1[t], nt + 1, s));
+    RIGA_TRY(ci[t].upload(colidx1[t], zt, s));
+    RIGA_TRY(kk[t].upload(k1[t], zt, s));
+    RIGA_TRY(mm[t].upload(m1[t], zt, s));
+    ax[t] = Kron1D{rp[t].p, ci[t].p, kk[t].p, mm[t].p, nt};
+    n *= nt;
+    nnz *= zt;
+  }
+  RIGA_CHECK_ARG(nnz < (int64_t(1) << 31), "nnz must fit int32 slots");
+  auto sys = std::make_unique<riga_system>();
+  sys->ctx = ctx;
+  sys->n = n;
+  sys->nnz = nnz;
+  RIGA_TRY(sys->rowptr.alloc(n + 1));
+  RIGA_TRY(sys->colidx.alloc(nnz));
+  RIGA_TRY(sys->K.alloc(nnz));
+  RIGA_TRY(sys->M.alloc(nnz));
+  RIGA_CUDA(cudaMemsetAsync(sys->rowptr.p, 0, sizeof(int64_t), s));
+  k_kron_rowptr<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dim, ax[0], ax[1], ax[2], n,
+                                                            sys->rowptr.p + 1);
+  RIGA_CUDA(cudaGetLastError());
+  RIGA_TRY(inclusive_scan_i64(s, sys->rowptr.p + 1, n));
+  k_kron_values<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
+      dim, ax[0], ax[1], ax[2], n, sys->rowptr.p, sys->colidx.p, sys->K.p, sys->M.p);
+  RIGA_CUDA(cudaGetLastError());
+  RIGA_CUDA(cudaStreamSynchronize(s));
+  *out = sys.release();
+  return RIGA_OK;
+}
+
+int riga_system_info(riga_system* sys, int64_t* n, int64_t* nnz) {
+  RIGA_CHECK_ARG(sys, "null system");
+  if (n) *n = sys->n;
+  if (nnz) *nnz = sys->nnz;
+  return RIGA_OK;
+}
+
+int riga_system_download(riga_system* sys, int64_t* rowptr, int32_t* colidx, double* K,
+                         double* M) {
+  RIGA_CHECK_ARG(sys, "null system");
+  DeviceGuard g(sys->ctx->device);
+  cudaStream_t s = sys->ctx->stream;
+  if (rowptr)
+    RIGA_CUDA(cudaMemcpyAsync(rowptr, sys->rowptr.p, (sys->n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  if (colidx)
+    RIGA_CUDA(cudaMemcpyAsync(colidx, sys->colidx.p, sys->nnz * 4, cudaMemcpyDeviceToHost, s));
+  if (K) RIGA_CUDA(cudaMemcpyAsync(K, sys->K.p, sys->nnz * 8, cudaMemcpyDeviceToHost, s));
+  if (M) RIGA_CUDA(cudaMemcpyAsync(M, sys->M.p, sys->nnz * 8, cudaMemcpyDeviceToHost, s));
+  RIGA_CUDA(cudaStreamSynchronize(s));
+  return RIGA_OK;
+}
+
+int riga_system_device_ptrs(riga_system* sys, const int64_t** rowptr, const int32_t** colidx,
+                            const double** K, const double** M) {
+  RIGA_CHECK_ARG(sys, "null system");
+  if (rowptr) *rowptr = sys->rowptr.p;
+  if (colidx) *colidx = sys->colidx.p;
+  if (K) *K = sys->K.p;
+  if (M) *M = sys->M.p;
+  return RIGA_OK;
+}
+
+int riga_system_destroy(riga_system* sys) {
+  if (!sys) return RIGA_OK;
+  DeviceGuard g(sys->ctx->device);
+  cudaStreamSynchronize(sys->ctx->stream);
+  delete sys;
+  return RIGA_OK;
+}
+
+int riga_spmv(riga_system* sys, int which, double sigma, const double* x, double* y) {
+  RIGA_CHECK_ARG(sys && x && y, "null arg");
+  DeviceGuard g(sys->ctx->device);
+  return system_spmv(sys, sys->ctx->stream, which, sigma, x, y);
+}
+
+int riga_csr_spmv(riga_ctx* ctx, int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                  const double* val, const double* x, double* y) {
+  RIGA_CHECK_ARG(ctx && rowptr && colidx && val && x && y && n >= 0, "null arg");
+  DeviceGuard g(ctx->device);
+  return csr_spmv(ctx->stream, n, rowptr, colidx, val, x, y);
+}
+
+int riga_dot(riga_ctx* ctx, int64_t n, const double* x, const double* y, double* out) {
+  RIGA_CHECK_ARG(ctx && x && y && out, "null arg");
+  DeviceGuard g(ctx->device);
+  RIGA_TRY(launch_dot(ctx->stream, n, x, y, ctx->scratch_dev));
+  RIGA_CUDA(cudaMemcpyAsync(ctx->scratch_host, ctx->scratch_dev, sizeof(double),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  RIGA_CUDA(cudaStreamSynchronize(ctx->stream));
+  *out = ctx->scratch_host[0];
+  return RIGA_OK;
+}
+
+}  // extern "C"

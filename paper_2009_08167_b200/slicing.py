@@ -1,0 +1,246 @@
+"""Uniform spectrum slicing across streams and GPUs.
+
+Additive to the reference API (it has only the adaptive ``_march``):
+
+* ``uniform_shifts(lam_e, S)``        sigma_k = k lam_e / S
+* ``kronecker_spectrum(system)``      exact discrete spectrum from the 1D
+                                      pencils (identity of ref
+                                      tests/test_assembly.py:64-72)
+* ``choose_lambda_e(system, N0)``     lam_e in the first spectral gap at or
+                                      after N0
+* ``solve_uniform_slices(...)``       every slice (sigma_k, sigma_k+1] with
+                                      reference ``solve_slice`` semantics
+                                      (fresh pool, rng seed_k, m = 2 count_k),
+                                      but each boundary shift is factored
+                                      once, slices run concurrently on
+                                      several CUDA streams of a GPU, and
+                                      across ranks (one process per GPU) the
+                                      slices are partitioned by LPT on their
+                                      inertia counts.  The only collectives
+                                      are all-gathers of the boundary
+                                      inertias and of the eigenvalues (plus
+                                      boundary pairs for de-duplication).
+"""
+from __future__ import annotations
+
+import math
+import threading
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+import torch
+
+from . import device as _dev
+from .eigensolver import (CountMismatch, SolverOptions, _Boundary, _Pencil, _Pool, _solve_interval)
+from .sparsela import CostCounters, Symbolic, mass_matvec, separator_ordering
+
+
+def uniform_shifts(lam_e: float, S: int) -> np.ndarray:
+    return np.array([k * lam_e / S for k in range(S + 1)])
+
+
+def kronecker_spectrum(system) -> np.ndarray:
+    """Sorted discrete eigenvalues from the Dirichlet-reduced 1D pencils."""
+    mus = [scipy.linalg.eigh(k.toarray(), m.toarray(), eigvals_only=True, driver="gvd")
+           for k, m in zip(system.k1d, system.m1d)]
+    lam = mus[0]
+    for mu in mus[1:]:
+        lam = np.add.outer(mu, lam).ravel()
+    return np.sort(lam)
+
+
+def choose_lambda_e(system, n0: int, lam: np.ndarray | None = None):
+    """(lam_e, count): midpoint of the first gap at or after the n0-th
+    eigenvalue; gaps within 1e-8 relative are cluster-internal."""
+    lam = kronecker_spectrum(system) if lam is None else lam
+    i = n0 - 1
+    while i + 1 < lam.size and lam[i + 1] - lam[i] <= 1e-8 * lam[i + 1]:
+        i += 1
+    if i + 1 >= lam.size:
+        return float(lam[-1] * (1 + 1e-6)), int(lam.size)
+    return 0.5 * float(lam[i] + lam[i + 1]), i + 1
+
+
+def lpt_assign(counts, world: int) -> list:
+    """Longest-processing-time assignment of slices to ranks."""
+    load = [0] * world
+    out = [[] for _ in range(world)]
+    for k in sorted(range(len(counts)), key=lambda k: (-counts[k], k)):
+        r = min(range(world), key=lambda r: (load[r], r))
+        out[r].append(k)
+        load[r] += max(counts[k], 1)
+    return [sorted(v) for v in out]
+
+
+@dataclass
+class SlicesResult:
+    shifts: np.ndarray            # boundaries actually used (after ZeroPivot nudges)
+    nu: np.ndarray                # inertia nu(sigma_k)
+    expected: np.ndarray          # per-slice counts from inertia
+    found: np.ndarray             # per-slice counts found (all ranks)
+    eigenvalues: np.ndarray       # all ranks, sorted
+    local_slices: list            # slice ids solved on this rank
+    local_eigenvalues: dict       # slice id -> eigenvalues
+    local_vectors: dict           # slice id -> vectors (rows; torch on device or numpy)
+    counters: CostCounters
+    timings: dict = field(default_factory=dict)
+    factor_ms: list = field(default_factory=list)
+
+
+def _allgather(obj, group_world):
+    if group_world <= 1:
+        return [obj]
+    import torch.distributed as dist
+
+    out = [None] * group_world
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams: int = 4,
+                         rank: int = 0, world: int = 1, vectors_to_host: bool = True,
+                         pencil_symbolic: Symbolic | None = None, perm=None,
+                         **opts) -> SlicesResult:
+    """Solve every slice (shifts[k], shifts[k+1]] (see module docstring)."""
+    t_all = time.perf_counter()
+    shifts = np.asarray(shifts, dtype=np.float64)
+    S = shifts.size - 1
+    seeds = list(range(S)) if seeds is None else list(seeds)
+    counters = CostCounters()
+    base_ctx = _dev.current()
+    if perm is None:
+        perm = separator_ordering(system)
+    sym = pencil_symbolic or Symbolic.on_device(system.device, perm)
+
+    def make_pencil(ctx, cnt):
+        p = _Pencil.__new__(_Pencil)
+        p.system, p.ctx, p.M, p.n = system, ctx, system.M, system.dof_count
+        p.perm, p.counters, p.symbolic = perm, cnt, sym
+        return p
+
+    # --- 1. boundary pass: each rank factors its share of the S+1 shifts ---
+    t0 = time.perf_counter()
+    mine_b = [k for k in range(S + 1) if k % world == rank]
+    bnd = {}
+    scale = float(shifts[-1] - shifts[0]) if S else 1.0
+    bcnt = CostCounters()
+    pen0 = make_pencil(base_ctx, bcnt)
+    kept = {}
+    with torch.cuda.stream(base_ctx.stream):
+        for k in mine_b:
+            sig, fact = pen0.factor(float(shifts[k]), scale)
+            bnd[k] = (sig, fact.n_negative, fact.device_ms)
+            if k < S:
+                kept[k] = (sig, fact)
+    counters.merge(bcnt)
+    counters.nsh += len(mine_b)
+    allb = {}
+    for part in _allgather(bnd, world):
+        allb.update(part)
+    sig_used = np.array([allb[k][0] for k in range(S + 1)])
+    nu = np.array([allb[k][1] for k in range(S + 1)], dtype=np.int64)
+    expected = np.diff(nu)
+    t_bnd = time.perf_counter() - t0
+
+    # --- 2. LPT assignment of slices to ranks -------------------------------
+    assign = lpt_assign(list(expected), world)
+    my = assign[rank]
+    # drop factors this rank does not need
+    kept = {k: v for k, v in kept.items() if k in my}
+
+    # --- 3. solve my slices concurrently on `streams` CUDA streams ----------
+    results = {}
+    errors = []
+    lock = threading.Lock()
+    queue = sorted(my, key=lambda k: -expected[k])
+
+    def worker(widx):
+        ctx = _dev.Context(base_ctx.device)
+        cnt = CostCounters()
+        with ctx:
+            while True:
+                with lock:
+                    if not queue:
+                        break
+                    k = queue.pop(0)
+                try:
+                    pen = make_pencil(ctx, cnt)
+                    lo, hi = float(sig_used[k]), float(sig_used[k + 1])
+                    if k in kept:
+                        lob = _Boundary(lo, int(nu[k]), kept[k][1])
+                    else:
+                        s2, f2 = pen.factor(lo, scale)
+                        lob = _Boundary(s2, f2.n_negative, f2)
+                        cnt.nsh += 1
+                    hib = _Boundary(hi, int(nu[k + 1]), None)
+                    count = int(expected[k])
+                    pool = _Pool()
+                    if count > 0:
+                        m = max(2, min(m_factor * count, system.dof_count))
+                        so = SolverOptions(m=m, **opts)
+                        rng = np.random.default_rng(seeds[k])
+                        _solve_interval(pen, lob, hib, pool, so, rng, scale)
+                    idx = sorted((i for i, lam in enumerate(pool.lams) if lob.sigma < lam <= hib.sigma),
+                                 key=lambda i: pool.lams[i])
+                    lams = np.array([pool.lams[i] for i in idx])
+                    if idx:
+                        X = torch.stack([pool.vecs[i] for i in idx])
+                        X = X.cpu().numpy() if vectors_to_host else X
+                    else:
+                        X = np.empty((0, system.dof_count))
+                    ctx.synchronize()
+                    with lock:
+                        results[k] = (lams, X)
+                except Exception as e:  # surfaced after join
+                    with lock:
+                        errors.append((k, e))
+        with lock:
+            counters.merge(cnt)
+
+    t0 = time.perf_counter()
+    nthreads = max(1, min(streams, len(my)))
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(nthreads)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        k, e = errors[0]
+        raise RuntimeError(f"slice {k} failed on rank {rank}: {e}") from e
+    t_sl = time.perf_counter() - t0
+
+    # --- 4. boundary de-duplication + global eigenvalue gather --------------
+    local_eigs = {k: results[k][0] for k in my}
+    near = {}
+    for k in my:
+        for j, lam in enumerate(results[k][0]):
+            for b in (k, k + 1):
+                if 0 < b < S and abs(lam - sig_used[b]) <= 1e-7 * max(abs(lam), 1.0):
+                    near.setdefault(b, []).append((k, j, float(lam)))
+    gathered = _allgather((local_eigs, near), world)
+    found = np.zeros(S, dtype=np.int64)
+    all_eigs = []
+    bnear = {}
+    for le, nr in gathered:
+        for k, v in le.items():
+            found[k] = v.size
+            all_eigs.append(v)
+        for b, lst in nr.items():
+            bnear.setdefault(b, []).extend(lst)
+    # duplicates can only arise from pairs of two adjacent slices sitting
+    # within 1e-7 of their shared boundary; inertia already fixes each
+    # slice's count, so a pair on both sides would show up as found > expected
+    for k in range(S):
+        if found[k] != expected[k]:
+            raise CountMismatch(f"slice {k} expected {expected[k]} found {found[k]}",
+                                interval=(sig_used[k], sig_used[k + 1]), expected=int(expected[k]),
+                                found=int(found[k]))
+    eig = np.sort(np.concatenate(all_eigs)) if all_eigs else np.empty(0)
+    res = SlicesResult(sig_used, nu, expected, found, eig, my, local_eigs,
+                       {k: results[k][1] for k in my}, counters)
+    res.timings = {"boundary_s": t_bnd, "slices_s": t_sl, "total_s": time.perf_counter() - t_all,
+                   "boundary_pairs": sum(len(v) for v in bnear.values())}
+    res.factor_ms = [allb[k][2] for k in range(S + 1)]
+    return res

@@ -1,0 +1,510 @@
+"""Sparse symmetric LDL^T, solves and mass products on the B200 engine.
+
+API mirror of /root/reference/pkg/src/rigaeig/sparsela.py (same names,
+argument meaning, exceptions and counter conventions):
+
+* factor_ldl   -> riga_symbolic_* (host C++, once per pattern) +
+                  riga_factor_create (multifrontal supernodal LDL^T on the
+                  device, FP64 tensor-core Schur updates, inertia from D)
+* solve_fb     -> riga_factor_solve (supernodal forward/backward sweeps)
+* mass_matvec  -> riga_spmv / riga_csr_spmv (CSR SpMV kernel)
+* separator_ordering / nested_dissection_graph stay on the host.
+
+FLOP conventions are the reference's (sparsela.py:1-17): factorization
+sum_j colcount_j^2 on the exact unamalgamated structure, solves
+2 fill_nnz, mat-vec 2 nnz.  ``LDLFactorization.permutation`` is the
+elimination order actually used: a postorder of the requested ordering's
+elimination tree (same fill, same column counts, same factor_flops).
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _lib
+from . import device as _dev
+from .assembly import DeviceSystem, DiscreteSystem, SymSparseMatrix
+from .bspline import separator_basis_indices
+
+
+class ZeroPivot(Exception):
+    """Pivot at or numerically at zero: the shift hit an eigenvalue."""
+
+
+class NegativeNorm(Exception):
+    """v^T M v < 0 for the mass inner product: M is not positive definite."""
+
+
+@dataclass
+class OpCounter:
+    flops: int = 0
+    calls: int = 0
+    seconds: float = 0.0
+
+    def add(self, flops: int, seconds: float) -> None:
+        self.flops += int(flops)
+        self.calls += 1
+        self.seconds += seconds
+
+    def merge(self, other: "OpCounter") -> None:
+        self.flops += other.flops
+        self.calls += other.calls
+        self.seconds += other.seconds
+
+
+@dataclass
+class CostCounters:
+    fact: OpCounter = field(default_factory=OpCounter)
+    fb: OpCounter = field(default_factory=OpCounter)
+    matvec: OpCounter = field(default_factory=OpCounter)
+    nsh: int = 0
+    nit: int = 0
+    retries: int = 0
+    steps_per_iteration: list = field(default_factory=list)
+
+    @property
+    def nfa(self) -> int:
+        return self.fact.calls
+
+    @property
+    def nfb(self) -> int:
+        return self.fb.calls
+
+    @property
+    def nmv(self) -> int:
+        return self.matvec.calls
+
+    def merge(self, other: "CostCounters") -> None:
+        self.fact.merge(other.fact)
+        self.fb.merge(other.fb)
+        self.matvec.merge(other.matvec)
+        self.nsh += other.nsh
+        self.nit += other.nit
+        self.retries += other.retries
+        self.steps_per_iteration.extend(other.steps_per_iteration)
+
+
+# ---------------------------------------------------------------------------
+# symbolic analysis (host C++ in the engine)
+# ---------------------------------------------------------------------------
+
+STAT_NAMES = ("fill_nnz", "factor_flops", "n_supernodes", "max_front", "n_levels",
+              "panel_entries", "cb_entries", "max_ncol", "fundamental_supernodes",
+              "stored_L_entries", "n_small_fronts", "n_large_fronts", "nnz_lower",
+              "tree_height", "relaxed_flops")
+
+
+class Symbolic:
+    """riga_symbolic handle: ordering + supernodal structure of one pattern."""
+
+    def __init__(self, handle, device_system: DeviceSystem | None, n: int):
+        self.handle = handle
+        self.system = device_system  # keeps the device pattern alive
+        self.n = n
+        st = np.zeros(16, np.int64)
+        _lib.check(_lib.lib().riga_symbolic_stats(handle, _lib.ptr(st)))
+        self.stats = {k: int(v) for k, v in zip(STAT_NAMES, st)}
+        self._order = None
+
+    @classmethod
+    def on_device(cls, dsys: DeviceSystem, perm: np.ndarray) -> "Symbolic":
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().riga_symbolic_create(dsys.handle, _lib.ptr(perm), ctypes.byref(h)),
+                   "symbolic")
+        return cls(h, dsys, dsys.n)
+
+    @classmethod
+    def host_only(cls, A, perm: np.ndarray) -> "Symbolic":
+        A = sp.csr_array(A)
+        A.sort_indices()
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        rp = np.ascontiguousarray(A.indptr, np.int64)
+        ci = np.ascontiguousarray(A.indices, np.int32)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().riga_symbolic_analyze(A.shape[0], _lib.ptr(rp), _lib.ptr(ci),
+                                                    _lib.ptr(perm), ctypes.byref(h)), "symbolic")
+        return cls(h, None, A.shape[0])
+
+    @property
+    def order(self) -> np.ndarray:
+        if self._order is None:
+            o = np.empty(self.n, np.int64)
+            _lib.check(_lib.lib().riga_symbolic_order(self.handle, _lib.ptr(o)))
+            self._order = o
+        return self._order
+
+    def colcounts(self) -> np.ndarray:
+        c = np.empty(self.n, np.int64)
+        _lib.check(_lib.lib().riga_symbolic_colcounts(self.handle, _lib.ptr(c)))
+        return c
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.lib().riga_symbolic_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# factorization
+# ---------------------------------------------------------------------------
+
+
+class LDLFactorization:
+    """P A P^T = L diag(D) L^T on the device (ref sparsela.py:178-203).
+
+    Attributes read by reference callers: ``n``, ``n_negative``,
+    ``inertia``, ``fill_nnz``, ``factor_flops``, ``permutation``, ``D``,
+    ``Lp``/``Li``/``Lx`` and ``l_matrix()`` (the latter materialised lazily
+    from the device panels).
+    """
+
+    def __init__(self, handle, symbolic: Symbolic, ctx, n_negative: int, sigma: float):
+        self.handle = handle
+        self.symbolic = symbolic
+        self.ctx = ctx
+        self.sigma = sigma
+        n = symbolic.n
+        self.inertia = (int(n_negative), 0, int(n - n_negative))
+        self.fill_nnz = symbolic.stats["fill_nnz"]
+        self.factor_flops = symbolic.stats["factor_flops"]
+        self._D = None
+        self._L = None
+        ms = ctypes.c_float(0)
+        _lib.lib().riga_factor_time_ms(handle, ctypes.byref(ms))
+        self.device_ms = float(ms.value)
+
+    @property
+    def n(self) -> int:
+        return self.symbolic.n
+
+    @property
+    def n_negative(self) -> int:
+        return self.inertia[0]
+
+    @property
+    def permutation(self) -> np.ndarray:
+        return self.symbolic.order
+
+    @property
+    def D(self) -> np.ndarray:
+        if self._D is None:
+            D = np.empty(self.n, np.float64)
+            _lib.check(_lib.lib().riga_factor_D(self.handle, _lib.ptr(D)))
+            self._D = D
+        return self._D
+
+    def _export(self):
+        if self._L is None:
+            m = self.symbolic.stats["stored_L_entries"]
+            Lp = np.empty(self.n + 1, np.int64)
+            Li = np.empty(m, np.int32)
+            Lx = np.empty(m, np.float64)
+            _lib.check(_lib.lib().riga_factor_export(self.handle, _lib.ptr(Lp), _lib.ptr(Li), _lib.ptr(Lx)))
+            self._L = (Lp, Li, Lx)
+        return self._L
+
+    @property
+    def Lp(self):
+        return self._export()[0]
+
+    @property
+    def Li(self):
+        return self._export()[1]
+
+    @property
+    def Lx(self):
+        return self._export()[2]
+
+    def l_matrix(self) -> sp.csc_array:
+        Lp, Li, Lx = self._export()
+        n = self.n
+        L = sp.csc_array((Lx, Li, Lp), shape=(n, n))
+        return sp.csc_array(L + sp.eye_array(n, format="csc"))
+
+    def solve_device(self, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        out = torch.empty_like(b) if out is None else out
+        _lib.check(_lib.lib().riga_factor_solve(self.handle, _lib.ptr(b), _lib.ptr(out)), "solve")
+        return out
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.lib().riga_factor_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def numeric_factor(symbolic: Symbolic, sigma: float, ctx=None, rel_zero_tol: float = 1e-14):
+    """Device LDL^T of K - sigma M on the symbolic's pattern; raises ZeroPivot."""
+    ctx = ctx or _dev.current()
+    h = ctypes.c_void_p()
+    neg = ctypes.c_int64(0)
+    bad = ctypes.c_int64(0)
+    st = _lib.lib().riga_factor_create(ctx.handle, symbolic.handle, float(sigma), rel_zero_tol,
+                                       ctypes.byref(h), ctypes.byref(neg), ctypes.byref(bad))
+    if st == _lib.ZERO_PIVOT:
+        msg = _lib.last_error()
+        if h.value:
+            _lib.lib().riga_factor_destroy(h)
+        raise ZeroPivot(msg)
+    _lib.check(st, "factor")
+    return LDLFactorization(h, symbolic, ctx, neg.value, sigma)
+
+
+def _as_csr(A) -> sp.csr_array:
+    if isinstance(A, SymSparseMatrix):
+        return A.csr
+    return sp.csr_array(A)
+
+
+def factor_ldl(A, ordering="nd", counters: CostCounters | None = None) -> LDLFactorization:
+    """Factor symmetric A as P A P^T = L D L^T without pivoting (ref :212-262).
+
+    ``ordering``: "natural", "nd" or an explicit permutation.  Raises
+    ZeroPivot on a pivot below 1e-14 max|A|, ValueError on bad arguments.
+    """
+    t0 = time.perf_counter()
+    if isinstance(A, SymSparseMatrix) and A.device is not None:
+        n = A.dimension
+    else:
+        A = _as_csr(A)
+        n = A.shape[0]
+    if isinstance(ordering, str):
+        if ordering == "natural":
+            perm = np.arange(n, dtype=np.int64)
+        elif ordering == "nd":
+            perm = nested_dissection_graph(_as_csr(A))
+        else:
+            raise ValueError(f"unknown ordering strategy {ordering!r}")
+    else:
+        perm = np.asarray(ordering, dtype=np.int64)
+        if perm.shape != (n,):
+            raise ValueError("permutation length does not match matrix dimension")
+    ctx = _dev.current()
+    if isinstance(A, SymSparseMatrix) and A.device is not None and A.which == 0:
+        dsys, sigma = A.device, 0.0
+    else:
+        csr = _as_csr(A)
+        if csr.nnz == 0 or not np.any(csr.data):
+            raise ZeroPivot("matrix is identically zero")
+        dsys, sigma = DeviceSystem.upload(ctx, csr), 0.0
+    sym = Symbolic.on_device(dsys, perm)
+    fact = numeric_factor(sym, sigma, ctx)
+    if counters is not None:
+        counters.fact.add(fact.factor_flops, time.perf_counter() - t0)
+    return fact
+
+
+def solve_fb(fact: LDLFactorization, b, counters: CostCounters | None = None):
+    """A^{-1} b (ref :265-277).  numpy in -> numpy out; torch CUDA in -> torch out."""
+    is_t = isinstance(b, torch.Tensor)
+    shape = tuple(b.shape) if is_t else np.shape(b)
+    if shape != (fact.n,):
+        raise ValueError(f"rhs has shape {shape}, expected ({fact.n},)")
+    t0 = time.perf_counter()
+    bd = _dev.to_device(b, fact.ctx)
+    with torch.cuda.stream(fact.ctx.stream):
+        x = fact.solve_device(bd)
+        out = x if is_t else _dev.to_host(x)
+    if counters is not None:
+        counters.fb.add(2 * fact.fill_nnz, time.perf_counter() - t0)
+    return out
+
+
+# device copies of host matrices handed to mass_matvec (keyed by id, weakly)
+_upload_cache: dict = {}
+
+
+def _device_matrix(M, ctx):
+    """(DeviceSystem, which) for a SymSparseMatrix or host CSR."""
+    if isinstance(M, SymSparseMatrix) and M.device is not None:
+        return M.device, M.which
+    csr = _as_csr(M)
+    key = (id(M), ctx.device)
+    hit = _upload_cache.get(key)
+    if hit is not None and hit[0]() is M:
+        return hit[1], 0
+    dsys = DeviceSystem.upload(ctx, csr)
+    try:
+        wr = weakref.ref(M)
+    except TypeError:
+        return dsys, 0
+    _upload_cache[key] = (wr, dsys)
+    return dsys, 0
+
+
+def mass_matvec(M, v, counters: CostCounters | None = None):
+    """y = M v on the device; charges 2 nnz(M) (ref :280-290)."""
+    is_t = isinstance(v, torch.Tensor)
+    n = M.dimension if isinstance(M, SymSparseMatrix) else _as_csr(M).shape[0]
+    shape = tuple(v.shape) if is_t else np.shape(v)
+    if shape != (n,):
+        raise ValueError(f"vector has shape {shape}, expected ({n},)")
+    ctx = _dev.current()
+    t0 = time.perf_counter()
+    dsys, which = _device_matrix(M, ctx)
+    vd = _dev.to_device(v, ctx)
+    with torch.cuda.stream(ctx.stream):
+        y = torch.empty_like(vd)
+        _lib.check(_lib.lib().riga_spmv(dsys.handle, which, 0.0, _lib.ptr(vd), _lib.ptr(y)), "spmv")
+        out = y if is_t else _dev.to_host(y)
+    if counters is not None:
+        counters.matvec.add(2 * dsys.nnz, time.perf_counter() - t0)
+    return out
+
+
+def m_inner(u, v, M=None) -> float:
+    """v^T M u (Euclidean when M is None); ref :293-297."""
+    if M is None:
+        if isinstance(u, torch.Tensor) or isinstance(v, torch.Tensor):
+            return float(torch.dot(_dev.to_device(v), _dev.to_device(u)))
+        return float(np.dot(v, u))
+    Mu = mass_matvec(M, u)
+    if isinstance(Mu, torch.Tensor):
+        return float(torch.dot(_dev.to_device(v), Mu))
+    return float(np.dot(v, Mu))
+
+
+def m_norm(v, M=None) -> float:
+    sq = m_inner(v, v, M)
+    if sq < -1e-12:
+        raise NegativeNorm(f"v^T M v = {sq} < 0")
+    return float(np.sqrt(max(sq, 0.0)))
+
+
+# ---------------------------------------------------------------------------
+# orderings (host)
+# ---------------------------------------------------------------------------
+
+
+def _c0_lines(system: DiscreteSystem):
+    return [separator_basis_indices(s) - 1 for s in system.spaces]
+
+
+def separator_ordering(system: DiscreteSystem) -> np.ndarray:
+    """Nested dissection aligned with the rIGA C0 planes (ref :319-392).
+
+    Each box is cut at the C0 interface nearest its middle (width one,
+    longest axis with a candidate first); without one, at a width-p slab in
+    the middle of its longest axis; boxes no longer than max(2p, 8) are
+    leaves.  Order: leaves (recursion order), then separators deepest first.
+    """
+    ext = [s.basis_count - 2 for s in system.spaces]
+    p = system.spaces[0].degree
+    d = system.dim
+    lines = _c0_lines(system)
+    strides = [int(np.prod(ext[:t])) for t in range(d)]
+    leaf = max(2 * p, 8)
+    leaves: list = []
+    seps: list = []
+
+    def cells(box):
+        idx = np.zeros(1, dtype=np.int64)
+        for t in range(d):
+            ax = np.arange(box[t][0], box[t][1], dtype=np.int64) * strides[t]
+            idx = (ax[:, None] + idx[None, :]).ravel()
+        return idx
+
+    stack = [(tuple((0, e) for e in ext), 0, False)]
+    # explicit stack: (box, depth, emitted_children) to avoid deep recursion
+    post = []
+    while stack:
+        box, depth, done = stack.pop()
+        if done:
+            post.append((box, depth))
+            continue
+        widths = [b - a for a, b in box]
+        cut = None
+        for t in sorted(range(d), key=lambda t: -widths[t]):
+            a, b = box[t]
+            cand = lines[t][(lines[t] >= a + 1) & (lines[t] <= b - 2)]
+            if cand.size:
+                c = int(cand[np.argmin(np.abs(cand - (a + b - 1) / 2.0))])
+                cut = (t, c, c + 1)
+                break
+        if cut is None:
+            t = int(np.argmax(widths))
+            if widths[t] <= leaf:
+                leaves.append(cells(box))
+                continue
+            a, b = box[t]
+            s0 = min(max(a + (widths[t] - p) // 2, a + 1), b - 1 - p)
+            cut = (t, s0, s0 + p)
+        t, s0, s1 = cut
+        lo = list(box); lo[t] = (box[t][0], s0)
+        hi = list(box); hi[t] = (s1, box[t][1])
+        mid = list(box); mid[t] = (s0, s1)
+        # children are visited left then right; the separator after both
+        stack.append((tuple(mid), depth, True))
+        stack.append((tuple(hi), depth + 1, False))
+        stack.append((tuple(lo), depth + 1, False))
+    for box, depth in post:
+        while len(seps) <= depth:
+            seps.append([])
+        seps[depth].append(cells(box))
+    chunks = leaves
+    for lev in reversed(seps):
+        chunks.extend(lev)
+    order = np.concatenate(chunks)
+    if order.size != system.dof_count:
+        raise AssertionError("dissection did not enumerate every DOF")
+    return order
+
+
+def nested_dissection_graph(pattern, leaf: int = 16) -> np.ndarray:
+    """BFS level-set nested dissection for non-tensor patterns (ref :395-447)."""
+    A = _as_csr(pattern)
+    n = A.shape[0]
+    ip, ix = A.indptr, A.indices
+    out = []
+    todo = [np.arange(n, dtype=np.int64)]
+    # process as the reference's recursion does: depth-first, low part first,
+    # separator appended after both halves -> emulate with an explicit stack
+    stack = [("visit", todo[0])]
+    while stack:
+        kind, vs = stack.pop()
+        if kind == "emit":
+            out.append(vs)
+            continue
+        if vs.size <= leaf:
+            out.append(vs)
+            continue
+        loc = np.full(n, -1, dtype=np.int64)
+        loc[vs] = np.arange(vs.size)
+        lev = np.full(vs.size, -1, dtype=np.int64)
+        lev[0] = 0
+        front, depth = [int(vs[0])], 0
+        while front:
+            nxt = []
+            for u in front:
+                for w in ix[ip[u]:ip[u + 1]]:
+                    lw = loc[w]
+                    if lw >= 0 and lev[lw] < 0:
+                        lev[lw] = depth + 1
+                        nxt.append(int(w))
+            front, depth = nxt, depth + 1
+        seen = lev >= 0
+        if not seen.all():
+            stack.append(("visit", vs[~seen]))
+            stack.append(("visit", vs[seen]))
+            continue
+        t = int(np.median(lev))
+        lo, hi = vs[lev < t], vs[lev > t]
+        if lo.size == 0 or hi.size == 0:
+            out.append(vs)
+            continue
+        stack.append(("emit", vs[lev == t]))
+        stack.append(("visit", hi))
+        stack.append(("visit", lo))
+    return np.concatenate(out)
