@@ -1,0 +1,398 @@
+"""Benchmark: eigenpairs/s of the spectrum-sliced shift-invert Lanczos solve.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3]
+                    [--impl ours|reference] [--streams S]
+
+One step = the whole hot path over the workload: factor every uniform
+shift (inertia), run restarted shift-invert Lanczos on every slice
+(sigma_k, sigma_k+1], lock every eigenpair the inertia promises, and bring
+eigenvalues + eigenvectors to the host.  Default workload: BASELINE
+configs[2] (cfg3: 2D 256x256 elements, p=4, rIGA BS=16, 16 uniform
+slices over [0, lam_e], first 2000 eigenpairs) -- the configuration the
+metric is quoted on "at 1/2/4/8 B200" with slices distributed across GPUs.
+
+``value`` is measured with the system resident in HBM; ``e2e`` through the
+public API from host CSR buffers (upload, ordering, symbolic, solve,
+eigenpairs to host).  ``--impl reference`` times the CPU oracle port of
+the reference path (oracle/, the reference is Python so nothing compiles
+into oracle/_ref) on the host cores, on a bounded sample of the workload.
+Multi-GPU: one process per GPU (torchrun); slices are partitioned by LPT
+over the boundary inertias (weak in the number of slices per GPU:
+"scaling" is "strong" -- the total work is fixed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+if "--impl" in sys.argv and "reference" in sys.argv:
+    # the reference's CPU path: one BLAS thread per worker process
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_FP64_TFLOPS = 37.16  # tools/fp64_peak.cu on this pool's B200 (DMMA m8n8k4 loop)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sample-q", type=int, default=8, help="eigenpairs per slice in the CPU sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(
+        os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle port of the reference path, bounded sample)
+# ---------------------------------------------------------------------------
+
+_W = {}
+
+
+def _worker_init(cfgname):
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(1)
+    except Exception:
+        pass
+    from oracle import rigaeig_port as O
+    from paper_2009_08167_b200.configs import CONFIGS
+
+    c = CONFIGS[cfgname]
+    _W["sys"] = O.build_system(c.d, c.ne, c.p, c.level)
+
+
+def _worker_task(task):
+    from oracle import rigaeig_port as O
+
+    k, lo, hi, q = task
+    t0 = time.perf_counter()
+    r = O.solve_slice(_W["sys"], (lo, hi), seed=k, m=2 * q)
+    return k, r.eigenvalues.size, r.expected_count, time.perf_counter() - t0
+
+
+def cpu_sample_tasks(cfgname, q):
+    """Bounded sample: the q lowest eigenpairs above every uniform shift."""
+    from oracle import rigaeig_port as O
+    from paper_2009_08167_b200.configs import CONFIGS
+
+    c = CONFIGS[cfgname]
+    lam = O.kronecker_spectrum(c.d, c.ne, c.p, c.level)
+    lam_e, _ = O.lambda_e_for(lam, c.n0)
+    tasks = []
+    for k in range(c.slices):
+        lo = k * lam_e / c.slices
+        i0 = int(np.sum(lam < lo))
+        i = i0 + q - 1
+        while i + 1 < lam.size and lam[i + 1] - lam[i] <= 1e-8 * lam[i + 1]:
+            i += 1
+        hi = 0.5 * (lam[i] + lam[i + 1])
+        tasks.append((k, lo, hi, i + 1 - i0))
+    return tasks
+
+
+def run_cpu_sample(cfgname, q, steps=1, warmup=0):
+    import multiprocessing as mp
+
+    tasks = cpu_sample_tasks(cfgname, q)
+    workers = min(os.cpu_count() or 1, len(tasks))
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    ctxmp = mp.get_context("spawn")
+    times = []
+    with ctxmp.Pool(workers, initializer=_worker_init, initargs=(cfgname,)) as pool:
+        for it in range(warmup + steps):
+            t0 = time.perf_counter()
+            out = pool.map(_worker_task, tasks, chunksize=1)
+            dt = time.perf_counter() - t0
+            for k, found, exp, _ in out:
+                if found != exp:
+                    raise RuntimeError(f"CPU sample slice {k}: {found} != {exp}")
+            if it >= warmup:
+                times.append(dt)
+    pairs = sum(t[3] for t in tasks)
+    return pairs, times, workers
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2009_08167_b200.configs import CONFIGS
+
+    c = CONFIGS[args.config]
+    pairs, times, workers = run_cpu_sample(args.config, args.sample_q, steps=args.steps,
+                                           warmup=min(args.warmup, 1))
+    t = float(np.mean(times))
+    v = pairs / t
+    sample = (f"{c.name}: the {args.sample_q} lowest eigenpairs above each of the {c.slices} uniform "
+              f"shifts ({pairs} pairs), oracle port of ref solve_slice (m = 2q), "
+              f"{workers} processes x 1 BLAS thread (ref cli.py:208-210 ProcessPool mode)")
+    line = {"impl": "reference", "metric": "eigenpairs/s", "value": v, "unit": "eigenpairs/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (deterministic pencil, seeded start vectors)",
+            "config": {"workload": c.text, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "eigenpairs/s", "cores": workers, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "eigenpairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        import subprocess
+
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ours(args):
+    import ctypes
+
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    import paper_2009_08167_b200 as P
+    from paper_2009_08167_b200 import _lib
+    from paper_2009_08167_b200 import device as D
+    from paper_2009_08167_b200.assembly import DeviceSystem, DiscreteSystem, SymSparseMatrix
+    from paper_2009_08167_b200.configs import CONFIGS
+    from paper_2009_08167_b200.sparsela import Symbolic
+
+    L = _lib.lib()
+    c = CONFIGS[args.config]
+    dev = torch.cuda.current_device()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t)
+        return float(t.item())
+
+    # ---- setup (untimed): device assembly, lam_e, ordering, symbolic -------
+    system = P.build_system(c.d, c.ne, c.p, c.level)
+    lam_e, count = P.choose_lambda_e(system, c.n0)
+    shifts = P.uniform_shifts(lam_e, c.slices)
+    perm = P.separator_ordering(system)
+    sym = Symbolic.on_device(system.device, perm)
+    seeds = list(range(c.slices))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{dev}")  # 256 MB > L2
+
+    def step():
+        return P.solve_uniform_slices(system, shifts, seeds=seeds, streams=args.streams, rank=rank,
+                                      world=world, pencil_symbolic=sym, perm=perm)
+
+    for _ in range(args.warmup):
+        r = step()
+        assert int(r.found.sum()) == count, (r.found, count)
+    # ---- timed region ------------------------------------------------------
+    times, found = [], 0
+    L.riga_prof_reset()
+    L.riga_prof_enable(1)
+    n0 = ctypes.c_int64()
+    L.riga_launch_count(ctypes.byref(n0))
+    clocks = ClockSampler(dev)
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = step()
+        torch.cuda.synchronize()
+        e1.record()
+        barrier()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+        found = int(r.found.sum())
+    clk = clocks.stop()
+    n1 = ctypes.c_int64()
+    L.riga_launch_count(ctypes.byref(n1))
+    L.riga_prof_enable(0)
+    ms = np.zeros(6)
+    work = np.zeros(6)
+    scopes = np.zeros(6, np.int64)
+    L.riga_prof_read(_lib.ptr(ms), _lib.ptr(work), _lib.ptr(scopes), 6)
+    t_step = max_over_ranks(float(np.mean(times)))
+    value = found / t_step
+    launches = int(sum_over_ranks(float(n1.value - n0.value)))
+    assert found == count, (found, count)
+
+    # ---- e2e through the public API from host buffers -----------------------
+    e2e = None
+    if not args.no_e2e:
+        Kh = system.K.csr.copy()
+        Mh = system.M.csr.copy()
+        h2d = Kh.nnz * (8 + 8 + 4) + (Kh.shape[0] + 1) * 8
+        ctx = D.current()
+        e2e_times, d2h = [], 0
+        for _ in range(max(1, min(args.steps, 2))):
+            flush.zero_()
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dsys = DeviceSystem.upload(ctx, Kh, Mh)
+            sys2 = DiscreteSystem(SymSparseMatrix(device=dsys, which=0), SymSparseMatrix(device=dsys, which=1),
+                                  system.spaces, system.dim, system.dof_count, system.k1d, system.m1d, dsys)
+            perm2 = P.separator_ordering(sys2)
+            r2 = P.solve_uniform_slices(sys2, shifts, seeds=seeds, streams=args.streams, rank=rank,
+                                        world=world, perm=perm2)
+            torch.cuda.synchronize()
+            e1.record()
+            barrier()
+            torch.cuda.synchronize()
+            e2e_times.append(e0.elapsed_time(e1) / 1e3)
+            d2h = sum(v.nbytes for v in r2.local_vectors.values()) + 8 * int(r2.found.sum())
+            assert int(r2.found.sum()) == count
+            del dsys, sys2, r2
+        te = max_over_ranks(float(np.mean(e2e_times)))
+        e2e = {"value": count / te, "unit": "eigenpairs/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(sum_over_ranks(d2h)), "ms_per_step": te * 1e3}
+
+    # ---- roofline ------------------------------------------------------------
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else open(os.devnull) as fh:
+        try:
+            peaks = json.load(fh)
+        except Exception:
+            peaks = {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    names = ["ldlt_factor", "supernodal_solve", "csr_spmv", "cgs2_pass", "vector_ops", "lift_restart"]
+    cats = {}
+    for i, nm in enumerate(names):
+        if scopes[i] == 0:
+            continue
+        t = ms[i] / 1e3
+        if i == 0:
+            ach = work[i] / t / 1e12
+            cats[nm] = {"device_ms": ms[i], "launch_groups": int(scopes[i]), "achieved": ach,
+                        "unit": "TFLOP/s", "peak": MEASURED_FP64_TFLOPS, "frac": ach / MEASURED_FP64_TFLOPS}
+        else:
+            ach = work[i] / t / 1e9
+            cats[nm] = {"device_ms": ms[i], "launch_groups": int(scopes[i]), "achieved": ach,
+                        "unit": "GB/s", "peak": hbm, "frac": ach / hbm}
+    dom = max(cats, key=lambda k: cats[k]["device_ms"])
+    d = cats[dom]
+    roofline = {"bound": "tensor" if dom == "ldlt_factor" else "hbm", "achieved": d["achieved"],
+                "peak": d["peak"], "unit": d["unit"], "frac": d["frac"], "traffic": None,
+                "kernel": dom, "peak_source": "tools/fp64_peak.cu (DMMA)" if dom == "ldlt_factor"
+                else f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
+                "per_launch_bytes": (work[names.index(dom)] / scopes[names.index(dom)])}
+
+    line = {"metric": "eigenpairs/s", "value": value, "unit": "eigenpairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic B-spline Laplace pencil; seeded standard-normal start vectors)",
+            "config": {"workload": c.text, "config": c.name, "d": c.d, "ne": c.ne, "p": c.p,
+                       "level": c.level, "N": system.dof_count, "eigenpairs": count, "slices": c.slices,
+                       "lambda_e": lam_e, "streams_per_gpu": args.streams,
+                       "parallelism": f"slices partitioned over {world} GPU(s) (LPT on inertia counts)",
+                       "l2": "working set > L2 (V+MV 2x251xNx8 B = 369 MB per slice); 256 MB flush between steps"},
+            "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "roofline_by_kernel": cats,
+            "ldlt": cats.get("ldlt_factor"), "clocks": clk,
+            "timing": {"per_step_s": times, "boundary_s": r.timings["boundary_s"],
+                       "slices_s": r.timings["slices_s"]}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        pairs, ctimes, workers = run_cpu_sample(args.config, args.sample_q, steps=1)
+        line["cpu_baseline"] = {"value": pairs / ctimes[0], "unit": "eigenpairs/s", "cores": workers,
+                                "kind": "port",
+                                "sample": f"{c.name}: the {args.sample_q} lowest eigenpairs above each uniform "
+                                          f"shift ({pairs} pairs), oracle port of ref solve_slice, "
+                                          f"{workers} processes x 1 BLAS thread"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

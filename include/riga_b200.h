@@ -110,6 +110,11 @@ int riga_symbolic_stats(riga_symbolic* sym, int64_t* stats16);
 int riga_symbolic_order(riga_symbolic* sym, int64_t* order_host);
 /* Exact column counts of L (diagonal included) in the caller's perm order. */
 int riga_symbolic_colcounts(riga_symbolic* sym, int64_t* counts_host);
+/* Supernode table (relaxed supernodes in postorder, n_supernodes entries
+ * each): first column, column count, front size, parent (-1 root), tree
+ * level (0 = leaf).  For analysis and tests.                              */
+int riga_symbolic_supernodes(riga_symbolic* sym, int64_t* col0, int64_t* ncol, int64_t* front,
+                             int64_t* parent, int64_t* level);
 int riga_symbolic_destroy(riga_symbolic* sym);
 
 /* ---- numeric multifrontal LDL^T of K - sigma M --------------------------
@@ -186,6 +191,17 @@ int riga_lanczos_project_locked(riga_lanczos* lz, double* x_dev, double* mx_dev,
 int riga_lanczos_gram(riga_lanczos* lz, double* G_host);
 /* Device pointers of V and MV (row-major, leading dimension *ld). */
 int riga_lanczos_basis(riga_lanczos* lz, double** V, double** MV, int64_t* ld);
+
+/* ---- measurement ---------------------------------------------------------
+ * Kernel launches issued by the engine since load (bench.py gpu_launches). */
+int riga_launch_count(int64_t* count);
+/* Per-category device timing with CUDA events on the launching stream:
+ * 0 factor (work = factor_flops), 1 solve (bytes 16 fill_nnz + 32 n),
+ * 2 SpMV (bytes 12 nnz + 4 (n+1) + 16 n), 3 CGS pass (bytes 2 rows n 8),
+ * 4 vector ops, 5 lift/restart.  read: ms, work, scope counts per category. */
+int riga_prof_enable(int on);
+int riga_prof_read(double* ms, double* work, int64_t* scopes, int ncat);
+int riga_prof_reset(void);
 
 /* ---- dense vector helpers on the device (stream of ctx) ----------------- */
 int riga_dot(riga_ctx* ctx, int64_t n, const double* x_dev, const double* y_dev, double* out_host);

@@ -45,6 +45,7 @@ SIGNATURES = {
     "riga_symbolic_stats": [_p, _p],
     "riga_symbolic_order": [_p, _p],
     "riga_symbolic_colcounts": [_p, _p],
+    "riga_symbolic_supernodes": [_p, _p, _p, _p, _p, _p],
     "riga_symbolic_destroy": [_p],
     "riga_factor_create": [_p, _p, _d, _d, _p, _p, _p],
     "riga_factor_solve": [_p, _p, _p],
@@ -68,6 +69,10 @@ SIGNATURES = {
     "riga_lanczos_gram": [_p, _p],
     "riga_lanczos_basis": [_p, _p, _p, _p],
     "riga_dot": [_p, _i64, _p, _p, _p],
+    "riga_launch_count": [_p],
+    "riga_prof_enable": [_i32],
+    "riga_prof_read": [_p, _p, _p, _i32],
+    "riga_prof_reset": [],
 }
 
 _LIB = None

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -40,38 +41,47 @@ const char* last_error();
     if (_s != RIGA_OK) return _s;   \
   } while (0)
 
-// Device buffer with RAII release (allocated on the owner's device).
+// Device buffer with RAII release.  Stream-ordered allocation
+// (cudaMallocAsync / cudaFreeAsync on the owner's stream): no device-wide
+// synchronisation, so concurrent slices on other streams keep running.
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
   }
-  int alloc(size_t count) {
+  int alloc(size_t count, cudaStream_t stream) {
     release();
+    s = stream;
     if (count == 0) return RIGA_OK;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    cudaError_t e = cudaMallocAsync(&p, count * sizeof(T), stream);
     if (e != cudaSuccess) {
       p = nullptr;
-      set_error(std::string("cudaMalloc of ") + std::to_string(count * sizeof(T)) +
+      set_error(std::string("cudaMallocAsync of ") + std::to_string(count * sizeof(T)) +
                 " bytes failed: " + cudaGetErrorString(e));
       return e == cudaErrorMemoryAllocation ? RIGA_OOM : RIGA_CUDA_ERROR;
     }
     n = count;
     return RIGA_OK;
   }
-  int upload(const T* host, size_t count, cudaStream_t s) {
-    int st = alloc(count);
-    if (st) return st;
-    if (count) RIGA_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  int upload(const T* host, size_t count, cudaStream_t st) {
+    int rc = alloc(count, st);
+    if (rc) return rc;
+    if (count) RIGA_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, st));
     return RIGA_OK;
+  }
+  void swap(DevBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(s, o.s);
   }
 };
 

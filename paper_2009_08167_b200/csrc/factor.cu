@@ -23,6 +23,7 @@
 #include "dmma.cuh"
 #include "internal.h"
 #include "kernels.cuh"
+#include "prof.h"
 
 namespace riga {
 
@@ -303,99 +304,6 @@ __global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restric
 }
 
 // ---------------------------------------------------------------------------
-// Supernodal solves, one CTA per supernode of a level.
-// ---------------------------------------------------------------------------
-__global__ void k_perm_gather(int64_t n, const int32_t* __restrict__ order,
-                              const double* __restrict__ b, double* __restrict__ xp) {
-  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k < n) xp[k] = b[order[k]];
-}
-__global__ void k_perm_scatter(int64_t n, const int32_t* __restrict__ order,
-                               const double* __restrict__ xp, double* __restrict__ x) {
-  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k < n) x[order[k]] = xp[k];
-}
-
-__global__ void __launch_bounds__(256) k_fwd(SymDev S, const int32_t* __restrict__ nodes,
-                                             const double* __restrict__ panel,
-                                             double* __restrict__ xp, double* __restrict__ upd) {
-  extern __shared__ double y[];
-  const int s = nodes[blockIdx.x];
-  const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
-  const double* P = panel + S.panel_off[s];
-  const int tid = threadIdx.x, lane = tid & 31;
-  for (int64_t i = tid; i < f; i += blockDim.x) y[i] = i < np ? xp[col0 + i] : 0.0;
-  __syncthreads();
-  for (int64_t t = S.child_ptr[s]; t < S.child_ptr[s + 1]; ++t) {
-    int c = S.child_list[t];
-    int64_t nuc = S.front[c] - S.ncol[c];
-    const int32_t* rp = S.relpos + S.upd_off[c];
-    const double* u = upd + S.upd_off[c];
-    for (int64_t a = tid; a < nuc; a += blockDim.x) y[rp[a]] += u[a];
-    __syncthreads();
-  }
-  for (int64_t kb = 0; kb < np; kb += 32) {
-    const int nbk = (int)imin(32, np - kb);
-    if (tid < 32) {
-      double yi = lane < nbk ? y[kb + lane] : 0.0;
-      for (int k = 0; k < nbk; ++k) {
-        double zk = __shfl_sync(0xffffffffu, yi, k);
-        if (lane > k && lane < nbk) yi -= P[(kb + k) * f + kb + lane] * zk;
-      }
-      if (lane < nbk) y[kb + lane] = yi;
-    }
-    __syncthreads();
-    for (int64_t i = kb + nbk + tid; i < f; i += blockDim.x) {
-      double acc = 0.0;
-      for (int k = 0; k < nbk; ++k) acc = fma(P[(kb + k) * f + i], y[kb + k], acc);
-      y[i] -= acc;
-    }
-    __syncthreads();
-  }
-  for (int64_t i = tid; i < np; i += blockDim.x) xp[col0 + i] = y[i];
-  double* u = upd + S.upd_off[s];
-  for (int64_t i = np + tid; i < f; i += blockDim.x) u[i - np] = y[i];
-}
-
-__global__ void __launch_bounds__(256) k_bwd(SymDev S, const int32_t* __restrict__ nodes,
-                                             const double* __restrict__ panel,
-                                             const double* __restrict__ D,
-                                             double* __restrict__ xp) {
-  extern __shared__ double y[];
-  const int s = nodes[blockIdx.x];
-  const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
-  const double* P = panel + S.panel_off[s];
-  const int32_t* rows = S.rows + S.rows_off[s];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
-  for (int64_t i = tid; i < f; i += blockDim.x)
-    y[i] = i < np ? xp[col0 + i] / D[col0 + i] : xp[rows[i]];
-  __syncthreads();
-  const int64_t nblk = (np + 31) / 32;
-  for (int64_t bi = nblk - 1; bi >= 0; --bi) {
-    const int64_t kb = bi * 32;
-    const int nbk = (int)imin(32, np - kb);
-    for (int c = w; c < nbk; c += nw) {
-      const double* Pc = P + (kb + c) * f;
-      double acc = 0.0;
-      for (int64_t i = kb + nbk + lane; i < f; i += 32) acc = fma(Pc[i], y[i], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) y[kb + c] -= acc;
-    }
-    __syncthreads();
-    if (tid < 32) {
-      double xc = lane < nbk ? y[kb + lane] : 0.0;
-      for (int k = nbk - 1; k >= 0; --k) {
-        double xk = __shfl_sync(0xffffffffu, xc, k);
-        if (lane < k) xc -= P[(kb + lane) * f + kb + k] * xk;
-      }
-      if (lane < nbk) y[kb + lane] = xc;
-    }
-    __syncthreads();
-  }
-  for (int64_t i = tid; i < np; i += blockDim.x) xp[col0 + i] = y[i];
-}
-
-// ---------------------------------------------------------------------------
 // host drivers
 // ---------------------------------------------------------------------------
 static int build_plan(riga_symbolic* sym) {
@@ -487,6 +395,7 @@ static int upload_symbolic(riga_symbolic* sym) {
   RIGA_TRY(up(sym->d_order, ord32, s));
   RIGA_TRY(up(sym->d_ea_items, sym->ea_items_host, s));
   RIGA_TRY(up(sym->d_large_nodes, sym->large_host, s));
+  RIGA_TRY(upload_solve_plan(sym, s));
   RIGA_CUDA(cudaStreamSynchronize(s));
   sym->on_device = true;
   return RIGA_OK;
@@ -498,9 +407,10 @@ static int set_smem_attrs() {
   int dev = 0, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  RIGA_CUDA(cudaFuncSetAttribute(k_small_front, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
-  RIGA_CUDA(cudaFuncSetAttribute(k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
-  RIGA_CUDA(cudaFuncSetAttribute(k_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  cudaFuncAttributes fa;
+  RIGA_CUDA(cudaFuncGetAttributes(&fa, k_small_front));
+  RIGA_CUDA(cudaFuncSetAttribute(k_small_front, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 maxsm - (int)fa.sharedSizeBytes));
   done = true;
   return RIGA_OK;
 }
@@ -511,13 +421,14 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   const SymbolicHost& h = sym->h;
   SymDev S = sym->dev();
   RIGA_TRY(set_smem_attrs());
+  ProfScope prof(kProfFactor, st, (double)h.factor_flops);
   double* scratch = nullptr;
   RIGA_CUDA(cudaMallocAsync(&scratch, 1024 * sizeof(double), st));
   RIGA_CUDA(cudaMemsetAsync(scratch, 0, 1024 * sizeof(double), st));
   int nb = (int)std::min<int64_t>(592, (sym->sys->nnz + 255) / 256);
   k_tol<<<std::max(nb, 1), 256, 0, st>>>(sym->sys->nnz, Kv, Mv, sigma, rel, scratch,
                                           reinterpret_cast<unsigned*>(scratch + 1000), F->tol.p,
-                                          F->stat.p, h.n);
+                                          F->stat.p, h.n); count_launch();
   RIGA_CUDA(cudaGetLastError());
   double* cbuf = nullptr;
   if (h.cb_total) RIGA_CUDA(cudaMallocAsync(&cbuf, h.cb_total * sizeof(double), st));
@@ -525,7 +436,7 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   if (h.cb_large) RIGA_CUDA(cudaMemsetAsync(cbuf, 0, h.cb_large * 8, st));
   if (sym->n_large) {
     k_asm_large<<<(unsigned)sym->n_large, 256, 0, st>>>(S, sym->d_large_nodes.p, Kv, Mv, sigma,
-                                                        F->panel.p);
+                                                        F->panel.p); count_launch();
     RIGA_CUDA(cudaGetLastError());
   }
   for (int64_t l = 0; l < h.nlevels; ++l) {
@@ -535,7 +446,7 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       if (!cnt) continue;
       dim3 g((unsigned)((P.ea_round_maxnu[r] + 31) / 32), (unsigned)cnt);
       if (g.x == 0) continue;
-      k_extend_add<<<g, 256, 0, st>>>(S, sym->d_ea_items.p + P.ea_round_begin[r], F->panel.p, cbuf);
+      k_extend_add<<<g, 256, 0, st>>>(S, sym->d_ea_items.p + P.ea_round_begin[r], F->panel.p, cbuf); count_launch();
       RIGA_CUDA(cudaGetLastError());
     }
     for (size_t c = 0; c + 1 < P.cls_begin.size(); ++c) {
@@ -545,7 +456,7 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       size_t smem = (size_t)fm * (fm | 1) * 8 + 2 * (size_t)fm * 8;
       k_small_front<<<(unsigned)cnt, 256, smem, st>>>(S, sym->d_level_nodes.p + P.cls_begin[c], Kv,
                                                        Mv, sigma, F->tol.p, F->panel.p, cbuf,
-                                                       F->D.p, F->stat.p);
+                                                       F->D.p, F->stat.p); count_launch();
       RIGA_CUDA(cudaGetLastError());
     }
     if (P.nlarge) {
@@ -554,19 +465,19 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       for (int64_t kb = 0; kb < P.max_np_large; kb += kNB) {
         unsigned rchunks = (unsigned)std::max<int64_t>(1, (P.max_f_large - kb + kPanelRows - 1) / kPanelRows);
         k_panel<<<dim3(rchunks, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p,
-                                                          F->D.p, F->stat.p);
+                                                          F->D.p, F->stat.p); count_launch();
         RIGA_CUDA(cudaGetLastError());
         int64_t m0 = kb + kNB;
         if (m0 < P.max_np_large) {
           int64_t ntj = (P.max_np_large - m0 + 63) / 64, nti = (P.max_f_large - m0 + 63) / 64;
           k_syrk<0><<<dim3((unsigned)(ntj * nti), nl), 128, 0, st>>>(S, ln, (int)kb, F->panel.p,
-                                                                    cbuf, F->D.p);
+                                                                    cbuf, F->D.p); count_launch();
           RIGA_CUDA(cudaGetLastError());
         }
       }
       if (P.max_nu_large > 0) {
         int64_t t = (P.max_nu_large + 63) / 64;
-        k_syrk<1><<<dim3((unsigned)(t * t), nl), 128, 0, st>>>(S, ln, 0, F->panel.p, cbuf, F->D.p);
+        k_syrk<1><<<dim3((unsigned)(t * t), nl), 128, 0, st>>>(S, ln, 0, F->panel.p, cbuf, F->D.p); count_launch();
         RIGA_CUDA(cudaGetLastError());
       }
     }
@@ -576,37 +487,16 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   return RIGA_OK;
 }
 
-int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x) {
-  riga_symbolic* sym = F->sym;
-  const SymbolicHost& h = sym->h;
-  SymDev S = sym->dev();
-  RIGA_TRY(set_smem_attrs());
-  unsigned g = (unsigned)((h.n + 255) / 256);
-  k_perm_gather<<<g, 256, 0, st>>>(h.n, sym->d_order.p, b, F->xperm.p);
-  for (int64_t l = 0; l < h.nlevels; ++l) {
-    const LevelPlan& P = sym->plan[l];
-    unsigned cnt = (unsigned)(h.level_ptr[l + 1] - h.level_ptr[l]);
-    k_fwd<<<cnt, 256, P.max_f * 8, st>>>(S, sym->d_level_nodes.p + P.begin, F->panel.p,
-                                          F->xperm.p, F->upd.p);
-  }
-  for (int64_t l = h.nlevels - 1; l >= 0; --l) {
-    const LevelPlan& P = sym->plan[l];
-    unsigned cnt = (unsigned)(h.level_ptr[l + 1] - h.level_ptr[l]);
-    k_bwd<<<cnt, 256, P.max_f * 8, st>>>(S, sym->d_level_nodes.p + P.begin, F->panel.p, F->D.p,
-                                          F->xperm.p);
-  }
-  k_perm_scatter<<<g, 256, 0, st>>>(h.n, sym->d_order.p, F->xperm.p, x);
-  RIGA_CUDA(cudaGetLastError());
-  return RIGA_OK;
-}
-
 }  // namespace riga
 
 using namespace riga;
 
 extern "C" {
 
-static int finish_symbolic(riga_symbolic* sym) { return build_plan(sym); }
+static int finish_symbolic(riga_symbolic* sym) {
+  RIGA_TRY(build_plan(sym));
+  return build_solve_plan(sym);
+}
 
 int riga_symbolic_analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx,
                           const int64_t* perm, riga_symbolic** out) {
@@ -668,6 +558,20 @@ int riga_symbolic_colcounts(riga_symbolic* sym, int64_t* counts) {
   return RIGA_OK;
 }
 
+int riga_symbolic_supernodes(riga_symbolic* sym, int64_t* col0, int64_t* ncol, int64_t* front,
+                             int64_t* parent, int64_t* level) {
+  RIGA_CHECK_ARG(sym, "null arg");
+  const SymbolicHost& h = sym->h;
+  for (int64_t s = 0; s < h.nsuper; ++s) {
+    if (col0) col0[s] = h.col0[s];
+    if (ncol) ncol[s] = h.ncol[s];
+    if (front) front[s] = h.front[s];
+    if (parent) parent[s] = h.sparent[s];
+    if (level) level[s] = h.level[s];
+  }
+  return RIGA_OK;
+}
+
 int riga_symbolic_destroy(riga_symbolic* sym) {
   if (!sym) return RIGA_OK;
   if (sym->ctx) {
@@ -692,12 +596,12 @@ int riga_factor_create(riga_ctx* ctx, riga_symbolic* sym, double sigma, double r
   F->ctx = ctx;
   F->sym = sym;
   F->sigma = sigma;
-  RIGA_TRY(F->panel.alloc(std::max<int64_t>(h.panel_total, 1)));
-  RIGA_TRY(F->D.alloc(h.n));
-  RIGA_TRY(F->xperm.alloc(h.n));
-  RIGA_TRY(F->upd.alloc(std::max<int64_t>(h.upd_total, 1)));
-  RIGA_TRY(F->stat.alloc(2));
-  RIGA_TRY(F->tol.alloc(2));
+  RIGA_TRY(F->panel.alloc(std::max<int64_t>(h.panel_total, 1), st));
+  RIGA_TRY(F->D.alloc(h.n, st));
+  RIGA_TRY(F->xperm.alloc(h.n, st));
+  RIGA_TRY(F->upd.alloc(std::max<int64_t>(h.upd_total, 1), st));
+  RIGA_TRY(F->stat.alloc(2, st));
+  RIGA_TRY(F->tol.alloc(2, st));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

@@ -34,6 +34,20 @@ struct LevelPlan {
   int64_t max_f = 0, max_np = 0;
 };
 
+struct I2 {
+  int32_t x, y;
+};
+
+// Task lists and pull map of the persistent solve kernels (solve.cu).
+struct SolvePlanHost {
+  std::vector<I2> fwd, bwd;  // tasks grouped by level
+  std::vector<int64_t> fwd_ptr, bwd_ptr, fwd_smem, bwd_smem;
+  std::vector<int32_t> nbp, flagoff, gsrc;
+  std::vector<int64_t> gptr;
+  int32_t nflags = 0;
+  int64_t sync_ints = 0;
+};
+
 struct riga_symbolic {
   riga_ctx* ctx = nullptr;
   riga_system* sys = nullptr;  // may be null (host-only analysis)
@@ -48,6 +62,10 @@ struct riga_symbolic {
   riga::DevBuf<int32_t> d_sparent, d_rows, d_relpos, d_child_list, d_asm_slot, d_asm_local;
   riga::DevBuf<int32_t> d_level_nodes, d_order, d_ea_items, d_large_nodes;
   int64_t n_large = 0;
+  SolvePlanHost sp;
+  riga::DevBuf<I2> d_tfwd, d_tbwd;
+  riga::DevBuf<int32_t> d_nbp, d_flagoff, d_gsrc;
+  riga::DevBuf<int64_t> d_gptr;
   SymDev dev() const {
     return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,
                   d_cb_off.p,   d_upd_off.p,   d_child_ptr.p,  d_asm_ptr.p,    d_sparent.p,
@@ -65,6 +83,8 @@ struct riga_factor {
   riga::DevBuf<double> xperm;  // solve workspace (n)
   riga::DevBuf<double> upd;    // solve contribution vectors (sum n_u)
   riga::DevBuf<int64_t> stat;  // [0] n_negative, [1] first bad pivot (n if none)
+  riga::DevBuf<int> sync;      // solve task tickets / completion flags
+  riga::DevBuf<double> cvec;   // backward L21^T x partial sums
   riga::DevBuf<double> tol;    // [0] max|A|, [1] zero_tol
   float factor_ms = 0.f;
 };
@@ -76,4 +96,6 @@ int system_spmv(riga_system* sys, cudaStream_t s, int which, double sigma, const
 int csr_spmv(cudaStream_t s, int64_t n, const int64_t* rowptr, const int32_t* colidx,
              const double* val, const double* x, double* y);
 int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x);
+int build_solve_plan(riga_symbolic* sym);
+int upload_solve_plan(riga_symbolic* sym, cudaStream_t s);
 }  // namespace riga

@@ -17,6 +17,7 @@
 
 #include "internal.h"
 #include "kernels.cuh"
+#include "prof.h"
 
 namespace riga {
 
@@ -214,24 +215,21 @@ int grow_locked(riga_lanczos* lz, int64_t need) {
   if (need <= lz->cap) return RIGA_OK;
   int64_t cap = std::max<int64_t>(8, lz->cap);
   while (cap < need) cap *= 2;
-  DevBuf<double> nL, nLM;
-  RIGA_TRY(nL.alloc(cap * lz->ld));
-  RIGA_TRY(nLM.alloc(cap * lz->ld));
   cudaStream_t s = lz->ctx->stream;
+  DevBuf<double> nL, nLM;
+  RIGA_TRY(nL.alloc(cap * lz->ld, s));
+  RIGA_TRY(nLM.alloc(cap * lz->ld, s));
   if (lz->nlocked) {
     RIGA_CUDA(cudaMemcpyAsync(nL.p, lz->L.p, lz->nlocked * lz->ld * 8, cudaMemcpyDeviceToDevice, s));
     RIGA_CUDA(cudaMemcpyAsync(nLM.p, lz->LM.p, lz->nlocked * lz->ld * 8, cudaMemcpyDeviceToDevice, s));
   }
-  RIGA_CUDA(cudaStreamSynchronize(s));
-  std::swap(lz->L.p, nL.p);
-  std::swap(lz->L.n, nL.n);
-  std::swap(lz->LM.p, nLM.p);
-  std::swap(lz->LM.n, nLM.n);
+  lz->L.swap(nL);
+  lz->LM.swap(nLM);
   lz->cap = cap;
   // coefficient / partial buffers sized for basis + locked rows
   int64_t R = lz->max_dim + 1 + cap;
-  RIGA_TRY(lz->coef.alloc(R));
-  RIGA_TRY(lz->partial.alloc((int64_t)lz->nblk * R));
+  RIGA_TRY(lz->coef.alloc(R, s));
+  RIGA_TRY(lz->partial.alloc((int64_t)lz->nblk * R, s));
   return RIGA_OK;
 }
 
@@ -244,10 +242,11 @@ int cgs(riga_lanczos* lz, int64_t kk, double* r, int passes) {
   Rows upd{lz->V.p, kk, lz->L.p, lz->nlocked, lz->ld};
   Rows none{nullptr, 0, nullptr, 0, lz->ld};
   for (int p = 0; p < passes; ++p) {
-    k_gemv_t<<<lz->nblk, 256, 0, s>>>(dots, lz->n, r, lz->partial.p);
-    k_reduce_rows<<<(unsigned)((R + 255) / 256), 256, 0, s>>>(R, lz->nblk, lz->partial.p, lz->coef.p);
+    ProfScope prof(kProfCgs, s, 2.0 * R * lz->n * 8.0);
+    k_gemv_t<<<lz->nblk, 256, 0, s>>>(dots, lz->n, r, lz->partial.p); count_launch();
+    k_reduce_rows<<<(unsigned)((R + 255) / 256), 256, 0, s>>>(R, lz->nblk, lz->partial.p, lz->coef.p); count_launch();
     k_gemv_n<<<(unsigned)((lz->n + 255) / 256), 256, R * 8, s>>>(upd, lz->n, lz->coef.p, r, none,
-                                                                 nullptr);
+                                                                 nullptr); count_launch();
   }
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
@@ -271,10 +270,11 @@ int read_scal(riga_lanczos* lz, int count) {
 int dot2(riga_lanczos* lz, const double* a, const double* b, const double* c, const double* d,
          int slot) {
   cudaStream_t s = lz->ctx->stream;
+  ProfScope prof(kProfVec, s, 32.0 * lz->n);
   int blocks = (int)std::min<int64_t>(296, (lz->n + 255) / 256);
   double* scratch = lz->scal.p + 16;
   k_dot2<<<blocks, 256, 0, s>>>(lz->n, a, b, c, d, scratch,
-                                reinterpret_cast<unsigned*>(lz->scal.p + 15), lz->scal.p + slot);
+                                reinterpret_cast<unsigned*>(lz->scal.p + 15), lz->scal.p + slot); count_launch();
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
 }
@@ -298,17 +298,18 @@ int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max
   lz->max_dim = std::min<int64_t>(max_dim, n);
   lz->nblk = (int)((lz->n + kChunk - 1) / kChunk);
   int64_t rows = lz->max_dim + 1;
-  RIGA_TRY(lz->V.alloc(rows * lz->ld));
-  RIGA_TRY(lz->MV.alloc(rows * lz->ld));
+  cudaStream_t cs = ctx->stream;
+  RIGA_TRY(lz->V.alloc(rows * lz->ld, cs));
+  RIGA_TRY(lz->MV.alloc(rows * lz->ld, cs));
   RIGA_CUDA(cudaMemsetAsync(lz->V.p, 0, rows * lz->ld * 8, ctx->stream));
   RIGA_CUDA(cudaMemsetAsync(lz->MV.p, 0, rows * lz->ld * 8, ctx->stream));
-  RIGA_TRY(lz->w.alloc(lz->ld));
-  RIGA_TRY(lz->r.alloc(lz->ld));
-  RIGA_TRY(lz->Mr.alloc(lz->ld));
-  RIGA_TRY(lz->tmp.alloc(lz->ld));
-  RIGA_TRY(lz->scal.alloc(16 + 2 * 296 + 16));
+  RIGA_TRY(lz->w.alloc(lz->ld, cs));
+  RIGA_TRY(lz->r.alloc(lz->ld, cs));
+  RIGA_TRY(lz->Mr.alloc(lz->ld, cs));
+  RIGA_TRY(lz->tmp.alloc(lz->ld, cs));
+  RIGA_TRY(lz->scal.alloc(16 + 2 * 296 + 16, cs));
   RIGA_CUDA(cudaMemsetAsync(lz->scal.p, 0, lz->scal.n * 8, ctx->stream));
-  RIGA_TRY(lz->cpl.alloc(rows));
+  RIGA_TRY(lz->cpl.alloc(rows, cs));
   RIGA_TRY(grow_locked(lz.get(), 8));
   RIGA_CUDA(cudaMallocHost(&lz->hbuf, std::max<int64_t>(64, 3 * rows + 8) * 8));
   RIGA_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -359,7 +360,7 @@ int riga_lanczos_set_start(riga_lanczos* lz, const double* r_host) {
   double* vk = lz->V.p + lz->k * lz->ld;
   double* mvk = lz->MV.p + lz->k * lz->ld;
   k_normalize2<<<(unsigned)((lz->n + 255) / 256), 256, 0, s>>>(lz->n, lz->scal.p, 0, lz->r.p, vk,
-                                                               lz->Mr.p, mvk);
+                                                               lz->Mr.p, mvk); count_launch();
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
 }
@@ -382,7 +383,7 @@ int riga_lanczos_fresh(riga_lanczos* lz, const double* r_host, int* accepted) {
     double* vk = lz->V.p + lz->k * lz->ld;
     double* mvk = lz->MV.p + lz->k * lz->ld;
     k_normalize2<<<(unsigned)((lz->n + 255) / 256), 256, 0, s>>>(lz->n, lz->scal.p, 0, lz->r.p, vk,
-                                                                 lz->Mr.p, mvk);
+                                                                 lz->Mr.p, mvk); count_launch();
     RIGA_CUDA(cudaGetLastError());
   }
   return RIGA_OK;
@@ -412,7 +413,7 @@ int step_core(riga_lanczos* lz, int64_t clo, double breakdown_tol, double* a_out
   const double* v = lz->V.p + k * ld;
   const double* Mv = lz->MV.p + k * ld;
   RIGA_TRY(dot2(lz, Mv, lz->w.p, lz->w.p, lz->w.p, 0));  // alpha, |w|^2
-  k_residual<<<g1, 256, 0, s>>>(n, lz->w.p, v, lz->scal.p, lz->V.p, ld, clo, k, lz->cpl.p, lz->r.p);
+  k_residual<<<g1, 256, 0, s>>>(n, lz->w.p, v, lz->scal.p, lz->V.p, ld, clo, k, lz->cpl.p, lz->r.p); count_launch();
   RIGA_TRY(cgs(lz, k + 1, lz->r.p, 2));
   RIGA_TRY(mass_apply(lz, lz->r.p, lz->Mr.p));
   RIGA_TRY(dot2(lz, lz->r.p, lz->Mr.p, lz->r.p, lz->Mr.p, 2));  // beta^2
@@ -425,7 +426,7 @@ int step_core(riga_lanczos* lz, int64_t clo, double breakdown_tol, double* a_out
   lz->k = k + 1;
   if (b <= std::max(breakdown_tol, 1e-13 * wn)) return RIGA_BREAKDOWN;
   k_normalize2<<<g1, 256, 0, s>>>(n, lz->scal.p, 2, lz->r.p, lz->V.p + (k + 1) * ld, lz->Mr.p,
-                                  lz->MV.p + (k + 1) * ld);
+                                  lz->MV.p + (k + 1) * ld); count_launch();
   lz->hbuf[8] = b;  // next step's coupling: beta e_k
   RIGA_CUDA(cudaMemcpyAsync(lz->cpl.p + k, lz->hbuf + 8, 8, cudaMemcpyHostToDevice, s));
   RIGA_CUDA(cudaGetLastError());
@@ -483,9 +484,10 @@ int riga_lanczos_step_given(riga_lanczos* lz, const double* w_dev, const double*
 static int lift_rows(riga_lanczos* lz, const double* Vb, int64_t k, const double* Wd, int64_t c,
                      double* X) {
   cudaStream_t s = lz->ctx->stream;
+  ProfScope prof(kProfLift, s, 8.0 * (double)k * lz->n * ((c + 7) / 8));
   const unsigned g1 = (unsigned)((lz->n + 255) / 256);
   for (int64_t q0 = 0; q0 < c; q0 += 8) {
-    k_lift<8><<<g1, 256, k * 8 * 8, s>>>(lz->n, Vb, lz->ld, k, Wd, q0, c, X, lz->ld);
+    k_lift<8><<<g1, 256, k * 8 * 8, s>>>(lz->n, Vb, lz->ld, k, Wd, q0, c, X, lz->ld); count_launch();
   }
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
@@ -497,11 +499,10 @@ int riga_lanczos_lift(riga_lanczos* lz, const double* W_host, int64_t c, double*
   DeviceGuard g(lz->ctx->device);
   cudaStream_t s = lz->ctx->stream;
   int64_t k = lz->k;
-  RIGA_TRY(lz->Wd.alloc(std::max<int64_t>(k * c, 1)));
+  RIGA_TRY(lz->Wd.alloc(std::max<int64_t>(k * c, 1), s));
   RIGA_CUDA(cudaMemcpyAsync(lz->Wd.p, W_host, k * c * 8, cudaMemcpyHostToDevice, s));
   RIGA_TRY(lift_rows(lz, lz->V.p, k, lz->Wd.p, c, X));
   RIGA_TRY(lift_rows(lz, lz->MV.p, k, lz->Wd.p, c, MX));
-  RIGA_CUDA(cudaStreamSynchronize(s));  // Wd reused by the caller's next call
   return RIGA_OK;
 }
 
@@ -513,9 +514,9 @@ int riga_lanczos_restart(riga_lanczos* lz, const double* W_host, int64_t c) {
   if (c > 0) {
     RIGA_CHECK_ARG(W_host, "null weights");
     DevBuf<double> nv, nmv;
-    RIGA_TRY(nv.alloc(c * ld));
-    RIGA_TRY(nmv.alloc(c * ld));
-    RIGA_TRY(lz->Wd.alloc(k * c));
+    RIGA_TRY(nv.alloc(c * ld, s));
+    RIGA_TRY(nmv.alloc(c * ld, s));
+    RIGA_TRY(lz->Wd.alloc(k * c, s));
     RIGA_CUDA(cudaMemcpyAsync(lz->Wd.p, W_host, k * c * 8, cudaMemcpyHostToDevice, s));
     RIGA_TRY(lift_rows(lz, lz->V.p, k, lz->Wd.p, c, nv.p));
     RIGA_TRY(lift_rows(lz, lz->MV.p, k, lz->Wd.p, c, nmv.p));
@@ -542,9 +543,9 @@ int riga_lanczos_project_locked(riga_lanczos* lz, double* x, double* mx, int pas
   Rows upd{lz->L.p, R, nullptr, 0, lz->ld};
   Rows upd2{lz->LM.p, R, nullptr, 0, lz->ld};
   for (int p = 0; p < passes; ++p) {
-    k_gemv_t<<<lz->nblk, 256, 0, s>>>(dots, lz->n, x, lz->partial.p);
-    k_reduce_rows<<<(unsigned)((R + 255) / 256), 256, 0, s>>>(R, lz->nblk, lz->partial.p, lz->coef.p);
-    k_gemv_n<<<(unsigned)((lz->n + 255) / 256), 256, R * 8, s>>>(upd, lz->n, lz->coef.p, x, upd2, mx);
+    k_gemv_t<<<lz->nblk, 256, 0, s>>>(dots, lz->n, x, lz->partial.p); count_launch();
+    k_reduce_rows<<<(unsigned)((R + 255) / 256), 256, 0, s>>>(R, lz->nblk, lz->partial.p, lz->coef.p); count_launch();
+    k_gemv_n<<<(unsigned)((lz->n + 255) / 256), 256, R * 8, s>>>(upd, lz->n, lz->coef.p, x, upd2, mx); count_launch();
   }
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
@@ -559,8 +560,8 @@ int riga_lanczos_gram(riga_lanczos* lz, double* G) {
   Rows dots{lz->MV.p, k, nullptr, 0, lz->ld};
   std::vector<double> row(k);
   for (int64_t i = 0; i < k; ++i) {
-    k_gemv_t<<<lz->nblk, 256, 0, s>>>(dots, lz->n, lz->V.p + i * lz->ld, lz->partial.p);
-    k_reduce_rows<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(k, lz->nblk, lz->partial.p, lz->coef.p);
+    k_gemv_t<<<lz->nblk, 256, 0, s>>>(dots, lz->n, lz->V.p + i * lz->ld, lz->partial.p); count_launch();
+    k_reduce_rows<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(k, lz->nblk, lz->partial.p, lz->coef.p); count_launch();
     RIGA_CUDA(cudaMemcpyAsync(G + i * k, lz->coef.p, k * 8, cudaMemcpyDeviceToHost, s));
     RIGA_CUDA(cudaStreamSynchronize(s));
   }

@@ -7,6 +7,7 @@
 
 #include "internal.h"
 #include "kernels.cuh"
+#include "prof.h"
 
 namespace riga {
 
@@ -123,6 +124,7 @@ int csr_spmv_impl(cudaStream_t s, int64_t n, const int64_t* rp, const int32_t* c
                   const double* B, double sigma, int mode, int64_t nnz, const double* x,
                   double* y) {
   if (n == 0) return RIGA_OK;
+  ProfScope prof(kProfSpmv, s, 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n);
   double avg = double(nnz) / double(n);
   int lanes = avg >= 48 ? 32 : (avg >= 20 ? 16 : (avg >= 8 ? 8 : 4));
   int64_t threads = n * lanes;
@@ -141,6 +143,7 @@ int csr_spmv_impl(cudaStream_t s, int64_t n, const int64_t* rp, const int32_t* c
     RIGA_SPMV_CASE(32)
   }
 #undef RIGA_SPMV_CASE
+  count_launch();
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
 }
@@ -207,7 +210,7 @@ int launch_dot(cudaStream_t s, int64_t n, const double* x, const double* y, doub
   int blocks = (int)std::min<int64_t>(592, std::max<int64_t>(1, (n + 255) / 256));
   double* partial = out_dev + 1;
   unsigned* ticket = reinterpret_cast<unsigned*>(out_dev + 1 + 592);
-  k_dot<<<blocks, 256, 0, s>>>(n, x, y, partial, ticket, out_dev);
+  k_dot<<<blocks, 256, 0, s>>>(n, x, y, partial, ticket, out_dev); count_launch();
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
 }
@@ -246,6 +249,14 @@ int riga_ctx_create(int device, void* stream_handle, riga_ctx** out) {
   }
   RIGA_CHECK_ARG(device >= 0 && device < c, "device index out of range");
   DeviceGuard g(device);
+  {
+    // keep freed stream-ordered allocations cached in the device pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   auto* ctx = new riga_ctx();
   ctx->device = device;
   if (stream_handle) {
@@ -344,17 +355,17 @@ int riga_system_assemble_kron(riga_ctx* ctx, int dim, const int64_t* n1,
   sys->ctx = ctx;
   sys->n = n;
   sys->nnz = nnz;
-  RIGA_TRY(sys->rowptr.alloc(n + 1));
-  RIGA_TRY(sys->colidx.alloc(nnz));
-  RIGA_TRY(sys->K.alloc(nnz));
-  RIGA_TRY(sys->M.alloc(nnz));
+  RIGA_TRY(sys->rowptr.alloc(n + 1, s));
+  RIGA_TRY(sys->colidx.alloc(nnz, s));
+  RIGA_TRY(sys->K.alloc(nnz, s));
+  RIGA_TRY(sys->M.alloc(nnz, s));
   RIGA_CUDA(cudaMemsetAsync(sys->rowptr.p, 0, sizeof(int64_t), s));
   k_kron_rowptr<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dim, ax[0], ax[1], ax[2], n,
-                                                            sys->rowptr.p + 1);
+                                                            sys->rowptr.p + 1); count_launch();
   RIGA_CUDA(cudaGetLastError());
   RIGA_TRY(inclusive_scan_i64(s, sys->rowptr.p + 1, n));
   k_kron_values<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
-      dim, ax[0], ax[1], ax[2], n, sys->rowptr.p, sys->colidx.p, sys->K.p, sys->M.p);
+      dim, ax[0], ax[1], ax[2], n, sys->rowptr.p, sys->colidx.p, sys->K.p, sys->M.p); count_launch();
   RIGA_CUDA(cudaGetLastError());
   RIGA_CUDA(cudaStreamSynchronize(s));
   *out = sys.release();

@@ -140,6 +140,14 @@ class Symbolic:
             self._order = o
         return self._order
 
+    def supernodes(self) -> dict:
+        """Relaxed supernode table: col0, ncol, front, parent, level."""
+        ns = self.stats["n_supernodes"]
+        arrs = {k: np.empty(ns, np.int64) for k in ("col0", "ncol", "front", "parent", "level")}
+        _lib.check(_lib.lib().riga_symbolic_supernodes(self.handle, *[_lib.ptr(arrs[k]) for k in
+                                                                     ("col0", "ncol", "front", "parent", "level")]))
+        return arrs
+
     def colcounts(self) -> np.ndarray:
         c = np.empty(self.n, np.int64)
         _lib.check(_lib.lib().riga_symbolic_colcounts(self.handle, _lib.ptr(c)))

@@ -1,0 +1,74 @@
+"""Aggregate Lanczos-step throughput with T host threads x T streams.
+
+    python tools/concurrency_probe.py [--config cfg3] [--steps 100]
+"""
+import argparse
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2009_08167_b200 as P  # noqa: E402
+from paper_2009_08167_b200 import device as D  # noqa: E402
+from paper_2009_08167_b200.configs import CONFIGS  # noqa: E402
+from paper_2009_08167_b200.eigensolver import DeviceShiftInvert  # noqa: E402
+from paper_2009_08167_b200.sparsela import Symbolic, numeric_factor  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--what", default="extend", choices=["extend", "solve"])
+    a = ap.parse_args()
+    c = CONFIGS[a.config]
+    s = P.build_system(c.d, c.ne, c.p, c.level)
+    lam_e, _ = P.choose_lambda_e(s, c.n0)
+    sh = P.uniform_shifts(lam_e, c.slices)
+    sym = Symbolic.on_device(s.device, P.separator_ordering(s))
+    for T in (1, 2, 4, 8, 16):
+        ctxs = [D.Context() for _ in range(T)]
+        facts, states = [], []
+        for i, ctx in enumerate(ctxs):
+            with ctx:
+                f = numeric_factor(sym, float(sh[i % c.slices]), ctx)
+                st = P.LanczosState(DeviceShiftInvert(f, s.M), s.dof_count, mass=s.M, shift=f.sigma,
+                                    max_dim=a.steps + 1, rng=np.random.default_rng(i), ctx=ctx)
+                facts.append(f)
+                states.append(st)
+        torch.cuda.synchronize()
+        bar = threading.Barrier(T)
+
+        def work(i):
+            bar.wait()
+            with ctxs[i]:
+                if a.what == "extend":
+                    P.lanczos_extend(states[i], a.steps)
+                else:
+                    b = torch.randn(s.dof_count, dtype=torch.float64, device="cuda")
+                    x = torch.empty_like(b)
+                    for _ in range(a.steps):
+                        facts[i].solve_device(b, x)
+                ctxs[i].synchronize()
+
+        th = [threading.Thread(target=work, args=(i,)) for i in range(T)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        dt = time.perf_counter() - t0
+        print(f"{a.what} threads={T:2d}: {T * a.steps / dt:8.1f} steps/s aggregate, "
+              f"{dt * 1e3 / a.steps:7.3f} ms per step per thread", flush=True)
+        del facts, states, ctxs
+        torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
