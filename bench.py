@@ -28,6 +28,8 @@ import os
 import sys
 import time
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # many concurrent slice streams
+
 if "--impl" in sys.argv and "reference" in sys.argv:
     # the reference's CPU path: one BLAS thread per worker process
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
@@ -48,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--streams", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sample-q", type=int, default=8, help="eigenpairs per slice in the CPU sample")

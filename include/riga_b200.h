@@ -186,6 +186,14 @@ int riga_lanczos_restart(riga_lanczos* lz, const double* W_host, int64_t c);
 /* In-place projection of (x, mx) against the locked set, `passes` times:
  * c = LM x; x -= L^T c; mx -= LM^T c (ref _sweep locking block :491-505).  */
 int riga_lanczos_project_locked(riga_lanczos* lz, double* x_dev, double* mx_dev, int passes);
+/* Lock c converged pairs (rows of X / MX, row stride ldx, device) in order,
+ * exactly as the reference's locking loop (ref _sweep :483-523): M-normalise,
+ * two projections against the locked set (which grows by the pairs accepted
+ * earlier in the batch), reject when the projected norm is < 0.3, else
+ * re-normalise and append.  X / MX are updated in place; accepted[q] = 0/1
+ * (host).  One host synchronisation for the whole batch.                  */
+int riga_lanczos_lock_batch(riga_lanczos* lz, double* X_dev, double* MX_dev, int64_t c, int64_t ldx,
+                            int* accepted);
 /* Gram matrix G = V[:k] MV[:k]^T to host (k x k row-major) for the
  * DEBUG_INVARIANTS checks (ref check_invariants :276-282).                 */
 int riga_lanczos_gram(riga_lanczos* lz, double* G_host);

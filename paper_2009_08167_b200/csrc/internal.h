@@ -40,12 +40,13 @@ struct I2 {
 
 // Task lists and pull map of the persistent solve kernels (solve.cu).
 struct SolvePlanHost {
-  std::vector<I2> fwd, bwd;  // tasks grouped by level
-  std::vector<int64_t> fwd_ptr, bwd_ptr, fwd_smem, bwd_smem;
-  std::vector<int32_t> nbp, flagoff, gsrc;
+  std::vector<I2> fwd, bwd;        // light tasks grouped by level
+  std::vector<int32_t> chains;     // large supernodes grouped by level
+  std::vector<int32_t> wholes;     // small supernodes (warp tasks) grouped by level
+  std::vector<int64_t> fwd_ptr, bwd_ptr, chain_ptr;
+  std::vector<int64_t> fwd_smem, bwd_smem, chf_smem, chb_smem;  // bytes per level launch
+  std::vector<int32_t> gsrc;
   std::vector<int64_t> gptr;
-  int32_t nflags = 0;
-  int64_t sync_ints = 0;
 };
 
 struct riga_symbolic {
@@ -64,7 +65,7 @@ struct riga_symbolic {
   int64_t n_large = 0;
   SolvePlanHost sp;
   riga::DevBuf<I2> d_tfwd, d_tbwd;
-  riga::DevBuf<int32_t> d_nbp, d_flagoff, d_gsrc;
+  riga::DevBuf<int32_t> d_chains, d_wholes, d_gsrc;
   riga::DevBuf<int64_t> d_gptr;
   SymDev dev() const {
     return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,
@@ -83,7 +84,6 @@ struct riga_factor {
   riga::DevBuf<double> xperm;  // solve workspace (n)
   riga::DevBuf<double> upd;    // solve contribution vectors (sum n_u)
   riga::DevBuf<int64_t> stat;  // [0] n_negative, [1] first bad pivot (n if none)
-  riga::DevBuf<int> sync;      // solve task tickets / completion flags
   riga::DevBuf<double> cvec;   // backward L21^T x partial sums
   riga::DevBuf<double> tol;    // [0] max|A|, [1] zero_tol
   float factor_ms = 0.f;
@@ -95,7 +95,9 @@ int launch_dot(cudaStream_t s, int64_t n, const double* x, const double* y, doub
 int system_spmv(riga_system* sys, cudaStream_t s, int which, double sigma, const double* x, double* y);
 int csr_spmv(cudaStream_t s, int64_t n, const int64_t* rowptr, const int32_t* colidx,
              const double* val, const double* x, double* y);
-int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x);
+int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x,
+                 bool b_permuted = false);
 int build_solve_plan(riga_symbolic* sym);
+int prepare_solve();
 int upload_solve_plan(riga_symbolic* sym, cudaStream_t s);
 }  // namespace riga

@@ -9,8 +9,15 @@
 // Layout: V and MV are (max_dim+1) rows of ld >= n doubles (row-major, each
 // basis vector contiguous); the pending normalised direction r (and M r)
 // always sits in row k.  Locked vectors L, LM: rows of ld doubles.
-// Reductions are two-phase with a fixed summation order (bitwise
-// reproducible run to run).
+//
+// The recurrence state (k, coupling window, locked count, stop flag) lives
+// in device memory (LzDev), so one Lanczos step -- permuted gather, the
+// supernodal solve, alpha/|w| dots, residual, CGS2 against basis + locked
+// set, M-SpMV, beta, normalisation -- is a fixed kernel sequence that is
+// captured once as a CUDA graph and replayed; the host syncs once per
+// extend.  A breakdown sets the stop flag and the remaining replays are
+// no-ops.  Reductions are two-phase with a fixed order (bitwise
+// reproducible).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -23,95 +30,176 @@ namespace riga {
 
 constexpr int kChunk = 512;  // columns per CTA in the tall-skinny GEMV
 
-struct Rows {  // up to two row blocks of one GEMV (basis + locked set)
-  const double* a;
-  int64_t na;
-  const double* b;
-  int64_t nb;
-  int64_t ld;
+struct LzDev {
+  int k;        // basis size; the pending direction sits in row k
+  int clo;      // coupling window [clo, k) applied by the next step
+  int nlocked;  // locked rows
+  int stop;     // 1 = breakdown, 2 = limit reached (later replays are no-ops)
+  int limit;    // extend target
+  int steps;    // steps executed since the last upload
+  int pad[2];
+  double btol;     // breakdown tolerance
+  double scal[8];  // [0] alpha, [1] |w|^2, [2] beta^2, [4] ref norm^2
 };
 
-// partial[blk * R + i] = sum_{c in chunk(blk)} row_i[c] * x[c],  R = na + nb
-__global__ void __launch_bounds__(256) k_gemv_t(Rows A, int64_t n, const double* __restrict__ x,
-                                                double* __restrict__ partial) {
-  __shared__ double xs[kChunk];
-  const int64_t c0 = (int64_t)blockIdx.x * kChunk;
-  const int cn = (int)imin(kChunk, n - c0);
-  for (int c = threadIdx.x; c < kChunk; c += blockDim.x) xs[c] = c < cn ? x[c0 + c] : 0.0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int64_t R = A.na + A.nb;
-  for (int64_t i = w; i < R; i += nw) {
-    const double* row = (i < A.na ? A.a + i * A.ld : A.b + (i - A.na) * A.ld) + c0;
+// rows used by a CGS pass: basis rows [0, k + add) and/or the locked set
+struct RowSel {
+  const double* V;
+  const double* L;
+  int64_t ld;
+  int add;        // basis rows = k + add (k from the device state)
+  int use_basis;  // 0: locked set only
+};
+
+__device__ __forceinline__ void rows_of(const RowSel& A, const LzDev* st, int64_t& na, int64_t& nb) {
+  na = A.use_basis ? (int64_t)st->k + A.add : 0;
+  nb = st->nlocked;
+}
+
+// ---- tall-skinny GEMVs of the Gram-Schmidt passes --------------------------
+// dots:   partial[chunk * Rmax + i] = sum_{c in chunk} row_i[c] x[c]
+//         grid (column chunks of kDotCols, row groups of kDotRows); every
+//         lane keeps its 32 x-values in registers and streams 16 double2
+//         per row (a warp reads 512 B contiguous per load).
+// reduce: coef[i] = sum_chunk partial[chunk * Rmax + i]   (fixed order)
+// update: upart[g][c] = sum_{i in group g} row_i[c] coef[i]  (grid columns x
+//         kUpdGroups), then y[c] -= sum_g upart[g][c]  (fixed order).
+constexpr int kDotCols = 1024;
+constexpr int kDotRows = 32;    // 8 warps x 4 rows
+constexpr int kUpdGroups = 8;
+constexpr int kUpdCols = 512;   // columns per update CTA (2 per thread)
+
+__device__ __forceinline__ const double* sel_row(const RowSel& A, int64_t na, int64_t i) {
+  return i < na ? A.V + i * A.ld : A.L + (i - na) * A.ld;
+}
+
+__global__ void __launch_bounds__(256) k_cgs_dots(RowSel A, const LzDev* st, int64_t n, int64_t Rmax,
+                                                  const double* __restrict__ x,
+                                                  double* __restrict__ partial) {
+  if (st->stop) return;
+  int64_t na, nb;
+  rows_of(A, st, na, nb);
+  const int64_t R = na + nb;
+  const int64_t r0 = (int64_t)blockIdx.y * kDotRows;
+  if (r0 >= R) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * kDotCols;
+  const bool full = c0 + kDotCols <= n;
+  double2 xv[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int64_t c = c0 + 64 * t + 2 * lane;
+    if (full) {
+      xv[t] = *reinterpret_cast<const double2*>(x + c);
+    } else {
+      xv[t].x = c < n ? x[c] : 0.0;
+      xv[t].y = c + 1 < n ? x[c + 1] : 0.0;
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < kDotRows / 8; ++rr) {
+    const int64_t i = r0 + w * (kDotRows / 8) + rr;
+    if (i >= R) break;
+    const double* row = sel_row(A, na, i);
     double acc = 0.0;
-    if (cn == kChunk) {
-      const double2* r2 = reinterpret_cast<const double2*>(row);
-#pragma unroll 4
-      for (int c = lane; c < kChunk / 2; c += 32) {
-        double2 v = __ldg(r2 + c);
-        acc = fma(v.x, xs[2 * c], acc);
-        acc = fma(v.y, xs[2 * c + 1], acc);
+    if (full) {
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(row + c0 + 64 * t + 2 * lane));
+        acc = fma(v.x, xv[t].x, acc);
+        acc = fma(v.y, xv[t].y, acc);
       }
     } else {
-      for (int c = lane; c < cn; c += 32) acc = fma(row[c], xs[c], acc);
+      for (int t = 0; t < 16; ++t) {
+        const int64_t c = c0 + 64 * t + 2 * lane;
+        if (c < n) acc = fma(row[c], xv[t].x, acc);
+        if (c + 1 < n) acc = fma(row[c + 1], xv[t].y, acc);
+      }
     }
     acc = warp_sum(acc);
-    if (lane == 0) partial[blockIdx.x * R + i] = acc;
+    if (lane == 0) partial[blockIdx.x * Rmax + i] = acc;
   }
 }
 
-// coef[i] = sum_b partial[b * R + i]   (fixed order)
-__global__ void k_reduce_rows(int64_t R, int nblk, const double* __restrict__ partial,
-                              double* __restrict__ coef) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void k_cgs_reduce(RowSel A, const LzDev* st, int nchunk, int64_t Rmax,
+                             const double* __restrict__ partial, double* __restrict__ coef) {
+  if (st->stop) return;
+  int64_t na, nb;
+  rows_of(A, st, na, nb);
+  const int64_t R = na + nb;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= R) return;
   double s = 0.0;
-  for (int b = 0; b < nblk; ++b) s += partial[(int64_t)b * R + i];
+  for (int b = 0; b < nchunk; ++b) s += partial[(int64_t)b * Rmax + i];
   coef[i] = s;
 }
 
-// y[c] -= sum_i row_i[c] * coef[i]  over both row blocks; optionally also
-// y2[c] -= sum_i row2_i[c] * coef[i] (the M-images, for locked projections)
-__global__ void __launch_bounds__(256) k_gemv_n(Rows A, int64_t n, const double* __restrict__ coef,
-                                                double* __restrict__ y, Rows A2,
-                                                double* __restrict__ y2) {
-  extern __shared__ double cs[];
-  const int64_t R = A.na + A.nb;
-  for (int64_t i = threadIdx.x; i < R; i += blockDim.x) cs[i] = coef[i];
+__global__ void __launch_bounds__(256) k_cgs_upd_part(RowSel A, const LzDev* st, int64_t n, int64_t ldu,
+                                                      const double* __restrict__ coef,
+                                                      double* __restrict__ upart) {
+  if (st->stop) return;
+  __shared__ double cs[1024];
+  int64_t na, nb;
+  rows_of(A, st, na, nb);
+  const int64_t R = na + nb;
+  const int64_t per = (R + kUpdGroups - 1) / kUpdGroups;
+  const int64_t i0 = (int64_t)blockIdx.y * per, i1 = imin(R, i0 + per);
+  const int cnt = (int)(i1 > i0 ? i1 - i0 : 0);
+  for (int t = threadIdx.x; t < cnt && t < 1024; t += blockDim.x) cs[t] = coef[i0 + t];
   __syncthreads();
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t c = (int64_t)blockIdx.x * kUpdCols + 2 * threadIdx.x;
   if (c >= n) return;
-  double acc = 0.0, acc2 = 0.0;
-  int64_t i = 0;
-  for (; i + 4 <= A.na; i += 4) {
-    double v0 = __ldg(A.a + (i + 0) * A.ld + c), v1 = __ldg(A.a + (i + 1) * A.ld + c);
-    double v2 = __ldg(A.a + (i + 2) * A.ld + c), v3 = __ldg(A.a + (i + 3) * A.ld + c);
-    acc = fma(v0, cs[i], acc);
-    acc = fma(v1, cs[i + 1], acc);
-    acc = fma(v2, cs[i + 2], acc);
-    acc = fma(v3, cs[i + 3], acc);
+  const bool pair = c + 1 < n;
+  double2 acc = make_double2(0.0, 0.0);
+  int t = 0;
+  if (pair) {
+    for (; t + 8 <= cnt; t += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(sel_row(A, na, i0 + t + u) + c));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double cf = t + u < 1024 ? cs[t + u] : coef[i0 + t + u];
+        acc.x = fma(v[u].x, cf, acc.x);
+        acc.y = fma(v[u].y, cf, acc.y);
+      }
+    }
   }
-  for (; i < A.na; ++i) acc = fma(__ldg(A.a + i * A.ld + c), cs[i], acc);
-  for (int64_t j = 0; j < A.nb; ++j) acc = fma(__ldg(A.b + j * A.ld + c), cs[A.na + j], acc);
-  y[c] -= acc;
-  if (y2) {
-    for (int64_t q = 0; q < A2.na; ++q) acc2 = fma(__ldg(A2.a + q * A2.ld + c), cs[q], acc2);
-    for (int64_t j = 0; j < A2.nb; ++j) acc2 = fma(__ldg(A2.b + j * A2.ld + c), cs[A2.na + j], acc2);
-    y2[c] -= acc2;
+  for (; t < cnt; ++t) {
+    const double* row = sel_row(A, na, i0 + t);
+    const double cf = t < 1024 ? cs[t] : coef[i0 + t];
+    acc.x = fma(row[c], cf, acc.x);
+    if (pair) acc.y = fma(row[c + 1], cf, acc.y);
   }
+  double* dst = upart + (int64_t)blockIdx.y * ldu + c;
+  dst[0] = acc.x;
+  if (pair) dst[1] = acc.y;
 }
 
-// scal[0] = <a, b>, scal[1] = <c, d> (two dots in one pass), deterministic
-__global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
-                       const double* __restrict__ c, const double* __restrict__ d,
-                       double* __restrict__ partial, unsigned* __restrict__ ticket,
-                       double* __restrict__ out) {
+__global__ void k_cgs_upd_final(const LzDev* st, int64_t n, int64_t ldu, const double* __restrict__ upart,
+                                double* __restrict__ y) {
+  if (st->stop) return;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double s = 0.0;
+#pragma unroll
+  for (int g = 0; g < kUpdGroups; ++g) s += upart[(int64_t)g * ldu + c];
+  y[c] -= s;
+}
+
+// out[0] = <a, b>, out[1] = <c, d>; `a` offset by k rows when koff_a != 0
+__global__ void k_dot2(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ a, int koff_a,
+                       const double* __restrict__ b, const double* __restrict__ c,
+                       const double* __restrict__ d, double* __restrict__ partial,
+                       unsigned* __restrict__ ticket, double* __restrict__ out) {
+  if (st->stop) return;
   __shared__ double red[32];
   __shared__ bool last;
+  const double* aa = a + (koff_a ? (int64_t)st->k * ld : 0);
   double s0 = 0.0, s1 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    s0 = fma(a[i], b[i], s0);
+    s0 = fma(aa[i], b[i], s0);
     s1 = fma(c[i], d[i], s1);
   }
   s0 = block_sum(s0, red);
@@ -139,59 +227,153 @@ __global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __
   }
 }
 
-// r = w - alpha v - sum_{i in [clo, k)} cpl[i] V[i]     (alpha = scal[0])
-__global__ void k_residual(int64_t n, const double* __restrict__ w, const double* __restrict__ v,
-                           const double* __restrict__ scal, const double* __restrict__ V,
-                           int64_t ld, int64_t clo, int64_t k, const double* __restrict__ cpl,
+// bp[j] = MV[k][order[j]]: the solve's right-hand side in elimination order
+__global__ void k_perm_row(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ MV,
+                           const int32_t* __restrict__ order, double* __restrict__ bp) {
+  if (st->stop) return;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) bp[j] = MV[(int64_t)st->k * ld + order[j]];
+}
+
+// r = w - alpha V[k] - sum_{i in [clo, k)} cpl[i] V[i]
+__global__ void k_residual(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ w,
+                           const double* __restrict__ V, const double* __restrict__ cpl,
                            double* __restrict__ r) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (st->stop) return;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
-  double alpha = scal[0];
-  double x = w[c] - alpha * v[c];
+  const int k = st->k, clo = st->clo;
+  const double alpha = st->scal[0];
+  double x = w[c] - alpha * V[(int64_t)k * ld + c];
   if (clo < k) {
     double acc = 0.0;
-    for (int64_t i = clo; i < k; ++i) acc = fma(V[i * ld + c], cpl[i], acc);
+    for (int i = clo; i < k; ++i) acc = fma(V[(int64_t)i * ld + c], cpl[i], acc);
     x -= acc;
   }
   r[c] = x;
 }
 
-// dst = src * (1 / sqrt(s))  for two vector pairs, s = scal[idx]
-__global__ void k_normalize2(int64_t n, const double* __restrict__ scal, int idx,
-                             const double* __restrict__ a, double* __restrict__ da,
-                             const double* __restrict__ b, double* __restrict__ db) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  double nrm = sqrt(fmax(scal[idx], 0.0));
-  da[c] = a[c] / nrm;
-  db[c] = b[c] / nrm;
+__device__ __forceinline__ bool broke_down(const LzDev* st, double& beta, double& wn) {
+  beta = sqrt(fmax(st->scal[2], 0.0));
+  wn = sqrt(fmax(st->scal[1], 0.0));
+  return beta <= fmax(st->btol, 1e-13 * wn);
 }
 
-// X[q][c] = sum_i W[i + q*k] * V[i][c]  for q < c_cnt (W column-major k x c)
+// V[k+1] = r / beta, MV[k+1] = Mr / beta (unless the step broke down)
+__global__ void k_normalize_next(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ r,
+                                 const double* __restrict__ Mr, double* __restrict__ V,
+                                 double* __restrict__ MV) {
+  if (st->stop) return;
+  double beta, wn;
+  if (broke_down(st, beta, wn)) return;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int64_t o = (int64_t)(st->k + 1) * ld + c;
+  V[o] = r[c] / beta;
+  MV[o] = Mr[c] / beta;
+}
+
+// bookkeeping of a finished step (one thread)
+__global__ void k_step_finish(LzDev* st, double* __restrict__ cpl, double* __restrict__ oa,
+                              double* __restrict__ ob, double* __restrict__ ow) {
+  if (st->stop) return;
+  double beta, wn;
+  const bool broke = broke_down(st, beta, wn);
+  const int k = st->k, i = st->steps;
+  oa[i] = st->scal[0];
+  ob[i] = beta;
+  ow[i] = wn;
+  st->steps = i + 1;
+  st->k = k + 1;
+  if (broke) {
+    st->stop = 1;
+    return;
+  }
+  cpl[k] = beta;
+  st->clo = k;
+  if (k + 1 >= st->limit) st->stop = 2;
+}
+
+// row k of V / MV = a, b scaled by 1 / sqrt(s[0])
+__global__ void k_normalize_k(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ s,
+                              const double* __restrict__ a, double* __restrict__ V,
+                              const double* __restrict__ b, double* __restrict__ MV) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const double nrm = sqrt(fmax(s[0], 0.0));
+  const int64_t o = (int64_t)st->k * ld + c;
+  V[o] = a[c] / nrm;
+  MV[o] = b[c] / nrm;
+}
+
+// X[q][c] = sum_i W[i + q*k] * V[i][c]  for q < qn (W column-major k x qn)
 template <int NQ>
 __global__ void __launch_bounds__(256) k_lift(int64_t n, const double* __restrict__ V, int64_t ld,
-                                              int64_t k, const double* __restrict__ W,
-                                              int64_t q0, int64_t qn, double* __restrict__ X,
-                                              int64_t ldx) {
-  extern __shared__ double ws[];  // k * NQ
-  for (int64_t t = threadIdx.x; t < k * NQ; t += blockDim.x) {
-    int64_t i = t % k, q = t / k;
-    ws[t] = (q0 + q < qn) ? W[(q0 + q) * k + i] : 0.0;
-  }
+                                              int k, const double* __restrict__ W, int q0, int qn,
+                                              double* __restrict__ X, int64_t ldx) {
+  extern __shared__ double ws[];  // NQ x k
+  for (int q = 0; q < NQ; ++q)
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+      ws[q * k + i] = (q0 + q < qn) ? W[(int64_t)(q0 + q) * k + i] : 0.0;
   __syncthreads();
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
   double acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-  for (int64_t i = 0; i < k; ++i) {
-    double v = __ldg(V + i * ld + c);
+  for (int i = 0; i < k; ++i) {
+    const double v = __ldg(V + (int64_t)i * ld + c);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = fma(ws[q * k + i], v, acc[q]);
   }
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
-    if (q0 + q < qn) X[(q0 + q) * ldx + c] = acc[q];
+    if (q0 + q < qn) X[(int64_t)(q0 + q) * ldx + c] = acc[q];
+}
+
+// --- batched locking (ref _sweep :483-523), one converged pair at a time ---
+// LzDev scal slots: [5] x.Mx before, [6] after projection; pad[0] = projected?
+__global__ void k_pair_begin(LzDev* st) {
+  st->pad[0] = st->nlocked > 0 ? 1 : 0;  // the reference projects only if something is locked
+  st->pad[1] = 0;                        // rejected?
+}
+
+// x, mx /= sqrt(s) (first normalisation; s <= 0 rejects the pair)
+__global__ void k_pair_scale(LzDev* st, int64_t n, double* __restrict__ x, double* __restrict__ mx,
+                             int slot, int only_if_projected) {
+  if (st->pad[1]) return;
+  if (only_if_projected && !st->pad[0]) return;
+  const double s = st->scal[slot];
+  const double nrm = sqrt(fmax(s, 0.0));
+  if (!only_if_projected && nrm <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->pad[1] = 1;
+    return;
+  }
+  if (only_if_projected && nrm < 0.3) {  // a copy of something known
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->pad[1] = 1;
+    return;
+  }
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  x[c] = x[c] / nrm;
+  mx[c] = mx[c] / nrm;
+}
+
+// append an accepted pair to the locked set (row nlocked) and record the flag
+__global__ void k_pair_append(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ x,
+                              const double* __restrict__ mx, double* __restrict__ L,
+                              double* __restrict__ LM) {
+  if (st->pad[1]) return;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int64_t o = (int64_t)st->nlocked * ld + c;
+  L[o] = x[c];
+  LM[o] = mx[c];
+}
+
+__global__ void k_pair_end(LzDev* st, int* __restrict__ flags, int q) {
+  flags[q] = st->pad[1] ? 0 : 1;
+  if (!st->pad[1]) st->nlocked += 1;
 }
 
 }  // namespace riga
@@ -204,16 +386,35 @@ struct riga_lanczos {
   riga_factor* op = nullptr;
   int64_t n = 0, ld = 0, max_dim = 0, k = 0;
   int64_t nlocked = 0, cap = 0;
-  DevBuf<double> V, MV, L, LM, w, r, Mr, coef, partial, scal, cpl, Wd, tmp;
+  DevBuf<double> V, MV, L, LM, w, r, Mr, bp, coef, partial, upart, cpl, Wd, outs, dscratch;
+  DevBuf<LzDev> st;
+  LzDev* hst = nullptr;    // pinned mirror
   double* hbuf = nullptr;  // pinned readback
   int nblk = 0;
+  // captured step graph (valid for one operator and one locked-buffer layout)
+  cudaGraphExec_t gexec = nullptr;
+  riga_factor* gop = nullptr;
+  const double* gL = nullptr;
+  int64_t gR = 0;
+  long long gnodes = 0;  // kernel launches per replay
+  cudaStream_t cur = nullptr;   // stream the step helpers launch on
+  cudaStream_t capst = nullptr; // private stream for graph capture (never legacy)
+  ~riga_lanczos() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (capst) cudaStreamDestroy(capst);
+  }
 };
 
 namespace {
 
+void drop_graph(riga_lanczos* lz) {
+  if (lz->gexec) cudaGraphExecDestroy(lz->gexec);
+  lz->gexec = nullptr;
+}
+
 int grow_locked(riga_lanczos* lz, int64_t need) {
   if (need <= lz->cap) return RIGA_OK;
-  int64_t cap = std::max<int64_t>(8, lz->cap);
+  int64_t cap = std::max<int64_t>(std::max<int64_t>(16, lz->max_dim), lz->cap);
   while (cap < need) cap *= 2;
   cudaStream_t s = lz->ctx->stream;
   DevBuf<double> nL, nLM;
@@ -226,56 +427,147 @@ int grow_locked(riga_lanczos* lz, int64_t need) {
   lz->L.swap(nL);
   lz->LM.swap(nLM);
   lz->cap = cap;
-  // coefficient / partial buffers sized for basis + locked rows
-  int64_t R = lz->max_dim + 1 + cap;
+  const int64_t R = lz->max_dim + 1 + cap;
   RIGA_TRY(lz->coef.alloc(R, s));
-  RIGA_TRY(lz->partial.alloc((int64_t)lz->nblk * R, s));
+  RIGA_TRY(lz->partial.alloc((int64_t)((lz->n + kDotCols - 1) / kDotCols) * R, s));
+  drop_graph(lz);
   return RIGA_OK;
 }
 
-// r -= V[:kk]^T (MV[:kk] r) + L^T (LM r), `passes` times (CGS2 when 2)
-int cgs(riga_lanczos* lz, int64_t kk, double* r, int passes) {
-  cudaStream_t s = lz->ctx->stream;
-  int64_t R = kk + lz->nlocked;
-  if (R == 0) return RIGA_OK;
-  Rows dots{lz->MV.p, kk, lz->LM.p, lz->nlocked, lz->ld};
-  Rows upd{lz->V.p, kk, lz->L.p, lz->nlocked, lz->ld};
-  Rows none{nullptr, 0, nullptr, 0, lz->ld};
+// push the host mirror of the recurrence state to the device
+int push_state(riga_lanczos* lz, int64_t clo, int64_t limit, double btol) {
+  LzDev& h = *lz->hst;
+  std::memset(&h, 0, sizeof(LzDev));
+  h.k = (int)lz->k;
+  h.clo = (int)clo;
+  h.nlocked = (int)lz->nlocked;
+  h.limit = (int)limit;
+  h.btol = btol;
+  RIGA_CUDA(cudaMemcpyAsync(lz->st.p, &h, sizeof(LzDev), cudaMemcpyHostToDevice, lz->ctx->stream));
+  return RIGA_OK;
+}
+
+int pull_state(riga_lanczos* lz) {
+  RIGA_CUDA(cudaMemcpyAsync(lz->hst, lz->st.p, sizeof(LzDev), cudaMemcpyDeviceToHost, lz->ctx->stream));
+  RIGA_CUDA(cudaStreamSynchronize(lz->ctx->stream));
+  return RIGA_OK;
+}
+
+RowSel sel_basis(riga_lanczos* lz, bool mv, int add) {
+  return RowSel{mv ? lz->MV.p : lz->V.p, mv ? lz->LM.p : lz->L.p, lz->ld, add, 1};
+}
+RowSel sel_locked(riga_lanczos* lz, bool mv) {
+  return RowSel{nullptr, mv ? lz->LM.p : lz->L.p, lz->ld, 0, 0};
+}
+
+// `passes` x: r -= U^T (D r) over the selected rows; r2 -= U2^T (D r) if given
+int cgs_passes(riga_lanczos* lz, RowSel dots, RowSel upd, RowSel upd2, double* r, double* r2,
+               int passes, int64_t rows_hint) {
+  cudaStream_t s = lz->cur;
+  const int64_t Rmax = lz->max_dim + 1 + lz->cap;
+  const int nchunk = (int)((lz->n + kDotCols - 1) / kDotCols);
+  const dim3 gd(nchunk, (unsigned)((Rmax + kDotRows - 1) / kDotRows));
+  const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
+  const unsigned gf = (unsigned)((lz->n + 255) / 256);
   for (int p = 0; p < passes; ++p) {
-    ProfScope prof(kProfCgs, s, 2.0 * R * lz->n * 8.0);
-    k_gemv_t<<<lz->nblk, 256, 0, s>>>(dots, lz->n, r, lz->partial.p); count_launch();
-    k_reduce_rows<<<(unsigned)((R + 255) / 256), 256, 0, s>>>(R, lz->nblk, lz->partial.p, lz->coef.p); count_launch();
-    k_gemv_n<<<(unsigned)((lz->n + 255) / 256), 256, R * 8, s>>>(upd, lz->n, lz->coef.p, r, none,
-                                                                 nullptr); count_launch();
+    ProfScope prof(kProfCgs, s, 2.0 * (double)rows_hint * lz->n * 8.0);
+    k_cgs_dots<<<gd, 256, 0, s>>>(dots, lz->st.p, lz->n, Rmax, r, lz->partial.p);
+    k_cgs_reduce<<<(unsigned)((Rmax + 255) / 256), 256, 0, s>>>(dots, lz->st.p, nchunk, Rmax, lz->partial.p,
+                                                                lz->coef.p);
+    k_cgs_upd_part<<<gu, 256, 0, s>>>(upd, lz->st.p, lz->n, lz->ld, lz->coef.p, lz->upart.p);
+    k_cgs_upd_final<<<gf, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->upart.p, r);
+    count_launch(4);
+    if (r2) {
+      k_cgs_upd_part<<<gu, 256, 0, s>>>(upd2, lz->st.p, lz->n, lz->ld, lz->coef.p, lz->upart.p);
+      k_cgs_upd_final<<<gf, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->upart.p, r2);
+      count_launch(2);
+    }
   }
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
 }
 
-// y = M x, or a copy for the Euclidean inner product (mass == NULL)
 int mass_apply(riga_lanczos* lz, const double* x, double* y) {
-  cudaStream_t s = lz->ctx->stream;
+  cudaStream_t s = lz->cur;
   if (lz->sys) return system_spmv(lz->sys, s, 1, 0.0, x, y);
   RIGA_CUDA(cudaMemcpyAsync(y, x, lz->n * 8, cudaMemcpyDeviceToDevice, s));
   return RIGA_OK;
 }
 
-int read_scal(riga_lanczos* lz, int count) {
-  cudaStream_t s = lz->ctx->stream;
-  RIGA_CUDA(cudaMemcpyAsync(lz->hbuf, lz->scal.p, count * 8, cudaMemcpyDeviceToHost, s));
-  RIGA_CUDA(cudaStreamSynchronize(s));
+int dot2(riga_lanczos* lz, const double* a, int koff_a, const double* b, const double* c,
+         const double* d, int slot) {
+  cudaStream_t s = lz->cur;
+  ProfScope prof(kProfVec, s, 32.0 * lz->n);
+  const int blocks = (int)std::min<int64_t>(296, (lz->n + 255) / 256);
+  k_dot2<<<blocks, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, a, koff_a, b, c, d, lz->dscratch.p,
+                                reinterpret_cast<unsigned*>(lz->dscratch.p + 2 * 296),
+                                lz->st.p->scal + slot);
+  count_launch();
+  RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
 }
 
-int dot2(riga_lanczos* lz, const double* a, const double* b, const double* c, const double* d,
-         int slot) {
-  cudaStream_t s = lz->ctx->stream;
-  ProfScope prof(kProfVec, s, 32.0 * lz->n);
-  int blocks = (int)std::min<int64_t>(296, (lz->n + 255) / 256);
-  double* scratch = lz->scal.p + 16;
-  k_dot2<<<blocks, 256, 0, s>>>(lz->n, a, b, c, d, scratch,
-                                reinterpret_cast<unsigned*>(lz->scal.p + 15), lz->scal.p + slot); count_launch();
+// the second half of a step, once w = H v is in lz->w (ref step :244-267)
+int step_tail(riga_lanczos* lz) {
+  cudaStream_t s = lz->cur;
+  const unsigned g1 = (unsigned)((lz->n + 255) / 256);
+  RIGA_TRY(dot2(lz, lz->MV.p, 1, lz->w.p, lz->w.p, lz->w.p, 0));  // alpha, |w|^2
+  k_residual<<<g1, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->w.p, lz->V.p, lz->cpl.p, lz->r.p);
+  count_launch();
+  RIGA_TRY(cgs_passes(lz, sel_basis(lz, true, 1), sel_basis(lz, false, 1), RowSel{}, lz->r.p, nullptr, 2,
+                      lz->k + 1 + lz->nlocked));
+  RIGA_TRY(mass_apply(lz, lz->r.p, lz->Mr.p));
+  RIGA_TRY(dot2(lz, lz->r.p, 0, lz->Mr.p, lz->r.p, lz->Mr.p, 2));  // beta^2
+  k_normalize_next<<<g1, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->r.p, lz->Mr.p, lz->V.p, lz->MV.p);
+  count_launch();
+  k_step_finish<<<1, 1, 0, s>>>(lz->st.p, lz->cpl.p, lz->outs.p, lz->outs.p + (lz->max_dim + 1),
+                                lz->outs.p + 2 * (lz->max_dim + 1));
+  count_launch();
   RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+// one full step with the device operator
+int step_full(riga_lanczos* lz) {
+  cudaStream_t s = lz->cur;
+  const unsigned g1 = (unsigned)((lz->n + 255) / 256);
+  k_perm_row<<<g1, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->MV.p, lz->op->sym->d_order.p, lz->bp.p);
+  count_launch();
+  RIGA_TRY(factor_solve(lz->op, s, lz->bp.p, lz->w.p, true));
+  return step_tail(lz);
+}
+
+int ensure_graph(riga_lanczos* lz) {
+  const int64_t Rmax = lz->max_dim + 1 + lz->cap;
+  if (lz->gexec && lz->gop == lz->op && lz->gL == lz->L.p && lz->gR == Rmax) return RIGA_OK;
+  drop_graph(lz);
+  cudaStream_t s = lz->ctx->stream;
+  // first-use allocations and kernel attributes must happen outside the capture
+  riga_factor* F = lz->op;
+  if (!F->cvec.p) RIGA_TRY(F->cvec.alloc(F->sym->h.n, s));
+  RIGA_TRY(prepare_solve());
+  RIGA_CUDA(cudaStreamSynchronize(s));
+  cudaGraph_t g = nullptr;
+  if (!lz->capst) RIGA_CUDA(cudaStreamCreateWithFlags(&lz->capst, cudaStreamNonBlocking));
+  const long long n0 = g_launches.load();
+  RIGA_CUDA(cudaStreamBeginCapture(lz->capst, cudaStreamCaptureModeThreadLocal));
+  lz->cur = lz->capst;
+  const int rc = step_full(lz);
+  lz->cur = lz->ctx->stream;
+  cudaError_t e = cudaStreamEndCapture(lz->capst, &g);
+  lz->gnodes = g_launches.load() - n0;
+  g_launches.fetch_sub(lz->gnodes);  // captured, not launched
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  RIGA_CUDA(e);
+  e = cudaGraphInstantiate(&lz->gexec, g, 0);
+  cudaGraphDestroy(g);
+  RIGA_CUDA(e);
+  lz->gop = lz->op;
+  lz->gL = lz->L.p;
+  lz->gR = Rmax;
   return RIGA_OK;
 }
 
@@ -292,27 +584,33 @@ int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max
   DeviceGuard g(ctx->device);
   auto lz = std::make_unique<riga_lanczos>();
   lz->ctx = ctx;
+  lz->cur = ctx->stream;
   lz->sys = mass;
   lz->n = n;
   lz->ld = (n + 3) / 4 * 4;
   lz->max_dim = std::min<int64_t>(max_dim, n);
   lz->nblk = (int)((lz->n + kChunk - 1) / kChunk);
-  int64_t rows = lz->max_dim + 1;
+  const int64_t rows = lz->max_dim + 1;
   cudaStream_t cs = ctx->stream;
   RIGA_TRY(lz->V.alloc(rows * lz->ld, cs));
   RIGA_TRY(lz->MV.alloc(rows * lz->ld, cs));
-  RIGA_CUDA(cudaMemsetAsync(lz->V.p, 0, rows * lz->ld * 8, ctx->stream));
-  RIGA_CUDA(cudaMemsetAsync(lz->MV.p, 0, rows * lz->ld * 8, ctx->stream));
+  RIGA_CUDA(cudaMemsetAsync(lz->V.p, 0, rows * lz->ld * 8, cs));
+  RIGA_CUDA(cudaMemsetAsync(lz->MV.p, 0, rows * lz->ld * 8, cs));
   RIGA_TRY(lz->w.alloc(lz->ld, cs));
   RIGA_TRY(lz->r.alloc(lz->ld, cs));
   RIGA_TRY(lz->Mr.alloc(lz->ld, cs));
-  RIGA_TRY(lz->tmp.alloc(lz->ld, cs));
-  RIGA_TRY(lz->scal.alloc(16 + 2 * 296 + 16, cs));
-  RIGA_CUDA(cudaMemsetAsync(lz->scal.p, 0, lz->scal.n * 8, ctx->stream));
+  RIGA_TRY(lz->bp.alloc(lz->ld, cs));
+  RIGA_TRY(lz->upart.alloc(kUpdGroups * lz->ld, cs));
   RIGA_TRY(lz->cpl.alloc(rows, cs));
-  RIGA_TRY(grow_locked(lz.get(), 8));
+  RIGA_TRY(lz->outs.alloc(3 * rows, cs));
+  RIGA_TRY(lz->dscratch.alloc(2 * 296 + 8, cs));
+  RIGA_CUDA(cudaMemsetAsync(lz->dscratch.p, 0, (2 * 296 + 8) * 8, cs));
+  RIGA_TRY(lz->st.alloc(1, cs));
+  RIGA_CUDA(cudaMemsetAsync(lz->st.p, 0, sizeof(LzDev), cs));
+  RIGA_TRY(grow_locked(lz.get(), 16));
+  RIGA_CUDA(cudaMallocHost(&lz->hst, sizeof(LzDev)));
   RIGA_CUDA(cudaMallocHost(&lz->hbuf, std::max<int64_t>(64, 3 * rows + 8) * 8));
-  RIGA_CUDA(cudaStreamSynchronize(ctx->stream));
+  RIGA_CUDA(cudaStreamSynchronize(cs));
   *out = lz.release();
   return RIGA_OK;
 }
@@ -322,6 +620,7 @@ int riga_lanczos_destroy(riga_lanczos* lz) {
   DeviceGuard g(lz->ctx->device);
   cudaStreamSynchronize(lz->ctx->stream);
   if (lz->hbuf) cudaFreeHost(lz->hbuf);
+  if (lz->hst) cudaFreeHost(lz->hst);
   delete lz;
   return RIGA_OK;
 }
@@ -329,6 +628,7 @@ int riga_lanczos_destroy(riga_lanczos* lz) {
 int riga_lanczos_set_operator(riga_lanczos* lz, riga_factor* f) {
   RIGA_CHECK_ARG(lz && f, "null arg");
   RIGA_CHECK_ARG(f->sym->h.n == lz->n, "operator dimension mismatch");
+  if (lz->op != f) drop_graph(lz);
   lz->op = f;
   return RIGA_OK;
 }
@@ -349,18 +649,18 @@ int riga_lanczos_set_start(riga_lanczos* lz, const double* r_host) {
   RIGA_CHECK_ARG(lz && r_host, "null arg");
   DeviceGuard g(lz->ctx->device);
   cudaStream_t s = lz->ctx->stream;
+  RIGA_TRY(push_state(lz, lz->k, lz->k, 0.0));
   RIGA_CUDA(cudaMemcpyAsync(lz->r.p, r_host, lz->n * 8, cudaMemcpyHostToDevice, s));
   RIGA_TRY(mass_apply(lz, lz->r.p, lz->Mr.p));
-  RIGA_TRY(dot2(lz, lz->r.p, lz->Mr.p, lz->r.p, lz->Mr.p, 0));
-  RIGA_TRY(read_scal(lz, 1));
-  if (!(std::sqrt(std::max(lz->hbuf[0], 0.0)) > 0.0)) {
+  RIGA_TRY(dot2(lz, lz->r.p, 0, lz->Mr.p, lz->r.p, lz->Mr.p, 0));
+  RIGA_TRY(pull_state(lz));
+  if (!(std::sqrt(std::max(lz->hst->scal[0], 0.0)) > 0.0)) {
     set_error("start vector has zero mass norm");
     return RIGA_BAD_ARG;
   }
-  double* vk = lz->V.p + lz->k * lz->ld;
-  double* mvk = lz->MV.p + lz->k * lz->ld;
-  k_normalize2<<<(unsigned)((lz->n + 255) / 256), 256, 0, s>>>(lz->n, lz->scal.p, 0, lz->r.p, vk,
-                                                               lz->Mr.p, mvk); count_launch();
+  k_normalize_k<<<(unsigned)((lz->n + 255) / 256), 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->st.p->scal,
+                                                                  lz->r.p, lz->V.p, lz->Mr.p, lz->MV.p);
+  count_launch();
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
 }
@@ -369,21 +669,22 @@ int riga_lanczos_fresh(riga_lanczos* lz, const double* r_host, int* accepted) {
   RIGA_CHECK_ARG(lz && r_host && accepted, "null arg");
   DeviceGuard g(lz->ctx->device);
   cudaStream_t s = lz->ctx->stream;
+  RIGA_TRY(push_state(lz, lz->k, lz->k, 0.0));
   RIGA_CUDA(cudaMemcpyAsync(lz->r.p, r_host, lz->n * 8, cudaMemcpyHostToDevice, s));
   RIGA_TRY(mass_apply(lz, lz->r.p, lz->Mr.p));
-  RIGA_TRY(dot2(lz, lz->r.p, lz->Mr.p, lz->r.p, lz->Mr.p, 4));  // ref norm^2 -> scal[4]
-  RIGA_TRY(cgs(lz, lz->k, lz->r.p, 2));
+  RIGA_TRY(dot2(lz, lz->r.p, 0, lz->Mr.p, lz->r.p, lz->Mr.p, 4));  // ref norm^2 -> scal[4]
+  RIGA_TRY(cgs_passes(lz, sel_basis(lz, true, 0), sel_basis(lz, false, 0), RowSel{}, lz->r.p, nullptr, 2,
+                      lz->k + lz->nlocked));
   RIGA_TRY(mass_apply(lz, lz->r.p, lz->Mr.p));
-  RIGA_TRY(dot2(lz, lz->r.p, lz->Mr.p, lz->r.p, lz->Mr.p, 0));
-  RIGA_TRY(read_scal(lz, 6));
-  double ref = std::sqrt(std::max(lz->hbuf[4], 0.0));
-  double nrm = std::sqrt(std::max(lz->hbuf[0], 0.0));
+  RIGA_TRY(dot2(lz, lz->r.p, 0, lz->Mr.p, lz->r.p, lz->Mr.p, 0));
+  RIGA_TRY(pull_state(lz));
+  const double ref = std::sqrt(std::max(lz->hst->scal[4], 0.0));
+  const double nrm = std::sqrt(std::max(lz->hst->scal[0], 0.0));
   *accepted = nrm > 1e-8 * std::max(ref, 1e-300);
   if (*accepted) {
-    double* vk = lz->V.p + lz->k * lz->ld;
-    double* mvk = lz->MV.p + lz->k * lz->ld;
-    k_normalize2<<<(unsigned)((lz->n + 255) / 256), 256, 0, s>>>(lz->n, lz->scal.p, 0, lz->r.p, vk,
-                                                                 lz->Mr.p, mvk); count_launch();
+    k_normalize_k<<<(unsigned)((lz->n + 255) / 256), 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->st.p->scal,
+                                                                    lz->r.p, lz->V.p, lz->Mr.p, lz->MV.p);
+    count_launch();
     RIGA_CUDA(cudaGetLastError());
   }
   return RIGA_OK;
@@ -400,52 +701,6 @@ int riga_lanczos_lock(riga_lanczos* lz, const double* x, const double* mx) {
   return RIGA_OK;
 }
 
-}  // extern "C"
-
-namespace {
-// Second half of a step once w = H v is in lz->w (ref step :244-267).
-// Returns RIGA_BREAKDOWN when beta is below the relative threshold.
-int step_core(riga_lanczos* lz, int64_t clo, double breakdown_tol, double* a_out, double* b_out,
-              double* w_out) {
-  cudaStream_t s = lz->ctx->stream;
-  const int64_t n = lz->n, ld = lz->ld, k = lz->k;
-  const unsigned g1 = (unsigned)((n + 255) / 256);
-  const double* v = lz->V.p + k * ld;
-  const double* Mv = lz->MV.p + k * ld;
-  RIGA_TRY(dot2(lz, Mv, lz->w.p, lz->w.p, lz->w.p, 0));  // alpha, |w|^2
-  k_residual<<<g1, 256, 0, s>>>(n, lz->w.p, v, lz->scal.p, lz->V.p, ld, clo, k, lz->cpl.p, lz->r.p); count_launch();
-  RIGA_TRY(cgs(lz, k + 1, lz->r.p, 2));
-  RIGA_TRY(mass_apply(lz, lz->r.p, lz->Mr.p));
-  RIGA_TRY(dot2(lz, lz->r.p, lz->Mr.p, lz->r.p, lz->Mr.p, 2));  // beta^2
-  RIGA_TRY(read_scal(lz, 4));
-  const double a = lz->hbuf[0], wn = std::sqrt(std::max(lz->hbuf[1], 0.0));
-  const double b = std::sqrt(std::max(lz->hbuf[2], 0.0));
-  *a_out = a;
-  *w_out = wn;
-  *b_out = b;
-  lz->k = k + 1;
-  if (b <= std::max(breakdown_tol, 1e-13 * wn)) return RIGA_BREAKDOWN;
-  k_normalize2<<<g1, 256, 0, s>>>(n, lz->scal.p, 2, lz->r.p, lz->V.p + (k + 1) * ld, lz->Mr.p,
-                                  lz->MV.p + (k + 1) * ld); count_launch();
-  lz->hbuf[8] = b;  // next step's coupling: beta e_k
-  RIGA_CUDA(cudaMemcpyAsync(lz->cpl.p + k, lz->hbuf + 8, 8, cudaMemcpyHostToDevice, s));
-  RIGA_CUDA(cudaGetLastError());
-  return RIGA_OK;
-}
-
-int first_coupling(riga_lanczos* lz, const double* coupling_host, int64_t* clo) {
-  *clo = lz->k;
-  if (coupling_host && lz->k > 0) {
-    RIGA_CUDA(cudaMemcpyAsync(lz->cpl.p, coupling_host, lz->k * 8, cudaMemcpyHostToDevice,
-                              lz->ctx->stream));
-    *clo = 0;
-  }
-  return RIGA_OK;
-}
-}  // namespace
-
-extern "C" {
-
 int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_host,
                         double breakdown_tol, double* alpha, double* beta, double* wnorm,
                         int64_t* steps) {
@@ -455,19 +710,28 @@ int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_
   cudaStream_t s = lz->ctx->stream;
   limit = std::min(limit, lz->max_dim);
   *steps = 0;
-  int64_t clo;
-  RIGA_TRY(first_coupling(lz, coupling_host, &clo));
-  int64_t i = 0;
-  while (lz->k < limit) {
-    const int64_t k = lz->k;
-    RIGA_TRY(factor_solve(lz->op, s, lz->MV.p + k * lz->ld, lz->w.p));  // w = H v
-    int rc = step_core(lz, clo, breakdown_tol, alpha + i, beta + i, wnorm + i);
-    ++i;
-    *steps = i;
-    if (rc) return rc;
-    clo = k;
+  if (lz->k >= limit) return RIGA_OK;
+  int64_t clo = lz->k;
+  if (coupling_host && lz->k > 0) {
+    RIGA_CUDA(cudaMemcpyAsync(lz->cpl.p, coupling_host, lz->k * 8, cudaMemcpyHostToDevice, s));
+    clo = 0;
   }
-  return RIGA_OK;
+  RIGA_TRY(ensure_graph(lz));
+  RIGA_TRY(push_state(lz, clo, limit, breakdown_tol));
+  for (int64_t i = lz->k; i < limit; ++i) RIGA_CUDA(cudaGraphLaunch(lz->gexec, s));
+  count_launch((int)((limit - lz->k) * lz->gnodes));
+  const int64_t rows = lz->max_dim + 1;
+  RIGA_CUDA(cudaMemcpyAsync(lz->hbuf, lz->outs.p, 3 * rows * 8, cudaMemcpyDeviceToHost, s));
+  RIGA_TRY(pull_state(lz));
+  const int ns = lz->hst->steps;
+  for (int i = 0; i < ns; ++i) {
+    alpha[i] = lz->hbuf[i];
+    beta[i] = lz->hbuf[rows + i];
+    wnorm[i] = lz->hbuf[2 * rows + i];
+  }
+  *steps = ns;
+  lz->k = lz->hst->k;
+  return lz->hst->stop == 1 ? RIGA_BREAKDOWN : RIGA_OK;
 }
 
 int riga_lanczos_step_given(riga_lanczos* lz, const double* w_dev, const double* coupling_host,
@@ -475,11 +739,26 @@ int riga_lanczos_step_given(riga_lanczos* lz, const double* w_dev, const double*
   RIGA_CHECK_ARG(lz && w_dev && alpha && beta && wnorm, "null arg");
   RIGA_CHECK_ARG(lz->k < lz->max_dim, "basis is full");
   DeviceGuard g(lz->ctx->device);
-  int64_t clo;
-  RIGA_TRY(first_coupling(lz, coupling_host, &clo));
-  RIGA_CUDA(cudaMemcpyAsync(lz->w.p, w_dev, lz->n * 8, cudaMemcpyDeviceToDevice, lz->ctx->stream));
-  return step_core(lz, clo, breakdown_tol, alpha, beta, wnorm);
+  cudaStream_t s = lz->ctx->stream;
+  int64_t clo = lz->k;
+  if (coupling_host && lz->k > 0) {
+    RIGA_CUDA(cudaMemcpyAsync(lz->cpl.p, coupling_host, lz->k * 8, cudaMemcpyHostToDevice, s));
+    clo = 0;
+  }
+  RIGA_TRY(push_state(lz, clo, lz->k + 1, breakdown_tol));
+  RIGA_CUDA(cudaMemcpyAsync(lz->w.p, w_dev, lz->n * 8, cudaMemcpyDeviceToDevice, s));
+  RIGA_TRY(step_tail(lz));
+  const int64_t rows = lz->max_dim + 1;
+  RIGA_CUDA(cudaMemcpyAsync(lz->hbuf, lz->outs.p, 3 * rows * 8, cudaMemcpyDeviceToHost, s));
+  RIGA_TRY(pull_state(lz));
+  *alpha = lz->hbuf[0];
+  *beta = lz->hbuf[rows];
+  *wnorm = lz->hbuf[2 * rows];
+  lz->k = lz->hst->k;
+  return lz->hst->stop == 1 ? RIGA_BREAKDOWN : RIGA_OK;
 }
+
+}  // extern "C"
 
 static int lift_rows(riga_lanczos* lz, const double* Vb, int64_t k, const double* Wd, int64_t c,
                      double* X) {
@@ -487,18 +766,21 @@ static int lift_rows(riga_lanczos* lz, const double* Vb, int64_t k, const double
   ProfScope prof(kProfLift, s, 8.0 * (double)k * lz->n * ((c + 7) / 8));
   const unsigned g1 = (unsigned)((lz->n + 255) / 256);
   for (int64_t q0 = 0; q0 < c; q0 += 8) {
-    k_lift<8><<<g1, 256, k * 8 * 8, s>>>(lz->n, Vb, lz->ld, k, Wd, q0, c, X, lz->ld); count_launch();
+    k_lift<8><<<g1, 256, k * 8 * 8, s>>>(lz->n, Vb, lz->ld, (int)k, Wd, (int)q0, (int)c, X, lz->ld);
+    count_launch();
   }
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
 }
+
+extern "C" {
 
 int riga_lanczos_lift(riga_lanczos* lz, const double* W_host, int64_t c, double* X, double* MX) {
   RIGA_CHECK_ARG(lz && W_host && X && MX && c >= 0, "null arg");
   if (c == 0) return RIGA_OK;
   DeviceGuard g(lz->ctx->device);
   cudaStream_t s = lz->ctx->stream;
-  int64_t k = lz->k;
+  const int64_t k = lz->k;
   RIGA_TRY(lz->Wd.alloc(std::max<int64_t>(k * c, 1), s));
   RIGA_CUDA(cudaMemcpyAsync(lz->Wd.p, W_host, k * c * 8, cudaMemcpyHostToDevice, s));
   RIGA_TRY(lift_rows(lz, lz->V.p, k, lz->Wd.p, c, X));
@@ -510,7 +792,7 @@ int riga_lanczos_restart(riga_lanczos* lz, const double* W_host, int64_t c) {
   RIGA_CHECK_ARG(lz && c >= 0 && c < lz->max_dim, "bad arg");
   DeviceGuard g(lz->ctx->device);
   cudaStream_t s = lz->ctx->stream;
-  int64_t k = lz->k, ld = lz->ld;
+  const int64_t k = lz->k, ld = lz->ld;
   if (c > 0) {
     RIGA_CHECK_ARG(W_host, "null weights");
     DevBuf<double> nv, nmv;
@@ -522,7 +804,6 @@ int riga_lanczos_restart(riga_lanczos* lz, const double* W_host, int64_t c) {
     RIGA_TRY(lift_rows(lz, lz->MV.p, k, lz->Wd.p, c, nmv.p));
     RIGA_CUDA(cudaMemcpyAsync(lz->V.p, nv.p, c * ld * 8, cudaMemcpyDeviceToDevice, s));
     RIGA_CUDA(cudaMemcpyAsync(lz->MV.p, nmv.p, c * ld * 8, cudaMemcpyDeviceToDevice, s));
-    RIGA_CUDA(cudaStreamSynchronize(s));
   }
   // keep the pending direction: row k -> row c
   if (c != k) {
@@ -533,38 +814,71 @@ int riga_lanczos_restart(riga_lanczos* lz, const double* W_host, int64_t c) {
   return RIGA_OK;
 }
 
+int riga_lanczos_lock_batch(riga_lanczos* lz, double* X, double* MX, int64_t c, int64_t ldx,
+                            int* accepted) {
+  RIGA_CHECK_ARG(lz && X && MX && accepted && c >= 0, "null arg");
+  if (c == 0) return RIGA_OK;
+  DeviceGuard g(lz->ctx->device);
+  cudaStream_t s = lz->ctx->stream;
+  RIGA_TRY(grow_locked(lz, lz->nlocked + c));
+  DevBuf<int> flags;
+  RIGA_TRY(flags.alloc(c, s));
+  RIGA_TRY(push_state(lz, lz->k, lz->k, 0.0));
+  const unsigned g1 = (unsigned)((lz->n + 255) / 256);
+  for (int64_t q = 0; q < c; ++q) {
+    double* x = X + q * ldx;
+    double* mx = MX + q * ldx;
+    k_pair_begin<<<1, 1, 0, s>>>(lz->st.p);
+    RIGA_TRY(dot2(lz, x, 0, mx, x, mx, 5));
+    k_pair_scale<<<g1, 256, 0, s>>>(lz->st.p, lz->n, x, mx, 5, 0);
+    // two passes against the locked set (empty set: the kernels do nothing)
+    RIGA_TRY(cgs_passes(lz, sel_locked(lz, true), sel_locked(lz, false), sel_locked(lz, true), x, mx, 2,
+                        lz->nlocked + q));
+    RIGA_TRY(dot2(lz, x, 0, mx, x, mx, 6));
+    k_pair_scale<<<g1, 256, 0, s>>>(lz->st.p, lz->n, x, mx, 6, 1);
+    k_pair_append<<<g1, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, x, mx, lz->L.p, lz->LM.p);
+    k_pair_end<<<1, 1, 0, s>>>(lz->st.p, flags.p, (int)q);
+    count_launch(6);
+  }
+  RIGA_CUDA(cudaGetLastError());
+  RIGA_CUDA(cudaMemcpyAsync(accepted, flags.p, c * sizeof(int), cudaMemcpyDeviceToHost, s));
+  RIGA_TRY(pull_state(lz));
+  lz->nlocked = lz->hst->nlocked;
+  return RIGA_OK;
+}
+
 int riga_lanczos_project_locked(riga_lanczos* lz, double* x, double* mx, int passes) {
   RIGA_CHECK_ARG(lz && x && mx, "null arg");
   if (!lz->nlocked) return RIGA_OK;
   DeviceGuard g(lz->ctx->device);
-  cudaStream_t s = lz->ctx->stream;
-  int64_t R = lz->nlocked;
-  Rows dots{lz->LM.p, R, nullptr, 0, lz->ld};
-  Rows upd{lz->L.p, R, nullptr, 0, lz->ld};
-  Rows upd2{lz->LM.p, R, nullptr, 0, lz->ld};
-  for (int p = 0; p < passes; ++p) {
-    k_gemv_t<<<lz->nblk, 256, 0, s>>>(dots, lz->n, x, lz->partial.p); count_launch();
-    k_reduce_rows<<<(unsigned)((R + 255) / 256), 256, 0, s>>>(R, lz->nblk, lz->partial.p, lz->coef.p); count_launch();
-    k_gemv_n<<<(unsigned)((lz->n + 255) / 256), 256, R * 8, s>>>(upd, lz->n, lz->coef.p, x, upd2, mx); count_launch();
-  }
-  RIGA_CUDA(cudaGetLastError());
-  return RIGA_OK;
+  RIGA_TRY(push_state(lz, lz->k, lz->k, 0.0));
+  return cgs_passes(lz, sel_locked(lz, true), sel_locked(lz, false), sel_locked(lz, true), x, mx, passes,
+                    lz->nlocked);
 }
 
 int riga_lanczos_gram(riga_lanczos* lz, double* G) {
   RIGA_CHECK_ARG(lz && G, "null arg");
   DeviceGuard g(lz->ctx->device);
   cudaStream_t s = lz->ctx->stream;
-  int64_t k = lz->k;
+  const int64_t k = lz->k;
   if (!k) return RIGA_OK;
-  Rows dots{lz->MV.p, k, nullptr, 0, lz->ld};
-  std::vector<double> row(k);
+  // G[i][j] = V[i] . MV[j]: row V[i] against MV[:k] (locked rows excluded)
+  const int64_t saved = lz->nlocked;
+  lz->nlocked = 0;
+  RIGA_TRY(push_state(lz, k, k, 0.0));
+  lz->nlocked = saved;
+  const RowSel dots = sel_basis(lz, true, 0);
+  const int64_t Rmax = lz->max_dim + 1 + lz->cap;
+  const int nchunk = (int)((lz->n + kDotCols - 1) / kDotCols);
+  const dim3 gd(nchunk, (unsigned)((Rmax + kDotRows - 1) / kDotRows));
   for (int64_t i = 0; i < k; ++i) {
-    k_gemv_t<<<lz->nblk, 256, 0, s>>>(dots, lz->n, lz->V.p + i * lz->ld, lz->partial.p); count_launch();
-    k_reduce_rows<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(k, lz->nblk, lz->partial.p, lz->coef.p); count_launch();
+    k_cgs_dots<<<gd, 256, 0, s>>>(dots, lz->st.p, lz->n, Rmax, lz->V.p + i * lz->ld, lz->partial.p);
+    k_cgs_reduce<<<(unsigned)((Rmax + 255) / 256), 256, 0, s>>>(dots, lz->st.p, nchunk, Rmax, lz->partial.p,
+                                                                lz->coef.p);
+    count_launch(2);
     RIGA_CUDA(cudaMemcpyAsync(G + i * k, lz->coef.p, k * 8, cudaMemcpyDeviceToHost, s));
-    RIGA_CUDA(cudaStreamSynchronize(s));
   }
+  RIGA_CUDA(cudaStreamSynchronize(s));
   return RIGA_OK;
 }
 

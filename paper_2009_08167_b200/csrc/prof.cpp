@@ -35,6 +35,8 @@ cudaEvent_t get_event() {
 ProfScope::ProfScope(int c, cudaStream_t st, double w) : cat(c), s(st), work(w) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_on) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
   e0 = get_event();
   cudaEventRecord(e0, s);
 }
