@@ -194,6 +194,21 @@ int riga_lanczos_project_locked(riga_lanczos* lz, double* x_dev, double* mx_dev,
  * (host).  One host synchronisation for the whole batch.                  */
 int riga_lanczos_lock_batch(riga_lanczos* lz, double* X_dev, double* MX_dev, int64_t c, int64_t ldx,
                             int* accepted);
+/* Block form of the same locking (one pass over the locked set per 8 pairs
+ * instead of per pair): M-normalise the c rows, then twice project against
+ * the locked set and against the earlier rows of the batch; returns the
+ * projected x.Mx per row (host) for the accept / 0.3 decision.  Equal to
+ * the sequential order to second order in the (1e-10-level) couplings.    */
+int riga_lanczos_lock_block(riga_lanczos* lz, double* X_dev, double* MX_dev, int64_t c, int64_t ldx,
+                            double* nrm2_host);
+/* Append c rows to the locked set, dividing row q by sqrt(nrm2[q]) first
+ * when scale[q] != 0.                                                     */
+int riga_lanczos_append_rows(riga_lanczos* lz, double* X_dev, double* MX_dev, int64_t c, int64_t ldx,
+                             const double* nrm2_host, const int* scale_host);
+/* Measurement hook: `passes` Gram-Schmidt passes of x against V[:k] and the
+ * locked set (the step's CGS kernels, launched directly on the context
+ * stream so CUDA events can bracket them); *rows = k + locked.            */
+int riga_lanczos_cgs_probe(riga_lanczos* lz, double* x_dev, int passes, int64_t* rows);
 /* Gram matrix G = V[:k] MV[:k]^T to host (k x k row-major) for the
  * DEBUG_INVARIANTS checks (ref check_invariants :276-282).                 */
 int riga_lanczos_gram(riga_lanczos* lz, double* G_host);

@@ -376,6 +376,124 @@ __global__ void k_pair_end(LzDev* st, int* __restrict__ flags, int q) {
   if (!st->pad[1]) st->nlocked += 1;
 }
 
+// --- batched locking: multi-vector Gram-Schmidt against a row set -----------
+// mdots: partial[chunk][i][q] = sum_{c in chunk} A_i[c] X_q[c]
+//        grid (column chunks of kMChunk, row groups of 32, q groups of 8)
+// mred:  C[i][q] = sum_chunk partial[chunk][i][q]
+// mupd:  Y_q[c] -= sum_i C[i][q] B_i[c]   (B read once per q group of 8)
+constexpr int kMChunk = 4096;
+
+__global__ void __launch_bounds__(256) k_mdots(const double* __restrict__ A, int64_t lda, int R,
+                                               const double* __restrict__ X, int64_t ldx, int c,
+                                               int64_t n, double* __restrict__ partial) {
+  extern __shared__ double xt[];  // 8 x 1024
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q0 = blockIdx.z * 8, nq = min(8, c - q0);
+  const int i = blockIdx.y * 32 + w * 4;
+  double acc[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[a][q] = 0.0;
+  const int64_t cbeg = (int64_t)blockIdx.x * kMChunk, cend = imin(n, cbeg + kMChunk);
+  for (int64_t s0 = cbeg; s0 < cend; s0 += 1024) {
+    const int sn = (int)imin(1024, cend - s0);
+    __syncthreads();
+    for (int q = 0; q < 8; ++q)
+      for (int t = threadIdx.x; t < 1024; t += blockDim.x)
+        xt[q * 1024 + t] = (q < nq && t < sn) ? X[(int64_t)(q0 + q) * ldx + s0 + t] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      if (i + a >= R) break;
+      const double* row = A + (int64_t)(i + a) * lda + s0;
+      for (int t = lane; t < sn; t += 32) {
+        const double v = row[t];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[a][q] = fma(v, xt[q * 1024 + t], acc[a][q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    if (i + a >= R) break;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double v = warp_sum(acc[a][q]);
+      if (lane == 0 && q < nq) partial[((int64_t)blockIdx.x * R + i + a) * c + q0 + q] = v;
+    }
+  }
+}
+
+__global__ void k_mred(int nchunk, int R, int c, const double* __restrict__ partial,
+                       double* __restrict__ C) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)R * c) return;
+  double s = 0.0;
+  for (int b = 0; b < nchunk; ++b) s += partial[(int64_t)b * R * c + t];
+  C[t] = s;
+}
+
+// mode 0: coefficients C[i][q] for all i < R;  mode 1: strictly-upper only
+// (i < q: the intra-batch projection onto earlier members)
+__global__ void __launch_bounds__(256) k_mupd(const double* __restrict__ B, int64_t ldb, int R,
+                                              const double* __restrict__ C, int c, int mode,
+                                              double* __restrict__ Y, int64_t ldy, int64_t n) {
+  __shared__ double cs[8][512];
+  const int q0 = blockIdx.y * 8, nq = min(8, c - q0);
+  const int64_t col = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  for (int i0 = 0; i0 < R; i0 += 512) {
+    const int ni = min(512, R - i0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < 8 * 512; t += blockDim.x) {
+      const int q = t / 512, ii = t % 512;
+      double v = 0.0;
+      if (q < nq && ii < ni) {
+        v = C[(int64_t)(i0 + ii) * c + q0 + q];
+        if (mode == 1 && i0 + ii >= q0 + q) v = 0.0;
+      }
+      cs[q][ii] = v;
+    }
+    __syncthreads();
+    if (col < n) {
+      for (int ii = 0; ii < ni; ++ii) {
+        const double v = B[(int64_t)(i0 + ii) * ldb + col];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = fma(v, cs[q][ii], acc[q]);
+      }
+    }
+  }
+  if (col < n)
+    for (int q = 0; q < nq; ++q) Y[(int64_t)(q0 + q) * ldy + col] -= acc[q];
+}
+
+// nrm2[q] = X_q . MX_q (one CTA per row, fixed order)
+__global__ void k_rowdots(const double* __restrict__ X, const double* __restrict__ MX, int64_t ld,
+                          int64_t n, double* __restrict__ out) {
+  __shared__ double red[32];
+  const double* x = X + (int64_t)blockIdx.x * ld;
+  const double* mx = MX + (int64_t)blockIdx.x * ld;
+  double s = 0.0;
+  for (int64_t c = threadIdx.x; c < n; c += blockDim.x) s = fma(x[c], mx[c], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// rows q with flag[q] != 0: X_q, MX_q /= sqrt(nrm2[q])
+__global__ void k_rowscale(double* __restrict__ X, double* __restrict__ MX, int64_t ld, int64_t n,
+                           const double* __restrict__ nrm2, const int* __restrict__ flag) {
+  const int q = blockIdx.y;
+  if (flag && !flag[q]) return;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const double nrm = sqrt(fmax(nrm2[q], 0.0));
+  X[(int64_t)q * ld + c] /= nrm;
+  MX[(int64_t)q * ld + c] /= nrm;
+}
+
 }  // namespace riga
 
 using namespace riga;
@@ -760,6 +878,105 @@ int riga_lanczos_step_given(riga_lanczos* lz, const double* w_dev, const double*
 
 }  // extern "C"
 
+
+namespace {
+
+// C (R x c) = A (R rows) . X^T (c rows)
+int mdots(riga_lanczos* lz, const double* A, int R, const double* X, int c, double* C, DevBuf<double>& part) {
+  cudaStream_t s = lz->ctx->stream;
+  if (R == 0 || c == 0) return RIGA_OK;
+  const int nchunk = (int)((lz->n + kMChunk - 1) / kMChunk);
+  RIGA_TRY(part.alloc((int64_t)nchunk * R * c, s));
+  const dim3 g(nchunk, (unsigned)((R + 31) / 32), (unsigned)((c + 7) / 8));
+  k_mdots<<<g, 256, 8 * 1024 * 8, s>>>(A, lz->ld, R, X, lz->ld, c, lz->n, part.p);
+  k_mred<<<(unsigned)(((int64_t)R * c + 255) / 256), 256, 0, s>>>(nchunk, R, c, part.p, C);
+  count_launch(2);
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+// Y_q -= sum_i C[i][q] B_i
+int mupd(riga_lanczos* lz, const double* B, int R, const double* C, int c, int mode, double* Y) {
+  if (R == 0 || c == 0) return RIGA_OK;
+  const dim3 g((unsigned)((lz->n + 255) / 256), (unsigned)((c + 7) / 8));
+  k_mupd<<<g, 256, 0, lz->ctx->stream>>>(B, lz->ld, R, C, c, mode, Y, lz->ld, lz->n);
+  count_launch();
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int riga_lanczos_lock_block(riga_lanczos* lz, double* X, double* MX, int64_t c, int64_t ldx,
+                            double* nrm2_host) {
+  RIGA_CHECK_ARG(lz && X && MX && nrm2_host && c >= 0, "null arg");
+  RIGA_CHECK_ARG(ldx == lz->ld, "rows must use the basis leading dimension");
+  if (c == 0) return RIGA_OK;
+  DeviceGuard g(lz->ctx->device);
+  cudaStream_t s = lz->ctx->stream;
+  static int attr = 0;
+  if (!attr) {
+    RIGA_CUDA(cudaFuncSetAttribute(k_mdots, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 1024 * 8));
+    attr = 1;
+  }
+  const int nl = (int)lz->nlocked, cc = (int)c;
+  DevBuf<double> part, C, G, nrm, Xt, MXt;
+  RIGA_TRY(C.alloc(std::max<int64_t>((int64_t)nl * cc, 1), s));
+  RIGA_TRY(G.alloc((int64_t)cc * cc, s));
+  RIGA_TRY(nrm.alloc(cc, s));
+  RIGA_TRY(Xt.alloc(c * lz->ld, s));
+  RIGA_TRY(MXt.alloc(c * lz->ld, s));
+  const dim3 gs((unsigned)((lz->n + 255) / 256), (unsigned)cc);
+  // M-normalise the lifted vectors (ref: x /= sqrt(x.Mx))
+  k_rowdots<<<cc, 256, 0, s>>>(X, MX, lz->ld, lz->n, nrm.p);
+  k_rowscale<<<gs, 256, 0, s>>>(X, MX, lz->ld, lz->n, nrm.p, nullptr);
+  count_launch(2);
+  for (int p = 0; p < 2; ++p) {
+    if (nl > 0) {  // against the locked set: C = LM X^T, X -= L^T C, MX -= LM^T C
+      RIGA_TRY(mdots(lz, lz->LM.p, nl, X, cc, C.p, part));
+      RIGA_TRY(mupd(lz, lz->L.p, nl, C.p, cc, 0, X));
+      RIGA_TRY(mupd(lz, lz->LM.p, nl, C.p, cc, 0, MX));
+    }
+    if (cc > 1) {  // against the earlier members of the batch
+      RIGA_TRY(mdots(lz, MX, cc, X, cc, G.p, part));
+      RIGA_CUDA(cudaMemcpyAsync(Xt.p, X, c * lz->ld * 8, cudaMemcpyDeviceToDevice, s));
+      RIGA_CUDA(cudaMemcpyAsync(MXt.p, MX, c * lz->ld * 8, cudaMemcpyDeviceToDevice, s));
+      RIGA_TRY(mupd(lz, Xt.p, cc, G.p, cc, 1, X));
+      RIGA_TRY(mupd(lz, MXt.p, cc, G.p, cc, 1, MX));
+    }
+  }
+  k_rowdots<<<cc, 256, 0, s>>>(X, MX, lz->ld, lz->n, nrm.p);
+  count_launch();
+  RIGA_CUDA(cudaMemcpyAsync(nrm2_host, nrm.p, c * 8, cudaMemcpyDeviceToHost, s));
+  RIGA_CUDA(cudaStreamSynchronize(s));
+  return RIGA_OK;
+}
+
+int riga_lanczos_append_rows(riga_lanczos* lz, double* X, double* MX, int64_t c, int64_t ldx,
+                             const double* nrm2_host, const int* scale_host) {
+  RIGA_CHECK_ARG(lz && X && MX && c >= 0 && ldx == lz->ld, "bad arg");
+  if (c == 0) return RIGA_OK;
+  DeviceGuard g(lz->ctx->device);
+  cudaStream_t s = lz->ctx->stream;
+  RIGA_TRY(grow_locked(lz, lz->nlocked + c));
+  DevBuf<double> nrm;
+  DevBuf<int> flag;
+  RIGA_TRY(nrm.upload(nrm2_host, c, s));
+  RIGA_TRY(flag.upload(scale_host, c, s));
+  const dim3 gs((unsigned)((lz->n + 255) / 256), (unsigned)c);
+  k_rowscale<<<gs, 256, 0, s>>>(X, MX, lz->ld, lz->n, nrm.p, flag.p);
+  count_launch();
+  RIGA_CUDA(cudaMemcpyAsync(lz->L.p + lz->nlocked * lz->ld, X, c * lz->ld * 8, cudaMemcpyDeviceToDevice, s));
+  RIGA_CUDA(cudaMemcpyAsync(lz->LM.p + lz->nlocked * lz->ld, MX, c * lz->ld * 8, cudaMemcpyDeviceToDevice, s));
+  lz->nlocked += c;
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+}  // extern "C"
+
 static int lift_rows(riga_lanczos* lz, const double* Vb, int64_t k, const double* Wd, int64_t c,
                      double* X) {
   cudaStream_t s = lz->ctx->stream;
@@ -845,6 +1062,15 @@ int riga_lanczos_lock_batch(riga_lanczos* lz, double* X, double* MX, int64_t c, 
   RIGA_TRY(pull_state(lz));
   lz->nlocked = lz->hst->nlocked;
   return RIGA_OK;
+}
+
+int riga_lanczos_cgs_probe(riga_lanczos* lz, double* x, int passes, int64_t* rows) {
+  RIGA_CHECK_ARG(lz && x && passes >= 0, "null arg");
+  DeviceGuard g(lz->ctx->device);
+  RIGA_TRY(push_state(lz, lz->k, lz->k, 0.0));
+  if (rows) *rows = lz->k + lz->nlocked;
+  return cgs_passes(lz, sel_basis(lz, true, 0), sel_basis(lz, false, 0), RowSel{}, x, nullptr, passes,
+                    lz->k + lz->nlocked);
 }
 
 int riga_lanczos_project_locked(riga_lanczos* lz, double* x, double* mx, int passes) {

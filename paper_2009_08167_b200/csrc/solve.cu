@@ -32,6 +32,7 @@ constexpr int kWholeMaxNp = 64;  // max pivots of a small supernode
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int64_t kChainSmemMax = 232448 - 4096;  // staged chain panels must fit this
+constexpr int64_t kPrefetchMaxBytes = 96ll << 20;  // prefetch the factor into L2 when it fits
 
 enum { kWholeGroup = 1, kUpd = 2, kColdot = 3 };
 
@@ -417,6 +418,21 @@ __global__ void __launch_bounds__(kSolveThreads) k_chain_bwd(SymDev S, const int
   }
 }
 
+// L2 warm-up: bulk-prefetch the factor panels (contiguous) so the level
+// kernels' latency-bound loads hit L2 (the factor of a 2D config fits in the
+// 126 MB L2, but the Gram-Schmidt traffic of the previous step evicts it)
+__global__ void k_prefetch_l2(const double* __restrict__ p, int64_t bytes) {
+  const int64_t chunk = 32768;
+  for (int64_t off = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * chunk; off < bytes;
+       off += (int64_t)gridDim.x * blockDim.x * chunk) {
+    const int64_t len = imin(chunk, bytes - off) & ~int64_t(15);
+    if (len > 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(p) + off),
+                   "r"((unsigned)len)
+                   : "memory");
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host: per-level task lists, pull map
 // ---------------------------------------------------------------------------
@@ -552,6 +568,12 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   SolveDev T{sym->d_gptr.p, sym->d_gsrc.p, b_permuted ? 1 : 0};
   const int2* tf = reinterpret_cast<const int2*>(sym->d_tfwd.p);
   const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
+  const int64_t pbytes = h.panel_total * 8;
+  if (pbytes <= kPrefetchMaxBytes) {
+    k_prefetch_l2<<<(unsigned)std::min<int64_t>(148, (pbytes / 32768 + 255) / 256 + 1), 256, 0, st>>>(F->panel.p,
+                                                                                                   pbytes);
+    count_launch();
+  }
   for (int64_t l = 0; l < h.nlevels; ++l) {
     const int nc = (int)(L.chain_ptr[l + 1] - L.chain_ptr[l]);
     if (nc) {
