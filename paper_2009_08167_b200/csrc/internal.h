@@ -43,6 +43,7 @@ struct SolvePlanHost {
   std::vector<I2> fwd, bwd;        // light tasks grouped by level
   std::vector<int32_t> chains;     // large supernodes grouped by level
   std::vector<int32_t> wholes;     // small supernodes (warp tasks) grouped by level
+  std::vector<int32_t> sub_ptr, sub_nodes;  // bottom subtrees (postorder ranges), one per warp
   std::vector<int64_t> fwd_ptr, bwd_ptr, chain_ptr;
   std::vector<int64_t> fwd_smem, bwd_smem, chf_smem, chb_smem;  // bytes per level launch
   std::vector<int32_t> gsrc;
@@ -65,7 +66,7 @@ struct riga_symbolic {
   int64_t n_large = 0;
   SolvePlanHost sp;
   riga::DevBuf<I2> d_tfwd, d_tbwd;
-  riga::DevBuf<int32_t> d_chains, d_wholes, d_gsrc;
+  riga::DevBuf<int32_t> d_chains, d_wholes, d_gsrc, d_sub_ptr, d_sub_nodes;
   riga::DevBuf<int64_t> d_gptr;
   SymDev dev() const {
     return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,

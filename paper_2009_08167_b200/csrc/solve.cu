@@ -29,6 +29,9 @@ namespace riga {
 
 constexpr int kWholeMaxF = 256;  // max front rows of a small (warp-task) supernode
 constexpr int kWholeMaxNp = 64;  // max pivots of a small supernode
+constexpr int kWarpPanel = 3328;  // doubles of a warp's staged panel (f * np <= this)
+constexpr int kWarpSmem = kWholeMaxF + kWarpPanel;  // doubles of smem per warp task
+constexpr int kSubtreeMax = 0;   // bottom-subtree walk per warp (0 = off: slower than level kernels)
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int64_t kChainSmemMax = 232448 - 4096;  // staged chain panels must fit this
@@ -44,11 +47,38 @@ struct SolveDev {
 
 __device__ __forceinline__ double gather_row(const SymDev& S, const SolveDev& T, int s, int64_t r,
                                              int64_t np, int64_t col0, const double* __restrict__ b,
-                                             const double* __restrict__ upd) {
+                                             const double* upd) {
   double v = r < np ? b[T.permuted ? col0 + r : S.order[col0 + r]] : 0.0;
   const int64_t g = S.rows_off[s] + r;
   for (int64_t q = T.gptr[g]; q < T.gptr[g + 1]; ++q) v += upd[T.gsrc[q]];
   return v;
+}
+
+// --- TMA bulk copy global -> shared, completion on an mbarrier --------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  unsigned ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(b), "r"(phase)
+        : "memory");
+  }
 }
 
 // unit-lower 32x32 diagonal block solve by one warp, row `lane` in registers
@@ -72,6 +102,168 @@ __device__ __forceinline__ double diag_solve_t(const double* __restrict__ P, int
   return xc;
 }
 
+// one warp: forward sweep of a small supernode (front in `yw`, <= kWholeMaxF rows).
+// 32-bit local indexing; loops are specialised on the real block width so a
+// tiny supernode (np = 7) does not pay for 32-wide predicated code.
+__device__ __forceinline__ void warp_whole_fwd(const SymDev& S, const SolveDev& T, int s,
+                                               const double* __restrict__ panel,
+                                               const double* __restrict__ b, double* xp, double* upd,
+                                               double* yw, int lane, uint64_t* bar) {
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const double* P = panel + S.panel_off[s];
+  const bool staged = bar && f * np <= kWarpPanel;
+  if (staged) {  // the whole panel to shared memory with one bulk copy, overlapping the gather
+    double* sp = yw + kWholeMaxF;
+    if (lane == 0) bulk_load(sp, P, (unsigned)(((f * np + 1) & ~1) * 8), bar);
+    P = sp;
+  }
+  for (int r = lane; r < f; r += 32) yw[r] = gather_row(S, T, s, r, np, col0, b, upd);
+  if (staged) mbar_wait(bar, 0);
+  __syncwarp();
+  for (int kb = 0; kb < np; kb += 32) {
+    const int nbk = min(32, np - kb);
+    double z = lane < nbk ? yw[kb + lane] : 0.0;
+    if (nbk == 32) {
+      z = diag_solve(P, f, kb, 32, lane, z);
+    } else {
+      const double* Pd = P + kb * f + kb + lane;
+      for (int k = 0; k + 1 < nbk; ++k) {
+        const double zk = __shfl_sync(0xffffffffu, z, k);
+        if (lane > k && lane < nbk) z = fma(-Pd[k * f], zk, z);
+      }
+    }
+    if (lane < nbk) yw[kb + lane] = z;
+    __syncwarp();
+    const double* Pc = P + kb * f;
+    for (int i = kb + nbk + lane; i < f; i += 32) {
+      double acc = 0.0;
+      if (nbk == 32) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc = fma(Pc[k * f + i], yw[kb + k], acc);
+      } else {
+        for (int k = 0; k < nbk; ++k) acc = fma(Pc[k * f + i], yw[kb + k], acc);
+      }
+      yw[i] -= acc;
+    }
+    __syncwarp();
+  }
+  for (int r = lane; r < np; r += 32) xp[col0 + r] = yw[r];
+  double* u = upd + S.upd_off[s];
+  for (int r = np + lane; r < f; r += 32) u[r - np] = yw[r];
+}
+
+// one warp: backward sweep of a small supernode
+__device__ __forceinline__ void warp_whole_bwd(const SymDev& S, int s, const double* __restrict__ panel,
+                                               const double* __restrict__ D, double* xp, double* x,
+                                               double* yw, int lane, uint64_t* bar) {
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const double* P = panel + S.panel_off[s];
+  const int32_t* rows = S.rows + S.rows_off[s];
+  const bool staged = bar && f * np <= kWarpPanel;
+  if (staged) {
+    double* sp = yw + kWholeMaxF;
+    if (lane == 0) bulk_load(sp, P, (unsigned)(((f * np + 1) & ~1) * 8), bar);
+    P = sp;
+  }
+  for (int r = lane; r < f; r += 32) yw[r] = r < np ? xp[col0 + r] / D[col0 + r] : xp[rows[r]];
+  if (staged) mbar_wait(bar, 0);
+  __syncwarp();
+  const int nblk = (np + 31) / 32;
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int kb = bi * 32;
+    const int nbk = min(32, np - kb);
+    double red;  // lane c: sum over rows below the block of L[i][kb+c] y[i]
+    if (nbk == 32) {
+      double acc[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+      for (int i = kb + 32 + lane; i < f; i += 32) {
+        const double yv = yw[i];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] = fma(P[(kb + c) * f + i], yv, acc[c]);
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < o; ++k) {
+          const bool hi = (lane & o) != 0;
+          const double send = hi ? acc[k] : acc[k + o];
+          const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+          acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
+        }
+      }
+      red = acc[0];
+    } else {
+      red = 0.0;
+      for (int c = 0; c < nbk; ++c) {
+        const double* Pc = P + (kb + c) * f;
+        double a = 0.0;
+        for (int i = kb + nbk + lane; i < f; i += 32) a = fma(Pc[i], yw[i], a);
+        a = warp_sum(a);
+        if (lane == c) red = a;
+      }
+    }
+    double xc = lane < nbk ? yw[kb + lane] - red : 0.0;
+    if (nbk == 32) {
+      xc = diag_solve_t(P, f, kb, 32, lane, xc);
+    } else {
+      const double* Pd = P + (kb + lane) * f + kb;
+      for (int k = nbk - 1; k >= 1; --k) {
+        const double xk = __shfl_sync(0xffffffffu, xc, k);
+        if (lane < k) xc = fma(-Pd[k], xk, xc);
+      }
+    }
+    if (lane < nbk) yw[kb + lane] = xc;
+    __syncwarp();
+  }
+  for (int r = lane; r < np; r += 32) {
+    xp[col0 + r] = yw[r];
+    x[S.order[col0 + r]] = yw[r];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bottom subtrees: one warp walks a whole subtree of small supernodes
+// (postorder forward, reverse postorder backward); the warp's own earlier
+// writes (update vectors, x) are visible to it after __syncwarp, so the
+// bottom of the tree needs one launch per sweep instead of one per level.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSolveThreads) k_subtree_fwd(SymDev S, SolveDev T,
+                                                               const int32_t* __restrict__ sub_ptr,
+                                                               const int32_t* __restrict__ sub_nodes, int nsub,
+                                                               const double* __restrict__ panel,
+                                                               const double* __restrict__ b,
+                                                               double* __restrict__ xp,
+                                                               double* __restrict__ upd) {
+  extern __shared__ double y[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = blockIdx.x * kSolveWarps + w;
+  if (t >= nsub) return;
+  for (int q = sub_ptr[t]; q < sub_ptr[t + 1]; ++q) {
+    warp_whole_fwd(S, T, sub_nodes[q], panel, b, xp, upd, y + w * kWholeMaxF, lane, nullptr);
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kSolveThreads) k_subtree_bwd(SymDev S,
+                                                               const int32_t* __restrict__ sub_ptr,
+                                                               const int32_t* __restrict__ sub_nodes, int nsub,
+                                                               const double* __restrict__ panel,
+                                                               const double* __restrict__ D,
+                                                               double* __restrict__ xp,
+                                                               double* __restrict__ x) {
+  extern __shared__ double y[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = blockIdx.x * kSolveWarps + w;
+  if (t >= nsub) return;
+  for (int q = sub_ptr[t + 1] - 1; q >= sub_ptr[t]; --q) {
+    warp_whole_bwd(S, sub_nodes[q], panel, D, xp, x, y + w * kWholeMaxF, lane, nullptr);
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // light kernels: WHOLE / UPD (forward), WHOLE / COLDOT (backward)
 // ---------------------------------------------------------------------------
@@ -82,42 +274,18 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_fwd(SymDev S, SolveDe
                                                             const double* __restrict__ b,
                                                             double* __restrict__ xp,
                                                             double* __restrict__ upd) {
-  extern __shared__ double y[];
+  extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
+  __shared__ uint64_t wbar[kSolveWarps];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int2 task = tasks[blockIdx.x];
   const int type = task.y >> 24, j = task.y & 0x00ffffff;
   if (type == kWholeGroup) {
     // warp w: small supernode wholes[task.x + w], whole front in a warp slice
     if (w >= j) return;
-    const int s = wholes[task.x + w];
-    const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
-    const double* P = panel + S.panel_off[s];
-    double* yw = y + w * kWholeMaxF;
-    for (int64_t r = lane; r < f; r += 32) yw[r] = gather_row(S, T, s, r, np, col0, b, upd);
+    if (lane == 0) mbar_init(&wbar[w], 1);
     __syncwarp();
-    for (int64_t kb = 0; kb < np; kb += 32) {
-      const int nbk = (int)imin(32, np - kb);
-      double z = lane < nbk ? yw[kb + lane] : 0.0;
-      z = diag_solve(P, f, kb, nbk, lane, z);
-      if (lane < nbk) yw[kb + lane] = z;
-      __syncwarp();
-      for (int64_t i0 = kb + nbk; i0 < f; i0 += 32) {
-        const int64_t i = i0 + lane;
-        const bool in = i < f;
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const double l = (in && k < nbk) ? P[(kb + k) * f + i] : 0.0;
-          acc = fma(l, __shfl_sync(0xffffffffu, z, k), acc);
-        }
-        if (in) yw[i] -= acc;
-      }
-      __syncwarp();
-    }
-    for (int64_t r = lane; r < np; r += 32) xp[col0 + r] = yw[r];
-    double* u = upd + S.upd_off[s];
-    for (int64_t r = np + lane; r < f; r += 32) u[r - np] = yw[r];
+    warp_whole_fwd(S, T, wholes[task.x + w], panel, b, xp, upd, y + w * kWarpSmem, lane, &wbar[w]);
     return;
   }
   const int s = task.x;
@@ -158,52 +326,18 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_bwd(SymDev S, SolveDe
                                                             double* __restrict__ xp,
                                                             double* __restrict__ cvec,
                                                             double* __restrict__ x) {
-  extern __shared__ double y[];
+  extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
+  __shared__ uint64_t wbar[kSolveWarps];
   double (*tile)[32][33] = reinterpret_cast<double (*)[32][33]>(y);  // COLDOT transposes
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int2 task = tasks[blockIdx.x];
   const int type = task.y >> 24, bj = task.y & 0x00ffffff;
   if (type == kWholeGroup) {
     if (w >= bj) return;
-    const int s = wholes[task.x + w];
-    const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
-    const double* P = panel + S.panel_off[s];
-    const int32_t* rows = S.rows + S.rows_off[s];
-    double* yw = y + w * kWholeMaxF;
-    for (int64_t r = lane; r < f; r += 32) yw[r] = r < np ? xp[col0 + r] / D[col0 + r] : xp[rows[r]];
+    if (lane == 0) mbar_init(&wbar[w], 1);
     __syncwarp();
-    const int64_t nblk = (np + 31) / 32;
-    for (int64_t bi = nblk - 1; bi >= 0; --bi) {
-      const int64_t kb = bi * 32;
-      const int nbk = (int)imin(32, np - kb);
-      double acc[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) acc[c] = 0.0;
-      for (int64_t i = kb + nbk + lane; i < f; i += 32) {
-        const double yv = yw[i];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] = fma(c < nbk ? P[(kb + c) * f + i] : 0.0, yv, acc[c]);
-      }
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-#pragma unroll
-        for (int k = 0; k < o; ++k) {
-          const bool hi = (lane & o) != 0;
-          const double send = hi ? acc[k] : acc[k + o];
-          const double recv = __shfl_xor_sync(0xffffffffu, send, o);
-          acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
-        }
-      }
-      double xc = lane < nbk ? yw[kb + lane] - acc[0] : 0.0;
-      xc = diag_solve_t(P, f, kb, nbk, lane, xc);
-      if (lane < nbk) yw[kb + lane] = xc;
-      __syncwarp();
-    }
-    for (int64_t r = lane; r < np; r += 32) {
-      xp[col0 + r] = yw[r];
-      x[S.order[col0 + r]] = yw[r];
-    }
+    warp_whole_bwd(S, wholes[task.x + w], panel, D, xp, x, y + w * kWarpSmem, lane, &wbar[w]);
     return;
   }
   const int s = task.x;
@@ -442,6 +576,30 @@ int build_solve_plan(riga_symbolic* sym) {
   const int64_t ns = h.nsuper;
   L = SolvePlanHost();
   auto large = [&](int64_t s) { return h.ncol[s] > kWholeMaxNp || h.front[s] > kWholeMaxF; };
+  // bottom subtrees of small supernodes, at most kSubtreeMax nodes each;
+  // supernodes are numbered in postorder, so a subtree is a contiguous range
+  std::vector<int32_t> size(ns, 1);
+  std::vector<char> ok(ns, 1);
+  for (int64_t s = 0; s < ns; ++s) {
+    if (large(s)) ok[s] = 0;
+    for (int64_t q = h.child_ptr[s]; q < h.child_ptr[s + 1]; ++q) {
+      const int32_t c = h.child_list[q];
+      size[s] += size[c];
+      if (!ok[c]) ok[s] = 0;
+    }
+    if (size[s] > kSubtreeMax) ok[s] = 0;
+  }
+  std::vector<char> in_sub(ns, 0);
+  L.sub_ptr.assign(1, 0);
+  for (int64_t s = 0; s < ns; ++s) {
+    const int32_t p = h.sparent[s];
+    if (!ok[s] || (p >= 0 && ok[p])) continue;  // not a maximal eligible subtree root
+    for (int64_t q = s - size[s] + 1; q <= s; ++q) {
+      L.sub_nodes.push_back((int32_t)q);
+      in_sub[q] = 1;
+    }
+    L.sub_ptr.push_back((int32_t)L.sub_nodes.size());
+  }
   L.fwd_ptr.assign(h.nlevels + 1, 0);
   L.bwd_ptr.assign(h.nlevels + 1, 0);
   L.chain_ptr.assign(h.nlevels + 1, 0);
@@ -459,6 +617,7 @@ int build_solve_plan(riga_symbolic* sym) {
     int64_t smf = 1, smb = 1, scf = 1, scb = 1;
     std::vector<int32_t> small;
     for (int32_t s : nodes) {
+      if (in_sub[s]) continue;
       if (large(s)) {
         const int64_t np = h.ncol[s], nblk = (np + 31) / 32;
         L.chains.push_back(s);
@@ -485,8 +644,8 @@ int build_solve_plan(riga_symbolic* sym) {
     }
     L.wholes.insert(L.wholes.end(), small.begin(), small.end());
     if (!small.empty()) {
-      smf = std::max<int64_t>(smf, kSolveWarps * kWholeMaxF);
-      smb = std::max<int64_t>(smb, kSolveWarps * kWholeMaxF);
+      smf = std::max<int64_t>(smf, kSolveWarps * kWarpSmem);
+      smb = std::max<int64_t>(smb, kSolveWarps * kWarpSmem);
     }
     L.fwd_ptr[l + 1] = (int64_t)L.fwd.size();
     L.bwd_ptr[l + 1] = (int64_t)L.bwd.size();
@@ -524,6 +683,10 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
   if (!L.bwd.empty()) RIGA_TRY(sym->d_tbwd.upload(L.bwd.data(), L.bwd.size(), s));
   if (!L.chains.empty()) RIGA_TRY(sym->d_chains.upload(L.chains.data(), L.chains.size(), s));
   if (!L.wholes.empty()) RIGA_TRY(sym->d_wholes.upload(L.wholes.data(), L.wholes.size(), s));
+  if (!L.sub_nodes.empty()) {
+    RIGA_TRY(sym->d_sub_nodes.upload(L.sub_nodes.data(), L.sub_nodes.size(), s));
+    RIGA_TRY(sym->d_sub_ptr.upload(L.sub_ptr.data(), L.sub_ptr.size(), s));
+  }
   RIGA_TRY(sym->d_gptr.upload(L.gptr.data(), L.gptr.size(), s));
   if (L.gsrc.empty())
     RIGA_TRY(sym->d_gsrc.alloc(1, s));
@@ -551,6 +714,8 @@ static int set_solve_attrs() {
   RIGA_TRY(raise_smem(k_rest_bwd, maxsm));
   RIGA_TRY(raise_smem(k_chain_fwd, maxsm));
   RIGA_TRY(raise_smem(k_chain_bwd, maxsm));
+  RIGA_TRY(raise_smem(k_subtree_fwd, maxsm));
+  RIGA_TRY(raise_smem(k_subtree_bwd, maxsm));
   done = true;
   return RIGA_OK;
 }
@@ -572,6 +737,12 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   if (pbytes <= kPrefetchMaxBytes) {
     k_prefetch_l2<<<(unsigned)std::min<int64_t>(148, (pbytes / 32768 + 255) / 256 + 1), 256, 0, st>>>(F->panel.p,
                                                                                                    pbytes);
+    count_launch();
+  }
+  const int nsub = (int)L.sub_ptr.size() - 1;
+  if (nsub > 0) {
+    k_subtree_fwd<<<(nsub + kSolveWarps - 1) / kSolveWarps, kSolveThreads, kSolveWarps * kWholeMaxF * 8, st>>>(
+        S, T, sym->d_sub_ptr.p, sym->d_sub_nodes.p, nsub, F->panel.p, b, F->xperm.p, F->upd.p);
     count_launch();
   }
   for (int64_t l = 0; l < h.nlevels; ++l) {
@@ -603,6 +774,11 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
                                                             F->xperm.p, F->cvec.p, x);
       count_launch();
     }
+  }
+  if (nsub > 0) {
+    k_subtree_bwd<<<(nsub + kSolveWarps - 1) / kSolveWarps, kSolveThreads, kSolveWarps * kWholeMaxF * 8, st>>>(
+        S, sym->d_sub_ptr.p, sym->d_sub_nodes.p, nsub, F->panel.p, F->D.p, F->xperm.p, x);
+    count_launch();
   }
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;

@@ -297,7 +297,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
       if ((pass == 0) != large) continue;
       int64_t f = S.front[s], np = S.ncol[s], nu = f - np;
       S.panel_off[s] = S.panel_total;
-      S.panel_total += f * np;
+      S.panel_total += (f * np + 1) & ~int64_t(1);  // 16-byte aligned panels (TMA bulk copies)
       S.cb_off[s] = S.cb_total;
       S.cb_total += nu * nu;
     }

@@ -152,6 +152,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
 
     # --- 3. solve my slices concurrently on `streams` CUDA streams ----------
     results = {}
+    slice_times = {}
     errors = []
     lock = threading.Lock()
     queue = sorted(my, key=lambda k: -expected[k])
@@ -166,6 +167,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                         break
                     k = queue.pop(0)
                 try:
+                    t_start = time.perf_counter()
                     pen = make_pencil(ctx, cnt)
                     lo, hi = float(sig_used[k]), float(sig_used[k + 1])
                     if k in kept:
@@ -193,6 +195,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                     ctx.synchronize()
                     with lock:
                         results[k] = (lams, X)
+                        slice_times[k] = (t_start - t0, time.perf_counter() - t0, cnt.nfb)
                 except Exception as e:  # surfaced after join
                     with lock:
                         errors.append((k, e))
@@ -241,6 +244,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     res = SlicesResult(sig_used, nu, expected, found, eig, my, local_eigs,
                        {k: results[k][1] for k in my}, counters)
     res.timings = {"boundary_s": t_bnd, "slices_s": t_sl, "total_s": time.perf_counter() - t_all,
-                   "boundary_pairs": sum(len(v) for v in bnear.values())}
+                   "boundary_pairs": sum(len(v) for v in bnear.values()),
+                   "slice_wall": {int(k): [round(a, 3), round(b, 3)] for k, (a, b, _) in slice_times.items()}}
     res.factor_ms = [allb[k][2] for k in range(S + 1)]
     return res

@@ -1,0 +1,20 @@
+"""Per-slice wall-clock timeline of one cfg3 solve_uniform_slices call."""
+import json, os, sys, time
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2009_08167_b200 as P  # noqa
+from paper_2009_08167_b200.configs import CONFIGS  # noqa
+from paper_2009_08167_b200.sparsela import Symbolic  # noqa
+c = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg3"]
+streams = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+s = P.build_system(c.d, c.ne, c.p, c.level)
+lam_e, cnt = P.choose_lambda_e(s, c.n0)
+sh = P.uniform_shifts(lam_e, c.slices)
+perm = P.separator_ordering(s)
+sym = Symbolic.on_device(s.device, perm)
+for it in range(2):
+    t0 = time.perf_counter()
+    r = P.solve_uniform_slices(s, sh, streams=streams, pencil_symbolic=sym, perm=perm)
+    print("total", round(time.perf_counter() - t0, 3), "boundary", round(r.timings["boundary_s"], 3),
+          "slices", round(r.timings["slices_s"], 3), "nfb", r.counters.nfb)
+print(json.dumps(r.timings["slice_wall"]))
