@@ -484,7 +484,7 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   }
   if (cbuf) RIGA_CUDA(cudaFreeAsync(cbuf, st));
   RIGA_CUDA(cudaFreeAsync(scratch, st));
-  return RIGA_OK;
+  return build_chain_inverse(F, st);
 }
 
 }  // namespace riga

@@ -40,6 +40,11 @@ struct I2 {
 
 // Task lists and pull map of the persistent solve kernels (solve.cu).
 struct SolvePlanHost {
+  int warp_stage = 0, l2_prefetch = 0, chain_inv = 1;
+  int64_t inv_total = 0;               // doubles of the inv(L11) blocks of the chain supernodes
+  std::vector<int64_t> inv_off;        // per supernode offset into linv (-1: none)
+  std::vector<I2> ifwd, ibwd, idiag, icol;  // (supernode, 32-row tile / 8-row group / 32-col block)
+  std::vector<int64_t> ifwd_ptr, ibwd_ptr, ifwd_smem;
   std::vector<I2> fwd, bwd;        // light tasks grouped by level
   std::vector<int32_t> chains;     // large supernodes grouped by level
   std::vector<int32_t> wholes;     // small supernodes (warp tasks) grouped by level
@@ -67,7 +72,8 @@ struct riga_symbolic {
   SolvePlanHost sp;
   riga::DevBuf<I2> d_tfwd, d_tbwd;
   riga::DevBuf<int32_t> d_chains, d_wholes, d_gsrc, d_sub_ptr, d_sub_nodes;
-  riga::DevBuf<int64_t> d_gptr;
+  riga::DevBuf<int64_t> d_gptr, d_inv_off;
+  riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_icol;
   SymDev dev() const {
     return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,
                   d_cb_off.p,   d_upd_off.p,   d_child_ptr.p,  d_asm_ptr.p,    d_sparent.p,
@@ -87,6 +93,7 @@ struct riga_factor {
   riga::DevBuf<int64_t> stat;  // [0] n_negative, [1] first bad pivot (n if none)
   riga::DevBuf<double> cvec;   // backward L21^T x partial sums
   riga::DevBuf<double> tol;    // [0] max|A|, [1] zero_tol
+  riga::DevBuf<double> linv;   // inv(L11) of the chain supernodes (solve.cu)
   float factor_ms = 0.f;
 };
 
@@ -101,4 +108,5 @@ int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x,
 int build_solve_plan(riga_symbolic* sym);
 int prepare_solve();
 int upload_solve_plan(riga_symbolic* sym, cudaStream_t s);
+int build_chain_inverse(riga_factor* F, cudaStream_t s);
 }  // namespace riga

@@ -19,6 +19,7 @@
 //             k_chain_bwd  transposed warp-specialised chain of each large
 //                          supernode's pivot part.
 // Stream order is the only synchronisation: no flags across CTAs.
+#include <cstdlib>
 #include <algorithm>
 
 #include "internal.h"
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_fwd(SymDev S, SolveDe
                                                             const double* __restrict__ panel,
                                                             const double* __restrict__ b,
                                                             double* __restrict__ xp,
-                                                            double* __restrict__ upd) {
+                                                            double* __restrict__ upd, int stage) {
   extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
@@ -283,9 +284,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_fwd(SymDev S, SolveDe
   if (type == kWholeGroup) {
     // warp w: small supernode wholes[task.x + w], whole front in a warp slice
     if (w >= j) return;
-    if (lane == 0) mbar_init(&wbar[w], 1);
+    if (stage && lane == 0) mbar_init(&wbar[w], 1);
     __syncwarp();
-    warp_whole_fwd(S, T, wholes[task.x + w], panel, b, xp, upd, y + w * kWarpSmem, lane, &wbar[w]);
+    warp_whole_fwd(S, T, wholes[task.x + w], panel, b, xp, upd, y + w * (stage ? kWarpSmem : kWholeMaxF), lane,
+                   stage ? &wbar[w] : nullptr);
     return;
   }
   const int s = task.x;
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_bwd(SymDev S, SolveDe
                                                             const double* __restrict__ D,
                                                             double* __restrict__ xp,
                                                             double* __restrict__ cvec,
-                                                            double* __restrict__ x) {
+                                                            double* __restrict__ x, int stage, int inv) {
   extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
@@ -335,9 +337,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_bwd(SymDev S, SolveDe
   const int type = task.y >> 24, bj = task.y & 0x00ffffff;
   if (type == kWholeGroup) {
     if (w >= bj) return;
-    if (lane == 0) mbar_init(&wbar[w], 1);
+    if (stage && lane == 0) mbar_init(&wbar[w], 1);
     __syncwarp();
-    warp_whole_bwd(S, wholes[task.x + w], panel, D, xp, x, y + w * kWarpSmem, lane, &wbar[w]);
+    warp_whole_bwd(S, wholes[task.x + w], panel, D, xp, x, y + w * (stage ? kWarpSmem : kWholeMaxF), lane,
+                   stage ? &wbar[w] : nullptr);
     return;
   }
   const int s = task.x;
@@ -368,7 +371,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_bwd(SymDev S, SolveDe
       double v = 0.0;
 #pragma unroll
       for (int q = 0; q < kSolveWarps; ++q) v += part[q][lane];
-      if (lane < nc) cvec[col0 + c0 + lane] = v;
+      if (lane < nc) {
+        double* c = cvec + col0 + c0 + lane;
+        *c = inv ? *c - v : v;  // inverse path: cvec already holds z ./ d
+      }
     }
   }
 }
@@ -552,6 +558,149 @@ __global__ void __launch_bounds__(kSolveThreads) k_chain_bwd(SymDev S, const int
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// chain supernodes through the explicit inverse of their pivot block
+//
+// The pivot block L11 (np x np, unit lower) of every large supernode is
+// inverted once per factorisation (k_trinv_diag / k_trinv_cols, part of the
+// numeric factorisation), so the dependent 32-column chain of the solve
+// becomes two parallel triangular mat-vecs:
+//     forward   z  = inv(L11) y1                 (k_inv_fwd, 32-row tiles)
+//     backward  x1 = inv(L11)^T (z ./ d - L21^T x2)  (k_inv_bwd, warp per row)
+// spread over many CTAs instead of one CTA walking np/32 serial steps.
+// Layout: inv(L11) column-major, ld np, at linv + inv_off[s]; entries above
+// the diagonal inside a diagonal 32x32 block are zero (the tiles read them).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_trinv_diag(SymDev S, const int2* __restrict__ tasks, int ntask,
+                                                    const double* __restrict__ panel,
+                                                    const int64_t* __restrict__ inv_off, double* linv) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= ntask) return;
+  const int s = tasks[t].x;
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int j0 = 32 * tasks[t].y, nb = min(32, np - j0);
+  const double* P = panel + S.panel_off[s];
+  // lane c: column c of inv(L_bb), rows in order: x_r = [r == c] - sum_{c<=k<r} L(r,k) x_k
+  double x[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    double v = r == lane ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < r; ++k) v = (k >= lane && r < nb) ? fma(-P[(int64_t)(j0 + k) * f + j0 + r], x[k], v) : v;
+    x[r] = v;
+  }
+  if (lane < nb) {
+    double* X = linv + inv_off[s] + (int64_t)(j0 + lane) * np + j0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r < nb) X[r] = x[r];
+  }
+}
+
+// one CTA per (supernode, 32-column block b): X(:, b) below the diagonal,
+// block row by block row, X_ib = -inv(L_ii) sum_{b<=k<i} L_ik X_kb
+__global__ void __launch_bounds__(256) k_trinv_cols(SymDev S, const int2* __restrict__ tasks,
+                                                    const double* __restrict__ panel,
+                                                    const int64_t* __restrict__ inv_off, double* linv) {
+  __shared__ double Ts[32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int s = tasks[blockIdx.x].x;
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int j0 = 32 * tasks[blockIdx.x].y;
+  const double* P = panel + S.panel_off[s];
+  double* X = linv + inv_off[s];  // plain (coherent) loads: this CTA reads what it wrote
+  const int c0 = 4 * w;           // this warp's 4 columns of the block
+  for (int i0 = j0 + 32; i0 < np; i0 += 32) {
+    const int nbi = min(32, np - i0);
+    const bool in = lane < nbi;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* Lr = P + i0 + lane;
+    for (int k = j0; k < i0; ++k) {
+      const double l = in ? Lr[(int64_t)k * f] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(l, X[(int64_t)(j0 + c0 + q) * np + k], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Ts[lane][c0 + q] = acc[q];
+    __syncthreads();
+    double o[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* Xi = X + (int64_t)i0 * np + i0 + lane;  // inv(L_ii)(lane, m) at Xi[m * np]
+    for (int m = 0; m < nbi; ++m) {
+      const double a = in ? Xi[(int64_t)m * np] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o[q] = fma(a, Ts[m][c0 + q], o[q]);
+    }
+    if (in) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (j0 + c0 + q < np) X[(int64_t)(j0 + c0 + q) * np + i0 + lane] = -o[q];
+    }
+    __syncthreads();
+  }
+}
+
+// forward: task (s, t) -> z rows [32t, 32t + 32) of supernode s
+__global__ void __launch_bounds__(256) k_inv_fwd(SymDev S, SolveDev T, const int2* __restrict__ tasks,
+                                                 const int64_t* __restrict__ inv_off,
+                                                 const double* __restrict__ linv,
+                                                 const double* __restrict__ D, const double* __restrict__ b,
+                                                 double* __restrict__ xp, const double* __restrict__ upd,
+                                                 double* __restrict__ cvec) {
+  extern __shared__ double y[];
+  __shared__ double part[8][32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int s = tasks[blockIdx.x].x;
+  const int np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const int r0 = 32 * tasks[blockIdx.x].y, r1 = min(np, r0 + 32);
+  for (int k = tid; k < r1; k += 256) y[k] = gather_row(S, T, s, k, np, col0, b, upd);
+  __syncthreads();
+  const int chunk = (r1 + 7) / 8;
+  const int k0 = w * chunk, k1 = min(r1, k0 + chunk);
+  const double* A = linv + inv_off[s] + r0 + lane;
+  double acc = 0.0;
+  if (r0 + lane < r1) {
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) acc = fma(A[(int64_t)k * np], y[k], acc);
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && r0 + lane < r1) {
+    double z = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) z += part[q][lane];
+    const int64_t g = col0 + r0 + lane;
+    xp[g] = z;
+    cvec[g] = z / D[g];  // backward right-hand side; COLDOT subtracts L21^T x2
+  }
+}
+
+// backward: warp per pivot row r, x1[r] = sum_{k>=r} inv(L11)(k, r) w[k], w in cvec
+__global__ void __launch_bounds__(256) k_inv_bwd(SymDev S, const int2* __restrict__ tasks,
+                                                 const int64_t* __restrict__ inv_off,
+                                                 const double* __restrict__ linv,
+                                                 const double* __restrict__ cvec, double* __restrict__ xp,
+                                                 double* __restrict__ x) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int s = tasks[blockIdx.x].x;
+  const int np = (int)S.ncol[s];
+  const int r = 8 * tasks[blockIdx.x].y + w;
+  if (r >= np) return;
+  const int64_t col0 = S.col0[s];
+  const double* A = linv + inv_off[s] + (int64_t)r * np;
+  const double* wv = cvec + col0;
+  double acc = 0.0;
+#pragma unroll 4
+  for (int k = r + lane; k < np; k += 32) acc = fma(A[k], wv[k], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    xp[col0 + r] = acc;
+    x[S.order[col0 + r]] = acc;
+  }
+}
+
 // L2 warm-up: bulk-prefetch the factor panels (contiguous) so the level
 // kernels' latency-bound loads hit L2 (the factor of a 2D config fits in the
 // 126 MB L2, but the Gram-Schmidt traffic of the previous step evicts it)
@@ -570,11 +719,28 @@ __global__ void k_prefetch_l2(const double* __restrict__ p, int64_t bytes) {
 // ---------------------------------------------------------------------------
 // host: per-level task lists, pull map
 // ---------------------------------------------------------------------------
+static int env_flag(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
 int build_solve_plan(riga_symbolic* sym) {
   const SymbolicHost& h = sym->h;
   SolvePlanHost& L = sym->sp;
   const int64_t ns = h.nsuper;
   L = SolvePlanHost();
+  // TMA staging of small panels (a 229 KB block per 8 warps) only pays for a
+  // solve running alone; concurrent slice streams want small blocks that
+  // co-reside, so it is opt-in (RIGA_WARP_STAGE=1), as is the per-solve L2
+  // prefetch of the factor (RIGA_L2_PREFETCH=1)
+  L.warp_stage = env_flag("RIGA_WARP_STAGE", 0);
+  L.l2_prefetch = env_flag("RIGA_L2_PREFETCH", 0);
+  // chain supernodes through inv(L11) (default) or the serial chain kernels
+  L.chain_inv = env_flag("RIGA_CHAIN_INV", 1);
+  L.inv_off.assign(ns, -1);
+  L.ifwd_ptr.assign(h.nlevels + 1, 0);
+  L.ibwd_ptr.assign(h.nlevels + 1, 0);
+  L.ifwd_smem.assign(h.nlevels, 8);
   auto large = [&](int64_t s) { return h.ncol[s] > kWholeMaxNp || h.front[s] > kWholeMaxF; };
   // bottom subtrees of small supernodes, at most kSubtreeMax nodes each;
   // supernodes are numbered in postorder, so a subtree is a contiguous range
@@ -621,6 +787,15 @@ int build_solve_plan(riga_symbolic* sym) {
       if (large(s)) {
         const int64_t np = h.ncol[s], nblk = (np + 31) / 32;
         L.chains.push_back(s);
+        L.inv_off[s] = L.inv_total;
+        L.inv_total += np * np;
+        for (int64_t t = 0; t < nblk; ++t) {
+          L.ifwd.push_back({s, (int32_t)t});
+          L.idiag.push_back({s, (int32_t)t});
+          if (t + 1 < nblk) L.icol.push_back({s, (int32_t)t});
+        }
+        for (int64_t g = 0; g < (np + 7) / 8; ++g) L.ibwd.push_back({s, (int32_t)g});
+        L.ifwd_smem[l] = std::max<int64_t>(L.ifwd_smem[l], np * 8);
         const int64_t want = np + chain_panel_doubles(np);
         const int64_t fit = want * 8 <= kChainSmemMax ? want : np;
         scf = std::max<int64_t>(scf, fit);
@@ -644,17 +819,26 @@ int build_solve_plan(riga_symbolic* sym) {
     }
     L.wholes.insert(L.wholes.end(), small.begin(), small.end());
     if (!small.empty()) {
-      smf = std::max<int64_t>(smf, kSolveWarps * kWarpSmem);
-      smb = std::max<int64_t>(smb, kSolveWarps * kWarpSmem);
+      const int64_t per = L.warp_stage ? kWarpSmem : kWholeMaxF;
+      smf = std::max<int64_t>(smf, kSolveWarps * per);
+      smb = std::max<int64_t>(smb, kSolveWarps * per);
     }
     L.fwd_ptr[l + 1] = (int64_t)L.fwd.size();
     L.bwd_ptr[l + 1] = (int64_t)L.bwd.size();
     L.chain_ptr[l + 1] = (int64_t)L.chains.size();
+    L.ifwd_ptr[l + 1] = (int64_t)L.ifwd.size();
+    L.ibwd_ptr[l + 1] = (int64_t)L.ibwd.size();
     L.fwd_smem[l] = smf * 8;
     L.bwd_smem[l] = smb * 8;
     L.chf_smem[l] = scf * 8;
     L.chb_smem[l] = scb * 8;
   }
+  // column-block inversion tasks: most work (leftmost blocks of the largest
+  // pivot blocks) first
+  std::stable_sort(L.icol.begin(), L.icol.end(), [&](const I2& a, const I2& b) {
+    const int64_t wa = (h.ncol[a.x] + 31) / 32 - a.y, wb = (h.ncol[b.x] + 31) / 32 - b.y;
+    return wa > wb;
+  });
   // pull map: front position -> sources in the update-vector buffer
   const int64_t nfront = h.rows_off[ns];
   std::vector<int64_t> cnt(nfront + 1, 0);
@@ -688,6 +872,13 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
     RIGA_TRY(sym->d_sub_ptr.upload(L.sub_ptr.data(), L.sub_ptr.size(), s));
   }
   RIGA_TRY(sym->d_gptr.upload(L.gptr.data(), L.gptr.size(), s));
+  if (L.chain_inv && L.inv_total) {
+    RIGA_TRY(sym->d_inv_off.upload(L.inv_off.data(), L.inv_off.size(), s));
+    RIGA_TRY(sym->d_ifwd.upload(L.ifwd.data(), L.ifwd.size(), s));
+    RIGA_TRY(sym->d_ibwd.upload(L.ibwd.data(), L.ibwd.size(), s));
+    RIGA_TRY(sym->d_idiag.upload(L.idiag.data(), L.idiag.size(), s));
+    if (!L.icol.empty()) RIGA_TRY(sym->d_icol.upload(L.icol.data(), L.icol.size(), s));
+  }
   if (L.gsrc.empty())
     RIGA_TRY(sym->d_gsrc.alloc(1, s));
   else
@@ -714,6 +905,7 @@ static int set_solve_attrs() {
   RIGA_TRY(raise_smem(k_rest_bwd, maxsm));
   RIGA_TRY(raise_smem(k_chain_fwd, maxsm));
   RIGA_TRY(raise_smem(k_chain_bwd, maxsm));
+  RIGA_TRY(raise_smem(k_inv_fwd, maxsm));
   RIGA_TRY(raise_smem(k_subtree_fwd, maxsm));
   RIGA_TRY(raise_smem(k_subtree_bwd, maxsm));
   done = true;
@@ -721,6 +913,25 @@ static int set_solve_attrs() {
 }
 
 int prepare_solve() { return set_solve_attrs(); }
+
+int build_chain_inverse(riga_factor* F, cudaStream_t st) {
+  riga_symbolic* sym = F->sym;
+  const SolvePlanHost& L = sym->sp;
+  if (!L.chain_inv || !L.inv_total) return RIGA_OK;
+  if (!F->linv.p) RIGA_TRY(F->linv.alloc(L.inv_total, st));
+  SymDev S = sym->dev();
+  const int nd = (int)L.idiag.size();
+  k_trinv_diag<<<(nd + 7) / 8, 256, 0, st>>>(S, reinterpret_cast<const int2*>(sym->d_idiag.p), nd, F->panel.p,
+                                             sym->d_inv_off.p, F->linv.p);
+  count_launch();
+  if (!L.icol.empty()) {
+    k_trinv_cols<<<(unsigned)L.icol.size(), 256, 0, st>>>(S, reinterpret_cast<const int2*>(sym->d_icol.p),
+                                                          F->panel.p, sym->d_inv_off.p, F->linv.p);
+    count_launch();
+  }
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
 
 int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bool b_permuted) {
   riga_symbolic* sym = F->sym;
@@ -734,7 +945,7 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   const int2* tf = reinterpret_cast<const int2*>(sym->d_tfwd.p);
   const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
   const int64_t pbytes = h.panel_total * 8;
-  if (pbytes <= kPrefetchMaxBytes) {
+  if (L.l2_prefetch && pbytes <= kPrefetchMaxBytes) {
     k_prefetch_l2<<<(unsigned)std::min<int64_t>(148, (pbytes / 32768 + 255) / 256 + 1), 256, 0, st>>>(F->panel.p,
                                                                                                    pbytes);
     count_launch();
@@ -747,7 +958,13 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   }
   for (int64_t l = 0; l < h.nlevels; ++l) {
     const int nc = (int)(L.chain_ptr[l + 1] - L.chain_ptr[l]);
-    if (nc) {
+    const int ni = (int)(L.ifwd_ptr[l + 1] - L.ifwd_ptr[l]);
+    if (L.chain_inv && ni) {
+      k_inv_fwd<<<ni, 256, L.ifwd_smem[l], st>>>(S, T, reinterpret_cast<const int2*>(sym->d_ifwd.p) + L.ifwd_ptr[l],
+                                                  sym->d_inv_off.p, F->linv.p, F->D.p, b, F->xperm.p, F->upd.p,
+                                                  F->cvec.p);
+      count_launch();
+    } else if (nc) {
       k_chain_fwd<<<nc, kSolveThreads, L.chf_smem[l], st>>>(S, T, sym->d_chains.p + L.chain_ptr[l],
                                                             (int)L.chf_smem[l], F->panel.p, b, F->xperm.p,
                                                             F->upd.p);
@@ -756,7 +973,7 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     const int nt = (int)(L.fwd_ptr[l + 1] - L.fwd_ptr[l]);
     if (nt) {
       k_rest_fwd<<<nt, kSolveThreads, L.fwd_smem[l], st>>>(S, T, tf + L.fwd_ptr[l], sym->d_wholes.p,
-                                                           F->panel.p, b, F->xperm.p, F->upd.p);
+                                                           F->panel.p, b, F->xperm.p, F->upd.p, L.warp_stage);
       count_launch();
     }
   }
@@ -764,11 +981,17 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     const int nt = (int)(L.bwd_ptr[l + 1] - L.bwd_ptr[l]);
     if (nt) {
       k_rest_bwd<<<nt, kSolveThreads, L.bwd_smem[l], st>>>(S, T, tb + L.bwd_ptr[l], sym->d_wholes.p,
-                                                           F->panel.p, F->D.p, F->xperm.p, F->cvec.p, x);
+                                                           F->panel.p, F->D.p, F->xperm.p, F->cvec.p, x, L.warp_stage,
+                                                           L.chain_inv);
       count_launch();
     }
     const int nc = (int)(L.chain_ptr[l + 1] - L.chain_ptr[l]);
-    if (nc) {
+    const int ni = (int)(L.ibwd_ptr[l + 1] - L.ibwd_ptr[l]);
+    if (L.chain_inv && ni) {
+      k_inv_bwd<<<ni, 256, 0, st>>>(S, reinterpret_cast<const int2*>(sym->d_ibwd.p) + L.ibwd_ptr[l],
+                                     sym->d_inv_off.p, F->linv.p, F->cvec.p, F->xperm.p, x);
+      count_launch();
+    } else if (nc) {
       k_chain_bwd<<<nc, kSolveThreads, L.chb_smem[l], st>>>(S, sym->d_chains.p + L.chain_ptr[l],
                                                             (int)L.chb_smem[l], F->panel.p, F->D.p,
                                                             F->xperm.p, F->cvec.p, x);

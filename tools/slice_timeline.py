@@ -12,7 +12,7 @@ lam_e, cnt = P.choose_lambda_e(s, c.n0)
 sh = P.uniform_shifts(lam_e, c.slices)
 perm = P.separator_ordering(s)
 sym = Symbolic.on_device(s.device, perm)
-for it in range(2):
+for it in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
     t0 = time.perf_counter()
     r = P.solve_uniform_slices(s, sh, streams=streams, pencil_symbolic=sym, perm=perm)
     print("total", round(time.perf_counter() - t0, 3), "boundary", round(r.timings["boundary_s"], 3),
