@@ -226,6 +226,150 @@ __device__ __forceinline__ void warp_whole_bwd(const SymDev& S, int s, const dou
 }
 
 // ---------------------------------------------------------------------------
+// small supernodes through G = [inv(L11); L21 inv(L11)] (f x np, ld f)
+//
+// Built once per factorisation (k_small_g), G turns a small supernode's
+// whole sweep into one dense mat-vec with no serial dependence:
+//     forward   z = G_top y1,  u = y2 - G_bot y1
+//     backward  x1 = G^T [z ./ d ; -x2]
+// G_top is lower triangular with explicit zeros above the diagonal.
+// ---------------------------------------------------------------------------
+struct GDev {
+  const double* g;        // all G blocks
+  const int64_t* g_off;   // per supernode offset (-1: large supernode)
+  int on;
+};
+
+// one CTA per small supernode (np <= 64): warp w owns columns w, w+8, ...;
+// lane owns rows lane, lane+32.  inv(L11) by column-oriented substitution
+// (x_k final at step k, broadcast by shuffle), then G_bot = L21 inv(L11).
+__global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __restrict__ nodes,
+                                                 const double* __restrict__ panel,
+                                                 const int64_t* __restrict__ g_off, double* __restrict__ gbuf) {
+  constexpr int LD = kWholeMaxNp + 1;
+  extern __shared__ double gsm[];
+  double* Ls = gsm;                     // L11 column-major, Ls[k * LD + r]
+  double* Xs = gsm + kWholeMaxNp * LD;  // inv(L11) column-major
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int s = nodes[blockIdx.x];
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const double* P = panel + S.panel_off[s];
+  double* G = gbuf + g_off[s];
+  for (int e = threadIdx.x; e < np * np; e += 256) {
+    const int k = e / np, r = e - k * np;
+    Ls[k * LD + r] = P[(int64_t)k * f + r];
+  }
+  __syncthreads();
+  double x[2][8];
+#pragma unroll
+  for (int ri = 0; ri < 2; ++ri)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[ri][j] = (lane + 32 * ri == w + 8 * j) ? 1.0 : 0.0;
+  for (int k = 0; k + 1 < np; ++k) {
+    const int kr = k >> 5, kl = k & 31;
+    const double l0 = lane > k && lane < np ? Ls[k * LD + lane] : 0.0;
+    const double l1 = lane + 32 > k && lane + 32 < np ? Ls[k * LD + lane + 32] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double xk = __shfl_sync(0xffffffffu, kr ? x[1][j] : x[0][j], kl);
+      x[0][j] = fma(-l0, xk, x[0][j]);
+      x[1][j] = fma(-l1, xk, x[1][j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int c = w + 8 * j;
+    if (c < np) {
+#pragma unroll
+      for (int ri = 0; ri < 2; ++ri) {
+        const int r = lane + 32 * ri;
+        if (r < np) {
+          Xs[c * LD + r] = x[ri][j];
+          G[(int64_t)c * f + r] = x[ri][j];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i0 = np; i0 < f; i0 += 32) {
+    const int i = i0 + lane;
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    for (int k = 0; k < np; ++k) {
+      const double l = i < f ? P[(int64_t)k * f + i] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = fma(l, w + 8 * j < np ? Xs[(w + 8 * j) * LD + k] : 0.0, acc[j]);
+    }
+    if (i < f) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (w + 8 * j < np) G[(int64_t)(w + 8 * j) * f + i] = acc[j];
+    }
+  }
+}
+
+__device__ __forceinline__ void warp_g_fwd(const SymDev& S, const SolveDev& T, const GDev& GD, int s,
+                                           const double* __restrict__ b, double* xp, double* upd, double* yw,
+                                           int lane) {
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const double* G = GD.g + GD.g_off[s];
+  for (int r = lane; r < f; r += 32) yw[r] = gather_row(S, T, s, r, np, col0, b, upd);
+  __syncwarp();
+  double* u = upd + S.upd_off[s] - np;
+  for (int i = lane; i < f; i += 32) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < np; ++k) acc = fma(G[k * f + i], yw[k], acc);
+    if (i < np)
+      xp[col0 + i] = acc;
+    else
+      u[i] = yw[i] - acc;
+  }
+}
+
+__device__ __forceinline__ void warp_g_bwd(const SymDev& S, const GDev& GD, int s, const double* __restrict__ D,
+                                           double* xp, double* x, double* yw, int lane) {
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const double* G = GD.g + GD.g_off[s];
+  const int32_t* rows = S.rows + S.rows_off[s];
+  for (int r = lane; r < f; r += 32) yw[r] = r < np ? xp[col0 + r] / D[col0 + r] : -xp[rows[r]];
+  __syncwarp();
+  // 8 columns at a time: every lane accumulates its rows, then a fold-reduce
+  // leaves column c0 + (lane & 7) summed over the warp in that lane
+  for (int c0 = 0; c0 < np; c0 += 8) {
+    double acc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+    for (int r = lane; r < f; r += 32) {
+      const double v = yw[r];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = fma(c0 + c < np ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
+    }
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) {
+#pragma unroll
+      for (int k = 0; k < o; ++k) {
+        const bool hi = (lane & o) != 0;
+        const double send = hi ? acc[k] : acc[k + o];
+        const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+        acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
+      }
+    }
+    double v = acc[0];
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    const int c = c0 + lane;
+    if (lane < 8 && c < np) {
+      xp[col0 + c] = v;
+      x[S.order[col0 + c]] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // bottom subtrees: one warp walks a whole subtree of small supernodes
 // (postorder forward, reverse postorder backward); the warp's own earlier
 // writes (update vectors, x) are visible to it after __syncwarp, so the
@@ -274,7 +418,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_fwd(SymDev S, SolveDe
                                                             const double* __restrict__ panel,
                                                             const double* __restrict__ b,
                                                             double* __restrict__ xp,
-                                                            double* __restrict__ upd, int stage) {
+                                                            double* __restrict__ upd, int stage, GDev GD) {
   extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
@@ -284,6 +428,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_fwd(SymDev S, SolveDe
   if (type == kWholeGroup) {
     // warp w: small supernode wholes[task.x + w], whole front in a warp slice
     if (w >= j) return;
+    if (GD.on) {
+      warp_g_fwd(S, T, GD, wholes[task.x + w], b, xp, upd, y + w * kWholeMaxF, lane);
+      return;
+    }
     if (stage && lane == 0) mbar_init(&wbar[w], 1);
     __syncwarp();
     warp_whole_fwd(S, T, wholes[task.x + w], panel, b, xp, upd, y + w * (stage ? kWarpSmem : kWholeMaxF), lane,
@@ -327,7 +475,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_bwd(SymDev S, SolveDe
                                                             const double* __restrict__ D,
                                                             double* __restrict__ xp,
                                                             double* __restrict__ cvec,
-                                                            double* __restrict__ x, int stage, int inv) {
+                                                            double* __restrict__ x, int stage, int inv, GDev GD) {
   extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
@@ -337,6 +485,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_bwd(SymDev S, SolveDe
   const int type = task.y >> 24, bj = task.y & 0x00ffffff;
   if (type == kWholeGroup) {
     if (w >= bj) return;
+    if (GD.on) {
+      warp_g_bwd(S, GD, wholes[task.x + w], D, xp, x, y + w * kWholeMaxF, lane);
+      return;
+    }
     if (stage && lane == 0) mbar_init(&wbar[w], 1);
     __syncwarp();
     warp_whole_bwd(S, wholes[task.x + w], panel, D, xp, x, y + w * (stage ? kWarpSmem : kWholeMaxF), lane,
@@ -737,6 +889,9 @@ int build_solve_plan(riga_symbolic* sym) {
   L.l2_prefetch = env_flag("RIGA_L2_PREFETCH", 0);
   // chain supernodes through inv(L11) (default) or the serial chain kernels
   L.chain_inv = env_flag("RIGA_CHAIN_INV", 1);
+  // small supernodes through G = [inv(L11); L21 inv(L11)] (default) or substitution
+  L.small_g = env_flag("RIGA_SMALL_G", 1);
+  L.g_off.assign(ns, -1);
   L.inv_off.assign(ns, -1);
   L.ifwd_ptr.assign(h.nlevels + 1, 0);
   L.ibwd_ptr.assign(h.nlevels + 1, 0);
@@ -808,6 +963,8 @@ int build_solve_plan(riga_symbolic* sym) {
         }
       } else {
         small.push_back(s);
+        L.g_off[s] = L.g_total;
+        L.g_total += h.front[s] * h.ncol[s];
       }
     }
     // small supernodes: groups of 8, one warp each
@@ -872,6 +1029,7 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
     RIGA_TRY(sym->d_sub_ptr.upload(L.sub_ptr.data(), L.sub_ptr.size(), s));
   }
   RIGA_TRY(sym->d_gptr.upload(L.gptr.data(), L.gptr.size(), s));
+  if (L.small_g && L.g_total) RIGA_TRY(sym->d_g_off.upload(L.g_off.data(), L.g_off.size(), s));
   if (L.chain_inv && L.inv_total) {
     RIGA_TRY(sym->d_inv_off.upload(L.inv_off.data(), L.inv_off.size(), s));
     RIGA_TRY(sym->d_ifwd.upload(L.ifwd.data(), L.ifwd.size(), s));
@@ -917,9 +1075,21 @@ int prepare_solve() { return set_solve_attrs(); }
 int build_chain_inverse(riga_factor* F, cudaStream_t st) {
   riga_symbolic* sym = F->sym;
   const SolvePlanHost& L = sym->sp;
+  SymDev S = sym->dev();
+  if (L.small_g && L.g_total) {
+    if (!F->gsmall.p) RIGA_TRY(F->gsmall.alloc(L.g_total, st));
+    const int nw = (int)L.wholes.size();
+    constexpr int smem = 2 * kWholeMaxNp * (kWholeMaxNp + 1) * 8;
+    static bool attr = false;
+    if (!attr) {
+      RIGA_CUDA(cudaFuncSetAttribute(k_small_g, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    k_small_g<<<nw, 256, smem, st>>>(S, sym->d_wholes.p, F->panel.p, sym->d_g_off.p, F->gsmall.p);
+    count_launch();
+  }
   if (!L.chain_inv || !L.inv_total) return RIGA_OK;
   if (!F->linv.p) RIGA_TRY(F->linv.alloc(L.inv_total, st));
-  SymDev S = sym->dev();
   const int nd = (int)L.idiag.size();
   k_trinv_diag<<<(nd + 7) / 8, 256, 0, st>>>(S, reinterpret_cast<const int2*>(sym->d_idiag.p), nd, F->panel.p,
                                              sym->d_inv_off.p, F->linv.p);
@@ -942,6 +1112,7 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   SymDev S = sym->dev();
   if (!F->cvec.p) RIGA_TRY(F->cvec.alloc(h.n, st));
   SolveDev T{sym->d_gptr.p, sym->d_gsrc.p, b_permuted ? 1 : 0};
+  const GDev GD{F->gsmall.p, sym->d_g_off.p, L.small_g && L.g_total ? 1 : 0};
   const int2* tf = reinterpret_cast<const int2*>(sym->d_tfwd.p);
   const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
   const int64_t pbytes = h.panel_total * 8;
@@ -973,7 +1144,7 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     const int nt = (int)(L.fwd_ptr[l + 1] - L.fwd_ptr[l]);
     if (nt) {
       k_rest_fwd<<<nt, kSolveThreads, L.fwd_smem[l], st>>>(S, T, tf + L.fwd_ptr[l], sym->d_wholes.p,
-                                                           F->panel.p, b, F->xperm.p, F->upd.p, L.warp_stage);
+                                                           F->panel.p, b, F->xperm.p, F->upd.p, L.warp_stage, GD);
       count_launch();
     }
   }
@@ -982,7 +1153,7 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     if (nt) {
       k_rest_bwd<<<nt, kSolveThreads, L.bwd_smem[l], st>>>(S, T, tb + L.bwd_ptr[l], sym->d_wholes.p,
                                                            F->panel.p, F->D.p, F->xperm.p, F->cvec.p, x, L.warp_stage,
-                                                           L.chain_inv);
+                                                           L.chain_inv, GD);
       count_launch();
     }
     const int nc = (int)(L.chain_ptr[l + 1] - L.chain_ptr[l]);
