@@ -43,6 +43,7 @@ struct SolvePlanHost {
   int warp_stage = 0, l2_prefetch = 0, chain_inv = 1, small_g = 1;
   int64_t g_total = 0;                 // doubles of G = [inv(L11); L21 inv(L11)] of the small supernodes
   std::vector<int64_t> g_off;          // per supernode offset into gsmall (-1: large)
+  std::vector<I2> gfwd, gbwd;          // G warp tasks: (supernode, row tile) / (supernode, column group)
   int64_t inv_total = 0;               // doubles of the inv(L11) blocks of the chain supernodes
   std::vector<int64_t> inv_off;        // per supernode offset into linv (-1: none)
   std::vector<I2> ifwd, ibwd, idiag, icol;  // (supernode, 32-row tile / 8-row group / 32-col block)
@@ -75,7 +76,7 @@ struct riga_symbolic {
   riga::DevBuf<I2> d_tfwd, d_tbwd;
   riga::DevBuf<int32_t> d_chains, d_wholes, d_gsrc, d_sub_ptr, d_sub_nodes;
   riga::DevBuf<int64_t> d_gptr, d_inv_off, d_g_off;
-  riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_icol;
+  riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_icol, d_gfwd, d_gbwd;
   SymDev dev() const {
     return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,
                   d_cb_off.p,   d_upd_off.p,   d_child_ptr.p,  d_asm_ptr.p,    d_sparent.p,

@@ -38,7 +38,7 @@ constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int64_t kChainSmemMax = 232448 - 4096;  // staged chain panels must fit this
 constexpr int64_t kPrefetchMaxBytes = 96ll << 20;  // prefetch the factor into L2 when it fits
 
-enum { kWholeGroup = 1, kUpd = 2, kColdot = 3 };
+enum { kWholeGroup = 1, kUpd = 2, kColdot = 3, kGTiles = 4 };
 
 struct SolveDev {
   const int64_t* gptr;  // pull map over front positions (rows_off indexing)
@@ -237,6 +237,7 @@ __device__ __forceinline__ void warp_whole_bwd(const SymDev& S, int s, const dou
 struct GDev {
   const double* g;        // all G blocks
   const int64_t* g_off;   // per supernode offset (-1: large supernode)
+  const int2* tiles;      // warp tasks: (supernode, 32-row tile) forward / (supernode, 8-column group) backward
   int on;
 };
 
@@ -369,6 +370,66 @@ __device__ __forceinline__ void warp_g_bwd(const SymDev& S, const GDev& GD, int 
   }
 }
 
+// warp task (s, t): rows [32 t, 32 t + 32) of [z; u] = [0; y2] + [1; -1] .* (G y1)
+__device__ __forceinline__ void warp_gtile_fwd(const SymDev& S, const SolveDev& T, const GDev& GD, int2 task,
+                                               const double* __restrict__ b, double* xp, double* upd, double* yw,
+                                               int lane) {
+  const int s = task.x;
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const double* G = GD.g + GD.g_off[s];
+  for (int r = lane; r < np; r += 32) yw[r] = gather_row(S, T, s, r, np, col0, b, upd);
+  const int i = 32 * task.y + lane;
+  const double yi = (i >= np && i < f) ? gather_row(S, T, s, i, np, col0, b, upd) : 0.0;
+  __syncwarp();
+  if (i >= f) return;
+  double acc = 0.0;
+  const double* Gi = G + i;
+#pragma unroll 8
+  for (int k = 0; k < np; ++k) acc = fma(Gi[k * f], yw[k], acc);
+  if (i < np)
+    xp[col0 + i] = acc;
+  else
+    upd[S.upd_off[s] + i - np] = yi - acc;
+}
+
+// warp task (s, g): x1 for columns [8 g, 8 g + 8) = G^T [z ./ d ; -x2]
+__device__ __forceinline__ void warp_gtile_bwd(const SymDev& S, const GDev& GD, int2 task,
+                                               const double* __restrict__ D, double* xp, double* x, int lane) {
+  const int s = task.x;
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const int c0 = 8 * task.y;
+  const double* G = GD.g + GD.g_off[s];
+  const int32_t* rows = S.rows + S.rows_off[s];
+  double acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+  for (int r = (c0 & ~31) + lane; r < f; r += 32) {  // G(r, c) = 0 above the diagonal
+    const double v = r < np ? xp[col0 + r] / D[col0 + r] : -xp[rows[r]];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = fma(c0 + c < np ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
+  }
+#pragma unroll
+  for (int o = 4; o >= 1; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const bool hi = (lane & o) != 0;
+      const double send = hi ? acc[k] : acc[k + o];
+      const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+      acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
+    }
+  }
+  double v = acc[0];
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 16);
+  const int c = c0 + lane;
+  if (lane < 8 && c < np) {
+    xp[col0 + c] = v;
+    x[S.order[col0 + c]] = v;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // bottom subtrees: one warp walks a whole subtree of small supernodes
 // (postorder forward, reverse postorder backward); the warp's own earlier
@@ -412,7 +473,8 @@ __global__ void __launch_bounds__(kSolveThreads) k_subtree_bwd(SymDev S,
 // ---------------------------------------------------------------------------
 // light kernels: WHOLE / UPD (forward), WHOLE / COLDOT (backward)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSolveThreads, 2) k_rest_fwd(SymDev S, SolveDev T,
+template <bool GT>
+__global__ void __launch_bounds__(kSolveThreads, GT ? 4 : 2) k_rest_fwd(SymDev S, SolveDev T,
                                                             const int2* __restrict__ tasks,
                                                             const int32_t* __restrict__ wholes,
                                                             const double* __restrict__ panel,
@@ -425,7 +487,12 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_fwd(SymDev S, SolveDe
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int2 task = tasks[blockIdx.x];
   const int type = task.y >> 24, j = task.y & 0x00ffffff;
-  if (type == kWholeGroup) {
+  if (GT && type == kGTiles) {
+    if (w >= j) return;
+    warp_gtile_fwd(S, T, GD, GD.tiles[task.x + w], b, xp, upd, y + w * kWholeMaxNp, lane);
+    return;
+  }
+  if (!GT && type == kWholeGroup) {
     // warp w: small supernode wholes[task.x + w], whole front in a warp slice
     if (w >= j) return;
     if (GD.on) {
@@ -468,7 +535,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_fwd(SymDev S, SolveDe
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 2) k_rest_bwd(SymDev S, SolveDev T,
+template <bool GT>
+__global__ void __launch_bounds__(kSolveThreads, GT ? 4 : 2) k_rest_bwd(SymDev S, SolveDev T,
                                                             const int2* __restrict__ tasks,
                                                             const int32_t* __restrict__ wholes,
                                                             const double* __restrict__ panel,
@@ -479,11 +547,15 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_bwd(SymDev S, SolveDe
   extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
-  double (*tile)[32][33] = reinterpret_cast<double (*)[32][33]>(y);  // COLDOT transposes
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int2 task = tasks[blockIdx.x];
   const int type = task.y >> 24, bj = task.y & 0x00ffffff;
-  if (type == kWholeGroup) {
+  if (GT && type == kGTiles) {
+    if (w >= bj) return;
+    warp_gtile_bwd(S, GD, GD.tiles[task.x + w], D, xp, x, lane);
+    return;
+  }
+  if (!GT && type == kWholeGroup) {
     if (w >= bj) return;
     if (GD.on) {
       warp_g_bwd(S, GD, wholes[task.x + w], D, xp, x, y + w * kWholeMaxF, lane);
@@ -500,32 +572,40 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_rest_bwd(SymDev S, SolveDe
   const double* P = panel + S.panel_off[s];
   const int32_t* rows = S.rows + S.rows_off[s];
   {
-    // kColdot: c[col] = sum_{update rows r} L[r][col] x[rows[r]], col in block bj
-    const int64_t c0 = 32 * (int64_t)bj;
-    const int nc = (int)imin(32, np - c0);
-    const int nbu = (int)((f - np + 31) / 32);
-    double acc = 0.0;
-    for (int q = w; q < nbu; q += kSolveWarps) {
-      const int64_t r0 = np + 32 * (int64_t)q, r1 = imin(r0 + 32, f), r = r0 + lane;
-      const double xv = r < r1 ? xp[rows[r]] : 0.0;
-#pragma unroll 8
-      for (int k = 0; k < 32; ++k) tile[w][k][lane] = (r < r1 && k < nc) ? P[(c0 + k) * f + r] : 0.0;
-      __syncwarp();
-      double a2 = 0.0;
-#pragma unroll 8
-      for (int rr = 0; rr < 32; ++rr) a2 = fma(tile[w][lane][rr], __shfl_sync(0xffffffffu, xv, rr), a2);
-      acc += lane < nc ? a2 : 0.0;
-      __syncwarp();
+    // kColdot: c[col] = sum_{update rows r} L[r][col] x[rows[r]], col in block bj;
+    // warp w: 8-column group (w & 3) over every other 32-row strip (w >> 2),
+    // fold-reduced across lanes, then the two row halves summed in order
+    const int64_t c0 = 32 * (int64_t)bj + 8 * (w & 3);
+    double acc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+    for (int64_t r = np + 32 * (w >> 2) + lane; r < f; r += 64) {
+      const double xv = xp[rows[r]];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = fma(c0 + c < np ? P[(c0 + c) * f + r] : 0.0, xv, acc[c]);
     }
-    part[w][lane] = acc;
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) {
+#pragma unroll
+      for (int k = 0; k < o; ++k) {
+        const bool hi = (lane & o) != 0;
+        const double send = hi ? acc[k] : acc[k + o];
+        const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+        acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
+      }
+    }
+    double v = acc[0];
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    if (lane < 8) part[w][lane] = v;
     __syncthreads();
     if (w == 0) {
-      double v = 0.0;
-#pragma unroll
-      for (int q = 0; q < kSolveWarps; ++q) v += part[q][lane];
-      if (lane < nc) {
-        double* c = cvec + col0 + c0 + lane;
-        *c = inv ? *c - v : v;  // inverse path: cvec already holds z ./ d
+      const int g = lane >> 3, e = lane & 7;
+      const int64_t col = 32 * (int64_t)bj + lane;
+      if (col < np) {
+        const double t = part[g][e] + part[g + 4][e];
+        double* c = cvec + col0 + col;
+        *c = inv ? *c - t : t;  // inverse path: cvec already holds z ./ d
       }
     }
   }
@@ -959,7 +1039,6 @@ int build_solve_plan(riga_symbolic* sym) {
         for (int64_t u = 0; u < nbu; ++u) L.fwd.push_back({s, code(kUpd, (int)u)});
         if (nbu > 0) {
           for (int64_t bb = 0; bb < nblk; ++bb) L.bwd.push_back({s, code(kColdot, (int)bb)});
-          smb = std::max<int64_t>(smb, kSolveWarps * 32 * 33);
         }
       } else {
         small.push_back(s);
@@ -967,16 +1046,36 @@ int build_solve_plan(riga_symbolic* sym) {
         L.g_total += h.front[s] * h.ncol[s];
       }
     }
-    // small supernodes: groups of 8, one warp each
-    for (size_t q = 0; q < small.size(); q += kSolveWarps) {
-      const int cnt = (int)std::min<size_t>(kSolveWarps, small.size() - q);
-      const int32_t first = (int32_t)L.wholes.size() + (int32_t)q;
-      L.fwd.push_back({first, code(kWholeGroup, cnt)});
-      L.bwd.push_back({first, code(kWholeGroup, cnt)});
+    if (L.small_g) {
+      // small supernodes through G: warp tasks (32-row tiles forward,
+      // 8-column groups backward), 8 per CTA
+      std::vector<I2> tf, tb;
+      for (int32_t s : small) {
+        for (int32_t t = 0; t < (int32_t)((h.front[s] + 31) / 32); ++t) tf.push_back({s, t});
+        for (int32_t g = 0; g < (int32_t)((h.ncol[s] + 7) / 8); ++g) tb.push_back({s, g});
+      }
+      for (size_t q = 0; q < tf.size(); q += kSolveWarps) {
+        const int cnt = (int)std::min<size_t>(kSolveWarps, tf.size() - q);
+        L.fwd.push_back({(int32_t)(L.gfwd.size() + q), code(kGTiles, cnt)});
+      }
+      for (size_t q = 0; q < tb.size(); q += kSolveWarps) {
+        const int cnt = (int)std::min<size_t>(kSolveWarps, tb.size() - q);
+        L.bwd.push_back({(int32_t)(L.gbwd.size() + q), code(kGTiles, cnt)});
+      }
+      L.gfwd.insert(L.gfwd.end(), tf.begin(), tf.end());
+      L.gbwd.insert(L.gbwd.end(), tb.begin(), tb.end());
+    } else {
+      // small supernodes: groups of 8, one warp each
+      for (size_t q = 0; q < small.size(); q += kSolveWarps) {
+        const int cnt = (int)std::min<size_t>(kSolveWarps, small.size() - q);
+        const int32_t first = (int32_t)L.wholes.size() + (int32_t)q;
+        L.fwd.push_back({first, code(kWholeGroup, cnt)});
+        L.bwd.push_back({first, code(kWholeGroup, cnt)});
+      }
     }
     L.wholes.insert(L.wholes.end(), small.begin(), small.end());
     if (!small.empty()) {
-      const int64_t per = L.warp_stage ? kWarpSmem : kWholeMaxF;
+      const int64_t per = L.small_g ? kWholeMaxNp : L.warp_stage ? kWarpSmem : kWholeMaxF;
       smf = std::max<int64_t>(smf, kSolveWarps * per);
       smb = std::max<int64_t>(smb, kSolveWarps * per);
     }
@@ -1029,7 +1128,11 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
     RIGA_TRY(sym->d_sub_ptr.upload(L.sub_ptr.data(), L.sub_ptr.size(), s));
   }
   RIGA_TRY(sym->d_gptr.upload(L.gptr.data(), L.gptr.size(), s));
-  if (L.small_g && L.g_total) RIGA_TRY(sym->d_g_off.upload(L.g_off.data(), L.g_off.size(), s));
+  if (L.small_g && L.g_total) {
+    RIGA_TRY(sym->d_g_off.upload(L.g_off.data(), L.g_off.size(), s));
+    RIGA_TRY(sym->d_gfwd.upload(L.gfwd.data(), L.gfwd.size(), s));
+    RIGA_TRY(sym->d_gbwd.upload(L.gbwd.data(), L.gbwd.size(), s));
+  }
   if (L.chain_inv && L.inv_total) {
     RIGA_TRY(sym->d_inv_off.upload(L.inv_off.data(), L.inv_off.size(), s));
     RIGA_TRY(sym->d_ifwd.upload(L.ifwd.data(), L.ifwd.size(), s));
@@ -1059,8 +1162,10 @@ static int set_solve_attrs() {
   int dev = 0, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  RIGA_TRY(raise_smem(k_rest_fwd, maxsm));
-  RIGA_TRY(raise_smem(k_rest_bwd, maxsm));
+  RIGA_TRY(raise_smem(k_rest_fwd<false>, maxsm));
+  RIGA_TRY(raise_smem(k_rest_bwd<false>, maxsm));
+  RIGA_TRY(raise_smem(k_rest_fwd<true>, maxsm));
+  RIGA_TRY(raise_smem(k_rest_bwd<true>, maxsm));
   RIGA_TRY(raise_smem(k_chain_fwd, maxsm));
   RIGA_TRY(raise_smem(k_chain_bwd, maxsm));
   RIGA_TRY(raise_smem(k_inv_fwd, maxsm));
@@ -1112,7 +1217,9 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   SymDev S = sym->dev();
   if (!F->cvec.p) RIGA_TRY(F->cvec.alloc(h.n, st));
   SolveDev T{sym->d_gptr.p, sym->d_gsrc.p, b_permuted ? 1 : 0};
-  const GDev GD{F->gsmall.p, sym->d_g_off.p, L.small_g && L.g_total ? 1 : 0};
+  const int gon = L.small_g && L.g_total ? 1 : 0;
+  const GDev GDf{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gfwd.p), gon};
+  const GDev GDb{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gbwd.p), gon};
   const int2* tf = reinterpret_cast<const int2*>(sym->d_tfwd.p);
   const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
   const int64_t pbytes = h.panel_total * 8;
@@ -1143,17 +1250,17 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     }
     const int nt = (int)(L.fwd_ptr[l + 1] - L.fwd_ptr[l]);
     if (nt) {
-      k_rest_fwd<<<nt, kSolveThreads, L.fwd_smem[l], st>>>(S, T, tf + L.fwd_ptr[l], sym->d_wholes.p,
-                                                           F->panel.p, b, F->xperm.p, F->upd.p, L.warp_stage, GD);
+      (gon ? k_rest_fwd<true> : k_rest_fwd<false>)<<<nt, kSolveThreads, L.fwd_smem[l], st>>>(S, T, tf + L.fwd_ptr[l], sym->d_wholes.p,
+                                                           F->panel.p, b, F->xperm.p, F->upd.p, L.warp_stage, GDf);
       count_launch();
     }
   }
   for (int64_t l = h.nlevels - 1; l >= 0; --l) {
     const int nt = (int)(L.bwd_ptr[l + 1] - L.bwd_ptr[l]);
     if (nt) {
-      k_rest_bwd<<<nt, kSolveThreads, L.bwd_smem[l], st>>>(S, T, tb + L.bwd_ptr[l], sym->d_wholes.p,
+      (gon ? k_rest_bwd<true> : k_rest_bwd<false>)<<<nt, kSolveThreads, L.bwd_smem[l], st>>>(S, T, tb + L.bwd_ptr[l], sym->d_wholes.p,
                                                            F->panel.p, F->D.p, F->xperm.p, F->cvec.p, x, L.warp_stage,
-                                                           L.chain_inv, GD);
+                                                           L.chain_inv, GDb);
       count_launch();
     }
     const int nc = (int)(L.chain_ptr[l + 1] - L.chain_ptr[l]);
