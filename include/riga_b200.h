@@ -52,6 +52,10 @@ const char* riga_last_error(void);
 int riga_version(void);
 /* Number of CUDA devices visible (0 on a CPU-only host). */
 int riga_device_count(int* count);
+/* Stream-ordered pool of `device` (where every engine buffer lives):
+ * out[0] reserved bytes, out[1] reserved high-water, out[2] used bytes,
+ * out[3] used high-water.  reset_high != 0 resets both high-water marks. */
+int riga_mem_info(int device, int reset_high, int64_t* out4);
 /* Context = (device, stream).  stream_handle: 0 -> create a private
  * non-blocking stream; otherwise a cudaStream_t owned by the caller. */
 int riga_ctx_create(int device, void* stream_handle, riga_ctx** out);

@@ -28,6 +28,7 @@ _pp = ctypes.POINTER(ctypes.c_void_p)
 SIGNATURES = {
     "riga_version": [],
     "riga_device_count": [_p],
+    "riga_mem_info": [ctypes.c_int, ctypes.c_int, _p],
     "riga_ctx_create": [_i32, _p, _p],
     "riga_ctx_destroy": [_p],
     "riga_ctx_synchronize": [_p],

@@ -1,6 +1,7 @@
 // Shared internals of libriga_b200.so (host + device).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -88,6 +89,7 @@ struct DevBuf {
 }  // namespace riga
 
 struct riga_ctx {
+  std::atomic<int> refs{1};  // riga_ctx_destroy + every object created on it
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -109,3 +111,27 @@ struct DeviceGuard {
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
   }
 };
+
+namespace riga {
+// Objects keep their context (and so the stream their buffers are freed on)
+// alive: declared as the FIRST member of an object, it is destroyed last,
+// after every DevBuf of the object has been released on the stream.
+void ctx_release(riga_ctx* c);
+struct CtxRef {
+  riga_ctx* c = nullptr;
+  CtxRef() = default;
+  CtxRef(const CtxRef&) = delete;
+  CtxRef& operator=(const CtxRef&) = delete;
+  void set(riga_ctx* x) {
+    if (x == c) return;
+    if (x) x->refs.fetch_add(1);
+    ctx_release(c);
+    c = x;
+  }
+  ~CtxRef() { ctx_release(c); }
+};
+// Process-wide cache of pinned host blocks: cudaMallocHost / cudaFreeHost
+// synchronise the device, so blocks are recycled instead of freed.
+void* pinned_get(size_t bytes);
+void pinned_put(void* p);
+}  // namespace riga

@@ -520,6 +520,7 @@ int riga_symbolic_create(riga_system* sys, const int64_t* perm, riga_symbolic** 
   RIGA_TRY(riga_system_download(sys, rp.data(), ci.data(), nullptr, nullptr));
   auto sym = std::make_unique<riga_symbolic>();
   sym->ctx = sys->ctx;
+  sym->ctxref.set(sys->ctx);
   sym->sys = sys;
   std::string err;
   if (analyze(sys->n, rp.data(), ci.data(), perm, sym->h, err)) {
@@ -594,6 +595,7 @@ int riga_factor_create(riga_ctx* ctx, riga_symbolic* sym, double sigma, double r
   const SymbolicHost& h = sym->h;
   auto F = std::make_unique<riga_factor>();
   F->ctx = ctx;
+  F->ctxref.set(ctx);
   F->sym = sym;
   F->sigma = sigma;
   RIGA_TRY(F->panel.alloc(std::max<int64_t>(h.panel_total, 1), st));
@@ -602,6 +604,7 @@ int riga_factor_create(riga_ctx* ctx, riga_symbolic* sym, double sigma, double r
   RIGA_TRY(F->upd.alloc(std::max<int64_t>(h.upd_total, 1), st));
   RIGA_TRY(F->stat.alloc(2, st));
   RIGA_TRY(F->tol.alloc(2, st));
+  RIGA_TRY(F->cvec.alloc(h.n, st));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

@@ -7,6 +7,7 @@
 #include "symbolic.h"
 
 struct riga_system {
+  riga::CtxRef ctxref;
   riga_ctx* ctx = nullptr;
   int64_t n = 0, nnz = 0;
   riga::DevBuf<int64_t> rowptr;
@@ -59,6 +60,7 @@ struct SolvePlanHost {
 };
 
 struct riga_symbolic {
+  riga::CtxRef ctxref;
   riga_ctx* ctx = nullptr;
   riga_system* sys = nullptr;  // may be null (host-only analysis)
   riga::SymbolicHost h;
@@ -86,6 +88,7 @@ struct riga_symbolic {
 };
 
 struct riga_factor {
+  riga::CtxRef ctxref;
   riga_ctx* ctx = nullptr;
   riga_symbolic* sym = nullptr;
   double sigma = 0.0;

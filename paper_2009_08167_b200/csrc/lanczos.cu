@@ -499,6 +499,7 @@ __global__ void k_rowscale(double* __restrict__ X, double* __restrict__ MX, int6
 using namespace riga;
 
 struct riga_lanczos {
+  riga::CtxRef ctxref;
   riga_ctx* ctx = nullptr;
   riga_system* sys = nullptr;
   riga_factor* op = nullptr;
@@ -520,6 +521,8 @@ struct riga_lanczos {
   ~riga_lanczos() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (capst) cudaStreamDestroy(capst);
+    if (hbuf) riga::pinned_put(hbuf);
+    if (hst) riga::pinned_put(hst);
   }
 };
 
@@ -662,18 +665,17 @@ int ensure_graph(riga_lanczos* lz) {
   cudaStream_t s = lz->ctx->stream;
   // first-use allocations and kernel attributes must happen outside the capture
   riga_factor* F = lz->op;
-  if (!F->cvec.p) RIGA_TRY(F->cvec.alloc(F->sym->h.n, s));
   RIGA_TRY(prepare_solve());
   RIGA_CUDA(cudaStreamSynchronize(s));
   cudaGraph_t g = nullptr;
   if (!lz->capst) RIGA_CUDA(cudaStreamCreateWithFlags(&lz->capst, cudaStreamNonBlocking));
-  const long long n0 = g_launches.load();
+  const long long n0 = t_launches;
   RIGA_CUDA(cudaStreamBeginCapture(lz->capst, cudaStreamCaptureModeThreadLocal));
   lz->cur = lz->capst;
   const int rc = step_full(lz);
   lz->cur = lz->ctx->stream;
   cudaError_t e = cudaStreamEndCapture(lz->capst, &g);
-  lz->gnodes = g_launches.load() - n0;
+  lz->gnodes = t_launches - n0;
   g_launches.fetch_sub(lz->gnodes);  // captured, not launched
   if (rc) {
     if (g) cudaGraphDestroy(g);
@@ -702,6 +704,7 @@ int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max
   DeviceGuard g(ctx->device);
   auto lz = std::make_unique<riga_lanczos>();
   lz->ctx = ctx;
+  lz->ctxref.set(ctx);
   lz->cur = ctx->stream;
   lz->sys = mass;
   lz->n = n;
@@ -726,8 +729,12 @@ int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max
   RIGA_TRY(lz->st.alloc(1, cs));
   RIGA_CUDA(cudaMemsetAsync(lz->st.p, 0, sizeof(LzDev), cs));
   RIGA_TRY(grow_locked(lz.get(), 16));
-  RIGA_CUDA(cudaMallocHost(&lz->hst, sizeof(LzDev)));
-  RIGA_CUDA(cudaMallocHost(&lz->hbuf, std::max<int64_t>(64, 3 * rows + 8) * 8));
+  lz->hst = static_cast<LzDev*>(pinned_get(sizeof(LzDev)));
+  lz->hbuf = static_cast<double*>(pinned_get(std::max<int64_t>(64, 3 * rows + 8) * 8));
+  if (!lz->hst || !lz->hbuf) {
+    set_error("pinned host allocation failed");
+    return RIGA_OOM;
+  }
   RIGA_CUDA(cudaStreamSynchronize(cs));
   *out = lz.release();
   return RIGA_OK;
@@ -737,8 +744,6 @@ int riga_lanczos_destroy(riga_lanczos* lz) {
   if (!lz) return RIGA_OK;
   DeviceGuard g(lz->ctx->device);
   cudaStreamSynchronize(lz->ctx->stream);
-  if (lz->hbuf) cudaFreeHost(lz->hbuf);
-  if (lz->hst) cudaFreeHost(lz->hst);
   delete lz;
   return RIGA_OK;
 }

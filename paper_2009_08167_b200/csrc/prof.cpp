@@ -8,6 +8,7 @@
 namespace riga {
 
 std::atomic<long long> g_launches{0};
+thread_local long long t_launches = 0;
 
 namespace {
 struct Rec {

@@ -20,7 +20,13 @@ enum ProfCat {
 };
 
 extern std::atomic<long long> g_launches;
-inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// launches issued by this thread (graph capture is thread-local, so the
+// kernels a capture recorded are this counter's difference across it)
+extern thread_local long long t_launches;
+inline void count_launch(int n = 1) {
+  g_launches.fetch_add(n, std::memory_order_relaxed);
+  t_launches += n;
+}
 
 struct ProfScope {
   int cat;

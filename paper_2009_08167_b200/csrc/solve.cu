@@ -1215,7 +1215,6 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   ProfScope prof(kProfSolve, st, 16.0 * h.fill_nnz + 32.0 * h.n);
   RIGA_TRY(set_solve_attrs());
   SymDev S = sym->dev();
-  if (!F->cvec.p) RIGA_TRY(F->cvec.alloc(h.n, st));
   SolveDev T{sym->d_gptr.p, sym->d_gsrc.p, b_permuted ? 1 : 0};
   const int gon = L.small_g && L.g_total ? 1 : 0;
   const GDev GDf{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gfwd.p), gon};

@@ -2,6 +2,9 @@
 //
 //  riga_system_assemble_kron  <- kron_assemble   ref assembly.py:139-186
 //  riga_spmv / riga_csr_spmv  <- mass_matvec     ref sparsela.py:280-290
+#include <map>
+#include <mutex>
+#include <unordered_map>
 #include <cstring>
 #include <mutex>
 
@@ -215,6 +218,52 @@ int launch_dot(cudaStream_t s, int64_t n, const double* x, const double* y, doub
   return RIGA_OK;
 }
 
+// ---- context lifetime / pinned host cache --------------------------------
+void ctx_release(riga_ctx* c) {
+  if (!c) return;
+  if (c->refs.fetch_sub(1) != 1) return;
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);  // this stream only: pending reads into scratch_host
+  if (c->scratch_dev) cudaFreeAsync(c->scratch_dev, c->stream);
+  if (c->scratch_host) pinned_put(c->scratch_host);
+  if (c->own_stream) cudaStreamDestroy(c->stream);  // released once its work drains
+  delete c;
+}
+
+namespace {
+std::mutex g_pin_mu;
+std::multimap<size_t, void*> g_pin_free;
+std::unordered_map<void*, size_t> g_pin_size;
+}  // namespace
+
+void* pinned_get(size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_free.lower_bound(bytes);
+    if (it != g_pin_free.end() && it->first <= 2 * bytes) {
+      void* p = it->second;
+      g_pin_free.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_size[p] = bytes;
+  return p;
+}
+
+void pinned_put(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  auto it = g_pin_size.find(p);
+  if (it != g_pin_size.end()) g_pin_free.emplace(it->second, p);
+}
+
 }  // namespace riga
 
 using namespace riga;
@@ -236,6 +285,26 @@ int riga_device_count(int* count) {
     c = 0;
   }
   *count = c;
+  return RIGA_OK;
+}
+
+int riga_mem_info(int device, int reset_high, int64_t* out4) {
+  RIGA_CHECK_ARG(out4, "null out");
+  DeviceGuard g(device);
+  cudaMemPool_t pool;
+  RIGA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  const cudaMemPoolAttr attrs[4] = {cudaMemPoolAttrReservedMemCurrent, cudaMemPoolAttrReservedMemHigh,
+                                    cudaMemPoolAttrUsedMemCurrent, cudaMemPoolAttrUsedMemHigh};
+  for (int i = 0; i < 4; ++i) {
+    uint64_t v = 0;
+    RIGA_CUDA(cudaMemPoolGetAttribute(pool, attrs[i], &v));
+    out4[i] = (int64_t)v;
+  }
+  if (reset_high) {
+    uint64_t z = 0;
+    RIGA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &z));
+    RIGA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &z));
+  }
   return RIGA_OK;
 }
 
@@ -270,10 +339,13 @@ int riga_ctx_create(int device, void* stream_handle, riga_ctx** out) {
     }
     ctx->own_stream = true;
   }
-  cudaError_t e = cudaMallocHost(&ctx->scratch_host, 4096 * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&ctx->scratch_dev, kDotScratch * 4 * sizeof(double));
+  ctx->scratch_host = static_cast<double*>(pinned_get(4096 * sizeof(double)));
+  cudaError_t e = ctx->scratch_host ? cudaSuccess : cudaErrorMemoryAllocation;
+  if (e == cudaSuccess)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&ctx->scratch_dev), kDotScratch * 4 * sizeof(double), ctx->stream);
   if (e != cudaSuccess) {
     set_error(std::string("ctx scratch: ") + cudaGetErrorString(e));
+    ctx_release(ctx);
     return RIGA_CUDA_ERROR;
   }
   cudaMemsetAsync(ctx->scratch_dev, 0, kDotScratch * 4 * sizeof(double), ctx->stream);
@@ -283,13 +355,7 @@ int riga_ctx_create(int device, void* stream_handle, riga_ctx** out) {
 }
 
 int riga_ctx_destroy(riga_ctx* ctx) {
-  if (!ctx) return RIGA_OK;
-  DeviceGuard g(ctx->device);
-  cudaStreamSynchronize(ctx->stream);
-  if (ctx->scratch_host) cudaFreeHost(ctx->scratch_host);
-  if (ctx->scratch_dev) cudaFree(ctx->scratch_dev);
-  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
-  delete ctx;
+  ctx_release(ctx);
   return RIGA_OK;
 }
 
@@ -315,6 +381,7 @@ int riga_system_upload(riga_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row
   DeviceGuard g(ctx->device);
   auto sys = std::make_unique<riga_system>();
   sys->ctx = ctx;
+  sys->ctxref.set(ctx);
   sys->n = n;
   sys->nnz = nnz;
   RIGA_TRY(sys->rowptr.upload(rowptr, n + 1, ctx->stream));
@@ -353,6 +420,7 @@ int riga_system_assemble_kron(riga_ctx* ctx, int dim, const int64_t* n1,
   RIGA_CHECK_ARG(nnz < (int64_t(1) << 31), "nnz must fit int32 slots");
   auto sys = std::make_unique<riga_system>();
   sys->ctx = ctx;
+  sys->ctxref.set(ctx);
   sys->n = n;
   sys->nnz = nnz;
   RIGA_TRY(sys->rowptr.alloc(n + 1, s));

@@ -76,6 +76,24 @@ def current() -> Context:
         return _default[dev]
 
 
+class Owned:
+    """Owner of one engine handle, destroyed with it.  Zero-copy tensors of
+    engine memory reference this (not the Python object that created it), so
+    no reference cycle runs through a tensor -- torch holds its data owner
+    in C++, out of reach of the cycle collector."""
+
+    def __init__(self, handle, destroy: str):
+        self.handle, self._destroy = handle, destroy
+
+    def __del__(self):
+        try:
+            if self.handle:
+                getattr(_lib.lib(), self._destroy)(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 class _CAI:
     """__cuda_array_interface__ exporter for engine-owned memory."""
 
@@ -104,3 +122,10 @@ def to_device(x, ctx: Context | None = None) -> torch.Tensor:
 
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.detach().to("cpu").numpy()
+
+
+def mem_info(device: int = 0, reset_high: bool = False) -> dict:
+    """Engine memory pool (stream-ordered allocations) of `device`, bytes."""
+    out = np.zeros(4, dtype=np.int64)
+    _lib.check(_lib.lib().riga_mem_info(int(device), int(bool(reset_high)), _lib.ptr(out)))
+    return {"reserved": int(out[0]), "reserved_high": int(out[1]), "used": int(out[2]), "used_high": int(out[3])}

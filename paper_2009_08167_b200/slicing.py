@@ -89,6 +89,46 @@ class SlicesResult:
     factor_ms: list = field(default_factory=list)
 
 
+_ctx_free: dict = {}
+_ctx_lock = threading.Lock()
+
+
+def _take_ctx(device: int):
+    """A slice-worker context (own stream) from a per-device free list:
+    streams are reused across calls, so torch's per-stream block cache and
+    the engine pool do not fragment over many calls."""
+    with _ctx_lock:
+        lst = _ctx_free.setdefault(device, [])
+        if lst:
+            return lst.pop()
+    return _dev.Context(device)
+
+
+def _give_ctx(ctx) -> None:
+    ctx.synchronize()
+    with _ctx_lock:
+        _ctx_free.setdefault(ctx.device, []).append(ctx)
+
+
+class _blas_threads:
+    """Limit the BLAS/OpenMP pools for the duration of a block (None: no-op)."""
+
+    def __init__(self, n):
+        self.n, self.ctl = n, None
+
+    def __enter__(self):
+        if self.n is not None:
+            from threadpoolctl import threadpool_limits
+
+            self.ctl = threadpool_limits(limits=self.n)
+        return self
+
+    def __exit__(self, *exc):
+        if self.ctl is not None:
+            self.ctl.restore_original_limits()
+        return False
+
+
 def _allgather(obj, group_world):
     if group_world <= 1:
         return [obj]
@@ -158,7 +198,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     queue = sorted(my, key=lambda k: -expected[k])
 
     def worker(widx):
-        ctx = _dev.Context(base_ctx.device)
+        ctx = _take_ctx(base_ctx.device)
         cnt = CostCounters()
         with ctx:
             while True:
@@ -201,14 +241,18 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                         errors.append((k, e))
         with lock:
             counters.merge(cnt)
+        _give_ctx(ctx)
 
     t0 = time.perf_counter()
     nthreads = max(1, min(streams, len(my)))
     threads = [threading.Thread(target=worker, args=(i,)) for i in range(nthreads)]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
+    # the host side of each slice (Rayleigh-Ritz eigh, small dense algebra)
+    # runs in its own thread: one BLAS thread each, not nthreads x cores
+    with _blas_threads(1 if nthreads > 1 else None):
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
     if errors:
         k, e = errors[0]
         raise RuntimeError(f"slice {k} failed on rank {rank}: {e}") from e
