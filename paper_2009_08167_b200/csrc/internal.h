@@ -52,7 +52,9 @@ struct SolvePlanHost {
   std::vector<I2> fwd, bwd;        // light tasks grouped by level
   std::vector<int32_t> chains;     // large supernodes grouped by level
   std::vector<int32_t> wholes;     // small supernodes (warp tasks) grouped by level
-  std::vector<int32_t> sub_ptr, sub_nodes;  // bottom subtrees (postorder ranges), one per warp
+  int sub_levels = 0, nsub = 0;        // bottom subtrees: height bound, count
+  std::vector<int32_t> sub_fptr, sub_bptr;  // per subtree (sub_levels + 1) local-level task bounds
+  std::vector<I2> sub_ftiles, sub_btiles;   // their G warp tasks (row tiles / column groups)
   std::vector<int64_t> fwd_ptr, bwd_ptr, chain_ptr;
   std::vector<int64_t> fwd_smem, bwd_smem, chf_smem, chb_smem;  // bytes per level launch
   std::vector<int32_t> gsrc;
@@ -76,9 +78,9 @@ struct riga_symbolic {
   int64_t n_large = 0;
   SolvePlanHost sp;
   riga::DevBuf<I2> d_tfwd, d_tbwd;
-  riga::DevBuf<int32_t> d_chains, d_wholes, d_gsrc, d_sub_ptr, d_sub_nodes;
+  riga::DevBuf<int32_t> d_chains, d_wholes, d_gsrc, d_sub_fptr, d_sub_bptr;
   riga::DevBuf<int64_t> d_gptr, d_inv_off, d_g_off;
-  riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_icol, d_gfwd, d_gbwd;
+  riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_icol, d_gfwd, d_gbwd, d_sub_ftiles, d_sub_btiles;
   SymDev dev() const {
     return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,
                   d_cb_off.p,   d_upd_off.p,   d_child_ptr.p,  d_asm_ptr.p,    d_sparent.p,

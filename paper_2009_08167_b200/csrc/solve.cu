@@ -32,7 +32,6 @@ constexpr int kWholeMaxF = 256;  // max front rows of a small (warp-task) supern
 constexpr int kWholeMaxNp = 64;  // max pivots of a small supernode
 constexpr int kWarpPanel = 3328;  // doubles of a warp's staged panel (f * np <= this)
 constexpr int kWarpSmem = kWholeMaxF + kWarpPanel;  // doubles of smem per warp task
-constexpr int kSubtreeMax = 0;   // bottom-subtree walk per warp (0 = off: slower than level kernels)
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int64_t kChainSmemMax = 232448 - 4096;  // staged chain panels must fit this
@@ -239,6 +238,10 @@ struct GDev {
   const int64_t* g_off;   // per supernode offset (-1: large supernode)
   const int2* tiles;      // warp tasks: (supernode, 32-row tile) forward / (supernode, 8-column group) backward
   int on;
+  const double* D;        // pivots
+  double* wz;             // z ./ d of the small supernodes (forward -> backward), so the
+                          // backward column groups of one supernode never read the x
+                          // another group of it is writing
 };
 
 // one CTA per small supernode (np <= 64): warp w owns columns w, w+8, ...;
@@ -387,10 +390,12 @@ __device__ __forceinline__ void warp_gtile_fwd(const SymDev& S, const SolveDev& 
   const double* Gi = G + i;
 #pragma unroll 8
   for (int k = 0; k < np; ++k) acc = fma(Gi[k * f], yw[k], acc);
-  if (i < np)
+  if (i < np) {
     xp[col0 + i] = acc;
-  else
+    GD.wz[col0 + i] = acc / GD.D[col0 + i];
+  } else {
     upd[S.upd_off[s] + i - np] = yi - acc;
+  }
 }
 
 // warp task (s, g): x1 for columns [8 g, 8 g + 8) = G^T [z ./ d ; -x2]
@@ -406,7 +411,7 @@ __device__ __forceinline__ void warp_gtile_bwd(const SymDev& S, const GDev& GD, 
 #pragma unroll
   for (int c = 0; c < 8; ++c) acc[c] = 0.0;
   for (int r = (c0 & ~31) + lane; r < f; r += 32) {  // G(r, c) = 0 above the diagonal
-    const double v = r < np ? xp[col0 + r] / D[col0 + r] : -xp[rows[r]];
+    const double v = r < np ? GD.wz[col0 + r] : -xp[rows[r]];
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[c] = fma(c0 + c < np ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
   }
@@ -431,42 +436,34 @@ __device__ __forceinline__ void warp_gtile_bwd(const SymDev& S, const GDev& GD, 
 }
 
 // ---------------------------------------------------------------------------
-// bottom subtrees: one warp walks a whole subtree of small supernodes
-// (postorder forward, reverse postorder backward); the warp's own earlier
-// writes (update vectors, x) are visible to it after __syncwarp, so the
-// bottom of the tree needs one launch per sweep instead of one per level.
+// bottom subtrees (G mode): one CTA per maximal subtree of small supernodes
+// of height < sub_levels.  Its local levels run back to back separated by
+// __syncthreads (CTA-scope visibility of the update vectors / x it wrote),
+// so the bottom of the tree costs one launch per sweep instead of one per
+// level, and each CTA's chain of small mat-vecs overlaps the others'.
+// sub_ptr[i * (SL + 1) + j]: first task of local level j of subtree i.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSolveThreads) k_subtree_fwd(SymDev S, SolveDev T,
-                                                               const int32_t* __restrict__ sub_ptr,
-                                                               const int32_t* __restrict__ sub_nodes, int nsub,
-                                                               const double* __restrict__ panel,
-                                                               const double* __restrict__ b,
-                                                               double* __restrict__ xp,
-                                                               double* __restrict__ upd) {
-  extern __shared__ double y[];
+__global__ void __launch_bounds__(kSolveThreads, 4) k_sub_fwd(SymDev S, SolveDev T, GDev GD,
+                                                              const int32_t* __restrict__ sub_ptr, int SL,
+                                                              const double* __restrict__ b, double* xp, double* upd) {
+  __shared__ double y[kSolveWarps * kWholeMaxNp];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int t = blockIdx.x * kSolveWarps + w;
-  if (t >= nsub) return;
-  for (int q = sub_ptr[t]; q < sub_ptr[t + 1]; ++q) {
-    warp_whole_fwd(S, T, sub_nodes[q], panel, b, xp, upd, y + w * kWholeMaxF, lane, nullptr);
-    __syncwarp();
+  const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
+  for (int j = 0; j < SL; ++j) {
+    for (int t = p[j] + w; t < p[j + 1]; t += kSolveWarps)
+      warp_gtile_fwd(S, T, GD, GD.tiles[t], b, xp, upd, y + w * kWholeMaxNp, lane);
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads) k_subtree_bwd(SymDev S,
-                                                               const int32_t* __restrict__ sub_ptr,
-                                                               const int32_t* __restrict__ sub_nodes, int nsub,
-                                                               const double* __restrict__ panel,
-                                                               const double* __restrict__ D,
-                                                               double* __restrict__ xp,
-                                                               double* __restrict__ x) {
-  extern __shared__ double y[];
+__global__ void __launch_bounds__(kSolveThreads, 4) k_sub_bwd(SymDev S, GDev GD, const int32_t* __restrict__ sub_ptr,
+                                                              int SL, const double* __restrict__ D, double* xp,
+                                                              double* x) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int t = blockIdx.x * kSolveWarps + w;
-  if (t >= nsub) return;
-  for (int q = sub_ptr[t + 1] - 1; q >= sub_ptr[t]; --q) {
-    warp_whole_bwd(S, sub_nodes[q], panel, D, xp, x, y + w * kWholeMaxF, lane, nullptr);
-    __syncwarp();
+  const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
+  for (int j = SL - 1; j >= 0; --j) {
+    for (int t = p[j] + w; t < p[j + 1]; t += kSolveWarps) warp_gtile_bwd(S, GD, GD.tiles[t], D, xp, x, lane);
+    __syncthreads();
   }
 }
 
@@ -977,29 +974,46 @@ int build_solve_plan(riga_symbolic* sym) {
   L.ibwd_ptr.assign(h.nlevels + 1, 0);
   L.ifwd_smem.assign(h.nlevels, 8);
   auto large = [&](int64_t s) { return h.ncol[s] > kWholeMaxNp || h.front[s] > kWholeMaxF; };
-  // bottom subtrees of small supernodes, at most kSubtreeMax nodes each;
-  // supernodes are numbered in postorder, so a subtree is a contiguous range
-  std::vector<int32_t> size(ns, 1);
-  std::vector<char> ok(ns, 1);
-  for (int64_t s = 0; s < ns; ++s) {
-    if (large(s)) ok[s] = 0;
-    for (int64_t q = h.child_ptr[s]; q < h.child_ptr[s + 1]; ++q) {
-      const int32_t c = h.child_list[q];
-      size[s] += size[c];
-      if (!ok[c]) ok[s] = 0;
-    }
-    if (size[s] > kSubtreeMax) ok[s] = 0;
-  }
+  // bottom subtrees (G mode): maximal subtrees of small supernodes of height
+  // < sub_levels; supernodes are numbered in postorder, so a subtree is a
+  // contiguous range
+  L.sub_levels = L.small_g ? env_flag("RIGA_SUB_LEVELS", 0) : 0;
   std::vector<char> in_sub(ns, 0);
-  L.sub_ptr.assign(1, 0);
-  for (int64_t s = 0; s < ns; ++s) {
-    const int32_t p = h.sparent[s];
-    if (!ok[s] || (p >= 0 && ok[p])) continue;  // not a maximal eligible subtree root
-    for (int64_t q = s - size[s] + 1; q <= s; ++q) {
-      L.sub_nodes.push_back((int32_t)q);
-      in_sub[q] = 1;
+  if (L.sub_levels > 0) {
+    const int SL = L.sub_levels;
+    std::vector<int32_t> size(ns, 1);
+    std::vector<char> ok(ns, 1);
+    for (int64_t s = 0; s < ns; ++s) {
+      if (large(s) || h.level[s] >= SL) ok[s] = 0;
+      for (int64_t q = h.child_ptr[s]; q < h.child_ptr[s + 1]; ++q) {
+        const int32_t c = h.child_list[q];
+        size[s] += size[c];
+        if (!ok[c]) ok[s] = 0;
+      }
     }
-    L.sub_ptr.push_back((int32_t)L.sub_nodes.size());
+    for (int64_t s = 0; s < ns; ++s) {
+      const int32_t par = h.sparent[s];
+      if (!ok[s] || (par >= 0 && ok[par])) continue;  // not a maximal subtree root
+      std::vector<std::vector<int32_t>> byl(SL);
+      for (int64_t q = s - size[s] + 1; q <= s; ++q) {
+        byl[h.level[q]].push_back((int32_t)q);
+        in_sub[q] = 1;
+        L.g_off[q] = L.g_total;
+        L.g_total += h.front[q] * h.ncol[q];
+        L.wholes.push_back((int32_t)q);
+      }
+      for (int j = 0; j < SL; ++j) {
+        L.sub_fptr.push_back((int32_t)L.sub_ftiles.size());
+        L.sub_bptr.push_back((int32_t)L.sub_btiles.size());
+        for (int32_t q : byl[j]) {
+          for (int32_t t = 0; t < (int32_t)((h.front[q] + 31) / 32); ++t) L.sub_ftiles.push_back({q, t});
+          for (int32_t g = 0; g < (int32_t)((h.ncol[q] + 7) / 8); ++g) L.sub_btiles.push_back({q, g});
+        }
+      }
+      L.sub_fptr.push_back((int32_t)L.sub_ftiles.size());
+      L.sub_bptr.push_back((int32_t)L.sub_btiles.size());
+      ++L.nsub;
+    }
   }
   L.fwd_ptr.assign(h.nlevels + 1, 0);
   L.bwd_ptr.assign(h.nlevels + 1, 0);
@@ -1123,9 +1137,11 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
   if (!L.bwd.empty()) RIGA_TRY(sym->d_tbwd.upload(L.bwd.data(), L.bwd.size(), s));
   if (!L.chains.empty()) RIGA_TRY(sym->d_chains.upload(L.chains.data(), L.chains.size(), s));
   if (!L.wholes.empty()) RIGA_TRY(sym->d_wholes.upload(L.wholes.data(), L.wholes.size(), s));
-  if (!L.sub_nodes.empty()) {
-    RIGA_TRY(sym->d_sub_nodes.upload(L.sub_nodes.data(), L.sub_nodes.size(), s));
-    RIGA_TRY(sym->d_sub_ptr.upload(L.sub_ptr.data(), L.sub_ptr.size(), s));
+  if (L.nsub) {
+    RIGA_TRY(sym->d_sub_fptr.upload(L.sub_fptr.data(), L.sub_fptr.size(), s));
+    RIGA_TRY(sym->d_sub_bptr.upload(L.sub_bptr.data(), L.sub_bptr.size(), s));
+    RIGA_TRY(sym->d_sub_ftiles.upload(L.sub_ftiles.data(), L.sub_ftiles.size(), s));
+    RIGA_TRY(sym->d_sub_btiles.upload(L.sub_btiles.data(), L.sub_btiles.size(), s));
   }
   RIGA_TRY(sym->d_gptr.upload(L.gptr.data(), L.gptr.size(), s));
   if (L.small_g && L.g_total) {
@@ -1169,8 +1185,6 @@ static int set_solve_attrs() {
   RIGA_TRY(raise_smem(k_chain_fwd, maxsm));
   RIGA_TRY(raise_smem(k_chain_bwd, maxsm));
   RIGA_TRY(raise_smem(k_inv_fwd, maxsm));
-  RIGA_TRY(raise_smem(k_subtree_fwd, maxsm));
-  RIGA_TRY(raise_smem(k_subtree_bwd, maxsm));
   done = true;
   return RIGA_OK;
 }
@@ -1217,8 +1231,8 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   SymDev S = sym->dev();
   SolveDev T{sym->d_gptr.p, sym->d_gsrc.p, b_permuted ? 1 : 0};
   const int gon = L.small_g && L.g_total ? 1 : 0;
-  const GDev GDf{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gfwd.p), gon};
-  const GDev GDb{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gbwd.p), gon};
+  const GDev GDf{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gfwd.p), gon, F->D.p, F->cvec.p};
+  const GDev GDb{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gbwd.p), gon, F->D.p, F->cvec.p};
   const int2* tf = reinterpret_cast<const int2*>(sym->d_tfwd.p);
   const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
   const int64_t pbytes = h.panel_total * 8;
@@ -1227,10 +1241,11 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
                                                                                                    pbytes);
     count_launch();
   }
-  const int nsub = (int)L.sub_ptr.size() - 1;
-  if (nsub > 0) {
-    k_subtree_fwd<<<(nsub + kSolveWarps - 1) / kSolveWarps, kSolveThreads, kSolveWarps * kWholeMaxF * 8, st>>>(
-        S, T, sym->d_sub_ptr.p, sym->d_sub_nodes.p, nsub, F->panel.p, b, F->xperm.p, F->upd.p);
+  if (L.nsub && gon) {
+    const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_ftiles.p), 1, F->D.p,
+                  F->cvec.p};
+    k_sub_fwd<<<(unsigned)L.nsub, kSolveThreads, 0, st>>>(S, T, Gs, sym->d_sub_fptr.p, L.sub_levels, b, F->xperm.p,
+                                                          F->upd.p);
     count_launch();
   }
   for (int64_t l = 0; l < h.nlevels; ++l) {
@@ -1275,9 +1290,11 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
       count_launch();
     }
   }
-  if (nsub > 0) {
-    k_subtree_bwd<<<(nsub + kSolveWarps - 1) / kSolveWarps, kSolveThreads, kSolveWarps * kWholeMaxF * 8, st>>>(
-        S, sym->d_sub_ptr.p, sym->d_sub_nodes.p, nsub, F->panel.p, F->D.p, F->xperm.p, x);
+  if (L.nsub && gon) {
+    const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_btiles.p), 1, F->D.p,
+                  F->cvec.p};
+    k_sub_bwd<<<(unsigned)L.nsub, kSolveThreads, 0, st>>>(S, Gs, sym->d_sub_bptr.p, L.sub_levels, F->D.p,
+                                                          F->xperm.p, x);
     count_launch();
   }
   RIGA_CUDA(cudaGetLastError());
