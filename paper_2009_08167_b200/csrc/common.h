@@ -130,6 +130,10 @@ struct CtxRef {
   }
   ~CtxRef() { ctx_release(c); }
 };
+// Wait for a stream with a blocking-sync event: the host thread sleeps
+// instead of spinning (16 slice threads spinning in cudaStreamSynchronize
+// would take every core and starve the threads that launch work).
+cudaError_t stream_sync(cudaStream_t s);
 // Process-wide cache of pinned host blocks: cudaMallocHost / cudaFreeHost
 // synchronise the device, so blocks are recycled instead of freed.
 void* pinned_get(size_t bytes);

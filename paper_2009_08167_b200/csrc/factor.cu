@@ -396,7 +396,7 @@ static int upload_symbolic(riga_symbolic* sym) {
   RIGA_TRY(up(sym->d_ea_items, sym->ea_items_host, s));
   RIGA_TRY(up(sym->d_large_nodes, sym->large_host, s));
   RIGA_TRY(upload_solve_plan(sym, s));
-  RIGA_CUDA(cudaStreamSynchronize(s));
+  RIGA_CUDA(stream_sync(s));
   sym->on_device = true;
   return RIGA_OK;
 }
@@ -577,7 +577,7 @@ int riga_symbolic_destroy(riga_symbolic* sym) {
   if (!sym) return RIGA_OK;
   if (sym->ctx) {
     DeviceGuard g(sym->ctx->device);
-    cudaStreamSynchronize(sym->ctx->stream);
+    stream_sync(sym->ctx->stream);
     delete sym;
   } else {
     delete sym;
@@ -620,7 +620,7 @@ int riga_factor_create(riga_ctx* ctx, riga_symbolic* sym, double sigma, double r
   double tol[2];
   RIGA_CUDA(cudaMemcpyAsync(stat, F->stat.p, sizeof(stat), cudaMemcpyDeviceToHost, st));
   RIGA_CUDA(cudaMemcpyAsync(tol, F->tol.p, sizeof(tol), cudaMemcpyDeviceToHost, st));
-  RIGA_CUDA(cudaStreamSynchronize(st));
+  RIGA_CUDA(stream_sync(st));
   cudaEventElapsedTime(&F->factor_ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -659,7 +659,7 @@ int riga_factor_D(riga_factor* f, double* D) {
   RIGA_CHECK_ARG(f && D, "null arg");
   DeviceGuard g(f->ctx->device);
   RIGA_CUDA(cudaMemcpyAsync(D, f->D.p, f->sym->h.n * 8, cudaMemcpyDeviceToHost, f->ctx->stream));
-  RIGA_CUDA(cudaStreamSynchronize(f->ctx->stream));
+  RIGA_CUDA(stream_sync(f->ctx->stream));
   return RIGA_OK;
 }
 
@@ -670,7 +670,7 @@ int riga_factor_export(riga_factor* f, int64_t* Lp, int32_t* Li, double* Lx) {
   std::vector<double> panel(h.panel_total);
   RIGA_CUDA(cudaMemcpyAsync(panel.data(), f->panel.p, h.panel_total * 8, cudaMemcpyDeviceToHost,
                             f->ctx->stream));
-  RIGA_CUDA(cudaStreamSynchronize(f->ctx->stream));
+  RIGA_CUDA(stream_sync(f->ctx->stream));
   int64_t q = 0;
   Lp[0] = 0;
   for (int64_t s = 0; s < h.nsuper; ++s) {
@@ -692,7 +692,7 @@ int riga_factor_export(riga_factor* f, int64_t* Lp, int32_t* Li, double* Lx) {
 int riga_factor_destroy(riga_factor* f) {
   if (!f) return RIGA_OK;
   DeviceGuard g(f->ctx->device);
-  cudaStreamSynchronize(f->ctx->stream);
+  stream_sync(f->ctx->stream);
   delete f;
   return RIGA_OK;
 }

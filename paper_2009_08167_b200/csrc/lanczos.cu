@@ -570,7 +570,7 @@ int push_state(riga_lanczos* lz, int64_t clo, int64_t limit, double btol) {
 
 int pull_state(riga_lanczos* lz) {
   RIGA_CUDA(cudaMemcpyAsync(lz->hst, lz->st.p, sizeof(LzDev), cudaMemcpyDeviceToHost, lz->ctx->stream));
-  RIGA_CUDA(cudaStreamSynchronize(lz->ctx->stream));
+  RIGA_CUDA(stream_sync(lz->ctx->stream));
   return RIGA_OK;
 }
 
@@ -666,7 +666,7 @@ int ensure_graph(riga_lanczos* lz) {
   // first-use allocations and kernel attributes must happen outside the capture
   riga_factor* F = lz->op;
   RIGA_TRY(prepare_solve());
-  RIGA_CUDA(cudaStreamSynchronize(s));
+  RIGA_CUDA(stream_sync(s));
   cudaGraph_t g = nullptr;
   if (!lz->capst) RIGA_CUDA(cudaStreamCreateWithFlags(&lz->capst, cudaStreamNonBlocking));
   const long long n0 = t_launches;
@@ -735,7 +735,7 @@ int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max
     set_error("pinned host allocation failed");
     return RIGA_OOM;
   }
-  RIGA_CUDA(cudaStreamSynchronize(cs));
+  RIGA_CUDA(stream_sync(cs));
   *out = lz.release();
   return RIGA_OK;
 }
@@ -743,7 +743,7 @@ int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max
 int riga_lanczos_destroy(riga_lanczos* lz) {
   if (!lz) return RIGA_OK;
   DeviceGuard g(lz->ctx->device);
-  cudaStreamSynchronize(lz->ctx->stream);
+  stream_sync(lz->ctx->stream);
   delete lz;
   return RIGA_OK;
 }
@@ -955,7 +955,7 @@ int riga_lanczos_lock_block(riga_lanczos* lz, double* X, double* MX, int64_t c, 
   k_rowdots<<<cc, 256, 0, s>>>(X, MX, lz->ld, lz->n, nrm.p);
   count_launch();
   RIGA_CUDA(cudaMemcpyAsync(nrm2_host, nrm.p, c * 8, cudaMemcpyDeviceToHost, s));
-  RIGA_CUDA(cudaStreamSynchronize(s));
+  RIGA_CUDA(stream_sync(s));
   return RIGA_OK;
 }
 
@@ -1109,7 +1109,7 @@ int riga_lanczos_gram(riga_lanczos* lz, double* G) {
     count_launch(2);
     RIGA_CUDA(cudaMemcpyAsync(G + i * k, lz->coef.p, k * 8, cudaMemcpyDeviceToHost, s));
   }
-  RIGA_CUDA(cudaStreamSynchronize(s));
+  RIGA_CUDA(stream_sync(s));
   return RIGA_OK;
 }
 

@@ -470,8 +470,8 @@ __global__ void __launch_bounds__(kSolveThreads, 4) k_sub_bwd(SymDev S, GDev GD,
 // ---------------------------------------------------------------------------
 // light kernels: WHOLE / UPD (forward), WHOLE / COLDOT (backward)
 // ---------------------------------------------------------------------------
-template <bool GT>
-__global__ void __launch_bounds__(kSolveThreads, GT ? 4 : 2) k_rest_fwd(SymDev S, SolveDev T,
+template <bool GT, int MINB = 4>
+__global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDev S, SolveDev T,
                                                             const int2* __restrict__ tasks,
                                                             const int32_t* __restrict__ wholes,
                                                             const double* __restrict__ panel,
@@ -532,8 +532,8 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? 4 : 2) k_rest_fwd(SymDev S
   }
 }
 
-template <bool GT>
-__global__ void __launch_bounds__(kSolveThreads, GT ? 4 : 2) k_rest_bwd(SymDev S, SolveDev T,
+template <bool GT, int MINB = 4>
+__global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDev S, SolveDev T,
                                                             const int2* __restrict__ tasks,
                                                             const int32_t* __restrict__ wholes,
                                                             const double* __restrict__ panel,
@@ -968,6 +968,7 @@ int build_solve_plan(riga_symbolic* sym) {
   L.chain_inv = env_flag("RIGA_CHAIN_INV", 1);
   // small supernodes through G = [inv(L11); L21 inv(L11)] (default) or substitution
   L.small_g = env_flag("RIGA_SMALL_G", 1);
+  L.occ = env_flag("RIGA_REST_OCC", 4);  // CTAs per SM the G-mode level kernels are register-bounded for
   L.g_off.assign(ns, -1);
   L.inv_off.assign(ns, -1);
   L.ifwd_ptr.assign(h.nlevels + 1, 0);
@@ -1180,8 +1181,12 @@ static int set_solve_attrs() {
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   RIGA_TRY(raise_smem(k_rest_fwd<false>, maxsm));
   RIGA_TRY(raise_smem(k_rest_bwd<false>, maxsm));
-  RIGA_TRY(raise_smem(k_rest_fwd<true>, maxsm));
-  RIGA_TRY(raise_smem(k_rest_bwd<true>, maxsm));
+  RIGA_TRY(raise_smem(k_rest_fwd<true, 4>, maxsm));
+  RIGA_TRY(raise_smem(k_rest_bwd<true, 4>, maxsm));
+  RIGA_TRY(raise_smem(k_rest_fwd<true, 6>, maxsm));
+  RIGA_TRY(raise_smem(k_rest_bwd<true, 6>, maxsm));
+  RIGA_TRY(raise_smem(k_rest_fwd<true, 8>, maxsm));
+  RIGA_TRY(raise_smem(k_rest_bwd<true, 8>, maxsm));
   RIGA_TRY(raise_smem(k_chain_fwd, maxsm));
   RIGA_TRY(raise_smem(k_chain_bwd, maxsm));
   RIGA_TRY(raise_smem(k_inv_fwd, maxsm));
@@ -1264,7 +1269,8 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     }
     const int nt = (int)(L.fwd_ptr[l + 1] - L.fwd_ptr[l]);
     if (nt) {
-      (gon ? k_rest_fwd<true> : k_rest_fwd<false>)<<<nt, kSolveThreads, L.fwd_smem[l], st>>>(S, T, tf + L.fwd_ptr[l], sym->d_wholes.p,
+      (gon ? (L.occ == 8 ? k_rest_fwd<true, 8> : L.occ == 6 ? k_rest_fwd<true, 6> : k_rest_fwd<true, 4>)
+           : k_rest_fwd<false>)<<<nt, kSolveThreads, L.fwd_smem[l], st>>>(S, T, tf + L.fwd_ptr[l], sym->d_wholes.p,
                                                            F->panel.p, b, F->xperm.p, F->upd.p, L.warp_stage, GDf);
       count_launch();
     }
@@ -1272,7 +1278,8 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   for (int64_t l = h.nlevels - 1; l >= 0; --l) {
     const int nt = (int)(L.bwd_ptr[l + 1] - L.bwd_ptr[l]);
     if (nt) {
-      (gon ? k_rest_bwd<true> : k_rest_bwd<false>)<<<nt, kSolveThreads, L.bwd_smem[l], st>>>(S, T, tb + L.bwd_ptr[l], sym->d_wholes.p,
+      (gon ? (L.occ == 8 ? k_rest_bwd<true, 8> : L.occ == 6 ? k_rest_bwd<true, 6> : k_rest_bwd<true, 4>)
+           : k_rest_bwd<false>)<<<nt, kSolveThreads, L.bwd_smem[l], st>>>(S, T, tb + L.bwd_ptr[l], sym->d_wholes.p,
                                                            F->panel.p, F->D.p, F->xperm.p, F->cvec.p, x, L.warp_stage,
                                                            L.chain_inv, GDb);
       count_launch();

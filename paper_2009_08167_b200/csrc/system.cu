@@ -155,7 +155,7 @@ int csr_spmv(cudaStream_t s, int64_t n, const int64_t* rowptr, const int32_t* co
              const double* val, const double* x, double* y) {
   int64_t nnz = 0;
   RIGA_CUDA(cudaMemcpyAsync(&nnz, rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  RIGA_CUDA(cudaStreamSynchronize(s));
+  RIGA_CUDA(stream_sync(s));
   return csr_spmv_impl(s, n, rowptr, colidx, val, nullptr, 0.0, 0, nnz, x, y);
 }
 
@@ -223,11 +223,26 @@ void ctx_release(riga_ctx* c) {
   if (!c) return;
   if (c->refs.fetch_sub(1) != 1) return;
   DeviceGuard g(c->device);
-  cudaStreamSynchronize(c->stream);  // this stream only: pending reads into scratch_host
+  stream_sync(c->stream);  // this stream only: pending reads into scratch_host
   if (c->scratch_dev) cudaFreeAsync(c->scratch_dev, c->stream);
   if (c->scratch_host) pinned_put(c->scratch_host);
   if (c->own_stream) cudaStreamDestroy(c->stream);  // released once its work drains
   delete c;
+}
+
+cudaError_t stream_sync(cudaStream_t s) {
+  thread_local cudaEvent_t ev = nullptr;
+  thread_local int ev_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!ev || ev_dev != dev) {
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventBlockingSync | cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    ev_dev = dev;
+  }
+  cudaError_t e = cudaEventRecord(ev, s);
+  if (e != cudaSuccess) return e;
+  return cudaEventSynchronize(ev);
 }
 
 namespace {
@@ -362,7 +377,7 @@ int riga_ctx_destroy(riga_ctx* ctx) {
 int riga_ctx_synchronize(riga_ctx* ctx) {
   RIGA_CHECK_ARG(ctx, "null ctx");
   DeviceGuard g(ctx->device);
-  RIGA_CUDA(cudaStreamSynchronize(ctx->stream));
+  RIGA_CUDA(stream_sync(ctx->stream));
   return RIGA_OK;
 }
 
@@ -388,7 +403,7 @@ int riga_system_upload(riga_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row
   RIGA_TRY(sys->colidx.upload(colidx, nnz, ctx->stream));
   RIGA_TRY(sys->K.upload(K, nnz, ctx->stream));
   RIGA_TRY(sys->M.upload(M, nnz, ctx->stream));
-  RIGA_CUDA(cudaStreamSynchronize(ctx->stream));
+  RIGA_CUDA(stream_sync(ctx->stream));
   *out = sys.release();
   return RIGA_OK;
 }
@@ -435,7 +450,7 @@ int riga_system_assemble_kron(riga_ctx* ctx, int dim, const int64_t* n1,
   k_kron_values<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
       dim, ax[0], ax[1], ax[2], n, sys->rowptr.p, sys->colidx.p, sys->K.p, sys->M.p); count_launch();
   RIGA_CUDA(cudaGetLastError());
-  RIGA_CUDA(cudaStreamSynchronize(s));
+  RIGA_CUDA(stream_sync(s));
   *out = sys.release();
   return RIGA_OK;
 }
@@ -458,7 +473,7 @@ int riga_system_download(riga_system* sys, int64_t* rowptr, int32_t* colidx, dou
     RIGA_CUDA(cudaMemcpyAsync(colidx, sys->colidx.p, sys->nnz * 4, cudaMemcpyDeviceToHost, s));
   if (K) RIGA_CUDA(cudaMemcpyAsync(K, sys->K.p, sys->nnz * 8, cudaMemcpyDeviceToHost, s));
   if (M) RIGA_CUDA(cudaMemcpyAsync(M, sys->M.p, sys->nnz * 8, cudaMemcpyDeviceToHost, s));
-  RIGA_CUDA(cudaStreamSynchronize(s));
+  RIGA_CUDA(stream_sync(s));
   return RIGA_OK;
 }
 
@@ -475,7 +490,7 @@ int riga_system_device_ptrs(riga_system* sys, const int64_t** rowptr, const int3
 int riga_system_destroy(riga_system* sys) {
   if (!sys) return RIGA_OK;
   DeviceGuard g(sys->ctx->device);
-  cudaStreamSynchronize(sys->ctx->stream);
+  stream_sync(sys->ctx->stream);
   delete sys;
   return RIGA_OK;
 }
@@ -499,7 +514,7 @@ int riga_dot(riga_ctx* ctx, int64_t n, const double* x, const double* y, double*
   RIGA_TRY(launch_dot(ctx->stream, n, x, y, ctx->scratch_dev));
   RIGA_CUDA(cudaMemcpyAsync(ctx->scratch_host, ctx->scratch_dev, sizeof(double),
                             cudaMemcpyDeviceToHost, ctx->stream));
-  RIGA_CUDA(cudaStreamSynchronize(ctx->stream));
+  RIGA_CUDA(stream_sync(ctx->stream));
   *out = ctx->scratch_host[0];
   return RIGA_OK;
 }

@@ -224,6 +224,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                         so = SolverOptions(m=m, **opts)
                         rng = np.random.default_rng(seeds[k])
                         _solve_interval(pen, lob, hib, pool, so, rng, scale)
+                    t_col = time.perf_counter()
                     idx = sorted((i for i, lam in enumerate(pool.lams) if lob.sigma < lam <= hib.sigma),
                                  key=lambda i: pool.lams[i])
                     lams = np.array([pool.lams[i] for i in idx])
@@ -233,6 +234,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                     else:
                         X = np.empty((0, system.dof_count))
                     ctx.synchronize()
+                    cnt.phase("collect", time.perf_counter() - t_col)
                     with lock:
                         results[k] = (lams, X)
                         slice_times[k] = (t_start - t0, time.perf_counter() - t0, cnt.nfb)

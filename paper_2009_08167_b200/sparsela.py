@@ -67,6 +67,10 @@ class CostCounters:
     nit: int = 0
     retries: int = 0
     steps_per_iteration: list = field(default_factory=list)
+    phase_s: dict = field(default_factory=dict)  # host wall seconds per driver phase (engine extension)
+
+    def phase(self, name: str, dt: float) -> None:
+        self.phase_s[name] = self.phase_s.get(name, 0.0) + dt
 
     @property
     def nfa(self) -> int:
@@ -88,6 +92,8 @@ class CostCounters:
         self.nit += other.nit
         self.retries += other.retries
         self.steps_per_iteration.extend(other.steps_per_iteration)
+        for k, v in other.phase_s.items():
+            self.phase(k, v)
 
 
 # ---------------------------------------------------------------------------

@@ -14,7 +14,10 @@ perm = P.separator_ordering(s)
 sym = Symbolic.on_device(s.device, perm)
 for it in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
     t0 = time.perf_counter()
+    c0 = os.times()
     r = P.solve_uniform_slices(s, sh, streams=streams, pencil_symbolic=sym, perm=perm)
     print("total", round(time.perf_counter() - t0, 3), "boundary", round(r.timings["boundary_s"], 3),
-          "slices", round(r.timings["slices_s"], 3), "nfb", r.counters.nfb)
+          "slices", round(r.timings["slices_s"], 3), "nfb", r.counters.nfb,
+          "cpu_s", round((os.times().user - c0.user) + (os.times().system - c0.system), 2))
 print(json.dumps(r.timings["slice_wall"]))
+print("phase seconds summed over slices", {k: round(v, 3) for k, v in r.counters.phase_s.items()})
