@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libriga_b200.so")
+# RIGA_LIB: load an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("RIGA_LIB") or os.path.join(HERE, "libriga_b200.so")
 
 OK, ZERO_PIVOT, BAD_ARG, CUDA_ERROR, OOM, BREAKDOWN, NO_DEVICE = range(7)
 

@@ -29,7 +29,8 @@
 namespace riga {
 
 constexpr int kWholeMaxF = 256;  // max front rows of a small (warp-task) supernode
-constexpr int kWholeMaxNp = 64;  // max pivots of a small supernode
+constexpr int kWholeMaxNp = 64;  // max pivots of a small supernode (substitution mode)
+constexpr int kGMaxNp = 128;     // max pivots of a G-mode supernode (any front size)
 constexpr int kWarpPanel = 3328;  // doubles of a warp's staged panel (f * np <= this)
 constexpr int kWarpSmem = kWholeMaxF + kWarpPanel;  // doubles of smem per warp task
 constexpr int kSolveThreads = 256;
@@ -244,52 +245,53 @@ struct GDev {
                           // another group of it is writing
 };
 
-// one CTA per small supernode (np <= 64): warp w owns columns w, w+8, ...;
-// lane owns rows lane, lane+32.  inv(L11) by column-oriented substitution
-// (x_k final at step k, broadcast by shuffle), then G_bot = L21 inv(L11).
+// one CTA per G-mode supernode (np <= 128).  inv(L11) by column-oriented
+// substitution: warp w owns columns w + 8 j (8 per round), lanes own rows
+// lane + 32 ri; x_k is final at step k and broadcast by shuffle.  Then
+// G_bot = L21 inv(L11) from inv(L11) in shared memory.
 __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __restrict__ nodes,
                                                  const double* __restrict__ panel,
                                                  const int64_t* __restrict__ g_off, double* __restrict__ gbuf) {
-  constexpr int LD = kWholeMaxNp + 1;
-  extern __shared__ double gsm[];
-  double* Ls = gsm;                     // L11 column-major, Ls[k * LD + r]
-  double* Xs = gsm + kWholeMaxNp * LD;  // inv(L11) column-major
+  constexpr int LD = kGMaxNp + 1;
+  extern __shared__ double Xs[];  // inv(L11) column-major, Xs[c * LD + r]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int s = nodes[blockIdx.x];
   const int f = (int)S.front[s], np = (int)S.ncol[s];
   const double* P = panel + S.panel_off[s];
   double* G = gbuf + g_off[s];
-  for (int e = threadIdx.x; e < np * np; e += 256) {
-    const int k = e / np, r = e - k * np;
-    Ls[k * LD + r] = P[(int64_t)k * f + r];
-  }
-  __syncthreads();
-  double x[2][8];
+  for (int jb = 0; 64 * jb < np; ++jb) {
+    double x[4][8];
 #pragma unroll
-  for (int ri = 0; ri < 2; ++ri)
+    for (int ri = 0; ri < 4; ++ri)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) x[ri][j] = (lane + 32 * ri == w + 8 * j) ? 1.0 : 0.0;
-  for (int k = 0; k + 1 < np; ++k) {
-    const int kr = k >> 5, kl = k & 31;
-    const double l0 = lane > k && lane < np ? Ls[k * LD + lane] : 0.0;
-    const double l1 = lane + 32 > k && lane + 32 < np ? Ls[k * LD + lane + 32] : 0.0;
+      for (int j = 0; j < 8; ++j) x[ri][j] = (lane + 32 * ri == w + 8 * (8 * jb + j)) ? 1.0 : 0.0;
+    for (int k = 64 * jb; k + 1 < np; ++k) {
+      const int kr = k >> 5, kl = k & 31;
+      double l[4];
+#pragma unroll
+      for (int ri = 0; ri < 4; ++ri) {
+        const int r = lane + 32 * ri;
+        l[ri] = (r > k && r < np) ? P[(int64_t)k * f + r] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double own = kr == 0 ? x[0][j] : kr == 1 ? x[1][j] : kr == 2 ? x[2][j] : x[3][j];
+        const double xk = __shfl_sync(0xffffffffu, own, kl);
+#pragma unroll
+        for (int ri = 0; ri < 4; ++ri) x[ri][j] = fma(-l[ri], xk, x[ri][j]);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const double xk = __shfl_sync(0xffffffffu, kr ? x[1][j] : x[0][j], kl);
-      x[0][j] = fma(-l0, xk, x[0][j]);
-      x[1][j] = fma(-l1, xk, x[1][j]);
-    }
-  }
+      const int c = w + 8 * (8 * jb + j);
+      if (c < np) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int c = w + 8 * j;
-    if (c < np) {
-#pragma unroll
-      for (int ri = 0; ri < 2; ++ri) {
-        const int r = lane + 32 * ri;
-        if (r < np) {
-          Xs[c * LD + r] = x[ri][j];
-          G[(int64_t)c * f + r] = x[ri][j];
+        for (int ri = 0; ri < 4; ++ri) {
+          const int r = lane + 32 * ri;
+          if (r < np) {
+            Xs[c * LD + r] = x[ri][j];
+            G[(int64_t)c * f + r] = x[ri][j];
+          }
         }
       }
     }
@@ -297,78 +299,25 @@ __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __rest
   __syncthreads();
   for (int i0 = np; i0 < f; i0 += 32) {
     const int i = i0 + lane;
-    double acc[8];
+    for (int jb = 0; 64 * jb < np; ++jb) {
+      double acc[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-    for (int k = 0; k < np; ++k) {
-      const double l = i < f ? P[(int64_t)k * f + i] : 0.0;
+      for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+      for (int k = 64 * jb; k < np; ++k) {  // inv(L11)(k, c) = 0 for k < c
+        const double l = i < f ? P[(int64_t)k * f + i] : 0.0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = fma(l, w + 8 * j < np ? Xs[(w + 8 * j) * LD + k] : 0.0, acc[j]);
-    }
-    if (i < f) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (w + 8 * j < np) G[(int64_t)(w + 8 * j) * f + i] = acc[j];
-    }
-  }
-}
-
-__device__ __forceinline__ void warp_g_fwd(const SymDev& S, const SolveDev& T, const GDev& GD, int s,
-                                           const double* __restrict__ b, double* xp, double* upd, double* yw,
-                                           int lane) {
-  const int f = (int)S.front[s], np = (int)S.ncol[s];
-  const int64_t col0 = S.col0[s];
-  const double* G = GD.g + GD.g_off[s];
-  for (int r = lane; r < f; r += 32) yw[r] = gather_row(S, T, s, r, np, col0, b, upd);
-  __syncwarp();
-  double* u = upd + S.upd_off[s] - np;
-  for (int i = lane; i < f; i += 32) {
-    double acc = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < np; ++k) acc = fma(G[k * f + i], yw[k], acc);
-    if (i < np)
-      xp[col0 + i] = acc;
-    else
-      u[i] = yw[i] - acc;
-  }
-}
-
-__device__ __forceinline__ void warp_g_bwd(const SymDev& S, const GDev& GD, int s, const double* __restrict__ D,
-                                           double* xp, double* x, double* yw, int lane) {
-  const int f = (int)S.front[s], np = (int)S.ncol[s];
-  const int64_t col0 = S.col0[s];
-  const double* G = GD.g + GD.g_off[s];
-  const int32_t* rows = S.rows + S.rows_off[s];
-  for (int r = lane; r < f; r += 32) yw[r] = r < np ? xp[col0 + r] / D[col0 + r] : -xp[rows[r]];
-  __syncwarp();
-  // 8 columns at a time: every lane accumulates its rows, then a fold-reduce
-  // leaves column c0 + (lane & 7) summed over the warp in that lane
-  for (int c0 = 0; c0 < np; c0 += 8) {
-    double acc[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-    for (int r = lane; r < f; r += 32) {
-      const double v = yw[r];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc[c] = fma(c0 + c < np ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
-    }
-#pragma unroll
-    for (int o = 4; o >= 1; o >>= 1) {
-#pragma unroll
-      for (int k = 0; k < o; ++k) {
-        const bool hi = (lane & o) != 0;
-        const double send = hi ? acc[k] : acc[k + o];
-        const double recv = __shfl_xor_sync(0xffffffffu, send, o);
-        acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
+        for (int j = 0; j < 8; ++j) {
+          const int c = w + 8 * (8 * jb + j);
+          acc[j] = fma(l, c < np ? Xs[c * LD + k] : 0.0, acc[j]);
+        }
       }
-    }
-    double v = acc[0];
-    v += __shfl_xor_sync(0xffffffffu, v, 8);
-    v += __shfl_xor_sync(0xffffffffu, v, 16);
-    const int c = c0 + lane;
-    if (lane < 8 && c < np) {
-      xp[col0 + c] = v;
-      x[S.order[col0 + c]] = v;
+      if (i < f) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = w + 8 * (8 * jb + j);
+          if (c < np) G[(int64_t)c * f + i] = acc[j];
+        }
+      }
     }
   }
 }
@@ -446,12 +395,12 @@ __device__ __forceinline__ void warp_gtile_bwd(const SymDev& S, const GDev& GD, 
 __global__ void __launch_bounds__(kSolveThreads, 4) k_sub_fwd(SymDev S, SolveDev T, GDev GD,
                                                               const int32_t* __restrict__ sub_ptr, int SL,
                                                               const double* __restrict__ b, double* xp, double* upd) {
-  __shared__ double y[kSolveWarps * kWholeMaxNp];
+  __shared__ double y[kSolveWarps * kGMaxNp];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
   for (int j = 0; j < SL; ++j) {
     for (int t = p[j] + w; t < p[j + 1]; t += kSolveWarps)
-      warp_gtile_fwd(S, T, GD, GD.tiles[t], b, xp, upd, y + w * kWholeMaxNp, lane);
+      warp_gtile_fwd(S, T, GD, GD.tiles[t], b, xp, upd, y + w * kGMaxNp, lane);
     __syncthreads();
   }
 }
@@ -486,16 +435,12 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDe
   const int type = task.y >> 24, j = task.y & 0x00ffffff;
   if (GT && type == kGTiles) {
     if (w >= j) return;
-    warp_gtile_fwd(S, T, GD, GD.tiles[task.x + w], b, xp, upd, y + w * kWholeMaxNp, lane);
+    warp_gtile_fwd(S, T, GD, GD.tiles[task.x + w], b, xp, upd, y + w * kGMaxNp, lane);
     return;
   }
   if (!GT && type == kWholeGroup) {
     // warp w: small supernode wholes[task.x + w], whole front in a warp slice
     if (w >= j) return;
-    if (GD.on) {
-      warp_g_fwd(S, T, GD, wholes[task.x + w], b, xp, upd, y + w * kWholeMaxF, lane);
-      return;
-    }
     if (stage && lane == 0) mbar_init(&wbar[w], 1);
     __syncwarp();
     warp_whole_fwd(S, T, wholes[task.x + w], panel, b, xp, upd, y + w * (stage ? kWarpSmem : kWholeMaxF), lane,
@@ -554,10 +499,6 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDe
   }
   if (!GT && type == kWholeGroup) {
     if (w >= bj) return;
-    if (GD.on) {
-      warp_g_bwd(S, GD, wholes[task.x + w], D, xp, x, y + w * kWholeMaxF, lane);
-      return;
-    }
     if (stage && lane == 0) mbar_init(&wbar[w], 1);
     __syncwarp();
     warp_whole_bwd(S, wholes[task.x + w], panel, D, xp, x, y + w * (stage ? kWarpSmem : kWholeMaxF), lane,
@@ -974,7 +915,9 @@ int build_solve_plan(riga_symbolic* sym) {
   L.ifwd_ptr.assign(h.nlevels + 1, 0);
   L.ibwd_ptr.assign(h.nlevels + 1, 0);
   L.ifwd_smem.assign(h.nlevels, 8);
-  auto large = [&](int64_t s) { return h.ncol[s] > kWholeMaxNp || h.front[s] > kWholeMaxF; };
+  auto large = [&](int64_t s) {
+    return L.small_g ? h.ncol[s] > kGMaxNp : (h.ncol[s] > kWholeMaxNp || h.front[s] > kWholeMaxF);
+  };
   // bottom subtrees (G mode): maximal subtrees of small supernodes of height
   // < sub_levels; supernodes are numbered in postorder, so a subtree is a
   // contiguous range
@@ -1090,7 +1033,7 @@ int build_solve_plan(riga_symbolic* sym) {
     }
     L.wholes.insert(L.wholes.end(), small.begin(), small.end());
     if (!small.empty()) {
-      const int64_t per = L.small_g ? kWholeMaxNp : L.warp_stage ? kWarpSmem : kWholeMaxF;
+      const int64_t per = L.small_g ? kGMaxNp : L.warp_stage ? kWarpSmem : kWholeMaxF;
       smf = std::max<int64_t>(smf, kSolveWarps * per);
       smb = std::max<int64_t>(smb, kSolveWarps * per);
     }
@@ -1203,7 +1146,7 @@ int build_chain_inverse(riga_factor* F, cudaStream_t st) {
   if (L.small_g && L.g_total) {
     if (!F->gsmall.p) RIGA_TRY(F->gsmall.alloc(L.g_total, st));
     const int nw = (int)L.wholes.size();
-    constexpr int smem = 2 * kWholeMaxNp * (kWholeMaxNp + 1) * 8;
+    constexpr int smem = kGMaxNp * (kGMaxNp + 1) * 8;
     static bool attr = false;
     if (!attr) {
       RIGA_CUDA(cudaFuncSetAttribute(k_small_g, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -25,14 +25,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--what", default="extend", choices=["extend", "solve"])
+    ap.add_argument("--what", default="extend", choices=["extend", "solve", "solveg"])
+    ap.add_argument("--threads", default="1,2,4,8,16")
     a = ap.parse_args()
     c = CONFIGS[a.config]
     s = P.build_system(c.d, c.ne, c.p, c.level)
     lam_e, _ = P.choose_lambda_e(s, c.n0)
     sh = P.uniform_shifts(lam_e, c.slices)
     sym = Symbolic.on_device(s.device, P.separator_ordering(s))
-    for T in (1, 2, 4, 8, 16):
+    for T in [int(t) for t in a.threads.split(",")]:
         ctxs = [D.Context() for _ in range(T)]
         facts, states = [], []
         for i, ctx in enumerate(ctxs):
@@ -44,12 +45,30 @@ def main():
                 states.append(st)
         torch.cuda.synchronize()
         bar = threading.Barrier(T)
+        graphs = [None] * T
+        if a.what == "solveg":
+            # a CUDA graph of 20 solves per stream: the device cost, not the host launches
+            for i in range(T):
+                with ctxs[i]:
+                    b = torch.randn(s.dof_count, dtype=torch.float64, device="cuda")
+                    x = torch.empty_like(b)
+                    facts[i].solve_device(b, x)
+                    ctxs[i].synchronize()
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=ctxs[i].stream, capture_error_mode="thread_local"):
+                        for _ in range(20):
+                            facts[i].solve_device(b, x)
+                    graphs[i] = (g, b, x)
+            torch.cuda.synchronize()
 
         def work(i):
             bar.wait()
             with ctxs[i]:
                 if a.what == "extend":
                     P.lanczos_extend(states[i], a.steps)
+                elif a.what == "solveg":
+                    for _ in range(a.steps // 20):
+                        graphs[i][0].replay()
                 else:
                     b = torch.randn(s.dof_count, dtype=torch.float64, device="cuda")
                     x = torch.empty_like(b)
