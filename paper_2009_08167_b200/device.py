@@ -20,13 +20,14 @@ class Context:
     """An engine context (device, stream).  Wraps a torch stream so that
     torch allocations/copies and engine kernels are ordered on one stream."""
 
-    def __init__(self, device: int | None = None, stream: torch.cuda.Stream | None = None):
+    def __init__(self, device: int | None = None, stream: torch.cuda.Stream | None = None, priority: int = 0):
         if not torch.cuda.is_available() or _lib.device_count() == 0:
             raise RuntimeError("no CUDA device visible: the B200 engine has no CPU fallback")
         if device is None:
             device = torch.cuda.current_device()
         self.device = int(device)
-        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device, priority=priority)
+        self.priority = priority
         h = ctypes.c_void_p()
         # torch's default stream has handle 0; the engine reads 0 as "make a
         # private stream", so pass cudaStreamLegacy (0x1) to stay ordered

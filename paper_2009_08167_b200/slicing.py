@@ -93,21 +93,38 @@ _ctx_free: dict = {}
 _ctx_lock = threading.Lock()
 
 
-def _take_ctx(device: int):
-    """A slice-worker context (own stream) from a per-device free list:
-    streams are reused across calls, so torch's per-stream block cache and
-    the engine pool do not fragment over many calls."""
+def _take_ctx(device: int, priority: int = 0):
+    """A slice-worker context (own stream) from a per-(device, priority) free
+    list: streams are reused across calls, so torch's per-stream block cache
+    and the engine pool do not fragment over many calls."""
     with _ctx_lock:
-        lst = _ctx_free.setdefault(device, [])
+        lst = _ctx_free.setdefault((device, priority), [])
         if lst:
             return lst.pop()
-    return _dev.Context(device)
+    return _dev.Context(device, priority=priority)
 
 
 def _give_ctx(ctx) -> None:
     ctx.synchronize()
     with _ctx_lock:
-        _ctx_free.setdefault(ctx.device, []).append(ctx)
+        _ctx_free.setdefault((ctx.device, ctx.priority), []).append(ctx)
+
+
+def _priorities(work: list) -> list:
+    """Stream priority per slice: the slices with the most work get the
+    highest priorities, so the block scheduler lets them run ahead and the
+    light slices fill the gaps instead of leaving a tail of heavy ones."""
+    import os
+
+    if not work or os.environ.get("RIGA_SLICE_PRIORITY", "1") == "0":
+        return [0] * len(work)
+    least, greatest = torch.cuda.Stream.priority_range()  # e.g. (0, -5)
+    levels = least - greatest + 1
+    order = sorted(range(len(work)), key=lambda i: (-work[i], i))
+    pr = [0] * len(work)
+    for rank, i in enumerate(order):
+        pr[i] = greatest + (rank * levels) // len(work)
+    return pr
 
 
 class _blas_threads:
@@ -196,16 +213,27 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     errors = []
     lock = threading.Lock()
     queue = sorted(my, key=lambda k: -expected[k])
+    order = list(queue)
+    one_per_thread = len(my) <= max(1, streams)
+    # one slice per stream: stream priorities by expected work; otherwise a
+    # shared queue (largest first) on default-priority streams
+    prio = _priorities([int(expected[k]) for k in order]) if one_per_thread else [0] * len(order)
 
     def worker(widx):
-        ctx = _take_ctx(base_ctx.device)
+        ctx = _take_ctx(base_ctx.device, prio[widx])
         cnt = CostCounters()
+        mine = [order[widx]] if one_per_thread else None
         with ctx:
             while True:
                 with lock:
-                    if not queue:
-                        break
-                    k = queue.pop(0)
+                    if mine is not None:
+                        if not mine:
+                            break
+                        k = mine.pop()
+                    else:
+                        if not queue:
+                            break
+                        k = queue.pop(0)
                 try:
                     t_start = time.perf_counter()
                     pen = make_pencil(ctx, cnt)

@@ -40,7 +40,7 @@ def main():
     pr.disable()
     dt = time.perf_counter() - t0
     print(f"slice {k}: {r.eigenvalues.size} eigenpairs in {dt:.3f} s; nfb {r.counters.nfb} nit {r.counters.nit}")
-    pstats.Stats(pr).sort_stats("cumulative").print_stats(35)
+    pstats.Stats(pr).sort_stats("cumulative").print_stats(45)
 
 
 if __name__ == "__main__":
