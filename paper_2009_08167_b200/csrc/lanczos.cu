@@ -57,88 +57,93 @@ __device__ __forceinline__ void rows_of(const RowSel& A, const LzDev* st, int64_
 }
 
 // ---- tall-skinny GEMVs of the Gram-Schmidt passes --------------------------
-// dots:   partial[chunk * Rmax + i] = sum_{c in chunk} row_i[c] x[c]
-//         grid (column chunks of kDotCols, row groups of kDotRows); every
-//         lane keeps its 32 x-values in registers and streams 16 double2
-//         per row (a warp reads 512 B contiguous per load).
-// reduce: coef[i] = sum_chunk partial[chunk * Rmax + i]   (fixed order)
+// dots:   partial[chunk * Rmax + i] = sum_{c in chunk} row_i[c] x[c], then
+//         coef[i] = sum_chunk partial (fixed order, by the CTA finishing the
+//         row group's last chunk)
 // update: upart[g][c] = sum_{i in group g} row_i[c] coef[i]  (grid columns x
-//         kUpdGroups), then y[c] -= sum_g upart[g][c]  (fixed order).
+//         kUpdGroups), then y[c] -= sum_g upart[g][c]  (fixed order, by the
+//         last group of the column strip)
 constexpr int kDotCols = 1024;
-constexpr int kDotRows = 32;    // 8 warps x 4 rows
 constexpr int kUpdGroups = 8;
 constexpr int kUpdCols = 512;   // columns per update CTA (2 per thread)
+constexpr int kUpdUnroll = 8;   // row loads in flight per thread
 
 __device__ __forceinline__ const double* sel_row(const RowSel& A, int64_t na, int64_t i) {
   return i < na ? A.V + i * A.ld : A.L + (i - na) * A.ld;
 }
 
-__global__ void __launch_bounds__(256) k_cgs_dots(RowSel A, const LzDev* st, int64_t n, int64_t Rmax,
-                                                  const double* __restrict__ x,
-                                                  double* __restrict__ partial) {
+// dots: warp tiles (row i, column chunk of kDotCols) handed out over a
+// fixed persistent grid (the step graph is captured once; R is read from the
+// device state), chunk-major so the warps of a CTA share their x chunk in
+// L1.  A lane issues its 16 double2 row loads and 16 x loads at once.  The
+// warp finishing the last chunk of a row (per-row ticket) reduces that row's
+// partials in fixed order into coef: no block barriers, no reduce launch.
+constexpr int kDotGrid = 2 * 148;
+__global__ void __launch_bounds__(256, 2) k_cgs_dots(RowSel A, const LzDev* st, int64_t n, int64_t Rmax,
+                                                     const double* __restrict__ x, double* __restrict__ partial,
+                                                     double* __restrict__ coef, unsigned* __restrict__ tickets) {
   if (st->stop) return;
   int64_t na, nb;
   rows_of(A, st, na, nb);
   const int64_t R = na + nb;
-  const int64_t r0 = (int64_t)blockIdx.y * kDotRows;
-  if (r0 >= R) return;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * kDotCols;
-  const bool full = c0 + kDotCols <= n;
-  double2 xv[16];
-#pragma unroll
-  for (int t = 0; t < 16; ++t) {
-    const int64_t c = c0 + 64 * t + 2 * lane;
-    if (full) {
-      xv[t] = *reinterpret_cast<const double2*>(x + c);
-    } else {
-      xv[t].x = c < n ? x[c] : 0.0;
-      xv[t].y = c + 1 < n ? x[c + 1] : 0.0;
-    }
-  }
-#pragma unroll
-  for (int rr = 0; rr < kDotRows / 8; ++rr) {
-    const int64_t i = r0 + w * (kDotRows / 8) + rr;
-    if (i >= R) break;
-    const double* row = sel_row(A, na, i);
+  const int lane = threadIdx.x & 31;
+  const int nchunk = (int)((n + kDotCols - 1) / kDotCols);
+  const int64_t ntiles = (int64_t)nchunk * R;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += nwarps) {
+    const int chunk = (int)(t / R);
+    const int64_t i = t - (int64_t)chunk * R;
+    const int64_t c0 = (int64_t)chunk * kDotCols;
+    const double* row = sel_row(A, na, i) + c0;
     double acc = 0.0;
-    if (full) {
+    if (c0 + kDotCols <= n) {
+      double2 v[16], xv[16];
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const double2 v = __ldcs(reinterpret_cast<const double2*>(row + c0 + 64 * t + 2 * lane));
-        acc = fma(v.x, xv[t].x, acc);
-        acc = fma(v.y, xv[t].y, acc);
+      for (int u = 0; u < 16; ++u) {
+        v[u] = __ldcs(reinterpret_cast<const double2*>(row) + 32 * u + lane);
+        xv[u] = __ldg(reinterpret_cast<const double2*>(x + c0) + 32 * u + lane);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        acc = fma(v[u].x, xv[u].x, acc);
+        acc = fma(v[u].y, xv[u].y, acc);
       }
     } else {
-      for (int t = 0; t < 16; ++t) {
-        const int64_t c = c0 + 64 * t + 2 * lane;
-        if (c < n) acc = fma(row[c], xv[t].x, acc);
-        if (c + 1 < n) acc = fma(row[c + 1], xv[t].y, acc);
+      for (int64_t c = 2 * lane; c0 + c < n; c += 64) {
+        acc = fma(row[c], x[c0 + c], acc);
+        if (c0 + c + 1 < n) acc = fma(row[c + 1], x[c0 + c + 1], acc);
       }
     }
     acc = warp_sum(acc);
-    if (lane == 0) partial[blockIdx.x * Rmax + i] = acc;
+    unsigned done = 0;
+    if (lane == 0) {
+      partial[(int64_t)chunk * Rmax + i] = acc;
+      __threadfence();
+      done = atomicAdd(&tickets[i], 1u);
+    }
+    done = __shfl_sync(0xffffffffu, done, 0);
+    if (done == (unsigned)nchunk - 1) {
+      __threadfence();
+      double v = 0.0;
+      for (int b = lane; b < nchunk; b += 32) v += __ldcg(partial + (int64_t)b * Rmax + i);
+      v = warp_sum(v);
+      if (lane == 0) {
+        coef[i] = v;
+        tickets[i] = 0;
+      }
+    }
   }
 }
 
-__global__ void k_cgs_reduce(RowSel A, const LzDev* st, int nchunk, int64_t Rmax,
-                             const double* __restrict__ partial, double* __restrict__ coef) {
-  if (st->stop) return;
-  int64_t na, nb;
-  rows_of(A, st, na, nb);
-  const int64_t R = na + nb;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= R) return;
-  double s = 0.0;
-  for (int b = 0; b < nchunk; ++b) s += partial[(int64_t)b * Rmax + i];
-  coef[i] = s;
-}
-
-__global__ void __launch_bounds__(256) k_cgs_upd_part(RowSel A, const LzDev* st, int64_t n, int64_t ldu,
-                                                      const double* __restrict__ coef,
-                                                      double* __restrict__ upart) {
+// y[c] -= sum_i row_i[c] coef[i]: CTA (column strip, row group g) writes
+// upart[g]; the last group of a strip to finish sums the kUpdGroups parts
+// in order and updates y (no separate final launch)
+__global__ void __launch_bounds__(256) k_cgs_upd(RowSel A, const LzDev* st, int64_t n, int64_t ldu,
+                                                 const double* __restrict__ coef, double* __restrict__ upart,
+                                                 double* __restrict__ y, unsigned* __restrict__ tickets) {
   if (st->stop) return;
   __shared__ double cs[1024];
+  __shared__ bool last;
   int64_t na, nb;
   rows_of(A, st, na, nb);
   const int64_t R = na + nb;
@@ -148,43 +153,54 @@ __global__ void __launch_bounds__(256) k_cgs_upd_part(RowSel A, const LzDev* st,
   for (int t = threadIdx.x; t < cnt && t < 1024; t += blockDim.x) cs[t] = coef[i0 + t];
   __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * kUpdCols + 2 * threadIdx.x;
-  if (c >= n) return;
+  const bool valid = c < n;
   const bool pair = c + 1 < n;
   double2 acc = make_double2(0.0, 0.0);
-  int t = 0;
-  if (pair) {
-    for (; t + 8 <= cnt; t += 8) {
-      double2 v[8];
+  if (valid) {
+    if (pair) {
+      // kUpdUnroll rows per round trip, the last round predicated (no serial tail)
+      for (int t = 0; t < cnt; t += kUpdUnroll) {
+        double2 v[kUpdUnroll];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(sel_row(A, na, i0 + t + u) + c));
+        for (int u = 0; u < kUpdUnroll; ++u)
+          v[u] = t + u < cnt ? __ldcs(reinterpret_cast<const double2*>(sel_row(A, na, i0 + t + u) + c))
+                             : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double cf = t + u < 1024 ? cs[t + u] : coef[i0 + t + u];
-        acc.x = fma(v[u].x, cf, acc.x);
-        acc.y = fma(v[u].y, cf, acc.y);
+        for (int u = 0; u < kUpdUnroll; ++u) {
+          if (t + u < cnt) {
+            const double cf = t + u < 1024 ? cs[t + u] : coef[i0 + t + u];
+            acc.x = fma(v[u].x, cf, acc.x);
+            acc.y = fma(v[u].y, cf, acc.y);
+          }
+        }
+      }
+    } else {
+      for (int t = 0; t < cnt; ++t) {
+        const double cf = t < 1024 ? cs[t] : coef[i0 + t];
+        acc.x = fma(sel_row(A, na, i0 + t)[c], cf, acc.x);
       }
     }
+    double* dst = upart + (int64_t)blockIdx.y * ldu + c;
+    dst[0] = acc.x;
+    if (pair) dst[1] = acc.y;
   }
-  for (; t < cnt; ++t) {
-    const double* row = sel_row(A, na, i0 + t);
-    const double cf = t < 1024 ? cs[t] : coef[i0 + t];
-    acc.x = fma(row[c], cf, acc.x);
-    if (pair) acc.y = fma(row[c + 1], cf, acc.y);
-  }
-  double* dst = upart + (int64_t)blockIdx.y * ldu + c;
-  dst[0] = acc.x;
-  if (pair) dst[1] = acc.y;
-}
-
-__global__ void k_cgs_upd_final(const LzDev* st, int64_t n, int64_t ldu, const double* __restrict__ upart,
-                                double* __restrict__ y) {
-  if (st->stop) return;
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  double s = 0.0;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (valid) {
+    double sx = 0.0, sy = 0.0;
 #pragma unroll
-  for (int g = 0; g < kUpdGroups; ++g) s += upart[(int64_t)g * ldu + c];
-  y[c] -= s;
+    for (int g = 0; g < kUpdGroups; ++g) {
+      sx += __ldcg(upart + (int64_t)g * ldu + c);
+      if (pair) sy += __ldcg(upart + (int64_t)g * ldu + c + 1);
+    }
+    y[c] -= sx;
+    if (pair) y[c + 1] -= sy;
+  }
+  if (threadIdx.x == 0) tickets[blockIdx.x] = 0;
 }
 
 // out[0] = <a, b>, out[1] = <c, d>; `a` offset by k rows when koff_a != 0
@@ -506,6 +522,7 @@ struct riga_lanczos {
   int64_t n = 0, ld = 0, max_dim = 0, k = 0;
   int64_t nlocked = 0, cap = 0;
   DevBuf<double> V, MV, L, LM, w, r, Mr, bp, coef, partial, upart, cpl, Wd, outs, dscratch;
+  DevBuf<unsigned> tk_dots, tk_upd;  // last-block tickets of the Gram-Schmidt kernels (self-resetting)
   DevBuf<LzDev> st;
   LzDev* hst = nullptr;    // pinned mirror
   double* hbuf = nullptr;  // pinned readback
@@ -551,6 +568,8 @@ int grow_locked(riga_lanczos* lz, int64_t need) {
   const int64_t R = lz->max_dim + 1 + cap;
   RIGA_TRY(lz->coef.alloc(R, s));
   RIGA_TRY(lz->partial.alloc((int64_t)((lz->n + kDotCols - 1) / kDotCols) * R, s));
+  RIGA_TRY(lz->tk_dots.alloc(R, s));
+  RIGA_CUDA(cudaMemsetAsync(lz->tk_dots.p, 0, R * sizeof(unsigned), s));
   drop_graph(lz);
   return RIGA_OK;
 }
@@ -586,22 +605,16 @@ int cgs_passes(riga_lanczos* lz, RowSel dots, RowSel upd, RowSel upd2, double* r
                int passes, int64_t rows_hint) {
   cudaStream_t s = lz->cur;
   const int64_t Rmax = lz->max_dim + 1 + lz->cap;
-  const int nchunk = (int)((lz->n + kDotCols - 1) / kDotCols);
-  const dim3 gd(nchunk, (unsigned)((Rmax + kDotRows - 1) / kDotRows));
   const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
-  const unsigned gf = (unsigned)((lz->n + 255) / 256);
   for (int p = 0; p < passes; ++p) {
     ProfScope prof(kProfCgs, s, 2.0 * (double)rows_hint * lz->n * 8.0);
-    k_cgs_dots<<<gd, 256, 0, s>>>(dots, lz->st.p, lz->n, Rmax, r, lz->partial.p);
-    k_cgs_reduce<<<(unsigned)((Rmax + 255) / 256), 256, 0, s>>>(dots, lz->st.p, nchunk, Rmax, lz->partial.p,
-                                                                lz->coef.p);
-    k_cgs_upd_part<<<gu, 256, 0, s>>>(upd, lz->st.p, lz->n, lz->ld, lz->coef.p, lz->upart.p);
-    k_cgs_upd_final<<<gf, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->upart.p, r);
-    count_launch(4);
+    k_cgs_dots<<<kDotGrid, 256, 0, s>>>(dots, lz->st.p, lz->n, Rmax, r, lz->partial.p, lz->coef.p,
+                                        lz->tk_dots.p);
+    k_cgs_upd<<<gu, 256, 0, s>>>(upd, lz->st.p, lz->n, lz->ld, lz->coef.p, lz->upart.p, r, lz->tk_upd.p);
+    count_launch(2);
     if (r2) {
-      k_cgs_upd_part<<<gu, 256, 0, s>>>(upd2, lz->st.p, lz->n, lz->ld, lz->coef.p, lz->upart.p);
-      k_cgs_upd_final<<<gf, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->upart.p, r2);
-      count_launch(2);
+      k_cgs_upd<<<gu, 256, 0, s>>>(upd2, lz->st.p, lz->n, lz->ld, lz->coef.p, lz->upart.p, r2, lz->tk_upd.p);
+      count_launch();
     }
   }
   RIGA_CUDA(cudaGetLastError());
@@ -663,8 +676,7 @@ int ensure_graph(riga_lanczos* lz) {
   if (lz->gexec && lz->gop == lz->op && lz->gL == lz->L.p && lz->gR == Rmax) return RIGA_OK;
   drop_graph(lz);
   cudaStream_t s = lz->ctx->stream;
-  // first-use allocations and kernel attributes must happen outside the capture
-  riga_factor* F = lz->op;
+  // kernel attributes must be set outside the capture
   RIGA_TRY(prepare_solve());
   RIGA_CUDA(stream_sync(s));
   cudaGraph_t g = nullptr;
@@ -722,6 +734,8 @@ int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max
   RIGA_TRY(lz->Mr.alloc(lz->ld, cs));
   RIGA_TRY(lz->bp.alloc(lz->ld, cs));
   RIGA_TRY(lz->upart.alloc(kUpdGroups * lz->ld, cs));
+  RIGA_TRY(lz->tk_upd.alloc((lz->n + kUpdCols - 1) / kUpdCols, cs));
+  RIGA_CUDA(cudaMemsetAsync(lz->tk_upd.p, 0, ((lz->n + kUpdCols - 1) / kUpdCols) * sizeof(unsigned), cs));
   RIGA_TRY(lz->cpl.alloc(rows, cs));
   RIGA_TRY(lz->outs.alloc(3 * rows, cs));
   RIGA_TRY(lz->dscratch.alloc(2 * 296 + 8, cs));
@@ -1100,13 +1114,10 @@ int riga_lanczos_gram(riga_lanczos* lz, double* G) {
   lz->nlocked = saved;
   const RowSel dots = sel_basis(lz, true, 0);
   const int64_t Rmax = lz->max_dim + 1 + lz->cap;
-  const int nchunk = (int)((lz->n + kDotCols - 1) / kDotCols);
-  const dim3 gd(nchunk, (unsigned)((Rmax + kDotRows - 1) / kDotRows));
   for (int64_t i = 0; i < k; ++i) {
-    k_cgs_dots<<<gd, 256, 0, s>>>(dots, lz->st.p, lz->n, Rmax, lz->V.p + i * lz->ld, lz->partial.p);
-    k_cgs_reduce<<<(unsigned)((Rmax + 255) / 256), 256, 0, s>>>(dots, lz->st.p, nchunk, Rmax, lz->partial.p,
-                                                                lz->coef.p);
-    count_launch(2);
+    k_cgs_dots<<<kDotGrid, 256, 0, s>>>(dots, lz->st.p, lz->n, Rmax, lz->V.p + i * lz->ld, lz->partial.p,
+                                        lz->coef.p, lz->tk_dots.p);
+    count_launch();
     RIGA_CUDA(cudaMemcpyAsync(G + i * k, lz->coef.p, k * 8, cudaMemcpyDeviceToHost, s));
   }
   RIGA_CUDA(stream_sync(s));

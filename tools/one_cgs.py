@@ -1,0 +1,39 @@
+"""Build an m-step Lanczos basis of the middle cfg3 slice, then run
+`--probes` CGS2 probes against it (for ncu of the Gram-Schmidt kernels)."""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2009_08167_b200 as P  # noqa: E402
+from paper_2009_08167_b200 import _lib  # noqa: E402
+from paper_2009_08167_b200.configs import CONFIGS  # noqa: E402
+from paper_2009_08167_b200.eigensolver import DeviceShiftInvert  # noqa: E402
+from paper_2009_08167_b200.sparsela import Symbolic, numeric_factor  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg3")
+ap.add_argument("--m", type=int, default=250)
+ap.add_argument("--probes", type=int, default=3)
+a = ap.parse_args()
+c = CONFIGS[a.config]
+s = P.build_system(c.d, c.ne, c.p, c.level)
+lam_e, _ = P.choose_lambda_e(s, c.n0)
+sh = P.uniform_shifts(lam_e, c.slices)
+sym = Symbolic.on_device(s.device, P.separator_ordering(s))
+f = numeric_factor(sym, float(sh[len(sh) // 2]))
+st = P.LanczosState(DeviceShiftInvert(f, s.M), s.dof_count, mass=s.M, shift=f.sigma, max_dim=a.m + 1,
+                    rng=np.random.default_rng(0))
+P.lanczos_extend(st, a.m)
+x = torch.randn(s.dof_count, dtype=torch.float64, device="cuda")
+rows = ctypes.c_int64(0)
+torch.cuda.synchronize()
+for _ in range(a.probes):
+    _lib.check(_lib.lib().riga_lanczos_cgs_probe(st.handle, _lib.ptr(x), 2, ctypes.byref(rows)))
+torch.cuda.synchronize()
+print("rows", rows.value)
