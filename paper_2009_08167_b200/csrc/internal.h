@@ -6,6 +6,14 @@
 #include "common.h"
 #include "symbolic.h"
 
+// 1D factor of a Kronecker-assembled system (x = axis 0 is fastest)
+struct KronAxis {
+  int64_t n = 0;
+  riga::DevBuf<int64_t> rp;
+  riga::DevBuf<int32_t> ci;
+  riga::DevBuf<double> k, m;
+};
+
 struct riga_system {
   riga::CtxRef ctxref;
   riga_ctx* ctx = nullptr;
@@ -13,6 +21,8 @@ struct riga_system {
   riga::DevBuf<int64_t> rowptr;
   riga::DevBuf<int32_t> colidx;
   riga::DevBuf<double> K, M;
+  int kdim = 0;      // > 0: M = M_z (x) M_y (x) M_x is applied axis by axis
+  KronAxis kax[3];
 };
 
 // Device copy of the symbolic analysis (read-only, shared by all factors).
@@ -110,6 +120,8 @@ namespace riga {
 // kernels shared between translation units
 int launch_dot(cudaStream_t s, int64_t n, const double* x, const double* y, double* out_dev);
 int system_spmv(riga_system* sys, cudaStream_t s, int which, double sigma, const double* x, double* y);
+// y = M x through the 1D factors (kdim > 0); t1, t2: n-vector scratch
+int kron_mass_apply(riga_system* sys, cudaStream_t s, const double* x, double* y, double* t1, double* t2);
 int csr_spmv(cudaStream_t s, int64_t n, const int64_t* rowptr, const int32_t* colidx,
              const double* val, const double* x, double* y);
 int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x,

@@ -523,6 +523,8 @@ struct riga_lanczos {
   int64_t nlocked = 0, cap = 0;
   DevBuf<double> V, MV, L, LM, w, r, Mr, bp, coef, partial, upart, cpl, Wd, outs, dscratch;
   DevBuf<unsigned> tk_dots, tk_upd;  // last-block tickets of the Gram-Schmidt kernels (self-resetting)
+  DevBuf<double> kt1, kt2;           // scratch of the Kronecker mass product
+  bool kron_ok = false;
   DevBuf<LzDev> st;
   LzDev* hst = nullptr;    // pinned mirror
   double* hbuf = nullptr;  // pinned readback
@@ -623,6 +625,7 @@ int cgs_passes(riga_lanczos* lz, RowSel dots, RowSel upd, RowSel upd2, double* r
 
 int mass_apply(riga_lanczos* lz, const double* x, double* y) {
   cudaStream_t s = lz->cur;
+  if (lz->sys && lz->sys->kdim && lz->kron_ok) return kron_mass_apply(lz->sys, s, x, y, lz->kt1.p, lz->kt2.p);
   if (lz->sys) return system_spmv(lz->sys, s, 1, 0.0, x, y);
   RIGA_CUDA(cudaMemcpyAsync(y, x, lz->n * 8, cudaMemcpyDeviceToDevice, s));
   return RIGA_OK;
@@ -741,6 +744,11 @@ int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max
   RIGA_TRY(lz->dscratch.alloc(2 * 296 + 8, cs));
   RIGA_CUDA(cudaMemsetAsync(lz->dscratch.p, 0, (2 * 296 + 8) * 8, cs));
   RIGA_TRY(lz->st.alloc(1, cs));
+  if (mass && mass->kdim && !getenv("RIGA_CSR_MASS")) {
+    RIGA_TRY(lz->kt1.alloc(n, cs));
+    RIGA_TRY(lz->kt2.alloc(n, cs));
+    lz->kron_ok = true;
+  }
   RIGA_CUDA(cudaMemsetAsync(lz->st.p, 0, sizeof(LzDev), cs));
   RIGA_TRY(grow_locked(lz.get(), 16));
   lz->hst = static_cast<LzDev*>(pinned_get(sizeof(LzDev)));

@@ -177,6 +177,41 @@ int system_spmv(riga_system* sys, cudaStream_t s, int which, double sigma, const
 }
 
 // ---------------------------------------------------------------------------
+// Kronecker mass product: M = M_z (x) M_y (x) M_x applied one axis at a time
+// (out[.., i, ..] = sum_j m_axis[i][j] in[.., j, ..]), so a step reads the
+// n-vector a few times instead of the nnz = prod(2 p + 1) n CSR entries.
+// ---------------------------------------------------------------------------
+__global__ void k_kron_axis(int64_t n, int64_t nax, int64_t stride, const int64_t* __restrict__ rp,
+                            const int32_t* __restrict__ ci, const double* __restrict__ m,
+                            const double* __restrict__ in, double* __restrict__ out) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t i = (r / stride) % nax;
+  const int64_t base = r - i * stride;
+  double acc = 0.0;
+  for (int64_t q = rp[i]; q < rp[i + 1]; ++q) acc = fma(m[q], in[base + (int64_t)ci[q] * stride], acc);
+  out[r] = acc;
+}
+
+int kron_mass_apply(riga_system* sys, cudaStream_t s, const double* x, double* y, double* t1, double* t2) {
+  const int d = sys->kdim;
+  const int64_t n = sys->n;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  const double* in = x;
+  int64_t stride = 1;
+  for (int t = 0; t < d; ++t) {
+    double* out = t == d - 1 ? y : (t % 2 == 0 ? t1 : t2);
+    const KronAxis& a = sys->kax[t];
+    k_kron_axis<<<g, 256, 0, s>>>(n, a.n, stride, a.rp.p, a.ci.p, a.m.p, in, out);
+    count_launch();
+    in = out;
+    stride *= a.n;
+  }
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+// ---------------------------------------------------------------------------
 // Dot product, deterministic: per-block partials + last-block final sum.
 // ---------------------------------------------------------------------------
 __global__ void k_dot(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
@@ -451,6 +486,15 @@ int riga_system_assemble_kron(riga_ctx* ctx, int dim, const int64_t* n1,
       dim, ax[0], ax[1], ax[2], n, sys->rowptr.p, sys->colidx.p, sys->K.p, sys->M.p); count_launch();
   RIGA_CUDA(cudaGetLastError());
   RIGA_CUDA(stream_sync(s));
+  // keep the 1D factors: the Lanczos mass products run axis by axis
+  sys->kdim = dim;
+  for (int t = 0; t < dim; ++t) {
+    sys->kax[t].n = n1[t];
+    sys->kax[t].rp.swap(rp[t]);
+    sys->kax[t].ci.swap(ci[t]);
+    sys->kax[t].k.swap(kk[t]);
+    sys->kax[t].m.swap(mm[t]);
+  }
   *out = sys.release();
   return RIGA_OK;
 }
