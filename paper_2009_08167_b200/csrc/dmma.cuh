@@ -95,3 +95,91 @@ __device__ __forceinline__ void dmma_syrk_tile(const double* __restrict__ L, int
 }
 
 }  // namespace riga
+
+namespace riga {
+
+// C(i, j) = alpha * sum_{t in [k0, k1)} A(i, t) B(t, j) for the 64x64 tile at
+// (i0, j0), i < mend, j < nend; A(i, t) = A[t * lda + i] (column-major),
+// B(t, j) = B[j * ldb + t] (column-major, t contiguous); C(i, j) =
+// C[j * ldc + i] is overwritten.  blockDim.x == 128, 4 warps x 32x32.
+__device__ __forceinline__ void dmma_gemm_tile(const double* __restrict__ A, int64_t lda,
+                                               const double* __restrict__ B, int64_t ldb, int64_t k0,
+                                               int64_t k1, int64_t i0, int64_t j0, int64_t mend, int64_t nend,
+                                               double* __restrict__ C, int64_t ldc, double alpha) {
+  __shared__ double As[2][16][72];
+  __shared__ double Bs[2][16][72];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  double ra[8], rb[8];
+  auto load = [&](int64_t kt) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 128 * u;
+      {  // A: 16 k x 64 rows, rows contiguous
+        const int t = idx >> 6, i = idx & 63;
+        const int64_t kk = kt + t;
+        ra[u] = (kk < k1 && i0 + i < mend) ? A[kk * lda + i0 + i] : 0.0;
+      }
+      {  // B: 64 cols x 16 k, k contiguous
+        const int t = idx & 15, j = idx >> 4;
+        const int64_t kk = kt + t;
+        rb[u] = (kk < k1 && j0 + j < nend) ? B[(j0 + j) * ldb + kk] : 0.0;
+      }
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 128 * u;
+      As[buf][idx >> 6][idx & 63] = ra[u];
+      Bs[buf][idx & 15][idx >> 4] = rb[u];
+    }
+  };
+  int buf = 0;
+  if (k0 < k1) {
+    load(k0);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t kt = k0; kt < k1; kt += 16) {
+    const bool more = kt + 16 < k1;
+    if (more) load(kt + 16);
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const int kr = k4 * 4 + (lane & 3);
+      double av[4], bv[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) av[m] = As[buf][kr][wm * 32 + m * 8 + (lane >> 2)];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bv[q] = Bs[buf][kr][wn * 32 + q * 8 + (lane >> 2)];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[m][q][0], acc[m][q][1], av[m], bv[q]);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  const int r = lane >> 2, cc = (lane & 3) * 2;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int64_t i = i0 + wm * 32 + m * 8 + r;
+    if (i >= mend) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t j = j0 + wn * 32 + q * 8 + cc;
+      if (j < nend) C[j * ldc + i] = alpha * acc[m][q][0];
+      if (j + 1 < nend) C[(j + 1) * ldc + i] = alpha * acc[m][q][1];
+    }
+  }
+}
+
+}  // namespace riga

@@ -12,10 +12,14 @@
 //     k_small_front  one CTA per front with f <= kSmallFront: the whole front
 //                    (originals + children) in shared memory, dense LDL^T of
 //                    the pivot block, Schur complement written back
-//     large fronts   right-looking blocked LDL^T in HBM: k_panel (diagonal
-//                    block + L21 rows), k_syrk<0> (trailing panel update)
-//                    and k_syrk<1> (update block -= L21 D L21^T, K = n_p),
-//                    both on FP64 tensor cores (mma.sync m8n8k4 -> DMMA)
+//     large fronts   right-looking blocked LDL^T in HBM, two-level: outer
+//                    blocks of kNBO = 128 pivot columns, each factored 32
+//                    at a time (k_panel: diagonal block + L21 rows;
+//                    k_syrk<0>: rank-32 update inside the outer block), then
+//                    one rank-128 update of the trailing pivot columns
+//                    (k_syrk<2>) and finally update block -= L21 D L21^T
+//                    (k_syrk<1>, K = n_p), all on FP64 tensor cores
+//                    (mma.sync m8n8k4 -> DMMA)
 // Inertia = count of negative pivots (integer atomics, order independent).
 #include <algorithm>
 #include <cstring>
@@ -28,6 +32,7 @@
 namespace riga {
 
 constexpr int kNB = 32;         // panel block width of the large-front path
+constexpr int kNBO = 128;       // outer block: trailing updates run as rank-kNBO DMMA GEMMs
 constexpr int kPanelRows = 128;  // rows per CTA in k_panel
 
 // ---------------------------------------------------------------------------
@@ -256,11 +261,13 @@ __global__ void __launch_bounds__(kPanelRows) k_panel(SymDev S, const int32_t* _
   }
 }
 
-// Trailing update on FP64 tensor cores:
-//   MODE 0: panel columns [kb+nbk, np), rows [kb+nbk, f), K = [kb, kb+nbk)
-//   MODE 1: update block rows/cols [np, f) (stored separately), K = [0, np)
+// Trailing updates on FP64 tensor cores (rows always run to f):
+// MODE 0: rank-nbk update of the panel-block columns [kq + nbk, min(kbo + kNBO, np))
+//         by panel columns [kq, kq + nbk)              (inside an outer block)
+// MODE 1: update block -= L21 D L21^T, K = np
+// MODE 2: trailing pivot columns [kbo + kNBO, np) by the outer block's kNBO columns
 template <int MODE>
-__global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restrict__ nodes, int kb,
+__global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restrict__ nodes, int kq, int kbo,
                                               double* __restrict__ panel,
                                               double* __restrict__ cb,
                                               const double* __restrict__ D) {
@@ -268,13 +275,19 @@ __global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restric
   const int64_t f = S.front[s], np = S.ncol[s];
   int64_t m0, nend, k0, k1;
   if (MODE == 0) {
-    if (kb >= np) return;
-    int64_t nbk = imin(kNB, np - kb);
-    m0 = kb + nbk;
-    if (m0 >= np) return;
+    if (kq >= np) return;
+    int64_t nbk = imin(kNB, np - kq);
+    m0 = kq + nbk;
+    nend = imin((int64_t)kbo + kNBO, np);
+    if (m0 >= nend) return;
+    k0 = kq;
+    k1 = kq + nbk;
+  } else if (MODE == 2) {
+    k0 = kbo;
+    k1 = imin((int64_t)kbo + kNBO, np);
+    m0 = k1;
     nend = np;
-    k0 = kb;
-    k1 = kb + nbk;
+    if (k0 >= np || m0 >= np) return;
   } else {
     if (np >= f) return;
     m0 = np;
@@ -291,7 +304,7 @@ __global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restric
   const double* Dk = D + S.col0[s];
   double* C;
   int64_t ldc, coff;
-  if (MODE == 0) {
+  if (MODE != 1) {
     C = panel + S.panel_off[s];
     ldc = f;
     coff = 0;
@@ -462,22 +475,33 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
     if (P.nlarge) {
       const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
       unsigned nl = (unsigned)P.nlarge;
-      for (int64_t kb = 0; kb < P.max_np_large; kb += kNB) {
-        unsigned rchunks = (unsigned)std::max<int64_t>(1, (P.max_f_large - kb + kPanelRows - 1) / kPanelRows);
-        k_panel<<<dim3(rchunks, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p,
-                                                          F->D.p, F->stat.p); count_launch();
-        RIGA_CUDA(cudaGetLastError());
-        int64_t m0 = kb + kNB;
+      for (int64_t kbo = 0; kbo < P.max_np_large; kbo += kNBO) {
+        // factor the outer block's columns 32 at a time (panel + in-block update)
+        for (int64_t kb = kbo; kb < std::min<int64_t>(kbo + kNBO, P.max_np_large); kb += kNB) {
+          unsigned rchunks = (unsigned)std::max<int64_t>(1, (P.max_f_large - kb + kPanelRows - 1) / kPanelRows);
+          k_panel<<<dim3(rchunks, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p,
+                                                            F->D.p, F->stat.p); count_launch();
+          RIGA_CUDA(cudaGetLastError());
+          int64_t m0 = kb + kNB, nend = std::min<int64_t>(kbo + kNBO, P.max_np_large);
+          if (m0 < nend) {
+            int64_t ntj = (nend - m0 + 63) / 64, nti = (P.max_f_large - m0 + 63) / 64;
+            k_syrk<0><<<dim3((unsigned)(ntj * nti), nl), 128, 0, st>>>(S, ln, (int)kb, (int)kbo, F->panel.p,
+                                                                      cbuf, F->D.p); count_launch();
+            RIGA_CUDA(cudaGetLastError());
+          }
+        }
+        // trailing pivot columns: one rank-kNBO update
+        int64_t m0 = kbo + kNBO;
         if (m0 < P.max_np_large) {
           int64_t ntj = (P.max_np_large - m0 + 63) / 64, nti = (P.max_f_large - m0 + 63) / 64;
-          k_syrk<0><<<dim3((unsigned)(ntj * nti), nl), 128, 0, st>>>(S, ln, (int)kb, F->panel.p,
-                                                                    cbuf, F->D.p); count_launch();
+          k_syrk<2><<<dim3((unsigned)(ntj * nti), nl), 128, 0, st>>>(S, ln, 0, (int)kbo, F->panel.p, cbuf,
+                                                                    F->D.p); count_launch();
           RIGA_CUDA(cudaGetLastError());
         }
       }
       if (P.max_nu_large > 0) {
         int64_t t = (P.max_nu_large + 63) / 64;
-        k_syrk<1><<<dim3((unsigned)(t * t), nl), 128, 0, st>>>(S, ln, 0, F->panel.p, cbuf, F->D.p); count_launch();
+        k_syrk<1><<<dim3((unsigned)(t * t), nl), 128, 0, st>>>(S, ln, 0, 0, F->panel.p, cbuf, F->D.p); count_launch();
         RIGA_CUDA(cudaGetLastError());
       }
     }

@@ -57,7 +57,10 @@ struct SolvePlanHost {
   std::vector<I2> gfwd, gbwd;          // G warp tasks: (supernode, row tile) / (supernode, column group)
   int64_t inv_total = 0;               // doubles of the inv(L11) blocks of the chain supernodes
   std::vector<int64_t> inv_off;        // per supernode offset into linv (-1: none)
-  std::vector<I2> ifwd, ibwd, idiag, icol;  // (supernode, 32-row tile / 8-row group / 32-col block)
+  std::vector<I2> ifwd, ibwd, idiag;  // (supernode, 32-row tile / 8-row group / 32-col block)
+  std::vector<I2> dbl_tasks;            // doubling inversion pairs (supernode, q), by level
+  std::vector<int64_t> dbl_ptr, dbl_size, dbl_tiles, dbl_toff;
+  int64_t dbl_tmax = 0;                 // doubles of T scratch (largest level)
   std::vector<int64_t> ifwd_ptr, ibwd_ptr, ifwd_smem;
   std::vector<I2> fwd, bwd;        // light tasks grouped by level
   std::vector<int32_t> chains;     // large supernodes grouped by level
@@ -90,7 +93,8 @@ struct riga_symbolic {
   riga::DevBuf<I2> d_tfwd, d_tbwd;
   riga::DevBuf<int32_t> d_chains, d_wholes, d_gsrc, d_sub_fptr, d_sub_bptr;
   riga::DevBuf<int64_t> d_gptr, d_inv_off, d_g_off;
-  riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_icol, d_gfwd, d_gbwd, d_sub_ftiles, d_sub_btiles;
+  riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_dbl_tasks, d_gfwd, d_gbwd, d_sub_ftiles, d_sub_btiles;
+  riga::DevBuf<int64_t> d_dbl_toff;
   SymDev dev() const {
     return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,
                   d_cb_off.p,   d_upd_off.p,   d_child_ptr.p,  d_asm_ptr.p,    d_sparent.p,

@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "dmma.cuh"
 #include "kernels.cuh"
 #include "prof.h"
 
@@ -733,7 +734,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_chain_bwd(SymDev S, const int
 // chain supernodes through the explicit inverse of their pivot block
 //
 // The pivot block L11 (np x np, unit lower) of every large supernode is
-// inverted once per factorisation (k_trinv_diag / k_trinv_cols, part of the
+// inverted once per factorisation (k_trinv_diag + doubling GEMMs, part of the
 // numeric factorisation), so the dependent 32-column chain of the solve
 // becomes two parallel triangular mat-vecs:
 //     forward   z  = inv(L11) y1                 (k_inv_fwd, 32-row tiles)
@@ -769,46 +770,46 @@ __global__ void __launch_bounds__(256) k_trinv_diag(SymDev S, const int2* __rest
   }
 }
 
-// one CTA per (supernode, 32-column block b): X(:, b) below the diagonal,
-// block row by block row, X_ib = -inv(L_ii) sum_{b<=k<i} L_ik X_kb
-__global__ void __launch_bounds__(256) k_trinv_cols(SymDev S, const int2* __restrict__ tasks,
-                                                    const double* __restrict__ panel,
-                                                    const int64_t* __restrict__ inv_off, double* linv) {
-  __shared__ double Ts[32][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int s = tasks[blockIdx.x].x;
-  const int f = (int)S.front[s], np = (int)S.ncol[s];
-  const int j0 = 32 * tasks[blockIdx.x].y;
-  const double* P = panel + S.panel_off[s];
-  double* X = linv + inv_off[s];  // plain (coherent) loads: this CTA reads what it wrote
-  const int c0 = 4 * w;           // this warp's 4 columns of the block
-  for (int i0 = j0 + 32; i0 < np; i0 += 32) {
-    const int nbi = min(32, np - i0);
-    const bool in = lane < nbi;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    const double* Lr = P + i0 + lane;
-    for (int k = j0; k < i0; ++k) {
-      const double l = in ? Lr[(int64_t)k * f] : 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = fma(l, X[(int64_t)(j0 + c0 + q) * np + k], acc[q]);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) Ts[lane][c0 + q] = acc[q];
-    __syncthreads();
-    double o[4] = {0.0, 0.0, 0.0, 0.0};
-    const double* Xi = X + (int64_t)i0 * np + i0 + lane;  // inv(L_ii)(lane, m) at Xi[m * np]
-    for (int m = 0; m < nbi; ++m) {
-      const double a = in ? Xi[(int64_t)m * np] : 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) o[q] = fma(a, Ts[m][c0 + q], o[q]);
-    }
-    if (in) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (j0 + c0 + q < np) X[(int64_t)(j0 + c0 + q) * np + i0 + lane] = -o[q];
-    }
-    __syncthreads();
-  }
+// Doubling: with inv(A) and inv(C) of two adjacent diagonal blocks of size
+// s (A = [a0, a0+s), C = [c0, c0+sc), c0 = a0 + s) known,
+//     inv([A 0; B C]) = [inv(A) 0; -inv(C) B inv(A)  inv(C)],
+// so level s (s = 32, 64, 128, ...) fills every off-diagonal block X21 with
+// two batched DMMA GEMMs: T = B inv(A) (K range skips inv(A)'s zero upper
+// part), then X21 = -inv(C) T (K range stops at the tile's last row).
+// Task (supernode, q): the pair starting at a0 = 2 q s.
+__global__ void __launch_bounds__(128) k_trinv_gemm1(SymDev S, const int2* __restrict__ tasks, int sz,
+                                                     const double* __restrict__ panel,
+                                                     const int64_t* __restrict__ inv_off,
+                                                     const int64_t* __restrict__ t_off, const double* linv,
+                                                     double* tbuf) {
+  const int2 task = tasks[blockIdx.y];
+  const int s = task.x;
+  const int64_t f = S.front[s], np = S.ncol[s];
+  const int64_t a0 = 2 * (int64_t)task.y * sz, c0 = a0 + sz, sc = imin(sz, np - c0);
+  const int64_t nti = (sc + 63) / 64, ntj = (sz + 63) / 64;
+  if (blockIdx.x >= nti * ntj) return;
+  const int64_t i0 = 64 * (blockIdx.x % nti), j0 = 64 * (blockIdx.x / nti);
+  const double* B = panel + S.panel_off[s] + a0 * f + c0;   // B(i, t) = L(c0 + i, a0 + t)
+  const double* Ai = linv + inv_off[s] + a0 * np + a0;      // inv(A)(t, j) at [j np + t]
+  double* T = tbuf + t_off[blockIdx.y];                      // T(i, j) at [j sc + i]
+  dmma_gemm_tile(B, f, Ai, np, j0, sz, i0, j0, sc, sz, T, sc, 1.0);
+}
+
+__global__ void __launch_bounds__(128) k_trinv_gemm2(SymDev S, const int2* __restrict__ tasks, int sz,
+                                                     const int64_t* __restrict__ inv_off,
+                                                     const int64_t* __restrict__ t_off, const double* tbuf,
+                                                     double* linv) {
+  const int2 task = tasks[blockIdx.y];
+  const int s = task.x;
+  const int64_t np = S.ncol[s];
+  const int64_t a0 = 2 * (int64_t)task.y * sz, c0 = a0 + sz, sc = imin(sz, np - c0);
+  const int64_t nti = (sc + 63) / 64, ntj = (sz + 63) / 64;
+  if (blockIdx.x >= nti * ntj) return;
+  const int64_t i0 = 64 * (blockIdx.x % nti), j0 = 64 * (blockIdx.x / nti);
+  double* X = linv + inv_off[s];
+  const double* Ci = X + c0 * np + c0;   // inv(C)(i, t) at [t np + i]
+  const double* T = tbuf + t_off[blockIdx.y];  // T(t, j) at [j sc + t]
+  dmma_gemm_tile(Ci, np, T, sc, 0, imin(i0 + 64, sc), i0, j0, sc, sz, X + a0 * np + c0, np, -1.0);
 }
 
 // forward: task (s, t) -> z rows [32t, 32t + 32) of supernode s
@@ -985,7 +986,6 @@ int build_solve_plan(riga_symbolic* sym) {
         for (int64_t t = 0; t < nblk; ++t) {
           L.ifwd.push_back({s, (int32_t)t});
           L.idiag.push_back({s, (int32_t)t});
-          if (t + 1 < nblk) L.icol.push_back({s, (int32_t)t});
         }
         for (int64_t g = 0; g < (np + 7) / 8; ++g) L.ibwd.push_back({s, (int32_t)g});
         L.ifwd_smem[l] = std::max<int64_t>(L.ifwd_smem[l], np * 8);
@@ -1047,12 +1047,31 @@ int build_solve_plan(riga_symbolic* sym) {
     L.chf_smem[l] = scf * 8;
     L.chb_smem[l] = scb * 8;
   }
-  // column-block inversion tasks: most work (leftmost blocks of the largest
-  // pivot blocks) first
-  std::stable_sort(L.icol.begin(), L.icol.end(), [&](const I2& a, const I2& b) {
-    const int64_t wa = (h.ncol[a.x] + 31) / 32 - a.y, wb = (h.ncol[b.x] + 31) / 32 - b.y;
-    return wa > wb;
-  });
+  // doubling levels of the pivot-block inversions: level l pairs adjacent
+  // diagonal blocks of size 32 << l; T scratch offsets per task
+  for (int64_t sz = 32, lev = 0;; sz *= 2, ++lev) {
+    std::vector<I2> tk;
+    std::vector<int64_t> toff;
+    int64_t tt = 0, maxt = 0;
+    for (int32_t s : L.chains) {
+      const int64_t np = h.ncol[s];
+      for (int64_t q = 0; 2 * q * sz + sz < np; ++q) {
+        const int64_t sc = std::min<int64_t>(sz, np - (2 * q * sz + sz));
+        tk.push_back({s, (int32_t)q});
+        toff.push_back(tt);
+        tt += sc * sz;
+        maxt = std::max<int64_t>(maxt, ((sc + 63) / 64) * ((sz + 63) / 64));
+      }
+    }
+    if (tk.empty()) break;
+    L.dbl_size.push_back(sz);
+    L.dbl_ptr.push_back((int64_t)L.dbl_tasks.size());
+    L.dbl_tiles.push_back(maxt);
+    L.dbl_tasks.insert(L.dbl_tasks.end(), tk.begin(), tk.end());
+    L.dbl_toff.insert(L.dbl_toff.end(), toff.begin(), toff.end());
+    L.dbl_tmax = std::max(L.dbl_tmax, tt);
+  }
+  L.dbl_ptr.push_back((int64_t)L.dbl_tasks.size());
   // pull map: front position -> sources in the update-vector buffer
   const int64_t nfront = h.rows_off[ns];
   std::vector<int64_t> cnt(nfront + 1, 0);
@@ -1098,7 +1117,10 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
     RIGA_TRY(sym->d_ifwd.upload(L.ifwd.data(), L.ifwd.size(), s));
     RIGA_TRY(sym->d_ibwd.upload(L.ibwd.data(), L.ibwd.size(), s));
     RIGA_TRY(sym->d_idiag.upload(L.idiag.data(), L.idiag.size(), s));
-    if (!L.icol.empty()) RIGA_TRY(sym->d_icol.upload(L.icol.data(), L.icol.size(), s));
+    if (!L.dbl_tasks.empty()) {
+      RIGA_TRY(sym->d_dbl_tasks.upload(L.dbl_tasks.data(), L.dbl_tasks.size(), s));
+      RIGA_TRY(sym->d_dbl_toff.upload(L.dbl_toff.data(), L.dbl_toff.size(), s));
+    }
   }
   if (L.gsrc.empty())
     RIGA_TRY(sym->d_gsrc.alloc(1, s));
@@ -1157,14 +1179,25 @@ int build_chain_inverse(riga_factor* F, cudaStream_t st) {
   }
   if (!L.chain_inv || !L.inv_total) return RIGA_OK;
   if (!F->linv.p) RIGA_TRY(F->linv.alloc(L.inv_total, st));
+  // the doubling GEMMs read whole diagonal blocks: the upper triangles must be zero
+  RIGA_CUDA(cudaMemsetAsync(F->linv.p, 0, L.inv_total * sizeof(double), st));
   const int nd = (int)L.idiag.size();
   k_trinv_diag<<<(nd + 7) / 8, 256, 0, st>>>(S, reinterpret_cast<const int2*>(sym->d_idiag.p), nd, F->panel.p,
                                              sym->d_inv_off.p, F->linv.p);
   count_launch();
-  if (!L.icol.empty()) {
-    k_trinv_cols<<<(unsigned)L.icol.size(), 256, 0, st>>>(S, reinterpret_cast<const int2*>(sym->d_icol.p),
-                                                          F->panel.p, sym->d_inv_off.p, F->linv.p);
-    count_launch();
+  if (!L.dbl_tasks.empty()) {
+    DevBuf<double> tbuf;
+    RIGA_TRY(tbuf.alloc(std::max<int64_t>(L.dbl_tmax, 1), st));
+    const int2* dt = reinterpret_cast<const int2*>(sym->d_dbl_tasks.p);
+    for (size_t l = 0; l < L.dbl_size.size(); ++l) {
+      const int64_t t0 = L.dbl_ptr[l], nt = L.dbl_ptr[l + 1] - t0;
+      const dim3 g((unsigned)L.dbl_tiles[l], (unsigned)nt);
+      k_trinv_gemm1<<<g, 128, 0, st>>>(S, dt + t0, (int)L.dbl_size[l], F->panel.p, sym->d_inv_off.p,
+                                       sym->d_dbl_toff.p + t0, F->linv.p, tbuf.p);
+      k_trinv_gemm2<<<g, 128, 0, st>>>(S, dt + t0, (int)L.dbl_size[l], sym->d_inv_off.p, sym->d_dbl_toff.p + t0,
+                                       tbuf.p, F->linv.p);
+      count_launch(2);
+    }
   }
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
