@@ -21,6 +21,36 @@ __global__ void dmma_loop(double* out, int iters) {
   if (s == 12345.0) out[threadIdx.x] = s;
 }
 
+// sm_90+ f64 shapes: m16n8k4 (A 2, B 1, C 4 doubles per lane), m16n8k16 (A 8, B 4, C 4)
+__global__ void dmma16_loop(double* out, int iters, int kind) {
+  double a[8], b[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = 1.0 + (threadIdx.x + i) * 1e-9;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = 1.0 - (threadIdx.x + i) * 1e-9;
+  double c[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (kind == 0) {
+        asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3]) : "d"(a[0]), "d"(a[1]), "d"(b[0]));
+      } else {
+        asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                     : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                       "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
 __global__ void dfma_loop(double* out, int iters) {
   double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
   double c[8];
@@ -55,6 +85,20 @@ int main() {
       cudaEventElapsedTime(&ms, e0, e1);
       flops = 2.0 * sms * threads * (double)iters * 8 * 2.0;
       if (rep) printf("DFMA warps/CTA=%d: %.2f TFLOP/s (%.3f ms)\n", warps, flops / ms / 1e9, ms);
+    }
+  }
+  for (int kind = 0; kind < 2; ++kind) {
+    for (int warps = 4; warps <= 16; warps *= 2) {
+      int threads = warps * 32, iters = kind ? 4000 : 20000;
+      float ms = 0;
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(e0);
+        dmma16_loop<<<sms * 2, threads>>>(out, iters, kind);
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+      }
+      double flops = 2.0 * sms * threads / 32 * (double)iters * 4 * (kind ? 16.0 * 8 * 16 * 2 : 16.0 * 8 * 4 * 2);
+      printf("%s warps/CTA=%d: %.2f TFLOP/s\n", kind ? "m16n8k16" : "m16n8k4", warps, flops / ms / 1e9);
     }
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
