@@ -184,6 +184,14 @@ __global__ void __launch_bounds__(256) k_small_front(SymDev S, const int32_t* __
 // Large fronts, panel step kb: factor the diagonal block [kb, kb+nbk) (one
 // warp, redundantly per CTA) and turn the rows below it into L.
 // ---------------------------------------------------------------------------
+// Panel step of a large front, in two launches so no CTA reads the diagonal
+// block while another overwrites it with its factor:
+//   ROWS = false: one CTA per front factors the nbk x nbk diagonal block
+//                 (unblocked LDL^T by warp 0, lane = row) and writes L_dd, D
+//                 and the inertia / zero-pivot counters;
+//   ROWS = true:  kPanelRows rows per CTA: L21 = A21 L_dd^{-T} D^{-1} from the
+//                 factored L_dd and D written by the first launch.
+template <bool ROWS>
 __global__ void __launch_bounds__(kPanelRows) k_panel(SymDev S, const int32_t* __restrict__ nodes,
                                                       int kb, const double* __restrict__ tol,
                                                       double* __restrict__ panel,
@@ -195,34 +203,31 @@ __global__ void __launch_bounds__(kPanelRows) k_panel(SymDev S, const int32_t* _
   const int64_t f = S.front[s], np = S.ncol[s];
   if (kb >= np) return;
   const int nbk = (int)imin(kNB, np - kb);
-  const int64_t rbeg = kb + nbk + (int64_t)blockIdx.x * kPanelRows;
-  const bool writer = blockIdx.x == 0;
-  if (!writer && rbeg >= f) return;
+  const int64_t col0 = S.col0[s];
   double* P = panel + S.panel_off[s];
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int idx = tid; idx < kNB * kNB; idx += blockDim.x) {
-    int c = idx / kNB, r = idx % kNB;
-    Ld[c][r] = (c < nbk && r < nbk && r >= c) ? P[(kb + c) * f + kb + r] : 0.0;
-  }
-  __syncthreads();
-  if (tid < 32) {  // unblocked LDL^T of the diagonal block by warp 0; lane = row
-    for (int k = 0; k < nbk; ++k) {
-      double d = Ld[k][k];
-      double ci = Ld[k][lane];
-      double li = ci / d;
-      __syncwarp();
-      if (lane > k && lane < nbk) {
-        for (int j = k + 1; j <= lane; ++j) Ld[j][lane] -= li * Ld[k][j];
-      }
-      __syncwarp();
-      if (lane > k && lane < nbk) Ld[k][lane] = li;
-      __syncwarp();
+  if (!ROWS) {
+    for (int idx = tid; idx < kNB * kNB; idx += blockDim.x) {
+      int c = idx / kNB, r = idx % kNB;
+      Ld[c][r] = (c < nbk && r < nbk && r >= c) ? P[(kb + c) * f + kb + r] : 0.0;
     }
-    if (lane < nbk) dd[lane] = Ld[lane][lane];
-  }
-  __syncthreads();
-  if (writer) {
-    const int64_t col0 = S.col0[s];
+    __syncthreads();
+    if (tid < 32) {  // unblocked LDL^T of the diagonal block by warp 0; lane = row
+      for (int k = 0; k < nbk; ++k) {
+        double d = Ld[k][k];
+        double ci = Ld[k][lane];
+        double li = ci / d;
+        __syncwarp();
+        if (lane > k && lane < nbk) {
+          for (int j = k + 1; j <= lane; ++j) Ld[j][lane] -= li * Ld[k][j];
+        }
+        __syncwarp();
+        if (lane > k && lane < nbk) Ld[k][lane] = li;
+        __syncwarp();
+      }
+      if (lane < nbk) dd[lane] = Ld[lane][lane];
+    }
+    __syncthreads();
     for (int idx = tid; idx < nbk * nbk; idx += blockDim.x) {
       int c = idx / nbk, r = idx % nbk;
       if (r >= c) P[(kb + c) * f + kb + r] = Ld[c][r];
@@ -240,7 +245,16 @@ __global__ void __launch_bounds__(kPanelRows) k_panel(SymDev S, const int32_t* _
       if (neg) atomicAdd((unsigned long long*)&stat[0], (unsigned long long)neg);
       if (bad != INT64_MAX) atomicMin((long long*)&stat[1], (long long)bad);
     }
+    return;
   }
+  const int64_t rbeg = kb + nbk + (int64_t)blockIdx.x * kPanelRows;
+  if (rbeg >= f) return;
+  for (int idx = tid; idx < kNB * kNB; idx += blockDim.x) {
+    int c = idx / kNB, r = idx % kNB;
+    Ld[c][r] = (c < nbk && r < nbk && r > c) ? P[(kb + c) * f + kb + r] : 0.0;
+  }
+  if (tid < kNB) dd[tid] = tid < nbk ? D[col0 + kb + tid] : 1.0;
+  __syncthreads();
   const int64_t r = rbeg + tid;
   if (r < f) {
     double x[kNB];
@@ -414,6 +428,14 @@ static int upload_symbolic(riga_symbolic* sym) {
   return RIGA_OK;
 }
 
+__global__ void k_zero_cb(SymDev S, const int32_t* __restrict__ nodes, double* __restrict__ cb) {
+  const int s = nodes[blockIdx.y];
+  const int64_t nu = S.front[s] - S.ncol[s], len = nu * nu;
+  double* c = cb + S.cb_off[s];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    c[i] = 0.0;
+}
+
 static int set_smem_attrs() {
   static bool done = false;
   if (done) return RIGA_OK;
@@ -446,7 +468,6 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   double* cbuf = nullptr;
   if (h.cb_total) RIGA_CUDA(cudaMallocAsync(&cbuf, h.cb_total * sizeof(double), st));
   if (h.panel_large) RIGA_CUDA(cudaMemsetAsync(F->panel.p, 0, h.panel_large * 8, st));
-  if (h.cb_large) RIGA_CUDA(cudaMemsetAsync(cbuf, 0, h.cb_large * 8, st));
   if (sym->n_large) {
     k_asm_large<<<(unsigned)sym->n_large, 256, 0, st>>>(S, sym->d_large_nodes.p, Kv, Mv, sigma,
                                                         F->panel.p); count_launch();
@@ -454,6 +475,11 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   }
   for (int64_t l = 0; l < h.nlevels; ++l) {
     const LevelPlan& P = sym->plan[l];
+    if (P.nlarge && P.max_nu_large > 0) {  // large fronts accumulate into their (reused) update blocks
+      const unsigned gx = (unsigned)std::min<int64_t>(256, (P.max_nu_large * P.max_nu_large + 1023) / 1024);
+      k_zero_cb<<<dim3(gx, (unsigned)P.nlarge), 256, 0, st>>>(S, sym->d_level_nodes.p + P.begin + P.nsmall, cbuf);
+      count_launch();
+    }
     for (size_t r = 0; r + 1 < P.ea_round_begin.size(); ++r) {
       int64_t cnt = P.ea_round_begin[r + 1] - P.ea_round_begin[r];
       if (!cnt) continue;
@@ -479,8 +505,11 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
         // factor the outer block's columns 32 at a time (panel + in-block update)
         for (int64_t kb = kbo; kb < std::min<int64_t>(kbo + kNBO, P.max_np_large); kb += kNB) {
           unsigned rchunks = (unsigned)std::max<int64_t>(1, (P.max_f_large - kb + kPanelRows - 1) / kPanelRows);
-          k_panel<<<dim3(rchunks, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p,
-                                                            F->D.p, F->stat.p); count_launch();
+          k_panel<false><<<dim3(1, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p, F->D.p,
+                                                             F->stat.p);
+          k_panel<true><<<dim3(rchunks, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p,
+                                                                  F->D.p, F->stat.p);
+          count_launch(2);
           RIGA_CUDA(cudaGetLastError());
           int64_t m0 = kb + kNB, nend = std::min<int64_t>(kbo + kNBO, P.max_np_large);
           if (m0 < nend) {

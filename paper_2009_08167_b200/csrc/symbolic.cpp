@@ -18,6 +18,7 @@
 #include "symbolic.h"
 
 #include <algorithm>
+#include <map>
 #include <numeric>
 #include <string>
 
@@ -298,13 +299,9 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
       int64_t f = S.front[s], np = S.ncol[s], nu = f - np;
       S.panel_off[s] = S.panel_total;
       S.panel_total += (f * np + 1) & ~int64_t(1);  // 16-byte aligned panels (TMA bulk copies)
-      S.cb_off[s] = S.cb_total;
-      S.cb_total += nu * nu;
+      (void)nu;
     }
-    if (pass == 0) {
-      S.panel_large = S.panel_total;
-      S.cb_large = S.cb_total;
-    }
+    if (pass == 0) S.panel_large = S.panel_total;
   }
   for (int64_t s = 0; s < ns; ++s) {
     int64_t f = S.front[s], np = S.ncol[s], nu = f - np;
@@ -396,6 +393,65 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
     for (auto it = b; it != e; ++it)
       if (S.front[*it] <= kSmallFront) cnt++;
     S.level_nsmall[l] = cnt;
+  }
+  // ---- 5f. update-block memory plan ------------------------------------------
+  // A front's update block is written at its own level and consumed (extend-
+  // add) at its parent's level, so it is live on [level(s), level(parent)].
+  // First-fit offsets over that liveness: cb_total is the high-water mark, not
+  // the sum of all update blocks (cfg5: 26 GB summed).
+  {
+    std::map<int64_t, int64_t> freel;  // offset -> length of free gaps below the top
+    int64_t top = 0;
+    auto take = [&](int64_t need) {
+      for (auto it = freel.begin(); it != freel.end(); ++it) {
+        if (it->second >= need) {
+          const int64_t off = it->first, rest = it->second - need;
+          freel.erase(it);
+          if (rest) freel[off + need] = rest;
+          return off;
+        }
+      }
+      const int64_t off = top;
+      top += need;
+      return off;
+    };
+    auto give = [&](int64_t off, int64_t len) {
+      auto it = freel.emplace(off, len).first;
+      auto nx = std::next(it);
+      if (nx != freel.end() && it->first + it->second == nx->first) {
+        it->second += nx->second;
+        freel.erase(nx);
+      }
+      if (it != freel.begin()) {
+        auto pv = std::prev(it);
+        if (pv->first + pv->second == it->first) {
+          pv->second += it->second;
+          freel.erase(it);
+          it = pv;
+        }
+      }
+      if (it->first + it->second == top) {
+        top = it->first;
+        freel.erase(it);
+      }
+    };
+    std::vector<std::vector<int32_t>> consumed(S.nlevels);
+    for (int64_t l = 0; l < S.nlevels; ++l) {
+      for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
+        const int32_t s = S.level_nodes[q];
+        const int64_t nu = S.front[s] - S.ncol[s];
+        S.cb_off[s] = 0;
+        if (nu <= 0) continue;
+        S.cb_off[s] = take((nu * nu + 1) & ~int64_t(1));
+        if (S.sparent[s] >= 0) consumed[S.level[S.sparent[s]]].push_back(s);
+      }
+      S.cb_total = std::max(S.cb_total, top);
+      for (int32_t c : consumed[l]) {
+        const int64_t nu = S.front[c] - S.ncol[c];
+        give(S.cb_off[c], (nu * nu + 1) & ~int64_t(1));
+      }
+    }
+    S.cb_large = 0;
   }
   return 0;
 }

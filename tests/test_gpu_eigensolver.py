@@ -232,3 +232,49 @@ def test_uniform_slices_driver_cfg2(golden, golden_arrays):
     assert list(res.found) == c["slice_counts"]
     ref = np.concatenate([golden_arrays[f"cfg2_riga/slice{k}/eig"] for k in range(c["S"])])
     np.testing.assert_allclose(res.eigenvalues, np.sort(ref), rtol=1e-10)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["cfg3_riga", "cfg4_riga"])
+def test_large_config_slice0_matches_reference(golden, golden_arrays, name):
+    """Slice 0 of the 2D (N = 91,809) and 3D (N = 42,875) baseline configs against the reference's own
+    solve_slice eigenvalues (tests/golden), counts exact, residuals <= 1e-8."""
+    c = golden["configs"][name]
+    g = golden["slices"][f"{name}/0"]
+    s = P.build_system(c["d"], c["ne"], c["p"], c["level"])
+    r = P.solve_slice(s, (g["lo"], g["hi"]), seed=g["seed"], m=g["m"])
+    assert r.expected_count == g["expected"] == r.eigenvalues.size
+    np.testing.assert_allclose(r.eigenvalues, golden_arrays[f"{name}/slice0/eig"], rtol=1e-10)
+    K, M = s.K.csr, s.M.csr
+    worst = max(resid_ns(K, M, l, x) for l, x in zip(r.eigenvalues, r.vectors))
+    assert worst <= 1e-8, worst
+
+
+@pytest.mark.slow
+def test_uniform_slices_cfg4_match_kronecker_spectrum(golden):
+    """All 8 slices of the 3D config (inverse + doubling path): inertia counts equal the Kronecker counts
+    recorded from the reference, eigenvalues equal the exact discrete spectrum to 1e-10."""
+    c = golden["configs"]["cfg4_riga"]
+    s = P.build_system(c["d"], c["ne"], c["p"], c["level"])
+    lam = P.kronecker_spectrum(s)
+    shifts = P.uniform_shifts(c["lambda_e"], c["S"])
+    res = P.solve_uniform_slices(s, shifts, streams=8)
+    assert list(res.expected) == c["slice_counts"]
+    assert list(res.found) == c["slice_counts"]
+    np.testing.assert_allclose(res.eigenvalues, lam[: c["count"]], rtol=1e-10)
+
+
+@pytest.mark.slow
+def test_cfg5_slices_match_kronecker_spectrum(golden):
+    """Two slices of the largest config (3D 64^3, p = 3, N = 357,911): counts and eigenvalues against the
+    exact Kronecker spectrum."""
+    c = golden["configs"]["cfg5_riga"]
+    s = P.build_system(c["d"], c["ne"], c["p"], c["level"])
+    lam = P.kronecker_spectrum(s)
+    shifts = P.uniform_shifts(c["lambda_e"], c["S"])
+    for k in (0, c["S"] - 1):
+        lo, hi = float(shifts[k]), float(shifts[k + 1])
+        ref = lam[(lam > lo) & (lam <= hi)]
+        r = P.solve_slice(s, (lo, hi), seed=k, m=2 * ref.size)
+        assert r.expected_count == ref.size == r.eigenvalues.size == c["slice_counts"][k]
+        np.testing.assert_allclose(r.eigenvalues, ref, rtol=1e-10)
