@@ -177,6 +177,17 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
         p.perm, p.counters, p.symbolic = perm, cnt, sym
         return p
 
+    # --- memory plan: per-factor bytes (panels + inverse/G companions) and the
+    # transient update blocks; keep boundary factors only when they all fit,
+    # and cap the concurrent slices by what one slice needs ----------------
+    st_ = sym.stats
+    n = system.dof_count
+    fac_bytes = 8.0 * (1.35 * st_.get("panel_entries", 0) + 6 * n)
+    cb_bytes = 8.0 * st_.get("cb_entries", 0)
+    free_b, total_b = torch.cuda.mem_get_info(base_ctx.device)
+    budget = 0.85 * free_b
+    keep_factors = (S + 1) * fac_bytes <= 0.35 * budget
+
     # --- 1. boundary pass: each rank factors its share of the S+1 shifts ---
     t0 = time.perf_counter()
     mine_b = [k for k in range(S + 1) if k % world == rank]
@@ -189,8 +200,9 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
         for k in mine_b:
             sig, fact = pen0.factor(float(shifts[k]), scale)
             bnd[k] = (sig, fact.n_negative, fact.device_ms)
-            if k < S:
+            if k < S and keep_factors:
                 kept[k] = (sig, fact)
+            del fact
     counters.merge(bcnt)
     counters.nsh += len(mine_b)
     allb = {}
@@ -212,9 +224,18 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     slice_times = {}
     errors = []
     lock = threading.Lock()
+    factor_lock = threading.Lock()
     queue = sorted(my, key=lambda k: -expected[k])
     order = list(queue)
-    one_per_thread = len(my) <= max(1, streams)
+    m_max = max([m_factor * int(expected[k]) for k in my] + [2])
+    # per slice: its factor (unless kept), V + MV and the locked set L + LM
+    # (capacity >= m rows each), lifted/locking temporaries and pool vectors
+    per_slice = 1.2 * (fac_bytes * (0 if keep_factors else 1) + 16.0 * (m_max + 1) * n * 2
+                       + 8.0 * (3 * m_max + 16) * n)
+    kept_bytes = fac_bytes * len(kept)
+    cap = int(max(1, (budget - kept_bytes - cb_bytes) // max(per_slice, 1)))
+    nthreads = max(1, min(streams, len(my), cap))
+    one_per_thread = len(my) <= nthreads
     # one slice per stream: stream priorities by expected work; otherwise a
     # shared queue (largest first) on default-priority streams
     prio = _priorities([int(expected[k]) for k in order]) if one_per_thread else [0] * len(order)
@@ -241,7 +262,11 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                     if k in kept:
                         lob = _Boundary(lo, int(nu[k]), kept[k][1])
                     else:
-                        s2, f2 = pen.factor(lo, scale)
+                        # one refactorization at a time: its transient update
+                        # blocks (cb_bytes) are budgeted once
+                        with factor_lock:
+                            s2, f2 = pen.factor(lo, scale)
+                            ctx.synchronize()
                         lob = _Boundary(s2, f2.n_negative, f2)
                         cnt.nsh += 1
                     hib = _Boundary(hi, int(nu[k + 1]), None)
@@ -274,7 +299,6 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
         _give_ctx(ctx)
 
     t0 = time.perf_counter()
-    nthreads = max(1, min(streams, len(my)))
     threads = [threading.Thread(target=worker, args=(i,)) for i in range(nthreads)]
     # the host side of each slice (Rayleigh-Ritz eigh, small dense algebra)
     # runs in its own thread: one BLAS thread each, not nthreads x cores
@@ -318,6 +342,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     res = SlicesResult(sig_used, nu, expected, found, eig, my, local_eigs,
                        {k: results[k][1] for k in my}, counters)
     res.timings = {"boundary_s": t_bnd, "slices_s": t_sl, "total_s": time.perf_counter() - t_all,
+                   "streams_used": nthreads, "kept_boundary_factors": bool(keep_factors),
                    "boundary_pairs": sum(len(v) for v in bnear.values()),
                    "slice_wall": {int(k): [round(a, 3), round(b, 3)] for k, (a, b, _) in slice_times.items()}}
     res.factor_ms = [allb[k][2] for k in range(S + 1)]
