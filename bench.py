@@ -451,8 +451,6 @@ def ours(args):
         assert int(r.found.sum()) == count, (r.found, count)
     # ---- timed region ------------------------------------------------------
     times, found = [], 0
-    L.riga_prof_reset()
-    L.riga_prof_enable(1)
     n0 = ctypes.c_int64()
     L.riga_launch_count(ctypes.byref(n0))
     clocks = ClockSampler(dev)
@@ -472,11 +470,6 @@ def ours(args):
     clk = clocks.stop()
     n1 = ctypes.c_int64()
     L.riga_launch_count(ctypes.byref(n1))
-    L.riga_prof_enable(0)
-    ms = np.zeros(6)
-    work = np.zeros(6)
-    scopes = np.zeros(6, np.int64)
-    L.riga_prof_read(_lib.ptr(ms), _lib.ptr(work), _lib.ptr(scopes), 6)
     t_step = max_over_ranks(float(np.mean(times)))
     value = found / t_step
     launches = int(sum_over_ranks(float(n1.value - n0.value)))
@@ -551,14 +544,8 @@ def ours(args):
                        "l2": "working set > L2 (V+MV 2x251xNx8 B = 369 MB per slice); 256 MB flush between steps"},
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "roofline_by_kernel": cats,
             "ldlt": cats.get("ldlt_factor"), "clocks": clk,
-            # event pairs around each engine call on its slice stream: the 16
-            # slice streams overlap, so these stream times sum to more than
-            # the step (isolated per-kernel times are in roofline_by_kernel)
-            "stream_time_by_category_ms": {k: v for k, v in zip(
-                ["ldlt_factor", "supernodal_solve", "csr_spmv", "cgs2_pass", "vector_ops", "lift_restart"],
-                [float(x) for x in ms]) if v > 0},
             "timing": {"per_step_s": times, "boundary_s": r.timings["boundary_s"],
-                       "slices_s": r.timings["slices_s"]}}
+                       "slices_s": r.timings["slices_s"], "streams_used": r.timings.get("streams_used")}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         pairs, ctimes, workers = run_cpu_sample(args.config, args.sample_q, steps=1)
         line["cpu_baseline"] = {"value": pairs / ctimes[0], "unit": "eigenpairs/s", "cores": workers,

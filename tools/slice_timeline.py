@@ -20,6 +20,7 @@ for it in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
           "slices", round(r.timings["slices_s"], 3), "nfb", r.counters.nfb,
           "streams", r.timings.get("streams_used"), "kept", r.timings.get("kept_boundary_factors"),
           "cpu_s", round((os.times().user - c0.user) + (os.times().system - c0.system), 2))
+    print("   phases", {k: round(v, 2) for k, v in r.counters.phase_s.items() if k != "cgs_rows"})
     sw = r.timings["slice_wall"]
     print("   ends:", " ".join(f"{k}:{v[1]:.2f}" for k, v in sorted(sw.items(), key=lambda kv: kv[1][1])))
 print(json.dumps(r.timings["slice_wall"]))
