@@ -203,6 +203,267 @@ __global__ void __launch_bounds__(256) k_cgs_upd(RowSel A, const LzDev* st, int6
   if (threadIdx.x == 0) tickets[blockIdx.x] = 0;
 }
 
+__device__ __forceinline__ bool broke_down(const LzDev* st, double& beta, double& wn);
+
+// ---- delayed CGS2 (one sweep of dots + one sweep of updates per step) -----
+// The step's two Gram-Schmidt passes are the reference's (_orthogonalize,
+// eigensolver.py:204-212, two passes against basis + locked), reorganised
+// so that the second pass of the new direction r_k runs one step later,
+// inside the first pass of the next product w~ = H r~_k (delayed CGS2):
+//   dots:   s = U M r~,  z = U M w~       one read of MV/LM rows for both
+//   update: r~ -= U^T s, w~ -= U^T z      one read of V/L rows for both
+// with U = basis rows [0, k) + locked rows.  The recurrence coefficients
+// are corrected for the delay exactly (see k_dcgs_scalars), so the host
+// sees the same alpha, beta, |w| as with the undelayed passes up to
+// rounding.  Row k (the pending direction) is part of the row sweep with
+// a zero coefficient: its dots give r~.M r~ (z side: r~.M w~), and the
+// extra tile row R (x2 itself) gives |w~|^2.
+
+// dots of x1 = V[k] (pending row) and x2 against rows [0, k] + locked and,
+// as tile row R, x2.x2: coef[i] (x1 side), coef[Rmax + i] (x2 side)
+__global__ void __launch_bounds__(256, 2) k_dcgs_dots(RowSel A, const LzDev* st, int64_t n, int64_t Rmax,
+                                                      const double* __restrict__ Vbase,
+                                                      const double* __restrict__ x2, double* __restrict__ partial,
+                                                      double* __restrict__ coef, unsigned* __restrict__ tickets) {
+  if (st->stop) return;
+  int64_t na, nb;
+  rows_of(A, st, na, nb);
+  const int64_t R = na + nb, RT = R + 1;
+  const double* x1 = Vbase + (int64_t)st->k * A.ld;
+  const int lane = threadIdx.x & 31;
+  const int nchunk = (int)((n + kDotCols - 1) / kDotCols);
+  const int64_t P2 = (int64_t)nchunk * Rmax;
+  const int64_t ntiles = (int64_t)nchunk * RT;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += nwarps) {
+    const int chunk = (int)(t / RT);
+    const int64_t i = t - (int64_t)chunk * RT;
+    const int64_t c0 = (int64_t)chunk * kDotCols;
+    const double* row = (i < R ? sel_row(A, na, i) : x2) + c0;
+    double a1 = 0.0, a2 = 0.0;
+    if (c0 + kDotCols <= n) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 v[8], p[8], q[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int o = 32 * (8 * h + u) + lane;
+          v[u] = i < R ? __ldcs(reinterpret_cast<const double2*>(row) + o)
+                       : __ldg(reinterpret_cast<const double2*>(row) + o);
+          p[u] = __ldg(reinterpret_cast<const double2*>(x1 + c0) + o);
+          q[u] = __ldg(reinterpret_cast<const double2*>(x2 + c0) + o);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a1 = fma(v[u].x, p[u].x, a1);
+          a1 = fma(v[u].y, p[u].y, a1);
+          a2 = fma(v[u].x, q[u].x, a2);
+          a2 = fma(v[u].y, q[u].y, a2);
+        }
+      }
+    } else {
+      for (int64_t c = 2 * lane; c0 + c < n; c += 64) {
+        a1 = fma(row[c], x1[c0 + c], a1);
+        a2 = fma(row[c], x2[c0 + c], a2);
+        if (c0 + c + 1 < n) {
+          a1 = fma(row[c + 1], x1[c0 + c + 1], a1);
+          a2 = fma(row[c + 1], x2[c0 + c + 1], a2);
+        }
+      }
+    }
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    unsigned done = 0;
+    if (lane == 0) {
+      partial[(int64_t)chunk * Rmax + i] = a1;
+      partial[P2 + (int64_t)chunk * Rmax + i] = a2;
+      __threadfence();
+      done = atomicAdd(&tickets[i], 1u);
+    }
+    done = __shfl_sync(0xffffffffu, done, 0);
+    if (done == (unsigned)nchunk - 1) {
+      __threadfence();
+      double s1 = 0.0, s2 = 0.0;
+      for (int b = lane; b < nchunk; b += 32) {
+        s1 += __ldcg(partial + (int64_t)b * Rmax + i);
+        s2 += __ldcg(partial + P2 + (int64_t)b * Rmax + i);
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        coef[i] = s1;
+        coef[Rmax + i] = s2;
+        tickets[i] = 0;
+      }
+    }
+  }
+}
+
+// Scalars of the delayed pass (one CTA).  With r~ = eta v + U^T s (v the
+// finished direction, U M-orthonormal) and w~ = H r~:
+//   eta^2 = r~.M r~ - |s|^2
+//   alpha = v.M H v = (r~.M w~ - s.z) / eta^2 - (s.b) / eta,  b = U M H v
+// where b is the coupling column (beta_{k-1} e_{k-1} inside a run, the
+// arrowhead couplings after a restart, 0 on locked rows); the previous
+// step's beta becomes beta~ eta.  The coefficient of v in the first pass of
+// w~ / eta is (r~.M w~ - s.z) / eta^2.
+// scal: [0] alpha, [1] |w|^2, [5] eta, [6] coefficient of v
+__global__ void __launch_bounds__(256) k_dcgs_scalars(LzDev* st, int64_t Rmax, double* __restrict__ coef,
+                                                      double* __restrict__ cpl, double* __restrict__ ob) {
+  if (st->stop) return;
+  __shared__ double red[32];
+  const int k = st->k, clo = st->clo;
+  const int64_t R = (int64_t)k + 1 + st->nlocked;
+  const double vmv = coef[k], a0 = coef[Rmax + k], ww = coef[Rmax + R];
+  double ss = 0.0, sz = 0.0;
+  for (int64_t i = threadIdx.x; i < R; i += blockDim.x) {
+    if (i == k) continue;
+    const double s = coef[i];
+    ss = fma(s, s, ss);
+    sz = fma(s, coef[Rmax + i], sz);
+  }
+  ss = block_sum(ss, red);
+  sz = block_sum(sz, red);
+  const double eta = sqrt(fmax(vmv - ss, 1e-300));
+  double sb = 0.0;
+  for (int i = clo + threadIdx.x; i < k; i += blockDim.x) {
+    double b = cpl[i];
+    if (i == k - 1 && st->steps > 0) b *= eta;  // previous step's beta, finished now
+    sb = fma(coef[i], b, sb);
+  }
+  sb = block_sum(sb, red);
+  if (threadIdx.x == 0) {
+    if (st->steps > 0 && k >= 1) {
+      cpl[k - 1] *= eta;
+      ob[st->steps - 1] *= eta;
+    }
+    const double e2 = eta * eta;
+    st->scal[0] = (a0 - sz) / e2 - sb / eta;
+    st->scal[1] = ww / e2;
+    st->scal[5] = eta;
+    st->scal[6] = (a0 - sz) / e2;
+    coef[k] = 0.0;  // row k takes no part in its own update
+    coef[Rmax + k] = 0.0;
+  }
+}
+
+// r~ -= U^T s, w~ -= U^T z over the rows of A (row k with zero
+// coefficients); the last row group of a column strip finishes:
+//   vt = (r~ - U^T s) / eta          (the finished direction v_k)
+//   r  = (w~ - U^T z) / eta - c_v vt (first pass of the new residual)
+__global__ void __launch_bounds__(256) k_dcgs_upd(RowSel A, const LzDev* st, int64_t n, int64_t ldu,
+                                                  int64_t Rmax, const double* __restrict__ coef,
+                                                  double* __restrict__ upart, const double* __restrict__ w,
+                                                  double* __restrict__ vt, double* __restrict__ r,
+                                                  unsigned* __restrict__ tickets) {
+  if (st->stop) return;
+  __shared__ double cs[2][1024];
+  __shared__ bool last;
+  int64_t na, nb;
+  rows_of(A, st, na, nb);
+  const int64_t R = na + nb;
+  const int64_t per = (R + kUpdGroups - 1) / kUpdGroups;
+  const int64_t i0 = (int64_t)blockIdx.y * per, i1 = imin(R, i0 + per);
+  const int cnt = (int)(i1 > i0 ? i1 - i0 : 0);
+  for (int t = threadIdx.x; t < cnt && t < 1024; t += blockDim.x) {
+    cs[0][t] = coef[i0 + t];
+    cs[1][t] = coef[Rmax + i0 + t];
+  }
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * kUpdCols + 2 * threadIdx.x;
+  const bool valid = c < n;
+  const bool pair = c + 1 < n;
+  double2 as = make_double2(0.0, 0.0), az = make_double2(0.0, 0.0);
+  if (valid) {
+    if (pair) {
+      for (int t = 0; t < cnt; t += kUpdUnroll) {
+        double2 v[kUpdUnroll];
+#pragma unroll
+        for (int u = 0; u < kUpdUnroll; ++u)
+          v[u] = t + u < cnt ? __ldcs(reinterpret_cast<const double2*>(sel_row(A, na, i0 + t + u) + c))
+                             : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < kUpdUnroll; ++u) {
+          if (t + u < cnt) {
+            const double f = t + u < 1024 ? cs[0][t + u] : coef[i0 + t + u];
+            const double g = t + u < 1024 ? cs[1][t + u] : coef[Rmax + i0 + t + u];
+            as.x = fma(v[u].x, f, as.x);
+            as.y = fma(v[u].y, f, as.y);
+            az.x = fma(v[u].x, g, az.x);
+            az.y = fma(v[u].y, g, az.y);
+          }
+        }
+      }
+    } else {
+      for (int t = 0; t < cnt; ++t) {
+        const double x = sel_row(A, na, i0 + t)[c];
+        as.x = fma(x, t < 1024 ? cs[0][t] : coef[i0 + t], as.x);
+        az.x = fma(x, t < 1024 ? cs[1][t] : coef[Rmax + i0 + t], az.x);
+      }
+    }
+    double* dst = upart + (int64_t)blockIdx.y * ldu + c;
+    double* dsz = upart + (int64_t)(kUpdGroups + blockIdx.y) * ldu + c;
+    dst[0] = as.x;
+    dsz[0] = az.x;
+    if (pair) {
+      dst[1] = as.y;
+      dsz[1] = az.y;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (valid) {
+    const double eta = st->scal[5], cv = st->scal[6];
+    const double* vk = A.V + (int64_t)st->k * A.ld;
+    for (int e = 0; e < (pair ? 2 : 1); ++e) {
+      double ps = 0.0, pz = 0.0;
+#pragma unroll
+      for (int g = 0; g < kUpdGroups; ++g) {
+        ps += __ldcg(upart + (int64_t)g * ldu + c + e);
+        pz += __ldcg(upart + (int64_t)(kUpdGroups + g) * ldu + c + e);
+      }
+      const double v = (vk[c + e] - ps) / eta;
+      vt[c + e] = v;
+      r[c + e] = (w[c + e] - pz) / eta - cv * v;
+    }
+  }
+  if (threadIdx.x == 0) tickets[blockIdx.x] = 0;
+}
+
+// row k <- (vt, M vt); row k+1 <- (r, M r) / beta~ unless the step broke down
+__global__ void k_dcgs_store(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ vt,
+                             const double* __restrict__ mvt, const double* __restrict__ r,
+                             const double* __restrict__ Mr, double* __restrict__ V, double* __restrict__ MV) {
+  if (st->stop) return;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int64_t o = (int64_t)st->k * ld + c;
+  V[o] = vt[c];
+  MV[o] = mvt[c];
+  double beta, wn;
+  if (broke_down(st, beta, wn)) return;
+  V[o + ld] = r[c] / beta;
+  MV[o + ld] = Mr[c] / beta;
+}
+
+// finish of a run: row k /= sqrt(s) (its delayed second pass is done), the
+// last beta of the run *= sqrt(s)
+__global__ void k_dcgs_finish_row(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ s,
+                                  double* __restrict__ V, double* __restrict__ MV, double* __restrict__ ob,
+                                  int last) {
+  const double nrm = sqrt(fmax(s[0], 0.0));
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c == 0 && last >= 0) ob[last] *= nrm;
+  if (c >= n) return;
+  const int64_t o = (int64_t)st->k * ld + c;
+  V[o] /= nrm;
+  MV[o] /= nrm;
+}
+
 // out[0] = <a, b>, out[1] = <c, d>; `a` offset by k rows when koff_a != 0
 __global__ void k_dot2(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ a, int koff_a,
                        const double* __restrict__ b, const double* __restrict__ c,
@@ -522,6 +783,8 @@ struct riga_lanczos {
   int64_t n = 0, ld = 0, max_dim = 0, k = 0;
   int64_t nlocked = 0, cap = 0;
   DevBuf<double> V, MV, L, LM, w, r, Mr, bp, coef, partial, upart, cpl, Wd, outs, dscratch;
+  DevBuf<double> vt, mvt;            // finished direction of the delayed pass and its M product
+  bool delayed = true;               // delayed CGS2 step (RIGA_CGS=classic: two passes per step)
   DevBuf<unsigned> tk_dots, tk_upd;  // last-block tickets of the Gram-Schmidt kernels (self-resetting)
   DevBuf<double> kt1, kt2;           // scratch of the Kronecker mass product
   bool kron_ok = false;
@@ -568,8 +831,8 @@ int grow_locked(riga_lanczos* lz, int64_t need) {
   lz->LM.swap(nLM);
   lz->cap = cap;
   const int64_t R = lz->max_dim + 1 + cap;
-  RIGA_TRY(lz->coef.alloc(R, s));
-  RIGA_TRY(lz->partial.alloc((int64_t)((lz->n + kDotCols - 1) / kDotCols) * R, s));
+  RIGA_TRY(lz->coef.alloc(2 * R, s));
+  RIGA_TRY(lz->partial.alloc(2 * (int64_t)((lz->n + kDotCols - 1) / kDotCols) * R, s));
   RIGA_TRY(lz->tk_dots.alloc(R, s));
   RIGA_CUDA(cudaMemsetAsync(lz->tk_dots.p, 0, R * sizeof(unsigned), s));
   drop_graph(lz);
@@ -671,7 +934,48 @@ int step_full(riga_lanczos* lz) {
   k_perm_row<<<g1, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->MV.p, lz->op->sym->d_order.p, lz->bp.p);
   count_launch();
   RIGA_TRY(factor_solve(lz->op, s, lz->bp.p, lz->w.p, true));
-  return step_tail(lz);
+  if (!lz->delayed) return step_tail(lz);
+  // delayed CGS2: one dots sweep + one update sweep (see k_dcgs_dots)
+  const int64_t Rmax = lz->max_dim + 1 + lz->cap;
+  double* ob = lz->outs.p + (lz->max_dim + 1);
+  {
+    ProfScope prof(kProfCgs, s, 2.0 * (double)(lz->k + 1 + lz->nlocked) * lz->n * 8.0);
+    k_dcgs_dots<<<kDotGrid, 256, 0, s>>>(sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, lz->w.p,
+                                         lz->partial.p, lz->coef.p, lz->tk_dots.p);
+    k_dcgs_scalars<<<1, 256, 0, s>>>(lz->st.p, Rmax, lz->coef.p, lz->cpl.p, ob);
+    const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
+    k_dcgs_upd<<<gu, 256, 0, s>>>(sel_basis(lz, false, 1), lz->st.p, lz->n, lz->ld, Rmax, lz->coef.p,
+                                  lz->upart.p, lz->w.p, lz->vt.p, lz->r.p, lz->tk_upd.p);
+    count_launch(3);
+  }
+  RIGA_TRY(mass_apply(lz, lz->vt.p, lz->mvt.p));
+  RIGA_TRY(mass_apply(lz, lz->r.p, lz->Mr.p));
+  RIGA_TRY(dot2(lz, lz->r.p, 0, lz->Mr.p, lz->r.p, lz->Mr.p, 2));  // beta~^2
+  k_dcgs_store<<<g1, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->vt.p, lz->mvt.p, lz->r.p, lz->Mr.p, lz->V.p,
+                                  lz->MV.p);
+  k_step_finish<<<1, 1, 0, s>>>(lz->st.p, lz->cpl.p, lz->outs.p, ob, lz->outs.p + 2 * (lz->max_dim + 1));
+  count_launch(2);
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+// end of a delayed run: the pending row k gets its second pass against rows
+// [0, k) + locked and is renormalised; the run's last beta *= that norm
+int finish_pending(riga_lanczos* lz, int last) {
+  cudaStream_t s = lz->ctx->stream;
+  RIGA_TRY(push_state(lz, lz->k, lz->k, 0.0));
+  double* x = lz->V.p + lz->k * lz->ld;
+  double* mx = lz->MV.p + lz->k * lz->ld;
+  RIGA_TRY(cgs_passes(lz, sel_basis(lz, true, 0), sel_basis(lz, false, 0), RowSel{}, x, nullptr, 1,
+                      lz->k + lz->nlocked));
+  RIGA_TRY(mass_apply(lz, x, mx));
+  RIGA_TRY(dot2(lz, x, 0, mx, x, mx, 6));
+  k_dcgs_finish_row<<<(unsigned)((lz->n + 255) / 256), 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->st.p->scal + 6,
+                                                                     lz->V.p, lz->MV.p,
+                                                                     lz->outs.p + (lz->max_dim + 1), last);
+  count_launch();
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
 }
 
 int ensure_graph(riga_lanczos* lz) {
@@ -736,7 +1040,13 @@ int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max
   RIGA_TRY(lz->r.alloc(lz->ld, cs));
   RIGA_TRY(lz->Mr.alloc(lz->ld, cs));
   RIGA_TRY(lz->bp.alloc(lz->ld, cs));
-  RIGA_TRY(lz->upart.alloc(kUpdGroups * lz->ld, cs));
+  RIGA_TRY(lz->upart.alloc(2 * kUpdGroups * lz->ld, cs));
+  RIGA_TRY(lz->vt.alloc(lz->ld, cs));
+  RIGA_TRY(lz->mvt.alloc(lz->ld, cs));
+  {
+    const char* e = getenv("RIGA_CGS");
+    lz->delayed = !(e && std::strcmp(e, "classic") == 0);
+  }
   RIGA_TRY(lz->tk_upd.alloc((lz->n + kUpdCols - 1) / kUpdCols, cs));
   RIGA_CUDA(cudaMemsetAsync(lz->tk_upd.p, 0, ((lz->n + kUpdCols - 1) / kUpdCols) * sizeof(unsigned), cs));
   RIGA_TRY(lz->cpl.alloc(rows, cs));
@@ -866,8 +1176,22 @@ int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_
   for (int64_t i = lz->k; i < limit; ++i) RIGA_CUDA(cudaGraphLaunch(lz->gexec, s));
   count_launch((int)((limit - lz->k) * lz->gnodes));
   const int64_t rows = lz->max_dim + 1;
-  RIGA_CUDA(cudaMemcpyAsync(lz->hbuf, lz->outs.p, 3 * rows * 8, cudaMemcpyDeviceToHost, s));
-  RIGA_TRY(pull_state(lz));
+  if (lz->delayed) {
+    RIGA_TRY(pull_state(lz));
+    const int ns0 = lz->hst->steps, stop0 = lz->hst->stop, k0 = lz->hst->k;
+    if (stop0 != 1 && ns0 > 0) {
+      lz->k = k0;
+      RIGA_TRY(finish_pending(lz, ns0 - 1));
+    }
+    RIGA_CUDA(cudaMemcpyAsync(lz->hbuf, lz->outs.p, 3 * rows * 8, cudaMemcpyDeviceToHost, s));
+    RIGA_CUDA(stream_sync(s));
+    lz->hst->steps = ns0;
+    lz->hst->stop = stop0;
+    lz->hst->k = k0;
+  } else {
+    RIGA_CUDA(cudaMemcpyAsync(lz->hbuf, lz->outs.p, 3 * rows * 8, cudaMemcpyDeviceToHost, s));
+    RIGA_TRY(pull_state(lz));
+  }
   const int ns = lz->hst->steps;
   for (int i = 0; i < ns; ++i) {
     alpha[i] = lz->hbuf[i];

@@ -19,6 +19,8 @@ elimination tree (same fill, same column counts, same factor_flops).
 from __future__ import annotations
 
 import ctypes
+import os
+import threading
 import time
 import weakref
 from dataclasses import dataclass, field
@@ -31,6 +33,8 @@ from . import _lib
 from . import device as _dev
 from .assembly import DeviceSystem, DiscreteSystem, SymSparseMatrix
 from .bspline import separator_basis_indices
+
+_TRACE = os.environ.get("RIGA_TRACE") == "1"
 
 
 class ZeroPivot(Exception):
@@ -69,8 +73,15 @@ class CostCounters:
     steps_per_iteration: list = field(default_factory=list)
     phase_s: dict = field(default_factory=dict)  # host wall seconds per driver phase (engine extension)
 
+    trace: list | None = None  # (phase, t_start, t_end, thread) when RIGA_TRACE=1
+
     def phase(self, name: str, dt: float) -> None:
         self.phase_s[name] = self.phase_s.get(name, 0.0) + dt
+        if _TRACE and name != "cgs_rows":
+            t1 = time.perf_counter()
+            if self.trace is None:
+                self.trace = []
+            self.trace.append((name, t1 - dt, t1, threading.get_ident()))
 
     @property
     def nfa(self) -> int:
@@ -93,7 +104,9 @@ class CostCounters:
         self.retries += other.retries
         self.steps_per_iteration.extend(other.steps_per_iteration)
         for k, v in other.phase_s.items():
-            self.phase(k, v)
+            self.phase_s[k] = self.phase_s.get(k, 0.0) + v
+        if other.trace:
+            self.trace = (self.trace or []) + other.trace
 
 
 # ---------------------------------------------------------------------------

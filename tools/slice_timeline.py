@@ -1,5 +1,6 @@
 """Per-slice wall-clock timeline of one cfg3 solve_uniform_slices call."""
 import json, os, sys, time
+import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2009_08167_b200 as P  # noqa
@@ -25,3 +26,20 @@ for it in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
     print("   ends:", " ".join(f"{k}:{v[1]:.2f}" for k, v in sorted(sw.items(), key=lambda kv: kv[1][1])))
 print(json.dumps(r.timings["slice_wall"]))
 print("phase seconds summed over slices", {k: round(v, 3) for k, v in r.counters.phase_s.items()})
+if r.counters.trace and len(r.counters.trace) < 100000:
+    # slices per phase over time (50 ms bins, relative to the first event)
+    tr = r.counters.trace
+    t0 = min(a for _, a, _, _ in tr)
+    t1 = max(b for _, _, b, _ in tr)
+    names = sorted({n for n, *_ in tr})
+    nb = int((t1 - t0) / 0.05) + 1
+    occ = {n: np.zeros(nb) for n in names}
+    for n, a, b, _ in tr:
+        for i in range(nb):
+            lo, hi = t0 + 0.05 * i, t0 + 0.05 * (i + 1)
+            ov = min(b, hi) - max(a, lo)
+            if ov > 0:
+                occ[n][i] += ov / 0.05
+    print("bin_ms " + " ".join(f"{n[:7]:>7s}" for n in names))
+    for i in range(nb):
+        print(f"{50 * i:6d} " + " ".join(f"{occ[n][i]:7.2f}" for n in names))
