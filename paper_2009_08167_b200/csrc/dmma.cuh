@@ -183,3 +183,129 @@ __device__ __forceinline__ void dmma_gemm_tile(const double* __restrict__ A, int
 }
 
 }  // namespace riga
+
+namespace riga {
+
+// ---------------------------------------------------------------------------
+// 128 x 128 FP64 DMMA tile with a cp.async pipeline (large frontal updates).
+//
+//   C(i - coff, j - coff) -= sum_{t in [k0, k1)} A[t lda + i] d[t] B[t ldb + j]
+//   for i in [i0, i0 + 128), i < mend, and j in [j0, j0 + 128), j < nend.
+//
+// 256 threads = 8 warps as 2 (rows) x 4 (cols), each warp 64 x 32 = 8 x 4
+// DMMA.8x8x4 tiles (64 fp64 accumulators per thread).  k runs in steps of 16
+// through kT128Stages shared-memory stages filled by 8-byte cp.async (rows
+// of a front are not 16-byte aligned in general) with zero fill outside the
+// ranges; d (the pivots D, or nullptr for 1) multiplies the A fragments in
+// registers.  Pitch 132 doubles (== 4 mod 16): the 16 lanes of a half warp
+// (4 k rows x 4 columns) hit 16 distinct banks pairs.
+// ---------------------------------------------------------------------------
+constexpr int kT128 = 128;
+constexpr int kT128K = 16;
+constexpr int kT128P = 132;
+constexpr int kT128Stages = 3;
+constexpr int kT128StageDoubles = 2 * kT128K * kT128P + kT128K;
+constexpr size_t kT128Smem = (size_t)kT128Stages * kT128StageDoubles * sizeof(double);
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64_t lda,
+                                             const double* __restrict__ B, int64_t ldb,
+                                             const double* __restrict__ d, int64_t k0, int64_t k1,
+                                             int64_t i0, int64_t j0, int64_t mend, int64_t nend,
+                                             double* __restrict__ C, int64_t ldc, int64_t coff,
+                                             double* __restrict__ smem) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int m = 0; m < 8; ++m)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+  const int64_t nk = (k1 - k0 + kT128K - 1) / kT128K;
+  auto stage_ptr = [&](int s) { return smem + (int64_t)s * kT128StageDoubles; };
+  // thread -> (k row kr0 + 2u, column ci) of a stage; row/column predicates fixed per thread
+  const int ci = tid & 127, kr0 = tid >> 7;
+  const bool prow = i0 + ci < mend, pcol = j0 + ci < nend;
+  const double* Ab = A + (prow ? i0 + ci : 0);
+  const double* Bb = B + (pcol ? j0 + ci : 0);
+  auto load = [&](int s, int64_t kt) {
+    double* As = stage_ptr(s) + kr0 * kT128P + ci;
+    double* Bs = As + kT128K * kT128P;
+    const int64_t kb = kt + kr0;
+    const double* pa = Ab + kb * lda;
+    const double* pb = Bb + kb * ldb;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool kin = kb + 2 * u < k1;
+      cp_async8(As + 2 * u * kT128P, kin && prow ? pa : A, kin && prow);
+      cp_async8(Bs + 2 * u * kT128P, kin && pcol ? pb : B, kin && pcol);
+      pa += 2 * lda;
+      pb += 2 * ldb;
+    }
+    if (tid < kT128K) {
+      double* Ds = stage_ptr(s) + 2 * kT128K * kT128P;
+      const int64_t kk = kt + tid;
+      if (d) {
+        cp_async8(Ds + tid, kk < k1 ? d + kk : d, kk < k1);
+      } else {
+        Ds[tid] = 1.0;
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < kT128Stages - 1; ++s) {
+    if (s < nk) load(s, k0 + (int64_t)s * kT128K);
+    cp_async_commit();
+  }
+  for (int64_t it = 0; it < nk; ++it) {
+    cp_async_wait<kT128Stages - 2>();
+    __syncthreads();
+    {
+      const int64_t nx = it + kT128Stages - 1;
+      if (nx < nk) load((int)(nx % kT128Stages), k0 + nx * kT128K);
+      cp_async_commit();
+    }
+    const double* As = stage_ptr((int)(it % kT128Stages));
+    const double* Bs = As + kT128K * kT128P;
+    const double* Ds = Bs + kT128K * kT128P;
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const int kr = k4 * 4 + (lane & 3);
+      const double dk = Ds[kr];
+      double av[8], bv[4];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) av[m] = As[kr * kT128P + wm * 64 + m * 8 + (lane >> 2)] * dk;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bv[q] = Bs[kr * kT128P + wn * 32 + q * 8 + (lane >> 2)];
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[m][q][0], acc[m][q][1], av[m], bv[q]);
+    }
+  }
+  cp_async_wait<0>();
+  const int r = lane >> 2, cc = (lane & 3) * 2;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int64_t i = i0 + wm * 64 + m * 8 + r;
+    if (i >= mend) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t j = j0 + wn * 32 + q * 8 + cc;
+      if (j < nend) C[(j - coff) * ldc + (i - coff)] -= acc[m][q][0];
+      if (j + 1 < nend) C[(j + 1 - coff) * ldc + (i - coff)] -= acc[m][q][1];
+    }
+  }
+}
+
+}  // namespace riga

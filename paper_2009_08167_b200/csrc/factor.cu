@@ -275,6 +275,175 @@ __global__ void __launch_bounds__(kPanelRows) k_panel(SymDev S, const int32_t* _
   }
 }
 
+// ---------------------------------------------------------------------------
+// Outer block of a large front in two launches (replaces 4 x (k_panel<false>,
+// k_panel<true>, k_syrk<0>) per kNBO columns):
+//   k_diag_block  one CTA per front: the nb x nb diagonal block (nb <= kNBO)
+//                 in shared memory, factored 32 columns at a time (warp-0
+//                 unblocked LDL^T of the 32 x 32 block, row TRSM below it,
+//                 rank-32 update of the rest of the block); writes L11, D
+//                 and the inertia / zero-pivot counters
+//   k_l21         row chunks of all fronts: W = A21 L11^{-T} by a row-wise
+//                 forward sweep (warp per 4 rows, lanes over columns, L11 in
+//                 shared memory), L21 = W D^{-1}
+// ---------------------------------------------------------------------------
+constexpr int kL21Rows = 32;
+__host__ __device__ constexpr size_t diag_smem(int nbm) { return ((size_t)nbm * (nbm + 1) + 3 * (size_t)nbm) * sizeof(double); }
+__host__ __device__ constexpr size_t l21_smem(int nbm) {
+  return ((size_t)nbm * (nbm + 1) + (size_t)nbm * (kL21Rows + 1) + nbm) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(256) k_diag_block(SymDev S, const int32_t* __restrict__ nodes, int kb,
+                                                    int kDBP, const double* __restrict__ tol,
+                                                    double* __restrict__ panel, double* __restrict__ D,
+                                                    int64_t* __restrict__ stat) {
+  extern __shared__ double sm[];  // nb x kDBP block + nb pivots (kDBP = level max nb + 1)
+  const int s = nodes[blockIdx.x];
+  const int64_t f = S.front[s], np = S.ncol[s];
+  if (kb >= np) return;
+  const int nb = (int)imin(kNBO, np - kb);
+  const int64_t col0 = S.col0[s];
+  double* P = panel + S.panel_off[s];
+  double* A = sm;  // A[c * kDBP + r], lower triangle
+  double* dd = sm + (kDBP - 1) * kDBP;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    const int c = idx / nb, r = idx - c * nb;
+    if (r >= c) A[c * kDBP + r] = P[(int64_t)(kb + c) * f + kb + r];
+  }
+  __syncthreads();
+  // right-looking unblocked LDL^T of the block by all threads: per pivot k,
+  // l = A(k+1:, k) / d into a double-buffered vector, rank-1 update of the
+  // trailing lower triangle (warp per column), then column k <- l
+  double* lb0 = dd + (kDBP - 1);
+  double* lb1 = lb0 + (kDBP - 1);
+  for (int k = 0; k < nb; ++k) {
+    double* lb = (k & 1) ? lb1 : lb0;
+    const double d = A[k * kDBP + k];
+    if (tid == 0) dd[k] = d;
+    for (int r = k + 1 + tid; r < nb; r += blockDim.x) lb[r] = A[k * kDBP + r] / d;
+    __syncthreads();
+    for (int c = k + 1 + warp; c < nb; c += 8) {
+      const double ac = A[k * kDBP + c];
+      double* Ac = A + c * kDBP;
+      for (int r = c + lane; r < nb; r += 32) Ac[r] -= lb[r] * ac;
+    }
+    __syncthreads();
+    for (int r = k + 1 + tid; r < nb; r += blockDim.x) A[k * kDBP + r] = lb[r];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    const int c = idx / nb, r = idx - c * nb;
+    if (r >= c) P[(int64_t)(kb + c) * f + kb + r] = A[c * kDBP + r];
+  }
+  if (tid == 0) {
+    int neg = 0;
+    int64_t bad = INT64_MAX;
+    const double tv = tol[1];
+    for (int k = 0; k < nb; ++k) {
+      const double d = dd[k];
+      D[col0 + kb + k] = d;
+      if (d < 0.0) neg++;
+      if (fabs(d) < tv && bad == INT64_MAX) bad = col0 + kb + k;
+    }
+    if (neg) atomicAdd((unsigned long long*)&stat[0], (unsigned long long)neg);
+    if (bad != INT64_MAX) atomicMin((long long*)&stat[1], (long long)bad);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_l21(SymDev S, const int32_t* __restrict__ nodes, int kb, int kDBP,
+                                             int rows_per_cta, double* __restrict__ panel,
+                                             const double* __restrict__ D) {
+  extern __shared__ double sm[];
+  const int s = nodes[blockIdx.y];
+  const int64_t f = S.front[s], np = S.ncol[s];
+  if (kb >= np) return;
+  const int nb = (int)imin(kNBO, np - kb);
+  const int64_t rbeg = kb + nb + (int64_t)blockIdx.x * rows_per_cta;
+  if (rbeg >= f) return;
+  const int64_t rend = imin(f, rbeg + rows_per_cta);
+  double* P = panel + S.panel_off[s];
+  const int nbm = kDBP - 1;
+  double* Ls = sm;                   // Ls[t * kDBP + c] = L11(c, t), c > t
+  double* Wt = sm + nbm * kDBP;      // Wt[c * (kL21Rows + 1) + r]
+  double* dd = Wt + nbm * (kL21Rows + 1);
+  constexpr int WP = kL21Rows + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    const int t = idx / nb, c = idx - t * nb;
+    Ls[t * kDBP + c] = c > t ? P[(int64_t)(kb + t) * f + kb + c] : 0.0;
+  }
+  for (int c = tid; c < nb; c += blockDim.x) dd[c] = D[S.col0[s] + kb + c];
+  constexpr int RW = kL21Rows / 8;
+  for (int64_t r0 = rbeg; r0 < rend; r0 += kL21Rows) {
+    const int nr = (int)imin(kL21Rows, rend - r0);
+    __syncthreads();
+    for (int idx = tid; idx < nb * kL21Rows; idx += blockDim.x) {
+      const int c = idx / kL21Rows, r = idx - c * kL21Rows;
+      Wt[c * WP + r] = r < nr ? P[(int64_t)(kb + c) * f + r0 + r] : 0.0;
+    }
+    __syncthreads();
+    // W(r, :) L11^T = A21(r, :): forward sweep over the columns; lane owns
+    // columns lane + 32 u, a warp carries RW rows (independent chains)
+    double a[RW][4];
+#pragma unroll
+    for (int q = 0; q < RW; ++q)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = lane + 32 * u;
+        a[q][u] = c < nb ? Wt[c * WP + warp * RW + q] : 0.0;
+      }
+#pragma unroll
+    for (int u0 = 0; u0 < 4; ++u0) {
+      for (int cl = 0; cl < 32; ++cl) {
+        const int c = 32 * u0 + cl;
+        if (c >= nb) break;
+        double w[RW];
+#pragma unroll
+        for (int q = 0; q < RW; ++q) w[q] = __shfl_sync(0xffffffffu, a[q][u0], cl);
+        const double* Lc = Ls + c * kDBP;
+#pragma unroll
+        for (int u = u0; u < 4; ++u) {
+          const int j = lane + 32 * u;
+          if (u == u0 && lane <= cl) continue;
+          const double l = j < nb ? Lc[j] : 0.0;
+#pragma unroll
+          for (int q = 0; q < RW; ++q) a[q][u] = fma(-w[q], l, a[q][u]);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RW; ++q)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = lane + 32 * u;
+        if (c < nb) Wt[c * WP + warp * RW + q] = a[q][u] / dd[c];
+      }
+    __syncthreads();
+    for (int idx = tid; idx < nb * kL21Rows; idx += blockDim.x) {
+      const int c = idx / kL21Rows, r = idx - c * kL21Rows;
+      if (r < nr) P[(int64_t)(kb + c) * f + r0 + r] = Wt[c * WP + r];
+    }
+  }
+}
+
+// update block -= L21 D L21^T on 128 x 128 DMMA tiles (large K = n_p)
+__global__ void __launch_bounds__(256, 1) k_syrk128(SymDev S, const int32_t* __restrict__ nodes,
+                                                    double* __restrict__ panel, double* __restrict__ cb,
+                                                    const double* __restrict__ D) {
+  extern __shared__ double sm[];
+  const int s = nodes[blockIdx.y];
+  const int64_t f = S.front[s], np = S.ncol[s];
+  if (np >= f) return;
+  const int64_t nt = (f - np + kT128 - 1) / kT128;
+  const int64_t ti = blockIdx.x / nt, tj = blockIdx.x % nt;
+  if (ti >= nt || ti < tj) return;
+  const double* L = panel + S.panel_off[s];
+  dmma_tile128(L, f, L, f, D + S.col0[s], 0, np, np + ti * kT128, np + tj * kT128, f, f, cb + S.cb_off[s],
+               f - np, np, sm);
+}
+
 // Trailing updates on FP64 tensor cores (rows always run to f):
 // MODE 0: rank-nbk update of the panel-block columns [kq + nbk, min(kbo + kNBO, np))
 //         by panel columns [kq, kq + nbk)              (inside an outer block)
@@ -436,9 +605,24 @@ __global__ void k_zero_cb(SymDev S, const int32_t* __restrict__ nodes, double* _
     c[i] = 0.0;
 }
 
+static bool g_block_path = true;  // RIGA_FACTOR_PANEL=32: the 32-column panel chain
+static bool g_tile128 = true;      // RIGA_FACTOR_TILE128=0: 64 x 64 tiles for the update blocks
+static int64_t g_block_max_fronts = 0;  // RIGA_FACTOR_BLOCK_FRONTS=n: block path for levels with <= n large fronts (opt-in: slower today)
+
 static int set_smem_attrs() {
   static bool done = false;
   if (done) return RIGA_OK;
+  {
+    const char* e = getenv("RIGA_FACTOR_PANEL");
+    g_block_path = !(e && std::strcmp(e, "32") == 0);
+    e = getenv("RIGA_FACTOR_TILE128");
+    g_tile128 = !(e && std::strcmp(e, "0") == 0);
+    e = getenv("RIGA_FACTOR_BLOCK_FRONTS");
+    if (e) g_block_max_fronts = atoll(e);
+  }
+  RIGA_CUDA(cudaFuncSetAttribute(k_diag_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem(kNBO)));
+  RIGA_CUDA(cudaFuncSetAttribute(k_l21, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l21_smem(kNBO)));
+  RIGA_CUDA(cudaFuncSetAttribute(k_syrk128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem));
   int dev = 0, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -502,8 +686,24 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
       unsigned nl = (unsigned)P.nlarge;
       for (int64_t kbo = 0; kbo < P.max_np_large; kbo += kNBO) {
+        const bool blockp = g_block_path && (int64_t)P.nlarge <= g_block_max_fronts;
+        if (blockp) {
+          // diagonal block in one CTA per front, then L21 for every row below it
+          const int nbm = (int)std::min<int64_t>(kNBO, P.max_np_large - kbo);
+          k_diag_block<<<nl, 256, diag_smem(nbm), st>>>(S, ln, (int)kbo, nbm + 1, F->tol.p, F->panel.p, F->D.p,
+                                                        F->stat.p);
+          // rows per CTA: about two waves over all fronts of the level, >= 32
+          const int64_t rows = std::max<int64_t>(1, P.max_f_large - kbo);  // bound over fronts with nb < nbm
+          int64_t rpc = (rows * (int64_t)nl + 2 * 148 - 1) / (2 * 148);
+          rpc = std::max<int64_t>(kL21Rows, (rpc + kL21Rows - 1) / kL21Rows * kL21Rows);
+          const unsigned rchunks = (unsigned)((rows + rpc - 1) / rpc);
+          k_l21<<<dim3(rchunks, nl), 256, l21_smem(nbm), st>>>(S, ln, (int)kbo, nbm + 1, (int)rpc, F->panel.p,
+                                                               F->D.p);
+          count_launch(2);
+          RIGA_CUDA(cudaGetLastError());
+        }
         // factor the outer block's columns 32 at a time (panel + in-block update)
-        for (int64_t kb = kbo; kb < std::min<int64_t>(kbo + kNBO, P.max_np_large); kb += kNB) {
+        for (int64_t kb = kbo; !blockp && kb < std::min<int64_t>(kbo + kNBO, P.max_np_large); kb += kNB) {
           unsigned rchunks = (unsigned)std::max<int64_t>(1, (P.max_f_large - kb + kPanelRows - 1) / kPanelRows);
           k_panel<false><<<dim3(1, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p, F->D.p,
                                                              F->stat.p);
@@ -528,7 +728,12 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
           RIGA_CUDA(cudaGetLastError());
         }
       }
-      if (P.max_nu_large > 0) {
+      if (P.max_nu_large > 0 && g_tile128 && P.max_np_large >= 128 && P.max_nu_large >= 256) {
+        const int64_t t = (P.max_nu_large + kT128 - 1) / kT128;
+        k_syrk128<<<dim3((unsigned)(t * t), nl), 256, kT128Smem, st>>>(S, ln, F->panel.p, cbuf, F->D.p);
+        count_launch();
+        RIGA_CUDA(cudaGetLastError());
+      } else if (P.max_nu_large > 0) {
         int64_t t = (P.max_nu_large + 63) / 64;
         k_syrk<1><<<dim3((unsigned)(t * t), nl), 128, 0, st>>>(S, ln, 0, 0, F->panel.p, cbuf, F->D.p); count_launch();
         RIGA_CUDA(cudaGetLastError());

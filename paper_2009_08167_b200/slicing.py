@@ -283,7 +283,13 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                     lams = np.array([pool.lams[i] for i in idx])
                     if idx:
                         X = torch.stack([pool.vecs[i] for i in idx])
-                        X = X.cpu().numpy() if vectors_to_host else X
+                        if vectors_to_host:
+                            # pinned staging + async copy on the slice stream
+                            # (a pageable .cpu() would serialise the slices)
+                            H = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
+                            H.copy_(X, non_blocking=True)
+                            ctx.synchronize()
+                            X = H.numpy()
                     else:
                         X = np.empty((0, system.dof_count))
                     ctx.synchronize()

@@ -15,6 +15,15 @@ __global__ void __launch_bounds__(128) syrk_tiles(const double* A, int64_t lda, 
   dmma_syrk_tile(A, lda, D, 0, k, ti * 64, tj * 64, n, n, C, n, 0);
 }
 
+__global__ void __launch_bounds__(256, 1) syrk_tiles128(const double* A, int64_t lda, const double* D, int64_t k,
+                                                        double* C, int64_t n) {
+  extern __shared__ double sm[];
+  const int64_t nt = (n + 127) / 128;
+  const int64_t ti = blockIdx.x / nt, tj = blockIdx.x % nt;
+  if (ti < tj) return;
+  dmma_tile128(A, lda, A, lda, D, 0, k, ti * 128, tj * 128, n, n, C, n, 0, sm);
+}
+
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 4096, k = argc > 2 ? atoll(argv[2]) : 2048;
   double *A, *C, *D;
@@ -37,6 +46,19 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&ms, e0, e1);
     const double flops = (double)n * (n + 64) * k;  // lower tiles incl. diagonal, 2 flops per mac / 2
     if (rep) printf("syrk tile n=%lld k=%lld: %.3f ms  %.2f TFLOP/s\n", (long long)n, (long long)k, ms,
+                    flops / ms / 1e9);
+  }
+  cudaFuncSetAttribute(syrk_tiles128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem);
+  const int64_t nt2 = (n + 127) / 128;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0);
+    syrk_tiles128<<<(unsigned)(nt2 * nt2), 256, kT128Smem>>>(A, n, D, k, C, n);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = (double)n * (n + 128) * k;
+    if (rep) printf("syrk tile128 n=%lld k=%lld: %.3f ms  %.2f TFLOP/s\n", (long long)n, (long long)k, ms,
                     flops / ms / 1e9);
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
