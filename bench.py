@@ -29,6 +29,7 @@ import sys
 import time
 
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # many concurrent slice streams
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "backend:cudaMallocAsync")  # stream-ordered torch allocations
 
 if "--impl" in sys.argv and "reference" in sys.argv:
     # the reference's CPU path: one BLAS thread per worker process

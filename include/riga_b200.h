@@ -153,6 +153,10 @@ int riga_factor_destroy(riga_factor* f);
 int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max_dim,
                         riga_lanczos** out);
 int riga_lanczos_destroy(riga_lanczos* lz);
+/* Empty the state for reuse by a new LanczosState with the same n, max_dim
+ * and mass (k = 0, no locked rows; buffers and the captured step graph are
+ * kept, so a reused state allocates nothing).                              */
+int riga_lanczos_reset(riga_lanczos* lz);
 /* Operator for the next extend: H = (K - shift M)^{-1} M via factor f.     */
 int riga_lanczos_set_operator(riga_lanczos* lz, riga_factor* f);
 /* Current basis size k (host view). */
@@ -175,6 +179,9 @@ int riga_lanczos_locked_count(riga_lanczos* lz, int64_t* count);
 int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_host,
                         double breakdown_tol, double* alpha, double* beta, double* wnorm,
                         int64_t* steps);
+/* Device milliseconds of the last extend's step replays (CUDA events on
+ * the state's stream around the replayed step graphs; 0 if none ran).      */
+int riga_lanczos_last_extend_ms(riga_lanczos* lz, float* ms);
 /* One step with a caller-computed w = H v (device vector of length n), for
  * operators that are not a device factor (ref LanczosState(apply_op=...)
  * with an arbitrary callable).  Outputs as riga_lanczos_extend (1 step).   */

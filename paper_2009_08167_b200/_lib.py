@@ -57,6 +57,7 @@ SIGNATURES = {
     "riga_factor_destroy": [_p],
     "riga_lanczos_create": [_p, _p, _i64, _i64, _p],
     "riga_lanczos_destroy": [_p],
+    "riga_lanczos_reset": [_p],
     "riga_lanczos_set_operator": [_p, _p],
     "riga_lanczos_k": [_p, _p],
     "riga_lanczos_set_start": [_p, _p],
@@ -64,6 +65,7 @@ SIGNATURES = {
     "riga_lanczos_lock": [_p, _p, _p],
     "riga_lanczos_locked_count": [_p, _p],
     "riga_lanczos_extend": [_p, _i64, _p, _d, _p, _p, _p, _p],
+    "riga_lanczos_last_extend_ms": [_p, _p],
     "riga_lanczos_step_given": [_p, _p, _p, _d, _p, _p, _p],
     "riga_lanczos_lift": [_p, _p, _i64, _p, _p],
     "riga_lanczos_restart": [_p, _p, _i64],

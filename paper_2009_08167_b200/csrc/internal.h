@@ -51,7 +51,7 @@ struct I2 {
 
 // Task lists and pull map of the persistent solve kernels (solve.cu).
 struct SolvePlanHost {
-  int warp_stage = 0, l2_prefetch = 0, chain_inv = 1, small_g = 1, occ = 4;
+  int warp_stage = 0, l2_prefetch = 0, chain_inv = 1, small_g = 1, occ = 4, rest_cap = 1 << 30;
   int64_t g_total = 0;                 // doubles of G = [inv(L11); L21 inv(L11)] of the small supernodes
   std::vector<int64_t> g_off;          // per supernode offset into gsmall (-1: large)
   std::vector<I2> gfwd, gbwd;          // G warp tasks: (supernode, row tile) / (supernode, column group)

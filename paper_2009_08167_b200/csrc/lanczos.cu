@@ -798,9 +798,13 @@ struct riga_lanczos {
   const double* gL = nullptr;
   int64_t gR = 0;
   long long gnodes = 0;  // kernel launches per replay
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // around the last extend's replays
+  bool ev_valid = false;
   cudaStream_t cur = nullptr;   // stream the step helpers launch on
   cudaStream_t capst = nullptr; // private stream for graph capture (never legacy)
   ~riga_lanczos() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (capst) cudaStreamDestroy(capst);
     if (hbuf) riga::pinned_put(hbuf);
@@ -1080,6 +1084,15 @@ int riga_lanczos_destroy(riga_lanczos* lz) {
   return RIGA_OK;
 }
 
+int riga_lanczos_reset(riga_lanczos* lz) {
+  RIGA_CHECK_ARG(lz, "null arg");
+  DeviceGuard g(lz->ctx->device);
+  lz->k = 0;
+  lz->nlocked = 0;
+  lz->ev_valid = false;
+  return push_state(lz, 0, 0, 0.0);
+}
+
 int riga_lanczos_set_operator(riga_lanczos* lz, riga_factor* f) {
   RIGA_CHECK_ARG(lz && f, "null arg");
   RIGA_CHECK_ARG(f->sym->h.n == lz->n, "operator dimension mismatch");
@@ -1173,7 +1186,14 @@ int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_
   }
   RIGA_TRY(ensure_graph(lz));
   RIGA_TRY(push_state(lz, clo, limit, breakdown_tol));
+  if (!lz->ev0) {
+    RIGA_CUDA(cudaEventCreate(&lz->ev0));
+    RIGA_CUDA(cudaEventCreate(&lz->ev1));
+  }
+  RIGA_CUDA(cudaEventRecord(lz->ev0, s));
   for (int64_t i = lz->k; i < limit; ++i) RIGA_CUDA(cudaGraphLaunch(lz->gexec, s));
+  RIGA_CUDA(cudaEventRecord(lz->ev1, s));
+  lz->ev_valid = true;
   count_launch((int)((limit - lz->k) * lz->gnodes));
   const int64_t rows = lz->max_dim + 1;
   if (lz->delayed) {
@@ -1201,6 +1221,16 @@ int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_
   *steps = ns;
   lz->k = lz->hst->k;
   return lz->hst->stop == 1 ? RIGA_BREAKDOWN : RIGA_OK;
+}
+
+int riga_lanczos_last_extend_ms(riga_lanczos* lz, float* ms) {
+  RIGA_CHECK_ARG(lz && ms, "null arg");
+  *ms = 0.0f;
+  if (!lz->ev_valid) return RIGA_OK;
+  DeviceGuard g(lz->ctx->device);
+  RIGA_CUDA(cudaEventSynchronize(lz->ev1));
+  RIGA_CUDA(cudaEventElapsedTime(ms, lz->ev0, lz->ev1));
+  return RIGA_OK;
 }
 
 int riga_lanczos_step_given(riga_lanczos* lz, const double* w_dev, const double* coupling_host,

@@ -336,10 +336,20 @@ __device__ __forceinline__ void warp_gtile_fwd(const SymDev& S, const SolveDev& 
   const double yi = (i >= np && i < f) ? gather_row(S, T, s, i, np, col0, b, upd) : 0.0;
   __syncwarp();
   if (i >= f) return;
-  double acc = 0.0;
+  // 4 partial sums, 16 independent G loads in flight per lane
+  double a4[4] = {0.0, 0.0, 0.0, 0.0};
   const double* Gi = G + i;
+  int k = 0;
+  for (; k + 16 <= np; k += 16) {
+    double g[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) g[u] = Gi[(k + u) * f];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) a4[u & 3] = fma(g[u], yw[k + u], a4[u & 3]);
+  }
 #pragma unroll 8
-  for (int k = 0; k < np; ++k) acc = fma(Gi[k * f], yw[k], acc);
+  for (; k < np; ++k) a4[0] = fma(Gi[k * f], yw[k], a4[0]);
+  const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
   if (i < np) {
     xp[col0 + i] = acc;
     GD.wz[col0 + i] = acc / GD.D[col0 + i];
@@ -360,10 +370,25 @@ __device__ __forceinline__ void warp_gtile_bwd(const SymDev& S, const GDev& GD, 
   double acc[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-  for (int r = (c0 & ~31) + lane; r < f; r += 32) {  // G(r, c) = 0 above the diagonal
+  const int nc = min(8, np - c0);
+  int r = (c0 & ~31) + lane;  // G(r, c) = 0 above the diagonal
+  for (; r + 32 < f; r += 64) {  // two row strips per round: 16 G loads in flight per lane
+    const int r2 = r + 32;
+    const double v1 = r < np ? GD.wz[col0 + r] : -xp[rows[r]];
+    const double v2 = r2 < np ? GD.wz[col0 + r2] : -xp[rows[r2]];
+    double g1[8], g2[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      g1[c] = c < nc ? G[(c0 + c) * f + r] : 0.0;
+      g2[c] = c < nc ? G[(c0 + c) * f + r2] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = fma(g2[c], v2, fma(g1[c], v1, acc[c]));
+  }
+  if (r < f) {
     const double v = r < np ? GD.wz[col0 + r] : -xp[rows[r]];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] = fma(c0 + c < np ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
+    for (int c = 0; c < 8; ++c) acc[c] = fma(c < nc ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
   }
 #pragma unroll
   for (int o = 4; o >= 1; o >>= 1) {
@@ -422,7 +447,7 @@ __global__ void __launch_bounds__(kSolveThreads, 4) k_sub_bwd(SymDev S, GDev GD,
 // ---------------------------------------------------------------------------
 template <bool GT, int MINB = 4>
 __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDev S, SolveDev T,
-                                                            const int2* __restrict__ tasks,
+                                                            const int2* __restrict__ tasks, int ntask,
                                                             const int32_t* __restrict__ wholes,
                                                             const double* __restrict__ panel,
                                                             const double* __restrict__ b,
@@ -432,21 +457,25 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDe
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int2 task = tasks[blockIdx.x];
+  // grid-stride over the level's tasks (the grid may be capped below ntask)
+  for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
+  const int2 task = tasks[ti];
   const int type = task.y >> 24, j = task.y & 0x00ffffff;
   if (GT && type == kGTiles) {
-    if (w >= j) return;
-    warp_gtile_fwd(S, T, GD, GD.tiles[task.x + w], b, xp, upd, y + w * kGMaxNp, lane);
-    return;
+    if (w < j) warp_gtile_fwd(S, T, GD, GD.tiles[task.x + w], b, xp, upd, y + w * kGMaxNp, lane);
+    __syncwarp();
+    continue;
   }
   if (!GT && type == kWholeGroup) {
     // warp w: small supernode wholes[task.x + w], whole front in a warp slice
-    if (w >= j) return;
-    if (stage && lane == 0) mbar_init(&wbar[w], 1);
+    if (w < j) {
+      if (stage && lane == 0) mbar_init(&wbar[w], 1);
+      __syncwarp();
+      warp_whole_fwd(S, T, wholes[task.x + w], panel, b, xp, upd, y + w * (stage ? kWarpSmem : kWholeMaxF), lane,
+                     stage ? &wbar[w] : nullptr);
+    }
     __syncwarp();
-    warp_whole_fwd(S, T, wholes[task.x + w], panel, b, xp, upd, y + w * (stage ? kWarpSmem : kWholeMaxF), lane,
-                   stage ? &wbar[w] : nullptr);
-    return;
+    continue;
   }
   const int s = task.x;
   const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
@@ -475,12 +504,14 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDe
       for (int q = 0; q < kSolveWarps; ++q) v -= part[q][lane];
       upd[S.upd_off[s] + r - np] = v;
     }
+    __syncthreads();  // part[] is reused by the next task of this CTA
+  }
   }
 }
 
 template <bool GT, int MINB = 4>
 __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDev S, SolveDev T,
-                                                            const int2* __restrict__ tasks,
+                                                            const int2* __restrict__ tasks, int ntask,
                                                             const int32_t* __restrict__ wholes,
                                                             const double* __restrict__ panel,
                                                             const double* __restrict__ D,
@@ -491,20 +522,23 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDe
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int2 task = tasks[blockIdx.x];
+  for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
+  const int2 task = tasks[ti];
   const int type = task.y >> 24, bj = task.y & 0x00ffffff;
   if (GT && type == kGTiles) {
-    if (w >= bj) return;
-    warp_gtile_bwd(S, GD, GD.tiles[task.x + w], D, xp, x, lane);
-    return;
+    if (w < bj) warp_gtile_bwd(S, GD, GD.tiles[task.x + w], D, xp, x, lane);
+    __syncwarp();
+    continue;
   }
   if (!GT && type == kWholeGroup) {
-    if (w >= bj) return;
-    if (stage && lane == 0) mbar_init(&wbar[w], 1);
+    if (w < bj) {
+      if (stage && lane == 0) mbar_init(&wbar[w], 1);
+      __syncwarp();
+      warp_whole_bwd(S, wholes[task.x + w], panel, D, xp, x, y + w * (stage ? kWarpSmem : kWholeMaxF), lane,
+                     stage ? &wbar[w] : nullptr);
+    }
     __syncwarp();
-    warp_whole_bwd(S, wholes[task.x + w], panel, D, xp, x, y + w * (stage ? kWarpSmem : kWholeMaxF), lane,
-                   stage ? &wbar[w] : nullptr);
-    return;
+    continue;
   }
   const int s = task.x;
   const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
@@ -547,6 +581,8 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDe
         *c = inv ? *c - t : t;  // inverse path: cvec already holds z ./ d
       }
     }
+    __syncthreads();  // part[] is reused by the next task of this CTA
+  }
   }
 }
 
@@ -910,6 +946,7 @@ int build_solve_plan(riga_symbolic* sym) {
   // small supernodes through G = [inv(L11); L21 inv(L11)] (default) or substitution
   L.small_g = env_flag("RIGA_SMALL_G", 1);
   L.occ = env_flag("RIGA_REST_OCC", 4);  // CTAs per SM the G-mode level kernels are register-bounded for
+  L.rest_cap = env_flag("RIGA_REST_CAP", 1 << 30);  // CTAs per level launch (grid-stride over the tasks)
   L.g_off.assign(ns, -1);
   L.inv_off.assign(ns, -1);
   L.ifwd_ptr.assign(h.nlevels + 1, 0);
@@ -1245,7 +1282,7 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     const int nt = (int)(L.fwd_ptr[l + 1] - L.fwd_ptr[l]);
     if (nt) {
       (gon ? (L.occ == 8 ? k_rest_fwd<true, 8> : L.occ == 6 ? k_rest_fwd<true, 6> : k_rest_fwd<true, 4>)
-           : k_rest_fwd<false>)<<<nt, kSolveThreads, L.fwd_smem[l], st>>>(S, T, tf + L.fwd_ptr[l], sym->d_wholes.p,
+           : k_rest_fwd<false>)<<<std::min(nt, L.rest_cap), kSolveThreads, L.fwd_smem[l], st>>>(S, T, tf + L.fwd_ptr[l], nt, sym->d_wholes.p,
                                                            F->panel.p, b, F->xperm.p, F->upd.p, L.warp_stage, GDf);
       count_launch();
     }
@@ -1254,7 +1291,7 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     const int nt = (int)(L.bwd_ptr[l + 1] - L.bwd_ptr[l]);
     if (nt) {
       (gon ? (L.occ == 8 ? k_rest_bwd<true, 8> : L.occ == 6 ? k_rest_bwd<true, 6> : k_rest_bwd<true, 4>)
-           : k_rest_bwd<false>)<<<nt, kSolveThreads, L.bwd_smem[l], st>>>(S, T, tb + L.bwd_ptr[l], sym->d_wholes.p,
+           : k_rest_bwd<false>)<<<std::min(nt, L.rest_cap), kSolveThreads, L.bwd_smem[l], st>>>(S, T, tb + L.bwd_ptr[l], nt, sym->d_wholes.p,
                                                            F->panel.p, F->D.p, F->xperm.p, F->cvec.p, x, L.warp_stage,
                                                            L.chain_inv, GDb);
       count_launch();

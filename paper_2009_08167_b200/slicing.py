@@ -284,8 +284,9 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                     if idx:
                         X = torch.stack([pool.vecs[i] for i in idx])
                         if vectors_to_host:
-                            # pinned staging + async copy on the slice stream
-                            # (a pageable .cpu() would serialise the slices)
+                            # pinned staging (torch's caching host allocator)
+                            # + async copy on the slice stream: a pageable
+                            # .cpu() would serialise the slices
                             H = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
                             H.copy_(X, non_blocking=True)
                             ctx.synchronize()

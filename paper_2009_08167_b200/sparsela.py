@@ -75,13 +75,13 @@ class CostCounters:
 
     trace: list | None = None  # (phase, t_start, t_end, thread) when RIGA_TRACE=1
 
-    def phase(self, name: str, dt: float) -> None:
+    def phase(self, name: str, dt: float, steps: int = 0) -> None:
         self.phase_s[name] = self.phase_s.get(name, 0.0) + dt
         if _TRACE and name != "cgs_rows":
             t1 = time.perf_counter()
             if self.trace is None:
                 self.trace = []
-            self.trace.append((name, t1 - dt, t1, threading.get_ident()))
+            self.trace.append((name, t1 - dt, t1, threading.get_ident(), steps))
 
     @property
     def nfa(self) -> int:

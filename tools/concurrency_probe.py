@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--what", default="extend", choices=["extend", "solve", "solveg"])
     ap.add_argument("--threads", default="1,2,4,8,16")
+    ap.add_argument("--prelock", type=int, default=0, help="lock this many random rows first (R = k + locked)")
+    ap.add_argument("--cycles", type=int, default=1, help="extend cycles per thread (thick restart keep 8 between)")
     a = ap.parse_args()
     c = CONFIGS[a.config]
     s = P.build_system(c.d, c.ne, c.p, c.level)
@@ -41,6 +43,12 @@ def main():
                 f = numeric_factor(sym, float(sh[i % c.slices]), ctx)
                 st = P.LanczosState(DeviceShiftInvert(f, s.M), s.dof_count, mass=s.M, shift=f.sigma,
                                     max_dim=a.steps + 1, rng=np.random.default_rng(i), ctx=ctx)
+                if a.prelock:
+                    g = torch.Generator(device="cuda").manual_seed(i)
+                    X = torch.randn(a.prelock, s.dof_count, dtype=torch.float64, device="cuda", generator=g)
+                    X /= X.norm(dim=1, keepdim=True)
+                    for q in range(a.prelock):
+                        st.lock(X[q], X[q])
                 facts.append(f)
                 states.append(st)
         torch.cuda.synchronize()
@@ -65,7 +73,10 @@ def main():
             bar.wait()
             with ctxs[i]:
                 if a.what == "extend":
-                    P.lanczos_extend(states[i], a.steps)
+                    for cyc in range(a.cycles):
+                        if cyc:
+                            P.thick_restart(states[i], 8)
+                        P.lanczos_extend(states[i], a.steps)
                 elif a.what == "solveg":
                     for _ in range(a.steps // 20):
                         graphs[i][0].replay()
@@ -83,7 +94,8 @@ def main():
         for t in th:
             t.join()
         dt = time.perf_counter() - t0
-        print(f"{a.what} threads={T:2d}: {T * a.steps / dt:8.1f} steps/s aggregate, "
+        tot = T * (a.steps + (a.cycles - 1) * (a.steps - 8)) if a.what == "extend" else T * a.steps
+        print(f"{a.what} threads={T:2d} cycles={a.cycles}: {tot / dt:8.1f} steps/s aggregate, "
               f"{dt * 1e3 / a.steps:7.3f} ms per step per thread", flush=True)
         del facts, states, ctxs
         torch.cuda.synchronize()

@@ -29,17 +29,25 @@ print("phase seconds summed over slices", {k: round(v, 3) for k, v in r.counters
 if r.counters.trace and len(r.counters.trace) < 100000:
     # slices per phase over time (50 ms bins, relative to the first event)
     tr = r.counters.trace
-    t0 = min(a for _, a, _, _ in tr)
-    t1 = max(b for _, _, b, _ in tr)
+    t0 = min(e[1] for e in tr)
+    t1 = max(e[2] for e in tr)
     names = sorted({n for n, *_ in tr})
     nb = int((t1 - t0) / 0.05) + 1
     occ = {n: np.zeros(nb) for n in names}
-    for n, a, b, _ in tr:
+    rate = np.zeros(nb)
+    for n, a, b, _, st in tr:
+        if st and b > a:  # steps spread uniformly over the extend call
+            for i in range(nb):
+                lo, hi = t0 + 0.05 * i, t0 + 0.05 * (i + 1)
+                ov = min(b, hi) - max(a, lo)
+                if ov > 0:
+                    rate[i] += st * ov / (b - a) / 0.05
+    for n, a, b, _, _ in tr:
         for i in range(nb):
             lo, hi = t0 + 0.05 * i, t0 + 0.05 * (i + 1)
             ov = min(b, hi) - max(a, lo)
             if ov > 0:
                 occ[n][i] += ov / 0.05
-    print("bin_ms " + " ".join(f"{n[:7]:>7s}" for n in names))
+    print("bin_ms " + " ".join(f"{n[:7]:>7s}" for n in names) + "  steps/s")
     for i in range(nb):
-        print(f"{50 * i:6d} " + " ".join(f"{occ[n][i]:7.2f}" for n in names))
+        print(f"{50 * i:6d} " + " ".join(f"{occ[n][i]:7.2f}" for n in names) + f" {rate[i]:8.0f}")
