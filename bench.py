@@ -168,45 +168,56 @@ def reference_arm(args):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons during the timed region, sampled in-process
+    through NVML (the library nvidia-smi reads) every 250 ms on a daemon
+    thread; falls back to an nvidia-smi subprocess if NVML is unavailable."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
-        import subprocess
+        import threading
 
-        self.p = None
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.stop_ev = threading.Event()
+        self.ok = False
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.bits = {"hw_slowdown": pynvml.nvmlClocksThrottleReasonHwSlowdown,
+                         "hw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                         "sw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                         "sw_power_cap": pynvml.nvmlClocksThrottleReasonSwPowerCap}
+            self.ok = True
         except Exception:
-            self.p = None
+            self.ok = False
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            if self.ok:
+                try:
+                    nv = self.nv
+                    self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                    self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                    for nm in self.NAMES:
+                        if r & self.bits[nm]:
+                            self.reasons.add(nm)
+                except Exception:
+                    pass
+            self.stop_ev.wait(0.25)
 
     def stop(self):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        out, _ = self.p.communicate()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 6:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(max(mx)) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self.stop_ev.set()
+        self.t.join()
+        if not self.ok or not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": float(max(self.mx)),
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "NVML (in-process)"}
 
 
 def kernel_roofline(P, D, L, system, shifts, sym, perm, c, flush, reps=10):
@@ -491,6 +502,7 @@ def ours(args):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             dsys = DeviceSystem.upload(ctx, Kh, Mh)
+            dsys.attach_kron(system.k1d, system.m1d)  # the public DiscreteSystem's 1D factors
             sys2 = DiscreteSystem(SymSparseMatrix(device=dsys, which=0), SymSparseMatrix(device=dsys, which=1),
                                   system.spaces, system.dim, system.dof_count, system.k1d, system.m1d, dsys)
             perm2 = P.separator_ordering(sys2)

@@ -78,6 +78,13 @@ int riga_system_assemble_kron(riga_ctx* ctx, int dim, const int64_t* n1,
                               const int64_t* const* rowptr1, const int32_t* const* colidx1,
                               const double* const* k1, const double* const* m1,
                               riga_system** out);
+/* Attach 1D factors to an uploaded pencil whose M is M_z (x) M_y (x) M_x
+ * (arguments as riga_system_assemble_kron; n must equal prod n1): the
+ * Lanczos mass products then run axis by axis instead of over the CSR.
+ * The caller asserts the Kronecker structure (DiscreteSystem.m1d).        */
+int riga_system_set_kron(riga_system* sys, int dim, const int64_t* n1,
+                         const int64_t* const* rowptr1, const int32_t* const* colidx1,
+                         const double* const* k1, const double* const* m1);
 int riga_system_info(riga_system* sys, int64_t* n, int64_t* nnz);
 int riga_system_download(riga_system* sys, int64_t* rowptr_host, int32_t* colidx_host,
                          double* K_host, double* M_host);

@@ -30,6 +30,21 @@ class DeviceSystem:
         self.handle, self.ctx, self.n, self.nnz = handle, ctx, n, nnz
         self._host = None
 
+    def attach_kron(self, k1d, m1d) -> None:
+        """Declare M = M_z (x) M_y (x) M_x (1D factors in x-fastest order, as
+        DiscreteSystem.k1d / m1d): Lanczos mass products then run axis by axis
+        (riga_system_set_kron)."""
+        d = len(m1d)
+        parts_k = [_csr_parts(sp.csr_array(k)) for k in k1d]
+        parts_m = [_csr_parts(sp.csr_array(m)) for m in m1d]
+        n1 = np.array([m.shape[0] for m in m1d], dtype=np.int64)
+        P = ctypes.c_void_p * d
+        rps = P(*[_lib.ptr(q[0]).value for q in parts_m])
+        cis = P(*[_lib.ptr(q[1]).value for q in parts_m])
+        kvs = P(*[_lib.ptr(q[2]).value for q in parts_k])
+        mvs = P(*[_lib.ptr(q[2]).value for q in parts_m])
+        _lib.check(_lib.lib().riga_system_set_kron(self.handle, d, _lib.ptr(n1), rps, cis, kvs, mvs), "set_kron")
+
     def host_arrays(self):
         if self._host is None:
             rp = np.empty(self.n + 1, np.int64)

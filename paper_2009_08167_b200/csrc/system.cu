@@ -499,6 +499,28 @@ int riga_system_assemble_kron(riga_ctx* ctx, int dim, const int64_t* n1,
   return RIGA_OK;
 }
 
+int riga_system_set_kron(riga_system* sys, int dim, const int64_t* n1, const int64_t* const* rowptr1,
+                         const int32_t* const* colidx1, const double* const* k1, const double* const* m1) {
+  RIGA_CHECK_ARG(sys && n1 && rowptr1 && colidx1 && k1 && m1, "null arg");
+  RIGA_CHECK_ARG(dim >= 1 && dim <= 3, "dim must be 1, 2 or 3");
+  int64_t n = 1;
+  for (int t = 0; t < dim; ++t) n *= n1[t];
+  RIGA_CHECK_ARG(n == sys->n, "1D factor sizes do not multiply to the system size");
+  DeviceGuard g(sys->ctx->device);
+  cudaStream_t s = sys->ctx->stream;
+  for (int t = 0; t < dim; ++t) {
+    const int64_t nt = n1[t], zt = rowptr1[t][nt];
+    sys->kax[t].n = nt;
+    RIGA_TRY(sys->kax[t].rp.upload(rowptr1[t], nt + 1, s));
+    RIGA_TRY(sys->kax[t].ci.upload(colidx1[t], zt, s));
+    RIGA_TRY(sys->kax[t].k.upload(k1[t], zt, s));
+    RIGA_TRY(sys->kax[t].m.upload(m1[t], zt, s));
+  }
+  RIGA_CUDA(stream_sync(s));
+  sys->kdim = dim;
+  return RIGA_OK;
+}
+
 int riga_system_info(riga_system* sys, int64_t* n, int64_t* nnz) {
   RIGA_CHECK_ARG(sys, "null system");
   if (n) *n = sys->n;

@@ -89,25 +89,36 @@ class SlicesResult:
     factor_ms: list = field(default_factory=list)
 
 
-_ctx_free: dict = {}
+_ctx_cache: dict = {}
 _ctx_lock = threading.Lock()
+_ctx_busy: set = set()
 
 
-def _take_ctx(device: int, priority: int = 0):
-    """A slice-worker context (own stream) from a per-(device, priority) free
-    list: streams are reused across calls, so torch's per-stream block cache
-    and the engine pool do not fragment over many calls."""
+def _take_ctx(device: int, key, priority: int = 0):
+    """The worker context (own stream) for `key` -- ("slice", k) or
+    ("boundary", i) -- reused across calls with the same key: slice k always
+    runs on the same stream, so its pooled Lanczos state (device buffers and
+    captured step graph, eigensolver._state_pool) is hit on every call and
+    torch's per-stream block cache does not fragment."""
     with _ctx_lock:
-        lst = _ctx_free.setdefault((device, priority), [])
-        if lst:
-            return lst.pop()
-    return _dev.Context(device, priority=priority)
+        ck = (device, key, priority)
+        ctx = _ctx_cache.get(ck)
+        if ctx is None or ck in _ctx_busy:  # a concurrent call holds it: a private one
+            ctx = _dev.Context(device, priority=priority)
+            if ck not in _ctx_cache:
+                _ctx_cache[ck] = ctx
+        if _ctx_cache.get(ck) is ctx:
+            _ctx_busy.add(ck)
+        ctx._cache_key = ck
+        return ctx
 
 
 def _give_ctx(ctx) -> None:
     ctx.synchronize()
     with _ctx_lock:
-        _ctx_free.setdefault((ctx.device, ctx.priority), []).append(ctx)
+        ck = getattr(ctx, "_cache_key", None)
+        if ck is not None and _ctx_cache.get(ck) is ctx:
+            _ctx_busy.discard(ck)
 
 
 def _priorities(work: list) -> list:
@@ -194,15 +205,46 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     bnd = {}
     scale = float(shifts[-1] - shifts[0]) if S else 1.0
     bcnt = CostCounters()
-    pen0 = make_pencil(base_ctx, bcnt)
     kept = {}
-    with torch.cuda.stream(base_ctx.stream):
-        for k in mine_b:
-            sig, fact = pen0.factor(float(shifts[k]), scale)
-            bnd[k] = (sig, fact.n_negative, fact.device_ms)
-            if k < S and keep_factors:
-                kept[k] = (sig, fact)
-            del fact
+    # independent factorizations on several streams at once (a small front
+    # tree leaves most of the GPU idle); concurrency capped by the transient
+    # update-block memory each one needs
+    nbw = int(max(1, min(8, len(mine_b), (0.5 * budget) // max(fac_bytes + cb_bytes, 1.0))))
+    bq = list(mine_b)
+    blk = threading.Lock()
+    berr = []
+
+    def bworker(bi):
+        ctx = _take_ctx(base_ctx.device, ("boundary", bi), 0)
+        cnt = CostCounters()
+        pen = make_pencil(ctx, cnt)
+        with ctx:
+            while True:
+                with blk:
+                    if not bq or berr:
+                        break
+                    k = bq.pop(0)
+                try:
+                    sig, fact = pen.factor(float(shifts[k]), scale)
+                    with blk:
+                        bnd[k] = (sig, fact.n_negative, fact.device_ms)
+                        if k < S and keep_factors:
+                            kept[k] = (sig, fact)
+                    del fact
+                except Exception as e:  # surfaced after join
+                    with blk:
+                        berr.append(e)
+        with blk:
+            bcnt.merge(cnt)
+        _give_ctx(ctx)
+
+    bth = [threading.Thread(target=bworker, args=(i,)) for i in range(nbw)]
+    for t in bth:
+        t.start()
+    for t in bth:
+        t.join()
+    if berr:
+        raise berr[0]
     counters.merge(bcnt)
     counters.nsh += len(mine_b)
     allb = {}
@@ -241,7 +283,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     prio = _priorities([int(expected[k]) for k in order]) if one_per_thread else [0] * len(order)
 
     def worker(widx):
-        ctx = _take_ctx(base_ctx.device, prio[widx])
+        ctx = _take_ctx(base_ctx.device, ("slice", order[widx] if one_per_thread else widx), prio[widx])
         cnt = CostCounters()
         mine = [order[widx]] if one_per_thread else None
         with ctx:
@@ -287,7 +329,9 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                             # pinned staging (torch's caching host allocator)
                             # + async copy on the slice stream: a pageable
                             # .cpu() would serialise the slices
+                            _tp = time.perf_counter()
                             H = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
+                            cnt.phase("collect_pin", time.perf_counter() - _tp)
                             H.copy_(X, non_blocking=True)
                             ctx.synchronize()
                             X = H.numpy()

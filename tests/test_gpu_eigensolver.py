@@ -278,3 +278,26 @@ def test_cfg5_slices_match_kronecker_spectrum(golden):
         r = P.solve_slice(s, (lo, hi), seed=k, m=2 * ref.size)
         assert r.expected_count == ref.size == r.eigenvalues.size == c["slice_counts"][k]
         np.testing.assert_allclose(r.eigenvalues, ref, rtol=1e-10)
+
+
+def test_uploaded_pencil_with_kron_factors_matches_device_assembly():
+    """Host CSR upload + attach_kron (the e2e path of bench.py): Lanczos mass
+    products run axis by axis on the uploaded pencil; the slice must agree
+    with the device-assembled system's to roundoff and keep the counts."""
+    from paper_2009_08167_b200 import device as D
+    from paper_2009_08167_b200.assembly import DeviceSystem, DiscreteSystem, SymSparseMatrix
+
+    s = P.build_system(2, 16, 3, 2)
+    lam = dense_eig(s)
+    hi = 0.5 * (lam[14] + lam[15])
+    dsys = DeviceSystem.upload(D.current(), s.K.csr.copy(), s.M.csr.copy())
+    dsys.attach_kron(s.k1d, s.m1d)
+    s2 = DiscreteSystem(SymSparseMatrix(device=dsys, which=0), SymSparseMatrix(device=dsys, which=1),
+                        s.spaces, s.dim, s.dof_count, s.k1d, s.m1d, dsys)
+    r1 = P.solve_slice(s, (0.0, hi), seed=3, m=30)
+    r2 = P.solve_slice(s2, (0.0, hi), seed=3, m=30)
+    assert r1.expected_count == r2.expected_count == 15
+    assert np.allclose(r2.eigenvalues, lam[:15], rtol=1e-10, atol=0)
+    assert np.allclose(r1.eigenvalues, r2.eigenvalues, rtol=1e-11, atol=0)
+    with pytest.raises(ValueError):
+        dsys.attach_kron(s.k1d[:1], s.m1d[:1])  # sizes do not multiply to n

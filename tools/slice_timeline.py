@@ -13,6 +13,9 @@ lam_e, cnt = P.choose_lambda_e(s, c.n0)
 sh = P.uniform_shifts(lam_e, c.slices)
 perm = P.separator_ordering(s)
 sym = Symbolic.on_device(s.device, perm)
+import gc
+if os.environ.get('NOGC'):
+    gc.disable()
 for it in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
     t0 = time.perf_counter()
     c0 = os.times()
