@@ -9,6 +9,38 @@ namespace riga {
 
 constexpr int kDotScratch = 1024;  // doubles of device scratch per reduction
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// The Lanczos step is a chain of ~60 dependent small kernels replayed as a
+// CUDA graph; launched with programmatic stream serialization, kernel N+1's
+// CTAs are scheduled while kernel N drains, and wait in pdl_start() until N
+// has completed and its writes are visible.  pdl_start() is the first
+// statement of every step kernel (no global access before it, so no
+// read-after-write or write-after-read hazard with the predecessor); the
+// trigger after the wait lets the successor launch one kernel ahead only.
+// Outside a PDL launch both instructions are no-ops.
+__device__ __forceinline__ void pdl_start() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+extern bool g_pdl;  // RIGA_PDL=1 enables
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 __host__ __device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ double warp_sum(double v) {

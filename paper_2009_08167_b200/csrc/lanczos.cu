@@ -82,6 +82,7 @@ constexpr int kDotGrid = 2 * 148;
 __global__ void __launch_bounds__(256, 2) k_cgs_dots(RowSel A, const LzDev* st, int64_t n, int64_t Rmax,
                                                      const double* __restrict__ x, double* __restrict__ partial,
                                                      double* __restrict__ coef, unsigned* __restrict__ tickets) {
+  pdl_start();
   if (st->stop) return;
   int64_t na, nb;
   rows_of(A, st, na, nb);
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(256, 2) k_cgs_dots(RowSel A, const LzDev* st, 
 __global__ void __launch_bounds__(256) k_cgs_upd(RowSel A, const LzDev* st, int64_t n, int64_t ldu,
                                                  const double* __restrict__ coef, double* __restrict__ upart,
                                                  double* __restrict__ y, unsigned* __restrict__ tickets) {
+  pdl_start();
   if (st->stop) return;
   __shared__ double cs[1024];
   __shared__ bool last;
@@ -225,6 +227,7 @@ __global__ void __launch_bounds__(256, 2) k_dcgs_dots(RowSel A, const LzDev* st,
                                                       const double* __restrict__ Vbase,
                                                       const double* __restrict__ x2, double* __restrict__ partial,
                                                       double* __restrict__ coef, unsigned* __restrict__ tickets) {
+  pdl_start();
   if (st->stop) return;
   int64_t na, nb;
   rows_of(A, st, na, nb);
@@ -310,6 +313,7 @@ __global__ void __launch_bounds__(256, 2) k_dcgs_dots(RowSel A, const LzDev* st,
 // scal: [0] alpha, [1] |w|^2, [5] eta, [6] coefficient of v
 __global__ void __launch_bounds__(256) k_dcgs_scalars(LzDev* st, int64_t Rmax, double* __restrict__ coef,
                                                       double* __restrict__ cpl, double* __restrict__ ob) {
+  pdl_start();
   if (st->stop) return;
   __shared__ double red[32];
   const int k = st->k, clo = st->clo;
@@ -356,6 +360,7 @@ __global__ void __launch_bounds__(256) k_dcgs_upd(RowSel A, const LzDev* st, int
                                                   double* __restrict__ upart, const double* __restrict__ w,
                                                   double* __restrict__ vt, double* __restrict__ r,
                                                   unsigned* __restrict__ tickets) {
+  pdl_start();
   if (st->stop) return;
   __shared__ double cs[2][1024];
   __shared__ bool last;
@@ -438,6 +443,7 @@ __global__ void __launch_bounds__(256) k_dcgs_upd(RowSel A, const LzDev* st, int
 __global__ void k_dcgs_store(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ vt,
                              const double* __restrict__ mvt, const double* __restrict__ r,
                              const double* __restrict__ Mr, double* __restrict__ V, double* __restrict__ MV) {
+  pdl_start();
   if (st->stop) return;
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
@@ -469,6 +475,7 @@ __global__ void k_dot2(const LzDev* st, int64_t n, int64_t ld, const double* __r
                        const double* __restrict__ b, const double* __restrict__ c,
                        const double* __restrict__ d, double* __restrict__ partial,
                        unsigned* __restrict__ ticket, double* __restrict__ out) {
+  pdl_start();
   if (st->stop) return;
   __shared__ double red[32];
   __shared__ bool last;
@@ -507,6 +514,7 @@ __global__ void k_dot2(const LzDev* st, int64_t n, int64_t ld, const double* __r
 // bp[j] = MV[k][order[j]]: the solve's right-hand side in elimination order
 __global__ void k_perm_row(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ MV,
                            const int32_t* __restrict__ order, double* __restrict__ bp) {
+  pdl_start();
   if (st->stop) return;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j < n) bp[j] = MV[(int64_t)st->k * ld + order[j]];
@@ -516,6 +524,7 @@ __global__ void k_perm_row(const LzDev* st, int64_t n, int64_t ld, const double*
 __global__ void k_residual(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ w,
                            const double* __restrict__ V, const double* __restrict__ cpl,
                            double* __restrict__ r) {
+  pdl_start();
   if (st->stop) return;
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
@@ -540,6 +549,7 @@ __device__ __forceinline__ bool broke_down(const LzDev* st, double& beta, double
 __global__ void k_normalize_next(const LzDev* st, int64_t n, int64_t ld, const double* __restrict__ r,
                                  const double* __restrict__ Mr, double* __restrict__ V,
                                  double* __restrict__ MV) {
+  pdl_start();
   if (st->stop) return;
   double beta, wn;
   if (broke_down(st, beta, wn)) return;
@@ -553,6 +563,7 @@ __global__ void k_normalize_next(const LzDev* st, int64_t n, int64_t ld, const d
 // bookkeeping of a finished step (one thread)
 __global__ void k_step_finish(LzDev* st, double* __restrict__ cpl, double* __restrict__ oa,
                               double* __restrict__ ob, double* __restrict__ ow) {
+  pdl_start();
   if (st->stop) return;
   double beta, wn;
   const bool broke = broke_down(st, beta, wn);
@@ -877,12 +888,12 @@ int cgs_passes(riga_lanczos* lz, RowSel dots, RowSel upd, RowSel upd2, double* r
   const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
   for (int p = 0; p < passes; ++p) {
     ProfScope prof(kProfCgs, s, 2.0 * (double)rows_hint * lz->n * 8.0);
-    k_cgs_dots<<<kDotGrid, 256, 0, s>>>(dots, lz->st.p, lz->n, Rmax, r, lz->partial.p, lz->coef.p,
-                                        lz->tk_dots.p);
-    k_cgs_upd<<<gu, 256, 0, s>>>(upd, lz->st.p, lz->n, lz->ld, lz->coef.p, lz->upart.p, r, lz->tk_upd.p);
+    RIGA_CUDA(launch(k_cgs_dots, kDotGrid, 256, 0, s, dots, lz->st.p, lz->n, Rmax, r, lz->partial.p, lz->coef.p,
+                                        lz->tk_dots.p));
+    RIGA_CUDA(launch(k_cgs_upd, gu, 256, 0, s, upd, lz->st.p, lz->n, lz->ld, lz->coef.p, lz->upart.p, r, lz->tk_upd.p));
     count_launch(2);
     if (r2) {
-      k_cgs_upd<<<gu, 256, 0, s>>>(upd2, lz->st.p, lz->n, lz->ld, lz->coef.p, lz->upart.p, r2, lz->tk_upd.p);
+      RIGA_CUDA(launch(k_cgs_upd, gu, 256, 0, s, upd2, lz->st.p, lz->n, lz->ld, lz->coef.p, lz->upart.p, r2, lz->tk_upd.p));
       count_launch();
     }
   }
@@ -903,9 +914,9 @@ int dot2(riga_lanczos* lz, const double* a, int koff_a, const double* b, const d
   cudaStream_t s = lz->cur;
   ProfScope prof(kProfVec, s, 32.0 * lz->n);
   const int blocks = (int)std::min<int64_t>(296, (lz->n + 255) / 256);
-  k_dot2<<<blocks, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, a, koff_a, b, c, d, lz->dscratch.p,
+  RIGA_CUDA(launch(k_dot2, blocks, 256, 0, s, lz->st.p, lz->n, lz->ld, a, koff_a, b, c, d, lz->dscratch.p,
                                 reinterpret_cast<unsigned*>(lz->dscratch.p + 2 * 296),
-                                lz->st.p->scal + slot);
+                                lz->st.p->scal + slot));
   count_launch();
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
@@ -916,16 +927,16 @@ int step_tail(riga_lanczos* lz) {
   cudaStream_t s = lz->cur;
   const unsigned g1 = (unsigned)((lz->n + 255) / 256);
   RIGA_TRY(dot2(lz, lz->MV.p, 1, lz->w.p, lz->w.p, lz->w.p, 0));  // alpha, |w|^2
-  k_residual<<<g1, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->w.p, lz->V.p, lz->cpl.p, lz->r.p);
+  RIGA_CUDA(launch(k_residual, g1, 256, 0, s, lz->st.p, lz->n, lz->ld, lz->w.p, lz->V.p, lz->cpl.p, lz->r.p));
   count_launch();
   RIGA_TRY(cgs_passes(lz, sel_basis(lz, true, 1), sel_basis(lz, false, 1), RowSel{}, lz->r.p, nullptr, 2,
                       lz->k + 1 + lz->nlocked));
   RIGA_TRY(mass_apply(lz, lz->r.p, lz->Mr.p));
   RIGA_TRY(dot2(lz, lz->r.p, 0, lz->Mr.p, lz->r.p, lz->Mr.p, 2));  // beta^2
-  k_normalize_next<<<g1, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->r.p, lz->Mr.p, lz->V.p, lz->MV.p);
+  RIGA_CUDA(launch(k_normalize_next, g1, 256, 0, s, lz->st.p, lz->n, lz->ld, lz->r.p, lz->Mr.p, lz->V.p, lz->MV.p));
   count_launch();
-  k_step_finish<<<1, 1, 0, s>>>(lz->st.p, lz->cpl.p, lz->outs.p, lz->outs.p + (lz->max_dim + 1),
-                                lz->outs.p + 2 * (lz->max_dim + 1));
+  RIGA_CUDA(launch(k_step_finish, 1, 1, 0, s, lz->st.p, lz->cpl.p, lz->outs.p, lz->outs.p + (lz->max_dim + 1),
+                                lz->outs.p + 2 * (lz->max_dim + 1)));
   count_launch();
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
@@ -935,7 +946,7 @@ int step_tail(riga_lanczos* lz) {
 int step_full(riga_lanczos* lz) {
   cudaStream_t s = lz->cur;
   const unsigned g1 = (unsigned)((lz->n + 255) / 256);
-  k_perm_row<<<g1, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->MV.p, lz->op->sym->d_order.p, lz->bp.p);
+  RIGA_CUDA(launch(k_perm_row, g1, 256, 0, s, lz->st.p, lz->n, lz->ld, lz->MV.p, lz->op->sym->d_order.p, lz->bp.p));
   count_launch();
   RIGA_TRY(factor_solve(lz->op, s, lz->bp.p, lz->w.p, true));
   if (!lz->delayed) return step_tail(lz);
@@ -944,20 +955,20 @@ int step_full(riga_lanczos* lz) {
   double* ob = lz->outs.p + (lz->max_dim + 1);
   {
     ProfScope prof(kProfCgs, s, 2.0 * (double)(lz->k + 1 + lz->nlocked) * lz->n * 8.0);
-    k_dcgs_dots<<<kDotGrid, 256, 0, s>>>(sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, lz->w.p,
-                                         lz->partial.p, lz->coef.p, lz->tk_dots.p);
-    k_dcgs_scalars<<<1, 256, 0, s>>>(lz->st.p, Rmax, lz->coef.p, lz->cpl.p, ob);
+    RIGA_CUDA(launch(k_dcgs_dots, kDotGrid, 256, 0, s, sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, lz->w.p,
+                                         lz->partial.p, lz->coef.p, lz->tk_dots.p));
+    RIGA_CUDA(launch(k_dcgs_scalars, 1, 256, 0, s, lz->st.p, Rmax, lz->coef.p, lz->cpl.p, ob));
     const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
-    k_dcgs_upd<<<gu, 256, 0, s>>>(sel_basis(lz, false, 1), lz->st.p, lz->n, lz->ld, Rmax, lz->coef.p,
-                                  lz->upart.p, lz->w.p, lz->vt.p, lz->r.p, lz->tk_upd.p);
+    RIGA_CUDA(launch(k_dcgs_upd, gu, 256, 0, s, sel_basis(lz, false, 1), lz->st.p, lz->n, lz->ld, Rmax, lz->coef.p,
+                                  lz->upart.p, lz->w.p, lz->vt.p, lz->r.p, lz->tk_upd.p));
     count_launch(3);
   }
   RIGA_TRY(mass_apply(lz, lz->vt.p, lz->mvt.p));
   RIGA_TRY(mass_apply(lz, lz->r.p, lz->Mr.p));
   RIGA_TRY(dot2(lz, lz->r.p, 0, lz->Mr.p, lz->r.p, lz->Mr.p, 2));  // beta~^2
-  k_dcgs_store<<<g1, 256, 0, s>>>(lz->st.p, lz->n, lz->ld, lz->vt.p, lz->mvt.p, lz->r.p, lz->Mr.p, lz->V.p,
-                                  lz->MV.p);
-  k_step_finish<<<1, 1, 0, s>>>(lz->st.p, lz->cpl.p, lz->outs.p, ob, lz->outs.p + 2 * (lz->max_dim + 1));
+  RIGA_CUDA(launch(k_dcgs_store, g1, 256, 0, s, lz->st.p, lz->n, lz->ld, lz->vt.p, lz->mvt.p, lz->r.p, lz->Mr.p, lz->V.p,
+                                  lz->MV.p));
+  RIGA_CUDA(launch(k_step_finish, 1, 1, 0, s, lz->st.p, lz->cpl.p, lz->outs.p, ob, lz->outs.p + 2 * (lz->max_dim + 1)));
   count_launch(2);
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;

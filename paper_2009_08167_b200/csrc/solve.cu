@@ -421,6 +421,7 @@ __device__ __forceinline__ void warp_gtile_bwd(const SymDev& S, const GDev& GD, 
 __global__ void __launch_bounds__(kSolveThreads, 4) k_sub_fwd(SymDev S, SolveDev T, GDev GD,
                                                               const int32_t* __restrict__ sub_ptr, int SL,
                                                               const double* __restrict__ b, double* xp, double* upd) {
+  pdl_start();
   __shared__ double y[kSolveWarps * kGMaxNp];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
@@ -434,6 +435,7 @@ __global__ void __launch_bounds__(kSolveThreads, 4) k_sub_fwd(SymDev S, SolveDev
 __global__ void __launch_bounds__(kSolveThreads, 4) k_sub_bwd(SymDev S, GDev GD, const int32_t* __restrict__ sub_ptr,
                                                               int SL, const double* __restrict__ D, double* xp,
                                                               double* x) {
+  pdl_start();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
   for (int j = SL - 1; j >= 0; --j) {
@@ -453,6 +455,7 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDe
                                                             const double* __restrict__ b,
                                                             double* __restrict__ xp,
                                                             double* __restrict__ upd, int stage, GDev GD) {
+  pdl_start();
   extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
@@ -518,6 +521,7 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDe
                                                             double* __restrict__ xp,
                                                             double* __restrict__ cvec,
                                                             double* __restrict__ x, int stage, int inv, GDev GD) {
+  pdl_start();
   extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
@@ -630,6 +634,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_chain_fwd(SymDev S, SolveDev 
                                                              const double* __restrict__ b,
                                                              double* __restrict__ xp,
                                                              const double* __restrict__ upd) {
+  pdl_start();
   extern __shared__ double y[];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = nodes[blockIdx.x];
@@ -689,6 +694,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_chain_bwd(SymDev S, const int
                                                              double* __restrict__ xp,
                                                              const double* __restrict__ cvec,
                                                              double* __restrict__ x) {
+  pdl_start();
   extern __shared__ double y[];
   __shared__ double red[kSolveWarps][32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -854,6 +860,7 @@ __global__ void __launch_bounds__(256) k_inv_fwd(SymDev S, SolveDev T, const int
                                                  const double* __restrict__ D, const double* __restrict__ b,
                                                  double* __restrict__ xp, const double* __restrict__ upd,
                                                  double* __restrict__ cvec) {
+  pdl_start();
   extern __shared__ double y[];
   __shared__ double part[8][32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -889,6 +896,7 @@ __global__ void __launch_bounds__(256) k_inv_bwd(SymDev S, const int2* __restric
                                                  const double* __restrict__ linv,
                                                  const double* __restrict__ cvec, double* __restrict__ xp,
                                                  double* __restrict__ x) {
+  pdl_start();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int s = tasks[blockIdx.x].x;
   const int np = (int)S.ncol[s];
@@ -911,6 +919,7 @@ __global__ void __launch_bounds__(256) k_inv_bwd(SymDev S, const int2* __restric
 // kernels' latency-bound loads hit L2 (the factor of a 2D config fits in the
 // 126 MB L2, but the Gram-Schmidt traffic of the previous step evicts it)
 __global__ void k_prefetch_l2(const double* __restrict__ p, int64_t bytes) {
+  pdl_start();
   const int64_t chunk = 32768;
   for (int64_t off = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * chunk; off < bytes;
        off += (int64_t)gridDim.x * blockDim.x * chunk) {
@@ -1254,66 +1263,66 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
   const int64_t pbytes = h.panel_total * 8;
   if (L.l2_prefetch && pbytes <= kPrefetchMaxBytes) {
-    k_prefetch_l2<<<(unsigned)std::min<int64_t>(148, (pbytes / 32768 + 255) / 256 + 1), 256, 0, st>>>(F->panel.p,
-                                                                                                   pbytes);
+    RIGA_CUDA(launch(k_prefetch_l2, (unsigned)std::min<int64_t>(148, (pbytes / 32768 + 255) / 256 + 1), 256, 0, st, F->panel.p,
+                                                                                                   pbytes));
     count_launch();
   }
   if (L.nsub && gon) {
     const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_ftiles.p), 1, F->D.p,
                   F->cvec.p};
-    k_sub_fwd<<<(unsigned)L.nsub, kSolveThreads, 0, st>>>(S, T, Gs, sym->d_sub_fptr.p, L.sub_levels, b, F->xperm.p,
-                                                          F->upd.p);
+    RIGA_CUDA(launch(k_sub_fwd, (unsigned)L.nsub, kSolveThreads, 0, st, S, T, Gs, sym->d_sub_fptr.p, L.sub_levels, b, F->xperm.p,
+                                                          F->upd.p));
     count_launch();
   }
   for (int64_t l = 0; l < h.nlevels; ++l) {
     const int nc = (int)(L.chain_ptr[l + 1] - L.chain_ptr[l]);
     const int ni = (int)(L.ifwd_ptr[l + 1] - L.ifwd_ptr[l]);
     if (L.chain_inv && ni) {
-      k_inv_fwd<<<ni, 256, L.ifwd_smem[l], st>>>(S, T, reinterpret_cast<const int2*>(sym->d_ifwd.p) + L.ifwd_ptr[l],
+      RIGA_CUDA(launch(k_inv_fwd, ni, 256, L.ifwd_smem[l], st, S, T, reinterpret_cast<const int2*>(sym->d_ifwd.p) + L.ifwd_ptr[l],
                                                   sym->d_inv_off.p, F->linv.p, F->D.p, b, F->xperm.p, F->upd.p,
-                                                  F->cvec.p);
+                                                  F->cvec.p));
       count_launch();
     } else if (nc) {
-      k_chain_fwd<<<nc, kSolveThreads, L.chf_smem[l], st>>>(S, T, sym->d_chains.p + L.chain_ptr[l],
+      RIGA_CUDA(launch(k_chain_fwd, nc, kSolveThreads, L.chf_smem[l], st, S, T, sym->d_chains.p + L.chain_ptr[l],
                                                             (int)L.chf_smem[l], F->panel.p, b, F->xperm.p,
-                                                            F->upd.p);
+                                                            F->upd.p));
       count_launch();
     }
     const int nt = (int)(L.fwd_ptr[l + 1] - L.fwd_ptr[l]);
     if (nt) {
-      (gon ? (L.occ == 8 ? k_rest_fwd<true, 8> : L.occ == 6 ? k_rest_fwd<true, 6> : k_rest_fwd<true, 4>)
-           : k_rest_fwd<false>)<<<std::min(nt, L.rest_cap), kSolveThreads, L.fwd_smem[l], st>>>(S, T, tf + L.fwd_ptr[l], nt, sym->d_wholes.p,
-                                                           F->panel.p, b, F->xperm.p, F->upd.p, L.warp_stage, GDf);
+      RIGA_CUDA(launch((gon ? (L.occ == 8 ? k_rest_fwd<true, 8> : L.occ == 6 ? k_rest_fwd<true, 6> : k_rest_fwd<true, 4>)
+           : k_rest_fwd<false>), std::min(nt, L.rest_cap), kSolveThreads, L.fwd_smem[l], st, S, T, tf + L.fwd_ptr[l], nt, sym->d_wholes.p,
+                                                           F->panel.p, b, F->xperm.p, F->upd.p, L.warp_stage, GDf));
       count_launch();
     }
   }
   for (int64_t l = h.nlevels - 1; l >= 0; --l) {
     const int nt = (int)(L.bwd_ptr[l + 1] - L.bwd_ptr[l]);
     if (nt) {
-      (gon ? (L.occ == 8 ? k_rest_bwd<true, 8> : L.occ == 6 ? k_rest_bwd<true, 6> : k_rest_bwd<true, 4>)
-           : k_rest_bwd<false>)<<<std::min(nt, L.rest_cap), kSolveThreads, L.bwd_smem[l], st>>>(S, T, tb + L.bwd_ptr[l], nt, sym->d_wholes.p,
+      RIGA_CUDA(launch((gon ? (L.occ == 8 ? k_rest_bwd<true, 8> : L.occ == 6 ? k_rest_bwd<true, 6> : k_rest_bwd<true, 4>)
+           : k_rest_bwd<false>), std::min(nt, L.rest_cap), kSolveThreads, L.bwd_smem[l], st, S, T, tb + L.bwd_ptr[l], nt, sym->d_wholes.p,
                                                            F->panel.p, F->D.p, F->xperm.p, F->cvec.p, x, L.warp_stage,
-                                                           L.chain_inv, GDb);
+                                                           L.chain_inv, GDb));
       count_launch();
     }
     const int nc = (int)(L.chain_ptr[l + 1] - L.chain_ptr[l]);
     const int ni = (int)(L.ibwd_ptr[l + 1] - L.ibwd_ptr[l]);
     if (L.chain_inv && ni) {
-      k_inv_bwd<<<ni, 256, 0, st>>>(S, reinterpret_cast<const int2*>(sym->d_ibwd.p) + L.ibwd_ptr[l],
-                                     sym->d_inv_off.p, F->linv.p, F->cvec.p, F->xperm.p, x);
+      RIGA_CUDA(launch(k_inv_bwd, ni, 256, 0, st, S, reinterpret_cast<const int2*>(sym->d_ibwd.p) + L.ibwd_ptr[l],
+                                     sym->d_inv_off.p, F->linv.p, F->cvec.p, F->xperm.p, x));
       count_launch();
     } else if (nc) {
-      k_chain_bwd<<<nc, kSolveThreads, L.chb_smem[l], st>>>(S, sym->d_chains.p + L.chain_ptr[l],
+      RIGA_CUDA(launch(k_chain_bwd, nc, kSolveThreads, L.chb_smem[l], st, S, sym->d_chains.p + L.chain_ptr[l],
                                                             (int)L.chb_smem[l], F->panel.p, F->D.p,
-                                                            F->xperm.p, F->cvec.p, x);
+                                                            F->xperm.p, F->cvec.p, x));
       count_launch();
     }
   }
   if (L.nsub && gon) {
     const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_btiles.p), 1, F->D.p,
                   F->cvec.p};
-    k_sub_bwd<<<(unsigned)L.nsub, kSolveThreads, 0, st>>>(S, Gs, sym->d_sub_bptr.p, L.sub_levels, F->D.p,
-                                                          F->xperm.p, x);
+    RIGA_CUDA(launch(k_sub_bwd, (unsigned)L.nsub, kSolveThreads, 0, st, S, Gs, sym->d_sub_bptr.p, L.sub_levels, F->D.p,
+                                                          F->xperm.p, x));
     count_launch();
   }
   RIGA_CUDA(cudaGetLastError());

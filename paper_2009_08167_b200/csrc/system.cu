@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t n, const int64_t* __restri
                                               const double* __restrict__ B, double sigma,
                                               const double* __restrict__ x,
                                               double* __restrict__ y) {
+  pdl_start();
   int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LANES;
   int sub = threadIdx.x % LANES;
   if (row >= n) return;
@@ -184,6 +185,7 @@ int system_spmv(riga_system* sys, cudaStream_t s, int which, double sigma, const
 __global__ void k_kron_axis(int64_t n, int64_t nax, int64_t stride, const int64_t* __restrict__ rp,
                             const int32_t* __restrict__ ci, const double* __restrict__ m,
                             const double* __restrict__ in, double* __restrict__ out) {
+  pdl_start();
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int64_t i = (r / stride) % nax;
@@ -202,7 +204,7 @@ int kron_mass_apply(riga_system* sys, cudaStream_t s, const double* x, double* y
   for (int t = 0; t < d; ++t) {
     double* out = t == d - 1 ? y : (t % 2 == 0 ? t1 : t2);
     const KronAxis& a = sys->kax[t];
-    k_kron_axis<<<g, 256, 0, s>>>(n, a.n, stride, a.rp.p, a.ci.p, a.m.p, in, out);
+    RIGA_CUDA(launch(k_kron_axis, g, 256, 0, s, n, a.n, stride, a.rp.p, a.ci.p, a.m.p, in, out));
     count_launch();
     in = out;
     stride *= a.n;
