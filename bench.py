@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sample-q", type=int, default=8, help="eigenpairs per slice in the CPU sample")
+    ap.add_argument("--ldlt-config", default="cfg5", help="config of the LDL^T TFLOP/s line ('' to skip)")
     return ap.parse_args()
 
 
@@ -220,6 +221,64 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "NVML (in-process)"}
 
 
+def dcgs_bytes(R, n):
+    """Algorithmic bytes of the step's Gram-Schmidt (delayed CGS2, SURVEY 8d's
+    2 passes x 2 x R x N x 8 reorganised): one dots sweep reads R rows of
+    MV / LM and the two vectors, one update sweep reads R rows of V / L and
+    the two vectors and writes the two results."""
+    return 2.0 * R * n * 8.0 + 6.0 * n * 8.0
+
+
+def ncu_traffic(kernel, d):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture (profiles/ncu_traffic.json), scaled
+    to this launch's algorithmic bytes (the capture may use another R)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        rec = json.load(open(p))[kernel]
+        return rec["dram_bytes"] * d["bytes_per_launch"] / rec["algorithmic_bytes"]
+    except Exception:
+        return None
+
+
+def ldlt_rate(P, D, cfgname, flush, reps=3):
+    """LDL^T FP64 rate on the largest single-GPU config (the one whose fronts
+    exercise the DMMA frontal updates): median device time of `reps`
+    factorizations at its first interior uniform shift, L2 flushed before
+    each; work = the reference's sum colcount^2 (sparsela.py:258)."""
+    import numpy as np
+    import torch
+    from paper_2009_08167_b200.configs import CONFIGS
+    from paper_2009_08167_b200.sparsela import Symbolic, numeric_factor
+
+    cc = CONFIGS[cfgname]
+    t0 = time.perf_counter()
+    s = P.build_system(cc.d, cc.ne, cc.p, cc.level)
+    lam_e, _ = P.choose_lambda_e(s, cc.n0)
+    sh = P.uniform_shifts(lam_e, cc.slices)
+    sym = Symbolic.on_device(s.device, P.separator_ordering(s))
+    t_setup = time.perf_counter() - t0
+    ms = []
+    for _ in range(reps + 1):
+        flush.zero_()
+        torch.cuda.synchronize()
+        f = numeric_factor(sym, float(sh[1]))
+        ms.append(f.device_ms)
+        flops = f.factor_flops
+        del f
+    fm = float(np.median(ms[1:]))
+    tf = flops / (fm / 1e3) / 1e12
+    out = {"config": cfgname, "N": s.dof_count, "ms": fm, "flops_per_launch": flops, "achieved": tf,
+           "unit": "TFLOP/s", "peak": MEASURED_FP64_TFLOPS, "frac": tf / MEASURED_FP64_TFLOPS,
+           "peak_source": "tools/fp64_peak.cu DMMA loop on this pool's B200",
+           "how": f"median of {reps} factorizations (after one warm-up), CUDA events on the factor stream, "
+                  "L2 flushed before each; flops = reference sum colcount^2",
+           "setup_s": t_setup}
+    del sym, s
+    torch.cuda.synchronize()
+    return out
+
+
 def kernel_roofline(P, D, L, system, shifts, sym, perm, c, flush, reps=10):
     """Time the hot kernels of one Lanczos step on the benchmark's own data
     (the middle slice: its factor, its m-vector basis), each bracketed by
@@ -279,7 +338,8 @@ def kernel_roofline(P, D, L, system, shifts, sym, perm, c, flush, reps=10):
             return float(np.median(ts))
 
         rows = ctypes.c_int64(0)
-        t_cgs = timed(lambda: _lib.check(L.riga_lanczos_cgs_probe(st.handle, _lib.ptr(x), 2, ctypes.byref(rows))))
+        st.k = st.k  # basis full (k = m): the probe uses rows [0, k] + locked
+        t_cgs = timed(lambda: _lib.check(L.riga_lanczos_dcgs_probe(st.handle, _lib.ptr(x), ctypes.byref(rows))))
         t_sol = timed(lambda: f.solve_device(b, y))
         # the system's SpMV runs on the system's context stream
         sstream = system.device.ctx.stream
@@ -287,15 +347,15 @@ def kernel_roofline(P, D, L, system, shifts, sym, perm, c, flush, reps=10):
                      sstream)
         ctx.synchronize()
     nnz = system.K.nnz
-    work = {"cgs2_pass": 2 * 2 * rows.value * n * 8.0, "supernodal_solve": 16.0 * f.fill_nnz + 32.0 * n,
+    work = {"dcgs_sweeps": dcgs_bytes(rows.value, n), "supernodal_solve": 16.0 * f.fill_nnz + 32.0 * n,
             "csr_spmv": 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n}
-    times = {"cgs2_pass": t_cgs, "supernodal_solve": t_sol, "csr_spmv": t_mv}
+    times = {"dcgs_sweeps": t_cgs, "supernodal_solve": t_sol, "csr_spmv": t_mv}
     cats = {}
     for name in work:
         ach = work[name] / (times[name] / 1e3) / 1e9
         cats[name] = {"ms": times[name], "bytes_per_launch": work[name], "achieved": ach, "unit": "GB/s",
                       "peak": hbm, "frac": ach / hbm}
-    cats["cgs2_pass"]["rows"] = int(rows.value)
+    cats["dcgs_sweeps"]["rows"] = int(rows.value)
     fm = float(np.median(fms))
     tf = f.factor_flops / (fm / 1e3) / 1e12
     cats["ldlt_factor"] = {"ms": fm, "flops_per_launch": f.factor_flops, "achieved": tf, "unit": "TFLOP/s",
@@ -347,7 +407,7 @@ def concurrent_rates(P, D, L, system, shifts, sym, streams, m, reps=6):
 
     run_all(ext)
     rows = ctypes.c_int64(0)
-    _lib.check(L.riga_lanczos_cgs_probe(states[0].handle, _lib.ptr(vecs[0][0]), 2, ctypes.byref(rows)))
+    _lib.check(L.riga_lanczos_dcgs_probe(states[0].handle, _lib.ptr(vecs[0][0]), ctypes.byref(rows)))
     graphs = []
     for i, ctx in enumerate(ctxs):
         with ctx:
@@ -380,7 +440,7 @@ def concurrent_rates(P, D, L, system, shifts, sym, streams, m, reps=6):
 
     def cgs(i):
         for _ in range(reps):
-            _lib.check(L.riga_lanczos_cgs_probe(states[i].handle, _lib.ptr(vecs[i][0]), 2, ctypes.byref(ctypes.c_int64())))
+            _lib.check(L.riga_lanczos_dcgs_probe(states[i].handle, _lib.ptr(vecs[i][0]), ctypes.byref(ctypes.c_int64())))
 
     def sol(i):
         for _ in range(reps):
@@ -391,11 +451,11 @@ def concurrent_rates(P, D, L, system, shifts, sym, streams, m, reps=6):
     span(sol)
     t_sol = span(sol)
     out = {"streams": streams,
-           "cgs2_pass": {"ms_span": t_cgs, "launches": streams * reps, "rows": int(rows.value),
-                         "bytes": streams * reps * 2 * 2 * rows.value * n * 8.0},
+           "dcgs_sweeps": {"ms_span": t_cgs, "launches": streams * reps, "rows": int(rows.value),
+                           "bytes": streams * reps * dcgs_bytes(rows.value, n)},
            "supernodal_solve": {"ms_span": t_sol, "launches": streams * reps * 10,
                                 "bytes": streams * reps * 10 * (16.0 * facts[0].fill_nnz + 32.0 * n)}}
-    for k in ("cgs2_pass", "supernodal_solve"):
+    for k in ("dcgs_sweeps", "supernodal_solve"):
         out[k]["achieved"] = out[k]["bytes"] / (out[k]["ms_span"] / 1e3) / 1e9
         out[k]["per_launch_ms"] = out[k]["ms_span"] / out[k]["launches"]
     del graphs, states, facts, ctxs
@@ -522,14 +582,17 @@ def ours(args):
 
     # ---- roofline: the step's kernels timed with CUDA events on their stream ---
     cats, hbm, src, reps = kernel_roofline(P, D, L, system, shifts, sym, perm, c, flush)
+    ldlt_large = None
+    if rank == 0 and args.ldlt_config and args.ldlt_config != c.name:
+        ldlt_large = ldlt_rate(P, D, args.ldlt_config, flush)
     rows_avg = float(r.counters.phase_s.get("cgs_rows", 0.0)) / max(r.counters.nfb, 1)
     m_mid = int(2 * np.median(r.expected))
     conc = concurrent_rates(P, D, L, system, shifts, sym, args.streams, m_mid)
     # per Lanczos step, in the concurrent regime: one solve, two Gram-Schmidt
     # passes over rows_avg rows (scaled from the probe's R), one SpMV
     share = {"supernodal_solve": conc["supernodal_solve"]["per_launch_ms"],
-             "cgs2_pass": conc["cgs2_pass"]["per_launch_ms"] * rows_avg / max(conc["cgs2_pass"]["rows"], 1)}
-    for k_ in ("cgs2_pass", "supernodal_solve"):
+             "dcgs_sweeps": conc["dcgs_sweeps"]["per_launch_ms"] * rows_avg / max(conc["dcgs_sweeps"]["rows"], 1)}
+    for k_ in ("dcgs_sweeps", "supernodal_solve"):
         cats[k_]["concurrent"] = {"achieved": conc[k_]["achieved"], "frac": conc[k_]["achieved"] / hbm,
                                   "unit": "GB/s", "streams": args.streams,
                                   "per_launch_ms_aggregate": conc[k_]["per_launch_ms"]}
@@ -539,7 +602,8 @@ def ours(args):
     dom = max(share, key=lambda k_: share[k_])
     d = cats[dom]
     roofline = {"bound": "hbm", "achieved": d["achieved"], "peak": hbm, "unit": "GB/s", "frac": d["frac"],
-                "traffic": None, "kernel": dom, "peak_source": src, "per_launch_bytes": d["bytes_per_launch"],
+                "traffic": ncu_traffic(dom, d), "kernel": dom, "peak_source": src,
+                "per_launch_bytes": d["bytes_per_launch"],
                 "how": "isolated launch: CUDA events on the engine stream, L2 flushed before each launch, "
                        "median of %d" % reps,
                 "concurrent": d["concurrent"],
@@ -556,7 +620,8 @@ def ours(args):
                        "parallelism": f"slices partitioned over {world} GPU(s) (LPT on inertia counts)",
                        "l2": "working set > L2 (V+MV 2x251xNx8 B = 369 MB per slice); 256 MB flush between steps"},
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "roofline_by_kernel": cats,
-            "ldlt": cats.get("ldlt_factor"), "clocks": clk,
+            "ldlt": ldlt_large if ldlt_large else cats.get("ldlt_factor"),
+            "ldlt_workload": cats.get("ldlt_factor"), "clocks": clk,
             "timing": {"per_step_s": times, "boundary_s": r.timings["boundary_s"],
                        "slices_s": r.timings["slices_s"], "streams_used": r.timings.get("streams_used")}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

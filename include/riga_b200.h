@@ -227,6 +227,10 @@ int riga_lanczos_append_rows(riga_lanczos* lz, double* X_dev, double* MX_dev, in
  * locked set (the step's CGS kernels, launched directly on the context
  * stream so CUDA events can bracket them); *rows = k + locked.            */
 int riga_lanczos_cgs_probe(riga_lanczos* lz, double* x_dev, int passes, int64_t* rows);
+/* Measurement hook: the step's delayed-CGS2 sweeps (one dots sweep of the
+ * pending row and w over V[:k+1] + locked, one update sweep) with w = w_dev;
+ * writes only scratch.  *rows = k + 1 + locked.                           */
+int riga_lanczos_dcgs_probe(riga_lanczos* lz, const double* w_dev, int64_t* rows);
 /* Gram matrix G = V[:k] MV[:k]^T to host (k x k row-major) for the
  * DEBUG_INVARIANTS checks (ref check_invariants :276-282).                 */
 int riga_lanczos_gram(riga_lanczos* lz, double* G_host);

@@ -73,6 +73,7 @@ SIGNATURES = {
     "riga_lanczos_project_locked": [_p, _p, _p, _i32],
     "riga_lanczos_lock_batch": [_p, _p, _p, _i64, _i64, _p],
     "riga_lanczos_cgs_probe": [_p, _p, _i32, _p],
+    "riga_lanczos_dcgs_probe": [_p, _p, _p],
     "riga_lanczos_lock_block": [_p, _p, _p, _i64, _i64, _p],
     "riga_lanczos_append_rows": [_p, _p, _p, _i64, _i64, _p, _p],
     "riga_lanczos_gram": [_p, _p],

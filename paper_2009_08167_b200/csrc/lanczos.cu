@@ -1465,6 +1465,24 @@ int riga_lanczos_cgs_probe(riga_lanczos* lz, double* x, int passes, int64_t* row
                     lz->k + lz->nlocked);
 }
 
+int riga_lanczos_dcgs_probe(riga_lanczos* lz, const double* w, int64_t* rows) {
+  RIGA_CHECK_ARG(lz && w && lz->k < lz->max_dim, "bad arg");
+  DeviceGuard g(lz->ctx->device);
+  cudaStream_t s = lz->ctx->stream;
+  RIGA_TRY(push_state(lz, lz->k, lz->k, 0.0));  // steps = 0: no beta correction
+  const int64_t Rmax = lz->max_dim + 1 + lz->cap;
+  if (rows) *rows = lz->k + 1 + lz->nlocked;
+  RIGA_CUDA(launch(k_dcgs_dots, kDotGrid, 256, 0, s, sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, w,
+                   lz->partial.p, lz->coef.p, lz->tk_dots.p));
+  RIGA_CUDA(launch(k_dcgs_scalars, 1, 256, 0, s, lz->st.p, Rmax, lz->coef.p, lz->cpl.p,
+                   lz->outs.p + (lz->max_dim + 1)));
+  const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
+  RIGA_CUDA(launch(k_dcgs_upd, gu, 256, 0, s, sel_basis(lz, false, 1), lz->st.p, lz->n, lz->ld, Rmax, lz->coef.p,
+                   lz->upart.p, w, lz->vt.p, lz->r.p, lz->tk_upd.p));
+  count_launch(3);
+  return RIGA_OK;
+}
+
 int riga_lanczos_project_locked(riga_lanczos* lz, double* x, double* mx, int passes) {
   RIGA_CHECK_ARG(lz && x && mx, "null arg");
   if (!lz->nlocked) return RIGA_OK;

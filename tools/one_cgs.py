@@ -20,6 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg3")
 ap.add_argument("--m", type=int, default=250)
 ap.add_argument("--probes", type=int, default=3)
+ap.add_argument("--dcgs", action="store_true", help="the step's delayed-CGS2 sweeps instead of classic passes")
 a = ap.parse_args()
 c = CONFIGS[a.config]
 s = P.build_system(c.d, c.ne, c.p, c.level)
@@ -33,7 +34,13 @@ P.lanczos_extend(st, a.m)
 x = torch.randn(s.dof_count, dtype=torch.float64, device="cuda")
 rows = ctypes.c_int64(0)
 torch.cuda.synchronize()
+torch.cuda.profiler.start()
 for _ in range(a.probes):
-    _lib.check(_lib.lib().riga_lanczos_cgs_probe(st.handle, _lib.ptr(x), 2, ctypes.byref(rows)))
+    if a.dcgs:
+        _lib.check(_lib.lib().riga_lanczos_dcgs_probe(st.handle, _lib.ptr(x), ctypes.byref(rows)))
+    else:
+        _lib.check(_lib.lib().riga_lanczos_cgs_probe(st.handle, _lib.ptr(x), 2, ctypes.byref(rows)))
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 torch.cuda.synchronize()
 print("rows", rows.value)
