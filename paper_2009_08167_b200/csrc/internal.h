@@ -72,6 +72,10 @@ struct SolvePlanHost {
   std::vector<int64_t> fwd_smem, bwd_smem, chf_smem, chb_smem;  // bytes per level launch
   std::vector<int32_t> gsrc;
   std::vector<int64_t> gptr;
+  // persistent phase-ordered solve (solve.cu k_solve_pers): tasks (type, a, b, phase)
+  int pers = 0, pers_ctas = 296;
+  std::vector<int> ptf, ptb;            // flattened int4 tasks
+  std::vector<int> pcf, pcb;            // tasks per phase
 };
 
 struct riga_symbolic {
@@ -95,6 +99,7 @@ struct riga_symbolic {
   riga::DevBuf<int64_t> d_gptr, d_inv_off, d_g_off;
   riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_dbl_tasks, d_gfwd, d_gbwd, d_sub_ftiles, d_sub_btiles;
   riga::DevBuf<int64_t> d_dbl_toff;
+  riga::DevBuf<int> d_ptf, d_ptb, d_pcf, d_pcb;
   SymDev dev() const {
     return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,
                   d_cb_off.p,   d_upd_off.p,   d_child_ptr.p,  d_asm_ptr.p,    d_sparent.p,
@@ -117,6 +122,7 @@ struct riga_factor {
   riga::DevBuf<double> tol;    // [0] max|A|, [1] zero_tol
   riga::DevBuf<double> linv;   // inv(L11) of the chain supernodes (solve.cu)
   riga::DevBuf<double> gsmall; // G of the small supernodes (solve.cu)
+  riga::DevBuf<unsigned> pctr; // persistent-solve task / phase counters (reset per solve)
   float factor_ms = 0.f;
 };
 

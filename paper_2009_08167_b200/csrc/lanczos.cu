@@ -1101,6 +1101,11 @@ int riga_lanczos_reset(riga_lanczos* lz) {
   lz->k = 0;
   lz->nlocked = 0;
   lz->ev_valid = false;
+  // the captured step graph holds the previous operator's device pointers;
+  // a new factor may reuse the old one's host address (riga_factor*), so the
+  // pointer comparison in ensure_graph cannot be trusted across states
+  drop_graph(lz);
+  lz->op = nullptr;
   return push_state(lz, 0, 0, 0.0);
 }
 

@@ -246,6 +246,57 @@ struct GDev {
                           // another group of it is writing
 };
 
+// ---- static-operand prefetch (before the PDL wait) -------------------------
+// Everything a level task reads that the previous kernels of the solve do
+// not write -- task lists, front metadata, the pull map, G / inv(L11) /
+// panel blocks -- is touched into L2 before griddepcontrol.wait, while the
+// predecessor level drains; after the wait only the dynamic vectors (update
+// vectors, z, x) are first touches, so a level's dependent-load chain runs
+// at L2 latency.  Without a PDL launch the wait is a no-op and the prefetch
+// simply runs first.
+__device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+__device__ __forceinline__ void pf_gather(const SymDev& S, const SolveDev& T, int s, int64_t r) {
+  const int64_t g = S.rows_off[s] + r;
+  const int64_t q0 = T.gptr[g], q1 = T.gptr[g + 1];
+  if (q1 > q0) pf_l2(T.gsrc + q0);
+}
+
+// forward G tile (s, t): the G rows of the tile and the gather metadata
+__device__ __forceinline__ void pf_gtile_fwd(const SymDev& S, const SolveDev& T, const GDev& GD, int2 task,
+                                             int lane) {
+  const int s = task.x;
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const double* G = GD.g + GD.g_off[s] + 32 * task.y;
+  for (int k = lane; k < np; k += 32) pf_l2(G + (int64_t)k * f);
+  for (int r = lane; r < np; r += 32) pf_gather(S, T, s, r);
+  const int i = 32 * task.y + lane;
+  if (i >= np && i < f) pf_gather(S, T, s, i);
+}
+
+// backward G column group (s, g): its 8 G columns and the front rows
+__device__ __forceinline__ void pf_gtile_bwd(const SymDev& S, const GDev& GD, int2 task, int lane) {
+  const int s = task.x;
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int c0 = 8 * task.y;
+  const double* G = GD.g + GD.g_off[s];
+  const int nc = min(8, np - c0);
+  for (int r = (c0 & ~31) + 32 * (lane >> 3); r < f; r += 128)
+    if ((lane & 7) < nc) pf_l2(G + (int64_t)(c0 + (lane & 7)) * f + r);
+  const int32_t* rows = S.rows + S.rows_off[s];
+  for (int r = np + 32 * lane; r < f; r += 32 * 32) pf_l2(rows + r);
+}
+
+// panel block [c0, c0 + nc) x rows [r0, r1) of a chain supernode (kUpd / kColdot)
+__device__ __forceinline__ void pf_panel(const double* P, int64_t f, int64_t c0, int nc, int64_t r0, int64_t r1,
+                                         int tid, int nthreads) {
+  const int64_t lines = (r1 - r0 + 31) / 32;
+  for (int64_t q = tid; q < nc * lines; q += nthreads) {
+    const int64_t c = c0 + q / lines, r = r0 + 32 * (q % lines);
+    pf_l2(P + c * f + r);
+  }
+}
+
 // one CTA per G-mode supernode (np <= 128).  inv(L11) by column-oriented
 // substitution: warp w owns columns w + 8 j (8 per round), lanes own rows
 // lane + 32 ri; x_k is final at step k and broadcast by shuffle.  Then
@@ -455,11 +506,23 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDe
                                                             const double* __restrict__ b,
                                                             double* __restrict__ xp,
                                                             double* __restrict__ upd, int stage, GDev GD) {
-  pdl_start();
   extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (blockIdx.x < ntask) {  // static operands of this CTA's first task -> L2
+    const int2 t0 = tasks[blockIdx.x];
+    const int ty = t0.y >> 24, jj = t0.y & 0x00ffffff;
+    if (GT && ty == kGTiles) {
+      if (w < jj) pf_gtile_fwd(S, T, GD, GD.tiles[t0.x + w], lane);
+    } else if (ty == kUpd) {
+      const int64_t f = S.front[t0.x], np = S.ncol[t0.x];
+      const int64_t r0 = np + 32 * (int64_t)jj;
+      pf_panel(panel + S.panel_off[t0.x], f, 0, (int)np, r0, imin(r0 + 32, f), tid, blockDim.x);
+      if (tid < 32 && r0 + tid < f) pf_gather(S, T, t0.x, r0 + tid);
+    }
+  }
+  pdl_start();
   // grid-stride over the level's tasks (the grid may be capped below ntask)
   for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
   const int2 task = tasks[ti];
@@ -521,11 +584,24 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDe
                                                             double* __restrict__ xp,
                                                             double* __restrict__ cvec,
                                                             double* __restrict__ x, int stage, int inv, GDev GD) {
-  pdl_start();
   extern __shared__ __align__(16) double y[];
   __shared__ double part[kSolveWarps][32];
   __shared__ uint64_t wbar[kSolveWarps];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (blockIdx.x < ntask) {  // static operands of this CTA's first task -> L2
+    const int2 t0 = tasks[blockIdx.x];
+    const int ty = t0.y >> 24, jj = t0.y & 0x00ffffff;
+    if (GT && ty == kGTiles) {
+      if (w < jj) pf_gtile_bwd(S, GD, GD.tiles[t0.x + w], lane);
+    } else if (ty == kColdot) {
+      const int64_t f = S.front[t0.x], np = S.ncol[t0.x];
+      const int64_t c0 = 32 * (int64_t)jj;
+      pf_panel(panel + S.panel_off[t0.x], f, c0, (int)imin(32, np - c0), np, f, tid, blockDim.x);
+      const int32_t* rows = S.rows + S.rows_off[t0.x];
+      for (int64_t r = np + 32 * tid; r < f; r += 32 * (int64_t)blockDim.x) pf_l2(rows + r);
+    }
+  }
+  pdl_start();
   for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
   const int2 task = tasks[ti];
   const int type = task.y >> 24, bj = task.y & 0x00ffffff;
@@ -860,13 +936,21 @@ __global__ void __launch_bounds__(256) k_inv_fwd(SymDev S, SolveDev T, const int
                                                  const double* __restrict__ D, const double* __restrict__ b,
                                                  double* __restrict__ xp, const double* __restrict__ upd,
                                                  double* __restrict__ cvec) {
-  pdl_start();
   extern __shared__ double y[];
   __shared__ double part[8][32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = tasks[blockIdx.x].x;
   const int np = (int)S.ncol[s];
   const int64_t col0 = S.col0[s];
+  {  // static operands -> L2: the 32-row strip of inv(L11), the gather metadata
+    const int rr0 = 32 * tasks[blockIdx.x].y, rr1 = min(np, rr0 + 32);
+    const double* A = linv + inv_off[s] + rr0;
+    for (int k = tid; k < rr1; k += 256) {
+      pf_l2(A + (int64_t)k * np);
+      pf_gather(S, T, s, k);
+    }
+  }
+  pdl_start();
   const int r0 = 32 * tasks[blockIdx.x].y, r1 = min(np, r0 + 32);
   for (int k = tid; k < r1; k += 256) y[k] = gather_row(S, T, s, k, np, col0, b, upd);
   __syncthreads();
@@ -896,11 +980,15 @@ __global__ void __launch_bounds__(256) k_inv_bwd(SymDev S, const int2* __restric
                                                  const double* __restrict__ linv,
                                                  const double* __restrict__ cvec, double* __restrict__ xp,
                                                  double* __restrict__ x) {
-  pdl_start();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int s = tasks[blockIdx.x].x;
   const int np = (int)S.ncol[s];
   const int r = 8 * tasks[blockIdx.x].y + w;
+  if (r < np) {  // static: this row of inv(L11) -> L2
+    const double* A = linv + inv_off[s] + (int64_t)r * np;
+    for (int k = (r & ~31) + 32 * lane; k < np; k += 32 * 32) pf_l2(A + k);
+  }
+  pdl_start();
   if (r >= np) return;
   const int64_t col0 = S.col0[s];
   const double* A = linv + inv_off[s] + (int64_t)r * np;
@@ -912,6 +1000,269 @@ __global__ void __launch_bounds__(256) k_inv_bwd(SymDev S, const int2* __restric
   if (lane == 0) {
     xp[col0 + r] = acc;
     x[S.order[col0 + r]] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent phase-ordered solve (one kernel per sweep).
+//
+// The level-by-level launches above cost one kernel per level and sweep
+// (~40 per cfg3 solve); with 16 slice streams the device's grid-launch rate,
+// not HBM, caps the aggregate solve rate (measured: 16 k solves/s from 16 to
+// 32 streams at 30 % warp occupancy).  Here a sweep is ONE kernel: the same
+// tasks, in the same phase order (forward per level: inv(L11) rows of the
+// chain supernodes, then G tiles + UPD rows; backward per level: G column
+// groups + COLDOT, then inv(L11)^T rows), are handed out by an atomic
+// counter in order; a CTA that takes a task of phase p waits (acquire spin)
+// until every task of phase p - 1 has completed (release counter), which by
+// induction covers all earlier phases.  Tasks are taken in order, so a
+// waiting CTA only waits on tasks already held by running CTAs: no deadlock
+// for any grid size.  Dynamic vectors are read through L2 (ld.global.cg):
+// another SM wrote them inside this kernel.
+// ---------------------------------------------------------------------------
+enum { kPInvF = 1, kPGtF = 2, kPUpd = 3, kPGtB = 4, kPCol = 5, kPInvB = 6 };
+
+struct PDev {
+  const int4* tasks;   // (type, a, b, phase), phase order
+  int ntask;
+  const int* phase_cnt;
+  unsigned* ctr;       // [0] next task, [1 + p] completed tasks of phase p
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ double p_gather(const SymDev& S, const SolveDev& T, int s, int64_t r, int64_t np,
+                                           int64_t col0, const double* b, const double* upd) {
+  double v = r < np ? __ldcg(b + (T.permuted ? col0 + r : S.order[col0 + r])) : 0.0;
+  const int64_t g = S.rows_off[s] + r;
+  for (int64_t q = T.gptr[g]; q < T.gptr[g + 1]; ++q) v += __ldcg(upd + T.gsrc[q]);
+  return v;
+}
+
+// forward G tile (s, t), one warp (as warp_gtile_fwd)
+__device__ __forceinline__ void p_gtile_fwd(const SymDev& S, const SolveDev& T, const GDev& GD, int2 task,
+                                            const double* b, double* xp, double* upd, double* yw, int lane) {
+  const int s = task.x;
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const double* G = GD.g + GD.g_off[s];
+  for (int r = lane; r < np; r += 32) yw[r] = p_gather(S, T, s, r, np, col0, b, upd);
+  const int i = 32 * task.y + lane;
+  const double yi = (i >= np && i < f) ? p_gather(S, T, s, i, np, col0, b, upd) : 0.0;
+  __syncwarp();
+  if (i < f) {
+    double a4[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* Gi = G + i;
+    int k = 0;
+    for (; k + 16 <= np; k += 16) {
+      double g[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) g[u] = Gi[(k + u) * f];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) a4[u & 3] = fma(g[u], yw[k + u], a4[u & 3]);
+    }
+    for (; k < np; ++k) a4[0] = fma(Gi[k * f], yw[k], a4[0]);
+    const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+    if (i < np) {
+      xp[col0 + i] = acc;
+      GD.wz[col0 + i] = acc / GD.D[col0 + i];
+    } else {
+      upd[S.upd_off[s] + i - np] = yi - acc;
+    }
+  }
+  __syncwarp();
+}
+
+// backward G column group (s, g), one warp (as warp_gtile_bwd)
+__device__ __forceinline__ void p_gtile_bwd(const SymDev& S, const GDev& GD, int2 task, double* xp, double* x,
+                                            int lane) {
+  const int s = task.x;
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const int c0 = 8 * task.y;
+  const double* G = GD.g + GD.g_off[s];
+  const int32_t* rows = S.rows + S.rows_off[s];
+  const int nc = min(8, np - c0);
+  double acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+  for (int r = (c0 & ~31) + lane; r < f; r += 32) {
+    const double v = r < np ? __ldcg(GD.wz + col0 + r) : -__ldcg(xp + rows[r]);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = fma(c < nc ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
+  }
+#pragma unroll
+  for (int o = 4; o >= 1; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const bool hi = (lane & o) != 0;
+      const double send = hi ? acc[k] : acc[k + o];
+      const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+      acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
+    }
+  }
+  double v = acc[0];
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 16);
+  const int c = c0 + lane;
+  if (lane < 8 && c < np) {
+    xp[col0 + c] = v;
+    x[S.order[col0 + c]] = v;
+  }
+}
+
+template <bool FWD>
+__global__ void __launch_bounds__(kSolveThreads, 2) k_solve_pers(SymDev S, SolveDev T, GDev GD, PDev PD,
+                                                                 const double* __restrict__ panel,
+                                                                 const int64_t* __restrict__ inv_off,
+                                                                 const double* __restrict__ linv,
+                                                                 const double* __restrict__ D,
+                                                                 const double* b, double* xp, double* upd,
+                                                                 double* cvec, double* x) {
+  pdl_start();
+  extern __shared__ __align__(16) double y[];
+  __shared__ double part[kSolveWarps][32];
+  __shared__ int s_task;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (;;) {
+    if (tid == 0) s_task = (int)atomicAdd(&PD.ctr[0], 1u);
+    __syncthreads();
+    const int t = s_task;
+    __syncthreads();
+    if (t >= PD.ntask) break;
+    const int4 tk = PD.tasks[t];
+    const int ph = tk.w;
+    if (tid == 0 && ph > 0) {
+      const unsigned need = (unsigned)PD.phase_cnt[ph - 1];
+      while (ld_acquire_u32(&PD.ctr[ph]) < need) __nanosleep(32);
+    }
+    __syncthreads();
+    if (FWD) {
+      if (tk.x == kPGtF) {
+        if (w < tk.z) p_gtile_fwd(S, T, GD, GD.tiles[tk.y + w], b, xp, upd, y + w * kGMaxNp, lane);
+      } else if (tk.x == kPInvF) {
+        // z rows [32 t, 32 t + 32) of chain supernode s = inv(L11) y1 (as k_inv_fwd)
+        const int s = tk.y;
+        const int np = (int)S.ncol[s];
+        const int64_t col0 = S.col0[s];
+        const int r0 = 32 * tk.z, r1 = min(np, r0 + 32);
+        for (int k = tid; k < r1; k += kSolveThreads) y[k] = p_gather(S, T, s, k, np, col0, b, upd);
+        __syncthreads();
+        const int chunk = (r1 + 7) / 8;
+        const int k0 = w * chunk, k1 = min(r1, k0 + chunk);
+        const double* A = linv + inv_off[s] + r0 + lane;
+        double acc = 0.0;
+        if (r0 + lane < r1) {
+#pragma unroll 4
+          for (int k = k0; k < k1; ++k) acc = fma(A[(int64_t)k * np], y[k], acc);
+        }
+        part[w][lane] = acc;
+        __syncthreads();
+        if (w == 0 && r0 + lane < r1) {
+          double z = 0.0;
+#pragma unroll
+          for (int q = 0; q < kSolveWarps; ++q) z += part[q][lane];
+          const int64_t g = col0 + r0 + lane;
+          xp[g] = z;
+          cvec[g] = z / D[g];
+        }
+      } else {  // kPUpd: update rows [np + 32 j, ...) of chain supernode s minus L21 z
+        const int s = tk.y, j = tk.z;
+        const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
+        const double* P = panel + S.panel_off[s];
+        const int nbp = (int)((np + 31) / 32);
+        const int64_t r0 = np + 32 * (int64_t)j, r1 = imin(r0 + 32, f), r = r0 + lane;
+        const bool in = r < r1;
+        double acc = 0.0;
+        for (int cb = w; cb < nbp; cb += kSolveWarps) {
+          const int64_t c0 = 32 * (int64_t)cb;
+          const int nc = (int)imin(32, np - c0);
+          const double zl = lane < nc ? __ldcg(xp + col0 + c0 + lane) : 0.0;
+#pragma unroll 8
+          for (int k = 0; k < 32; ++k) {
+            const double l = (in && k < nc) ? P[(c0 + k) * f + r] : 0.0;
+            acc = fma(l, __shfl_sync(0xffffffffu, zl, k), acc);
+          }
+        }
+        part[w][lane] = acc;
+        __syncthreads();
+        if (w == 0 && in) {
+          double v = p_gather(S, T, s, r, np, col0, b, upd);
+#pragma unroll
+          for (int q = 0; q < kSolveWarps; ++q) v -= part[q][lane];
+          upd[S.upd_off[s] + r - np] = v;
+        }
+      }
+    } else {
+      if (tk.x == kPGtB) {
+        if (w < tk.z) p_gtile_bwd(S, GD, GD.tiles[tk.y + w], xp, x, lane);
+      } else if (tk.x == kPCol) {
+        // cvec[col] -= sum_{update rows r} L[r][col] x[rows[r]], col in block bj (as kColdot)
+        const int s = tk.y, bj = tk.z;
+        const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
+        const double* P = panel + S.panel_off[s];
+        const int32_t* rows = S.rows + S.rows_off[s];
+        const int64_t c0 = 32 * (int64_t)bj + 8 * (w & 3);
+        double acc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+        for (int64_t r = np + 32 * (w >> 2) + lane; r < f; r += 64) {
+          const double xv = __ldcg(xp + rows[r]);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[c] = fma(c0 + c < np ? P[(c0 + c) * f + r] : 0.0, xv, acc[c]);
+        }
+#pragma unroll
+        for (int o = 4; o >= 1; o >>= 1) {
+#pragma unroll
+          for (int k = 0; k < o; ++k) {
+            const bool hi = (lane & o) != 0;
+            const double send = hi ? acc[k] : acc[k + o];
+            const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+            acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
+          }
+        }
+        double v = acc[0];
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        if (lane < 8) part[w][lane] = v;
+        __syncthreads();
+        if (w == 0) {
+          const int g = lane >> 3, e = lane & 7;
+          const int64_t col = 32 * (int64_t)bj + lane;
+          if (col < np) {
+            const double tt = part[g][e] + part[g + 4][e];
+            double* c = cvec + col0 + col;
+            *c = __ldcg(c) - tt;
+          }
+        }
+      } else {  // kPInvB: x1[r] = sum_{k >= r} inv(L11)(k, r) w[k], warp per row
+        const int s = tk.y;
+        const int np = (int)S.ncol[s];
+        const int r = 8 * tk.z + w;
+        if (r < np) {
+          const int64_t col0 = S.col0[s];
+          const double* A = linv + inv_off[s] + (int64_t)r * np;
+          const double* wv = cvec + col0;
+          double acc = 0.0;
+#pragma unroll 4
+          for (int k = r + lane; k < np; k += 32) acc = fma(A[k], __ldcg(wv + k), acc);
+          acc = warp_sum(acc);
+          if (lane == 0) {
+            xp[col0 + r] = acc;
+            x[S.order[col0 + r]] = acc;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(&PD.ctr[1 + ph], 1u);
+    }
   }
 }
 
@@ -1117,6 +1468,46 @@ int build_solve_plan(riga_symbolic* sym) {
     L.dbl_tmax = std::max(L.dbl_tmax, tt);
   }
   L.dbl_ptr.push_back((int64_t)L.dbl_tasks.size());
+  // persistent solve: the level lists above flattened into phases
+  L.pers = env_flag("RIGA_SOLVE_PERSIST", 0) && L.small_g && L.chain_inv && L.sub_levels == 0 && !L.warp_stage;
+  L.pers_ctas = env_flag("RIGA_SOLVE_CTAS", 2 * 148);
+  if (L.pers) {
+    int phase = 0;
+    auto push = [](std::vector<int>& v, int ty, int a, int bb, int ph) {
+      v.push_back(ty); v.push_back(a); v.push_back(bb); v.push_back(ph);
+    };
+    for (int64_t l = 0; l < h.nlevels; ++l) {
+      if (L.ifwd_ptr[l + 1] > L.ifwd_ptr[l]) {
+        for (int64_t q = L.ifwd_ptr[l]; q < L.ifwd_ptr[l + 1]; ++q) push(L.ptf, kPInvF, L.ifwd[q].x, L.ifwd[q].y, phase);
+        L.pcf.push_back((int)(L.ifwd_ptr[l + 1] - L.ifwd_ptr[l]));
+        ++phase;
+      }
+      if (L.fwd_ptr[l + 1] > L.fwd_ptr[l]) {
+        for (int64_t q = L.fwd_ptr[l]; q < L.fwd_ptr[l + 1]; ++q) {
+          const int ty = L.fwd[q].y >> 24, j = L.fwd[q].y & 0x00ffffff;
+          push(L.ptf, ty == kGTiles ? kPGtF : kPUpd, L.fwd[q].x, j, phase);
+        }
+        L.pcf.push_back((int)(L.fwd_ptr[l + 1] - L.fwd_ptr[l]));
+        ++phase;
+      }
+    }
+    phase = 0;
+    for (int64_t l = h.nlevels - 1; l >= 0; --l) {
+      if (L.bwd_ptr[l + 1] > L.bwd_ptr[l]) {
+        for (int64_t q = L.bwd_ptr[l]; q < L.bwd_ptr[l + 1]; ++q) {
+          const int ty = L.bwd[q].y >> 24, j = L.bwd[q].y & 0x00ffffff;
+          push(L.ptb, ty == kGTiles ? kPGtB : kPCol, L.bwd[q].x, j, phase);
+        }
+        L.pcb.push_back((int)(L.bwd_ptr[l + 1] - L.bwd_ptr[l]));
+        ++phase;
+      }
+      if (L.ibwd_ptr[l + 1] > L.ibwd_ptr[l]) {
+        for (int64_t q = L.ibwd_ptr[l]; q < L.ibwd_ptr[l + 1]; ++q) push(L.ptb, kPInvB, L.ibwd[q].x, L.ibwd[q].y, phase);
+        L.pcb.push_back((int)(L.ibwd_ptr[l + 1] - L.ibwd_ptr[l]));
+        ++phase;
+      }
+    }
+  }
   // pull map: front position -> sources in the update-vector buffer
   const int64_t nfront = h.rows_off[ns];
   std::vector<int64_t> cnt(nfront + 1, 0);
@@ -1167,6 +1558,12 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
       RIGA_TRY(sym->d_dbl_toff.upload(L.dbl_toff.data(), L.dbl_toff.size(), s));
     }
   }
+  if (L.pers) {
+    RIGA_TRY(sym->d_ptf.upload(L.ptf.data(), std::max<size_t>(L.ptf.size(), 4), s));
+    RIGA_TRY(sym->d_ptb.upload(L.ptb.data(), std::max<size_t>(L.ptb.size(), 4), s));
+    RIGA_TRY(sym->d_pcf.upload(L.pcf.data(), std::max<size_t>(L.pcf.size(), 1), s));
+    RIGA_TRY(sym->d_pcb.upload(L.pcb.data(), std::max<size_t>(L.pcb.size(), 1), s));
+  }
   if (L.gsrc.empty())
     RIGA_TRY(sym->d_gsrc.alloc(1, s));
   else
@@ -1200,6 +1597,8 @@ static int set_solve_attrs() {
   RIGA_TRY(raise_smem(k_chain_fwd, maxsm));
   RIGA_TRY(raise_smem(k_chain_bwd, maxsm));
   RIGA_TRY(raise_smem(k_inv_fwd, maxsm));
+  RIGA_TRY(raise_smem(k_solve_pers<true>, maxsm));
+  RIGA_TRY(raise_smem(k_solve_pers<false>, maxsm));
   done = true;
   return RIGA_OK;
 }
@@ -1210,6 +1609,7 @@ int build_chain_inverse(riga_factor* F, cudaStream_t st) {
   riga_symbolic* sym = F->sym;
   const SolvePlanHost& L = sym->sp;
   SymDev S = sym->dev();
+  if (L.pers && !F->pctr.p) RIGA_TRY(F->pctr.alloc(2 + L.pcf.size() + L.pcb.size(), st));
   if (L.small_g && L.g_total) {
     if (!F->gsmall.p) RIGA_TRY(F->gsmall.alloc(L.g_total, st));
     const int nw = (int)L.wholes.size();
@@ -1261,6 +1661,25 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   const GDev GDb{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gbwd.p), gon, F->D.p, F->cvec.p};
   const int2* tf = reinterpret_cast<const int2*>(sym->d_tfwd.p);
   const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
+  if (L.pers && gon) {
+    const int nf = (int)L.pcf.size(), nb = (int)L.pcb.size();
+    const int64_t nctr = 2 + nf + nb;
+    RIGA_CHECK_ARG(F->pctr.p && (int64_t)F->pctr.n >= nctr, "persistent-solve counters not allocated");
+    RIGA_CUDA(cudaMemsetAsync(F->pctr.p, 0, nctr * sizeof(unsigned), st));
+    int64_t maxnp = 0;
+    for (int32_t c : L.chains) maxnp = std::max<int64_t>(maxnp, h.ncol[c]);
+    const size_t smem = 8 * (size_t)std::max<int64_t>(kSolveWarps * kGMaxNp, maxnp);
+    const PDev pf{reinterpret_cast<const int4*>(sym->d_ptf.p), (int)(L.ptf.size() / 4), sym->d_pcf.p, F->pctr.p};
+    const PDev pb{reinterpret_cast<const int4*>(sym->d_ptb.p), (int)(L.ptb.size() / 4), sym->d_pcb.p,
+                  F->pctr.p + 1 + nf};
+    const int gf = std::max(1, std::min(L.pers_ctas, pf.ntask)), gb = std::max(1, std::min(L.pers_ctas, pb.ntask));
+    RIGA_CUDA(launch(k_solve_pers<true>, gf, kSolveThreads, smem, st, S, T, GDf, pf, F->panel.p, sym->d_inv_off.p,
+                     F->linv.p, F->D.p, b, F->xperm.p, F->upd.p, F->cvec.p, x));
+    RIGA_CUDA(launch(k_solve_pers<false>, gb, kSolveThreads, smem, st, S, T, GDb, pb, F->panel.p, sym->d_inv_off.p,
+                     F->linv.p, F->D.p, b, F->xperm.p, F->upd.p, F->cvec.p, x));
+    count_launch(2);
+    return RIGA_OK;
+  }
   const int64_t pbytes = h.panel_total * 8;
   if (L.l2_prefetch && pbytes <= kPrefetchMaxBytes) {
     RIGA_CUDA(launch(k_prefetch_l2, (unsigned)std::min<int64_t>(148, (pbytes / 32768 + 255) / 256 + 1), 256, 0, st, F->panel.p,

@@ -395,6 +395,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     res.timings = {"boundary_s": t_bnd, "slices_s": t_sl, "total_s": time.perf_counter() - t_all,
                    "streams_used": nthreads, "kept_boundary_factors": bool(keep_factors),
                    "boundary_pairs": sum(len(v) for v in bnear.values()),
-                   "slice_wall": {int(k): [round(a, 3), round(b, 3)] for k, (a, b, _) in slice_times.items()}}
+                   "slice_wall": {int(k): [round(a, 3), round(b, 3)] for k, (a, b, _) in slice_times.items()},
+                   "slice_nfb": {int(k): int(nf) for k, (_, _, nf) in slice_times.items()}}
     res.factor_ms = [allb[k][2] for k in range(S + 1)]
     return res

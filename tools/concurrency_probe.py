@@ -88,12 +88,19 @@ def main():
                 ctxs[i].synchronize()
 
         th = [threading.Thread(target=work, args=(i,)) for i in range(T)]
+        prof = os.environ.get("PROBE_PROFILE_RANGE") == "1"
+        if prof:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
         t0 = time.perf_counter()
         for t in th:
             t.start()
         for t in th:
             t.join()
         dt = time.perf_counter() - t0
+        if prof:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.stop()
         tot = T * (a.steps + (a.cycles - 1) * (a.steps - 8)) if a.what == "extend" else T * a.steps
         print(f"{a.what} threads={T:2d} cycles={a.cycles}: {tot / dt:8.1f} steps/s aggregate, "
               f"{dt * 1e3 / a.steps:7.3f} ms per step per thread", flush=True)

@@ -28,6 +28,7 @@ for it in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
     sw = r.timings["slice_wall"]
     print("   ends:", " ".join(f"{k}:{v[1]:.2f}" for k, v in sorted(sw.items(), key=lambda kv: kv[1][1])))
 print(json.dumps(r.timings["slice_wall"]))
+print("nfb per slice", json.dumps(r.timings.get("slice_nfb")))
 print("phase seconds summed over slices", {k: round(v, 3) for k, v in r.counters.phase_s.items()})
 if r.counters.trace and len(r.counters.trace) < 100000:
     # slices per phase over time (50 ms bins, relative to the first event)
