@@ -245,6 +245,12 @@ int riga_launch_count(int64_t* count);
  * 2 SpMV (bytes 12 nnz + 4 (n+1) + 16 n), 3 CGS pass (bytes 2 rows n 8),
  * 4 vector ops, 5 lift/restart.  read: ms, work, scope counts per category. */
 int riga_prof_enable(int on);
+/* Programmatic dependent launch of the step kernels on (1) / off (0) for
+ * graphs captured from now on (default: RIGA_PDL env, off).  It shortens a
+ * lone slice's step (~10 %); with many concurrent slice streams the waiting
+ * CTAs cost more than they hide, so the slicing driver enables it only with
+ * few slices per GPU.                                                       */
+int riga_set_pdl(int on);
 int riga_prof_read(double* ms, double* work, int64_t* scopes, int ncat);
 int riga_prof_reset(void);
 

@@ -309,3 +309,101 @@ __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64
 }
 
 }  // namespace riga
+
+namespace riga {
+
+// General-stride 64 x 64 FP64 DMMA tile (4 warps x 32 x 32):
+//   acc(i, j) = sum_{t in [k0, k1)} A(i, t) B(j, t)
+//   A(i, t) = A[i as_i + t as_t],  B(j, t) = B[j bs_j + t bs_t]
+//   C(i, j) = C[i cs_i + j cs_j]  <- alpha acc  (sub: C -= acc)
+// Operand loads are coalesced along whichever of i / t has unit stride.
+__device__ __forceinline__ void dmma_tile_gen(const double* __restrict__ A, int64_t as_i, int64_t as_t,
+                                              const double* __restrict__ B, int64_t bs_j, int64_t bs_t, int64_t k0,
+                                              int64_t k1, int64_t i0, int64_t j0, int64_t mend, int64_t nend,
+                                              double* __restrict__ C, int64_t cs_i, int64_t cs_j, double alpha,
+                                              bool sub) {
+  __shared__ double As[2][16][72];
+  __shared__ double Bs[2][16][72];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const bool a_icont = as_i == 1, b_jcont = bs_j == 1;
+  double ra[8], rb[8];
+  auto load = [&](int64_t kt) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 128 * u;
+      {
+        const int t = a_icont ? idx >> 6 : idx & 15, i = a_icont ? idx & 63 : idx >> 4;
+        const int64_t kk = kt + t;
+        ra[u] = (kk < k1 && i0 + i < mend) ? A[(i0 + i) * as_i + kk * as_t] : 0.0;
+      }
+      {
+        const int t = b_jcont ? idx >> 6 : idx & 15, j = b_jcont ? idx & 63 : idx >> 4;
+        const int64_t kk = kt + t;
+        rb[u] = (kk < k1 && j0 + j < nend) ? B[(j0 + j) * bs_j + kk * bs_t] : 0.0;
+      }
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 128 * u;
+      if (a_icont) As[buf][idx >> 6][idx & 63] = ra[u];
+      else As[buf][idx & 15][idx >> 4] = ra[u];
+      if (b_jcont) Bs[buf][idx >> 6][idx & 63] = rb[u];
+      else Bs[buf][idx & 15][idx >> 4] = rb[u];
+    }
+  };
+  int buf = 0;
+  if (k0 < k1) {
+    load(k0);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t kt = k0; kt < k1; kt += 16) {
+    const bool more = kt + 16 < k1;
+    if (more) load(kt + 16);
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const int kr = k4 * 4 + (lane & 3);
+      double av[4], bv[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) av[m] = As[buf][kr][wm * 32 + m * 8 + (lane >> 2)];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bv[q] = Bs[buf][kr][wn * 32 + q * 8 + (lane >> 2)];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[m][q][0], acc[m][q][1], av[m], bv[q]);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  const int r = lane >> 2, cc = (lane & 3) * 2;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int64_t i = i0 + wm * 32 + m * 8 + r;
+    if (i >= mend) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t j = j0 + wn * 32 + q * 8 + cc;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (j + e < nend) {
+          double* p = C + i * cs_i + (j + e) * cs_j;
+          *p = sub ? *p - acc[m][q][e] : alpha * acc[m][q][e];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace riga

@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "dmma.cuh"
 #include "internal.h"
 #include "kernels.cuh"
 #include "prof.h"
@@ -617,6 +618,41 @@ __global__ void __launch_bounds__(256) k_lift(int64_t n, const double* __restric
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
     if (q0 + q < qn) X[(int64_t)(q0 + q) * ldx + c] = acc[q];
+}
+
+// X = V[:k]^T W on FP64 tensor cores: C(col, q) = sum_t V[t][col] W[t + q k],
+// one 64 x 64 (column x Ritz vector) tile per CTA (dmma.cuh)
+__global__ void __launch_bounds__(128) k_lift_dmma(const double* __restrict__ V, int64_t ld, int64_t n, int k,
+                                                   const double* __restrict__ W, int c, double* __restrict__ X) {
+  dmma_gemm_tile(V, ld, W, k, 0, k, (int64_t)blockIdx.x * 64, (int64_t)blockIdx.y * 64, n, c, X, ld, 1.0);
+}
+
+// batched locking on FP64 tensor cores (dmma_tile_gen):
+//   k_mdots_dmma  partial[z][i][q] = sum_{t in K-chunk z} A_i[t] X_q[t]  (split-K over n)
+//   k_mupd_dmma   Y_q[col] -= sum_i C[i][q] B_i[col]
+constexpr int kMKChunk = 512;
+static const bool g_lift_dmma = [] {  // RIGA_LIFT_DMMA=0: the CUDA-core lift / locking kernels
+  const char* e = getenv("RIGA_LIFT_DMMA");
+  return !(e && e[0] == '0');
+}();
+
+__global__ void __launch_bounds__(128) k_mdots_dmma(const double* __restrict__ A, int64_t lda, int R,
+                                                    const double* __restrict__ X, int64_t ldx, int c, int64_t n,
+                                                    double* __restrict__ partial) {
+  const int64_t k0 = (int64_t)blockIdx.z * kMKChunk, k1 = imin(n, k0 + kMKChunk);
+  dmma_tile_gen(A, lda, 1, X, ldx, 1, k0, k1, (int64_t)blockIdx.x * 64, (int64_t)blockIdx.y * 64, R, c,
+                partial + (int64_t)blockIdx.z * R * c, c, 1, 1.0, false);
+}
+__global__ void __launch_bounds__(128) k_mupd_dmma(const double* __restrict__ B, int64_t ldb, int R,
+                                                   const double* __restrict__ C, int c, double* __restrict__ Y,
+                                                   int64_t ldy, int64_t n) {
+  dmma_tile_gen(B, 1, ldb, C, 1, c, 0, R, (int64_t)blockIdx.x * 64, (int64_t)blockIdx.y * 64, n, c, Y, 1, ldy,
+                1.0, true);
+}
+// mode 1 of k_mupd (strictly upper: earlier batch members only) as a mask on C
+__global__ void k_mask_upper(double* __restrict__ C, int c) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < c * c && t / c >= t % c) C[t] = 0.0;  // C[i][q], keep i < q
 }
 
 // --- batched locking (ref _sweep :483-523), one converged pair at a time ---
@@ -1282,6 +1318,16 @@ namespace {
 int mdots(riga_lanczos* lz, const double* A, int R, const double* X, int c, double* C, DevBuf<double>& part) {
   cudaStream_t s = lz->ctx->stream;
   if (R == 0 || c == 0) return RIGA_OK;
+  if (g_lift_dmma) {
+    const int nz = (int)((lz->n + kMKChunk - 1) / kMKChunk);
+    RIGA_TRY(part.alloc((int64_t)nz * R * c, s));
+    const dim3 g((unsigned)((R + 63) / 64), (unsigned)((c + 63) / 64), (unsigned)nz);
+    k_mdots_dmma<<<g, 128, 0, s>>>(A, lz->ld, R, X, lz->ld, c, lz->n, part.p);
+    k_mred<<<(unsigned)(((int64_t)R * c + 255) / 256), 256, 0, s>>>(nz, R, c, part.p, C);
+    count_launch(2);
+    RIGA_CUDA(cudaGetLastError());
+    return RIGA_OK;
+  }
   const int nchunk = (int)((lz->n + kMChunk - 1) / kMChunk);
   RIGA_TRY(part.alloc((int64_t)nchunk * R * c, s));
   const dim3 g(nchunk, (unsigned)((R + 31) / 32), (unsigned)((c + 7) / 8));
@@ -1295,6 +1341,13 @@ int mdots(riga_lanczos* lz, const double* A, int R, const double* X, int c, doub
 // Y_q -= sum_i C[i][q] B_i
 int mupd(riga_lanczos* lz, const double* B, int R, const double* C, int c, int mode, double* Y) {
   if (R == 0 || c == 0) return RIGA_OK;
+  if (g_lift_dmma && mode == 0) {
+    const dim3 g((unsigned)((lz->n + 63) / 64), (unsigned)((c + 63) / 64));
+    k_mupd_dmma<<<g, 128, 0, lz->ctx->stream>>>(B, lz->ld, R, C, c, Y, lz->ld, lz->n);
+    count_launch();
+    RIGA_CUDA(cudaGetLastError());
+    return RIGA_OK;
+  }
   const dim3 g((unsigned)((lz->n + 255) / 256), (unsigned)((c + 7) / 8));
   k_mupd<<<g, 256, 0, lz->ctx->stream>>>(B, lz->ld, R, C, c, mode, Y, lz->ld, lz->n);
   count_launch();
@@ -1338,10 +1391,14 @@ int riga_lanczos_lock_block(riga_lanczos* lz, double* X, double* MX, int64_t c, 
     }
     if (cc > 1) {  // against the earlier members of the batch
       RIGA_TRY(mdots(lz, MX, cc, X, cc, G.p, part));
+      if (g_lift_dmma) {  // mode 1 (earlier batch members only) as a mask, then plain updates
+        k_mask_upper<<<(unsigned)((cc * cc + 255) / 256), 256, 0, s>>>(G.p, cc);
+        count_launch();
+      }
       RIGA_CUDA(cudaMemcpyAsync(Xt.p, X, c * lz->ld * 8, cudaMemcpyDeviceToDevice, s));
       RIGA_CUDA(cudaMemcpyAsync(MXt.p, MX, c * lz->ld * 8, cudaMemcpyDeviceToDevice, s));
-      RIGA_TRY(mupd(lz, Xt.p, cc, G.p, cc, 1, X));
-      RIGA_TRY(mupd(lz, MXt.p, cc, G.p, cc, 1, MX));
+      RIGA_TRY(mupd(lz, Xt.p, cc, G.p, cc, g_lift_dmma ? 0 : 1, X));
+      RIGA_TRY(mupd(lz, MXt.p, cc, G.p, cc, g_lift_dmma ? 0 : 1, MX));
     }
   }
   k_rowdots<<<cc, 256, 0, s>>>(X, MX, lz->ld, lz->n, nrm.p);
@@ -1378,10 +1435,16 @@ static int lift_rows(riga_lanczos* lz, const double* Vb, int64_t k, const double
                      double* X) {
   cudaStream_t s = lz->ctx->stream;
   ProfScope prof(kProfLift, s, 8.0 * (double)k * lz->n * ((c + 7) / 8));
-  const unsigned g1 = (unsigned)((lz->n + 255) / 256);
-  for (int64_t q0 = 0; q0 < c; q0 += 8) {
-    k_lift<8><<<g1, 256, k * 8 * 8, s>>>(lz->n, Vb, lz->ld, (int)k, Wd, (int)q0, (int)c, X, lz->ld);
+  if (g_lift_dmma && c >= 16) {  // (a 64-wide tile wastes most of its MMAs on fewer vectors)
+    const dim3 g((unsigned)((lz->n + 63) / 64), (unsigned)((c + 63) / 64));
+    k_lift_dmma<<<g, 128, 0, s>>>(Vb, lz->ld, lz->n, (int)k, Wd, (int)c, X);
     count_launch();
+  } else {
+    const unsigned g1 = (unsigned)((lz->n + 255) / 256);
+    for (int64_t q0 = 0; q0 < c; q0 += 8) {
+      k_lift<8><<<g1, 256, k * 8 * 8, s>>>(lz->n, Vb, lz->ld, (int)k, Wd, (int)q0, (int)c, X, lz->ld);
+      count_launch();
+    }
   }
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;

@@ -65,6 +65,11 @@ int riga_launch_count(int64_t* count) {
   return RIGA_OK;
 }
 
+int riga_set_pdl(int on) {
+  riga::g_pdl = on != 0;
+  return RIGA_OK;
+}
+
 int riga_prof_enable(int on) {
   std::lock_guard<std::mutex> lk(riga::g_mu);
   riga::g_on = on != 0;

@@ -131,6 +131,10 @@ def _priorities(work: list) -> list:
         return [0] * len(work)
     least, greatest = torch.cuda.Stream.priority_range()  # e.g. (0, -5)
     levels = least - greatest + 1
+    lv = int(os.environ.get("RIGA_PRIO_LEVELS", "2") or 0)  # 2 levels: best of 2/3/6/none (cfg3 A/B)
+    if lv > 0:
+        levels = min(levels, lv)
+        greatest = least - (levels - 1)
     order = sorted(range(len(work)), key=lambda i: (-work[i], i))
     pr = [0] * len(work)
     for rank, i in enumerate(order):
@@ -278,6 +282,14 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     cap = int(max(1, (budget - kept_bytes - cb_bytes) // max(per_slice, 1)))
     nthreads = max(1, min(streams, len(my), cap))
     one_per_thread = len(my) <= nthreads
+    # few concurrent slices: each one's step latency is the bound -> PDL on
+    # (RIGA_PDL=0/1 overrides); many: off (waiting CTAs crowd the others)
+    import os
+
+    pdl_env = os.environ.get("RIGA_PDL")
+    from . import _lib as _L
+
+    _L.lib().riga_set_pdl(int(pdl_env == "1") if pdl_env in ("0", "1") else int(nthreads <= 4))
     # one slice per stream: stream priorities by expected work; otherwise a
     # shared queue (largest first) on default-priority streams
     prio = _priorities([int(expected[k]) for k in order]) if one_per_thread else [0] * len(order)
