@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Context, device CSR system (upload / Kronecker assembly), SpMV, dots.
 //
 //  riga_system_assemble_kron  <- kron_assemble   ref assembly.py:139-186
@@ -114,10 +115,25 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t n, const int64_t* __restri
   if (row >= n) return;
   int64_t b = rp[row], e = rp[row + 1];
   double acc = 0.0;
-  for (int64_t q = b + sub; q < e; q += LANES) {
-    double a = __ldg(A + q);
-    if (MODE == 1) a = __dsub_rn(a, __dmul_rn(sigma, __ldg(B + q)));
-    acc = fma(a, __ldg(x + __ldg(ci + q)), acc);
+  // 4 elements per lane per round: all value / index loads issued before the
+  // dependent x gathers (one round trip each instead of one per element)
+  constexpr int U = 4;
+  for (int64_t q0 = b + sub; q0 < e; q0 += U * LANES) {
+    double a[U];
+    int32_t c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * LANES;
+      const bool in = q < e;
+      a[u] = in ? __ldg(A + q) : 0.0;
+      if (MODE == 1) a[u] = in ? __dsub_rn(a[u], __dmul_rn(sigma, __ldg(B + q))) : 0.0;
+      c[u] = in ? __ldg(ci + q) : 0;
+    }
+    double xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = fma(a[u], xv[u], acc);
   }
 #pragma unroll
   for (int o = LANES / 2; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o, LANES);
@@ -130,7 +146,9 @@ int csr_spmv_impl(cudaStream_t s, int64_t n, const int64_t* rp, const int32_t* c
   if (n == 0) return RIGA_OK;
   ProfScope prof(kProfSpmv, s, 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n);
   double avg = double(nnz) / double(n);
-  int lanes = avg >= 48 ? 32 : (avg >= 20 ? 16 : (avg >= 8 ? 8 : 4));
+  // about 4 elements per lane (one unrolled round) for the stencil rows of these pencils
+  int lanes = avg >= 96 ? 32 : (avg >= 40 ? 16 : (avg >= 16 ? 8 : 4));
+  if (const char* e = getenv("RIGA_SPMV_LANES")) lanes = atoi(e);
   int64_t threads = n * lanes;
   int blocks = (int)((threads + 255) / 256);
 #define RIGA_SPMV_CASE(L)                                                                  \
