@@ -51,7 +51,8 @@ struct I2 {
 
 // Task lists and pull map of the persistent solve kernels (solve.cu).
 struct SolvePlanHost {
-  int warp_stage = 0, l2_prefetch = 0, chain_inv = 1, small_g = 1, occ = 4, rest_cap = 1 << 30;
+  int warp_stage = 0, l2_prefetch = 0, chain_inv = 1, small_g = 1, occ = 4, rest_cap = 1 << 30, g_groups = 1;
+  std::vector<int32_t> gsn_f, gsn_b;   // supernode groups of the kGSn tasks (forward / backward)
   int64_t g_total = 0;                 // doubles of G = [inv(L11); L21 inv(L11)] of the small supernodes
   std::vector<int64_t> g_off;          // per supernode offset into gsmall (-1: large)
   std::vector<I2> gfwd, gbwd;          // G warp tasks: (supernode, row tile) / (supernode, column group)
@@ -100,6 +101,7 @@ struct riga_symbolic {
   riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_dbl_tasks, d_gfwd, d_gbwd, d_sub_ftiles, d_sub_btiles;
   riga::DevBuf<int64_t> d_dbl_toff;
   riga::DevBuf<int> d_ptf, d_ptb, d_pcf, d_pcb;
+  riga::DevBuf<int32_t> d_gsn_f, d_gsn_b;
   SymDev dev() const {
     return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,
                   d_cb_off.p,   d_upd_off.p,   d_child_ptr.p,  d_asm_ptr.p,    d_sparent.p,

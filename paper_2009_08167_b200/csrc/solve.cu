@@ -39,7 +39,8 @@ constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int64_t kChainSmemMax = 232448 - 4096;  // staged chain panels must fit this
 constexpr int64_t kPrefetchMaxBytes = 96ll << 20;  // prefetch the factor into L2 when it fits
 
-enum { kWholeGroup = 1, kUpd = 2, kColdot = 3, kGTiles = 4 };
+enum { kWholeGroup = 1, kUpd = 2, kColdot = 3, kGTiles = 4, kGSn = 5 };
+constexpr int kGrpMaxF = 2048;  // front rows staged per backward supernode group
 
 struct SolveDev {
   const int64_t* gptr;  // pull map over front positions (rows_off indexing)
@@ -241,10 +242,84 @@ struct GDev {
   const int2* tiles;      // warp tasks: (supernode, 32-row tile) forward / (supernode, 8-column group) backward
   int on;
   const double* D;        // pivots
+  const int32_t* sn;      // supernode groups (kGSn tasks): ids, grouped per level
   double* wz;             // z ./ d of the small supernodes (forward -> backward), so the
                           // backward column groups of one supernode never read the x
                           // another group of it is writing
 };
+
+// ---- supernode-group G tasks (kGSn): one CTA per group of whole supernodes --
+// The tile-per-warp tasks above re-gather a supernode's pivot rows y1 in every
+// one of its ceil(f/32) forward tiles, and re-read its whole front vector in
+// every one of its ceil(np/8) backward column groups (each a pull-map or
+// rows[] indirection, sector-granular in L2).  A group task gathers them once
+// into shared memory and its 8 warps share them.
+
+// forward tile t of supernode s with y1 already in yw (shared)
+__device__ __forceinline__ void warp_gtile_fwd_y(const SymDev& S, const SolveDev& T, const GDev& GD, int s, int t,
+                                                 const double* __restrict__ b, double* xp, double* upd,
+                                                 const double* yw, int lane) {
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const double* G = GD.g + GD.g_off[s];
+  const int i = 32 * t + lane;
+  const double yi = (i >= np && i < f) ? gather_row(S, T, s, i, np, col0, b, upd) : 0.0;
+  if (i >= f) return;
+  double a4[4] = {0.0, 0.0, 0.0, 0.0};
+  const double* Gi = G + i;
+  int k = 0;
+  for (; k + 16 <= np; k += 16) {
+    double g[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) g[u] = Gi[(k + u) * f];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) a4[u & 3] = fma(g[u], yw[k + u], a4[u & 3]);
+  }
+  for (; k < np; ++k) a4[0] = fma(Gi[k * f], yw[k], a4[0]);
+  const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+  if (i < np) {
+    xp[col0 + i] = acc;
+    GD.wz[col0 + i] = acc / GD.D[col0 + i];
+  } else {
+    upd[S.upd_off[s] + i - np] = yi - acc;
+  }
+}
+
+// backward column group g of supernode s with the front vector [z ./ d; -x2] in vs (shared)
+__device__ __forceinline__ void warp_gbwd_v(const SymDev& S, const GDev& GD, int s, int g, const double* vs,
+                                            double* xp, double* x, int lane) {
+  const int f = (int)S.front[s], np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const int c0 = 8 * g;
+  const int nc = min(8, np - c0);
+  const double* G = GD.g + GD.g_off[s];
+  double acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+  for (int r = (c0 & ~31) + lane; r < f; r += 32) {
+    const double v = vs[r];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = fma(c < nc ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
+  }
+#pragma unroll
+  for (int o = 4; o >= 1; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const bool hi = (lane & o) != 0;
+      const double send = hi ? acc[k] : acc[k + o];
+      const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+      acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
+    }
+  }
+  double v = acc[0];
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 16);
+  const int c = c0 + lane;
+  if (lane < 8 && c < np) {
+    xp[col0 + c] = v;
+    x[S.order[col0 + c]] = v;
+  }
+}
 
 // ---- static-operand prefetch (before the PDL wait) -------------------------
 // Everything a level task reads that the previous kernels of the solve do
@@ -527,6 +602,30 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDe
   for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
   const int2 task = tasks[ti];
   const int type = task.y >> 24, j = task.y & 0x00ffffff;
+  if (GT && type == kGSn) {
+    const int32_t* sn = GD.sn + task.x;
+    int off = 0;
+    for (int q = 0; q < j; ++q) {  // y1 of every supernode of the group, once
+      const int s = sn[q];
+      const int np = (int)S.ncol[s];
+      const int64_t col0 = S.col0[s];
+      for (int r = tid; r < np; r += blockDim.x) y[off + r] = gather_row(S, T, s, r, np, col0, b, upd);
+      off += np;
+    }
+    __syncthreads();
+    int tb = 0;
+    off = 0;
+    for (int q = 0; q < j; ++q) {
+      const int s = sn[q];
+      const int nt = (int)((S.front[s] + 31) / 32);
+      for (int t = (w - tb % kSolveWarps + kSolveWarps) % kSolveWarps; t < nt; t += kSolveWarps)
+        warp_gtile_fwd_y(S, T, GD, s, t, b, xp, upd, y + off, lane);
+      tb += nt;
+      off += (int)S.ncol[s];
+    }
+    __syncthreads();
+    continue;
+  }
   if (GT && type == kGTiles) {
     if (w < j) warp_gtile_fwd(S, T, GD, GD.tiles[task.x + w], b, xp, upd, y + w * kGMaxNp, lane);
     __syncwarp();
@@ -605,6 +704,31 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDe
   for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
   const int2 task = tasks[ti];
   const int type = task.y >> 24, bj = task.y & 0x00ffffff;
+  if (GT && type == kGSn) {
+    const int32_t* sn = GD.sn + task.x;
+    int off = 0;
+    for (int q = 0; q < bj; ++q) {  // front vectors [z ./ d; -x2] of the group, once
+      const int s = sn[q];
+      const int f = (int)S.front[s], np = (int)S.ncol[s];
+      const int64_t col0 = S.col0[s];
+      const int32_t* rows = S.rows + S.rows_off[s];
+      for (int r = tid; r < f; r += blockDim.x) y[off + r] = r < np ? GD.wz[col0 + r] : -xp[rows[r]];
+      off += f;
+    }
+    __syncthreads();
+    int gb = 0;
+    off = 0;
+    for (int q = 0; q < bj; ++q) {
+      const int s = sn[q];
+      const int ng = (int)((S.ncol[s] + 7) / 8);
+      for (int g = (w - gb % kSolveWarps + kSolveWarps) % kSolveWarps; g < ng; g += kSolveWarps)
+        warp_gbwd_v(S, GD, s, g, y + off, xp, x, lane);
+      gb += ng;
+      off += (int)S.front[s];
+    }
+    __syncthreads();
+    continue;
+  }
   if (GT && type == kGTiles) {
     if (w < bj) warp_gtile_bwd(S, GD, GD.tiles[task.x + w], D, xp, x, lane);
     __syncwarp();
@@ -1306,6 +1430,9 @@ int build_solve_plan(riga_symbolic* sym) {
   // small supernodes through G = [inv(L11); L21 inv(L11)] (default) or substitution
   L.small_g = env_flag("RIGA_SMALL_G", 1);
   L.occ = env_flag("RIGA_REST_OCC", 4);  // CTAs per SM the G-mode level kernels are register-bounded for
+  // G supernodes as whole-supernode group tasks (shared gathers; opt-in: the
+  // gather -> barrier -> mat-vec chain is longer than the redundant gathers save)
+  L.g_groups = env_flag("RIGA_G_GROUPS", 0);
   L.rest_cap = env_flag("RIGA_REST_CAP", 1 << 30);  // CTAs per level launch (grid-stride over the tasks)
   L.g_off.assign(ns, -1);
   L.inv_off.assign(ns, -1);
@@ -1400,7 +1527,44 @@ int build_solve_plan(riga_symbolic* sym) {
         L.g_total += h.front[s] * h.ncol[s];
       }
     }
-    if (L.small_g) {
+    if (L.small_g && L.g_groups) {
+      // small supernodes through G, one CTA task per group of whole
+      // supernodes (shared gathers): forward groups of <= 8 row tiles,
+      // backward groups of <= 8 column groups and <= kGrpMaxF front rows
+      auto flush = [&](std::vector<int32_t>& cur, std::vector<int32_t>& dst, std::vector<I2>& tasks) {
+        if (cur.empty()) return;
+        tasks.push_back({(int32_t)dst.size(), code(kGSn, (int)cur.size())});
+        dst.insert(dst.end(), cur.begin(), cur.end());
+        cur.clear();
+      };
+      std::vector<int32_t> cur;
+      int64_t units = 0, rowsum = 0;
+      for (int32_t s : small) {
+        const int64_t nt = (h.front[s] + 31) / 32;
+        if (!cur.empty() && units + nt > kSolveWarps) {
+          flush(cur, L.gsn_f, L.fwd);
+          units = rowsum = 0;
+        }
+        cur.push_back(s);
+        units += nt;
+        rowsum += h.ncol[s];
+        smf = std::max<int64_t>(smf, rowsum);
+      }
+      flush(cur, L.gsn_f, L.fwd);
+      units = rowsum = 0;
+      for (int32_t s : small) {
+        const int64_t ng = (h.ncol[s] + 7) / 8;
+        if (!cur.empty() && (units + ng > kSolveWarps || rowsum + h.front[s] > kGrpMaxF)) {
+          flush(cur, L.gsn_b, L.bwd);
+          units = rowsum = 0;
+        }
+        cur.push_back(s);
+        units += ng;
+        rowsum += h.front[s];
+        smb = std::max<int64_t>(smb, rowsum);
+      }
+      flush(cur, L.gsn_b, L.bwd);
+    } else if (L.small_g) {
       // small supernodes through G: warp tasks (32-row tiles forward,
       // 8-column groups backward), 8 per CTA
       std::vector<I2> tf, tb;
@@ -1469,7 +1633,8 @@ int build_solve_plan(riga_symbolic* sym) {
   }
   L.dbl_ptr.push_back((int64_t)L.dbl_tasks.size());
   // persistent solve: the level lists above flattened into phases
-  L.pers = env_flag("RIGA_SOLVE_PERSIST", 0) && L.small_g && L.chain_inv && L.sub_levels == 0 && !L.warp_stage;
+  L.pers = env_flag("RIGA_SOLVE_PERSIST", 0) && L.small_g && !L.g_groups && L.chain_inv && L.sub_levels == 0 &&
+           !L.warp_stage;
   L.pers_ctas = env_flag("RIGA_SOLVE_CTAS", 2 * 148);
   if (L.pers) {
     int phase = 0;
@@ -1544,6 +1709,8 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
   }
   RIGA_TRY(sym->d_gptr.upload(L.gptr.data(), L.gptr.size(), s));
   if (L.small_g && L.g_total) {
+    if (!L.gsn_f.empty()) RIGA_TRY(sym->d_gsn_f.upload(L.gsn_f.data(), L.gsn_f.size(), s));
+    if (!L.gsn_b.empty()) RIGA_TRY(sym->d_gsn_b.upload(L.gsn_b.data(), L.gsn_b.size(), s));
     RIGA_TRY(sym->d_g_off.upload(L.g_off.data(), L.g_off.size(), s));
     RIGA_TRY(sym->d_gfwd.upload(L.gfwd.data(), L.gfwd.size(), s));
     RIGA_TRY(sym->d_gbwd.upload(L.gbwd.data(), L.gbwd.size(), s));
@@ -1657,8 +1824,10 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   SymDev S = sym->dev();
   SolveDev T{sym->d_gptr.p, sym->d_gsrc.p, b_permuted ? 1 : 0};
   const int gon = L.small_g && L.g_total ? 1 : 0;
-  const GDev GDf{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gfwd.p), gon, F->D.p, F->cvec.p};
-  const GDev GDb{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gbwd.p), gon, F->D.p, F->cvec.p};
+  const GDev GDf{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gfwd.p), gon, F->D.p,
+                 sym->d_gsn_f.p, F->cvec.p};
+  const GDev GDb{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gbwd.p), gon, F->D.p,
+                 sym->d_gsn_b.p, F->cvec.p};
   const int2* tf = reinterpret_cast<const int2*>(sym->d_tfwd.p);
   const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
   if (L.pers && gon) {
@@ -1688,7 +1857,7 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   }
   if (L.nsub && gon) {
     const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_ftiles.p), 1, F->D.p,
-                  F->cvec.p};
+                  nullptr, F->cvec.p};
     RIGA_CUDA(launch(k_sub_fwd, (unsigned)L.nsub, kSolveThreads, 0, st, S, T, Gs, sym->d_sub_fptr.p, L.sub_levels, b, F->xperm.p,
                                                           F->upd.p));
     count_launch();
@@ -1739,7 +1908,7 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   }
   if (L.nsub && gon) {
     const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_btiles.p), 1, F->D.p,
-                  F->cvec.p};
+                  nullptr, F->cvec.p};
     RIGA_CUDA(launch(k_sub_bwd, (unsigned)L.nsub, kSolveThreads, 0, st, S, Gs, sym->d_sub_bptr.p, L.sub_levels, F->D.p,
                                                           F->xperm.p, x));
     count_launch();
