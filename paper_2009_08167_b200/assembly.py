@@ -59,7 +59,7 @@ class DeviceSystem:
     @classmethod
     def upload(cls, ctx, A, B=None):
         """Device copy of host CSR A (and B on the same pattern, else zeros)."""
-        A = sp.csr_array(A)
+        A = A if isinstance(A, sp.csr_array) else sp.csr_array(A)
         A.sort_indices()
         n = A.shape[0]
         rp = np.ascontiguousarray(A.indptr, dtype=np.int64)
@@ -68,9 +68,10 @@ class DeviceSystem:
         if B is None:
             bv = np.zeros_like(av)
         else:
-            B = sp.csr_array(B)
+            B = B if isinstance(B, sp.csr_array) else sp.csr_array(B)
             B.sort_indices()
-            if not (np.array_equal(B.indptr, A.indptr) and np.array_equal(B.indices, A.indices)):
+            same = B.indptr is A.indptr and B.indices is A.indices  # one pattern object
+            if not same and not (np.array_equal(B.indptr, A.indptr) and np.array_equal(B.indices, A.indices)):
                 raise ValueError("K and M must share one sparsity pattern")
             bv = np.ascontiguousarray(B.data, dtype=np.float64)
         h = ctypes.c_void_p()
