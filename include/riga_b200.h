@@ -160,10 +160,10 @@ int riga_factor_destroy(riga_factor* f);
 int riga_lanczos_create(riga_ctx* ctx, riga_system* mass, int64_t n, int64_t max_dim,
                         riga_lanczos** out);
 int riga_lanczos_destroy(riga_lanczos* lz);
-/* Empty the state for reuse by a new LanczosState with the same n, max_dim
- * and mass (k = 0, no locked rows; buffers and the captured step graph are
- * kept, so a reused state allocates nothing).                              */
-int riga_lanczos_reset(riga_lanczos* lz);
+/* Empty the state for reuse by a new LanczosState with the same n and
+ * max_dim (k = 0, no locked rows; buffers are kept, so a reused state
+ * allocates nothing) and bind `mass` (same n; NULL = Euclidean).           */
+int riga_lanczos_reset(riga_lanczos* lz, riga_system* mass);
 /* Operator for the next extend: H = (K - shift M)^{-1} M via factor f.     */
 int riga_lanczos_set_operator(riga_lanczos* lz, riga_factor* f);
 /* Current basis size k (host view). */

@@ -58,7 +58,7 @@ SIGNATURES = {
     "riga_factor_destroy": [_p],
     "riga_lanczos_create": [_p, _p, _i64, _i64, _p],
     "riga_lanczos_destroy": [_p],
-    "riga_lanczos_reset": [_p],
+    "riga_lanczos_reset": [_p, _p],
     "riga_lanczos_set_operator": [_p, _p],
     "riga_lanczos_k": [_p, _p],
     "riga_lanczos_set_start": [_p, _p],

@@ -841,6 +841,7 @@ struct riga_lanczos {
   int nblk = 0;
   // captured step graph (valid for one operator and one locked-buffer layout)
   cudaGraphExec_t gexec = nullptr;
+  bool gvalid = false;  // false: gexec holds a stale operator (update before replay)
   riga_factor* gop = nullptr;
   const double* gL = nullptr;
   int64_t gR = 0;
@@ -886,7 +887,7 @@ int grow_locked(riga_lanczos* lz, int64_t need) {
   RIGA_TRY(lz->partial.alloc(2 * (int64_t)((lz->n + kDotCols - 1) / kDotCols) * R, s));
   RIGA_TRY(lz->tk_dots.alloc(R, s));
   RIGA_CUDA(cudaMemsetAsync(lz->tk_dots.p, 0, R * sizeof(unsigned), s));
-  drop_graph(lz);
+  lz->gvalid = false;
   return RIGA_OK;
 }
 
@@ -1031,8 +1032,7 @@ int finish_pending(riga_lanczos* lz, int last) {
 
 int ensure_graph(riga_lanczos* lz) {
   const int64_t Rmax = lz->max_dim + 1 + lz->cap;
-  if (lz->gexec && lz->gop == lz->op && lz->gL == lz->L.p && lz->gR == Rmax) return RIGA_OK;
-  drop_graph(lz);
+  if (lz->gexec && lz->gvalid && lz->gop == lz->op && lz->gL == lz->L.p && lz->gR == Rmax) return RIGA_OK;
   cudaStream_t s = lz->ctx->stream;
   // kernel attributes must be set outside the capture
   RIGA_TRY(prepare_solve());
@@ -1052,9 +1052,21 @@ int ensure_graph(riga_lanczos* lz) {
     return rc;
   }
   RIGA_CUDA(e);
-  e = cudaGraphInstantiate(&lz->gexec, g, 0);
+  // same kernel sequence, new parameters (operator / buffers): update the
+  // executable graph in place (cheaper than instantiating a new one)
+  bool updated = false;
+  if (lz->gexec) {
+    cudaGraphExecUpdateResultInfo info;
+    updated = cudaGraphExecUpdate(lz->gexec, g, &info) == cudaSuccess;
+    if (!updated) {
+      cudaGetLastError();
+      drop_graph(lz);
+    }
+  }
+  if (!updated) e = cudaGraphInstantiate(&lz->gexec, g, 0);
   cudaGraphDestroy(g);
   RIGA_CUDA(e);
+  lz->gvalid = true;
   lz->gop = lz->op;
   lz->gL = lz->L.p;
   lz->gR = Rmax;
@@ -1131,16 +1143,27 @@ int riga_lanczos_destroy(riga_lanczos* lz) {
   return RIGA_OK;
 }
 
-int riga_lanczos_reset(riga_lanczos* lz) {
+int riga_lanczos_reset(riga_lanczos* lz, riga_system* mass) {
   RIGA_CHECK_ARG(lz, "null arg");
+  RIGA_CHECK_ARG(!mass || mass->n == lz->n, "mass dimension mismatch");
   DeviceGuard g(lz->ctx->device);
+  lz->sys = mass;
+  if (mass && mass->kdim && !getenv("RIGA_CSR_MASS")) {
+    if (!lz->kt1.p) {
+      RIGA_TRY(lz->kt1.alloc(lz->n, lz->ctx->stream));
+      RIGA_TRY(lz->kt2.alloc(lz->n, lz->ctx->stream));
+    }
+    lz->kron_ok = true;
+  } else {
+    lz->kron_ok = false;
+  }
   lz->k = 0;
   lz->nlocked = 0;
   lz->ev_valid = false;
   // the captured step graph holds the previous operator's device pointers;
   // a new factor may reuse the old one's host address (riga_factor*), so the
   // pointer comparison in ensure_graph cannot be trusted across states
-  drop_graph(lz);
+  lz->gvalid = false;  // re-captured (and updated in place) before the next extend
   lz->op = nullptr;
   return push_state(lz, 0, 0, 0.0);
 }
@@ -1148,7 +1171,7 @@ int riga_lanczos_reset(riga_lanczos* lz) {
 int riga_lanczos_set_operator(riga_lanczos* lz, riga_factor* f) {
   RIGA_CHECK_ARG(lz && f, "null arg");
   RIGA_CHECK_ARG(f->sym->h.n == lz->n, "operator dimension mismatch");
-  if (lz->op != f) drop_graph(lz);
+  if (lz->op != f) lz->gvalid = false;
   lz->op = f;
   return RIGA_OK;
 }
