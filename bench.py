@@ -472,8 +472,15 @@ def ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        # one process per GPU; RIGA_DIST_BACKEND=gloo (+ more ranks than GPUs) only
+        # exercises the multi-rank code path functionally, it is not a scaling run
+        backend = os.environ.get("RIGA_DIST_BACKEND", "nccl")
+        local = local % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     import paper_2009_08167_b200 as P
@@ -491,17 +498,19 @@ def ours(args):
         if world > 1:
             torch.distributed.barrier()
 
+    coll_dev = f"cuda:{dev}" if os.environ.get("RIGA_DIST_BACKEND", "nccl") == "nccl" else "cpu"
+
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         torch.distributed.all_reduce(t)
         return float(t.item())
 

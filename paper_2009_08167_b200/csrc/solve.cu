@@ -1528,6 +1528,26 @@ int build_solve_plan(riga_symbolic* sym) {
       }
     }
     if (L.small_g && L.g_groups) {
+      // bit 0: forward groups, bit 1: backward groups (the other direction keeps warp tiles)
+      std::vector<I2> tf, tb;
+      for (int32_t s : small) {
+        for (int32_t t = 0; t < (int32_t)((h.front[s] + 31) / 32); ++t) tf.push_back({s, t});
+        for (int32_t g = 0; g < (int32_t)((h.ncol[s] + 7) / 8); ++g) tb.push_back({s, g});
+      }
+      if (!(L.g_groups & 1)) {
+        for (size_t q = 0; q < tf.size(); q += kSolveWarps) {
+          const int cnt = (int)std::min<size_t>(kSolveWarps, tf.size() - q);
+          L.fwd.push_back({(int32_t)(L.gfwd.size() + q), code(kGTiles, cnt)});
+        }
+        L.gfwd.insert(L.gfwd.end(), tf.begin(), tf.end());
+      }
+      if (!(L.g_groups & 2)) {
+        for (size_t q = 0; q < tb.size(); q += kSolveWarps) {
+          const int cnt = (int)std::min<size_t>(kSolveWarps, tb.size() - q);
+          L.bwd.push_back({(int32_t)(L.gbwd.size() + q), code(kGTiles, cnt)});
+        }
+        L.gbwd.insert(L.gbwd.end(), tb.begin(), tb.end());
+      }
       // small supernodes through G, one CTA task per group of whole
       // supernodes (shared gathers): forward groups of <= 8 row tiles,
       // backward groups of <= 8 column groups and <= kGrpMaxF front rows
@@ -1539,7 +1559,7 @@ int build_solve_plan(riga_symbolic* sym) {
       };
       std::vector<int32_t> cur;
       int64_t units = 0, rowsum = 0;
-      for (int32_t s : small) {
+      for (int32_t s : (L.g_groups & 1) ? small : std::vector<int32_t>()) {
         const int64_t nt = (h.front[s] + 31) / 32;
         if (!cur.empty() && units + nt > kSolveWarps) {
           flush(cur, L.gsn_f, L.fwd);
@@ -1552,7 +1572,7 @@ int build_solve_plan(riga_symbolic* sym) {
       }
       flush(cur, L.gsn_f, L.fwd);
       units = rowsum = 0;
-      for (int32_t s : small) {
+      for (int32_t s : (L.g_groups & 2) ? small : std::vector<int32_t>()) {
         const int64_t ng = (h.ncol[s] + 7) / 8;
         if (!cur.empty() && (units + ng > kSolveWarps || rowsum + h.front[s] > kGrpMaxF)) {
           flush(cur, L.gsn_b, L.bwd);
