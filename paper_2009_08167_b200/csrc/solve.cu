@@ -31,7 +31,8 @@ namespace riga {
 
 constexpr int kWholeMaxF = 256;  // max front rows of a small (warp-task) supernode
 constexpr int kWholeMaxNp = 64;  // max pivots of a small supernode (substitution mode)
-constexpr int kGMaxNp = 128;     // max pivots of a G-mode supernode (any front size)
+constexpr int kGMaxNp = 128;     // max pivots of a G-mode supernode (any front size; 160 measured: no gain)
+constexpr int kGRows = (kGMaxNp + 31) / 32;  // row strips of a lane in k_small_g
 constexpr int kWarpPanel = 3328;  // doubles of a warp's staged panel (f * np <= this)
 constexpr int kWarpSmem = kWholeMaxF + kWarpPanel;  // doubles of smem per warp task
 constexpr int kSolveThreads = 256;
@@ -387,25 +388,28 @@ __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __rest
   const double* P = panel + S.panel_off[s];
   double* G = gbuf + g_off[s];
   for (int jb = 0; 64 * jb < np; ++jb) {
-    double x[4][8];
+    double x[kGRows][8];
 #pragma unroll
-    for (int ri = 0; ri < 4; ++ri)
+    for (int ri = 0; ri < kGRows; ++ri)
 #pragma unroll
       for (int j = 0; j < 8; ++j) x[ri][j] = (lane + 32 * ri == w + 8 * (8 * jb + j)) ? 1.0 : 0.0;
     for (int k = 64 * jb; k + 1 < np; ++k) {
       const int kr = k >> 5, kl = k & 31;
-      double l[4];
+      double l[kGRows];
 #pragma unroll
-      for (int ri = 0; ri < 4; ++ri) {
+      for (int ri = 0; ri < kGRows; ++ri) {
         const int r = lane + 32 * ri;
         l[ri] = (r > k && r < np) ? P[(int64_t)k * f + r] : 0.0;
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const double own = kr == 0 ? x[0][j] : kr == 1 ? x[1][j] : kr == 2 ? x[2][j] : x[3][j];
+        double own = x[0][j];
+#pragma unroll
+        for (int ri = 1; ri < kGRows; ++ri)
+          if (kr == ri) own = x[ri][j];
         const double xk = __shfl_sync(0xffffffffu, own, kl);
 #pragma unroll
-        for (int ri = 0; ri < 4; ++ri) x[ri][j] = fma(-l[ri], xk, x[ri][j]);
+        for (int ri = 0; ri < kGRows; ++ri) x[ri][j] = fma(-l[ri], xk, x[ri][j]);
       }
     }
 #pragma unroll
@@ -413,7 +417,7 @@ __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __rest
       const int c = w + 8 * (8 * jb + j);
       if (c < np) {
 #pragma unroll
-        for (int ri = 0; ri < 4; ++ri) {
+        for (int ri = 0; ri < kGRows; ++ri) {
           const int r = lane + 32 * ri;
           if (r < np) {
             Xs[c * LD + r] = x[ri][j];
