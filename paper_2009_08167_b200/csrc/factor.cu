@@ -191,14 +191,20 @@ __global__ void __launch_bounds__(256) k_small_front(SymDev S, const int32_t* __
 //                 and the inertia / zero-pivot counters;
 //   ROWS = true:  kPanelRows rows per CTA: L21 = A21 L_dd^{-T} D^{-1} from the
 //                 factored L_dd and D written by the first launch.
+// Left-looking inside the outer block (kbo > 0 <= kb): the panel's columns
+// first take the contributions of the block's previous columns [kbo, kb)
+// (rank <= 96, row-local: no k_syrk<0> launch between panels);
+// kbo = kb disables it (right-looking in-block updates by k_syrk<0>).
+constexpr int kLL = kNBO - kNB;  // previous in-block columns at most
 template <bool ROWS>
 __global__ void __launch_bounds__(kPanelRows) k_panel(SymDev S, const int32_t* __restrict__ nodes,
-                                                      int kb, const double* __restrict__ tol,
+                                                      int kb, int kbo, const double* __restrict__ tol,
                                                       double* __restrict__ panel,
                                                       double* __restrict__ D,
                                                       int64_t* __restrict__ stat) {
   __shared__ double Ld[kNB][kNB + 1];  // Ld[col][row]
   __shared__ double dd[kNB];
+  __shared__ double Lp[kNB][kLL + 1];  // Lp[c][t] = L(kb + c, kbo + t) d_t (left-looking factor)
   const int s = nodes[blockIdx.y];
   const int64_t f = S.front[s], np = S.ncol[s];
   if (kb >= np) return;
@@ -206,10 +212,25 @@ __global__ void __launch_bounds__(kPanelRows) k_panel(SymDev S, const int32_t* _
   const int64_t col0 = S.col0[s];
   double* P = panel + S.panel_off[s];
   const int tid = threadIdx.x, lane = tid & 31;
+  const int nll = kb - kbo;  // 0, 32, 64 or 96
+  if (nll > 0) {
+    for (int idx = tid; idx < kNB * nll; idx += blockDim.x) {
+      const int t = idx / kNB, c = idx - t * kNB;
+      Lp[c][t] = c < nbk ? P[(int64_t)(kbo + t) * f + kb + c] * D[col0 + kbo + t] : 0.0;
+    }
+    __syncthreads();
+  }
   if (!ROWS) {
     for (int idx = tid; idx < kNB * kNB; idx += blockDim.x) {
       int c = idx / kNB, r = idx % kNB;
-      Ld[c][r] = (c < nbk && r < nbk && r >= c) ? P[(kb + c) * f + kb + r] : 0.0;
+      double v = (c < nbk && r < nbk && r >= c) ? P[(kb + c) * f + kb + r] : 0.0;
+      if (nll > 0 && c < nbk && r < nbk && r >= c) {
+        // A(kb+r, kb+c) -= sum_t L(kb+r, t) d_t L(kb+c, t); L(kb+r, t) d_t = Lp[r][t]
+        double acc = 0.0;
+        for (int t = 0; t < nll; ++t) acc = fma(Lp[r][t], P[(int64_t)(kbo + t) * f + kb + c], acc);
+        v -= acc;
+      }
+      Ld[c][r] = v;
     }
     __syncthreads();
     if (tid < 32) {  // unblocked LDL^T of the diagonal block by warp 0; lane = row
@@ -260,6 +281,11 @@ __global__ void __launch_bounds__(kPanelRows) k_panel(SymDev S, const int32_t* _
     double x[kNB];
 #pragma unroll
     for (int c = 0; c < kNB; ++c) x[c] = c < nbk ? P[(kb + c) * f + r] : 0.0;
+    for (int t = 0; t < nll; ++t) {  // left-looking: x -= L(r, kbo + t) * Lp[:, t]
+      const double a = P[(int64_t)(kbo + t) * f + r];
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) x[c] = fma(-a, Lp[c][t], x[c]);
+    }
 #pragma unroll
     for (int c = 0; c < kNB; ++c) {
       if (c < nbk) {
@@ -607,6 +633,7 @@ __global__ void k_zero_cb(SymDev S, const int32_t* __restrict__ nodes, double* _
 
 static bool g_block_path = true;  // RIGA_FACTOR_PANEL=32: the 32-column panel chain
 static bool g_tile128 = true;      // RIGA_FACTOR_TILE128=0: 64 x 64 tiles for the update blocks
+static bool g_left_looking = false;  // RIGA_PANEL_LL=1: left-looking in-block panel updates (no k_syrk<0>; measured no gain)
 static int64_t g_block_max_fronts = 0;  // RIGA_FACTOR_BLOCK_FRONTS=n: block path for levels with <= n large fronts (opt-in: slower today)
 
 static int set_smem_attrs() {
@@ -617,6 +644,8 @@ static int set_smem_attrs() {
     g_block_path = !(e && std::strcmp(e, "32") == 0);
     e = getenv("RIGA_FACTOR_TILE128");
     g_tile128 = !(e && std::strcmp(e, "0") == 0);
+    e = getenv("RIGA_PANEL_LL");
+    g_left_looking = e && std::strcmp(e, "1") == 0;
     e = getenv("RIGA_FACTOR_BLOCK_FRONTS");
     if (e) g_block_max_fronts = atoll(e);
   }
@@ -705,14 +734,15 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
         // factor the outer block's columns 32 at a time (panel + in-block update)
         for (int64_t kb = kbo; !blockp && kb < std::min<int64_t>(kbo + kNBO, P.max_np_large); kb += kNB) {
           unsigned rchunks = (unsigned)std::max<int64_t>(1, (P.max_f_large - kb + kPanelRows - 1) / kPanelRows);
-          k_panel<false><<<dim3(1, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p, F->D.p,
+          const int kll = g_left_looking ? (int)kbo : (int)kb;
+          k_panel<false><<<dim3(1, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, kll, F->tol.p, F->panel.p, F->D.p,
                                                              F->stat.p);
-          k_panel<true><<<dim3(rchunks, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p,
+          k_panel<true><<<dim3(rchunks, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, kll, F->tol.p, F->panel.p,
                                                                   F->D.p, F->stat.p);
           count_launch(2);
           RIGA_CUDA(cudaGetLastError());
           int64_t m0 = kb + kNB, nend = std::min<int64_t>(kbo + kNBO, P.max_np_large);
-          if (m0 < nend) {
+          if (!g_left_looking && m0 < nend) {
             int64_t ntj = (nend - m0 + 63) / 64, nti = (P.max_f_large - m0 + 63) / 64;
             k_syrk<0><<<dim3((unsigned)(ntj * nti), nl), 128, 0, st>>>(S, ln, (int)kb, (int)kbo, F->panel.p,
                                                                       cbuf, F->D.p); count_launch();
