@@ -54,7 +54,26 @@ __device__ __forceinline__ double gather_row(const SymDev& S, const SolveDev& T,
                                              const double* upd) {
   double v = r < np ? b[T.permuted ? col0 + r : S.order[col0 + r]] : 0.0;
   const int64_t g = S.rows_off[s] + r;
-  for (int64_t q = T.gptr[g]; q < T.gptr[g + 1]; ++q) v += upd[T.gsrc[q]];
+  const int64_t q0 = T.gptr[g], q1 = T.gptr[g + 1];
+  int64_t q = q0;
+  // up to 4 contributions per round: their index loads, then their value
+  // loads, issued together (a row of a 2D/3D front has 1-4 child sources)
+  for (; q + 4 <= q1; q += 4) {
+    const int32_t i0 = T.gsrc[q], i1 = T.gsrc[q + 1], i2 = T.gsrc[q + 2], i3 = T.gsrc[q + 3];
+    const double u0 = upd[i0], u1 = upd[i1], u2 = upd[i2], u3 = upd[i3];
+    v += u0;
+    v += u1;
+    v += u2;
+    v += u3;
+  }
+  if (q + 2 <= q1) {
+    const int32_t i0 = T.gsrc[q], i1 = T.gsrc[q + 1];
+    const double u0 = upd[i0], u1 = upd[i1];
+    v += u0;
+    v += u1;
+    q += 2;
+  }
+  if (q < q1) v += upd[T.gsrc[q]];
   return v;
 }
 
