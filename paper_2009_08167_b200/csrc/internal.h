@@ -33,6 +33,34 @@ struct SymDev {
   const int32_t *level_nodes, *order;
 };
 
+namespace riga {
+// device recurrence state of one Lanczos run (lanczos.cu)
+struct LzDev {
+  int k;        // basis size; the pending direction sits in row k
+  int clo;      // coupling window [clo, k) applied by the next step
+  int nlocked;  // locked rows
+  int stop;     // 1 = breakdown, 2 = limit reached (later replays are no-ops)
+  int limit;    // extend target
+  int steps;    // steps executed since the last upload
+  int pad[2];
+  double btol;     // breakdown tolerance
+  double scal[8];  // [0] alpha, [1] |w|^2, [2] beta^2, [4] ref norm^2
+};
+
+// One member of a lockstep group (riga_lzgroup): every buffer a batched step
+// kernel needs for that slice.  Read by the kernels at run time, so the
+// group's captured graph stays valid while members change.
+struct SlicePtrs {
+  LzDev* st;
+  int64_t rows, Rmax;  // max_dim + 1, max_dim + 1 + locked capacity
+  double *V, *MV, *L, *LM, *w, *r, *Mr, *bp, *vt, *mvt;
+  double *coef, *partial, *upart, *cpl, *outs, *dscratch, *kt1, *kt2, *ks1, *ks2;
+  unsigned *tk_dots, *tk_upd;
+  const double *panel, *D, *linv, *gsmall;
+  double *xperm, *upd, *cvec;
+};
+}  // namespace riga
+
 struct LevelPlan {
   int64_t begin = 0, nsmall = 0, nlarge = 0;  // offsets into level_nodes
   // small fronts: contiguous classes [cls_begin[c], cls_begin[c+1]) with max front cls_f[c]
@@ -140,6 +168,11 @@ int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x,
                  bool b_permuted = false);
 int build_solve_plan(riga_symbolic* sym);
 int prepare_solve();
+// the solve of a lockstep group: every level kernel covers all B members
+// (grid z = member); sym is the members' common symbolic analysis
+int factor_solve_group(riga_symbolic* sym, const SlicePtrs* tab, int B, cudaStream_t s);
+// y = M x for every member (z = 2 B: member x {vt -> mvt, r -> Mr})
+int kron_mass_group(riga_system* sys, cudaStream_t s, const SlicePtrs* tab, int B);
 int upload_solve_plan(riga_symbolic* sym, cudaStream_t s);
 int build_chain_inverse(riga_factor* F, cudaStream_t s);
 }  // namespace riga

@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(kSolveThreads, 4) k_sub_bwd(SymDev S, GDev GD,
 // light kernels: WHOLE / UPD (forward), WHOLE / COLDOT (backward)
 // ---------------------------------------------------------------------------
 template <bool GT, int MINB = 4>
-__global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDev S, SolveDev T,
+__device__ __forceinline__ void k_rest_fwd_body(SymDev S, SolveDev T,
                                                             const int2* __restrict__ tasks, int ntask,
                                                             const int32_t* __restrict__ wholes,
                                                             const double* __restrict__ panel,
@@ -698,7 +698,18 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDe
 }
 
 template <bool GT, int MINB = 4>
-__global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDev S, SolveDev T,
+__global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd(SymDev S, SolveDev T,
+                                                            const int2* __restrict__ tasks, int ntask,
+                                                            const int32_t* __restrict__ wholes,
+                                                            const double* __restrict__ panel,
+                                                            const double* __restrict__ b,
+                                                            double* __restrict__ xp,
+                                                            double* __restrict__ upd, int stage, GDev GD) {
+  k_rest_fwd_body<GT, MINB>(S, T, tasks, ntask, wholes, panel, b, xp, upd, stage, GD);
+}
+
+template <bool GT, int MINB = 4>
+__device__ __forceinline__ void k_rest_bwd_body(SymDev S, SolveDev T,
                                                             const int2* __restrict__ tasks, int ntask,
                                                             const int32_t* __restrict__ wholes,
                                                             const double* __restrict__ panel,
@@ -811,6 +822,18 @@ __global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDe
     __syncthreads();  // part[] is reused by the next task of this CTA
   }
   }
+}
+
+template <bool GT, int MINB = 4>
+__global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd(SymDev S, SolveDev T,
+                                                            const int2* __restrict__ tasks, int ntask,
+                                                            const int32_t* __restrict__ wholes,
+                                                            const double* __restrict__ panel,
+                                                            const double* __restrict__ D,
+                                                            double* __restrict__ xp,
+                                                            double* __restrict__ cvec,
+                                                            double* __restrict__ x, int stage, int inv, GDev GD) {
+  k_rest_bwd_body<GT, MINB>(S, T, tasks, ntask, wholes, panel, D, xp, cvec, x, stage, inv, GD);
 }
 
 // ---------------------------------------------------------------------------
@@ -1077,7 +1100,7 @@ __global__ void __launch_bounds__(128) k_trinv_gemm2(SymDev S, const int2* __res
 }
 
 // forward: task (s, t) -> z rows [32t, 32t + 32) of supernode s
-__global__ void __launch_bounds__(256) k_inv_fwd(SymDev S, SolveDev T, const int2* __restrict__ tasks,
+__device__ __forceinline__ void k_inv_fwd_body(SymDev S, SolveDev T, const int2* __restrict__ tasks,
                                                  const int64_t* __restrict__ inv_off,
                                                  const double* __restrict__ linv,
                                                  const double* __restrict__ D, const double* __restrict__ b,
@@ -1121,8 +1144,17 @@ __global__ void __launch_bounds__(256) k_inv_fwd(SymDev S, SolveDev T, const int
   }
 }
 
+__global__ void __launch_bounds__(256) k_inv_fwd(SymDev S, SolveDev T, const int2* __restrict__ tasks,
+                                                 const int64_t* __restrict__ inv_off,
+                                                 const double* __restrict__ linv,
+                                                 const double* __restrict__ D, const double* __restrict__ b,
+                                                 double* __restrict__ xp, const double* __restrict__ upd,
+                                                 double* __restrict__ cvec) {
+  k_inv_fwd_body(S, T, tasks, inv_off, linv, D, b, xp, upd, cvec);
+}
+
 // backward: warp per pivot row r, x1[r] = sum_{k>=r} inv(L11)(k, r) w[k], w in cvec
-__global__ void __launch_bounds__(256) k_inv_bwd(SymDev S, const int2* __restrict__ tasks,
+__device__ __forceinline__ void k_inv_bwd_body(SymDev S, const int2* __restrict__ tasks,
                                                  const int64_t* __restrict__ inv_off,
                                                  const double* __restrict__ linv,
                                                  const double* __restrict__ cvec, double* __restrict__ xp,
@@ -1148,6 +1180,14 @@ __global__ void __launch_bounds__(256) k_inv_bwd(SymDev S, const int2* __restric
     xp[col0 + r] = acc;
     x[S.order[col0 + r]] = acc;
   }
+}
+
+__global__ void __launch_bounds__(256) k_inv_bwd(SymDev S, const int2* __restrict__ tasks,
+                                                 const int64_t* __restrict__ inv_off,
+                                                 const double* __restrict__ linv,
+                                                 const double* __restrict__ cvec, double* __restrict__ xp,
+                                                 double* __restrict__ x) {
+  k_inv_bwd_body(S, tasks, inv_off, linv, cvec, xp, x);
 }
 
 // ---------------------------------------------------------------------------
@@ -1781,6 +1821,48 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
   return RIGA_OK;
 }
 
+// ---- lockstep group solve: the level kernels with a member dimension -------
+template <bool GT, int MINB = 4>
+__global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd_g(const SlicePtrs* tab, SymDev S, SolveDev T,
+                                                                            const int2* __restrict__ tasks, int ntask,
+                                                                            const int32_t* __restrict__ wholes, GDev GDs) {
+  const SlicePtrs& P = tab[blockIdx.z];
+  if (P.st->stop) return;
+  GDev GD = GDs;
+  GD.g = P.gsmall;
+  GD.D = P.D;
+  GD.wz = P.cvec;
+  k_rest_fwd_body<GT, MINB>(S, T, tasks, ntask, wholes, P.panel, P.bp, P.xperm, P.upd, 0, GD);
+}
+
+template <bool GT, int MINB = 4>
+__global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd_g(const SlicePtrs* tab, SymDev S, SolveDev T,
+                                                                            const int2* __restrict__ tasks, int ntask,
+                                                                            const int32_t* __restrict__ wholes, GDev GDs) {
+  const SlicePtrs& P = tab[blockIdx.z];
+  if (P.st->stop) return;
+  GDev GD = GDs;
+  GD.g = P.gsmall;
+  GD.D = P.D;
+  GD.wz = P.cvec;
+  k_rest_bwd_body<GT, MINB>(S, T, tasks, ntask, wholes, P.panel, P.D, P.xperm, P.cvec, P.w, 0, 1, GD);
+}
+
+__global__ void __launch_bounds__(256) k_inv_fwd_g(const SlicePtrs* tab, SymDev S, SolveDev T,
+                                                   const int2* __restrict__ tasks,
+                                                   const int64_t* __restrict__ inv_off) {
+  const SlicePtrs& P = tab[blockIdx.z];
+  if (P.st->stop) return;
+  k_inv_fwd_body(S, T, tasks, inv_off, P.linv, P.D, P.bp, P.xperm, P.upd, P.cvec);
+}
+
+__global__ void __launch_bounds__(256) k_inv_bwd_g(const SlicePtrs* tab, SymDev S, const int2* __restrict__ tasks,
+                                                   const int64_t* __restrict__ inv_off) {
+  const SlicePtrs& P = tab[blockIdx.z];
+  if (P.st->stop) return;
+  k_inv_bwd_body(S, tasks, inv_off, P.linv, P.cvec, P.xperm, P.w);
+}
+
 template <typename K>
 static int raise_smem(K kernel, int maxsm) {
   cudaFuncAttributes fa;
@@ -1807,6 +1889,9 @@ static int set_solve_attrs() {
   RIGA_TRY(raise_smem(k_chain_fwd, maxsm));
   RIGA_TRY(raise_smem(k_chain_bwd, maxsm));
   RIGA_TRY(raise_smem(k_inv_fwd, maxsm));
+  RIGA_TRY(raise_smem(k_rest_fwd_g<true, 4>, maxsm));
+  RIGA_TRY(raise_smem(k_rest_bwd_g<true, 4>, maxsm));
+  RIGA_TRY(raise_smem(k_inv_fwd_g, maxsm));
   RIGA_TRY(raise_smem(k_solve_pers<true>, maxsm));
   RIGA_TRY(raise_smem(k_solve_pers<false>, maxsm));
   done = true;
@@ -1852,6 +1937,53 @@ int build_chain_inverse(riga_factor* F, cudaStream_t st) {
       k_trinv_gemm2<<<g, 128, 0, st>>>(S, dt + t0, (int)L.dbl_size[l], sym->d_inv_off.p, sym->d_dbl_toff.p + t0,
                                        tbuf.p, F->linv.p);
       count_launch(2);
+    }
+  }
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+int factor_solve_group(riga_symbolic* sym, const SlicePtrs* tab, int B, cudaStream_t st) {
+  const SymbolicHost& h = sym->h;
+  const SolvePlanHost& L = sym->sp;
+  RIGA_CHECK_ARG(L.small_g && L.g_total && L.chain_inv && !L.sub_levels && !L.g_groups && !L.warp_stage,
+                 "lockstep groups need the default solve plan (G mode, chain inverses)");
+  RIGA_TRY(set_solve_attrs());
+  SymDev S = sym->dev();
+  SolveDev T{sym->d_gptr.p, sym->d_gsrc.p, 1};
+  const GDev GDf{nullptr, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gfwd.p), 1, nullptr,
+                 sym->d_gsn_f.p, nullptr};
+  const GDev GDb{nullptr, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gbwd.p), 1, nullptr,
+                 sym->d_gsn_b.p, nullptr};
+  const int2* tf = reinterpret_cast<const int2*>(sym->d_tfwd.p);
+  const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
+  const unsigned zb = (unsigned)B;
+  for (int64_t l = 0; l < h.nlevels; ++l) {
+    const int ni = (int)(L.ifwd_ptr[l + 1] - L.ifwd_ptr[l]);
+    if (ni) {
+      k_inv_fwd_g<<<dim3(ni, 1, zb), 256, L.ifwd_smem[l], st>>>(
+          tab, S, T, reinterpret_cast<const int2*>(sym->d_ifwd.p) + L.ifwd_ptr[l], sym->d_inv_off.p);
+      count_launch();
+    }
+    const int nt = (int)(L.fwd_ptr[l + 1] - L.fwd_ptr[l]);
+    if (nt) {
+      k_rest_fwd_g<true, 4><<<dim3(nt, 1, zb), kSolveThreads, L.fwd_smem[l], st>>>(tab, S, T, tf + L.fwd_ptr[l], nt,
+                                                                                 sym->d_wholes.p, GDf);
+      count_launch();
+    }
+  }
+  for (int64_t l = h.nlevels - 1; l >= 0; --l) {
+    const int nt = (int)(L.bwd_ptr[l + 1] - L.bwd_ptr[l]);
+    if (nt) {
+      k_rest_bwd_g<true, 4><<<dim3(nt, 1, zb), kSolveThreads, L.bwd_smem[l], st>>>(tab, S, T, tb + L.bwd_ptr[l], nt,
+                                                                                 sym->d_wholes.p, GDb);
+      count_launch();
+    }
+    const int ni = (int)(L.ibwd_ptr[l + 1] - L.ibwd_ptr[l]);
+    if (ni) {
+      k_inv_bwd_g<<<dim3(ni, 1, zb), 256, 0, st>>>(tab, S, reinterpret_cast<const int2*>(sym->d_ibwd.p) + L.ibwd_ptr[l],
+                                                   sym->d_inv_off.p);
+      count_launch();
     }
   }
   RIGA_CUDA(cudaGetLastError());

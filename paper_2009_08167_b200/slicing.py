@@ -294,7 +294,15 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     # shared queue (largest first) on default-priority streams
     prio = _priorities([int(expected[k]) for k in order]) if one_per_thread else [0] * len(order)
 
+    # lockstep group (RIGA_GROUP=1): the slices' extends share one batched step graph
+    from . import eigensolver as _E
+
+    group = None
+    if os.environ.get("RIGA_GROUP") == "1" and nthreads > 1:
+        group = _E.LanczosGroup(nthreads, ctx=_take_ctx(base_ctx.device, ("group",), 0))
+
     def worker(widx):
+        _E._tls.group = group
         ctx = _take_ctx(base_ctx.device, ("slice", order[widx] if one_per_thread else widx), prio[widx])
         cnt = CostCounters()
         mine = [order[widx]] if one_per_thread else None
@@ -370,6 +378,9 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
             t.start()
         for t in threads:
             t.join()
+    if group is not None:
+        group.close()
+        _give_ctx(group.ctx)
     if errors:
         k, e = errors[0]
         raise RuntimeError(f"slice {k} failed on rank {rank}: {e}") from e
