@@ -31,14 +31,16 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False, jobs: int = 4) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, jobs: int = 4, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile the library (out / defines: an A/B variant, e.g. variants/x.so with -DNAME=V)."""
+    if out is None and not force and not needs_build():
         return LIB
     nvcc = _nvcc()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if out is None else "build_variant")
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "--expt-relaxed-constexpr",
-              "-I", os.path.join(HERE, "..", "include")] + ARCH
+              "-I", os.path.join(HERE, "..", "include")] + ARCH + [f"-D{d}" for d in defines]
     procs, objs = [], []
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
@@ -51,18 +53,19 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 4) -> str:
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     failed = []
     for src, p in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if verbose or p.returncode:
-            sys.stderr.write(out.decode())
+            sys.stderr.write(log.decode())
         if p.returncode:
             failed.append(src)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    tmp = LIB + ".tmp"
+    target = LIB if out is None else out
+    tmp = target + ".tmp"
     subprocess.run([nvcc, "-shared", "-o", tmp] + objs + ARCH + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"],
                    check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -214,6 +214,12 @@ __device__ __forceinline__ bool broke_down(const LzDev* st, double& beta, double
 
 // dots of x1 = V[k] (pending row) and x2 against rows [0, k] + locked and,
 // as tile row R, x2.x2: coef[i] (x1 side), coef[Rmax + i] (x2 side)
+#ifndef RIGA_DOT_W
+#define RIGA_DOT_W 8  // double2 row loads per lane per round of the delayed-CGS2 dots
+#endif
+#ifndef RIGA_DOT_MINB
+#define RIGA_DOT_MINB 2
+#endif
 __device__ __forceinline__ void k_dcgs_dots_body(RowSel A, const LzDev* st, int64_t n, int64_t Rmax,
                                                       const double* __restrict__ Vbase,
                                                       const double* __restrict__ x2, double* __restrict__ partial,
@@ -237,18 +243,18 @@ __device__ __forceinline__ void k_dcgs_dots_body(RowSel A, const LzDev* st, int6
     double a1 = 0.0, a2 = 0.0;
     if (c0 + kDotCols <= n) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        double2 v[8], p[8], q[8];
+      for (int h = 0; h < 16 / RIGA_DOT_W; ++h) {
+        double2 v[RIGA_DOT_W], p[RIGA_DOT_W], q[RIGA_DOT_W];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int o = 32 * (8 * h + u) + lane;
+        for (int u = 0; u < RIGA_DOT_W; ++u) {
+          const int o = 32 * (RIGA_DOT_W * h + u) + lane;
           v[u] = i < R ? __ldcs(reinterpret_cast<const double2*>(row) + o)
                        : __ldg(reinterpret_cast<const double2*>(row) + o);
           p[u] = __ldg(reinterpret_cast<const double2*>(x1 + c0) + o);
           q[u] = __ldg(reinterpret_cast<const double2*>(x2 + c0) + o);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < RIGA_DOT_W; ++u) {
           a1 = fma(v[u].x, p[u].x, a1);
           a1 = fma(v[u].y, p[u].y, a1);
           a2 = fma(v[u].x, q[u].x, a2);
@@ -293,7 +299,7 @@ __device__ __forceinline__ void k_dcgs_dots_body(RowSel A, const LzDev* st, int6
   }
 }
 
-__global__ void __launch_bounds__(256, 2) k_dcgs_dots(RowSel A, const LzDev* st, int64_t n, int64_t Rmax,
+__global__ void __launch_bounds__(256, RIGA_DOT_MINB) k_dcgs_dots(RowSel A, const LzDev* st, int64_t n, int64_t Rmax,
                                                       const double* __restrict__ Vbase,
                                                       const double* __restrict__ x2, double* __restrict__ partial,
                                                       double* __restrict__ coef, unsigned* __restrict__ tickets) {
@@ -362,20 +368,54 @@ __device__ __forceinline__ void k_dcgs_upd_body(RowSel A, const LzDev* st, int64
                                                   int64_t Rmax, const double* __restrict__ coef,
                                                   double* __restrict__ upart, const double* __restrict__ w,
                                                   double* __restrict__ vt, double* __restrict__ r,
-                                                  unsigned* __restrict__ tickets) {
+                                                  unsigned* __restrict__ tickets, const double* __restrict__ cpl) {
   pdl_start();
   if (st->stop) return;
   __shared__ double cs[2][1024];
+  __shared__ double red[32];
   __shared__ bool last;
   int64_t na, nb;
   rows_of(A, st, na, nb);
   const int64_t R = na + nb;
+  const int k = st->k;
+  // scalars of the delayed pass (see k_dcgs_scalars), computed by every CTA
+  // in the same order; CTA (0, 0) publishes alpha, |w|^2, eta, c_v; the
+  // previous beta's correction by eta is applied by k_step_finish
+  double ss = 0.0, sz = 0.0;
+  for (int64_t i = threadIdx.x; i < R; i += blockDim.x) {
+    if (i == k) continue;
+    const double sv = coef[i];
+    ss = fma(sv, sv, ss);
+    sz = fma(sv, coef[Rmax + i], sz);
+  }
+  ss = block_sum(ss, red);
+  sz = block_sum(sz, red);
+  const double vmv = coef[k], a0 = coef[Rmax + k];
+  const double eta = sqrt(fmax(vmv - ss, 1e-300));
+  const double cv = (a0 - sz) / (eta * eta);
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    double sb = 0.0;
+    for (int i = st->clo + threadIdx.x; i < k; i += blockDim.x) {
+      double bb = cpl[i];
+      if (i == k - 1 && st->steps > 0) bb *= eta;  // previous step's beta, finished now
+      sb = fma(coef[i], bb, sb);
+    }
+    sb = block_sum(sb, red);
+    if (threadIdx.x == 0) {
+      LzDev* sw = const_cast<LzDev*>(st);
+      sw->scal[0] = cv - sb / eta;
+      sw->scal[1] = coef[Rmax + R] / (eta * eta);
+      sw->scal[5] = eta;
+      sw->scal[6] = cv;
+    }
+  }
   const int64_t per = (R + kUpdGroups - 1) / kUpdGroups;
   const int64_t i0 = (int64_t)blockIdx.y * per, i1 = imin(R, i0 + per);
   const int cnt = (int)(i1 > i0 ? i1 - i0 : 0);
   for (int t = threadIdx.x; t < cnt && t < 1024; t += blockDim.x) {
-    cs[0][t] = coef[i0 + t];
-    cs[1][t] = coef[Rmax + i0 + t];
+    const bool self = i0 + t == k;  // row k takes no part in its own update
+    cs[0][t] = self ? 0.0 : coef[i0 + t];
+    cs[1][t] = self ? 0.0 : coef[Rmax + i0 + t];
   }
   __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * kUpdCols + 2 * threadIdx.x;
@@ -425,8 +465,7 @@ __device__ __forceinline__ void k_dcgs_upd_body(RowSel A, const LzDev* st, int64
   if (!last) return;
   __threadfence();
   if (valid) {
-    const double eta = st->scal[5], cv = st->scal[6];
-    const double* vk = A.V + (int64_t)st->k * A.ld;
+    const double* vk = A.V + (int64_t)k * A.ld;
     for (int e = 0; e < (pair ? 2 : 1); ++e) {
       double ps = 0.0, pz = 0.0;
 #pragma unroll
@@ -446,8 +485,8 @@ __global__ void __launch_bounds__(256) k_dcgs_upd(RowSel A, const LzDev* st, int
                                                   int64_t Rmax, const double* __restrict__ coef,
                                                   double* __restrict__ upart, const double* __restrict__ w,
                                                   double* __restrict__ vt, double* __restrict__ r,
-                                                  unsigned* __restrict__ tickets) {
-  k_dcgs_upd_body(A, st, n, ldu, Rmax, coef, upart, w, vt, r, tickets);
+                                                  unsigned* __restrict__ tickets, const double* __restrict__ cpl) {
+  k_dcgs_upd_body(A, st, n, ldu, Rmax, coef, upart, w, vt, r, tickets, cpl);
 }
 
 // row k <- (vt, M vt); row k+1 <- (r, M r) / beta~ unless the step broke down
@@ -591,12 +630,16 @@ __global__ void k_normalize_next(const LzDev* st, int64_t n, int64_t ld, const d
 
 // bookkeeping of a finished step (one thread)
 __device__ __forceinline__ void k_step_finish_body(LzDev* st, double* __restrict__ cpl, double* __restrict__ oa,
-                              double* __restrict__ ob, double* __restrict__ ow) {
+                              double* __restrict__ ob, double* __restrict__ ow, int delayed) {
   pdl_start();
   if (st->stop) return;
   double beta, wn;
   const bool broke = broke_down(st, beta, wn);
   const int k = st->k, i = st->steps;
+  if (delayed && i > 0 && k >= 1) {  // the previous step's beta, finished by this step's pass: beta~ eta
+    cpl[k - 1] *= st->scal[5];
+    ob[i - 1] *= st->scal[5];
+  }
   oa[i] = st->scal[0];
   ob[i] = beta;
   ow[i] = wn;
@@ -612,8 +655,8 @@ __device__ __forceinline__ void k_step_finish_body(LzDev* st, double* __restrict
 }
 
 __global__ void k_step_finish(LzDev* st, double* __restrict__ cpl, double* __restrict__ oa,
-                              double* __restrict__ ob, double* __restrict__ ow) {
-  k_step_finish_body(st, cpl, oa, ob, ow);
+                              double* __restrict__ ob, double* __restrict__ ow, int delayed) {
+  k_step_finish_body(st, cpl, oa, ob, ow, delayed);
 }
 
 // row k of V / MV = a, b scaled by 1 / sqrt(s[0])
@@ -870,7 +913,8 @@ __global__ void __launch_bounds__(256) k_dcgs_scalars_g(const SlicePtrs* tab) {
 }
 __global__ void __launch_bounds__(256) k_dcgs_upd_g(const SlicePtrs* tab, int64_t n, int64_t ld) {
   const SlicePtrs& P = tab[blockIdx.z];
-  k_dcgs_upd_body(RowSel{P.V, P.L, ld, 1, 1}, P.st, n, ld, P.Rmax, P.coef, P.upart, P.w, P.vt, P.r, P.tk_upd);
+  k_dcgs_upd_body(RowSel{P.V, P.L, ld, 1, 1}, P.st, n, ld, P.Rmax, P.coef, P.upart, P.w, P.vt, P.r, P.tk_upd,
+                  P.cpl);
 }
 __global__ void k_dot2_g(const SlicePtrs* tab, int64_t n, int64_t ld) {
   const SlicePtrs& P = tab[blockIdx.z];
@@ -883,7 +927,7 @@ __global__ void k_dcgs_store_g(const SlicePtrs* tab, int64_t n, int64_t ld) {
 }
 __global__ void k_step_finish_g(const SlicePtrs* tab) {
   const SlicePtrs& P = tab[blockIdx.z];
-  k_step_finish_body(P.st, P.cpl, P.outs, P.outs + P.rows, P.outs + 2 * P.rows);
+  k_step_finish_body(P.st, P.cpl, P.outs, P.outs + P.rows, P.outs + 2 * P.rows, 1);
 }
 
 struct riga_lanczos {
@@ -1037,7 +1081,7 @@ int step_tail(riga_lanczos* lz) {
   RIGA_CUDA(launch(k_normalize_next, g1, 256, 0, s, lz->st.p, lz->n, lz->ld, lz->r.p, lz->Mr.p, lz->V.p, lz->MV.p));
   count_launch();
   RIGA_CUDA(launch(k_step_finish, 1, 1, 0, s, lz->st.p, lz->cpl.p, lz->outs.p, lz->outs.p + (lz->max_dim + 1),
-                                lz->outs.p + 2 * (lz->max_dim + 1)));
+                                lz->outs.p + 2 * (lz->max_dim + 1), 0));
   count_launch();
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
@@ -1058,18 +1102,17 @@ int step_full(riga_lanczos* lz) {
     ProfScope prof(kProfCgs, s, 2.0 * (double)(lz->k + 1 + lz->nlocked) * lz->n * 8.0);
     RIGA_CUDA(launch(k_dcgs_dots, kDotGrid, 256, 0, s, sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, lz->w.p,
                                          lz->partial.p, lz->coef.p, lz->tk_dots.p));
-    RIGA_CUDA(launch(k_dcgs_scalars, 1, 256, 0, s, lz->st.p, Rmax, lz->coef.p, lz->cpl.p, ob));
     const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
     RIGA_CUDA(launch(k_dcgs_upd, gu, 256, 0, s, sel_basis(lz, false, 1), lz->st.p, lz->n, lz->ld, Rmax, lz->coef.p,
-                                  lz->upart.p, lz->w.p, lz->vt.p, lz->r.p, lz->tk_upd.p));
-    count_launch(3);
+                     lz->upart.p, lz->w.p, lz->vt.p, lz->r.p, lz->tk_upd.p, lz->cpl.p));
+    count_launch(2);
   }
   RIGA_TRY(mass_apply(lz, lz->vt.p, lz->mvt.p));
   RIGA_TRY(mass_apply(lz, lz->r.p, lz->Mr.p));
   RIGA_TRY(dot2(lz, lz->r.p, 0, lz->Mr.p, lz->r.p, lz->Mr.p, 2));  // beta~^2
   RIGA_CUDA(launch(k_dcgs_store, g1, 256, 0, s, lz->st.p, lz->n, lz->ld, lz->vt.p, lz->mvt.p, lz->r.p, lz->Mr.p, lz->V.p,
                                   lz->MV.p));
-  RIGA_CUDA(launch(k_step_finish, 1, 1, 0, s, lz->st.p, lz->cpl.p, lz->outs.p, ob, lz->outs.p + 2 * (lz->max_dim + 1)));
+  RIGA_CUDA(launch(k_step_finish, 1, 1, 0, s, lz->st.p, lz->cpl.p, lz->outs.p, ob, lz->outs.p + 2 * (lz->max_dim + 1), 1));
   count_launch(2);
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
@@ -1629,12 +1672,10 @@ int riga_lanczos_dcgs_probe(riga_lanczos* lz, const double* w, int64_t* rows) {
   if (rows) *rows = lz->k + 1 + lz->nlocked;
   RIGA_CUDA(launch(k_dcgs_dots, kDotGrid, 256, 0, s, sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, w,
                    lz->partial.p, lz->coef.p, lz->tk_dots.p));
-  RIGA_CUDA(launch(k_dcgs_scalars, 1, 256, 0, s, lz->st.p, Rmax, lz->coef.p, lz->cpl.p,
-                   lz->outs.p + (lz->max_dim + 1)));
   const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
   RIGA_CUDA(launch(k_dcgs_upd, gu, 256, 0, s, sel_basis(lz, false, 1), lz->st.p, lz->n, lz->ld, Rmax, lz->coef.p,
-                   lz->upart.p, w, lz->vt.p, lz->r.p, lz->tk_upd.p));
-  count_launch(3);
+                   lz->upart.p, w, lz->vt.p, lz->r.p, lz->tk_upd.p, lz->cpl.p));
+  count_launch(2);
   return RIGA_OK;
 }
 
@@ -1761,9 +1802,8 @@ int group_graph(riga_lzgroup* g) {
     count_launch();
     if ((rc = factor_solve_group(g->gsym, g->tab.p, g->B, c))) break;
     k_dcgs_dots_g<<<dim3(kDotGrid, 1, B), 256, 0, c>>>(g->tab.p, n, ld);
-    k_dcgs_scalars_g<<<dim3(1, 1, B), 256, 0, c>>>(g->tab.p);
     k_dcgs_upd_g<<<dim3((unsigned)((n + kUpdCols - 1) / kUpdCols), kUpdGroups, B), 256, 0, c>>>(g->tab.p, n, ld);
-    count_launch(3);
+    count_launch(2);
     if ((rc = kron_mass_group(g->gsys, c, g->tab.p, g->B))) break;
     const unsigned blocks = (unsigned)std::min<int64_t>(296, (n + 255) / 256);
     k_dot2_g<<<dim3(blocks, 1, B), 256, 0, c>>>(g->tab.p, n, ld);

@@ -44,3 +44,18 @@ torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 torch.cuda.synchronize()
 print("rows", rows.value)
+if os.environ.get("TIME_DCGS"):
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    ts = []
+    for _ in range(20):
+        flush.sum()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st.ctx.stream)
+        _lib.check(_lib.lib().riga_lanczos_dcgs_probe(st.handle, _lib.ptr(x), ctypes.byref(rows)))
+        e1.record(st.ctx.stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    by = 2.0 * rows.value * s.dof_count * 8 + 6.0 * s.dof_count * 8
+    print(f"dcgs R={rows.value}: {ms * 1e3:.1f} us  {by / ms / 1e6:.0f} GB/s")
