@@ -55,6 +55,10 @@ __device__ __forceinline__ void rows_of(const RowSel& A, const LzDev* st, int64_
 //         kUpdGroups), then y[c] -= sum_g upart[g][c]  (fixed order, by the
 //         last group of the column strip)
 constexpr int kDotCols = 1024;
+#ifndef RIGA_DOT_COLS
+#define RIGA_DOT_COLS 2048  // columns of a delayed-CGS2 dots tile (>= kDotCols: partial buffers; 2048 > 1024 by 6 %)
+#endif
+constexpr int kDotColsD = RIGA_DOT_COLS;
 constexpr int kUpdGroups = 8;
 constexpr int kUpdCols = 512;   // columns per update CTA (2 per thread)
 constexpr int kUpdUnroll = 8;   // row loads in flight per thread
@@ -231,19 +235,19 @@ __device__ __forceinline__ void k_dcgs_dots_body(RowSel A, const LzDev* st, int6
   const int64_t R = na + nb, RT = R + 1;
   const double* x1 = Vbase + (int64_t)st->k * A.ld;
   const int lane = threadIdx.x & 31;
-  const int nchunk = (int)((n + kDotCols - 1) / kDotCols);
+  const int nchunk = (int)((n + kDotColsD - 1) / kDotColsD);
   const int64_t P2 = (int64_t)nchunk * Rmax;
   const int64_t ntiles = (int64_t)nchunk * RT;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += nwarps) {
     const int chunk = (int)(t / RT);
     const int64_t i = t - (int64_t)chunk * RT;
-    const int64_t c0 = (int64_t)chunk * kDotCols;
+    const int64_t c0 = (int64_t)chunk * kDotColsD;
     const double* row = (i < R ? sel_row(A, na, i) : x2) + c0;
     double a1 = 0.0, a2 = 0.0;
-    if (c0 + kDotCols <= n) {
+    if (c0 + kDotColsD <= n) {
 #pragma unroll
-      for (int h = 0; h < 16 / RIGA_DOT_W; ++h) {
+      for (int h = 0; h < kDotColsD / 64 / RIGA_DOT_W; ++h) {
         double2 v[RIGA_DOT_W], p[RIGA_DOT_W], q[RIGA_DOT_W];
 #pragma unroll
         for (int u = 0; u < RIGA_DOT_W; ++u) {
