@@ -519,7 +519,11 @@ def ours(args):
     lam_e, count = P.choose_lambda_e(system, c.n0)
     shifts = P.uniform_shifts(lam_e, c.slices)
     perm = P.separator_ordering(system)
-    sym = Symbolic.on_device(system.device, perm)
+    from paper_2009_08167_b200.slicing import solve_plan, solve_sub_levels
+
+    per_gpu = -(-c.slices // world)
+    with solve_plan(solve_sub_levels(min(args.streams, per_gpu))):
+        sym = Symbolic.on_device(system.device, perm)
     seeds = list(range(c.slices))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{dev}")  # 256 MB > L2
 

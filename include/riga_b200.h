@@ -268,6 +268,10 @@ int riga_prof_enable(int on);
  * CTAs cost more than they hide, so the slicing driver enables it only with
  * few slices per GPU.                                                       */
 int riga_set_pdl(int on);
+/* Height bound of the bottom subtrees whose solve runs as one CTA each, for
+ * symbolic analyses created from now on (default 6; RIGA_SUB_LEVELS
+ * overrides).  Few concurrent slices per GPU: 6 (latency); 16: 8.          */
+int riga_set_solve_sub_levels(int levels);
 int riga_prof_read(double* ms, double* work, int64_t* scopes, int ncat);
 int riga_prof_reset(void);
 

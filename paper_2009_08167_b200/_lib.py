@@ -87,6 +87,7 @@ SIGNATURES = {
     "riga_dot": [_p, _i64, _p, _p, _p],
     "riga_launch_count": [_p],
     "riga_set_pdl": [_i32],
+    "riga_set_solve_sub_levels": [_i32],
     "riga_prof_enable": [_i32],
     "riga_prof_read": [_p, _p, _p, _i32],
     "riga_prof_reset": [],

@@ -1477,6 +1477,13 @@ static int env_flag(const char* name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 
+// bottom subtrees of G supernodes below this height run as one CTA each
+// (k_sub_fwd/bwd).  cfg3 A/B of the solve: 6 is best for 1-4 concurrent
+// slices (lone solve 0.295 -> 0.253 ms), 8 for 16 (+17 % solves/s, lone
+// +28 % slower); riga_set_solve_sub_levels picks it per run, RIGA_SUB_LEVELS
+// overrides.  Read when a symbolic analysis builds its solve plan.
+static int g_sub_levels = 6;
+
 int build_solve_plan(riga_symbolic* sym) {
   const SymbolicHost& h = sym->h;
   SolvePlanHost& L = sym->sp;
@@ -1508,7 +1515,7 @@ int build_solve_plan(riga_symbolic* sym) {
   // bottom subtrees (G mode): maximal subtrees of small supernodes of height
   // < sub_levels; supernodes are numbered in postorder, so a subtree is a
   // contiguous range
-  L.sub_levels = L.small_g ? env_flag("RIGA_SUB_LEVELS", 0) : 0;
+  L.sub_levels = L.small_g ? env_flag("RIGA_SUB_LEVELS", g_sub_levels) : 0;
   std::vector<char> in_sub(ns, 0);
   if (L.sub_levels > 0) {
     const int SL = L.sub_levels;
@@ -1989,6 +1996,16 @@ int factor_solve_group(riga_symbolic* sym, const SlicePtrs* tab, int B, cudaStre
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
 }
+
+}  // namespace riga
+
+extern "C" int riga_set_solve_sub_levels(int levels) {
+  RIGA_CHECK_ARG(levels >= 0 && levels <= 64, "sub levels out of range");
+  riga::g_sub_levels = levels;
+  return RIGA_OK;
+}
+
+namespace riga {
 
 int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bool b_permuted) {
   riga_symbolic* sym = F->sym;

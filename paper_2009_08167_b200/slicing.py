@@ -171,6 +171,31 @@ def _allgather(obj, group_world):
     return out
 
 
+def solve_sub_levels(slices_per_gpu: int) -> int:
+    """Subtree height of the solve plan for a run with this many concurrent
+    slices per GPU (riga_set_solve_sub_levels: 8 for many, 6 for few)."""
+    return 8 if slices_per_gpu >= 12 else 6
+
+
+class solve_plan:
+    """Symbolic analyses created inside the block use `sub_levels`."""
+
+    def __init__(self, sub_levels: int):
+        self.levels = sub_levels
+
+    def __enter__(self):
+        from . import _lib as _L
+
+        _L.lib().riga_set_solve_sub_levels(int(self.levels))
+        return self
+
+    def __exit__(self, *exc):
+        from . import _lib as _L
+
+        _L.lib().riga_set_solve_sub_levels(6)
+        return False
+
+
 def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams: int = 4,
                          rank: int = 0, world: int = 1, vectors_to_host: bool = True,
                          pencil_symbolic: Symbolic | None = None, perm=None,
@@ -184,7 +209,11 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     base_ctx = _dev.current()
     if perm is None:
         perm = separator_ordering(system)
-    sym = pencil_symbolic or Symbolic.on_device(system.device, perm)
+    if pencil_symbolic is None:
+        with solve_plan(solve_sub_levels(min(streams, -(-S // max(world, 1))))):
+            sym = Symbolic.on_device(system.device, perm)
+    else:
+        sym = pencil_symbolic
 
     def make_pencil(ctx, cnt):
         p = _Pencil.__new__(_Pencil)
