@@ -22,6 +22,9 @@
 //                    (mma.sync m8n8k4 -> DMMA)
 // Inertia = count of negative pivots (integer atomics, order independent).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "dmma.cuh"
@@ -805,18 +808,30 @@ int riga_symbolic_create(riga_system* sys, const int64_t* perm, riga_symbolic** 
   DeviceGuard g(sys->ctx->device);
   std::vector<int64_t> rp(sys->n + 1);
   std::vector<int32_t> ci(sys->nnz);
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   RIGA_TRY(riga_system_download(sys, rp.data(), ci.data(), nullptr, nullptr));
   auto sym = std::make_unique<riga_symbolic>();
   sym->ctx = sys->ctx;
   sym->ctxref.set(sys->ctx);
   sym->sys = sys;
   std::string err;
+  const auto t1 = clk::now();
   if (analyze(sys->n, rp.data(), ci.data(), perm, sym->h, err)) {
     set_error("symbolic analysis: " + err);
     return RIGA_BAD_ARG;
   }
+  const auto t2 = clk::now();
   RIGA_TRY(finish_symbolic(sym.get()));
+  const auto t3 = clk::now();
   RIGA_TRY(upload_symbolic(sym.get()));
+  if (std::getenv("RIGA_SYM_TIME")) {
+    auto ms = [](clk::time_point a, clk::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    std::fprintf(stderr, "symbolic_create: download %.1f analyze %.1f plans %.1f upload %.1f ms\n", ms(t0, t1),
+                 ms(t1, t2), ms(t2, t3), ms(t3, clk::now()));
+  }
   *out = sym.release();
   return RIGA_OK;
 }

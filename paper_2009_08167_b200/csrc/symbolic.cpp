@@ -18,13 +18,53 @@
 #include "symbolic.h"
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <map>
 #include <numeric>
 #include <string>
+#include <thread>
 
 namespace riga {
 
 namespace {
+
+// Host threads for the pattern sweeps (column counts, front structures, the
+// scatter map): RIGA_SYM_THREADS, default min(16, hardware threads).
+int sym_threads(int64_t work) {
+  static const int t = [] {
+    const char* e = std::getenv("RIGA_SYM_THREADS");
+    const int h = (int)std::thread::hardware_concurrency();
+    return std::max(1, e ? std::atoi(e) : std::min(16, std::max(1, h)));
+  }();
+  return work < 4096 ? 1 : t;
+}
+
+template <class F>
+void par_run(int nt, F&& f) {  // f(thread index), joined before returning
+  if (nt <= 1) {
+    f(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(nt - 1);
+  for (int t = 1; t < nt; ++t) th.emplace_back([&f, t] { f(t); });
+  f(0);
+  for (auto& x : th) x.join();
+}
+
+// Dynamic chunks of [0, n) over nt threads: f(thread, begin, end).
+template <class F>
+void par_chunks(int nt, int64_t n, int64_t chunk, F&& f) {
+  std::atomic<int64_t> next{0};
+  par_run(nt, [&](int t) {
+    for (;;) {
+      const int64_t b = next.fetch_add(chunk);
+      if (b >= n) break;
+      f(t, b, std::min(n, b + chunk));
+    }
+  });
+}
 
 struct Relax {
   int64_t nrelax[3] = {4, 16, 48};
@@ -54,11 +94,37 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
   }
   // ---- 1. elimination tree in the caller's order ------------------------
   // upper entries of column k of PAP^T = neighbours c of perm[k] with ip[c] < k
+  // The permuted upper pattern is filtered in parallel first, so the serial
+  // ancestor walk reads only the entries it uses.
+  std::vector<int64_t> uptr(n + 1, 0);
+  std::vector<int32_t> upat;
+  {
+    const int nt = sym_threads(n);
+    par_chunks(nt, n, 2048, [&](int, int64_t k0, int64_t k1) {
+      for (int64_t k = k0; k < k1; ++k) {
+        const int64_t o = perm[k];
+        int64_t c = 0;
+        for (int64_t q = rowptr[o]; q < rowptr[o + 1]; ++q) c += ip[colidx[q]] < k;
+        uptr[k + 1] = c;
+      }
+    });
+    for (int64_t k = 0; k < n; ++k) uptr[k + 1] += uptr[k];
+    upat.resize(uptr[n]);
+    par_chunks(nt, n, 2048, [&](int, int64_t k0, int64_t k1) {
+      for (int64_t k = k0; k < k1; ++k) {
+        const int64_t o = perm[k];
+        int64_t w = uptr[k];
+        for (int64_t q = rowptr[o]; q < rowptr[o + 1]; ++q) {
+          const int32_t i = ip[colidx[q]];
+          if (i < k) upat[w++] = i;
+        }
+      }
+    });
+  }
   std::vector<int64_t> parent(n, -1), anc(n, -1);
   for (int64_t k = 0; k < n; ++k) {
-    int64_t o = perm[k];
-    for (int64_t q = rowptr[o]; q < rowptr[o + 1]; ++q) {
-      int64_t i = ip[colidx[q]];
+    for (int64_t q = uptr[k]; q < uptr[k + 1]; ++q) {
+      int64_t i = upat[q];
       while (i != -1 && i < k) {
         int64_t nxt = anc[i];
         anc[i] = k;
@@ -113,22 +179,39 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
   const std::vector<int32_t>& io = S.iorder;
 
   // ---- 3. exact column counts (row subtrees) -----------------------------
+  // Row k of L is the union of the tree paths from A's entries (i < k) up to
+  // k; rows are independent, so threads take row chunks with private marks
+  // and counts, summed afterwards.
   S.colcount.assign(n, 1);
   {
-    std::vector<int64_t> mark(n, -1);
-    for (int64_t k = 0; k < n; ++k) {
-      mark[k] = k;
-      int64_t o = S.order[k];
-      for (int64_t q = rowptr[o]; q < rowptr[o + 1]; ++q) {
-        int64_t i = io[colidx[q]];
-        if (i >= k) continue;
-        while (mark[i] != k) {
-          mark[i] = k;
-          S.colcount[i] += 1;
-          i = par[i];
+    const int nt = sym_threads(n);
+    std::vector<std::vector<int32_t>> cnt(nt), marks(nt);
+    par_chunks(nt, n, 1024, [&](int t, int64_t k0, int64_t k1) {
+      if (cnt[t].empty()) {
+        cnt[t].assign(n, 0);
+        marks[t].assign(n, -1);
+      }
+      int32_t* c = cnt[t].data();
+      int32_t* mark = marks[t].data();
+      for (int64_t k = k0; k < k1; ++k) {
+        mark[k] = (int32_t)k;
+        const int64_t o = S.order[k];
+        for (int64_t q = rowptr[o]; q < rowptr[o + 1]; ++q) {
+          int64_t i = io[colidx[q]];
+          if (i >= k) continue;
+          while (mark[i] != (int32_t)k) {
+            mark[i] = (int32_t)k;
+            c[i] += 1;
+            i = par[i];
+          }
         }
       }
-    }
+    });
+    par_chunks(nt, n, 16384, [&](int, int64_t b, int64_t e) {
+      for (const auto& c : cnt)
+        if (!c.empty())
+          for (int64_t i = b; i < e; ++i) S.colcount[i] += c[i];
+    });
   }
   S.fill_nnz = 0;
   S.factor_flops = 0;
@@ -247,43 +330,74 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
   // ---- 5a. front structures ---------------------------------------------
   // struct(s) = cols(s) U {rows > last(s) of A's lower columns in s}
   //           U {update rows of children > last(s)}, sorted.
+  // Supernodes of one tree level are independent (children sit at lower
+  // levels), so each level is one parallel sweep.
+  S.level.assign(ns, 0);
+  int32_t maxlev = 0;
+  for (int64_t s = 0; s < ns; ++s) {  // children precede parents
+    if (S.sparent[s] >= 0)
+      S.level[S.sparent[s]] = std::max(S.level[S.sparent[s]], S.level[s] + 1);
+    maxlev = std::max(maxlev, S.level[s]);
+  }
+  S.nlevels = maxlev + 1;
+  S.level_ptr.assign(S.nlevels + 1, 0);
+  for (int64_t s = 0; s < ns; ++s) S.level_ptr[S.level[s] + 1]++;
+  for (int64_t l = 0; l < S.nlevels; ++l) S.level_ptr[l + 1] += S.level_ptr[l];
+  S.level_nodes.resize(ns);
+  {
+    std::vector<int64_t> fillp(S.level_ptr.begin(), S.level_ptr.end() - 1);
+    for (int64_t s = 0; s < ns; ++s) S.level_nodes[fillp[S.level[s]]++] = (int32_t)s;
+  }
   S.front.resize(ns);
   S.rows_off.resize(ns + 1);
-  S.rows.clear();
-  std::vector<int64_t> mark(n, -1);
-  std::vector<int32_t> tmp;
-  S.rows_off[0] = 0;
-  for (int64_t s = 0; s < ns; ++s) {
-    int64_t a = S.col0[s], e = S.col0[s] + S.ncol[s] - 1;
-    tmp.clear();
-    for (int64_t j = a; j <= e; ++j) mark[j] = s;
-    for (int64_t j = a; j <= e; ++j) {
-      int64_t o = S.order[j];
-      for (int64_t q = rowptr[o]; q < rowptr[o + 1]; ++q) {
-        int64_t i = io[colidx[q]];
-        if (i > e && mark[i] != s) {
-          mark[i] = s;
-          tmp.push_back((int32_t)i);
+  {
+    std::vector<std::vector<int32_t>> fr(ns);
+    const int nt = sym_threads(n);
+    std::vector<std::vector<int32_t>> marks(nt);
+    auto one = [&](int32_t* mark, int64_t s) {
+      const int64_t a = S.col0[s], e = S.col0[s] + S.ncol[s] - 1;
+      std::vector<int32_t>& out = fr[s];
+      out.clear();
+      for (int64_t j = a; j <= e; ++j) out.push_back((int32_t)j);
+      const size_t head = out.size();
+      for (int64_t j = a; j <= e; ++j) mark[j] = (int32_t)s;
+      for (int64_t j = a; j <= e; ++j) {
+        const int64_t o = S.order[j];
+        for (int64_t q = rowptr[o]; q < rowptr[o + 1]; ++q) {
+          const int64_t i = io[colidx[q]];
+          if (i > e && mark[i] != (int32_t)s) {
+            mark[i] = (int32_t)s;
+            out.push_back((int32_t)i);
+          }
         }
       }
-    }
-    for (int64_t t = S.child_ptr[s]; t < S.child_ptr[s + 1]; ++t) {
-      int64_t c = S.child_list[t];
-      int64_t f_c = S.front[c], np_c = S.ncol[c];
-      const int32_t* rc = &S.rows[S.rows_off[c]];
-      for (int64_t u = np_c; u < f_c; ++u) {
-        int64_t i = rc[u];
-        if (i > e && mark[i] != s) {
-          mark[i] = s;
-          tmp.push_back((int32_t)i);
+      for (int64_t t = S.child_ptr[s]; t < S.child_ptr[s + 1]; ++t) {
+        const std::vector<int32_t>& rc = fr[S.child_list[t]];
+        for (size_t u = S.ncol[S.child_list[t]]; u < rc.size(); ++u) {
+          const int64_t i = rc[u];
+          if (i > e && mark[i] != (int32_t)s) {
+            mark[i] = (int32_t)s;
+            out.push_back((int32_t)i);
+          }
         }
       }
+      std::sort(out.begin() + head, out.end());
+      S.front[s] = (int64_t)out.size();
+    };
+    for (int64_t l = 0; l < S.nlevels; ++l) {
+      const int64_t b = S.level_ptr[l], cnt = S.level_ptr[l + 1] - b;
+      const int ntl = cnt < 64 ? 1 : nt;
+      par_chunks(ntl, cnt, 8, [&](int t, int64_t q0, int64_t q1) {
+        if (marks[t].empty()) marks[t].assign(n, -1);
+        for (int64_t q = q0; q < q1; ++q) one(marks[t].data(), S.level_nodes[b + q]);
+      });
     }
-    std::sort(tmp.begin(), tmp.end());
-    for (int64_t j = a; j <= e; ++j) S.rows.push_back((int32_t)j);
-    S.rows.insert(S.rows.end(), tmp.begin(), tmp.end());
-    S.front[s] = S.ncol[s] + (int64_t)tmp.size();
-    S.rows_off[s + 1] = (int64_t)S.rows.size();
+    S.rows_off[0] = 0;
+    for (int64_t s = 0; s < ns; ++s) S.rows_off[s + 1] = S.rows_off[s] + S.front[s];
+    S.rows.resize(S.rows_off[ns]);
+    par_chunks(nt, ns, 64, [&](int, int64_t s0, int64_t s1) {
+      for (int64_t s = s0; s < s1; ++s) std::copy(fr[s].begin(), fr[s].end(), S.rows.begin() + S.rows_off[s]);
+    });
   }
   // ---- 5b. storage offsets, statistics -------------------------------------
   S.panel_off.resize(ns);
@@ -336,51 +450,57 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
     }
   }
   // ---- 5d. original-entry scatter map (lower triangle, by supernode) ------
+  // Two parallel passes over supernodes: count, then fill at the prefix sums.
   S.asm_ptr.assign(ns + 1, 0);
-  S.asm_slot.clear();
-  S.asm_local.clear();
   {
-    std::vector<int32_t> pos(n, -1);
-    for (int64_t s = 0; s < ns; ++s) {
-      const int32_t* rs = &S.rows[S.rows_off[s]];
-      int64_t f = S.front[s];
-      for (int64_t u = 0; u < f; ++u) pos[rs[u]] = (int32_t)u;
-      for (int64_t j = S.col0[s]; j < S.col0[s] + S.ncol[s]; ++j) {
-        int64_t o = S.order[j];
-        for (int64_t q = rowptr[o]; q < rowptr[o + 1]; ++q) {
-          int64_t i = io[colidx[q]];
-          if (i < j) continue;
-          int32_t r = pos[i];
-          if (r < 0) {
-            err = "original entry outside its front";
-            return 1;
-          }
-          S.asm_slot.push_back(q);
-          S.asm_local.push_back((int32_t)((j - S.col0[s]) * f + r));
+    const int nt = sym_threads(n);
+    par_chunks(nt, ns, 32, [&](int, int64_t s0, int64_t s1) {
+      for (int64_t s = s0; s < s1; ++s) {
+        int64_t c = 0;
+        for (int64_t j = S.col0[s]; j < S.col0[s] + S.ncol[s]; ++j) {
+          const int64_t o = S.order[j];
+          for (int64_t q = rowptr[o]; q < rowptr[o + 1]; ++q) c += io[colidx[q]] >= j;
         }
+        S.asm_ptr[s + 1] = c;
       }
-      for (int64_t u = 0; u < f; ++u) pos[rs[u]] = -1;
-      S.asm_ptr[s + 1] = (int64_t)S.asm_slot.size();
+    });
+    for (int64_t s = 0; s < ns; ++s) S.asm_ptr[s + 1] += S.asm_ptr[s];
+    S.asm_slot.resize(S.asm_ptr[ns]);
+    S.asm_local.resize(S.asm_ptr[ns]);
+    std::vector<std::vector<int32_t>> poss(nt);
+    std::atomic<int> bad{0};
+    par_chunks(nt, ns, 32, [&](int t, int64_t s0, int64_t s1) {
+      if (poss[t].empty()) poss[t].assign(n, -1);
+      int32_t* pos = poss[t].data();
+      for (int64_t s = s0; s < s1; ++s) {
+        const int32_t* rs = &S.rows[S.rows_off[s]];
+        const int64_t f = S.front[s];
+        int64_t w = S.asm_ptr[s];
+        for (int64_t u = 0; u < f; ++u) pos[rs[u]] = (int32_t)u;
+        for (int64_t j = S.col0[s]; j < S.col0[s] + S.ncol[s]; ++j) {
+          const int64_t o = S.order[j];
+          for (int64_t q = rowptr[o]; q < rowptr[o + 1]; ++q) {
+            const int64_t i = io[colidx[q]];
+            if (i < j) continue;
+            const int32_t r = pos[i];
+            if (r < 0) {
+              bad = 1;
+              continue;
+            }
+            S.asm_slot[w] = q;
+            S.asm_local[w++] = (int32_t)((j - S.col0[s]) * f + r);
+          }
+        }
+        for (int64_t u = 0; u < f; ++u) pos[rs[u]] = -1;
+      }
+    });
+    if (bad) {
+      err = "original entry outside its front";
+      return 1;
     }
   }
   S.nnz_lower = (int64_t)S.asm_slot.size();
-  // ---- 5e. levels -----------------------------------------------------------
-  S.level.assign(ns, 0);
-  int32_t maxlev = 0;
-  for (int64_t s = 0; s < ns; ++s) {  // children precede parents
-    if (S.sparent[s] >= 0)
-      S.level[S.sparent[s]] = std::max(S.level[S.sparent[s]], S.level[s] + 1);
-    maxlev = std::max(maxlev, S.level[s]);
-  }
-  S.nlevels = maxlev + 1;
-  S.level_ptr.assign(S.nlevels + 1, 0);
-  for (int64_t s = 0; s < ns; ++s) S.level_ptr[S.level[s] + 1]++;
-  for (int64_t l = 0; l < S.nlevels; ++l) S.level_ptr[l + 1] += S.level_ptr[l];
-  S.level_nodes.resize(ns);
-  {
-    std::vector<int64_t> fillp(S.level_ptr.begin(), S.level_ptr.end() - 1);
-    for (int64_t s = 0; s < ns; ++s) S.level_nodes[fillp[S.level[s]]++] = (int32_t)s;
-  }
+  // ---- 5e. levels (computed in 5a): small fronts first within a level -------
   S.level_nsmall.assign(S.nlevels, 0);
   for (int64_t l = 0; l < S.nlevels; ++l) {
     auto b = S.level_nodes.begin() + S.level_ptr[l], e = S.level_nodes.begin() + S.level_ptr[l + 1];
