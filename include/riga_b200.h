@@ -186,6 +186,12 @@ int riga_lanczos_locked_count(riga_lanczos* lz, int64_t* count);
 int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_host,
                         double breakdown_tol, double* alpha, double* beta, double* wnorm,
                         int64_t* steps);
+/* Engine extension (no reference counterpart): run the step replays of
+ * later extends on `stream` (a cudaStream_t; NULL = the context stream),
+ * forked from and joined back to the context stream, so a driver can move a
+ * slice's extends between stream priorities; allocations stay on the
+ * context stream.  riga_lanczos_reset clears it.                           */
+int riga_lanczos_set_run_stream(riga_lanczos* lz, void* stream);
 /* Device milliseconds of the last extend's step replays (CUDA events on
  * the state's stream around the replayed step graphs; 0 if none ran).      */
 int riga_lanczos_last_extend_ms(riga_lanczos* lz, float* ms);

@@ -67,6 +67,7 @@ SIGNATURES = {
     "riga_lanczos_locked_count": [_p, _p],
     "riga_lanczos_extend": [_p, _i64, _p, _d, _p, _p, _p, _p],
     "riga_lanczos_last_extend_ms": [_p, _p],
+    "riga_lanczos_set_run_stream": [_p, _p],
     "riga_lzgroup_create": [_p, _i32, _p],
     "riga_lzgroup_destroy": [_p],
     "riga_lzgroup_begin": [_p, _i32, _p, _i64, _p, _d],

@@ -960,11 +960,18 @@ struct riga_lanczos {
   long long gnodes = 0;  // kernel launches per replay
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // around the last extend's replays
   bool ev_valid = false;
+  // optional stream the step replays run on (forked from / joined back to the
+  // context stream around each extend): lets a driver move a slice's extends
+  // between stream priorities without moving its allocations
+  cudaStream_t run = nullptr;
+  cudaEvent_t evf = nullptr, evj = nullptr;
   cudaStream_t cur = nullptr;   // stream the step helpers launch on
   cudaStream_t capst = nullptr; // private stream for graph capture (never legacy)
   ~riga_lanczos() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (evf) cudaEventDestroy(evf);
+    if (evj) cudaEventDestroy(evj);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (capst) cudaStreamDestroy(capst);
     if (hbuf) riga::pinned_put(hbuf);
@@ -1259,6 +1266,7 @@ int riga_lanczos_reset(riga_lanczos* lz, riga_system* mass) {
   RIGA_CHECK_ARG(!mass || mass->n == lz->n, "mass dimension mismatch");
   DeviceGuard g(lz->ctx->device);
   lz->sys = mass;
+  lz->run = nullptr;
   if (mass && mass->kdim && !getenv("RIGA_CSR_MASS")) {
     if (!lz->kt1.p) {
       RIGA_TRY(lz->kt1.alloc(lz->n, lz->ctx->stream));
@@ -1376,9 +1384,23 @@ int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_
     RIGA_CUDA(cudaEventCreate(&lz->ev0));
     RIGA_CUDA(cudaEventCreate(&lz->ev1));
   }
-  RIGA_CUDA(cudaEventRecord(lz->ev0, s));
-  for (int64_t i = lz->k; i < limit; ++i) RIGA_CUDA(cudaGraphLaunch(lz->gexec, s));
-  RIGA_CUDA(cudaEventRecord(lz->ev1, s));
+  cudaStream_t rs = s;
+  if (lz->run && lz->run != s) {  // fork onto the run stream
+    if (!lz->evf) {
+      RIGA_CUDA(cudaEventCreateWithFlags(&lz->evf, cudaEventDisableTiming));
+      RIGA_CUDA(cudaEventCreateWithFlags(&lz->evj, cudaEventDisableTiming));
+    }
+    RIGA_CUDA(cudaEventRecord(lz->evf, s));
+    RIGA_CUDA(cudaStreamWaitEvent(lz->run, lz->evf, 0));
+    rs = lz->run;
+  }
+  RIGA_CUDA(cudaEventRecord(lz->ev0, rs));
+  for (int64_t i = lz->k; i < limit; ++i) RIGA_CUDA(cudaGraphLaunch(lz->gexec, rs));
+  RIGA_CUDA(cudaEventRecord(lz->ev1, rs));
+  if (rs != s) {  // join: everything after the extend stays ordered on the context stream
+    RIGA_CUDA(cudaEventRecord(lz->evj, rs));
+    RIGA_CUDA(cudaStreamWaitEvent(s, lz->evj, 0));
+  }
   lz->ev_valid = true;
   count_launch((int)((limit - lz->k) * lz->gnodes));
   const int64_t rows = lz->max_dim + 1;
@@ -1407,6 +1429,12 @@ int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_
   *steps = ns;
   lz->k = lz->hst->k;
   return lz->hst->stop == 1 ? RIGA_BREAKDOWN : RIGA_OK;
+}
+
+int riga_lanczos_set_run_stream(riga_lanczos* lz, void* stream) {
+  RIGA_CHECK_ARG(lz, "null arg");
+  lz->run = (cudaStream_t)stream;
+  return RIGA_OK;
 }
 
 int riga_lanczos_last_extend_ms(riga_lanczos* lz, float* ms) {
