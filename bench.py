@@ -381,6 +381,12 @@ def concurrent_rates(P, D, L, system, shifts, sym, streams, m, reps=6):
 
     n = system.dof_count
     S = len(shifts) - 1
+    # as many concurrent (factor, basis) pairs as fit, like the slice driver's memory plan
+    st_ = sym.stats
+    per = 8.0 * (1.35 * st_.get("panel_entries", 0) + 6 * n) + 16.0 * (m + 2) * n * 2
+    torch.cuda.empty_cache()
+    free_b, _ = torch.cuda.mem_get_info()
+    streams = max(1, min(streams, int(0.7 * free_b // max(per, 1.0))))
     ctxs = [D.Context() for _ in range(streams)]
     facts, states, vecs = [], [], []
     for i, ctx in enumerate(ctxs):
@@ -625,7 +631,7 @@ def ours(args):
              "dcgs_sweeps": conc["dcgs_sweeps"]["per_launch_ms"] * rows_avg / max(conc["dcgs_sweeps"]["rows"], 1)}
     for k_ in ("dcgs_sweeps", "supernodal_solve"):
         cats[k_]["concurrent"] = {"achieved": conc[k_]["achieved"], "frac": conc[k_]["achieved"] / hbm,
-                                  "unit": "GB/s", "streams": args.streams,
+                                  "unit": "GB/s", "streams": conc["streams"],
                                   "per_launch_ms_aggregate": conc[k_]["per_launch_ms"]}
         cats[k_]["step_ms_aggregate"] = share[k_]
     # dominant = largest aggregate device time per Lanczos step in the

@@ -74,6 +74,16 @@ __device__ __forceinline__ const double* sel_row(const RowSel& A, int64_t na, in
 // warp finishing the last chunk of a row (per-row ticket) reduces that row's
 // partials in fixed order into coef: no block barriers, no reduce launch.
 constexpr int kDotGrid = 2 * 148;
+// CTAs of the delayed-CGS2 dots sweep (grid-stride over the row tiles):
+// RIGA_DOT_CTAS overrides 2 x 148 (two 125-register CTAs fill an SM's registers)
+static int dcgs_dot_grid() {
+  static const int g = [] {
+    const char* e = getenv("RIGA_DOT_CTAS");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : kDotGrid;
+  }();
+  return g;
+}
 __global__ void __launch_bounds__(256, 2) k_cgs_dots(RowSel A, const LzDev* st, int64_t n, int64_t Rmax,
                                                      const double* __restrict__ x, double* __restrict__ partial,
                                                      double* __restrict__ coef, unsigned* __restrict__ tickets) {
@@ -1111,7 +1121,7 @@ int step_full(riga_lanczos* lz) {
   double* ob = lz->outs.p + (lz->max_dim + 1);
   {
     ProfScope prof(kProfCgs, s, 2.0 * (double)(lz->k + 1 + lz->nlocked) * lz->n * 8.0);
-    RIGA_CUDA(launch(k_dcgs_dots, kDotGrid, 256, 0, s, sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, lz->w.p,
+    RIGA_CUDA(launch(k_dcgs_dots, dcgs_dot_grid(), 256, 0, s, sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, lz->w.p,
                                          lz->partial.p, lz->coef.p, lz->tk_dots.p));
     const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
     RIGA_CUDA(launch(k_dcgs_upd, gu, 256, 0, s, sel_basis(lz, false, 1), lz->st.p, lz->n, lz->ld, Rmax, lz->coef.p,
@@ -1702,7 +1712,7 @@ int riga_lanczos_dcgs_probe(riga_lanczos* lz, const double* w, int64_t* rows) {
   RIGA_TRY(push_state(lz, lz->k, lz->k, 0.0));  // steps = 0: no beta correction
   const int64_t Rmax = lz->max_dim + 1 + lz->cap;
   if (rows) *rows = lz->k + 1 + lz->nlocked;
-  RIGA_CUDA(launch(k_dcgs_dots, kDotGrid, 256, 0, s, sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, w,
+  RIGA_CUDA(launch(k_dcgs_dots, dcgs_dot_grid(), 256, 0, s, sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, w,
                    lz->partial.p, lz->coef.p, lz->tk_dots.p));
   const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
   RIGA_CUDA(launch(k_dcgs_upd, gu, 256, 0, s, sel_basis(lz, false, 1), lz->st.p, lz->n, lz->ld, Rmax, lz->coef.p,
