@@ -114,11 +114,15 @@ def cpu_sample_tasks(cfgname, q):
     return tasks
 
 
-def run_cpu_sample(cfgname, q, steps=1, warmup=0):
+def run_cpu_sample(cfgname, q, steps=1, warmup=0, proc_bytes=0.0):
     import multiprocessing as mp
 
     tasks = cpu_sample_tasks(cfgname, q)
     workers = min(os.cpu_count() or 1, len(tasks))
+    if proc_bytes > 0:  # host memory: each process holds the pencil and one factor
+        import psutil
+
+        workers = max(1, min(workers, int(0.6 * psutil.virtual_memory().available // proc_bytes)))
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     os.environ["OMP_NUM_THREADS"] = "1"
     ctxmp = mp.get_context("spawn")
@@ -662,7 +666,9 @@ def ours(args):
             "timing": {"per_step_s": times, "boundary_s": r.timings["boundary_s"],
                        "slices_s": r.timings["slices_s"], "streams_used": r.timings.get("streams_used")}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        pairs, ctimes, workers = run_cpu_sample(args.config, args.sample_q, steps=1)
+        # oracle process footprint: L (value + index) with working copies, plus the CSR pencil
+        pb = 3.0 * 12.0 * sym.stats["fill_nnz"] + 40.0 * system.K.nnz
+        pairs, ctimes, workers = run_cpu_sample(args.config, args.sample_q, steps=1, proc_bytes=pb)
         line["cpu_baseline"] = {"value": pairs / ctimes[0], "unit": "eigenpairs/s", "cores": workers,
                                 "kind": "port",
                                 "sample": f"{c.name}: the {args.sample_q} lowest eigenpairs above each uniform "

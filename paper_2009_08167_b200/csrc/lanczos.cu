@@ -61,7 +61,10 @@ constexpr int kDotCols = 1024;
 constexpr int kDotColsD = RIGA_DOT_COLS;
 constexpr int kUpdGroups = 8;
 constexpr int kUpdCols = 512;   // columns per update CTA (2 per thread)
-constexpr int kUpdUnroll = 8;   // row loads in flight per thread
+#ifndef RIGA_UPD_UNROLL
+#define RIGA_UPD_UNROLL 8
+#endif
+constexpr int kUpdUnroll = RIGA_UPD_UNROLL;  // row loads in flight per thread
 
 __device__ __forceinline__ const double* sel_row(const RowSel& A, int64_t na, int64_t i) {
   return i < na ? A.V + i * A.ld : A.L + (i - na) * A.ld;

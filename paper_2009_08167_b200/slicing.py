@@ -150,11 +150,14 @@ class _DynPriority:
     stream, the rest on a low-priority one.  A slice that converges slowly (more restarts than its peers)
     moves up instead of becoming a tail that runs alone at low concurrency."""
 
-    def __init__(self):
+    def __init__(self, always_low: bool = False):
         self.lock = threading.Lock()
         self.rem = {}
+        self.always_low = always_low
 
     def pick(self, key, remaining: int, solves: int, found: int) -> bool:
+        if self.always_low:
+            return False
         per_pair = solves / found if found > 0 else 6.0
         r = max(remaining, 0) * per_pair
         with self.lock:
@@ -349,8 +352,11 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     # shared queue (largest first) on default-priority streams
     prio = _priorities([int(expected[k]) for k in order]) if one_per_thread else [0] * len(order)
     dyn = None
-    if one_per_thread and nthreads > 1 and os.environ.get("RIGA_DYN_PRIO", "0") == "1":
-        dyn = _DynPriority()  # extends move between priorities; the slice streams themselves run high
+    dyn_mode = os.environ.get("RIGA_DYN_PRIO", "0")
+    if one_per_thread and nthreads > 1 and dyn_mode in ("1", "2"):
+        # extends replay on side streams; the slice streams themselves (locking, lifts, restarts) run high.
+        # mode 1: extends high or low by remaining work; mode 2: extends always low
+        dyn = _DynPriority(always_low=dyn_mode == "2")
         least, _ = torch.cuda.Stream.priority_range()
         prio = [least - 1] * len(order)
 
