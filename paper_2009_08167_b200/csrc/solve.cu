@@ -567,30 +567,46 @@ __device__ __forceinline__ void warp_gtile_bwd(const SymDev& S, const GDev& GD, 
 // level, and each CTA's chain of small mat-vecs overlaps the others'.
 // sub_ptr[i * (SL + 1) + j]: first task of local level j of subtree i.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSolveThreads, 4) k_sub_fwd(SymDev S, SolveDev T, GDev GD,
-                                                              const int32_t* __restrict__ sub_ptr, int SL,
-                                                              const double* __restrict__ b, double* xp, double* upd) {
+// NT threads per subtree CTA (RIGA_SUB_THREADS: 256, 512 or 1024): the warps
+// of a CTA stride over a local level's tiles, so a wider CTA keeps more of a
+// subtree's loads in flight
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_sub_fwd(SymDev S, SolveDev T, GDev GD,
+                                                           const int32_t* __restrict__ sub_ptr, int SL,
+                                                           const double* __restrict__ b, double* xp, double* upd) {
+  constexpr int NW = NT / 32;
   pdl_start();
-  __shared__ double y[kSolveWarps * kGMaxNp];
+  __shared__ double y[NW * kGMaxNp];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
   for (int j = 0; j < SL; ++j) {
-    for (int t = p[j] + w; t < p[j + 1]; t += kSolveWarps)
+    for (int t = p[j] + w; t < p[j + 1]; t += NW)
       warp_gtile_fwd(S, T, GD, GD.tiles[t], b, xp, upd, y + w * kGMaxNp, lane);
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 4) k_sub_bwd(SymDev S, GDev GD, const int32_t* __restrict__ sub_ptr,
-                                                              int SL, const double* __restrict__ D, double* xp,
-                                                              double* x) {
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_sub_bwd(SymDev S, GDev GD, const int32_t* __restrict__ sub_ptr,
+                                                           int SL, const double* __restrict__ D, double* xp,
+                                                           double* x) {
+  constexpr int NW = NT / 32;
   pdl_start();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
   for (int j = SL - 1; j >= 0; --j) {
-    for (int t = p[j] + w; t < p[j + 1]; t += kSolveWarps) warp_gtile_bwd(S, GD, GD.tiles[t], D, xp, x, lane);
+    for (int t = p[j] + w; t < p[j + 1]; t += NW) warp_gtile_bwd(S, GD, GD.tiles[t], D, xp, x, lane);
     __syncthreads();
   }
+}
+
+static int sub_threads() {
+  static const int v = [] {
+    const char* e = getenv("RIGA_SUB_THREADS");
+    const int t = e ? atoi(e) : 256;
+    return t >= 1024 ? 1024 : t >= 512 ? 512 : 256;
+  }();
+  return v;
 }
 
 // ---------------------------------------------------------------------------
@@ -2050,7 +2066,9 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   if (L.nsub && gon) {
     const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_ftiles.p), 1, F->D.p,
                   nullptr, F->cvec.p};
-    RIGA_CUDA(launch(k_sub_fwd, (unsigned)L.nsub, kSolveThreads, 0, st, S, T, Gs, sym->d_sub_fptr.p, L.sub_levels, b, F->xperm.p,
+    const int nt = sub_threads();
+    RIGA_CUDA(launch(nt == 1024 ? k_sub_fwd<1024> : nt == 512 ? k_sub_fwd<512> : k_sub_fwd<256>, (unsigned)L.nsub, nt, 0,
+                     st, S, T, Gs, sym->d_sub_fptr.p, L.sub_levels, b, F->xperm.p,
                                                           F->upd.p));
     count_launch();
   }
@@ -2101,7 +2119,9 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   if (L.nsub && gon) {
     const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_btiles.p), 1, F->D.p,
                   nullptr, F->cvec.p};
-    RIGA_CUDA(launch(k_sub_bwd, (unsigned)L.nsub, kSolveThreads, 0, st, S, Gs, sym->d_sub_bptr.p, L.sub_levels, F->D.p,
+    const int nt = sub_threads();
+    RIGA_CUDA(launch(nt == 1024 ? k_sub_bwd<1024> : nt == 512 ? k_sub_bwd<512> : k_sub_bwd<256>, (unsigned)L.nsub, nt, 0,
+                     st, S, Gs, sym->d_sub_bptr.p, L.sub_levels, F->D.p,
                                                           F->xperm.p, x));
     count_launch();
   }

@@ -12,7 +12,9 @@ s = P.build_system(c.d, c.ne, c.p, c.level)
 lam_e, cnt = P.choose_lambda_e(s, c.n0)
 sh = P.uniform_shifts(lam_e, c.slices)
 perm = P.separator_ordering(s)
-sym = Symbolic.on_device(s.device, perm)
+from paper_2009_08167_b200.slicing import solve_plan, solve_sub_levels  # noqa: E402
+with solve_plan(solve_sub_levels(min(streams, c.slices))):  # the plan the slice driver builds
+    sym = Symbolic.on_device(s.device, perm)
 import gc
 if os.environ.get('NOGC'):
     gc.disable()
