@@ -61,6 +61,10 @@ int riga_mem_info(int device, int reset_high, int64_t* out4);
 int riga_ctx_create(int device, void* stream_handle, riga_ctx** out);
 int riga_ctx_destroy(riga_ctx* ctx);
 int riga_ctx_synchronize(riga_ctx* ctx);
+/* Bytes the device's default stream-ordered pool holds but no allocation
+ * uses (freed engine buffers and torch tensors kept for reuse): memory
+ * planners count them as available.                                       */
+int riga_device_pool_reusable(int device, int64_t* bytes);
 /* Raw cudaStream_t of the context (for torch.cuda.ExternalStream). */
 int riga_ctx_stream(riga_ctx* ctx, void** stream_out);
 

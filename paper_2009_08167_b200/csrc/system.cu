@@ -475,6 +475,19 @@ int riga_ctx_synchronize(riga_ctx* ctx) {
   return RIGA_OK;
 }
 
+int riga_device_pool_reusable(int device, int64_t* bytes) {
+  RIGA_CHECK_ARG(bytes, "null arg");
+  *bytes = 0;
+  DeviceGuard g(device);
+  cudaMemPool_t pool;
+  RIGA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t reserved = 0, used = 0;
+  RIGA_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  RIGA_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  *bytes = reserved > used ? (int64_t)(reserved - used) : 0;
+  return RIGA_OK;
+}
+
 int riga_ctx_stream(riga_ctx* ctx, void** stream_out) {
   RIGA_CHECK_ARG(ctx && stream_out, "null arg");
   *stream_out = (void*)ctx->stream;

@@ -258,6 +258,16 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     fac_bytes = 8.0 * (1.35 * st_.get("panel_entries", 0) + 6 * n)
     cb_bytes = 8.0 * st_.get("cb_entries", 0)
     free_b, total_b = torch.cuda.mem_get_info(base_ctx.device)
+    # memory the stream-ordered pool keeps for reuse (freed buffers of earlier calls) and idle pooled Lanczos
+    # states (reused by the slice streams) is available to this call too
+    import ctypes
+
+    from . import _lib as _L0
+    from . import eigensolver as _E0
+
+    reuse = ctypes.c_int64(0)
+    _L0.check(_L0.lib().riga_device_pool_reusable(base_ctx.device, ctypes.byref(reuse)), "pool")
+    free_b += reuse.value + _E0.pooled_state_bytes(base_ctx.device)
     budget = 0.85 * free_b
     keep_factors = (S + 1) * fac_bytes <= 0.35 * budget
 
@@ -271,7 +281,10 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     # independent factorizations on several streams at once (a small front
     # tree leaves most of the GPU idle); concurrency capped by the transient
     # update-block memory each one needs
-    nbw = int(max(1, min(8, len(mine_b), (0.5 * budget) // max(fac_bytes + cb_bytes, 1.0))))
+    import os
+
+    nbw_cap = int(os.environ.get("RIGA_BOUNDARY_STREAMS", "8"))
+    nbw = int(max(1, min(nbw_cap, len(mine_b), (0.5 * budget) // max(fac_bytes + cb_bytes, 1.0))))
     bq = list(mine_b)
     blk = threading.Lock()
     berr = []

@@ -134,6 +134,39 @@ def test_symbolic_colcounts_equal_oracle():
     np.testing.assert_array_equal(sym.colcounts(), lnz + 1)
 
 
+def test_symbolic_parallel_sweeps_match_one_thread():
+    """The host analysis's threaded sweeps (column counts, front structures, scatter map) give the same
+    supernodes, structures and counts as one thread (RIGA_SYM_THREADS=1 in a child process)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from oracle import rigaeig_port as O
+
+    code = r"""
+import json, sys
+sys.path.insert(0, %r)
+import numpy as np
+import paper_2009_08167_b200 as P
+from oracle import rigaeig_port as O
+s = O.build_system(2, 64, 3, 2)
+perm = O.separator_ordering(s)
+sym = P.sparsela.Symbolic.host_only(s.K, perm)
+sn = sym.supernodes()
+print(json.dumps({"stats": {k: int(v) for k, v in sym.stats.items()}, "order": sym.order.tolist(),
+                  "cc": sym.colcounts().tolist(), "sn": {k: v.tolist() for k, v in sn.items()}}))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for threads in ("1", "8"):
+        env = dict(os.environ, RIGA_SYM_THREADS=threads)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert len(outs[0]["order"]) >= 4096  # large enough for the threaded paths
+    assert outs[0] == outs[1]
+
+
 def test_lpt_assignment():
     counts = [115, 125, 123, 125, 124, 126, 123, 126, 130, 127, 121, 128, 125, 125, 129, 128]
     for world in (1, 2, 4, 8):
