@@ -65,6 +65,10 @@ int riga_ctx_synchronize(riga_ctx* ctx);
  * uses (freed engine buffers and torch tensors kept for reuse): memory
  * planners count them as available.                                       */
 int riga_device_pool_reusable(int device, int64_t* bytes);
+/* Host threads waiting on the device block (on = 1) instead of spinning
+ * (cudaDeviceScheduleBlockingSync on the device's primary context): with a
+ * host thread per slice, spinning waiters compete for the host cores.      */
+int riga_set_blocking_sync(int device, int on);
 /* Raw cudaStream_t of the context (for torch.cuda.ExternalStream). */
 int riga_ctx_stream(riga_ctx* ctx, void** stream_out);
 

@@ -34,6 +34,7 @@ SIGNATURES = {
     "riga_ctx_destroy": [_p],
     "riga_ctx_synchronize": [_p],
     "riga_device_pool_reusable": [ctypes.c_int, _p],
+    "riga_set_blocking_sync": [ctypes.c_int, ctypes.c_int],
     "riga_ctx_stream": [_p, _p],
     "riga_system_upload": [_p, _i64, _i64, _p, _p, _p, _p, _p],
     "riga_system_assemble_kron": [_p, _i32, _p, _p, _p, _p, _p, _p],

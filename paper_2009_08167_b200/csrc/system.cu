@@ -475,6 +475,20 @@ int riga_ctx_synchronize(riga_ctx* ctx) {
   return RIGA_OK;
 }
 
+int riga_set_blocking_sync(int device, int on) {
+  DeviceGuard g(device);
+  unsigned flags = 0;
+  RIGA_CUDA(cudaGetDeviceFlags(&flags));
+  flags = (flags & ~(unsigned)cudaDeviceScheduleMask) | (on ? cudaDeviceScheduleBlockingSync : cudaDeviceScheduleAuto);
+  const cudaError_t e = cudaSetDeviceFlags(flags & ~(unsigned)cudaDeviceMapHost);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(std::string("cudaSetDeviceFlags: ") + cudaGetErrorString(e));
+    return RIGA_CUDA_ERROR;
+  }
+  return RIGA_OK;
+}
+
 int riga_device_pool_reusable(int device, int64_t* bytes) {
   RIGA_CHECK_ARG(bytes, "null arg");
   *bytes = 0;

@@ -171,6 +171,21 @@ class _DynPriority:
             self.rem.pop(key, None)
 
 
+_sync_mode_set: set = set()
+
+
+def _blocking_sync(device: int) -> None:
+    """Device waits of the slice threads block instead of spinning (RIGA_BLOCKING_SYNC=1); once per device."""
+    import os
+
+    if device in _sync_mode_set or os.environ.get("RIGA_BLOCKING_SYNC", "0") != "1":
+        return
+    from . import _lib as _L
+
+    _sync_mode_set.add(device)
+    _L.lib().riga_set_blocking_sync(device, 1)  # best effort: an active context may refuse the change
+
+
 class _blas_threads:
     """Limit the BLAS/OpenMP pools for the duration of a block (None: no-op)."""
 
@@ -236,6 +251,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     seeds = list(range(S)) if seeds is None else list(seeds)
     counters = CostCounters()
     base_ctx = _dev.current()
+    _blocking_sync(base_ctx.device)
     if perm is None:
         perm = separator_ordering(system)
     if pencil_symbolic is None:
