@@ -95,6 +95,7 @@ struct SolvePlanHost {
   std::vector<int32_t> chains;     // large supernodes grouped by level
   std::vector<int32_t> wholes;     // small supernodes (warp tasks) grouped by level
   int sub_levels = 0, nsub = 0;        // bottom subtrees: height bound, count
+  int sub_maxsn = 0;                   // most supernodes in one bottom subtree
   std::vector<int32_t> sub_fptr, sub_bptr;  // per subtree (sub_levels + 1) local-level task bounds
   std::vector<I2> sub_ftiles, sub_btiles;   // their G warp tasks (row tiles / column groups)
   std::vector<int64_t> fwd_ptr, bwd_ptr, chain_ptr;

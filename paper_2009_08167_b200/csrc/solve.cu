@@ -600,6 +600,109 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_sub_bwd(SymDev S, GDev GD, co
   }
 }
 
+// Dataflow variant (RIGA_SUB_DATAFLOW=1): no barrier between local levels.
+// Warps claim the subtree's tiles in level order from a shared counter; a
+// tile waits (shared-memory spin) only until its own dependencies are done:
+// forward, every tile of each child supernode; backward, every tile of the
+// parent.  Per-supernode remaining-tile counters live in shared memory
+// (subtree supernodes are a contiguous postorder range [base, base + nsn)).
+// The arithmetic of each tile is the level-synchronous kernel's, so the
+// results are bit-identical.
+constexpr int kSubMaxSn = 2048;
+
+__device__ __forceinline__ void sub_wait_zero(const volatile int* c) {
+  while (*c != 0) __nanosleep(32);
+  __threadfence_block();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_sub_fwd_df(SymDev S, SolveDev T, GDev GD,
+                                                              const int32_t* __restrict__ sub_ptr, int SL,
+                                                              const double* __restrict__ b, double* xp, double* upd) {
+  constexpr int NW = NT / 32;
+  pdl_start();
+  __shared__ double y[NW * kGMaxNp];
+  __shared__ int cnt[kSubMaxSn];
+  __shared__ int next;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
+  const int t0 = p[0], t1 = p[SL];
+  if (t1 <= t0) return;
+  const int base = GD.tiles[t0].x;                // first postorder supernode: a leaf
+  const int nsn = GD.tiles[t1 - 1].x - base + 1;  // the subtree root is the last tile's supernode
+  for (int i = threadIdx.x; i < nsn; i += NT) cnt[i] = (int)((S.front[base + i] + 31) / 32);
+  if (threadIdx.x == 0) next = t0;
+  __syncthreads();
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&next, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= t1) break;
+    const int2 task = GD.tiles[t];
+    const int s = task.x;
+    for (int64_t q = S.child_ptr[s] + lane; q < S.child_ptr[s + 1]; q += 32)
+      sub_wait_zero(cnt + (S.child_list[q] - base));
+    __syncwarp();
+    __threadfence_block();
+    warp_gtile_fwd(S, T, GD, task, b, xp, upd, y + w * kGMaxNp, lane);
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) atomicSub(cnt + (s - base), 1);
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_sub_bwd_df(SymDev S, GDev GD, const int32_t* __restrict__ sub_ptr,
+                                                              int SL, const double* __restrict__ D, double* xp,
+                                                              double* x) {
+  pdl_start();
+  __shared__ int cnt[kSubMaxSn];
+  __shared__ int next;
+  const int lane = threadIdx.x & 31;
+  const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
+  const int t0 = p[0], t1 = p[SL];
+  if (t1 <= t0) return;
+  // tiles are stored level by level upwards: claim them from the top level down
+  int base = 0x7fffffff, root = -1;
+  for (int t = p[0] + lane; t < p[1]; t += 32) base = min(base, GD.tiles[t].x);
+  for (int o = 16; o >= 1; o >>= 1) base = min(base, __shfl_xor_sync(0xffffffffu, base, o));
+  root = GD.tiles[t1 - 1].x;
+  const int nsn = root - base + 1;
+  for (int i = threadIdx.x; i < nsn; i += NT) cnt[i] = (int)((S.ncol[base + i] + 7) / 8);
+  if (threadIdx.x == 0) next = 0;
+  __syncthreads();
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&next, 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= t1 - t0) break;
+    // c-th claim: local levels from the top, each level's tiles in stored order
+    int j = SL - 1, off = c;
+    while (off >= p[j + 1] - p[j]) {
+      off -= p[j + 1] - p[j];
+      --j;
+    }
+    const int2 task = GD.tiles[p[j] + off];
+    const int s = task.x;
+    const int par = S.sparent[s];
+    if (par >= base && par <= root) sub_wait_zero(cnt + (par - base));
+    __syncwarp();
+    __threadfence_block();
+    warp_gtile_bwd(S, GD, task, D, xp, x, lane);
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) atomicSub(cnt + (s - base), 1);
+  }
+}
+
+static int sub_dataflow() {
+  static const int v = [] {
+    const char* e = getenv("RIGA_SUB_DATAFLOW");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 static int sub_threads() {
   static const int v = [] {
     const char* e = getenv("RIGA_SUB_THREADS");
@@ -1566,6 +1669,7 @@ int build_solve_plan(riga_symbolic* sym) {
       }
       L.sub_fptr.push_back((int32_t)L.sub_ftiles.size());
       L.sub_bptr.push_back((int32_t)L.sub_btiles.size());
+      L.sub_maxsn = std::max(L.sub_maxsn, size[s]);
       ++L.nsub;
     }
   }
@@ -2067,7 +2171,10 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_ftiles.p), 1, F->D.p,
                   nullptr, F->cvec.p};
     const int nt = sub_threads();
-    RIGA_CUDA(launch(nt == 1024 ? k_sub_fwd<1024> : nt == 512 ? k_sub_fwd<512> : k_sub_fwd<256>, (unsigned)L.nsub, nt, 0,
+    const bool df = sub_dataflow() && L.sub_maxsn <= kSubMaxSn;
+    RIGA_CUDA(launch(df ? (nt == 1024 ? k_sub_fwd_df<1024> : nt == 512 ? k_sub_fwd_df<512> : k_sub_fwd_df<256>)
+                        : (nt == 1024 ? k_sub_fwd<1024> : nt == 512 ? k_sub_fwd<512> : k_sub_fwd<256>),
+                     (unsigned)L.nsub, nt, 0,
                      st, S, T, Gs, sym->d_sub_fptr.p, L.sub_levels, b, F->xperm.p,
                                                           F->upd.p));
     count_launch();
@@ -2120,7 +2227,10 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_btiles.p), 1, F->D.p,
                   nullptr, F->cvec.p};
     const int nt = sub_threads();
-    RIGA_CUDA(launch(nt == 1024 ? k_sub_bwd<1024> : nt == 512 ? k_sub_bwd<512> : k_sub_bwd<256>, (unsigned)L.nsub, nt, 0,
+    const bool df = sub_dataflow() && L.sub_maxsn <= kSubMaxSn;
+    RIGA_CUDA(launch(df ? (nt == 1024 ? k_sub_bwd_df<1024> : nt == 512 ? k_sub_bwd_df<512> : k_sub_bwd_df<256>)
+                        : (nt == 1024 ? k_sub_bwd<1024> : nt == 512 ? k_sub_bwd<512> : k_sub_bwd<256>),
+                     (unsigned)L.nsub, nt, 0,
                      st, S, Gs, sym->d_sub_bptr.p, L.sub_levels, F->D.p,
                                                           F->xperm.p, x));
     count_launch();

@@ -275,3 +275,23 @@ def test_cfg5_inertia_matches_kronecker_counts(golden):
         x = f.solve_device(b)
         _lib.check(_lib.lib().riga_spmv(s.device.handle, 2, f.sigma, _lib.ptr(x), _lib.ptr(r)))
         assert float(torch.linalg.norm(r - b) / torch.linalg.norm(b)) < 1e-8
+
+
+@pytest.mark.gpu
+def test_dataflow_subtree_solve_is_bit_identical(tmp_path):
+    """Opt-in dataflow subtree kernels (RIGA_SUB_DATAFLOW=1: per-supernode dependency counters in shared memory
+    instead of a barrier per local level) give bit-identical solves to the level-synchronous kernels."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for df in ("0", "1"):
+        path = str(tmp_path / f"x{df}.npy")
+        env = dict(os.environ, RIGA_SUB_DATAFLOW=df)
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "sub_df_check.py"), "cfg4", path, "6"],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
