@@ -101,8 +101,9 @@ __global__ void k_kron_values(int dim, Kron1D x, Kron1D y, Kron1D z, int64_t n,
 // ---------------------------------------------------------------------------
 // CSR SpMV, LANES threads per row, fixed reduction order (deterministic).
 // mode 0: y = A x;  mode 1: y = (K - sigma M) x with A = K, B = M.
+// U elements per lane per round: chosen so one round covers a typical row.
 // ---------------------------------------------------------------------------
-template <int LANES, int MODE>
+template <int LANES, int U, int MODE>
 __global__ void __launch_bounds__(256) k_spmv(int64_t n, const int64_t* __restrict__ rp,
                                               const int32_t* __restrict__ ci,
                                               const double* __restrict__ A,
@@ -115,9 +116,8 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t n, const int64_t* __restri
   if (row >= n) return;
   int64_t b = rp[row], e = rp[row + 1];
   double acc = 0.0;
-  // 4 elements per lane per round: all value / index loads issued before the
+  // U elements per lane per round: all value / index loads issued before the
   // dependent x gathers (one round trip each instead of one per element)
-  constexpr int U = 4;
   for (int64_t q0 = b + sub; q0 < e; q0 += U * LANES) {
     double a[U];
     int32_t c[U];
@@ -146,24 +146,42 @@ int csr_spmv_impl(cudaStream_t s, int64_t n, const int64_t* rp, const int32_t* c
   if (n == 0) return RIGA_OK;
   ProfScope prof(kProfSpmv, s, 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n);
   double avg = double(nnz) / double(n);
-  // about 4 elements per lane (one unrolled round) for the stencil rows of these pencils
-  int lanes = avg >= 96 ? 32 : (avg >= 40 ? 16 : (avg >= 16 ? 8 : 4));
+  // 16 lanes per row for the stencil rows of these pencils (avg 70-285 nnz);
+  // U is the smallest of 4/6/8 whose one unrolled round covers a row 10 % above
+  // the average, else 8.  Swept on cfg3/4/5 (tools/spmv_sweep.sh): 32 lanes or
+  // 4-element rounds lose 5-30 % on the 3D pencils.
+  int lanes = avg >= 40 ? 16 : (avg >= 16 ? 8 : 4);
   if (const char* e = getenv("RIGA_SPMV_LANES")) lanes = atoi(e);
+  int per = (int)ceil(1.1 * avg / lanes);
+  int U = per <= 4 ? 4 : (per <= 6 ? 6 : 8);
+  if (const char* e = getenv("RIGA_SPMV_U")) U = atoi(e);
   int64_t threads = n * lanes;
   int blocks = (int)((threads + 255) / 256);
+#define RIGA_SPMV_LAUNCH(L, UU)                                                            \
+  if (mode == 0)                                                                           \
+    k_spmv<L, UU, 0><<<blocks, 256, 0, s>>>(n, rp, ci, A, B, sigma, x, y);                 \
+  else                                                                                     \
+    k_spmv<L, UU, 1><<<blocks, 256, 0, s>>>(n, rp, ci, A, B, sigma, x, y);
 #define RIGA_SPMV_CASE(L)                                                                  \
   case L:                                                                                  \
-    if (mode == 0)                                                                         \
-      k_spmv<L, 0><<<blocks, 256, 0, s>>>(n, rp, ci, A, B, sigma, x, y);                   \
-    else                                                                                   \
-      k_spmv<L, 1><<<blocks, 256, 0, s>>>(n, rp, ci, A, B, sigma, x, y);                   \
+    if (U == 8) {                                                                          \
+      RIGA_SPMV_LAUNCH(L, 8)                                                               \
+    } else if (U == 6) {                                                                   \
+      RIGA_SPMV_LAUNCH(L, 6)                                                               \
+    } else {                                                                               \
+      RIGA_SPMV_LAUNCH(L, 4)                                                               \
+    }                                                                                      \
     break;
   switch (lanes) {
     RIGA_SPMV_CASE(4)
     RIGA_SPMV_CASE(8)
     RIGA_SPMV_CASE(16)
     RIGA_SPMV_CASE(32)
+    default:
+      set_error("spmv: RIGA_SPMV_LANES must be 4, 8, 16 or 32");
+      return RIGA_BAD_ARG;
   }
+#undef RIGA_SPMV_LAUNCH
 #undef RIGA_SPMV_CASE
   count_launch();
   RIGA_CUDA(cudaGetLastError());

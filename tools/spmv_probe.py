@@ -22,4 +22,4 @@ for _ in range(20):
     e1.record(st); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
 by = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
 ms = float(np.median(ts))
-print(c.name, os.environ.get("RIGA_SPMV_LANES", "auto"), f"{ms*1e3:.1f} us  {by/ms/1e6:.0f} GB/s")
+print(c.name, os.environ.get("RIGA_SPMV_LANES", "auto"), os.environ.get("RIGA_SPMV_U", "autoU"), f"avg {nnz/n:.1f}", f"{ms*1e3:.1f} us  {by/ms/1e6:.0f} GB/s")
