@@ -104,6 +104,10 @@ int riga_system_destroy(riga_system* sys);
 /* y = A x on the device, A = K (which=0), M (which=1) or K - sigma M (2).
  * Replaces mass_matvec (ref sparsela.py:280-290, scipy csr_matvec).        */
 int riga_spmv(riga_system* sys, int which, double sigma, const double* x_dev, double* y_dev);
+/* Y[j] = A X[j] for nvec device vectors (rows, leading dimensions ldx /
+ * ldy >= n), A as riga_spmv, on ctx's stream (NULL = the system's).       */
+int riga_spmv_many(riga_ctx* ctx, riga_system* sys, int which, double sigma, const double* X_dev, int64_t ldx,
+                   int64_t nvec, double* Y_dev, int64_t ldy);
 /* Generic device CSR SpMV on caller arrays (any square CSR, e.g. a plain
  * scipy matrix handed to mass_matvec).                                     */
 int riga_csr_spmv(riga_ctx* ctx, int64_t n, const int64_t* rowptr_dev, const int32_t* colidx_dev,
@@ -148,6 +152,12 @@ int riga_factor_create(riga_ctx* ctx, riga_symbolic* sym, double sigma, double r
 /* x = A^{-1} b, b and x device vectors in ORIGINAL numbering (may alias).
  * Replaces solve_fb + _ldl_solve (ref sparsela.py:265-277, :162-175).      */
 int riga_factor_solve(riga_factor* f, const double* b_dev, double* x_dev);
+/* Block solve X[:, j] = A^{-1} B[:, j] for nrhs device vectors stored with
+ * leading dimensions ldb / ldx (>= n), on ctx's stream (NULL = the
+ * factor's; ordered after the factor's own stream).
+ * solve(fact, x, nrhs); used by the residual-gate refinement.             */
+int riga_factor_solve_many(riga_ctx* ctx, riga_factor* f, const double* B_dev, int64_t ldb, int64_t nrhs,
+                           double* X_dev, int64_t ldx);
 /* Timing of the last numeric factorization on the device (ms). */
 int riga_factor_time_ms(riga_factor* f, float* ms);
 /* D in elimination order (host double[n]). */
@@ -288,6 +298,17 @@ int riga_set_pdl(int on);
 int riga_set_solve_sub_levels(int levels);
 int riga_prof_read(double* ms, double* work, int64_t* scopes, int ncat);
 int riga_prof_reset(void);
+
+/* ---- eigenpair residuals (north-star gate) ---------------------------------
+ * For nvec device vectors x_v (rows of X, leading dimension ldx >= n) and
+ * host eigenvalues lam[v]: out[3 v + 0] = ||K x - lam M x||^2,
+ * out[3 v + 1] = ||M x||^2, out[3 v + 2] = ||K x||^2 (host), one fused
+ * pass over the CSR of K and M per 8 vectors, fixed-order reductions.
+ * Replaces the residual loop of solve_spectrum (ref eigensolver.py:784-792)
+ * and evaluates north_star's ||Ku - lam Mu|| / (|lam| ||Mu||) for every
+ * returned pair.  ctx selects the stream (NULL = the system's).            */
+int riga_residuals(riga_ctx* ctx, riga_system* sys, const double* X_dev, int64_t ldx, int64_t nvec,
+                   const double* lam_host, double* out_host);
 
 /* ---- dense vector helpers on the device (stream of ctx) ----------------- */
 int riga_dot(riga_ctx* ctx, int64_t n, const double* x_dev, const double* y_dev, double* out_host);

@@ -45,6 +45,7 @@ SIGNATURES = {
     "riga_system_destroy": [_p],
     "riga_spmv": [_p, _i32, _d, _p, _p],
     "riga_csr_spmv": [_p, _i64, _p, _p, _p, _p, _p],
+    "riga_spmv_many": [_p, _p, _i32, _d, _p, _i64, _i64, _p, _i64],
     "riga_symbolic_create": [_p, _p, _p],
     "riga_symbolic_analyze": [_i64, _p, _p, _p, _p],
     "riga_symbolic_stats": [_p, _p],
@@ -54,6 +55,7 @@ SIGNATURES = {
     "riga_symbolic_destroy": [_p],
     "riga_factor_create": [_p, _p, _d, _d, _p, _p, _p],
     "riga_factor_solve": [_p, _p, _p],
+    "riga_factor_solve_many": [_p, _p, _p, _i64, _i64, _p, _i64],
     "riga_factor_time_ms": [_p, _p],
     "riga_factor_D": [_p, _p],
     "riga_factor_export": [_p, _p, _p, _p],
@@ -87,6 +89,7 @@ SIGNATURES = {
     "riga_lanczos_append_rows": [_p, _p, _p, _i64, _i64, _p, _p],
     "riga_lanczos_gram": [_p, _p],
     "riga_lanczos_basis": [_p, _p, _p, _p],
+    "riga_residuals": [_p, _p, _p, _i64, _i64, _p, _p],
     "riga_dot": [_p, _i64, _p, _p, _p],
     "riga_launch_count": [_p],
     "riga_set_pdl": [_i32],

@@ -33,7 +33,8 @@ import scipy.linalg
 import torch
 
 from . import device as _dev
-from .eigensolver import (CountMismatch, SolverOptions, _Boundary, _Pencil, _Pool, _solve_interval)
+from .eigensolver import (CountMismatch, SolverOptions, _Boundary, _Pencil, _Pool, _solve_interval,
+                          residual_gate)
 from .sparsela import CostCounters, Symbolic, mass_matvec, separator_ordering
 
 
@@ -87,6 +88,68 @@ class SlicesResult:
     counters: CostCounters
     timings: dict = field(default_factory=dict)
     factor_ms: list = field(default_factory=list)
+    residuals: dict = field(default_factory=dict)  # slice id -> north-star residuals of its pairs
+    max_residual: float = 0.0                       # over all ranks
+    gate_rounds: dict = field(default_factory=dict)  # slice id -> refinement rounds the gate needed
+
+
+def boundary_dedup(entries: list, scale: float):
+    """De-duplicate pairs gathered from both sides of internal slice boundaries.
+
+    ``entries``: (slice k, index j, lam, x, M x) with x M-normalised, host arrays, every rank's pairs
+    within 1e-7 max(|lam|, 1) of an internal shift.  The rules are the reference's, applied in its
+    sequential slice order (k ascending):
+
+    * ``_Pool.add`` (ref eigensolver.py:407-420): a pair is a copy of an accepted one when
+      |lam_a - lam| <= 1e-7 max(|lam|, 1) and |x_a^T M x| > 0.1; the later copy is dropped;
+    * ``_dedup_and_orthonormalize`` (ref :670-712): accepted pairs cluster when consecutive gaps are
+      <= 1e-8 max(scale, |lam|); inside a cluster a member with |G_ab| > 1 - 1e-9 is dropped, then a
+      Loewdin step G^{-1/2} X re-orthonormalises the cluster when ||G - I||_max > 1e-10.
+
+    Returns (drop: set of (k, j), updates: {(k, j): (x, M x)}).  Pure host code: every rank computes
+    the same answer from the same gathered list.
+    """
+    drop = set()
+    acc = []  # accepted entries in slice order
+    for e in sorted(entries, key=lambda t: (t[0], t[1])):
+        k, j, lam, x, mx = e
+        close = 1e-7 * max(abs(lam), 1.0)
+        if any(abs(a[2] - lam) <= close and abs(float(np.dot(a[3], mx))) > 0.1 for a in acc):
+            drop.add((k, j))
+            continue
+        acc.append(e)
+    upd = {}
+    acc.sort(key=lambda t: t[2])
+    i = 0
+    while i < len(acc):
+        t = i + 1
+        while t < len(acc) and acc[t][2] - acc[t - 1][2] <= 1e-8 * max(scale, abs(acc[t][2])):
+            t += 1
+        cl = acc[i:t]
+        if len(cl) > 1:
+            X = np.stack([c[3] for c in cl])
+            MX = np.stack([c[4] for c in cl])
+            G = X @ MX.T
+            dup = set()
+            for a in range(len(cl)):
+                if a in dup:
+                    continue
+                for b in range(a + 1, len(cl)):
+                    if abs(G[a, b]) > 1.0 - 1e-9:
+                        dup.add(b)
+            for b in sorted(dup):
+                drop.add((cl[b][0], cl[b][1]))
+            keep = [a for a in range(len(cl)) if a not in dup]
+            cl = [cl[a] for a in keep]
+            G = G[np.ix_(keep, keep)]
+            if len(cl) > 1 and np.abs(G - np.eye(len(cl))).max() > 1e-10:
+                ev, evec = np.linalg.eigh(0.5 * (G + G.T))
+                T = evec @ np.diag(np.clip(ev, 1e-30, None) ** -0.5) @ evec.T
+                Xn, MXn = T @ X[keep], T @ MX[keep]
+                for a, c in enumerate(cl):
+                    upd[(c[0], c[1])] = (Xn[a], MXn[a])
+        i = t
+    return drop, upd
 
 
 _ctx_cache: dict = {}
@@ -291,7 +354,12 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     t0 = time.perf_counter()
     mine_b = [k for k in range(S + 1) if k % world == rank]
     bnd = {}
-    scale = float(shifts[-1] - shifts[0]) if S else 1.0
+    # ZeroPivot nudges and the bisection floor use the slice width, as the reference's solve_slice
+    # (ref eigensolver.py:645 scale = hi_req - lo_req); a shared boundary takes the narrower adjacent slice
+    widths = np.diff(shifts) if S else np.ones(1)
+
+    def bscale(k):
+        return float(min(widths[max(k - 1, 0)], widths[min(k, S - 1)])) if S else 1.0
     bcnt = CostCounters()
     kept = {}
     # independent factorizations on several streams at once (a small front
@@ -316,7 +384,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                         break
                     k = bq.pop(0)
                 try:
-                    sig, fact = pen.factor(float(shifts[k]), scale)
+                    sig, fact = pen.factor(float(shifts[k]), bscale(k))
                     with blk:
                         bnd[k] = (sig, fact.n_negative, fact.device_ms)
                         if k < S and keep_factors:
@@ -353,6 +421,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     kept = {k: v for k, v in kept.items() if k in my}
 
     # --- 3. solve my slices concurrently on `streams` CUDA streams ----------
+    gate = opts.get("residual_gate", SolverOptions.residual_gate)
     results = {}
     slice_times = {}
     errors = []
@@ -422,7 +491,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                         # one refactorization at a time: its transient update
                         # blocks (cb_bytes) are budgeted once
                         with factor_lock:
-                            s2, f2 = pen.factor(lo, scale)
+                            s2, f2 = pen.factor(lo, hi - lo)
                             ctx.synchronize()
                         lob = _Boundary(s2, f2.n_negative, f2)
                         cnt.nsh += 1
@@ -439,13 +508,19 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                         m = max(2, min(m_factor * count, system.dof_count))
                         so = SolverOptions(m=m, **opts)
                         rng = np.random.default_rng(seeds[k])
-                        _solve_interval(pen, lob, hib, pool, so, rng, scale)
+                        _solve_interval(pen, lob, hib, pool, so, rng, hi - lo)
                     t_col = time.perf_counter()
                     idx = sorted((i for i, lam in enumerate(pool.lams) if lob.sigma < lam <= hib.sigma),
                                  key=lambda i: pool.lams[i])
                     lams = np.array([pool.lams[i] for i in idx])
+                    res, rounds = np.empty(0), 0
                     if idx:
                         X = torch.stack([pool.vecs[i] for i in idx])
+                        # north-star residual gate (device residuals; block refinement with this slice's
+                        # lower-shift factor for any pair above the bound)
+                        _tg = time.perf_counter()
+                        lams, X, res, _, rounds = residual_gate(system, lob.fact, lams, X, ctx, gate, counters=cnt)
+                        cnt.phase("residual_gate", time.perf_counter() - _tg)
                         if vectors_to_host:
                             # pinned staging (torch's caching host allocator)
                             # + async copy on the slice stream: a pageable
@@ -461,7 +536,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                     ctx.synchronize()
                     cnt.phase("collect", time.perf_counter() - t_col)
                     with lock:
-                        results[k] = (lams, X)
+                        results[k] = (lams, X, res, rounds)
                         slice_times[k] = (t_start - t0, time.perf_counter() - t0, cnt.nfb)
                 except Exception as e:  # surfaced after join
                     with lock:
@@ -491,38 +566,101 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
         raise RuntimeError(f"slice {k} failed on rank {rank}: {e}") from e
     t_sl = time.perf_counter() - t0
 
+    def _refill(k, drop, bnear):
+        lams_k, X_k, _, _ = results[k]
+        pen = make_pencil(base_ctx, counters)
+        lo, hi = float(sig_used[k]), float(sig_used[k + 1])
+        dev = f"cuda:{base_ctx.device}"
+        with base_ctx:
+            s2, f2 = pen.factor(lo, hi - lo)
+            counters.nsh += 1
+            lob = _Boundary(s2, int(nu[k]), f2)
+            hib = _Boundary(hi, int(nu[k + 1]), None)
+            pool = _Pool()
+            for lam, x in zip(lams_k, X_k):
+                pool.lams.append(float(lam))
+                pool.vecs.append(torch.as_tensor(np.asarray(x) if isinstance(X_k, np.ndarray) else x, device=dev))
+            for kk, j, lam, x, _mx in bnear:
+                if kk != k and (kk, j) not in drop:
+                    pool.lams.append(float(lam))
+                    pool.vecs.append(torch.as_tensor(x, device=dev))
+            so = SolverOptions(m=max(2, min(m_factor * int(expected[k]), system.dof_count)), **opts)
+            _solve_interval(pen, lob, hib, pool, so, np.random.default_rng(seeds[k] + 104729), hi - lo)
+            idx = sorted((i for i, lam in enumerate(pool.lams) if lo < lam <= hi), key=lambda i: pool.lams[i])
+            lams = np.array([pool.lams[i] for i in idx])
+            X = torch.stack([pool.vecs[i] for i in idx])
+            lams, X, res, _, rounds = residual_gate(system, f2, lams, X, base_ctx, gate, counters=counters)
+            if vectors_to_host:
+                X = X.cpu().numpy()
+        return lams, X, res, rounds
+
     # --- 4. boundary de-duplication + global eigenvalue gather --------------
-    local_eigs = {k: results[k][0] for k in my}
-    near = {}
+    # pairs within 1e-7 max(|lam|, 1) of an internal boundary travel with their M-normalised vectors
+    # (host copies; none exist at the BASELINE configs, whose shifts sit >= 1e-4 relative from the
+    # spectrum); every rank applies the reference's _Pool.add / _dedup_and_orthonormalize rules to the
+    # same gathered set and patches its own slices
+    _td = time.perf_counter()
+    near = []
     for k in my:
-        for j, lam in enumerate(results[k][0]):
-            for b in (k, k + 1):
-                if 0 < b < S and abs(lam - sig_used[b]) <= 1e-7 * max(abs(lam), 1.0):
-                    near.setdefault(b, []).append((k, j, float(lam)))
-    gathered = _allgather((local_eigs, near), world)
+        lams_k, X_k = results[k][0], results[k][1]
+        for j, lam in enumerate(lams_k):
+            if any(0 < b < S and abs(lam - sig_used[b]) <= 1e-7 * max(abs(lam), 1.0) for b in (k, k + 1)):
+                xk = X_k[j] if isinstance(X_k, np.ndarray) else X_k[j].cpu().numpy()
+                mxk = mass_matvec(system.M, xk)
+                near.append((int(k), int(j), float(lam), np.asarray(xk), np.asarray(mxk)))
+    scale_all = max([float(np.max(np.abs(results[k][0]))) for k in my if results[k][0].size] + [1.0])
+    gathered = _allgather(({k: results[k][0] for k in my}, near, scale_all), world)
+    bnear = sorted((e for _, nr, _ in gathered for e in nr), key=lambda e: (e[0], e[1]))
+    scale_all = max(g[2] for g in gathered)
+    drop, upd = boundary_dedup(bnear, scale_all)
+    for k in my:
+        lams_k, X_k, res_k, rr_k = results[k]
+        mine_upd = {j: v for (kk, j), v in upd.items() if kk == k}
+        mine_drop = sorted(j for (kk, j) in drop if kk == k)
+        if mine_upd:
+            for j, (xn, _mxn) in mine_upd.items():
+                if isinstance(X_k, np.ndarray):
+                    X_k[j] = xn
+                else:
+                    X_k[j] = torch.as_tensor(xn, device=X_k.device)
+        if mine_drop:
+            keep = np.setdiff1d(np.arange(lams_k.size), mine_drop)
+            lams_k = lams_k[keep]
+            X_k = X_k[keep] if isinstance(X_k, np.ndarray) else X_k[torch.as_tensor(keep, device=X_k.device)]
+            res_k = res_k[keep] if res_k.size else res_k
+        results[k] = (lams_k, X_k, res_k, rr_k)
+        if lams_k.size < expected[k]:
+            # a dropped copy took the place of one of this slice's own pairs: search (lo, hi] again with
+            # every known pair deflated (the reference's shared pool gives its sweeps the same window)
+            results[k] = _refill(k, drop, bnear)
+    local_eigs = {k: results[k][0] for k in my}
+    if drop:
+        local_eigs_g = _allgather(local_eigs, world)
+    else:
+        local_eigs_g = [g[0] for g in gathered]
+    t_dedup = time.perf_counter() - _td
     found = np.zeros(S, dtype=np.int64)
     all_eigs = []
-    bnear = {}
-    for le, nr in gathered:
+    for le in local_eigs_g:
         for k, v in le.items():
             found[k] = v.size
             all_eigs.append(v)
-        for b, lst in nr.items():
-            bnear.setdefault(b, []).extend(lst)
-    # duplicates can only arise from pairs of two adjacent slices sitting
-    # within 1e-7 of their shared boundary; inertia already fixes each
-    # slice's count, so a pair on both sides would show up as found > expected
     for k in range(S):
         if found[k] != expected[k]:
             raise CountMismatch(f"slice {k} expected {expected[k]} found {found[k]}",
                                 interval=(sig_used[k], sig_used[k + 1]), expected=int(expected[k]),
                                 found=int(found[k]))
+    max_res = max([float(results[k][2].max()) for k in my if results[k][2].size] + [0.0])
+    max_res = max(_allgather(max_res, world))
     eig = np.sort(np.concatenate(all_eigs)) if all_eigs else np.empty(0)
     res = SlicesResult(sig_used, nu, expected, found, eig, my, local_eigs,
                        {k: results[k][1] for k in my}, counters)
+    res.residuals = {k: results[k][2] for k in my}
+    res.max_residual = max_res
+    res.gate_rounds = {k: int(results[k][3]) for k in my}
     res.timings = {"boundary_s": t_bnd, "slices_s": t_sl, "total_s": time.perf_counter() - t_all,
-                   "streams_used": nthreads, "kept_boundary_factors": bool(keep_factors),
-                   "boundary_pairs": sum(len(v) for v in bnear.values()),
+                   "dedup_s": t_dedup, "streams_used": nthreads, "kept_boundary_factors": bool(keep_factors),
+                   "boundary_pairs": len(bnear), "boundary_duplicates": len(drop),
                    "slice_wall": {int(k): [round(a, 3), round(b, 3)] for k, (a, b, _) in slice_times.items()},
                    "slice_nfb": {int(k): int(nf) for k, (_, _, nf) in slice_times.items()}}
     res.factor_ms = [allb[k][2] for k in range(S + 1)]

@@ -391,6 +391,65 @@ def mass_matvec(M, v, counters: CostCounters | None = None):
     return out
 
 
+def _rows(X: torch.Tensor) -> torch.Tensor:
+    if X.dim() != 2 or X.stride(1) != 1:
+        X = X.contiguous()
+    return X
+
+
+def solve_many(fact: LDLFactorization, B: torch.Tensor, ctx=None, counters: CostCounters | None = None):
+    """Rows X[j] = A^{-1} B[j] of a device block (SURVEY §8b solve(fact, x, nrhs); ref solve_fb :265-277
+    applied per column), on ctx's stream."""
+    ctx = ctx or _dev.current()
+    B = _rows(B)
+    with torch.cuda.stream(ctx.stream):
+        X = torch.empty_like(B)
+    _lib.check(_lib.lib().riga_factor_solve_many(ctx.handle, fact.handle, _lib.ptr(B), B.stride(0), B.shape[0],
+                                                 _lib.ptr(X), X.stride(0)), "solve_many")
+    if counters is not None:
+        for _ in range(B.shape[0]):
+            counters.fb.add(2 * fact.fill_nnz, 0.0)
+    return X
+
+
+def spmv_many(system, which: int, X: torch.Tensor, ctx=None, counters: CostCounters | None = None):
+    """Rows Y[j] = A X[j], A = K (0) or M (1) of a device pencil (ref mass_matvec :280-290 per row)."""
+    ctx = ctx or _dev.current()
+    dsys = system.device
+    X = _rows(X)
+    with torch.cuda.stream(ctx.stream):
+        Y = torch.empty_like(X)
+    _lib.check(_lib.lib().riga_spmv_many(ctx.handle, dsys.handle, which, 0.0, _lib.ptr(X), X.stride(0), X.shape[0],
+                                         _lib.ptr(Y), Y.stride(0)), "spmv_many")
+    if counters is not None:
+        for _ in range(X.shape[0]):
+            counters.matvec.add(2 * dsys.nnz, 0.0)
+    return Y
+
+
+def pair_residuals(system, X: torch.Tensor, lams, ctx=None):
+    """Residuals of eigenpairs (rows of device block X, eigenvalues lams) on the device, one fused pass over
+    K and M per 8 pairs (riga_residuals):
+
+    * north_star: ||K x - lam M x|| / (|lam| ||M x||)
+    * reference:  ||K x - lam M x|| / ||K x||  (ref eigensolver.py:784-792)
+    """
+    ctx = ctx or _dev.current()
+    lams = np.ascontiguousarray(np.asarray(lams, dtype=np.float64))
+    c = lams.size
+    if c == 0:
+        return np.empty(0), np.empty(0)
+    X = _rows(X)
+    out = np.empty(3 * c)
+    _lib.check(_lib.lib().riga_residuals(ctx.handle, system.device.handle, _lib.ptr(X), X.stride(0), c,
+                                         _lib.ptr(lams), _lib.ptr(out)), "residuals")
+    out = out.reshape(c, 3)
+    num = np.sqrt(out[:, 0])
+    north = num / np.maximum(np.abs(lams) * np.sqrt(out[:, 1]), 1e-300)
+    ref = num / np.maximum(np.sqrt(out[:, 2]), 1e-300)
+    return north, ref
+
+
 def m_inner(u, v, M=None) -> float:
     """v^T M u (Euclidean when M is None); ref :293-297."""
     if M is None:
