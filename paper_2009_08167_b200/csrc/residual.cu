@@ -44,12 +44,15 @@ __global__ void __launch_bounds__(kResThreads) k_resid(int64_t n, const int64_t*
   double acc[NV][3];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v][0] = acc[v][1] = acc[v][2] = 0.0;
-  for (int64_t row = (int64_t)blockIdx.x * kResRows + grp; row < n; row += (int64_t)gridDim.x * kResRows) {
+  // the row-group loop bound is CTA-uniform (base), so every lane reaches the width-16 shuffles
+  for (int64_t base = (int64_t)blockIdx.x * kResRows; base < n; base += (int64_t)gridDim.x * kResRows) {
+    const int64_t row = base + grp;
+    const bool valid = row < n;
     double kx[NV], mx[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) kx[v] = mx[v] = 0.0;
-    const int64_t e = rp[row + 1];
-    for (int64_t q = rp[row] + sub; q < e; q += kResLanes) {
+    const int64_t e = valid ? rp[row + 1] : 0;
+    for (int64_t q = (valid ? rp[row] : 0) + sub; q < e; q += kResLanes) {
       const double kv = __ldg(K + q), mv = __ldg(M + q);
       const int64_t c = __ldg(ci + q);
 #pragma unroll
@@ -69,7 +72,7 @@ __global__ void __launch_bounds__(kResThreads) k_resid(int64_t n, const int64_t*
         mx[v] += __shfl_down_sync(0xffffffffu, mx[v], o, kResLanes);
       }
     }
-    if (sub == 0) {
+    if (sub == 0 && valid) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const double r = kx[v] - lv[v] * mx[v];

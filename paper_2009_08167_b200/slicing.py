@@ -513,13 +513,21 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                     idx = sorted((i for i, lam in enumerate(pool.lams) if lob.sigma < lam <= hib.sigma),
                                  key=lambda i: pool.lams[i])
                     lams = np.array([pool.lams[i] for i in idx])
-                    res, rounds = np.empty(0), 0
+                    res, rounds = np.empty(0), None
                     if idx:
                         X = torch.stack([pool.vecs[i] for i in idx])
                         # north-star residual gate (device residuals; block refinement with this slice's
-                        # lower-shift factor for any pair above the bound)
+                        # midpoint factor for any slice with a pair above the bound)
                         _tg = time.perf_counter()
-                        lams, X, res, _, rounds = residual_gate(system, lob.fact, lams, X, ctx, gate, counters=cnt)
+                        def fac_mid(sg, pen=pen, lo=lo, hi=hi):
+                            with factor_lock:  # transient update blocks budgeted once
+                                f = pen.factor(sg, hi - lo)[1]
+                                ctx.synchronize()
+                            cnt.nsh += 1
+                            return f
+
+                        lams, X, res, _, rounds = residual_gate(system, fac_mid, (lo, hi), lams, X, ctx, gate,
+                                                                counters=cnt)
                         cnt.phase("residual_gate", time.perf_counter() - _tg)
                         if vectors_to_host:
                             # pinned staging (torch's caching host allocator)
@@ -589,7 +597,8 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
             idx = sorted((i for i, lam in enumerate(pool.lams) if lo < lam <= hi), key=lambda i: pool.lams[i])
             lams = np.array([pool.lams[i] for i in idx])
             X = torch.stack([pool.vecs[i] for i in idx])
-            lams, X, res, _, rounds = residual_gate(system, f2, lams, X, base_ctx, gate, counters=counters)
+            lams, X, res, _, rounds = residual_gate(system, lambda sg: pen.factor(sg, hi - lo)[1], (lo, hi),
+                                                    lams, X, base_ctx, gate, counters=counters)
             if vectors_to_host:
                 X = X.cpu().numpy()
         return lams, X, res, rounds
@@ -657,7 +666,8 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                        {k: results[k][1] for k in my}, counters)
     res.residuals = {k: results[k][2] for k in my}
     res.max_residual = max_res
-    res.gate_rounds = {k: int(results[k][3]) for k in my}
+    res.gate_rounds = {k: (results[k][3].rounds if results[k][3] is not None else 0) for k in my}
+    res.gate_info = {k: results[k][3] for k in my}
     res.timings = {"boundary_s": t_bnd, "slices_s": t_sl, "total_s": time.perf_counter() - t_all,
                    "dedup_s": t_dedup, "streams_used": nthreads, "kept_boundary_factors": bool(keep_factors),
                    "boundary_pairs": len(bnear), "boundary_duplicates": len(drop),
