@@ -778,6 +778,45 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   return build_chain_inverse(F, st);
 }
 
+// Chain supernodes whose inverse probe (build_chain_inverse) exceeds the
+// tolerance get a local refinement step in every solve: per-supernode device
+// flags, per-level host flags (levels without one launch nothing extra).
+int flag_inverse_refinement(riga_factor* F, cudaStream_t st) {
+  riga_symbolic* sym = F->sym;
+  const SolvePlanHost& L = sym->sp;
+  const SymbolicHost& h = sym->h;
+  F->fix_level.assign(h.nlevels, 0);
+  F->n_fix = 0;
+  if (!L.inv_fix || !L.chain_inv || L.ifwd.empty() || !F->inv_err.p) return RIGA_OK;
+  static const double tol = [] {
+    const char* e = getenv("RIGA_INV_FIX_TOL");
+    return e && *e ? atof(e) : 1e-11;
+  }();
+  std::vector<unsigned long long> eb(h.nsuper);
+  RIGA_CUDA(cudaMemcpyAsync(eb.data(), F->inv_err.p, h.nsuper * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  RIGA_CUDA(stream_sync(st));
+  std::vector<int> flag(h.nsuper, 0);
+  double emax = 0.0;
+  int nchain = 0;
+  for (int64_t l = 0; l < h.nlevels; ++l)
+    for (int64_t t = L.ifwd_ptr[l]; t < L.ifwd_ptr[l + 1]; ++t) {
+      const int sn = L.ifwd[t].x;
+      if (L.ifwd[t].y == 0) ++nchain;
+      const double e = __longlong_as_double_host((long long)eb[sn]);
+      emax = std::max(emax, e);
+      if (e > tol || e != e) {
+        if (!flag[sn]) ++F->n_fix;
+        flag[sn] = 1;
+        F->fix_level[l] = 1;
+      }
+    }
+  if (getenv("RIGA_INV_FIX_DEBUG"))
+    fprintf(stderr, "[riga] inverse probe: %d of %d chain supernodes above %.1e (max %.3e)\n", F->n_fix, nchain, tol,
+            emax);
+  RIGA_TRY(F->fix_flag.upload(flag.data(), flag.size(), st));
+  return RIGA_OK;
+}
+
 }  // namespace riga
 
 using namespace riga;
@@ -927,6 +966,7 @@ int riga_factor_create(riga_ctx* ctx, riga_symbolic* sym, double sigma, double r
   cudaEventElapsedTime(&F->factor_ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  RIGA_TRY(flag_inverse_refinement(F.get(), st));
   if (n_negative) *n_negative = stat[0];
   if (bad_pivot) *bad_pivot = stat[1] < h.n ? stat[1] : -1;
   if (tol[0] == 0.0) {

@@ -1,6 +1,7 @@
 // Handle definitions shared by the translation units of libriga_b200.so.
 #pragma once
 
+#include <cstring>
 #include <memory>
 
 #include "common.h"
@@ -80,6 +81,7 @@ struct I2 {
 // Task lists and pull map of the persistent solve kernels (solve.cu).
 struct SolvePlanHost {
   int warp_stage = 0, l2_prefetch = 0, chain_inv = 1, small_g = 1, occ = 4, rest_cap = 1 << 30, g_groups = 1;
+  int inv_fix = 1;  // local refinement step after each inv(L11) application
   std::vector<int32_t> gsn_f, gsn_b;   // supernode groups of the kGSn tasks (forward / backward)
   int64_t g_total = 0;                 // doubles of G = [inv(L11); L21 inv(L11)] of the small supernodes
   std::vector<int64_t> g_off;          // per supernode offset into gsmall (-1: large)
@@ -153,6 +155,11 @@ struct riga_factor {
   riga::DevBuf<double> tol;    // [0] max|A|, [1] zero_tol
   riga::DevBuf<double> linv;   // inv(L11) of the chain supernodes (solve.cu)
   riga::DevBuf<double> gsmall; // G of the small supernodes (solve.cu)
+  riga::DevBuf<double> rfix;   // chain-supernode refinement residuals (n)
+  riga::DevBuf<unsigned long long> inv_err;  // per supernode: inverse accuracy probe (double bits)
+  riga::DevBuf<int> fix_flag;  // per supernode: 1 = refine after the inverse application
+  std::vector<char> fix_level; // per level: any flagged chain supernode
+  int n_fix = 0;               // flagged chain supernodes
   riga::DevBuf<unsigned> pctr; // persistent-solve task / phase counters (reset per solve)
   float factor_ms = 0.f;
 };
@@ -176,4 +183,10 @@ int factor_solve_group(riga_symbolic* sym, const SlicePtrs* tab, int B, cudaStre
 int kron_mass_group(riga_system* sys, cudaStream_t s, const SlicePtrs* tab, int B);
 int upload_solve_plan(riga_symbolic* sym, cudaStream_t s);
 int build_chain_inverse(riga_factor* F, cudaStream_t s);
+int flag_inverse_refinement(riga_factor* F, cudaStream_t s);
+inline double __longlong_as_double_host(long long v) {
+  double d;
+  memcpy(&d, &v, sizeof d);
+  return d;
+}
 }  // namespace riga

@@ -1310,6 +1310,209 @@ __global__ void __launch_bounds__(256) k_inv_bwd(SymDev S, const int2* __restric
 }
 
 // ---------------------------------------------------------------------------
+// Chain supernodes: one step of local iterative refinement after each explicit
+// inverse application.  Applying inv(L11) is not backward stable when L11 is
+// ill-conditioned (unpivoted indefinite LDL^T): on cfg5 the inverse-only solve
+// has backward error 1e-8 against 2e-11 for substitution, which caps the
+// Lanczos residuals above north_star's 1e-8.  With z = inv~ y the correction
+// z += inv~ (y - L11 z) leaves an error E L11 E y (quadratic in the inverse's
+// error E): substitution-level accuracy for two extra sweeps over L11 / inv.
+//   forward:  r = y - L11 z  (rows: warps split K, lanes = 32 rows, as k_inv_fwd)
+//             z += inv(L11) r;  cvec = z / d
+//   backward: r = w - L11^T x1  (warp per pivot row: column of L11, coalesced)
+//             x1 += inv(L11)^T r
+// ---------------------------------------------------------------------------
+// Factor-time accuracy probe of each chain inverse: u = inv~ v for a fixed v, then
+// err[s] = max_i |(L11 u)_i - v_i| / max|v| (the solve's local backward error on
+// this supernode).  Supernodes above RIGA_INV_FIX_TOL (1e-11) get the refinement step.
+__device__ __forceinline__ double chk_v(int k) { return 1.0 + (double)((k * 7919) % 13) / 13.0; }
+
+__global__ void __launch_bounds__(256) k_inv_chk1(SymDev S, const int2* __restrict__ tasks,
+                                                  const int64_t* __restrict__ inv_off,
+                                                  const double* __restrict__ linv, double* __restrict__ u) {
+  __shared__ double part[8][32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int s = tasks[blockIdx.x].x;
+  const int np = (int)S.ncol[s];
+  const int r0 = 32 * tasks[blockIdx.x].y, r1 = min(np, r0 + 32);
+  const int chunk = (r1 + 7) / 8;
+  const int k0 = w * chunk, k1 = min(r1, k0 + chunk);
+  const double* A = linv + inv_off[s] + r0 + lane;
+  double acc = 0.0;
+  if (r0 + lane < r1)
+    for (int k = k0; k < k1; ++k) acc = fma(A[(int64_t)k * np], chk_v(k), acc);
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && r0 + lane < r1) {
+    double z = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) z += part[q][lane];
+    u[S.col0[s] + r0 + lane] = z;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_inv_chk2(SymDev S, const int2* __restrict__ tasks,
+                                                  const double* __restrict__ panel, const double* __restrict__ u,
+                                                  unsigned long long* __restrict__ err) {
+  __shared__ double part[8][32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int s = tasks[blockIdx.x].x;
+  const int np = (int)S.ncol[s];
+  const int f = (int)S.front[s];
+  const int64_t col0 = S.col0[s];
+  const int r0 = 32 * tasks[blockIdx.x].y, r1 = min(np, r0 + 32);
+  const int i = r0 + lane;
+  const int chunk = (r1 + 7) / 8;
+  const int k0 = w * chunk, k1 = min(r1, k0 + chunk);
+  const double* P = panel + S.panel_off[s] + i;
+  double acc = 0.0;
+  if (i < r1) {
+    const int kk1 = min(k1, i);
+    for (int k = k0; k < kk1; ++k) acc = fma(P[(int64_t)k * f], u[col0 + k], acc);
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0) {
+    double e = 0.0;
+    if (i < r1) {
+      double t = u[col0 + i];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t += part[q][lane];
+      e = fabs(t - chk_v(i)) / 2.0;  // max|v| < 2
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if (lane == 0 && e > 0.0) atomicMax(err + s, (unsigned long long)__double_as_longlong(e));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_inv_fix_fwd_res(SymDev S, SolveDev T, const int2* __restrict__ tasks,
+                                                         const int* __restrict__ flag, const double* __restrict__ panel,
+                                                         const double* __restrict__ b, const double* __restrict__ xp,
+                                                         const double* __restrict__ upd, double* __restrict__ rfix) {
+  extern __shared__ double zsh[];
+  __shared__ double part[8][32];
+  pdl_start();
+  if (!flag[tasks[blockIdx.x].x]) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int s = tasks[blockIdx.x].x;
+  const int np = (int)S.ncol[s];
+  const int f = (int)S.front[s];
+  const int64_t col0 = S.col0[s];
+  const int r0 = 32 * tasks[blockIdx.x].y, r1 = min(np, r0 + 32);
+  for (int k = tid; k < r1; k += 256) zsh[k] = xp[col0 + k];
+  __syncthreads();
+  const int i = r0 + lane;
+  const int kend = r1 - 1;  // rows i of this tile use the columns k < i <= r1 - 1
+  const int chunk = (kend + 7) / 8;
+  const int k0 = w * chunk, k1 = min(kend, k0 + chunk);
+  const double* P = panel + S.panel_off[s] + i;
+  double acc = 0.0;
+  if (i < r1) {
+    const int kk1 = min(k1, i);
+#pragma unroll 4
+    for (int k = k0; k < kk1; ++k) acc = fma(P[(int64_t)k * f], zsh[k], acc);
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && i < r1) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += part[q][lane];
+    const double y = gather_row(S, T, s, i, np, col0, b, upd);
+    rfix[col0 + i] = (y - zsh[i]) - t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_inv_fix_fwd_apply(SymDev S, const int2* __restrict__ tasks,
+                                                           const int* __restrict__ flag,
+                                                           const int64_t* __restrict__ inv_off,
+                                                           const double* __restrict__ linv,
+                                                           const double* __restrict__ D,
+                                                           const double* __restrict__ rfix, double* __restrict__ xp,
+                                                           double* __restrict__ cvec) {
+  extern __shared__ double y[];
+  __shared__ double part[8][32];
+  pdl_start();
+  if (!flag[tasks[blockIdx.x].x]) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int s = tasks[blockIdx.x].x;
+  const int np = (int)S.ncol[s];
+  const int64_t col0 = S.col0[s];
+  const int r0 = 32 * tasks[blockIdx.x].y, r1 = min(np, r0 + 32);
+  for (int k = tid; k < r1; k += 256) y[k] = rfix[col0 + k];
+  __syncthreads();
+  const int chunk = (r1 + 7) / 8;
+  const int k0 = w * chunk, k1 = min(r1, k0 + chunk);
+  const double* A = linv + inv_off[s] + r0 + lane;
+  double acc = 0.0;
+  if (r0 + lane < r1) {
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) acc = fma(A[(int64_t)k * np], y[k], acc);
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && r0 + lane < r1) {
+    double dz = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dz += part[q][lane];
+    const int64_t g = col0 + r0 + lane;
+    const double z = xp[g] + dz;
+    xp[g] = z;
+    cvec[g] = z / D[g];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_inv_fix_bwd_res(SymDev S, const int2* __restrict__ tasks,
+                                                         const int* __restrict__ flag, const double* __restrict__ panel,
+                                                         const double* __restrict__ cvec,
+                                                         const double* __restrict__ xp, double* __restrict__ rfix) {
+  pdl_start();
+  if (!flag[tasks[blockIdx.x].x]) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int s = tasks[blockIdx.x].x;
+  const int np = (int)S.ncol[s];
+  const int r = 8 * tasks[blockIdx.x].y + w;
+  if (r >= np) return;
+  const int f = (int)S.front[s];
+  const int64_t col0 = S.col0[s];
+  const double* P = panel + S.panel_off[s] + (int64_t)r * f;  // column r of L11
+  const double* xv = xp + col0;
+  double acc = 0.0;
+#pragma unroll 4
+  for (int k = r + 1 + lane; k < np; k += 32) acc = fma(P[k], xv[k], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) rfix[col0 + r] = (cvec[col0 + r] - xv[r]) - acc;
+}
+
+__global__ void __launch_bounds__(256) k_inv_fix_bwd_apply(SymDev S, const int2* __restrict__ tasks,
+                                                           const int* __restrict__ flag,
+                                                           const int64_t* __restrict__ inv_off,
+                                                           const double* __restrict__ linv,
+                                                           const double* __restrict__ rfix, double* __restrict__ xp,
+                                                           double* __restrict__ x) {
+  pdl_start();
+  if (!flag[tasks[blockIdx.x].x]) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int s = tasks[blockIdx.x].x;
+  const int np = (int)S.ncol[s];
+  const int r = 8 * tasks[blockIdx.x].y + w;
+  if (r >= np) return;
+  const int64_t col0 = S.col0[s];
+  const double* A = linv + inv_off[s] + (int64_t)r * np;
+  const double* rv = rfix + col0;
+  double acc = 0.0;
+#pragma unroll 4
+  for (int k = r + lane; k < np; k += 32) acc = fma(A[k], rv[k], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    const double v = xp[col0 + r] + acc;
+    xp[col0 + r] = v;
+    x[S.order[col0 + r]] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Persistent phase-ordered solve (one kernel per sweep).
 //
 // The level-by-level launches above cost one kernel per level and sweep
@@ -1616,6 +1819,8 @@ int build_solve_plan(riga_symbolic* sym) {
   L.l2_prefetch = env_flag("RIGA_L2_PREFETCH", 0);
   // chain supernodes through inv(L11) (default) or the serial chain kernels
   L.chain_inv = env_flag("RIGA_CHAIN_INV", 1);
+  // one local refinement step after every inv(L11) application (backward stability; RIGA_INV_FIX=0 off)
+  L.inv_fix = env_flag("RIGA_INV_FIX", 1);
   // small supernodes through G = [inv(L11); L21 inv(L11)] (default) or substitution
   L.small_g = env_flag("RIGA_SMALL_G", 1);
   L.occ = env_flag("RIGA_REST_OCC", 4);  // CTAs per SM the G-mode level kernels are register-bounded for
@@ -2016,6 +2221,8 @@ static int set_solve_attrs() {
   RIGA_TRY(raise_smem(k_chain_fwd, maxsm));
   RIGA_TRY(raise_smem(k_chain_bwd, maxsm));
   RIGA_TRY(raise_smem(k_inv_fwd, maxsm));
+  RIGA_TRY(raise_smem(k_inv_fix_fwd_res, maxsm));
+  RIGA_TRY(raise_smem(k_inv_fix_fwd_apply, maxsm));
   RIGA_TRY(raise_smem(k_rest_fwd_g<true, 4>, maxsm));
   RIGA_TRY(raise_smem(k_rest_bwd_g<true, 4>, maxsm));
   RIGA_TRY(raise_smem(k_inv_fwd_g, maxsm));
@@ -2046,6 +2253,8 @@ int build_chain_inverse(riga_factor* F, cudaStream_t st) {
   }
   if (!L.chain_inv || !L.inv_total) return RIGA_OK;
   if (!F->linv.p) RIGA_TRY(F->linv.alloc(L.inv_total, st));
+  if (L.inv_fix && !F->rfix.p) RIGA_TRY(F->rfix.alloc(sym->h.n, st));
+  if (L.inv_fix && !F->inv_err.p) RIGA_TRY(F->inv_err.alloc(sym->h.nsuper, st));
   // the doubling GEMMs read whole diagonal blocks: the upper triangles must be zero
   RIGA_CUDA(cudaMemsetAsync(F->linv.p, 0, L.inv_total * sizeof(double), st));
   const int nd = (int)L.idiag.size();
@@ -2065,6 +2274,14 @@ int build_chain_inverse(riga_factor* F, cudaStream_t st) {
                                        tbuf.p, F->linv.p);
       count_launch(2);
     }
+  }
+  if (L.inv_fix && !L.ifwd.empty()) {
+    const int nt = (int)L.ifwd.size();
+    const int2* it = reinterpret_cast<const int2*>(sym->d_ifwd.p);
+    RIGA_CUDA(cudaMemsetAsync(F->inv_err.p, 0, sym->h.nsuper * sizeof(unsigned long long), st));
+    k_inv_chk1<<<nt, 256, 0, st>>>(S, it, sym->d_inv_off.p, F->linv.p, F->rfix.p);
+    k_inv_chk2<<<nt, 256, 0, st>>>(S, it, F->panel.p, F->rfix.p, F->inv_err.p);
+    count_launch(2);
   }
   RIGA_CUDA(cudaGetLastError());
   return RIGA_OK;
@@ -2183,10 +2400,17 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     const int nc = (int)(L.chain_ptr[l + 1] - L.chain_ptr[l]);
     const int ni = (int)(L.ifwd_ptr[l + 1] - L.ifwd_ptr[l]);
     if (L.chain_inv && ni) {
-      RIGA_CUDA(launch(k_inv_fwd, ni, 256, L.ifwd_smem[l], st, S, T, reinterpret_cast<const int2*>(sym->d_ifwd.p) + L.ifwd_ptr[l],
-                                                  sym->d_inv_off.p, F->linv.p, F->D.p, b, F->xperm.p, F->upd.p,
-                                                  F->cvec.p));
+      const int2* it = reinterpret_cast<const int2*>(sym->d_ifwd.p) + L.ifwd_ptr[l];
+      RIGA_CUDA(launch(k_inv_fwd, ni, 256, L.ifwd_smem[l], st, S, T, it, sym->d_inv_off.p, F->linv.p, F->D.p, b,
+                       F->xperm.p, F->upd.p, F->cvec.p));
       count_launch();
+      if (L.inv_fix && F->fix_level[l]) {
+        RIGA_CUDA(launch(k_inv_fix_fwd_res, ni, 256, L.ifwd_smem[l], st, S, T, it, F->fix_flag.p, F->panel.p, b,
+                         F->xperm.p, F->upd.p, F->rfix.p));
+        RIGA_CUDA(launch(k_inv_fix_fwd_apply, ni, 256, L.ifwd_smem[l], st, S, it, F->fix_flag.p, sym->d_inv_off.p,
+                         F->linv.p, F->D.p, F->rfix.p, F->xperm.p, F->cvec.p));
+        count_launch(2);
+      }
     } else if (nc) {
       RIGA_CUDA(launch(k_chain_fwd, nc, kSolveThreads, L.chf_smem[l], st, S, T, sym->d_chains.p + L.chain_ptr[l],
                                                             (int)L.chf_smem[l], F->panel.p, b, F->xperm.p,
@@ -2213,9 +2437,16 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
     const int nc = (int)(L.chain_ptr[l + 1] - L.chain_ptr[l]);
     const int ni = (int)(L.ibwd_ptr[l + 1] - L.ibwd_ptr[l]);
     if (L.chain_inv && ni) {
-      RIGA_CUDA(launch(k_inv_bwd, ni, 256, 0, st, S, reinterpret_cast<const int2*>(sym->d_ibwd.p) + L.ibwd_ptr[l],
-                                     sym->d_inv_off.p, F->linv.p, F->cvec.p, F->xperm.p, x));
+      const int2* it = reinterpret_cast<const int2*>(sym->d_ibwd.p) + L.ibwd_ptr[l];
+      RIGA_CUDA(launch(k_inv_bwd, ni, 256, 0, st, S, it, sym->d_inv_off.p, F->linv.p, F->cvec.p, F->xperm.p, x));
       count_launch();
+      if (L.inv_fix && F->fix_level[l]) {
+        RIGA_CUDA(launch(k_inv_fix_bwd_res, ni, 256, 0, st, S, it, F->fix_flag.p, F->panel.p, F->cvec.p, F->xperm.p,
+                         F->rfix.p));
+        RIGA_CUDA(launch(k_inv_fix_bwd_apply, ni, 256, 0, st, S, it, F->fix_flag.p, sym->d_inv_off.p, F->linv.p,
+                         F->rfix.p, F->xperm.p, x));
+        count_launch(2);
+      }
     } else if (nc) {
       RIGA_CUDA(launch(k_chain_bwd, nc, kSolveThreads, L.chb_smem[l], st, S, sym->d_chains.p + L.chain_ptr[l],
                                                             (int)L.chb_smem[l], F->panel.p, F->D.p,
