@@ -1,6 +1,6 @@
 """One slice through solve_slice with the residual gate; prints the gate history (GPU).
 
-    RIGA_GATE_MODE=xy|y python tools/gate_slice.py cfg5_riga 31
+    python tools/gate_slice.py cfg5_riga 31
 """
 import json
 import os
