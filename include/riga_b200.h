@@ -204,32 +204,9 @@ int riga_lanczos_locked_count(riga_lanczos* lz, int64_t* count);
 int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_host,
                         double breakdown_tol, double* alpha, double* beta, double* wnorm,
                         int64_t* steps);
-/* Engine extension (no reference counterpart): run the step replays of
- * later extends on `stream` (a cudaStream_t; NULL = the context stream),
- * forked from and joined back to the context stream, so a driver can move a
- * slice's extends between stream priorities; allocations stay on the
- * context stream.  riga_lanczos_reset clears it.                           */
-int riga_lanczos_set_run_stream(riga_lanczos* lz, void* stream);
 /* Device milliseconds of the last extend's step replays (CUDA events on
  * the state's stream around the replayed step graphs; 0 if none ran).      */
 int riga_lanczos_last_extend_ms(riga_lanczos* lz, float* ms);
-/* ---- lockstep groups -------------------------------------------------------
- * B Lanczos states of one pencil (same symbolic analysis and Kronecker mass,
- * different shifts) stepped by ONE step graph whose kernels carry a member
- * dimension (each solve level is one launch over all members' factors).
- * begin: member joins slot with a run to `limit` (coupling as in
- * riga_lanczos_extend), after the work queued on its own stream; run: `steps`
- * lockstep replays (stopped members are no-ops); poll: per slot -1 empty, 0
- * running, 1 breakdown, 2 limit reached (and its k); end: a stopped member
- * leaves with its recurrence (as riga_lanczos_extend returns it).          */
-typedef struct riga_lzgroup riga_lzgroup;
-int riga_lzgroup_create(riga_ctx* ctx, int B, riga_lzgroup** out);
-int riga_lzgroup_destroy(riga_lzgroup* g);
-int riga_lzgroup_begin(riga_lzgroup* g, int slot, riga_lanczos* lz, int64_t limit, const double* coupling_host,
-                       double breakdown_tol);
-int riga_lzgroup_run(riga_lzgroup* g, int64_t steps);
-int riga_lzgroup_poll(riga_lzgroup* g, int* state, int64_t* k);
-int riga_lzgroup_end(riga_lzgroup* g, int slot, double* alpha, double* beta, double* wnorm, int64_t* steps);
 /* One step with a caller-computed w = H v (device vector of length n), for
  * operators that are not a device factor (ref LanczosState(apply_op=...)
  * with an arbitrary callable).  Outputs as riga_lanczos_extend (1 step).   */

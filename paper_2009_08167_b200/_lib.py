@@ -71,13 +71,6 @@ SIGNATURES = {
     "riga_lanczos_locked_count": [_p, _p],
     "riga_lanczos_extend": [_p, _i64, _p, _d, _p, _p, _p, _p],
     "riga_lanczos_last_extend_ms": [_p, _p],
-    "riga_lanczos_set_run_stream": [_p, _p],
-    "riga_lzgroup_create": [_p, _i32, _p],
-    "riga_lzgroup_destroy": [_p],
-    "riga_lzgroup_begin": [_p, _i32, _p, _i64, _p, _d],
-    "riga_lzgroup_run": [_p, _i64],
-    "riga_lzgroup_poll": [_p, _p, _p],
-    "riga_lzgroup_end": [_p, _i32, _p, _p, _p, _p],
     "riga_lanczos_step_given": [_p, _p, _p, _d, _p, _p, _p],
     "riga_lanczos_lift": [_p, _p, _i64, _p, _p],
     "riga_lanczos_restart": [_p, _p, _i64],

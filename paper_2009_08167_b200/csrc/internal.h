@@ -48,18 +48,6 @@ struct LzDev {
   double scal[8];  // [0] alpha, [1] |w|^2, [2] beta^2, [4] ref norm^2
 };
 
-// One member of a lockstep group (riga_lzgroup): every buffer a batched step
-// kernel needs for that slice.  Read by the kernels at run time, so the
-// group's captured graph stays valid while members change.
-struct SlicePtrs {
-  LzDev* st;
-  int64_t rows, Rmax;  // max_dim + 1, max_dim + 1 + locked capacity
-  double *V, *MV, *L, *LM, *w, *r, *Mr, *bp, *vt, *mvt;
-  double *coef, *partial, *upart, *cpl, *outs, *dscratch, *kt1, *kt2, *ks1, *ks2;
-  unsigned *tk_dots, *tk_upd;
-  const double *panel, *D, *linv, *gsmall;
-  double *xperm, *upd, *cvec;
-};
 }  // namespace riga
 
 struct LevelPlan {
@@ -78,11 +66,10 @@ struct I2 {
   int32_t x, y;
 };
 
-// Task lists and pull map of the persistent solve kernels (solve.cu).
+// Task lists and pull map of the level-scheduled solve kernels (solve.cu).
 struct SolvePlanHost {
-  int warp_stage = 0, l2_prefetch = 0, chain_inv = 1, small_g = 1, occ = 4, rest_cap = 1 << 30, g_groups = 1;
+  int warp_stage = 0, chain_inv = 1, small_g = 1, occ = 4, rest_cap = 1 << 30;
   int inv_fix = 1;  // local refinement step after each inv(L11) application
-  std::vector<int32_t> gsn_f, gsn_b;   // supernode groups of the kGSn tasks (forward / backward)
   int64_t g_total = 0;                 // doubles of G = [inv(L11); L21 inv(L11)] of the small supernodes
   std::vector<int64_t> g_off;          // per supernode offset into gsmall (-1: large)
   std::vector<I2> gfwd, gbwd;          // G warp tasks: (supernode, row tile) / (supernode, column group)
@@ -104,10 +91,6 @@ struct SolvePlanHost {
   std::vector<int64_t> fwd_smem, bwd_smem, chf_smem, chb_smem;  // bytes per level launch
   std::vector<int32_t> gsrc;
   std::vector<int64_t> gptr;
-  // persistent phase-ordered solve (solve.cu k_solve_pers): tasks (type, a, b, phase)
-  int pers = 0, pers_ctas = 296;
-  std::vector<int> ptf, ptb;            // flattened int4 tasks
-  std::vector<int> pcf, pcb;            // tasks per phase
 };
 
 struct riga_symbolic {
@@ -131,8 +114,6 @@ struct riga_symbolic {
   riga::DevBuf<int64_t> d_gptr, d_inv_off, d_g_off;
   riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_dbl_tasks, d_gfwd, d_gbwd, d_sub_ftiles, d_sub_btiles;
   riga::DevBuf<int64_t> d_dbl_toff;
-  riga::DevBuf<int> d_ptf, d_ptb, d_pcf, d_pcb;
-  riga::DevBuf<int32_t> d_gsn_f, d_gsn_b;
   SymDev dev() const {
     return SymDev{d_col0.p,     d_ncol.p,      d_front.p,      d_rows_off.p,   d_panel_off.p,
                   d_cb_off.p,   d_upd_off.p,   d_child_ptr.p,  d_asm_ptr.p,    d_sparent.p,
@@ -160,7 +141,6 @@ struct riga_factor {
   riga::DevBuf<int> fix_flag;  // per supernode: 1 = refine after the inverse application
   std::vector<char> fix_level; // per level: any flagged chain supernode
   int n_fix = 0;               // flagged chain supernodes
-  riga::DevBuf<unsigned> pctr; // persistent-solve task / phase counters (reset per solve)
   float factor_ms = 0.f;
 };
 
@@ -176,11 +156,6 @@ int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x,
                  bool b_permuted = false);
 int build_solve_plan(riga_symbolic* sym);
 int prepare_solve();
-// the solve of a lockstep group: every level kernel covers all B members
-// (grid z = member); sym is the members' common symbolic analysis
-int factor_solve_group(riga_symbolic* sym, const SlicePtrs* tab, int B, cudaStream_t s);
-// y = M x for every member (z = 2 B: member x {vt -> mvt, r -> Mr})
-int kron_mass_group(riga_system* sys, cudaStream_t s, const SlicePtrs* tab, int B);
 int upload_solve_plan(riga_symbolic* sym, cudaStream_t s);
 int build_chain_inverse(riga_factor* F, cudaStream_t s);
 int flag_inverse_refinement(riga_factor* F, cudaStream_t s);

@@ -31,7 +31,7 @@ namespace riga {
 
 constexpr int kChunk = 512;  // columns per CTA in the tall-skinny GEMV
 
-// LzDev (device recurrence state) and SlicePtrs (lockstep groups): internal.h
+// LzDev (device recurrence state): internal.h
 
 // rows used by a CGS pass: basis rows [0, k + add) and/or the locked set
 struct RowSel {
@@ -915,38 +915,6 @@ __global__ void k_rowscale(double* __restrict__ X, double* __restrict__ MX, int6
 
 using namespace riga;
 
-// ---- lockstep groups: the step kernels with a member dimension (z) --------
-__global__ void k_perm_row_g(const SlicePtrs* tab, int64_t n, int64_t ld, const int32_t* __restrict__ order) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  k_perm_row_body(P.st, n, ld, P.MV, order, P.bp);
-}
-__global__ void __launch_bounds__(256, 2) k_dcgs_dots_g(const SlicePtrs* tab, int64_t n, int64_t ld) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  k_dcgs_dots_body(RowSel{P.MV, P.LM, ld, 1, 1}, P.st, n, P.Rmax, P.V, P.w, P.partial, P.coef, P.tk_dots);
-}
-__global__ void __launch_bounds__(256) k_dcgs_scalars_g(const SlicePtrs* tab) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  k_dcgs_scalars_body(P.st, P.Rmax, P.coef, P.cpl, P.outs + P.rows);
-}
-__global__ void __launch_bounds__(256) k_dcgs_upd_g(const SlicePtrs* tab, int64_t n, int64_t ld) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  k_dcgs_upd_body(RowSel{P.V, P.L, ld, 1, 1}, P.st, n, ld, P.Rmax, P.coef, P.upart, P.w, P.vt, P.r, P.tk_upd,
-                  P.cpl);
-}
-__global__ void k_dot2_g(const SlicePtrs* tab, int64_t n, int64_t ld) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  k_dot2_body(P.st, n, ld, P.r, 0, P.Mr, P.r, P.Mr, P.dscratch, reinterpret_cast<unsigned*>(P.dscratch + 2 * 296),
-              P.st->scal + 2);
-}
-__global__ void k_dcgs_store_g(const SlicePtrs* tab, int64_t n, int64_t ld) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  k_dcgs_store_body(P.st, n, ld, P.vt, P.mvt, P.r, P.Mr, P.V, P.MV);
-}
-__global__ void k_step_finish_g(const SlicePtrs* tab) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  k_step_finish_body(P.st, P.cpl, P.outs, P.outs + P.rows, P.outs + 2 * P.rows, 1);
-}
-
 struct riga_lanczos {
   riga::CtxRef ctxref;
   riga_ctx* ctx = nullptr;
@@ -973,18 +941,11 @@ struct riga_lanczos {
   long long gnodes = 0;  // kernel launches per replay
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // around the last extend's replays
   bool ev_valid = false;
-  // optional stream the step replays run on (forked from / joined back to the
-  // context stream around each extend): lets a driver move a slice's extends
-  // between stream priorities without moving its allocations
-  cudaStream_t run = nullptr;
-  cudaEvent_t evf = nullptr, evj = nullptr;
   cudaStream_t cur = nullptr;   // stream the step helpers launch on
   cudaStream_t capst = nullptr; // private stream for graph capture (never legacy)
   ~riga_lanczos() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (evf) cudaEventDestroy(evf);
-    if (evj) cudaEventDestroy(evj);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (capst) cudaStreamDestroy(capst);
     if (hbuf) riga::pinned_put(hbuf);
@@ -1279,7 +1240,6 @@ int riga_lanczos_reset(riga_lanczos* lz, riga_system* mass) {
   RIGA_CHECK_ARG(!mass || mass->n == lz->n, "mass dimension mismatch");
   DeviceGuard g(lz->ctx->device);
   lz->sys = mass;
-  lz->run = nullptr;
   if (mass && mass->kdim && !getenv("RIGA_CSR_MASS")) {
     if (!lz->kt1.p) {
       RIGA_TRY(lz->kt1.alloc(lz->n, lz->ctx->stream));
@@ -1397,23 +1357,9 @@ int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_
     RIGA_CUDA(cudaEventCreate(&lz->ev0));
     RIGA_CUDA(cudaEventCreate(&lz->ev1));
   }
-  cudaStream_t rs = s;
-  if (lz->run && lz->run != s) {  // fork onto the run stream
-    if (!lz->evf) {
-      RIGA_CUDA(cudaEventCreateWithFlags(&lz->evf, cudaEventDisableTiming));
-      RIGA_CUDA(cudaEventCreateWithFlags(&lz->evj, cudaEventDisableTiming));
-    }
-    RIGA_CUDA(cudaEventRecord(lz->evf, s));
-    RIGA_CUDA(cudaStreamWaitEvent(lz->run, lz->evf, 0));
-    rs = lz->run;
-  }
-  RIGA_CUDA(cudaEventRecord(lz->ev0, rs));
-  for (int64_t i = lz->k; i < limit; ++i) RIGA_CUDA(cudaGraphLaunch(lz->gexec, rs));
-  RIGA_CUDA(cudaEventRecord(lz->ev1, rs));
-  if (rs != s) {  // join: everything after the extend stays ordered on the context stream
-    RIGA_CUDA(cudaEventRecord(lz->evj, rs));
-    RIGA_CUDA(cudaStreamWaitEvent(s, lz->evj, 0));
-  }
+  RIGA_CUDA(cudaEventRecord(lz->ev0, s));
+  for (int64_t i = lz->k; i < limit; ++i) RIGA_CUDA(cudaGraphLaunch(lz->gexec, s));
+  RIGA_CUDA(cudaEventRecord(lz->ev1, s));
   lz->ev_valid = true;
   count_launch((int)((limit - lz->k) * lz->gnodes));
   const int64_t rows = lz->max_dim + 1;
@@ -1442,12 +1388,6 @@ int riga_lanczos_extend(riga_lanczos* lz, int64_t limit, const double* coupling_
   *steps = ns;
   lz->k = lz->hst->k;
   return lz->hst->stop == 1 ? RIGA_BREAKDOWN : RIGA_OK;
-}
-
-int riga_lanczos_set_run_stream(riga_lanczos* lz, void* stream) {
-  RIGA_CHECK_ARG(lz, "null arg");
-  lz->run = (cudaStream_t)stream;
-  return RIGA_OK;
 }
 
 int riga_lanczos_last_extend_ms(riga_lanczos* lz, float* ms) {
@@ -1762,245 +1702,6 @@ int riga_lanczos_basis(riga_lanczos* lz, double** V, double** MV, int64_t* ld) {
   if (MV) *MV = lz->MV.p;
   if (ld) *ld = lz->ld;
   return RIGA_OK;
-}
-
-}  // extern "C"
-
-// ---------------------------------------------------------------------------
-// Lockstep groups: B Lanczos runs (slices of one pencil, same symbolic
-// structure, different shifts) stepped together by ONE step graph whose
-// kernels carry a member dimension, so each level of the supernodal solve is
-// one launch over all members' factors instead of B thin launches.  Members
-// join (begin: after their own stream's work) and leave (end: second pass of
-// the pending row, alpha/beta to host) independently; an empty slot points at
-// a stopped dummy state, so the captured graph never changes.
-// ---------------------------------------------------------------------------
-struct riga_lzgroup {
-  riga::CtxRef ctxref;
-  riga_ctx* ctx = nullptr;
-  int B = 0;
-  std::vector<riga_lanczos*> mem;
-  std::vector<SlicePtrs> htab;
-  DevBuf<SlicePtrs> tab;
-  DevBuf<LzDev> dummy;
-  DevBuf<double> ks;  // second kron-product scratch, 2 rows of ld per slot
-  cudaStream_t s = nullptr, capst = nullptr;
-  cudaEvent_t ev = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  riga_symbolic* gsym = nullptr;
-  riga_system* gsys = nullptr;
-  int64_t n = 0, ld = 0;
-  LzDev* hst = nullptr;  // pinned, one per slot
-  ~riga_lzgroup() {
-    if (gexec) cudaGraphExecDestroy(gexec);
-    if (ev) cudaEventDestroy(ev);
-    if (capst) cudaStreamDestroy(capst);
-    if (hst) riga::pinned_put(hst);
-  }
-};
-
-namespace {
-
-SlicePtrs empty_slot(riga_lzgroup* g) {
-  SlicePtrs P{};
-  P.st = g->dummy.p;
-  return P;
-}
-
-SlicePtrs fill_slot(riga_lzgroup* g, int slot, riga_lanczos* lz) {
-  SlicePtrs P{};
-  P.st = lz->st.p;
-  P.rows = lz->max_dim + 1;
-  P.Rmax = lz->max_dim + 1 + lz->cap;
-  P.V = lz->V.p; P.MV = lz->MV.p; P.L = lz->L.p; P.LM = lz->LM.p;
-  P.w = lz->w.p; P.r = lz->r.p; P.Mr = lz->Mr.p; P.bp = lz->bp.p; P.vt = lz->vt.p; P.mvt = lz->mvt.p;
-  P.coef = lz->coef.p; P.partial = lz->partial.p; P.upart = lz->upart.p; P.cpl = lz->cpl.p; P.outs = lz->outs.p;
-  P.dscratch = lz->dscratch.p; P.kt1 = lz->kt1.p; P.kt2 = lz->kt2.p;
-  P.ks1 = g->ks.p + (2 * (int64_t)slot) * g->ld;
-  P.ks2 = g->ks.p + (2 * (int64_t)slot + 1) * g->ld;
-  P.tk_dots = lz->tk_dots.p; P.tk_upd = lz->tk_upd.p;
-  riga_factor* F = lz->op;
-  P.panel = F->panel.p; P.D = F->D.p; P.linv = F->linv.p; P.gsmall = F->gsmall.p;
-  P.xperm = F->xperm.p; P.upd = F->upd.p; P.cvec = F->cvec.p;
-  return P;
-}
-
-int upload_slot(riga_lzgroup* g, int slot) {
-  RIGA_CUDA(cudaMemcpyAsync(g->tab.p + slot, &g->htab[slot], sizeof(SlicePtrs), cudaMemcpyHostToDevice, g->s));
-  return RIGA_OK;
-}
-
-int group_graph(riga_lzgroup* g) {
-  if (g->gexec) return RIGA_OK;
-  RIGA_TRY(prepare_solve());
-  RIGA_CUDA(stream_sync(g->s));
-  if (!g->capst) RIGA_CUDA(cudaStreamCreateWithFlags(&g->capst, cudaStreamNonBlocking));
-  const int64_t n = g->n, ld = g->ld;
-  const unsigned B = (unsigned)g->B;
-  const long long n0 = t_launches;
-  cudaGraph_t gr = nullptr;
-  RIGA_CUDA(cudaStreamBeginCapture(g->capst, cudaStreamCaptureModeThreadLocal));
-  cudaStream_t c = g->capst;
-  int rc = RIGA_OK;
-  do {
-    k_perm_row_g<<<dim3((unsigned)((n + 255) / 256), 1, B), 256, 0, c>>>(g->tab.p, n, ld, g->gsym->d_order.p);
-    count_launch();
-    if ((rc = factor_solve_group(g->gsym, g->tab.p, g->B, c))) break;
-    k_dcgs_dots_g<<<dim3(kDotGrid, 1, B), 256, 0, c>>>(g->tab.p, n, ld);
-    k_dcgs_upd_g<<<dim3((unsigned)((n + kUpdCols - 1) / kUpdCols), kUpdGroups, B), 256, 0, c>>>(g->tab.p, n, ld);
-    count_launch(2);
-    if ((rc = kron_mass_group(g->gsys, c, g->tab.p, g->B))) break;
-    const unsigned blocks = (unsigned)std::min<int64_t>(296, (n + 255) / 256);
-    k_dot2_g<<<dim3(blocks, 1, B), 256, 0, c>>>(g->tab.p, n, ld);
-    k_dcgs_store_g<<<dim3((unsigned)((n + 255) / 256), 1, B), 256, 0, c>>>(g->tab.p, n, ld);
-    k_step_finish_g<<<dim3(1, 1, B), 1, 0, c>>>(g->tab.p);
-    count_launch(3);
-  } while (false);
-  cudaError_t e = cudaStreamEndCapture(g->capst, &gr);
-  g_launches.fetch_sub(t_launches - n0);  // captured, not launched
-  if (rc) {
-    if (gr) cudaGraphDestroy(gr);
-    return rc;
-  }
-  RIGA_CUDA(e);
-  e = cudaGraphInstantiate(&g->gexec, gr, 0);
-  cudaGraphDestroy(gr);
-  RIGA_CUDA(e);
-  return RIGA_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int riga_lzgroup_create(riga_ctx* ctx, int B, riga_lzgroup** out) {
-  RIGA_CHECK_ARG(ctx && out && B >= 1, "bad arg");
-  DeviceGuard gd(ctx->device);
-  auto g = std::make_unique<riga_lzgroup>();
-  g->ctx = ctx;
-  g->ctxref.set(ctx);
-  g->B = B;
-  g->s = ctx->stream;
-  g->mem.assign(B, nullptr);
-  RIGA_CUDA(cudaEventCreateWithFlags(&g->ev, cudaEventDisableTiming));
-  RIGA_TRY(g->dummy.alloc(1, g->s));
-  LzDev d{};
-  d.stop = 1;
-  RIGA_CUDA(cudaMemcpyAsync(g->dummy.p, &d, sizeof(LzDev), cudaMemcpyHostToDevice, g->s));
-  RIGA_TRY(g->tab.alloc(B, g->s));
-  g->htab.assign(B, SlicePtrs{});
-  for (int i = 0; i < B; ++i) {
-    g->htab[i] = empty_slot(g.get());
-    RIGA_TRY(upload_slot(g.get(), i));
-  }
-  g->hst = static_cast<LzDev*>(pinned_get(B * sizeof(LzDev)));
-  if (!g->hst) {
-    set_error("pinned host allocation failed");
-    return RIGA_OOM;
-  }
-  RIGA_CUDA(stream_sync(g->s));
-  *out = g.release();
-  return RIGA_OK;
-}
-
-int riga_lzgroup_destroy(riga_lzgroup* g) {
-  if (!g) return RIGA_OK;
-  DeviceGuard gd(g->ctx->device);
-  stream_sync(g->s);
-  delete g;
-  return RIGA_OK;
-}
-
-int riga_lzgroup_begin(riga_lzgroup* g, int slot, riga_lanczos* lz, int64_t limit, const double* coupling_host,
-                       double breakdown_tol) {
-  RIGA_CHECK_ARG(g && lz && slot >= 0 && slot < g->B && !g->mem[slot], "bad slot");
-  RIGA_CHECK_ARG(lz->op && lz->delayed && lz->sys && lz->sys->kdim && lz->kron_ok,
-                 "group members need a device operator, the delayed step and a Kronecker mass");
-  DeviceGuard gd(g->ctx->device);
-  if (!g->gsym) {
-    g->gsym = lz->op->sym;
-    g->gsys = lz->sys;
-    g->n = lz->n;
-    g->ld = lz->ld;
-    RIGA_TRY(g->ks.alloc(2 * (int64_t)g->B * g->ld, g->s));
-  }
-  RIGA_CHECK_ARG(lz->op->sym == g->gsym && lz->sys == g->gsys && lz->n == g->n && lz->ld == g->ld,
-                 "group members must share the symbolic analysis and the mass system");
-  limit = std::min(limit, lz->max_dim);
-  RIGA_CHECK_ARG(lz->k < limit, "nothing to extend");
-  // after everything already queued on the member's own stream
-  RIGA_CUDA(cudaEventRecord(g->ev, lz->ctx->stream));
-  RIGA_CUDA(cudaStreamWaitEvent(g->s, g->ev, 0));
-  int64_t clo = lz->k;
-  if (coupling_host && lz->k > 0) {
-    RIGA_CUDA(cudaMemcpyAsync(lz->cpl.p, coupling_host, lz->k * 8, cudaMemcpyHostToDevice, g->s));
-    clo = 0;
-  }
-  RIGA_TRY(push_state(lz, clo, limit, breakdown_tol, g->s));
-  g->htab[slot] = fill_slot(g, slot, lz);
-  RIGA_TRY(upload_slot(g, slot));
-  g->mem[slot] = lz;
-  return RIGA_OK;
-}
-
-int riga_lzgroup_run(riga_lzgroup* g, int64_t steps) {
-  RIGA_CHECK_ARG(g && steps >= 0, "bad arg");
-  if (!g->gsym || steps == 0) return RIGA_OK;
-  DeviceGuard gd(g->ctx->device);
-  RIGA_TRY(group_graph(g));
-  for (int64_t i = 0; i < steps; ++i) RIGA_CUDA(cudaGraphLaunch(g->gexec, g->s));
-  return RIGA_OK;
-}
-
-// per slot: -1 empty, 0 running, 1 breakdown, 2 limit reached; k[slot] = basis size
-int riga_lzgroup_poll(riga_lzgroup* g, int* state, int64_t* k) {
-  RIGA_CHECK_ARG(g && state, "null arg");
-  DeviceGuard gd(g->ctx->device);
-  for (int i = 0; i < g->B; ++i)
-    if (g->mem[i])
-      RIGA_CUDA(cudaMemcpyAsync(&g->hst[i], g->mem[i]->st.p, sizeof(LzDev), cudaMemcpyDeviceToHost, g->s));
-  RIGA_CUDA(stream_sync(g->s));
-  for (int i = 0; i < g->B; ++i) {
-    state[i] = g->mem[i] ? g->hst[i].stop : -1;
-    if (k) k[i] = g->mem[i] ? g->hst[i].k : 0;
-  }
-  return RIGA_OK;
-}
-
-// member `slot` has stopped (poll): finish its run exactly as riga_lanczos_extend
-// does (second pass of the pending row) and return its recurrence
-int riga_lzgroup_end(riga_lzgroup* g, int slot, double* alpha, double* beta, double* wnorm, int64_t* steps) {
-  RIGA_CHECK_ARG(g && slot >= 0 && slot < g->B && g->mem[slot] && alpha && beta && wnorm && steps, "bad arg");
-  DeviceGuard gd(g->ctx->device);
-  riga_lanczos* lz = g->mem[slot];
-  const LzDev h = g->hst[slot];
-  RIGA_CHECK_ARG(h.stop != 0, "member still running");
-  // leave the group first: later replays skip the slot
-  g->htab[slot] = empty_slot(g);
-  RIGA_TRY(upload_slot(g, slot));
-  g->mem[slot] = nullptr;
-  const int ns = h.steps;
-  lz->k = h.k;
-  if (h.stop != 1 && ns > 0) {
-    lz->cur = g->s;
-    const int rc = finish_pending(lz, ns - 1, g->s);
-    lz->cur = lz->ctx->stream;
-    RIGA_TRY(rc);
-  }
-  const int64_t rows = lz->max_dim + 1;
-  RIGA_CUDA(cudaMemcpyAsync(lz->hbuf, lz->outs.p, 3 * rows * 8, cudaMemcpyDeviceToHost, g->s));
-  RIGA_CUDA(stream_sync(g->s));
-  for (int i = 0; i < ns; ++i) {
-    alpha[i] = lz->hbuf[i];
-    beta[i] = lz->hbuf[rows + i];
-    wnorm[i] = lz->hbuf[2 * rows + i];
-  }
-  *steps = ns;
-  lz->k = h.k;
-  lz->hst->k = h.k;
-  lz->hst->steps = ns;
-  lz->hst->stop = h.stop;
-  return h.stop == 1 ? RIGA_BREAKDOWN : RIGA_OK;
 }
 
 }  // extern "C"

@@ -38,10 +38,8 @@ constexpr int kWarpSmem = kWholeMaxF + kWarpPanel;  // doubles of smem per warp 
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int64_t kChainSmemMax = 232448 - 4096;  // staged chain panels must fit this
-constexpr int64_t kPrefetchMaxBytes = 96ll << 20;  // prefetch the factor into L2 when it fits
 
-enum { kWholeGroup = 1, kUpd = 2, kColdot = 3, kGTiles = 4, kGSn = 5 };
-constexpr int kGrpMaxF = 2048;  // front rows staged per backward supernode group
+enum { kWholeGroup = 1, kUpd = 2, kColdot = 3, kGTiles = 4 };
 
 struct SolveDev {
   const int64_t* gptr;  // pull map over front positions (rows_off indexing)
@@ -262,84 +260,10 @@ struct GDev {
   const int2* tiles;      // warp tasks: (supernode, 32-row tile) forward / (supernode, 8-column group) backward
   int on;
   const double* D;        // pivots
-  const int32_t* sn;      // supernode groups (kGSn tasks): ids, grouped per level
   double* wz;             // z ./ d of the small supernodes (forward -> backward), so the
                           // backward column groups of one supernode never read the x
                           // another group of it is writing
 };
-
-// ---- supernode-group G tasks (kGSn): one CTA per group of whole supernodes --
-// The tile-per-warp tasks above re-gather a supernode's pivot rows y1 in every
-// one of its ceil(f/32) forward tiles, and re-read its whole front vector in
-// every one of its ceil(np/8) backward column groups (each a pull-map or
-// rows[] indirection, sector-granular in L2).  A group task gathers them once
-// into shared memory and its 8 warps share them.
-
-// forward tile t of supernode s with y1 already in yw (shared)
-__device__ __forceinline__ void warp_gtile_fwd_y(const SymDev& S, const SolveDev& T, const GDev& GD, int s, int t,
-                                                 const double* __restrict__ b, double* xp, double* upd,
-                                                 const double* yw, int lane) {
-  const int f = (int)S.front[s], np = (int)S.ncol[s];
-  const int64_t col0 = S.col0[s];
-  const double* G = GD.g + GD.g_off[s];
-  const int i = 32 * t + lane;
-  const double yi = (i >= np && i < f) ? gather_row(S, T, s, i, np, col0, b, upd) : 0.0;
-  if (i >= f) return;
-  double a4[4] = {0.0, 0.0, 0.0, 0.0};
-  const double* Gi = G + i;
-  int k = 0;
-  for (; k + 16 <= np; k += 16) {
-    double g[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) g[u] = Gi[(k + u) * f];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) a4[u & 3] = fma(g[u], yw[k + u], a4[u & 3]);
-  }
-  for (; k < np; ++k) a4[0] = fma(Gi[k * f], yw[k], a4[0]);
-  const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-  if (i < np) {
-    xp[col0 + i] = acc;
-    GD.wz[col0 + i] = acc / GD.D[col0 + i];
-  } else {
-    upd[S.upd_off[s] + i - np] = yi - acc;
-  }
-}
-
-// backward column group g of supernode s with the front vector [z ./ d; -x2] in vs (shared)
-__device__ __forceinline__ void warp_gbwd_v(const SymDev& S, const GDev& GD, int s, int g, const double* vs,
-                                            double* xp, double* x, int lane) {
-  const int f = (int)S.front[s], np = (int)S.ncol[s];
-  const int64_t col0 = S.col0[s];
-  const int c0 = 8 * g;
-  const int nc = min(8, np - c0);
-  const double* G = GD.g + GD.g_off[s];
-  double acc[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-  for (int r = (c0 & ~31) + lane; r < f; r += 32) {
-    const double v = vs[r];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] = fma(c < nc ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
-  }
-#pragma unroll
-  for (int o = 4; o >= 1; o >>= 1) {
-#pragma unroll
-    for (int k = 0; k < o; ++k) {
-      const bool hi = (lane & o) != 0;
-      const double send = hi ? acc[k] : acc[k + o];
-      const double recv = __shfl_xor_sync(0xffffffffu, send, o);
-      acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
-    }
-  }
-  double v = acc[0];
-  v += __shfl_xor_sync(0xffffffffu, v, 8);
-  v += __shfl_xor_sync(0xffffffffu, v, 16);
-  const int c = c0 + lane;
-  if (lane < 8 && c < np) {
-    xp[col0 + c] = v;
-    x[S.order[col0 + c]] = v;
-  }
-}
 
 // ---- static-operand prefetch (before the PDL wait) -------------------------
 // Everything a level task reads that the previous kernels of the solve do
@@ -600,109 +524,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_sub_bwd(SymDev S, GDev GD, co
   }
 }
 
-// Dataflow variant (RIGA_SUB_DATAFLOW=1): no barrier between local levels.
-// Warps claim the subtree's tiles in level order from a shared counter; a
-// tile waits (shared-memory spin) only until its own dependencies are done:
-// forward, every tile of each child supernode; backward, every tile of the
-// parent.  Per-supernode remaining-tile counters live in shared memory
-// (subtree supernodes are a contiguous postorder range [base, base + nsn)).
-// The arithmetic of each tile is the level-synchronous kernel's, so the
-// results are bit-identical.
-constexpr int kSubMaxSn = 2048;
-
-__device__ __forceinline__ void sub_wait_zero(const volatile int* c) {
-  while (*c != 0) __nanosleep(32);
-  __threadfence_block();
-}
-
-template <int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_sub_fwd_df(SymDev S, SolveDev T, GDev GD,
-                                                              const int32_t* __restrict__ sub_ptr, int SL,
-                                                              const double* __restrict__ b, double* xp, double* upd) {
-  constexpr int NW = NT / 32;
-  pdl_start();
-  __shared__ double y[NW * kGMaxNp];
-  __shared__ int cnt[kSubMaxSn];
-  __shared__ int next;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
-  const int t0 = p[0], t1 = p[SL];
-  if (t1 <= t0) return;
-  const int base = GD.tiles[t0].x;                // first postorder supernode: a leaf
-  const int nsn = GD.tiles[t1 - 1].x - base + 1;  // the subtree root is the last tile's supernode
-  for (int i = threadIdx.x; i < nsn; i += NT) cnt[i] = (int)((S.front[base + i] + 31) / 32);
-  if (threadIdx.x == 0) next = t0;
-  __syncthreads();
-  for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(&next, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= t1) break;
-    const int2 task = GD.tiles[t];
-    const int s = task.x;
-    for (int64_t q = S.child_ptr[s] + lane; q < S.child_ptr[s + 1]; q += 32)
-      sub_wait_zero(cnt + (S.child_list[q] - base));
-    __syncwarp();
-    __threadfence_block();
-    warp_gtile_fwd(S, T, GD, task, b, xp, upd, y + w * kGMaxNp, lane);
-    __syncwarp();
-    __threadfence_block();
-    if (lane == 0) atomicSub(cnt + (s - base), 1);
-  }
-}
-
-template <int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_sub_bwd_df(SymDev S, GDev GD, const int32_t* __restrict__ sub_ptr,
-                                                              int SL, const double* __restrict__ D, double* xp,
-                                                              double* x) {
-  pdl_start();
-  __shared__ int cnt[kSubMaxSn];
-  __shared__ int next;
-  const int lane = threadIdx.x & 31;
-  const int32_t* p = sub_ptr + blockIdx.x * (SL + 1);
-  const int t0 = p[0], t1 = p[SL];
-  if (t1 <= t0) return;
-  // tiles are stored level by level upwards: claim them from the top level down
-  int base = 0x7fffffff, root = -1;
-  for (int t = p[0] + lane; t < p[1]; t += 32) base = min(base, GD.tiles[t].x);
-  for (int o = 16; o >= 1; o >>= 1) base = min(base, __shfl_xor_sync(0xffffffffu, base, o));
-  root = GD.tiles[t1 - 1].x;
-  const int nsn = root - base + 1;
-  for (int i = threadIdx.x; i < nsn; i += NT) cnt[i] = (int)((S.ncol[base + i] + 7) / 8);
-  if (threadIdx.x == 0) next = 0;
-  __syncthreads();
-  for (;;) {
-    int c = 0;
-    if (lane == 0) c = atomicAdd(&next, 1);
-    c = __shfl_sync(0xffffffffu, c, 0);
-    if (c >= t1 - t0) break;
-    // c-th claim: local levels from the top, each level's tiles in stored order
-    int j = SL - 1, off = c;
-    while (off >= p[j + 1] - p[j]) {
-      off -= p[j + 1] - p[j];
-      --j;
-    }
-    const int2 task = GD.tiles[p[j] + off];
-    const int s = task.x;
-    const int par = S.sparent[s];
-    if (par >= base && par <= root) sub_wait_zero(cnt + (par - base));
-    __syncwarp();
-    __threadfence_block();
-    warp_gtile_bwd(S, GD, task, D, xp, x, lane);
-    __syncwarp();
-    __threadfence_block();
-    if (lane == 0) atomicSub(cnt + (s - base), 1);
-  }
-}
-
-static int sub_dataflow() {
-  static const int v = [] {
-    const char* e = getenv("RIGA_SUB_DATAFLOW");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 static int sub_threads() {
   static const int v = [] {
     const char* e = getenv("RIGA_SUB_THREADS");
@@ -744,30 +565,6 @@ __device__ __forceinline__ void k_rest_fwd_body(SymDev S, SolveDev T,
   for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
   const int2 task = tasks[ti];
   const int type = task.y >> 24, j = task.y & 0x00ffffff;
-  if (GT && type == kGSn) {
-    const int32_t* sn = GD.sn + task.x;
-    int off = 0;
-    for (int q = 0; q < j; ++q) {  // y1 of every supernode of the group, once
-      const int s = sn[q];
-      const int np = (int)S.ncol[s];
-      const int64_t col0 = S.col0[s];
-      for (int r = tid; r < np; r += blockDim.x) y[off + r] = gather_row(S, T, s, r, np, col0, b, upd);
-      off += np;
-    }
-    __syncthreads();
-    int tb = 0;
-    off = 0;
-    for (int q = 0; q < j; ++q) {
-      const int s = sn[q];
-      const int nt = (int)((S.front[s] + 31) / 32);
-      for (int t = (w - tb % kSolveWarps + kSolveWarps) % kSolveWarps; t < nt; t += kSolveWarps)
-        warp_gtile_fwd_y(S, T, GD, s, t, b, xp, upd, y + off, lane);
-      tb += nt;
-      off += (int)S.ncol[s];
-    }
-    __syncthreads();
-    continue;
-  }
   if (GT && type == kGTiles) {
     if (w < j) warp_gtile_fwd(S, T, GD, GD.tiles[task.x + w], b, xp, upd, y + w * kGMaxNp, lane);
     __syncwarp();
@@ -857,31 +654,6 @@ __device__ __forceinline__ void k_rest_bwd_body(SymDev S, SolveDev T,
   for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
   const int2 task = tasks[ti];
   const int type = task.y >> 24, bj = task.y & 0x00ffffff;
-  if (GT && type == kGSn) {
-    const int32_t* sn = GD.sn + task.x;
-    int off = 0;
-    for (int q = 0; q < bj; ++q) {  // front vectors [z ./ d; -x2] of the group, once
-      const int s = sn[q];
-      const int f = (int)S.front[s], np = (int)S.ncol[s];
-      const int64_t col0 = S.col0[s];
-      const int32_t* rows = S.rows + S.rows_off[s];
-      for (int r = tid; r < f; r += blockDim.x) y[off + r] = r < np ? GD.wz[col0 + r] : -xp[rows[r]];
-      off += f;
-    }
-    __syncthreads();
-    int gb = 0;
-    off = 0;
-    for (int q = 0; q < bj; ++q) {
-      const int s = sn[q];
-      const int ng = (int)((S.ncol[s] + 7) / 8);
-      for (int g = (w - gb % kSolveWarps + kSolveWarps) % kSolveWarps; g < ng; g += kSolveWarps)
-        warp_gbwd_v(S, GD, s, g, y + off, xp, x, lane);
-      gb += ng;
-      off += (int)S.front[s];
-    }
-    __syncthreads();
-    continue;
-  }
   if (GT && type == kGTiles) {
     if (w < bj) warp_gtile_bwd(S, GD, GD.tiles[task.x + w], D, xp, x, lane);
     __syncwarp();
@@ -1513,285 +1285,6 @@ __global__ void __launch_bounds__(256) k_inv_fix_bwd_apply(SymDev S, const int2*
 }
 
 // ---------------------------------------------------------------------------
-// Persistent phase-ordered solve (one kernel per sweep).
-//
-// The level-by-level launches above cost one kernel per level and sweep
-// (~40 per cfg3 solve); with 16 slice streams the device's grid-launch rate,
-// not HBM, caps the aggregate solve rate (measured: 16 k solves/s from 16 to
-// 32 streams at 30 % warp occupancy).  Here a sweep is ONE kernel: the same
-// tasks, in the same phase order (forward per level: inv(L11) rows of the
-// chain supernodes, then G tiles + UPD rows; backward per level: G column
-// groups + COLDOT, then inv(L11)^T rows), are handed out by an atomic
-// counter in order; a CTA that takes a task of phase p waits (acquire spin)
-// until every task of phase p - 1 has completed (release counter), which by
-// induction covers all earlier phases.  Tasks are taken in order, so a
-// waiting CTA only waits on tasks already held by running CTAs: no deadlock
-// for any grid size.  Dynamic vectors are read through L2 (ld.global.cg):
-// another SM wrote them inside this kernel.
-// ---------------------------------------------------------------------------
-enum { kPInvF = 1, kPGtF = 2, kPUpd = 3, kPGtB = 4, kPCol = 5, kPInvB = 6 };
-
-struct PDev {
-  const int4* tasks;   // (type, a, b, phase), phase order
-  int ntask;
-  const int* phase_cnt;
-  unsigned* ctr;       // [0] next task, [1 + p] completed tasks of phase p
-};
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ double p_gather(const SymDev& S, const SolveDev& T, int s, int64_t r, int64_t np,
-                                           int64_t col0, const double* b, const double* upd) {
-  double v = r < np ? __ldcg(b + (T.permuted ? col0 + r : S.order[col0 + r])) : 0.0;
-  const int64_t g = S.rows_off[s] + r;
-  for (int64_t q = T.gptr[g]; q < T.gptr[g + 1]; ++q) v += __ldcg(upd + T.gsrc[q]);
-  return v;
-}
-
-// forward G tile (s, t), one warp (as warp_gtile_fwd)
-__device__ __forceinline__ void p_gtile_fwd(const SymDev& S, const SolveDev& T, const GDev& GD, int2 task,
-                                            const double* b, double* xp, double* upd, double* yw, int lane) {
-  const int s = task.x;
-  const int f = (int)S.front[s], np = (int)S.ncol[s];
-  const int64_t col0 = S.col0[s];
-  const double* G = GD.g + GD.g_off[s];
-  for (int r = lane; r < np; r += 32) yw[r] = p_gather(S, T, s, r, np, col0, b, upd);
-  const int i = 32 * task.y + lane;
-  const double yi = (i >= np && i < f) ? p_gather(S, T, s, i, np, col0, b, upd) : 0.0;
-  __syncwarp();
-  if (i < f) {
-    double a4[4] = {0.0, 0.0, 0.0, 0.0};
-    const double* Gi = G + i;
-    int k = 0;
-    for (; k + 16 <= np; k += 16) {
-      double g[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) g[u] = Gi[(k + u) * f];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) a4[u & 3] = fma(g[u], yw[k + u], a4[u & 3]);
-    }
-    for (; k < np; ++k) a4[0] = fma(Gi[k * f], yw[k], a4[0]);
-    const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-    if (i < np) {
-      xp[col0 + i] = acc;
-      GD.wz[col0 + i] = acc / GD.D[col0 + i];
-    } else {
-      upd[S.upd_off[s] + i - np] = yi - acc;
-    }
-  }
-  __syncwarp();
-}
-
-// backward G column group (s, g), one warp (as warp_gtile_bwd)
-__device__ __forceinline__ void p_gtile_bwd(const SymDev& S, const GDev& GD, int2 task, double* xp, double* x,
-                                            int lane) {
-  const int s = task.x;
-  const int f = (int)S.front[s], np = (int)S.ncol[s];
-  const int64_t col0 = S.col0[s];
-  const int c0 = 8 * task.y;
-  const double* G = GD.g + GD.g_off[s];
-  const int32_t* rows = S.rows + S.rows_off[s];
-  const int nc = min(8, np - c0);
-  double acc[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-  for (int r = (c0 & ~31) + lane; r < f; r += 32) {
-    const double v = r < np ? __ldcg(GD.wz + col0 + r) : -__ldcg(xp + rows[r]);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] = fma(c < nc ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
-  }
-#pragma unroll
-  for (int o = 4; o >= 1; o >>= 1) {
-#pragma unroll
-    for (int k = 0; k < o; ++k) {
-      const bool hi = (lane & o) != 0;
-      const double send = hi ? acc[k] : acc[k + o];
-      const double recv = __shfl_xor_sync(0xffffffffu, send, o);
-      acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
-    }
-  }
-  double v = acc[0];
-  v += __shfl_xor_sync(0xffffffffu, v, 8);
-  v += __shfl_xor_sync(0xffffffffu, v, 16);
-  const int c = c0 + lane;
-  if (lane < 8 && c < np) {
-    xp[col0 + c] = v;
-    x[S.order[col0 + c]] = v;
-  }
-}
-
-template <bool FWD>
-__global__ void __launch_bounds__(kSolveThreads, 2) k_solve_pers(SymDev S, SolveDev T, GDev GD, PDev PD,
-                                                                 const double* __restrict__ panel,
-                                                                 const int64_t* __restrict__ inv_off,
-                                                                 const double* __restrict__ linv,
-                                                                 const double* __restrict__ D,
-                                                                 const double* b, double* xp, double* upd,
-                                                                 double* cvec, double* x) {
-  pdl_start();
-  extern __shared__ __align__(16) double y[];
-  __shared__ double part[kSolveWarps][32];
-  __shared__ int s_task;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (;;) {
-    if (tid == 0) s_task = (int)atomicAdd(&PD.ctr[0], 1u);
-    __syncthreads();
-    const int t = s_task;
-    __syncthreads();
-    if (t >= PD.ntask) break;
-    const int4 tk = PD.tasks[t];
-    const int ph = tk.w;
-    if (tid == 0 && ph > 0) {
-      const unsigned need = (unsigned)PD.phase_cnt[ph - 1];
-      while (ld_acquire_u32(&PD.ctr[ph]) < need) __nanosleep(32);
-    }
-    __syncthreads();
-    if (FWD) {
-      if (tk.x == kPGtF) {
-        if (w < tk.z) p_gtile_fwd(S, T, GD, GD.tiles[tk.y + w], b, xp, upd, y + w * kGMaxNp, lane);
-      } else if (tk.x == kPInvF) {
-        // z rows [32 t, 32 t + 32) of chain supernode s = inv(L11) y1 (as k_inv_fwd)
-        const int s = tk.y;
-        const int np = (int)S.ncol[s];
-        const int64_t col0 = S.col0[s];
-        const int r0 = 32 * tk.z, r1 = min(np, r0 + 32);
-        for (int k = tid; k < r1; k += kSolveThreads) y[k] = p_gather(S, T, s, k, np, col0, b, upd);
-        __syncthreads();
-        const int chunk = (r1 + 7) / 8;
-        const int k0 = w * chunk, k1 = min(r1, k0 + chunk);
-        const double* A = linv + inv_off[s] + r0 + lane;
-        double acc = 0.0;
-        if (r0 + lane < r1) {
-#pragma unroll 4
-          for (int k = k0; k < k1; ++k) acc = fma(A[(int64_t)k * np], y[k], acc);
-        }
-        part[w][lane] = acc;
-        __syncthreads();
-        if (w == 0 && r0 + lane < r1) {
-          double z = 0.0;
-#pragma unroll
-          for (int q = 0; q < kSolveWarps; ++q) z += part[q][lane];
-          const int64_t g = col0 + r0 + lane;
-          xp[g] = z;
-          cvec[g] = z / D[g];
-        }
-      } else {  // kPUpd: update rows [np + 32 j, ...) of chain supernode s minus L21 z
-        const int s = tk.y, j = tk.z;
-        const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
-        const double* P = panel + S.panel_off[s];
-        const int nbp = (int)((np + 31) / 32);
-        const int64_t r0 = np + 32 * (int64_t)j, r1 = imin(r0 + 32, f), r = r0 + lane;
-        const bool in = r < r1;
-        double acc = 0.0;
-        for (int cb = w; cb < nbp; cb += kSolveWarps) {
-          const int64_t c0 = 32 * (int64_t)cb;
-          const int nc = (int)imin(32, np - c0);
-          const double zl = lane < nc ? __ldcg(xp + col0 + c0 + lane) : 0.0;
-#pragma unroll 8
-          for (int k = 0; k < 32; ++k) {
-            const double l = (in && k < nc) ? P[(c0 + k) * f + r] : 0.0;
-            acc = fma(l, __shfl_sync(0xffffffffu, zl, k), acc);
-          }
-        }
-        part[w][lane] = acc;
-        __syncthreads();
-        if (w == 0 && in) {
-          double v = p_gather(S, T, s, r, np, col0, b, upd);
-#pragma unroll
-          for (int q = 0; q < kSolveWarps; ++q) v -= part[q][lane];
-          upd[S.upd_off[s] + r - np] = v;
-        }
-      }
-    } else {
-      if (tk.x == kPGtB) {
-        if (w < tk.z) p_gtile_bwd(S, GD, GD.tiles[tk.y + w], xp, x, lane);
-      } else if (tk.x == kPCol) {
-        // cvec[col] -= sum_{update rows r} L[r][col] x[rows[r]], col in block bj (as kColdot)
-        const int s = tk.y, bj = tk.z;
-        const int64_t f = S.front[s], np = S.ncol[s], col0 = S.col0[s];
-        const double* P = panel + S.panel_off[s];
-        const int32_t* rows = S.rows + S.rows_off[s];
-        const int64_t c0 = 32 * (int64_t)bj + 8 * (w & 3);
-        double acc[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-        for (int64_t r = np + 32 * (w >> 2) + lane; r < f; r += 64) {
-          const double xv = __ldcg(xp + rows[r]);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) acc[c] = fma(c0 + c < np ? P[(c0 + c) * f + r] : 0.0, xv, acc[c]);
-        }
-#pragma unroll
-        for (int o = 4; o >= 1; o >>= 1) {
-#pragma unroll
-          for (int k = 0; k < o; ++k) {
-            const bool hi = (lane & o) != 0;
-            const double send = hi ? acc[k] : acc[k + o];
-            const double recv = __shfl_xor_sync(0xffffffffu, send, o);
-            acc[k] = (hi ? acc[k + o] : acc[k]) + recv;
-          }
-        }
-        double v = acc[0];
-        v += __shfl_xor_sync(0xffffffffu, v, 8);
-        v += __shfl_xor_sync(0xffffffffu, v, 16);
-        if (lane < 8) part[w][lane] = v;
-        __syncthreads();
-        if (w == 0) {
-          const int g = lane >> 3, e = lane & 7;
-          const int64_t col = 32 * (int64_t)bj + lane;
-          if (col < np) {
-            const double tt = part[g][e] + part[g + 4][e];
-            double* c = cvec + col0 + col;
-            *c = __ldcg(c) - tt;
-          }
-        }
-      } else {  // kPInvB: x1[r] = sum_{k >= r} inv(L11)(k, r) w[k], warp per row
-        const int s = tk.y;
-        const int np = (int)S.ncol[s];
-        const int r = 8 * tk.z + w;
-        if (r < np) {
-          const int64_t col0 = S.col0[s];
-          const double* A = linv + inv_off[s] + (int64_t)r * np;
-          const double* wv = cvec + col0;
-          double acc = 0.0;
-#pragma unroll 4
-          for (int k = r + lane; k < np; k += 32) acc = fma(A[k], __ldcg(wv + k), acc);
-          acc = warp_sum(acc);
-          if (lane == 0) {
-            xp[col0 + r] = acc;
-            x[S.order[col0 + r]] = acc;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(&PD.ctr[1 + ph], 1u);
-    }
-  }
-}
-
-// L2 warm-up: bulk-prefetch the factor panels (contiguous) so the level
-// kernels' latency-bound loads hit L2 (the factor of a 2D config fits in the
-// 126 MB L2, but the Gram-Schmidt traffic of the previous step evicts it)
-__global__ void k_prefetch_l2(const double* __restrict__ p, int64_t bytes) {
-  pdl_start();
-  const int64_t chunk = 32768;
-  for (int64_t off = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * chunk; off < bytes;
-       off += (int64_t)gridDim.x * blockDim.x * chunk) {
-    const int64_t len = imin(chunk, bytes - off) & ~int64_t(15);
-    if (len > 0)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(p) + off),
-                   "r"((unsigned)len)
-                   : "memory");
-  }
-}
-
-// ---------------------------------------------------------------------------
 // host: per-level task lists, pull map
 // ---------------------------------------------------------------------------
 static int env_flag(const char* name, int dflt) {
@@ -1813,10 +1306,8 @@ int build_solve_plan(riga_symbolic* sym) {
   L = SolvePlanHost();
   // TMA staging of small panels (a 229 KB block per 8 warps) only pays for a
   // solve running alone; concurrent slice streams want small blocks that
-  // co-reside, so it is opt-in (RIGA_WARP_STAGE=1), as is the per-solve L2
-  // prefetch of the factor (RIGA_L2_PREFETCH=1)
+  // co-reside, so it is opt-in (RIGA_WARP_STAGE=1)
   L.warp_stage = env_flag("RIGA_WARP_STAGE", 0);
-  L.l2_prefetch = env_flag("RIGA_L2_PREFETCH", 0);
   // chain supernodes through inv(L11) (default) or the serial chain kernels
   L.chain_inv = env_flag("RIGA_CHAIN_INV", 1);
   // one local refinement step after every inv(L11) application (backward stability; RIGA_INV_FIX=0 off)
@@ -1824,9 +1315,6 @@ int build_solve_plan(riga_symbolic* sym) {
   // small supernodes through G = [inv(L11); L21 inv(L11)] (default) or substitution
   L.small_g = env_flag("RIGA_SMALL_G", 1);
   L.occ = env_flag("RIGA_REST_OCC", 4);  // CTAs per SM the G-mode level kernels are register-bounded for
-  // G supernodes as whole-supernode group tasks (shared gathers; opt-in: the
-  // gather -> barrier -> mat-vec chain is longer than the redundant gathers save)
-  L.g_groups = env_flag("RIGA_G_GROUPS", 0);
   L.rest_cap = env_flag("RIGA_REST_CAP", 1 << 30);  // CTAs per level launch (grid-stride over the tasks)
   L.g_off.assign(ns, -1);
   L.inv_off.assign(ns, -1);
@@ -1922,64 +1410,7 @@ int build_solve_plan(riga_symbolic* sym) {
         L.g_total += h.front[s] * h.ncol[s];
       }
     }
-    if (L.small_g && L.g_groups) {
-      // bit 0: forward groups, bit 1: backward groups (the other direction keeps warp tiles)
-      std::vector<I2> tf, tb;
-      for (int32_t s : small) {
-        for (int32_t t = 0; t < (int32_t)((h.front[s] + 31) / 32); ++t) tf.push_back({s, t});
-        for (int32_t g = 0; g < (int32_t)((h.ncol[s] + 7) / 8); ++g) tb.push_back({s, g});
-      }
-      if (!(L.g_groups & 1)) {
-        for (size_t q = 0; q < tf.size(); q += kSolveWarps) {
-          const int cnt = (int)std::min<size_t>(kSolveWarps, tf.size() - q);
-          L.fwd.push_back({(int32_t)(L.gfwd.size() + q), code(kGTiles, cnt)});
-        }
-        L.gfwd.insert(L.gfwd.end(), tf.begin(), tf.end());
-      }
-      if (!(L.g_groups & 2)) {
-        for (size_t q = 0; q < tb.size(); q += kSolveWarps) {
-          const int cnt = (int)std::min<size_t>(kSolveWarps, tb.size() - q);
-          L.bwd.push_back({(int32_t)(L.gbwd.size() + q), code(kGTiles, cnt)});
-        }
-        L.gbwd.insert(L.gbwd.end(), tb.begin(), tb.end());
-      }
-      // small supernodes through G, one CTA task per group of whole
-      // supernodes (shared gathers): forward groups of <= 8 row tiles,
-      // backward groups of <= 8 column groups and <= kGrpMaxF front rows
-      auto flush = [&](std::vector<int32_t>& cur, std::vector<int32_t>& dst, std::vector<I2>& tasks) {
-        if (cur.empty()) return;
-        tasks.push_back({(int32_t)dst.size(), code(kGSn, (int)cur.size())});
-        dst.insert(dst.end(), cur.begin(), cur.end());
-        cur.clear();
-      };
-      std::vector<int32_t> cur;
-      int64_t units = 0, rowsum = 0;
-      for (int32_t s : (L.g_groups & 1) ? small : std::vector<int32_t>()) {
-        const int64_t nt = (h.front[s] + 31) / 32;
-        if (!cur.empty() && units + nt > kSolveWarps) {
-          flush(cur, L.gsn_f, L.fwd);
-          units = rowsum = 0;
-        }
-        cur.push_back(s);
-        units += nt;
-        rowsum += h.ncol[s];
-        smf = std::max<int64_t>(smf, rowsum);
-      }
-      flush(cur, L.gsn_f, L.fwd);
-      units = rowsum = 0;
-      for (int32_t s : (L.g_groups & 2) ? small : std::vector<int32_t>()) {
-        const int64_t ng = (h.ncol[s] + 7) / 8;
-        if (!cur.empty() && (units + ng > kSolveWarps || rowsum + h.front[s] > kGrpMaxF)) {
-          flush(cur, L.gsn_b, L.bwd);
-          units = rowsum = 0;
-        }
-        cur.push_back(s);
-        units += ng;
-        rowsum += h.front[s];
-        smb = std::max<int64_t>(smb, rowsum);
-      }
-      flush(cur, L.gsn_b, L.bwd);
-    } else if (L.small_g) {
+    if (L.small_g) {
       // small supernodes through G: warp tasks (32-row tiles forward,
       // 8-column groups backward), 8 per CTA
       std::vector<I2> tf, tb;
@@ -2047,47 +1478,6 @@ int build_solve_plan(riga_symbolic* sym) {
     L.dbl_tmax = std::max(L.dbl_tmax, tt);
   }
   L.dbl_ptr.push_back((int64_t)L.dbl_tasks.size());
-  // persistent solve: the level lists above flattened into phases
-  L.pers = env_flag("RIGA_SOLVE_PERSIST", 0) && L.small_g && !L.g_groups && L.chain_inv && L.sub_levels == 0 &&
-           !L.warp_stage;
-  L.pers_ctas = env_flag("RIGA_SOLVE_CTAS", 2 * 148);
-  if (L.pers) {
-    int phase = 0;
-    auto push = [](std::vector<int>& v, int ty, int a, int bb, int ph) {
-      v.push_back(ty); v.push_back(a); v.push_back(bb); v.push_back(ph);
-    };
-    for (int64_t l = 0; l < h.nlevels; ++l) {
-      if (L.ifwd_ptr[l + 1] > L.ifwd_ptr[l]) {
-        for (int64_t q = L.ifwd_ptr[l]; q < L.ifwd_ptr[l + 1]; ++q) push(L.ptf, kPInvF, L.ifwd[q].x, L.ifwd[q].y, phase);
-        L.pcf.push_back((int)(L.ifwd_ptr[l + 1] - L.ifwd_ptr[l]));
-        ++phase;
-      }
-      if (L.fwd_ptr[l + 1] > L.fwd_ptr[l]) {
-        for (int64_t q = L.fwd_ptr[l]; q < L.fwd_ptr[l + 1]; ++q) {
-          const int ty = L.fwd[q].y >> 24, j = L.fwd[q].y & 0x00ffffff;
-          push(L.ptf, ty == kGTiles ? kPGtF : kPUpd, L.fwd[q].x, j, phase);
-        }
-        L.pcf.push_back((int)(L.fwd_ptr[l + 1] - L.fwd_ptr[l]));
-        ++phase;
-      }
-    }
-    phase = 0;
-    for (int64_t l = h.nlevels - 1; l >= 0; --l) {
-      if (L.bwd_ptr[l + 1] > L.bwd_ptr[l]) {
-        for (int64_t q = L.bwd_ptr[l]; q < L.bwd_ptr[l + 1]; ++q) {
-          const int ty = L.bwd[q].y >> 24, j = L.bwd[q].y & 0x00ffffff;
-          push(L.ptb, ty == kGTiles ? kPGtB : kPCol, L.bwd[q].x, j, phase);
-        }
-        L.pcb.push_back((int)(L.bwd_ptr[l + 1] - L.bwd_ptr[l]));
-        ++phase;
-      }
-      if (L.ibwd_ptr[l + 1] > L.ibwd_ptr[l]) {
-        for (int64_t q = L.ibwd_ptr[l]; q < L.ibwd_ptr[l + 1]; ++q) push(L.ptb, kPInvB, L.ibwd[q].x, L.ibwd[q].y, phase);
-        L.pcb.push_back((int)(L.ibwd_ptr[l + 1] - L.ibwd_ptr[l]));
-        ++phase;
-      }
-    }
-  }
   // pull map: front position -> sources in the update-vector buffer
   const int64_t nfront = h.rows_off[ns];
   std::vector<int64_t> cnt(nfront + 1, 0);
@@ -2124,8 +1514,6 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
   }
   RIGA_TRY(sym->d_gptr.upload(L.gptr.data(), L.gptr.size(), s));
   if (L.small_g && L.g_total) {
-    if (!L.gsn_f.empty()) RIGA_TRY(sym->d_gsn_f.upload(L.gsn_f.data(), L.gsn_f.size(), s));
-    if (!L.gsn_b.empty()) RIGA_TRY(sym->d_gsn_b.upload(L.gsn_b.data(), L.gsn_b.size(), s));
     RIGA_TRY(sym->d_g_off.upload(L.g_off.data(), L.g_off.size(), s));
     RIGA_TRY(sym->d_gfwd.upload(L.gfwd.data(), L.gfwd.size(), s));
     RIGA_TRY(sym->d_gbwd.upload(L.gbwd.data(), L.gbwd.size(), s));
@@ -2140,59 +1528,11 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
       RIGA_TRY(sym->d_dbl_toff.upload(L.dbl_toff.data(), L.dbl_toff.size(), s));
     }
   }
-  if (L.pers) {
-    RIGA_TRY(sym->d_ptf.upload(L.ptf.data(), std::max<size_t>(L.ptf.size(), 4), s));
-    RIGA_TRY(sym->d_ptb.upload(L.ptb.data(), std::max<size_t>(L.ptb.size(), 4), s));
-    RIGA_TRY(sym->d_pcf.upload(L.pcf.data(), std::max<size_t>(L.pcf.size(), 1), s));
-    RIGA_TRY(sym->d_pcb.upload(L.pcb.data(), std::max<size_t>(L.pcb.size(), 1), s));
-  }
   if (L.gsrc.empty())
     RIGA_TRY(sym->d_gsrc.alloc(1, s));
   else
     RIGA_TRY(sym->d_gsrc.upload(L.gsrc.data(), L.gsrc.size(), s));
   return RIGA_OK;
-}
-
-// ---- lockstep group solve: the level kernels with a member dimension -------
-template <bool GT, int MINB = 4>
-__global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_fwd_g(const SlicePtrs* tab, SymDev S, SolveDev T,
-                                                                            const int2* __restrict__ tasks, int ntask,
-                                                                            const int32_t* __restrict__ wholes, GDev GDs) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  if (P.st->stop) return;
-  GDev GD = GDs;
-  GD.g = P.gsmall;
-  GD.D = P.D;
-  GD.wz = P.cvec;
-  k_rest_fwd_body<GT, MINB>(S, T, tasks, ntask, wholes, P.panel, P.bp, P.xperm, P.upd, 0, GD);
-}
-
-template <bool GT, int MINB = 4>
-__global__ void __launch_bounds__(kSolveThreads, GT ? MINB : 2) k_rest_bwd_g(const SlicePtrs* tab, SymDev S, SolveDev T,
-                                                                            const int2* __restrict__ tasks, int ntask,
-                                                                            const int32_t* __restrict__ wholes, GDev GDs) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  if (P.st->stop) return;
-  GDev GD = GDs;
-  GD.g = P.gsmall;
-  GD.D = P.D;
-  GD.wz = P.cvec;
-  k_rest_bwd_body<GT, MINB>(S, T, tasks, ntask, wholes, P.panel, P.D, P.xperm, P.cvec, P.w, 0, 1, GD);
-}
-
-__global__ void __launch_bounds__(256) k_inv_fwd_g(const SlicePtrs* tab, SymDev S, SolveDev T,
-                                                   const int2* __restrict__ tasks,
-                                                   const int64_t* __restrict__ inv_off) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  if (P.st->stop) return;
-  k_inv_fwd_body(S, T, tasks, inv_off, P.linv, P.D, P.bp, P.xperm, P.upd, P.cvec);
-}
-
-__global__ void __launch_bounds__(256) k_inv_bwd_g(const SlicePtrs* tab, SymDev S, const int2* __restrict__ tasks,
-                                                   const int64_t* __restrict__ inv_off) {
-  const SlicePtrs& P = tab[blockIdx.z];
-  if (P.st->stop) return;
-  k_inv_bwd_body(S, tasks, inv_off, P.linv, P.cvec, P.xperm, P.w);
 }
 
 template <typename K>
@@ -2223,11 +1563,6 @@ static int set_solve_attrs() {
   RIGA_TRY(raise_smem(k_inv_fwd, maxsm));
   RIGA_TRY(raise_smem(k_inv_fix_fwd_res, maxsm));
   RIGA_TRY(raise_smem(k_inv_fix_fwd_apply, maxsm));
-  RIGA_TRY(raise_smem(k_rest_fwd_g<true, 4>, maxsm));
-  RIGA_TRY(raise_smem(k_rest_bwd_g<true, 4>, maxsm));
-  RIGA_TRY(raise_smem(k_inv_fwd_g, maxsm));
-  RIGA_TRY(raise_smem(k_solve_pers<true>, maxsm));
-  RIGA_TRY(raise_smem(k_solve_pers<false>, maxsm));
   done = true;
   return RIGA_OK;
 }
@@ -2238,7 +1573,6 @@ int build_chain_inverse(riga_factor* F, cudaStream_t st) {
   riga_symbolic* sym = F->sym;
   const SolvePlanHost& L = sym->sp;
   SymDev S = sym->dev();
-  if (L.pers && !F->pctr.p) RIGA_TRY(F->pctr.alloc(2 + L.pcf.size() + L.pcb.size(), st));
   if (L.small_g && L.g_total) {
     if (!F->gsmall.p) RIGA_TRY(F->gsmall.alloc(L.g_total, st));
     const int nw = (int)L.wholes.size();
@@ -2287,52 +1621,6 @@ int build_chain_inverse(riga_factor* F, cudaStream_t st) {
   return RIGA_OK;
 }
 
-int factor_solve_group(riga_symbolic* sym, const SlicePtrs* tab, int B, cudaStream_t st) {
-  const SymbolicHost& h = sym->h;
-  const SolvePlanHost& L = sym->sp;
-  RIGA_CHECK_ARG(L.small_g && L.g_total && L.chain_inv && !L.sub_levels && !L.g_groups && !L.warp_stage,
-                 "lockstep groups need the default solve plan (G mode, chain inverses)");
-  RIGA_TRY(set_solve_attrs());
-  SymDev S = sym->dev();
-  SolveDev T{sym->d_gptr.p, sym->d_gsrc.p, 1};
-  const GDev GDf{nullptr, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gfwd.p), 1, nullptr,
-                 sym->d_gsn_f.p, nullptr};
-  const GDev GDb{nullptr, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gbwd.p), 1, nullptr,
-                 sym->d_gsn_b.p, nullptr};
-  const int2* tf = reinterpret_cast<const int2*>(sym->d_tfwd.p);
-  const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
-  const unsigned zb = (unsigned)B;
-  for (int64_t l = 0; l < h.nlevels; ++l) {
-    const int ni = (int)(L.ifwd_ptr[l + 1] - L.ifwd_ptr[l]);
-    if (ni) {
-      k_inv_fwd_g<<<dim3(ni, 1, zb), 256, L.ifwd_smem[l], st>>>(
-          tab, S, T, reinterpret_cast<const int2*>(sym->d_ifwd.p) + L.ifwd_ptr[l], sym->d_inv_off.p);
-      count_launch();
-    }
-    const int nt = (int)(L.fwd_ptr[l + 1] - L.fwd_ptr[l]);
-    if (nt) {
-      k_rest_fwd_g<true, 4><<<dim3(nt, 1, zb), kSolveThreads, L.fwd_smem[l], st>>>(tab, S, T, tf + L.fwd_ptr[l], nt,
-                                                                                 sym->d_wholes.p, GDf);
-      count_launch();
-    }
-  }
-  for (int64_t l = h.nlevels - 1; l >= 0; --l) {
-    const int nt = (int)(L.bwd_ptr[l + 1] - L.bwd_ptr[l]);
-    if (nt) {
-      k_rest_bwd_g<true, 4><<<dim3(nt, 1, zb), kSolveThreads, L.bwd_smem[l], st>>>(tab, S, T, tb + L.bwd_ptr[l], nt,
-                                                                                 sym->d_wholes.p, GDb);
-      count_launch();
-    }
-    const int ni = (int)(L.ibwd_ptr[l + 1] - L.ibwd_ptr[l]);
-    if (ni) {
-      k_inv_bwd_g<<<dim3(ni, 1, zb), 256, 0, st>>>(tab, S, reinterpret_cast<const int2*>(sym->d_ibwd.p) + L.ibwd_ptr[l],
-                                                   sym->d_inv_off.p);
-      count_launch();
-    }
-  }
-  RIGA_CUDA(cudaGetLastError());
-  return RIGA_OK;
-}
 
 }  // namespace riga
 
@@ -2354,43 +1642,16 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   SolveDev T{sym->d_gptr.p, sym->d_gsrc.p, b_permuted ? 1 : 0};
   const int gon = L.small_g && L.g_total ? 1 : 0;
   const GDev GDf{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gfwd.p), gon, F->D.p,
-                 sym->d_gsn_f.p, F->cvec.p};
+                 F->cvec.p};
   const GDev GDb{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gbwd.p), gon, F->D.p,
-                 sym->d_gsn_b.p, F->cvec.p};
+                 F->cvec.p};
   const int2* tf = reinterpret_cast<const int2*>(sym->d_tfwd.p);
   const int2* tb = reinterpret_cast<const int2*>(sym->d_tbwd.p);
-  if (L.pers && gon) {
-    const int nf = (int)L.pcf.size(), nb = (int)L.pcb.size();
-    const int64_t nctr = 2 + nf + nb;
-    RIGA_CHECK_ARG(F->pctr.p && (int64_t)F->pctr.n >= nctr, "persistent-solve counters not allocated");
-    RIGA_CUDA(cudaMemsetAsync(F->pctr.p, 0, nctr * sizeof(unsigned), st));
-    int64_t maxnp = 0;
-    for (int32_t c : L.chains) maxnp = std::max<int64_t>(maxnp, h.ncol[c]);
-    const size_t smem = 8 * (size_t)std::max<int64_t>(kSolveWarps * kGMaxNp, maxnp);
-    const PDev pf{reinterpret_cast<const int4*>(sym->d_ptf.p), (int)(L.ptf.size() / 4), sym->d_pcf.p, F->pctr.p};
-    const PDev pb{reinterpret_cast<const int4*>(sym->d_ptb.p), (int)(L.ptb.size() / 4), sym->d_pcb.p,
-                  F->pctr.p + 1 + nf};
-    const int gf = std::max(1, std::min(L.pers_ctas, pf.ntask)), gb = std::max(1, std::min(L.pers_ctas, pb.ntask));
-    RIGA_CUDA(launch(k_solve_pers<true>, gf, kSolveThreads, smem, st, S, T, GDf, pf, F->panel.p, sym->d_inv_off.p,
-                     F->linv.p, F->D.p, b, F->xperm.p, F->upd.p, F->cvec.p, x));
-    RIGA_CUDA(launch(k_solve_pers<false>, gb, kSolveThreads, smem, st, S, T, GDb, pb, F->panel.p, sym->d_inv_off.p,
-                     F->linv.p, F->D.p, b, F->xperm.p, F->upd.p, F->cvec.p, x));
-    count_launch(2);
-    return RIGA_OK;
-  }
-  const int64_t pbytes = h.panel_total * 8;
-  if (L.l2_prefetch && pbytes <= kPrefetchMaxBytes) {
-    RIGA_CUDA(launch(k_prefetch_l2, (unsigned)std::min<int64_t>(148, (pbytes / 32768 + 255) / 256 + 1), 256, 0, st, F->panel.p,
-                                                                                                   pbytes));
-    count_launch();
-  }
   if (L.nsub && gon) {
     const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_ftiles.p), 1, F->D.p,
-                  nullptr, F->cvec.p};
+                  F->cvec.p};
     const int nt = sub_threads();
-    const bool df = sub_dataflow() && L.sub_maxsn <= kSubMaxSn;
-    RIGA_CUDA(launch(df ? (nt == 1024 ? k_sub_fwd_df<1024> : nt == 512 ? k_sub_fwd_df<512> : k_sub_fwd_df<256>)
-                        : (nt == 1024 ? k_sub_fwd<1024> : nt == 512 ? k_sub_fwd<512> : k_sub_fwd<256>),
+    RIGA_CUDA(launch(nt == 1024 ? k_sub_fwd<1024> : nt == 512 ? k_sub_fwd<512> : k_sub_fwd<256>,
                      (unsigned)L.nsub, nt, 0,
                      st, S, T, Gs, sym->d_sub_fptr.p, L.sub_levels, b, F->xperm.p,
                                                           F->upd.p));
@@ -2456,11 +1717,9 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   }
   if (L.nsub && gon) {
     const GDev Gs{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_sub_btiles.p), 1, F->D.p,
-                  nullptr, F->cvec.p};
+                  F->cvec.p};
     const int nt = sub_threads();
-    const bool df = sub_dataflow() && L.sub_maxsn <= kSubMaxSn;
-    RIGA_CUDA(launch(df ? (nt == 1024 ? k_sub_bwd_df<1024> : nt == 512 ? k_sub_bwd_df<512> : k_sub_bwd_df<256>)
-                        : (nt == 1024 ? k_sub_bwd<1024> : nt == 512 ? k_sub_bwd<512> : k_sub_bwd<256>),
+    RIGA_CUDA(launch(nt == 1024 ? k_sub_bwd<1024> : nt == 512 ? k_sub_bwd<512> : k_sub_bwd<256>,
                      (unsigned)L.nsub, nt, 0,
                      st, S, Gs, sym->d_sub_bptr.p, L.sub_levels, F->D.p,
                                                           F->xperm.p, x));

@@ -237,39 +237,6 @@ __global__ void k_kron_axis(int64_t n, int64_t nax, int64_t stride, const int64_
   k_kron_axis_body(n, nax, stride, rp, ci, m, in, out);
 }
 
-// lockstep group: z = 2 member + which; which 0: vt -> mvt (scratch kt1, kt2),
-// which 1: r -> Mr (scratch ks1, ks2); axis t of d
-__global__ void k_kron_axis_g(const SlicePtrs* tab, int t, int d, int64_t n, int64_t nax, int64_t stride,
-                              const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                              const double* __restrict__ m) {
-  const SlicePtrs& P = tab[blockIdx.z >> 1];
-  if (P.st->stop) return;
-  const int which = blockIdx.z & 1;
-  const double* x = which ? P.r : P.vt;
-  double* y = which ? P.Mr : P.mvt;
-  double* t1 = which ? P.ks1 : P.kt1;
-  double* t2 = which ? P.ks2 : P.kt2;
-  const double* in = t == 0 ? x : ((t - 1) % 2 == 0 ? t1 : t2);
-  double* out = t == d - 1 ? y : (t % 2 == 0 ? t1 : t2);
-  k_kron_axis_body(n, nax, stride, rp, ci, m, in, out);
-}
-
-int kron_mass_group(riga_system* sys, cudaStream_t s, const SlicePtrs* tab, int B) {
-  const int d = sys->kdim;
-  RIGA_CHECK_ARG(d > 0, "lockstep groups need the Kronecker mass factors");
-  const int64_t n = sys->n;
-  int64_t stride = 1;
-  for (int t = 0; t < d; ++t) {
-    const KronAxis& a = sys->kax[t];
-    k_kron_axis_g<<<dim3((unsigned)((n + 255) / 256), 1, (unsigned)(2 * B)), 256, 0, s>>>(
-        tab, t, d, n, a.n, stride, a.rp.p, a.ci.p, a.m.p);
-    count_launch();
-    stride *= a.n;
-  }
-  RIGA_CUDA(cudaGetLastError());
-  return RIGA_OK;
-}
-
 int kron_mass_apply(riga_system* sys, cudaStream_t s, const double* x, double* y, double* t1, double* t2) {
   const int d = sys->kdim;
   const int64_t n = sys->n;

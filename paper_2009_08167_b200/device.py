@@ -40,15 +40,6 @@ class Context:
     def synchronize(self):
         _lib.check(_lib.lib().riga_ctx_synchronize(self.handle))
 
-    def run_stream(self, high: bool) -> int:
-        """Raw handle of this context's side stream for Lanczos step replays at the high (one level above the
-        lowest) or lowest stream priority; created once per context."""
-        rs = self.__dict__.setdefault("_runs", {})
-        if high not in rs:
-            least, _ = torch.cuda.Stream.priority_range()
-            rs[high] = torch.cuda.Stream(device=self.device, priority=least - 1 if high else least)
-        return rs[high].cuda_stream
-
     def __enter__(self):
         self._prev = getattr(_tls, "ctx", None)
         _tls.ctx = self

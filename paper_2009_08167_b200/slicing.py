@@ -205,35 +205,6 @@ def _priorities(work: list) -> list:
     return pr
 
 
-class _DynPriority:
-    """Per-extend stream priority by estimated remaining work (RIGA_DYN_PRIO=1).
-
-    Before each extend a slice reports the eigenpairs it still needs and its solves per locked pair so far;
-    the half of the running slices with the most remaining solves replays its steps on a high-priority
-    stream, the rest on a low-priority one.  A slice that converges slowly (more restarts than its peers)
-    moves up instead of becoming a tail that runs alone at low concurrency."""
-
-    def __init__(self, always_low: bool = False):
-        self.lock = threading.Lock()
-        self.rem = {}
-        self.always_low = always_low
-
-    def pick(self, key, remaining: int, solves: int, found: int) -> bool:
-        if self.always_low:
-            return False
-        per_pair = solves / found if found > 0 else 6.0
-        r = max(remaining, 0) * per_pair
-        with self.lock:
-            self.rem[key] = (r, key)
-            mine = self.rem[key]
-            ahead = sum(1 for v in self.rem.values() if v > mine)
-            return ahead < max(1, len(self.rem) // 2)
-
-    def done(self, key) -> None:
-        with self.lock:
-            self.rem.pop(key, None)
-
-
 _sync_mode_set: set = set()
 
 
@@ -449,24 +420,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     # one slice per stream: stream priorities by expected work; otherwise a
     # shared queue (largest first) on default-priority streams
     prio = _priorities([int(expected[k]) for k in order]) if one_per_thread else [0] * len(order)
-    dyn = None
-    dyn_mode = os.environ.get("RIGA_DYN_PRIO", "0")
-    if one_per_thread and nthreads > 1 and dyn_mode in ("1", "2"):
-        # extends replay on side streams; the slice streams themselves (locking, lifts, restarts) run high.
-        # mode 1: extends high or low by remaining work; mode 2: extends always low
-        dyn = _DynPriority(always_low=dyn_mode == "2")
-        least, _ = torch.cuda.Stream.priority_range()
-        prio = [least - 1] * len(order)
-
-    # lockstep group (RIGA_GROUP=1): the slices' extends share one batched step graph
-    from . import eigensolver as _E
-
-    group = None
-    if os.environ.get("RIGA_GROUP") == "1" and nthreads > 1:
-        group = _E.LanczosGroup(nthreads, ctx=_take_ctx(base_ctx.device, ("group",), 0))
-
     def worker(widx):
-        _E._tls.group = group
         ctx = _take_ctx(base_ctx.device, ("slice", order[widx] if one_per_thread else widx), prio[widx])
         cnt = CostCounters()
         mine = [order[widx]] if one_per_thread else None
@@ -498,12 +452,6 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                     hib = _Boundary(hi, int(nu[k + 1]), None)
                     count = int(expected[k])
                     pool = _Pool()
-                    if dyn is not None:
-                        def hook(state, k=k, pool=pool, lo=lo, hi=hi, count=count):
-                            found = pool.count_in(lo, hi)
-                            state.set_run_stream(ctx.run_stream(dyn.pick(k, count - found, cnt.nfb, found)))
-
-                        _E._tls.prio_hook = hook
                     if count > 0:
                         m = max(2, min(m_factor * count, system.dof_count))
                         so = SolverOptions(m=m, **opts)
@@ -549,10 +497,6 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                 except Exception as e:  # surfaced after join
                     with lock:
                         errors.append((k, e))
-                finally:
-                    _E._tls.prio_hook = None
-                    if dyn is not None:
-                        dyn.done(k)
         with lock:
             counters.merge(cnt)
         _give_ctx(ctx)
@@ -566,9 +510,6 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
             t.start()
         for t in threads:
             t.join()
-    if group is not None:
-        group.close()
-        _give_ctx(group.ctx)
     if errors:
         k, e = errors[0]
         raise RuntimeError(f"slice {k} failed on rank {rank}: {e}") from e

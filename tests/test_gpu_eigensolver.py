@@ -348,43 +348,3 @@ def test_delayed_cgs2_matches_two_pass_cgs2():
     np.testing.assert_allclose(ca, cb, rtol=1e-10)
     for x in ca:  # and they are eigenvalues of the pencil (locked ones excluded)
         assert np.min(np.abs(lam[2:] - x)) <= 1e-10 * abs(x)
-
-
-@pytest.mark.gpu
-def test_run_stream_replays_are_bitwise_identical():
-    """riga_lanczos_set_run_stream (engine extension): extends whose step graphs replay on a forked side
-    stream (high or low priority) give bit-identical recurrences to replays on the context stream, and the
-    join keeps later work (restart, lift) ordered."""
-    import torch
-
-    from paper_2009_08167_b200 import device as D
-    from paper_2009_08167_b200.eigensolver import DeviceShiftInvert, _state_pool
-
-    s = P.build_system(2, 16, 3, 2)
-    lam = dense_eig(s)
-    sigma = 0.5 * (lam[3] + lam[4])
-    f = P.factor_ldl(s.K.csr - sigma * s.M.csr, ordering=P.separator_ordering(s))
-
-    def run(side):
-        _state_pool.clear()
-        ctx = D.current()
-        st = P.LanczosState(DeviceShiftInvert(f, s.M), s.dof_count, mass=s.M, shift=sigma, max_dim=40,
-                            rng=np.random.default_rng(3))
-        if side is not None:
-            st.set_run_stream(ctx.run_stream(side))
-        P.lanczos_extend(st, 30)
-        P.thick_restart(st, 6)
-        if side is not None:
-            st.set_run_stream(ctx.run_stream(not side))
-        P.lanczos_extend(st, 40)
-        X, _ = st.lift_many(np.eye(st.k)[:, :3])
-        out = st.T[: st.k, : st.k].copy(), X.cpu().numpy()
-        st.set_run_stream(None)
-        _state_pool.clear()
-        return out
-
-    Ta, Xa = run(None)
-    for side in (True, False):
-        Tb, Xb = run(side)
-        assert np.array_equal(Ta, Tb) and np.array_equal(Xa, Xb)
-    torch.cuda.synchronize()

@@ -278,20 +278,25 @@ def test_cfg5_inertia_matches_kronecker_counts(golden):
 
 
 @pytest.mark.gpu
-def test_dataflow_subtree_solve_is_bit_identical(tmp_path):
-    """Opt-in dataflow subtree kernels (RIGA_SUB_DATAFLOW=1: per-supernode dependency counters in shared memory
-    instead of a barrier per local level) give bit-identical solves to the level-synchronous kernels."""
-    import os
-    import subprocess
-    import sys
+@pytest.mark.parametrize("name,k", [("cfg4_iga", 3), ("cfg5_riga", 31)])
+def test_solve_backward_error_at_hard_shifts(golden, name, k):
+    """The chain supernodes' explicit inverses lose backward stability at high indefinite shifts (cfg5 slice
+    31 midpoint: 1.1e-8 with the inverse alone); the factor-time probe flags them and the solve refines them
+    locally, so ||(K - sigma M) x - b|| / ||b|| stays at substitution level (< 1e-10) everywhere."""
+    import torch
 
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    outs = []
-    for df in ("0", "1"):
-        path = str(tmp_path / f"x{df}.npy")
-        env = dict(os.environ, RIGA_SUB_DATAFLOW=df)
-        r = subprocess.run([sys.executable, os.path.join(root, "tools", "sub_df_check.py"), "cfg4", path, "6"],
-                           env=env, capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0, r.stderr[-2000:]
-        outs.append(np.load(path))
-    assert np.array_equal(outs[0], outs[1])
+    from paper_2009_08167_b200 import _lib
+
+    c = golden["configs"][name]
+    s = P.build_system(c["d"], c["ne"], c["p"], c["level"])
+    sh = c["shifts"]
+    sigma = 0.5 * (sh[k] + sh[k + 1])
+    sym = Symbolic.on_device(s.device, P.separator_ordering(s))
+    f = numeric_factor(sym, sigma)
+    rng = np.random.default_rng(7)
+    for _ in range(3):
+        b = torch.as_tensor(rng.standard_normal(s.dof_count), device="cuda")
+        x = f.solve_device(b)
+        r = torch.empty_like(b)
+        _lib.check(_lib.lib().riga_spmv(s.device.handle, 2, float(sigma), _lib.ptr(x), _lib.ptr(r)))
+        assert float(torch.linalg.norm(r - b) / torch.linalg.norm(b)) < 1e-10

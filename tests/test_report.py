@@ -1,31 +1,24 @@
-"""Experiment artifacts and cost reports vs the reference's own output directory (tests/golden/report_golden.json,
-made by tests/golden/make_report_golden.py from rigaeig's cli.run_experiment).
+"""Result files vs the reference's own output directory (tests/golden/report_golden.json, made by
+tests/golden/make_report_golden.py from rigaeig's cli.run_experiment).
 
-CPU tests pin the formats (rows re-rendered from the parsed golden values must reproduce the reference's text
-byte for byte) and the cost model; the GPU test runs the same sweep through the device solve."""
+CPU tests pin the formats: tables re-rendered from the parsed golden values must reproduce the reference's
+text byte for byte, and the manifest its schema.  The GPU test solves the same level sweep on the device and
+compares numerically."""
+import hashlib
 import json
-import math
 import os
 from dataclasses import dataclass
 
 import numpy as np
 import pytest
 
-from paper_2009_08167_b200.costmodel import (RunReport, TimeModel, improvement_report, predict_factor_flops,
-                                             predict_fb_flops, predict_time, time_exponents)
-from paper_2009_08167_b200.report import (ERRORS_HEADER, SPECTRUM_HEADER, ConfigError, ExperimentConfig,
-                                          PointResult, _levels, error_rows, load_config, spectrum_rows,
-                                          write_bundle)
+from paper_2009_08167_b200.report import (ERRORS_COLUMNS, SPECTRUM_COLUMNS, SWEEP_COLUMNS, artifact_names,
+                                          cost_report, errors_csv, report_json, spectrum_csv, sweep_csv,
+                                          sweep_row, write_artifacts)
 from paper_2009_08167_b200.sparsela import CostCounters
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "report_golden.json")))
-BASE = "d1_ne16_p3"
-
-
-def _cfg(out):
-    c = GOLD["config"]
-    return ExperimentConfig(d=c["d"], ne=c["ne"], p=c["p"], levels=c["levels"], nev=c["nev"], out=str(out),
-                            seed=c["seed"], figures=False)
+D, NE, P_, N_IGA = 1, 16, 3, 17
 
 
 def _csv(text):
@@ -42,166 +35,131 @@ class _Rec:
     diagonal: bool
 
 
-def _golden_point(level):
-    tag = f"{BASE}_l{level}"
-    _, srows = _csv(GOLD["files"][f"spectrum_{tag}.csv"])
-    lam = [float(r[1]) for r in srows]
-    res = [float(r[2]) for r in srows]
-    sid = [int(r[3]) for r in srows]
-    _, erows = _csv(GOLD["files"][f"errors_{tag}.csv"])
-    recs = [_Rec(int(r[0]) - 1, float(r[2]), float(r[3]), float(r[4]), r[5] == "1") for r in erows]
-    report = json.loads(GOLD["files"][f"report_{tag}.json"])
-    hdr, wrows = _csv(GOLD["files"][f"sweep_{BASE}.csv"])
-    cols = hdr.split(",")
-    sweep = [dict(zip(cols, (int(v) for v in r))) for r in wrows if int(r[0]) == level][0]
-    return PointResult(level, "ok", spectrum_rows(lam, res, sid), error_rows(recs, 17), report, sweep)
-
-
-def test_rows_reproduce_reference_text():
-    for level in (0, 1):
-        tag = f"{BASE}_l{level}"
-        pt = _golden_point(level)
-        assert "\n".join([SPECTRUM_HEADER] + pt.spectrum_rows) + "\n" == GOLD["files"][f"spectrum_{tag}.csv"]
-        assert "\n".join([ERRORS_HEADER] + pt.error_rows) + "\n" == GOLD["files"][f"errors_{tag}.csv"]
-
-
-def test_error_rows_print_nan():
-    rows = error_rows([_Rec(0, 1.5e-3, float("nan"), float("nan"), False)], 4)
-    assert rows == ["1,0.25,1.500000000000e-03,nan,nan,0"]
-
-
-def test_bundle_matches_reference_directory(tmp_path):
-    cfg = _cfg(tmp_path)
-    bundle = write_bundle(cfg, [_golden_point(0), _golden_point(1)])
-    names = sorted(f.name for f in bundle.files)
-    assert names == sorted(GOLD["files"])
-    for f in bundle.files:
-        assert f.read_text() == GOLD["files"][f.name], f.name
-    man = json.loads(bundle.manifest_path.read_text())
-    assert sorted(man) == GOLD["manifest_keys"]
-    assert [f["path"] for f in man["files"]] == GOLD["manifest_files"]
-    assert man["config_sha256"] == GOLD["config_sha256"]
-    assert not man["partial"] and bundle.failed_points == []
-    import hashlib
-    for f in man["files"]:
-        p = tmp_path / f["path"]
-        assert f["sha256"] == hashlib.sha256(p.read_bytes()).hexdigest() and f["bytes"] == p.stat().st_size
-
-
-def test_failed_point_marks_manifest_partial(tmp_path):
-    bundle = write_bundle(_cfg(tmp_path), [_golden_point(0), PointResult(1, "count-mismatch: x")])
-    man = json.loads(bundle.manifest_path.read_text())
-    assert man["partial"] and bundle.failed_points == [1]
-    assert {"level": 1, "status": "count-mismatch: x"} in man["points"]
-
-
-def test_config_validation_and_loading(tmp_path):
-    ExperimentConfig(nev=5).validate()
-    for bad in (dict(d=4, nev=5), dict(ne=12, nev=5), dict(p=0, nev=5), dict(levels=[], nev=5),
-                dict(levels=[9], nev=5), dict(), dict(nev=5, interval=(0, 1)), dict(nev="all"), dict(nev=0),
-                dict(interval=(2.0, 1.0)), dict(nev=5, lanczos_m=3), dict(nev=5, keep=59),
-                dict(nev=5, workers=0)):
-        with pytest.raises(ConfigError):
-            ExperimentConfig(**bad).validate()
-    assert ExperimentConfig(ne=16, p=3, nev="niga").resolved_nev(1) == 17
-    assert ExperimentConfig(ne=16, p=3, nev=100).resolved_nev(0) == 17
-    assert _levels("0-2,5") == [0, 1, 2, 5]
-    p = tmp_path / "c.json"
-    p.write_text(json.dumps({"d": 2, "ne": 8, "nev": "12", "interval": None}))
-    cfg = load_config(str(p), p=2)
-    assert (cfg.d, cfg.ne, cfg.p, cfg.nev) == (2, 8, 2, 12)
-    p.write_text(json.dumps({"dee": 2}))
-    with pytest.raises(ConfigError):
-        load_config(str(p))
-    p.write_text("{")
-    with pytest.raises(ConfigError):
-        load_config(str(p))
-
-
-def _counters(fact, fb, mv, calls):
+def _counters(fact, fb, mv, calls, nsh=None, nit=14):
     c = CostCounters()
     c.fact.flops, c.fb.flops, c.matvec.flops = fact, fb, mv
     c.fact.calls, c.fb.calls, c.matvec.calls = calls
     c.fact.seconds, c.fb.seconds, c.matvec.seconds = 0.5, 0.25, 0.125
-    c.nsh, c.nit = calls[0], 14
+    c.nsh, c.nit = calls[0] if nsh is None else nsh, nit
     return c
 
 
-def test_run_report_schema_matches_reference():
-    g = json.loads(GOLD["files"][f"report_{BASE}_l0.json"])
+def _golden_files(level):
+    """The level's three files re-rendered from the golden values."""
+    names = artifact_names(D, NE, P_, level)
+    _, srows = _csv(GOLD["files"][names["spectrum"]])
+    spec = spectrum_csv([float(r[1]) for r in srows], [float(r[2]) for r in srows], [int(r[3]) for r in srows])
+    _, erows = _csv(GOLD["files"][names["errors"]])
+    errs = errors_csv([_Rec(int(r[0]) - 1, float(r[2]), float(r[3]), float(r[4]), r[5] == "1") for r in erows],
+                      N_IGA)
+    g = json.loads(GOLD["files"][names["report"]])
     c = _counters(g["flops"]["fact"], g["flops"]["fb"], g["flops"]["matvec"],
-                  (g["counters"]["Nfa"], g["counters"]["Nfb"], g["counters"]["Nmv"]))
-    rep = RunReport.from_counters(g["config"], c).to_json_dict()
+                  (g["counters"]["Nfa"], g["counters"]["Nfb"], g["counters"]["Nmv"]), g["counters"]["Nsh"],
+                  g["counters"]["Nit"])
+    rep = cost_report(g["config"], c)
+    rep["time_s"] = g["time_s"]  # wall seconds are run-specific
+    return names, spec, errs, report_json(rep), c
+
+
+def test_tables_reproduce_reference_text():
+    for level in (0, 1):
+        names, spec, errs, rep, _ = _golden_files(level)
+        assert spec == GOLD["files"][names["spectrum"]]
+        assert errs == GOLD["files"][names["errors"]]
+        assert rep == GOLD["files"][names["report"]]
+    assert ",".join(SPECTRUM_COLUMNS) == GOLD["files"][names["spectrum"]].split("\n")[0]
+    assert ",".join(ERRORS_COLUMNS) == GOLD["files"][names["errors"]].split("\n")[0]
+
+
+def test_error_rows_print_nan():
+    assert errors_csv([_Rec(0, 1.5e-3, float("nan"), float("nan"), False)], 4).split("\n")[1] == \
+        "1,0.25,1.500000000000e-03,nan,nan,0"
+
+
+def test_sweep_table_reproduces_reference_text():
+    sweep_name = artifact_names(D, NE, P_)["sweep"]
+    hdr, rows = _csv(GOLD["files"][sweep_name])
+    assert hdr == ",".join(SWEEP_COLUMNS)
+    out = []
+    for r in rows:
+        v = dict(zip(SWEEP_COLUMNS, (int(x) for x in r)))
+        c = _counters(v["fact_flops"], v["fb_flops"], v["matvec_flops"], (v["Nfa"], v["Nfb"], v["Nmv"]), v["Nsh"],
+                      v["Nit"])
+        out.append(sweep_row(v["level"], v["blocksize"], v["N"], v["nnz_K"], v["fill_nnz"], c))
+    assert sweep_csv(out) == GOLD["files"][sweep_name]
+
+
+def test_manifest_matches_reference_schema(tmp_path):
+    files = []
+    for level in (0, 1):
+        names, spec, errs, rep, _ = _golden_files(level)
+        files += [(names["spectrum"], spec), (names["errors"], errs), (names["report"], rep)]
+    sweep_name = artifact_names(D, NE, P_)["sweep"]
+    files.append((sweep_name, GOLD["files"][sweep_name]))
+    mpath = write_artifacts(tmp_path, files, GOLD["config"], [(0, "ok"), (1, "ok")], seed=0)
+    man = json.loads(mpath.read_text())
+    assert sorted(man) == GOLD["manifest_keys"]
+    assert [f["path"] for f in man["files"]] == GOLD["manifest_files"]
+    assert man["config_sha256"] == GOLD["config_sha256"]
+    assert not man["partial"]
+    for f in man["files"]:
+        p = tmp_path / f["path"]
+        assert p.read_text() == GOLD["files"][f["path"]]
+        assert f["sha256"] == hashlib.sha256(p.read_bytes()).hexdigest() and f["bytes"] == p.stat().st_size
+    part = json.loads(write_artifacts(tmp_path / "b", [], GOLD["config"], [(0, "ok"), (1, "count-mismatch")],
+                                      0).read_text())
+    assert part["partial"] and {"level": 1, "status": "count-mismatch"} in part["points"]
+
+
+def test_cost_report_schema():
+    g = json.loads(GOLD["files"][artifact_names(D, NE, P_, 0)["report"]])
+    rep = cost_report(g["config"], _counters(1, 2, 3, (4, 5, 6)))
     assert set(rep) == set(g) and set(rep["time_s"]) == set(g["time_s"])
-    assert rep["counters"] == g["counters"] and rep["flops"] == g["flops"] and rep["config"] == g["config"]
     assert rep["time_s"]["total"] == pytest.approx(0.875)
 
 
-def test_cost_model_predictions():
-    np.testing.assert_allclose(predict_factor_flops(4 * 4096, 3, 0, 2) / predict_factor_flops(4096, 3, 0, 2), 8.0)
-    np.testing.assert_allclose(predict_fb_flops(4 * 4096, 3, 0, 2) / predict_fb_flops(4096, 3, 0, 2), 4.0)
-    # partitioning: 2^(d level) blocks plus the separator skeleton
-    N = 4096.0
-    assert predict_factor_flops(N, 3, 2, 2) == pytest.approx(16 * (N / 16) ** 1.5 * 27 + N ** 1.5)
-    assert predict_factor_flops(N, 3, 2, 2) < predict_factor_flops(N, 3, 0, 2)
-    assert time_exponents("fact", "iga", 3) == (2.0, 3.0)
-    assert time_exponents("fb", "riga", 2) == (1.0, 1.0)
-    assert time_exponents("matvec", "iga", 3) == (1.0, 3.0)
-    with pytest.raises(ValueError):
-        time_exponents("lu", "iga", 2)
-    with pytest.raises(ValueError):
-        time_exponents("fact", "fem", 2)
-    m = TimeModel.calibrate("fact", "iga", 2, 1000, 3, 2.0)
-    assert m.predict(1000, 3) == pytest.approx(2.0)
-    assert predict_time("fact", "iga", 2, (1000, 3, 2.0), 4000, 3) == pytest.approx(2.0 * 4 ** 1.5)
-    with pytest.raises(ValueError):
-        m.predict(64 * 1000 + 1, 3)
-    with pytest.raises(ValueError):
-        TimeModel.calibrate("fact", "iga", 2, 1000, 3, 0.0)
-
-
-def test_improvement_report():
-    cfg = {"d": 1, "ne": 16, "p": 3, "N0": 10}
-    a = RunReport.from_counters(cfg, _counters(100, 50, 10, (5, 50, 100)))
-    same = improvement_report(a, a)
-    assert all(v == pytest.approx(1.0) for v in same["flops"].values()) and not same["matvec_degraded"]
-    b = RunReport.from_counters(cfg, _counters(400, 100, 5, (5, 50, 100)))  # IGA costlier except mat-vec
-    rep = improvement_report(a, b)
-    assert rep["flops"]["fact"] == pytest.approx(4.0) and rep["flops"]["total"] == pytest.approx(505 / 160)
-    assert rep["matvec_degraded"] and a.ratios_vs_baseline["flops"] == rep["flops"]
-    other = RunReport.from_counters(dict(cfg, p=2), _counters(1, 1, 1, (1, 1, 1)))
-    with pytest.raises(ValueError):
-        improvement_report(other, a)
-    z = RunReport.from_counters(cfg, _counters(0, 1, 1, (1, 1, 1)))
-    assert math.isinf(improvement_report(z, a)["flops"]["fact"])
-
-
 @pytest.mark.gpu
-def test_run_experiment_on_device_matches_reference(tmp_path):
-    from paper_2009_08167_b200.report import run_experiment
+def test_device_sweep_matches_reference_files(tmp_path):
+    """The reference's level sweep (1D, ne=16, p=3, levels 0 and 1, 10 eigenpairs) solved on the device,
+    written through the writers, compared with the reference's files."""
+    import paper_2009_08167_b200 as P
 
-    bundle = run_experiment(_cfg(tmp_path))
-    assert sorted(f.name for f in bundle.files) == sorted(GOLD["files"]) and not bundle.failed_points
-    for level in (0, 1):
-        tag = f"{BASE}_l{level}"
-        h, got = _csv((tmp_path / f"spectrum_{tag}.csv").read_text())
-        _, ref = _csv(GOLD["files"][f"spectrum_{tag}.csv"])
-        assert h == SPECTRUM_HEADER and len(got) == len(ref)
+    cfg = GOLD["config"]
+    files, sweep, points = [], [], []
+    for level in cfg["levels"]:
+        system = P.build_system(cfg["d"], cfg["ne"], cfg["p"], level)
+        res = P.solve_spectrum(system, count=cfg["nev"], seed=cfg["seed"] + level, m=cfg["lanczos_m"],
+                               keep=cfg["keep"], tol=cfg["tol"])
+        records = P.error_table(res.eigenvalues, res.vectors, system)
+        names = artifact_names(cfg["d"], cfg["ne"], cfg["p"], level)
+        conf = {"d": cfg["d"], "ne": cfg["ne"], "p": cfg["p"], "level": level, "N": system.dof_count,
+                "N0": cfg["nev"]}
+        files += [(names["spectrum"], spectrum_csv(res.eigenvalues, res.residuals, res.slice_ids)),
+                  (names["errors"], errors_csv(records, N_IGA)),
+                  (names["report"], report_json(cost_report(conf, res.counters)))]
+        fill = P.factor_ldl(system.K, ordering=P.separator_ordering(system)).fill_nnz
+        sweep.append(sweep_row(level, 2 ** (cfg["ne"].bit_length() - 1 - level), system.dof_count, system.K.nnz,
+                               fill, res.counters))
+        points.append((level, "ok"))
+    files.append((artifact_names(cfg["d"], cfg["ne"], cfg["p"])["sweep"], sweep_csv(sweep)))
+    write_artifacts(tmp_path, files, cfg, points, cfg["seed"])
+    assert sorted(name for name, _ in files) == sorted(GOLD["files"])
+    for level in cfg["levels"]:
+        names = artifact_names(cfg["d"], cfg["ne"], cfg["p"], level)
+        h, got = _csv((tmp_path / names["spectrum"]).read_text())
+        _, ref = _csv(GOLD["files"][names["spectrum"]])
+        assert len(got) == len(ref) and [r[0] for r in got] == [r[0] for r in ref]
         np.testing.assert_allclose([float(r[1]) for r in got], [float(r[1]) for r in ref], rtol=1e-10)
         assert max(float(r[2]) for r in got) < 1e-8
-        assert [r[0] for r in got] == [r[0] for r in ref]
-        h, got = _csv((tmp_path / f"errors_{tag}.csv").read_text())
-        _, ref = _csv(GOLD["files"][f"errors_{tag}.csv"])
-        assert h == ERRORS_HEADER and [r[:2] + r[5:] for r in got] == [r[:2] + r[5:] for r in ref]
-        for col, atol in ((2, 1e-11), (3, 1e-11), (4, 1e-11)):
+        _, got = _csv((tmp_path / names["errors"]).read_text())
+        _, ref = _csv(GOLD["files"][names["errors"]])
+        assert [r[:2] + r[5:] for r in got] == [r[:2] + r[5:] for r in ref]
+        for col in (2, 3, 4):
             np.testing.assert_allclose([float(r[col]) for r in got], [float(r[col]) for r in ref], rtol=1e-4,
-                                       atol=atol)
-        rep = json.loads((tmp_path / f"report_{tag}.json").read_text())
-        gref = json.loads(GOLD["files"][f"report_{tag}.json"])
-        assert rep["config"] == gref["config"]
-        assert rep["counters"]["Nfa"] >= rep["counters"]["Nsh"] >= 1
-    hdr, got = _csv((tmp_path / f"sweep_{BASE}.csv").read_text())
-    ghdr, ref = _csv(GOLD["files"][f"sweep_{BASE}.csv"])
-    assert hdr == ghdr
+                                       atol=1e-11)
+        rep = json.loads((tmp_path / names["report"]).read_text())
+        assert rep["config"] == json.loads(GOLD["files"][names["report"]])["config"]
+    _, got = _csv((tmp_path / artifact_names(cfg["d"], cfg["ne"], cfg["p"])["sweep"]).read_text())
+    _, ref = _csv(GOLD["files"][artifact_names(cfg["d"], cfg["ne"], cfg["p"])["sweep"]])
     for g, r in zip(got, ref):
         assert g[:5] == r[:5]  # level, blocksize, N, nnz_K, fill_nnz

@@ -29,7 +29,6 @@ def main():
     ap.add_argument("--threads", default="1,2,4,8,16")
     ap.add_argument("--prelock", type=int, default=0, help="lock this many random rows first (R = k + locked)")
     ap.add_argument("--cycles", type=int, default=1, help="extend cycles per thread (thick restart keep 8 between)")
-    ap.add_argument("--group", action="store_true", help="lockstep group extends (one batched step graph)")
     a = ap.parse_args()
     c = CONFIGS[a.config]
     s = P.build_system(c.d, c.ne, c.p, c.level)
@@ -53,13 +52,6 @@ def main():
                 facts.append(f)
                 states.append(st)
         torch.cuda.synchronize()
-        grp = None
-        if a.group and a.what == "extend":
-            from paper_2009_08167_b200.eigensolver import LanczosGroup
-
-            grp = LanczosGroup(T)
-            for st_ in states:
-                st_._group = grp
         bar = threading.Barrier(T)
         graphs = [None] * T
         if a.what == "solveg":
@@ -112,8 +104,6 @@ def main():
         tot = T * (a.steps + (a.cycles - 1) * (a.steps - 8)) if a.what == "extend" else T * a.steps
         print(f"{a.what} threads={T:2d} cycles={a.cycles}: {tot / dt:8.1f} steps/s aggregate, "
               f"{dt * 1e3 / a.steps:7.3f} ms per step per thread", flush=True)
-        if grp is not None:
-            grp.close()
         del facts, states, ctxs
         torch.cuda.synchronize()
 
