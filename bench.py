@@ -13,9 +13,10 @@ metric is quoted on "at 1/2/4/8 B200" with slices distributed across GPUs.
 
 ``value`` is measured with the system resident in HBM; ``e2e`` through the
 public API from host CSR buffers (upload, ordering, symbolic, solve,
-eigenpairs to host).  ``--impl reference`` times the CPU oracle port of
-the reference path (oracle/, the reference is Python so nothing compiles
-into oracle/_ref) on the host cores, on a bounded sample of the workload.
+eigenpairs to host).  ``--impl reference`` times the reference's own
+package (rigaeig v0.1.0, installed by build() into oracle/_ref; the oracle
+port when it is absent) on the host cores, on a bounded sample of the
+workload (``--sample-q 0``: the whole workload, for calibration).
 Multi-GPU: one process per GPU (torchrun); slices are partitioned by LPT
 over the boundary inertias (weak in the number of slices per GPU:
 "scaling" is "strong" -- the total work is fixed).
@@ -69,6 +70,24 @@ def dist_env():
 # ---------------------------------------------------------------------------
 
 _W = {}
+REF_DIR = os.path.join(ROOT, "oracle", "_ref")  # the reference package installed by build() (rigaeig v0.1.0)
+
+
+def ref_kind() -> str:
+    """'reference' when the reference's own package (oracle/_ref/rigaeig) is importable, else 'port'."""
+    return "reference" if os.path.isdir(os.path.join(REF_DIR, "rigaeig")) else "port"
+
+
+def _ref_module():
+    if ref_kind() == "reference":
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        import rigaeig
+
+        return rigaeig
+    from oracle import rigaeig_port
+
+    return rigaeig_port
 
 
 def _worker_init(cfgname):
@@ -78,24 +97,24 @@ def _worker_init(cfgname):
         threadpool_limits(1)
     except Exception:
         pass
-    from oracle import rigaeig_port as O
     from paper_2009_08167_b200.configs import CONFIGS
 
     c = CONFIGS[cfgname]
-    _W["sys"] = O.build_system(c.d, c.ne, c.p, c.level)
+    R = _ref_module()
+    _W["R"] = R
+    _W["sys"] = R.build_system(c.d, c.ne, c.p, c.level)
 
 
 def _worker_task(task):
-    from oracle import rigaeig_port as O
-
-    k, lo, hi, q = task
+    k, lo, hi, m = task
     t0 = time.perf_counter()
-    r = O.solve_slice(_W["sys"], (lo, hi), seed=k, m=2 * q)
+    r = _W["R"].solve_slice(_W["sys"], (lo, hi), seed=k, m=m)
     return k, r.eigenvalues.size, r.expected_count, time.perf_counter() - t0
 
 
 def cpu_sample_tasks(cfgname, q):
-    """Bounded sample: the q lowest eigenpairs above every uniform shift."""
+    """Bounded sample: the q lowest eigenpairs above every uniform shift, m = 2 q (q = 0: the whole workload,
+    every slice with m = 2 count_k as the GPU arm)."""
     from oracle import rigaeig_port as O
     from paper_2009_08167_b200.configs import CONFIGS
 
@@ -104,14 +123,19 @@ def cpu_sample_tasks(cfgname, q):
     lam_e, _ = O.lambda_e_for(lam, c.n0)
     tasks = []
     for k in range(c.slices):
-        lo = k * lam_e / c.slices
+        lo, top = k * lam_e / c.slices, (k + 1) * lam_e / c.slices
         i0 = int(np.sum(lam < lo))
+        if q <= 0:
+            cnt = int(np.sum((lam > lo) & (lam <= top)))
+            tasks.append((k, lo, top, 2 * cnt, cnt))
+            continue
         i = i0 + q - 1
         while i + 1 < lam.size and lam[i + 1] - lam[i] <= 1e-8 * lam[i + 1]:
             i += 1
         hi = 0.5 * (lam[i] + lam[i + 1])
-        tasks.append((k, lo, hi, i + 1 - i0))
-    return tasks
+        tasks.append((k, lo, hi, 2 * (i + 1 - i0), i + 1 - i0))
+    # longest first: the pool drains evenly
+    return sorted(tasks, key=lambda t: -t[4])
 
 
 def run_cpu_sample(cfgname, q, steps=1, warmup=0, proc_bytes=0.0):
@@ -130,15 +154,39 @@ def run_cpu_sample(cfgname, q, steps=1, warmup=0, proc_bytes=0.0):
     with ctxmp.Pool(workers, initializer=_worker_init, initargs=(cfgname,)) as pool:
         for it in range(warmup + steps):
             t0 = time.perf_counter()
-            out = pool.map(_worker_task, tasks, chunksize=1)
+            out = pool.map(_worker_task, [t[:4] for t in tasks], chunksize=1)
             dt = time.perf_counter() - t0
             for k, found, exp, _ in out:
                 if found != exp:
                     raise RuntimeError(f"CPU sample slice {k}: {found} != {exp}")
             if it >= warmup:
                 times.append(dt)
-    pairs = sum(t[3] for t in tasks)
+    pairs = sum(t[4] for t in tasks)
     return pairs, times, workers
+
+
+def _sample_text(c, q, pairs, workers, kind):
+    what = ("the reference's rigaeig.solve_slice (oracle/_ref, rigaeig v0.1.0)" if kind == "reference"
+            else "oracle port of ref solve_slice")
+    if q <= 0:
+        return (f"{c.name}: the whole workload ({pairs} pairs), every uniform slice with m = 2 count_k, {what}, "
+                f"{workers} processes x 1 BLAS thread (ref cli.py:208-210 ProcessPool mode)")
+    return (f"{c.name}: the {q} lowest eigenpairs above each of the {c.slices} uniform shifts ({pairs} pairs), "
+            f"{what} with m = 2q, {workers} processes x 1 BLAS thread (ref cli.py:208-210 ProcessPool mode)")
+
+
+CALIBRATION = os.path.join(ROOT, "profiles", "r2_reference_full_cfg3.json")
+
+
+def _calibration(q):
+    """Full-workload vs sample rate of the reference on the GPU box host (tools: bench.py --impl reference
+    --sample-q 0, committed under profiles/)."""
+    try:
+        cal = json.load(open(CALIBRATION))
+    except (OSError, ValueError):
+        return None
+    return {"full_run_eigenpairs_per_s": cal.get("value"), "full_run_s": cal.get("ms_per_step", 0) / 1e3,
+            "source": os.path.relpath(CALIBRATION, ROOT), "sample_q": q}
 
 
 def reference_arm(args):
@@ -148,21 +196,24 @@ def reference_arm(args):
     from paper_2009_08167_b200.configs import CONFIGS
 
     c = CONFIGS[args.config]
-    pairs, times, workers = run_cpu_sample(args.config, args.sample_q, steps=args.steps,
-                                           warmup=min(args.warmup, 1))
+    kind = ref_kind()
+    warm = min(args.warmup, 1)
+    pairs, times, workers = run_cpu_sample(args.config, args.sample_q, steps=args.steps, warmup=warm)
     t = float(np.mean(times))
     v = pairs / t
-    sample = (f"{c.name}: the {args.sample_q} lowest eigenpairs above each of the {c.slices} uniform "
-              f"shifts ({pairs} pairs), oracle port of ref solve_slice (m = 2q), "
-              f"{workers} processes x 1 BLAS thread (ref cli.py:208-210 ProcessPool mode)")
+    sample = _sample_text(c, args.sample_q, pairs, workers, kind)
+    cal = _calibration(args.sample_q)
+    if cal and cal["full_run_eigenpairs_per_s"]:
+        cal["sample_over_full"] = v / cal["full_run_eigenpairs_per_s"]
     line = {"impl": "reference", "metric": "eigenpairs/s", "value": v, "unit": "eigenpairs/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": warm,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (deterministic pencil, seeded start vectors)",
-            "config": {"workload": c.text, "sample": sample},
-            "cpu_baseline": {"value": v, "unit": "eigenpairs/s", "cores": workers, "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": v, "unit": "eigenpairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": c.text, "config": c.name, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "eigenpairs/s", "cores": workers, "kind": kind,
+                             "sample": sample, "calibration": cal},
+            "e2e": {"value": v, "unit": "eigenpairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "per_step_s": times}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -682,11 +733,13 @@ def ours(args):
         # oracle process footprint: L (value + index) with working copies, plus the CSR pencil
         pb = 3.0 * 12.0 * sym.stats["fill_nnz"] + 40.0 * system.K.nnz
         pairs, ctimes, workers = run_cpu_sample(args.config, args.sample_q, steps=1, proc_bytes=pb)
+        cal = _calibration(args.sample_q)
+        if cal and cal["full_run_eigenpairs_per_s"]:
+            cal["sample_over_full"] = pairs / ctimes[0] / cal["full_run_eigenpairs_per_s"]
         line["cpu_baseline"] = {"value": pairs / ctimes[0], "unit": "eigenpairs/s", "cores": workers,
-                                "kind": "port",
-                                "sample": f"{c.name}: the {args.sample_q} lowest eigenpairs above each uniform "
-                                          f"shift ({pairs} pairs), oracle port of ref solve_slice, "
-                                          f"{workers} processes x 1 BLAS thread"}
+                                "kind": ref_kind(),
+                                "sample": _sample_text(c, args.sample_q, pairs, workers, ref_kind()),
+                                "calibration": cal}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
