@@ -218,12 +218,15 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// EPI 0: C -= acc (the Schur-complement updates); EPI 1: C = acc / dj[j] (the blocked TRSM
+// L21 = A21 X^T D^{-1}; C may alias A: a CTA's rows are read completely before its epilogue writes).
+template <int EPI = 0>
 __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64_t lda,
                                              const double* __restrict__ B, int64_t ldb,
                                              const double* __restrict__ d, int64_t k0, int64_t k1,
                                              int64_t i0, int64_t j0, int64_t mend, int64_t nend,
-                                             double* __restrict__ C, int64_t ldc, int64_t coff,
-                                             double* __restrict__ smem) {
+                                             double* C, int64_t ldc, int64_t coff,
+                                             double* __restrict__ smem, const double* __restrict__ dj = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;
   double acc[8][4][2];
@@ -294,6 +297,7 @@ __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64
     }
   }
   cp_async_wait<0>();
+  if (EPI == 1) __syncthreads();  // in-place: every warp's operand reads precede the writes
   const int r = lane >> 2, cc = (lane & 3) * 2;
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
@@ -302,8 +306,13 @@ __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t j = j0 + wn * 32 + q * 8 + cc;
-      if (j < nend) C[(j - coff) * ldc + (i - coff)] -= acc[m][q][0];
-      if (j + 1 < nend) C[(j + 1 - coff) * ldc + (i - coff)] -= acc[m][q][1];
+      if (EPI == 0) {
+        if (j < nend) C[(j - coff) * ldc + (i - coff)] -= acc[m][q][0];
+        if (j + 1 < nend) C[(j + 1 - coff) * ldc + (i - coff)] -= acc[m][q][1];
+      } else {
+        if (j < nend) C[(j - coff) * ldc + (i - coff)] = acc[m][q][0] / dj[j];
+        if (j + 1 < nend) C[(j + 1 - coff) * ldc + (i - coff)] = acc[m][q][1] / dj[j + 1];
+      }
     }
   }
 }

@@ -529,6 +529,255 @@ __global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restric
 }
 
 // ---------------------------------------------------------------------------
+// Large fronts: blocked right-looking LDL^T with 128-column outer blocks,
+// three launches per block (all large fronts of a level batched in grid y):
+//   k_diag128   one CTA per front: the nb x nb diagonal block (nb <= 128) in
+//               shared memory, 32-column sub-panels factored by one warp in
+//               registers, the rows below them by substitution, the rest of
+//               the block updated on DMMA; writes L11 (d on the diagonal), D,
+//               the inertia / zero-pivot counters and X = inv(L11) (unit
+//               lower: 32 x 32 diagonal inverses by substitution, off-diagonal
+//               blocks X_ij = -X_ii sum_k L_ik X_kj on DMMA) for the TRSM
+//   k_trsm128   L21 = A21 X^T D^{-1} for every row below the block: 128 x 128
+//               DMMA tiles over the block's columns, in place
+//   k_trail128  trailing pivot columns -= L21 D L21^T (K = nb), 128 x 128 DMMA
+//               tiles, lower triangle
+// The update block (-= L21 D L21^T with K = n_p) follows as k_syrk128.
+// X only ever inverts a 128 x 128 diagonal block (not a whole supernode), so
+// the TRSM keeps substitution-level accuracy (checked by the reconstruction,
+// inertia and solve-residual tests).
+// Shared layout of k_diag128 (pitch kDBP, A[c * kDBP + r]): strict lower =
+// L(r, c), diagonal = d, strict upper A[r * kDBP + c] (r > c) = X(r, c).
+// ---------------------------------------------------------------------------
+constexpr int kDB = 128;
+constexpr int kDBP = kDB + 1;
+constexpr int kTsP = 33;
+constexpr size_t kDiag128Smem = ((size_t)kDB * kDBP + kDB + 4 * 32 * kTsP) * sizeof(double);
+
+// acc(i, j) += sum_{t < kcount} fa(i, t) fb(t, j) for a 32 x 32 warp tile (kcount % 4 == 0)
+template <class FA, class FB>
+__device__ __forceinline__ void warp_mma32(double (&acc)[4][4][2], FA fa, FB fb, int kcount) {
+  const int lane = threadIdx.x & 31;
+  for (int k4 = 0; k4 < kcount; k4 += 4) {
+    const int kr = k4 + (lane & 3);
+    double av[4], bv[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) av[m] = fa(m * 8 + (lane >> 2), kr);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bv[q] = fb(kr, q * 8 + (lane >> 2));
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[m][q][0], acc[m][q][1], av[m], bv[q]);
+  }
+}
+
+__device__ __forceinline__ void zero_acc(double (&acc)[4][4][2]) {
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+}
+
+__global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
+                                                 const double* __restrict__ tol, double* __restrict__ panel,
+                                                 double* __restrict__ D, int64_t* __restrict__ stat,
+                                                 double* __restrict__ xbuf) {
+  extern __shared__ double sm[];
+  double* A = sm;
+  double* dd = A + kDB * kDBP;
+  double* Ts = dd + kDB;  // 4 warps x 32 x kTsP scratch (inverse products)
+  const int s = nodes[blockIdx.x];
+  const int64_t f = S.front[s], np = S.ncol[s];
+  if (kbo >= np) return;
+  const int nb = (int)imin(kDB, np - kbo);
+  const int nbp = (nb + 31) & ~31;
+  const int64_t col0 = S.col0[s];
+  double* P = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;  // (r, c) of the block at P[c f + r]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < nbp * nbp; idx += blockDim.x) {
+    const int c = idx / nbp, r = idx - c * nbp;
+    double v = 0.0;
+    if (r >= c) v = (r < nb && c < nb) ? P[(int64_t)c * f + r] : (r == c ? 1.0 : 0.0);
+    A[c * kDBP + r] = v;
+  }
+  __syncthreads();
+  for (int kb = 0; kb < nbp; kb += 32) {
+    // (1) the 32 x 32 diagonal sub-block by warp 0: lane = row, a[j] = A(kb + lane, kb + j)
+    if (warp == 0) {
+      double a[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) a[j] = A[(kb + j) * kDBP + kb + lane];
+      double dl = 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const double dk = __shfl_sync(0xffffffffu, a[k], k);
+        const double lk = a[k] / dk;
+#pragma unroll
+        for (int j = k + 1; j < 32; ++j) {
+          const double ajk = __shfl_sync(0xffffffffu, a[k], j);  // A(kb + j, kb + k), not yet scaled
+          if (lane >= j) a[j] = fma(-lk, ajk, a[j]);
+        }
+        if (lane == k) dl = dk;
+        if (lane > k) a[k] = lk;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j <= lane) A[(kb + j) * kDBP + kb + lane] = j == lane ? dl : a[j];
+      dd[kb + lane] = dl;
+    }
+    __syncthreads();
+    // (2) rows below the sub-block inside the block: L(r, kb + c), thread per row
+    const int nr = nbp - kb - 32;
+    if (tid < nr) {
+      const int r = kb + 32 + tid;
+      double x[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) x[c] = A[(kb + c) * kDBP + r];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        double w = x[c];
+#pragma unroll
+        for (int t = 0; t < c; ++t) w = fma(-x[t] * dd[kb + t], A[(kb + t) * kDBP + kb + c], w);
+        x[c] = w / dd[kb + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) A[(kb + c) * kDBP + r] = x[c];
+    }
+    __syncthreads();
+    // (3) the rest of the block -= L D L^T (rank 32) on DMMA: 32 x 32 lower tiles, one per warp
+    const int n3 = nr / 32;
+    for (int t = warp; t < n3 * (n3 + 1) / 2; t += 8) {
+      int ti = 0;
+      while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+      const int tj = t - ti * (ti + 1) / 2;
+      const int i0 = kb + 32 + 32 * ti, j0 = kb + 32 + 32 * tj;
+      double acc[4][4][2];
+      zero_acc(acc);
+      warp_mma32(acc, [&](int i, int k) { return A[(kb + k) * kDBP + i0 + i] * dd[kb + k]; },
+                 [&](int k, int j) { return A[(kb + k) * kDBP + j0 + j]; }, 32);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = i0 + m * 8 + (lane >> 2), j = j0 + q * 8 + (lane & 3) * 2 + e;
+            if (i >= j) A[j * kDBP + i] -= acc[m][q][e];
+          }
+    }
+    __syncthreads();
+  }
+  // pivots: D, inertia, first zero pivot
+  if (tid == 0) {
+    int neg = 0;
+    int64_t bad = INT64_MAX;
+    const double tv = tol[1];
+    for (int k = 0; k < nb; ++k) {
+      const double d = dd[k];
+      D[col0 + kbo + k] = d;
+      if (d < 0.0) neg++;
+      if (fabs(d) < tv && bad == INT64_MAX) bad = col0 + kbo + k;
+    }
+    if (neg) atomicAdd((unsigned long long*)&stat[0], (unsigned long long)neg);
+    if (bad != INT64_MAX) atomicMin((long long*)&stat[1], (long long)bad);
+  }
+  // L11 (d on the diagonal) back to the panel
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    const int c = idx / nb, r = idx - c * nb;
+    if (r >= c) P[(int64_t)c * f + r] = A[c * kDBP + r];
+  }
+  // X = inv(L11): (i) 32 x 32 diagonal inverses, warp per block, lane = column
+  const int nblk = nbp / 32;
+  if (warp < nblk) {
+    const int b = 32 * warp;
+    double x[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      double v = r == lane ? 1.0 : 0.0;
+#pragma unroll
+      for (int t = 0; t < r; ++t) v = fma(-A[(b + t) * kDBP + b + r], x[t], v);
+      x[r] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r > lane) A[(b + r) * kDBP + b + lane] = x[r];  // X(b + r, b + lane) at the upper slot
+  }
+  __syncthreads();
+  // (ii) off-diagonal blocks: warp jb owns block column jb, rows ib = jb + 1 .. nblk - 1 in order
+  auto Xget = [&](int r, int c) -> double { return r > c ? A[r * kDBP + c] : (r == c ? 1.0 : 0.0); };
+  if (warp < nblk - 1) {
+    const int jb = warp;
+    double* T = Ts + warp * 32 * kTsP;
+    for (int ib = jb + 1; ib < nblk; ++ib) {
+      double acc[4][4][2];
+      zero_acc(acc);
+      for (int kb = jb; kb < ib; ++kb)  // T = sum_k L_{ib,kb} X_{kb,jb}
+        warp_mma32(acc, [&](int i, int k) { return A[(32 * kb + k) * kDBP + 32 * ib + i]; },
+                   [&](int k, int j) { return Xget(32 * kb + k, 32 * jb + j); }, 32);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            T[(q * 8 + (lane & 3) * 2 + e) * kTsP + m * 8 + (lane >> 2)] = acc[m][q][e];
+      __syncwarp();
+      zero_acc(acc);  // X_{ib,jb} = -X_{ib,ib} T
+      warp_mma32(acc, [&](int i, int k) { return Xget(32 * ib + i, 32 * ib + k); },
+                 [&](int k, int j) { return T[j * kTsP + k]; }, 32);
+      __syncwarp();
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            A[(32 * ib + m * 8 + (lane >> 2)) * kDBP + 32 * jb + q * 8 + (lane & 3) * 2 + e] = -acc[m][q][e];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // X to the front's slot, xb[t kDB + j] = X(j, t) (the TRSM's B operand)
+  double* xb = xbuf + (int64_t)blockIdx.x * kDB * kDB;
+  for (int idx = tid; idx < kDB * kDB; idx += blockDim.x) {
+    const int t = idx / kDB, j = idx - t * kDB;
+    xb[idx] = (j < nbp && t < nbp) ? Xget(j, t) : (j == t ? 1.0 : 0.0);
+  }
+}
+
+// L21 = A21 X^T D^{-1}: rows [kbo + nb, f) of the block's columns, 128-row tiles, in place
+__global__ void __launch_bounds__(256, 1) k_trsm128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
+                                                    double* __restrict__ panel, const double* __restrict__ D,
+                                                    const double* __restrict__ xbuf) {
+  extern __shared__ double sm[];
+  const int s = nodes[blockIdx.y];
+  const int64_t f = S.front[s], np = S.ncol[s];
+  if (kbo >= np) return;
+  const int64_t nb = imin(kDB, np - kbo);
+  const int64_t i0 = kbo + nb + (int64_t)blockIdx.x * kT128;
+  if (i0 >= f) return;
+  double* Pc = panel + S.panel_off[s] + (int64_t)kbo * f;  // column kbo + t at Pc[t f]
+  dmma_tile128<1>(Pc, f, xbuf + (int64_t)blockIdx.y * kDB * kDB, kDB, nullptr, 0, nb, i0, 0, f, nb, Pc, f, 0, sm,
+                  D + S.col0[s] + kbo);
+}
+
+// trailing pivot columns [kbo + nb, n_p) -= L21 D L21^T over the block's nb columns (rows to f)
+__global__ void __launch_bounds__(256, 1) k_trail128(SymDev S, const int32_t* __restrict__ nodes, int kbo, int ntj,
+                                                     double* __restrict__ panel, const double* __restrict__ D) {
+  extern __shared__ double sm[];
+  const int s = nodes[blockIdx.y];
+  const int64_t f = S.front[s], np = S.ncol[s];
+  const int64_t m0 = kbo + kDB;
+  if (m0 >= np) return;
+  const int64_t ti = blockIdx.x / ntj, tj = blockIdx.x % ntj;
+  const int64_t i0 = m0 + ti * kT128, j0 = m0 + tj * kT128;
+  if (i0 >= f || j0 >= np || i0 + kT128 - 1 < j0) return;
+  double* L = panel + S.panel_off[s];
+  dmma_tile128<0>(L, f, L, f, D + S.col0[s], kbo, m0, i0, j0, f, np, L, f, 0, sm);
+}
+
+// ---------------------------------------------------------------------------
 // host drivers
 // ---------------------------------------------------------------------------
 static int build_plan(riga_symbolic* sym) {
@@ -637,6 +886,7 @@ __global__ void k_zero_cb(SymDev S, const int32_t* __restrict__ nodes, double* _
 static bool g_block_path = true;  // RIGA_FACTOR_PANEL=32: the 32-column panel chain
 static bool g_tile128 = true;      // RIGA_FACTOR_TILE128=0: 64 x 64 tiles for the update blocks
 static bool g_left_looking = false;  // RIGA_PANEL_LL=1: left-looking in-block panel updates (no k_syrk<0>; measured no gain)
+static bool g_old_path = false;  // RIGA_FACTOR_OLD=1: the 32-column panel chain (A/B)
 static int64_t g_block_max_fronts = 0;  // RIGA_FACTOR_BLOCK_FRONTS=n: block path for levels with <= n large fronts (opt-in: slower today)
 
 static int set_smem_attrs() {
@@ -649,12 +899,17 @@ static int set_smem_attrs() {
     g_tile128 = !(e && std::strcmp(e, "0") == 0);
     e = getenv("RIGA_PANEL_LL");
     g_left_looking = e && std::strcmp(e, "1") == 0;
+    e = getenv("RIGA_FACTOR_OLD");
+    g_old_path = e && std::strcmp(e, "1") == 0;
     e = getenv("RIGA_FACTOR_BLOCK_FRONTS");
     if (e) g_block_max_fronts = atoll(e);
   }
   RIGA_CUDA(cudaFuncSetAttribute(k_diag_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem(kNBO)));
   RIGA_CUDA(cudaFuncSetAttribute(k_l21, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l21_smem(kNBO)));
   RIGA_CUDA(cudaFuncSetAttribute(k_syrk128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem));
+  RIGA_CUDA(cudaFuncSetAttribute(k_trsm128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem));
+  RIGA_CUDA(cudaFuncSetAttribute(k_trail128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem));
+  RIGA_CUDA(cudaFuncSetAttribute(k_diag128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiag128Smem));
   int dev = 0, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -683,6 +938,11 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   RIGA_CUDA(cudaGetLastError());
   double* cbuf = nullptr;
   if (h.cb_total) RIGA_CUDA(cudaMallocAsync(&cbuf, h.cb_total * sizeof(double), st));
+  // per large front of a level: X = inv(L11) of its current 128-column block
+  int64_t max_nl = 0;
+  for (const LevelPlan& P : sym->plan) max_nl = std::max<int64_t>(max_nl, P.nlarge);
+  double* xbuf = nullptr;
+  if (max_nl && !g_old_path) RIGA_CUDA(cudaMallocAsync(&xbuf, max_nl * kDB * kDB * sizeof(double), st));
   if (h.panel_large) RIGA_CUDA(cudaMemsetAsync(F->panel.p, 0, h.panel_large * 8, st));
   if (sym->n_large) {
     k_asm_large<<<(unsigned)sym->n_large, 256, 0, st>>>(S, sym->d_large_nodes.p, Kv, Mv, sigma,
@@ -714,7 +974,24 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
                                                        F->D.p, F->stat.p); count_launch();
       RIGA_CUDA(cudaGetLastError());
     }
-    if (P.nlarge) {
+    if (P.nlarge && !g_old_path) {
+      const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
+      const unsigned nl = (unsigned)P.nlarge;
+      for (int64_t kbo = 0; kbo < P.max_np_large; kbo += kDB) {
+        k_diag128<<<nl, 256, kDiag128Smem, st>>>(S, ln, (int)kbo, F->tol.p, F->panel.p, F->D.p, F->stat.p, xbuf);
+        const unsigned nti = (unsigned)((P.max_f_large - kbo + kT128 - 1) / kT128);
+        k_trsm128<<<dim3(nti, nl), 256, kT128Smem, st>>>(S, ln, (int)kbo, F->panel.p, F->D.p, xbuf);
+        count_launch(2);
+        const int64_t m0 = kbo + kDB;
+        if (m0 < P.max_np_large) {
+          const int64_t ti = (P.max_f_large - m0 + kT128 - 1) / kT128, tj = (P.max_np_large - m0 + kT128 - 1) / kT128;
+          k_trail128<<<dim3((unsigned)(ti * tj), nl), 256, kT128Smem, st>>>(S, ln, (int)kbo, (int)tj, F->panel.p,
+                                                                            F->D.p);
+          count_launch();
+        }
+        RIGA_CUDA(cudaGetLastError());
+      }
+    } else if (P.nlarge) {
       const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
       unsigned nl = (unsigned)P.nlarge;
       for (int64_t kbo = 0; kbo < P.max_np_large; kbo += kNBO) {
@@ -761,6 +1038,10 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
           RIGA_CUDA(cudaGetLastError());
         }
       }
+    }
+    if (P.nlarge) {
+      const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
+      const unsigned nl = (unsigned)P.nlarge;
       if (P.max_nu_large > 0 && g_tile128 && P.max_np_large >= 128 && P.max_nu_large >= 256) {
         const int64_t t = (P.max_nu_large + kT128 - 1) / kT128;
         k_syrk128<<<dim3((unsigned)(t * t), nl), 256, kT128Smem, st>>>(S, ln, F->panel.p, cbuf, F->D.p);
@@ -774,6 +1055,7 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
     }
   }
   if (cbuf) RIGA_CUDA(cudaFreeAsync(cbuf, st));
+  if (xbuf) RIGA_CUDA(cudaFreeAsync(xbuf, st));
   RIGA_CUDA(cudaFreeAsync(scratch, st));
   return build_chain_inverse(F, st);
 }
