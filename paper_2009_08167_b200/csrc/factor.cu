@@ -529,30 +529,29 @@ __global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restric
 }
 
 // ---------------------------------------------------------------------------
-// Large fronts: blocked right-looking LDL^T with 128-column outer blocks,
-// three launches per block (all large fronts of a level batched in grid y):
+// Large fronts: blocked right-looking LDL^T with 128-column blocks, three
+// launches per block (all large fronts of a level batched in grid y):
 //   k_diag128   one CTA per front: the nb x nb diagonal block (nb <= 128) in
-//               shared memory, 32-column sub-panels factored by one warp in
-//               registers, the rows below them by substitution, the rest of
-//               the block updated on DMMA; writes L11 (d on the diagonal), D,
-//               the inertia / zero-pivot counters and X = inv(L11) (unit
-//               lower: 32 x 32 diagonal inverses by substitution, off-diagonal
-//               blocks X_ij = -X_ii sum_k L_ik X_kj on DMMA) for the TRSM
-//   k_trsm128   L21 = A21 X^T D^{-1} for every row below the block: 128 x 128
-//               DMMA tiles over the block's columns, in place
-//   k_trail128  trailing pivot columns -= L21 D L21^T (K = nb), 128 x 128 DMMA
-//               tiles, lower triangle
-// The update block (-= L21 D L21^T with K = n_p) follows as k_syrk128.
-// X only ever inverts a 128 x 128 diagonal block (not a whole supernode), so
-// the TRSM keeps substitution-level accuracy (checked by the reconstruction,
-// inertia and solve-residual tests).
-// Shared layout of k_diag128 (pitch kDBP, A[c * kDBP + r]): strict lower =
-// L(r, c), diagonal = d, strict upper A[r * kDBP + c] (r > c) = X(r, c).
+//               shared memory in 32-column steps -- warp 0 factors the 32 x 32
+//               sub-block and inverts its unit-lower factor in registers, the
+//               rows below it inside the block become L = A X^T D^{-1} (DMMA),
+//               the rest of the block takes the rank-32 update (DMMA); writes
+//               L11 (d on the diagonal), D, the inertia / zero-pivot counters
+//               and the four 32 x 32 diagonal inverses X_b for the TRSM
+//   k_trsm128   L21 = A21 L11^{-T} D^{-1} for every row below the block by
+//               blocked substitution: warp per 32 rows, per 32-column step
+//               W_b = (A_b - sum_{t<b} W_t D_t L_bt^T) X_b^T D_b^{-1} (DMMA)
+//   k_trail128  trailing columns -= L21 D L21^T (128 x 128 DMMA tiles)
+// Only 32 x 32 diagonal blocks are ever inverted: the TRSM keeps
+// substitution-level accuracy (the reconstruction, inertia and solve-residual
+// tests pin it; an explicit 128 x 128 inverse measured 1.9e-10 backward error
+// on cfg4 IGA against 4e-12).
 // ---------------------------------------------------------------------------
 constexpr int kDB = 128;
 constexpr int kDBP = kDB + 1;
-constexpr int kTsP = 33;
-constexpr size_t kDiag128Smem = ((size_t)kDB * kDBP + kDB + 4 * 32 * kTsP) * sizeof(double);
+constexpr int kXB = 32 * 33;  // one 32 x 32 inverse, pitch 33: X_b(r, c) at [c * 33 + r]
+constexpr size_t kDiag128Smem = ((size_t)kDB * kDBP + kDB + 4 * kXB) * sizeof(double);
+constexpr size_t kTrsmSmem = (size_t)4 * 32 * kDBP * sizeof(double);  // 4 warps x 32 rows x nb
 
 // acc(i, j) += sum_{t < kcount} fa(i, t) fb(t, j) for a 32 x 32 warp tile (kcount % 4 == 0)
 template <class FA, class FB>
@@ -579,14 +578,61 @@ __device__ __forceinline__ void zero_acc(double (&acc)[4][4][2]) {
     for (int q = 0; q < 4; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
 }
 
+// accumulator element e of (m, q): row m * 8 + lane / 4, column q * 8 + 2 (lane % 4) + e
+#define RIGA_ACC_FOR(body)                                                     \
+  _Pragma("unroll") for (int m = 0; m < 4; ++m)                                \
+    _Pragma("unroll") for (int q = 0; q < 4; ++q)                              \
+      _Pragma("unroll") for (int e = 0; e < 2; ++e) {                          \
+        const int ai = m * 8 + (lane >> 2), aj = q * 8 + (lane & 3) * 2 + e; \
+        body                                                                   \
+      }
+
+// Warp: unblocked LDL^T of the 32 x 32 lower block at A[c * ld + r] (r >= c) in
+// registers (lane = row), then X = inv(L) (unit lower, lane = column) into
+// Xs[c * 33 + r]; L (strict lower) and d (diagonal) are written back to A.
+__device__ __forceinline__ void warp_ldl32(double* A, int ld, double* Xs, double& d_out) {
+  const int lane = threadIdx.x & 31;
+  double a[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) a[j] = j <= lane ? A[j * ld + lane] : 0.0;
+  double dl = 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const double dk = __shfl_sync(0xffffffffu, a[k], k);
+    const double lk = a[k] / dk;
+#pragma unroll
+    for (int j = k + 1; j < 32; ++j) {
+      const double ajk = __shfl_sync(0xffffffffu, a[k], j);  // A(j, k), not yet scaled
+      if (lane >= j) a[j] = fma(-lk, ajk, a[j]);
+    }
+    if (lane == k) dl = dk;
+    if (lane > k) a[k] = lk;
+  }
+  // X = inv(L): lane owns column c = lane: x_r = [r == c] - sum_{t < r} L(r, t) x_t
+  double x[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    double v = r == lane ? 1.0 : 0.0;
+#pragma unroll
+    for (int t = 0; t < r; ++t) v = fma(-__shfl_sync(0xffffffffu, a[t], r), x[t], v);
+    x[r] = v;
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j <= lane) A[j * ld + lane] = j == lane ? dl : a[j];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) Xs[lane * 33 + r] = x[r];
+  d_out = dl;
+}
+
 __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
                                                  const double* __restrict__ tol, double* __restrict__ panel,
                                                  double* __restrict__ D, int64_t* __restrict__ stat,
                                                  double* __restrict__ xbuf) {
   extern __shared__ double sm[];
-  double* A = sm;
-  double* dd = A + kDB * kDBP;
-  double* Ts = dd + kDB;  // 4 warps x 32 x kTsP scratch (inverse products)
+  double* A = sm;               // A[c * kDBP + r], lower triangle
+  double* dd = A + kDB * kDBP;  // pivots
+  double* Xs = dd + kDB;        // the four 32 x 32 diagonal inverses
   const int s = nodes[blockIdx.x];
   const int64_t f = S.front[s], np = S.ncol[s];
   if (kbo >= np) return;
@@ -597,55 +643,30 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < nbp * nbp; idx += blockDim.x) {
     const int c = idx / nbp, r = idx - c * nbp;
-    double v = 0.0;
-    if (r >= c) v = (r < nb && c < nb) ? P[(int64_t)c * f + r] : (r == c ? 1.0 : 0.0);
-    A[c * kDBP + r] = v;
+    if (r >= c) A[c * kDBP + r] = (r < nb && c < nb) ? P[(int64_t)c * f + r] : (r == c ? 1.0 : 0.0);
   }
   __syncthreads();
   for (int kb = 0; kb < nbp; kb += 32) {
-    // (1) the 32 x 32 diagonal sub-block by warp 0: lane = row, a[j] = A(kb + lane, kb + j)
+    double* Xk = Xs + (kb / 32) * kXB;
     if (warp == 0) {
-      double a[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) a[j] = A[(kb + j) * kDBP + kb + lane];
-      double dl = 0.0;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const double dk = __shfl_sync(0xffffffffu, a[k], k);
-        const double lk = a[k] / dk;
-#pragma unroll
-        for (int j = k + 1; j < 32; ++j) {
-          const double ajk = __shfl_sync(0xffffffffu, a[k], j);  // A(kb + j, kb + k), not yet scaled
-          if (lane >= j) a[j] = fma(-lk, ajk, a[j]);
-        }
-        if (lane == k) dl = dk;
-        if (lane > k) a[k] = lk;
-      }
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j <= lane) A[(kb + j) * kDBP + kb + lane] = j == lane ? dl : a[j];
+      double dl;
+      warp_ldl32(A + kb * kDBP + kb, kDBP, Xk, dl);
       dd[kb + lane] = dl;
     }
     __syncthreads();
-    // (2) rows below the sub-block inside the block: L(r, kb + c), thread per row
+    // rows below the sub-block inside the block: L = A X^T D^{-1}, 32-row tiles on DMMA
     const int nr = nbp - kb - 32;
-    if (tid < nr) {
-      const int r = kb + 32 + tid;
-      double x[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) x[c] = A[(kb + c) * kDBP + r];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        double w = x[c];
-#pragma unroll
-        for (int t = 0; t < c; ++t) w = fma(-x[t] * dd[kb + t], A[(kb + t) * kDBP + kb + c], w);
-        x[c] = w / dd[kb + c];
-      }
-#pragma unroll
-      for (int c = 0; c < 32; ++c) A[(kb + c) * kDBP + r] = x[c];
+    if (warp < nr / 32) {
+      const int i0 = kb + 32 + 32 * warp;
+      double acc[4][4][2];
+      zero_acc(acc);
+      warp_mma32(acc, [&](int i, int k) { return A[(kb + k) * kDBP + i0 + i]; },
+                 [&](int k, int j) { return Xk[k * 33 + j]; }, 32);  // X(j, k) at [k * 33 + j]
+      __syncwarp();
+      RIGA_ACC_FOR(A[(kb + aj) * kDBP + i0 + ai] = acc[m][q][e] / dd[kb + aj];)
     }
     __syncthreads();
-    // (3) the rest of the block -= L D L^T (rank 32) on DMMA: 32 x 32 lower tiles, one per warp
+    // the rest of the block -= L D L^T (rank 32): 32 x 32 lower tiles, one per warp
     const int n3 = nr / 32;
     for (int t = warp; t < n3 * (n3 + 1) / 2; t += 8) {
       int ti = 0;
@@ -656,20 +677,11 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
       zero_acc(acc);
       warp_mma32(acc, [&](int i, int k) { return A[(kb + k) * kDBP + i0 + i] * dd[kb + k]; },
                  [&](int k, int j) { return A[(kb + k) * kDBP + j0 + j]; }, 32);
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = i0 + m * 8 + (lane >> 2), j = j0 + q * 8 + (lane & 3) * 2 + e;
-            if (i >= j) A[j * kDBP + i] -= acc[m][q][e];
-          }
+      RIGA_ACC_FOR(if (i0 + ai >= j0 + aj) A[(j0 + aj) * kDBP + i0 + ai] -= acc[m][q][e];)
     }
     __syncthreads();
   }
-  // pivots: D, inertia, first zero pivot
-  if (tid == 0) {
+  if (tid == 0) {  // pivots: D, inertia, first zero pivot
     int neg = 0;
     int64_t bad = INT64_MAX;
     const double tv = tol[1];
@@ -682,84 +694,63 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
     if (neg) atomicAdd((unsigned long long*)&stat[0], (unsigned long long)neg);
     if (bad != INT64_MAX) atomicMin((long long*)&stat[1], (long long)bad);
   }
-  // L11 (d on the diagonal) back to the panel
-  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {  // L11, d on the diagonal
     const int c = idx / nb, r = idx - c * nb;
     if (r >= c) P[(int64_t)c * f + r] = A[c * kDBP + r];
   }
-  // X = inv(L11): (i) 32 x 32 diagonal inverses, warp per block, lane = column
-  const int nblk = nbp / 32;
-  if (warp < nblk) {
-    const int b = 32 * warp;
-    double x[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      double v = r == lane ? 1.0 : 0.0;
-#pragma unroll
-      for (int t = 0; t < r; ++t) v = fma(-A[(b + t) * kDBP + b + r], x[t], v);
-      x[r] = v;
-    }
-#pragma unroll
-    for (int r = 0; r < 32; ++r)
-      if (r > lane) A[(b + r) * kDBP + b + lane] = x[r];  // X(b + r, b + lane) at the upper slot
-  }
-  __syncthreads();
-  // (ii) off-diagonal blocks: warp jb owns block column jb, rows ib = jb + 1 .. nblk - 1 in order
-  auto Xget = [&](int r, int c) -> double { return r > c ? A[r * kDBP + c] : (r == c ? 1.0 : 0.0); };
-  if (warp < nblk - 1) {
-    const int jb = warp;
-    double* T = Ts + warp * 32 * kTsP;
-    for (int ib = jb + 1; ib < nblk; ++ib) {
-      double acc[4][4][2];
-      zero_acc(acc);
-      for (int kb = jb; kb < ib; ++kb)  // T = sum_k L_{ib,kb} X_{kb,jb}
-        warp_mma32(acc, [&](int i, int k) { return A[(32 * kb + k) * kDBP + 32 * ib + i]; },
-                   [&](int k, int j) { return Xget(32 * kb + k, 32 * jb + j); }, 32);
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            T[(q * 8 + (lane & 3) * 2 + e) * kTsP + m * 8 + (lane >> 2)] = acc[m][q][e];
-      __syncwarp();
-      zero_acc(acc);  // X_{ib,jb} = -X_{ib,ib} T
-      warp_mma32(acc, [&](int i, int k) { return Xget(32 * ib + i, 32 * ib + k); },
-                 [&](int k, int j) { return T[j * kTsP + k]; }, 32);
-      __syncwarp();
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            A[(32 * ib + m * 8 + (lane >> 2)) * kDBP + 32 * jb + q * 8 + (lane & 3) * 2 + e] = -acc[m][q][e];
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  // X to the front's slot, xb[t kDB + j] = X(j, t) (the TRSM's B operand)
-  double* xb = xbuf + (int64_t)blockIdx.x * kDB * kDB;
-  for (int idx = tid; idx < kDB * kDB; idx += blockDim.x) {
-    const int t = idx / kDB, j = idx - t * kDB;
-    xb[idx] = (j < nbp && t < nbp) ? Xget(j, t) : (j == t ? 1.0 : 0.0);
-  }
+  double* xb = xbuf + (int64_t)blockIdx.x * 4 * kXB;
+  for (int idx = tid; idx < (nbp / 32) * kXB; idx += blockDim.x) xb[idx] = Xs[idx];
 }
 
-// L21 = A21 X^T D^{-1}: rows [kbo + nb, f) of the block's columns, 128-row tiles, in place
-__global__ void __launch_bounds__(256, 1) k_trsm128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
-                                                    double* __restrict__ panel, const double* __restrict__ D,
-                                                    const double* __restrict__ xbuf) {
+// L21 = A21 L11^{-T} D^{-1} for the rows below the block, by blocked substitution: each warp owns 32
+// rows (independent of the others), its nb columns staged in shared memory.
+__global__ void __launch_bounds__(128) k_trsm128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
+                                                 double* __restrict__ panel, const double* __restrict__ D,
+                                                 const double* __restrict__ xbuf) {
   extern __shared__ double sm[];
   const int s = nodes[blockIdx.y];
   const int64_t f = S.front[s], np = S.ncol[s];
   if (kbo >= np) return;
-  const int64_t nb = imin(kDB, np - kbo);
-  const int64_t i0 = kbo + nb + (int64_t)blockIdx.x * kT128;
-  if (i0 >= f) return;
-  double* Pc = panel + S.panel_off[s] + (int64_t)kbo * f;  // column kbo + t at Pc[t f]
-  dmma_tile128<1>(Pc, f, xbuf + (int64_t)blockIdx.y * kDB * kDB, kDB, nullptr, 0, nb, i0, 0, f, nb, Pc, f, 0, sm,
-                  D + S.col0[s] + kbo);
+  const int nb = (int)imin(kDB, np - kbo);
+  const int nbp = (nb + 31) & ~31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = kbo + nb + (int64_t)blockIdx.x * 128 + 32 * warp;
+  if (r0 >= f) return;
+  const int nr = (int)imin(32, f - r0);
+  const int64_t col0 = S.col0[s];
+  const double* dk = D + col0 + kbo;
+  const double* Lb = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;  // L11(r, c) at Lb[c f + r]
+  double* Pr = panel + S.panel_off[s] + (int64_t)kbo * f + r0;         // A21(row, c) at Pr[c f + row]
+  const double* xb = xbuf + (int64_t)blockIdx.y * 4 * kXB;
+  double* W = sm + warp * 32 * kDBP;  // W[c * kDBP + row], this warp's rows x nbp columns
+  for (int c = 0; c < nbp; ++c) W[c * kDBP + lane] = (c < nb && lane < nr) ? Pr[(int64_t)c * f + lane] : 0.0;
+  __syncwarp();
+  for (int kb = 0; kb < nbp; kb += 32) {
+    double acc[4][4][2];
+    RIGA_ACC_FOR(acc[m][q][e] = W[(kb + aj) * kDBP + ai];)
+    if (kb > 0) {  // T = A_b - sum_{t < b} W_t D_t L_bt^T
+      double neg[4][4][2];
+      zero_acc(neg);
+      warp_mma32(neg, [&](int i, int k) { return W[k * kDBP + i] * dk[k]; },
+                 [&](int k, int j) { return kb + j < nb ? Lb[(int64_t)k * f + kb + j] : 0.0; }, kb);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[m][q][0] -= neg[m][q][0], acc[m][q][1] -= neg[m][q][1];
+    }
+    __syncwarp();
+    RIGA_ACC_FOR(W[(kb + aj) * kDBP + ai] = acc[m][q][e];)
+    __syncwarp();
+    const double* Xk = xb + (kb / 32) * kXB;  // W_b = T X_b^T D_b^{-1}
+    zero_acc(acc);
+    warp_mma32(acc, [&](int i, int k) { return W[(kb + k) * kDBP + i]; },
+               [&](int k, int j) { return Xk[k * 33 + j]; }, 32);
+    __syncwarp();
+    RIGA_ACC_FOR(W[(kb + aj) * kDBP + ai] = kb + aj < nb ? acc[m][q][e] / dk[kb + aj] : 0.0;)
+    __syncwarp();
+  }
+  for (int c = 0; c < nb; ++c)
+    if (lane < nr) Pr[(int64_t)c * f + lane] = W[c * kDBP + lane];
 }
 
 // trailing pivot columns [kbo + nb, n_p) -= L21 D L21^T over the block's nb columns (rows to f)
@@ -907,7 +898,7 @@ static int set_smem_attrs() {
   RIGA_CUDA(cudaFuncSetAttribute(k_diag_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem(kNBO)));
   RIGA_CUDA(cudaFuncSetAttribute(k_l21, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l21_smem(kNBO)));
   RIGA_CUDA(cudaFuncSetAttribute(k_syrk128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem));
-  RIGA_CUDA(cudaFuncSetAttribute(k_trsm128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem));
+  RIGA_CUDA(cudaFuncSetAttribute(k_trsm128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem));
   RIGA_CUDA(cudaFuncSetAttribute(k_trail128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem));
   RIGA_CUDA(cudaFuncSetAttribute(k_diag128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiag128Smem));
   int dev = 0, maxsm = 0;
@@ -942,7 +933,7 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   int64_t max_nl = 0;
   for (const LevelPlan& P : sym->plan) max_nl = std::max<int64_t>(max_nl, P.nlarge);
   double* xbuf = nullptr;
-  if (max_nl && !g_old_path) RIGA_CUDA(cudaMallocAsync(&xbuf, max_nl * kDB * kDB * sizeof(double), st));
+  if (max_nl && !g_old_path) RIGA_CUDA(cudaMallocAsync(&xbuf, max_nl * 4 * kXB * sizeof(double), st));
   if (h.panel_large) RIGA_CUDA(cudaMemsetAsync(F->panel.p, 0, h.panel_large * 8, st));
   if (sym->n_large) {
     k_asm_large<<<(unsigned)sym->n_large, 256, 0, st>>>(S, sym->d_large_nodes.p, Kv, Mv, sigma,
@@ -979,8 +970,8 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       const unsigned nl = (unsigned)P.nlarge;
       for (int64_t kbo = 0; kbo < P.max_np_large; kbo += kDB) {
         k_diag128<<<nl, 256, kDiag128Smem, st>>>(S, ln, (int)kbo, F->tol.p, F->panel.p, F->D.p, F->stat.p, xbuf);
-        const unsigned nti = (unsigned)((P.max_f_large - kbo + kT128 - 1) / kT128);
-        k_trsm128<<<dim3(nti, nl), 256, kT128Smem, st>>>(S, ln, (int)kbo, F->panel.p, F->D.p, xbuf);
+        const unsigned nti = (unsigned)((P.max_f_large - kbo + 127) / 128);
+        k_trsm128<<<dim3(nti, nl), 128, kTrsmSmem, st>>>(S, ln, (int)kbo, F->panel.p, F->D.p, xbuf);
         count_launch(2);
         const int64_t m0 = kbo + kDB;
         if (m0 < P.max_np_large) {
