@@ -551,7 +551,7 @@ constexpr int kDB = 128;
 constexpr int kDBP = kDB + 1;
 constexpr int kXB = 32 * 33;  // one 32 x 32 inverse, pitch 33: X_b(r, c) at [c * 33 + r]
 constexpr size_t kDiag128Smem = ((size_t)kDB * kDBP + kDB + 4 * kXB) * sizeof(double);
-constexpr size_t kTrsmSmem = (size_t)4 * 32 * kDBP * sizeof(double);  // 4 warps x 32 rows x nb
+constexpr size_t kTrsmSmem = (size_t)4 * kDB * 33 * sizeof(double);  // 4 warps x nb columns x 32 rows (pitch 33)
 
 // acc(i, j) += sum_{t < kcount} fa(i, t) fb(t, j) for a 32 x 32 warp tile (kcount % 4 == 0)
 template <class FA, class FB>
@@ -722,16 +722,16 @@ __global__ void __launch_bounds__(128) k_trsm128(SymDev S, const int32_t* __rest
   const double* Lb = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;  // L11(r, c) at Lb[c f + r]
   double* Pr = panel + S.panel_off[s] + (int64_t)kbo * f + r0;         // A21(row, c) at Pr[c f + row]
   const double* xb = xbuf + (int64_t)blockIdx.y * 4 * kXB;
-  double* W = sm + warp * 32 * kDBP;  // W[c * kDBP + row], this warp's rows x nbp columns
-  for (int c = 0; c < nbp; ++c) W[c * kDBP + lane] = (c < nb && lane < nr) ? Pr[(int64_t)c * f + lane] : 0.0;
+  double* W = sm + warp * kDB * 33;  // W[c * 33 + row], this warp's rows x nbp columns
+  for (int c = 0; c < nbp; ++c) W[c * 33 + lane] = (c < nb && lane < nr) ? Pr[(int64_t)c * f + lane] : 0.0;
   __syncwarp();
   for (int kb = 0; kb < nbp; kb += 32) {
     double acc[4][4][2];
-    RIGA_ACC_FOR(acc[m][q][e] = W[(kb + aj) * kDBP + ai];)
+    RIGA_ACC_FOR(acc[m][q][e] = W[(kb + aj) * 33 + ai];)
     if (kb > 0) {  // T = A_b - sum_{t < b} W_t D_t L_bt^T
       double neg[4][4][2];
       zero_acc(neg);
-      warp_mma32(neg, [&](int i, int k) { return W[k * kDBP + i] * dk[k]; },
+      warp_mma32(neg, [&](int i, int k) { return W[k * 33 + i] * dk[k]; },
                  [&](int k, int j) { return kb + j < nb ? Lb[(int64_t)k * f + kb + j] : 0.0; }, kb);
 #pragma unroll
       for (int m = 0; m < 4; ++m)
@@ -739,18 +739,18 @@ __global__ void __launch_bounds__(128) k_trsm128(SymDev S, const int32_t* __rest
         for (int q = 0; q < 4; ++q) acc[m][q][0] -= neg[m][q][0], acc[m][q][1] -= neg[m][q][1];
     }
     __syncwarp();
-    RIGA_ACC_FOR(W[(kb + aj) * kDBP + ai] = acc[m][q][e];)
+    RIGA_ACC_FOR(W[(kb + aj) * 33 + ai] = acc[m][q][e];)
     __syncwarp();
     const double* Xk = xb + (kb / 32) * kXB;  // W_b = T X_b^T D_b^{-1}
     zero_acc(acc);
-    warp_mma32(acc, [&](int i, int k) { return W[(kb + k) * kDBP + i]; },
+    warp_mma32(acc, [&](int i, int k) { return W[(kb + k) * 33 + i]; },
                [&](int k, int j) { return Xk[k * 33 + j]; }, 32);
     __syncwarp();
-    RIGA_ACC_FOR(W[(kb + aj) * kDBP + ai] = kb + aj < nb ? acc[m][q][e] / dk[kb + aj] : 0.0;)
+    RIGA_ACC_FOR(W[(kb + aj) * 33 + ai] = kb + aj < nb ? acc[m][q][e] / dk[kb + aj] : 0.0;)
     __syncwarp();
   }
   for (int c = 0; c < nb; ++c)
-    if (lane < nr) Pr[(int64_t)c * f + lane] = W[c * kDBP + lane];
+    if (lane < nr) Pr[(int64_t)c * f + lane] = W[c * 33 + lane];
 }
 
 // trailing pivot columns [kbo + nb, n_p) -= L21 D L21^T over the block's nb columns (rows to f)
