@@ -26,6 +26,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "dmma.cuh"
 #include "internal.h"
@@ -533,25 +534,22 @@ __global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restric
 // launches per block (all large fronts of a level batched in grid y):
 //   k_diag128   one CTA per front: the nb x nb diagonal block (nb <= 128) in
 //               shared memory in 32-column steps -- warp 0 factors the 32 x 32
-//               sub-block and inverts its unit-lower factor in registers, the
-//               rows below it inside the block become L = A X^T D^{-1} (DMMA),
-//               the rest of the block takes the rank-32 update (DMMA); writes
-//               L11 (d on the diagonal), D, the inertia / zero-pivot counters
-//               and the four 32 x 32 diagonal inverses X_b for the TRSM
+//               sub-block in registers, the rows below it inside the block
+//               are solved by substitution (thread per row), the rest of the
+//               block takes the rank-32 update on DMMA; writes L11 (d on the
+//               diagonal), D and the inertia / zero-pivot counters
 //   k_trsm128   L21 = A21 L11^{-T} D^{-1} for every row below the block by
-//               blocked substitution: warp per 32 rows, per 32-column step
-//               W_b = (A_b - sum_{t<b} W_t D_t L_bt^T) X_b^T D_b^{-1} (DMMA)
+//               blocked substitution: warp per 32 rows, per 32-column step the
+//               update from the earlier steps on DMMA, then substitution
 //   k_trail128  trailing columns -= L21 D L21^T (128 x 128 DMMA tiles)
-// Only 32 x 32 diagonal blocks are ever inverted: the TRSM keeps
-// substitution-level accuracy (the reconstruction, inertia and solve-residual
-// tests pin it; an explicit 128 x 128 inverse measured 1.9e-10 backward error
-// on cfg4 IGA against 4e-12).
+// No triangular factor is ever inverted explicitly: explicit inverses (128 x
+// 128 or even 32 x 32 diagonal blocks) measured 1.6-1.9e-10 solve backward
+// error on cfg4 IGA against 4e-12 for substitution.
 // ---------------------------------------------------------------------------
 constexpr int kDB = 128;
 constexpr int kDBP = kDB + 1;
-constexpr int kXB = 32 * 33;  // one 32 x 32 inverse, pitch 33: X_b(r, c) at [c * 33 + r]
-constexpr size_t kDiag128Smem = ((size_t)kDB * kDBP + kDB + 4 * kXB) * sizeof(double);
-constexpr size_t kTrsmSmem = (size_t)4 * kDB * 33 * sizeof(double);  // 4 warps x nb columns x 32 rows (pitch 33)
+constexpr size_t kDiag128Smem = ((size_t)kDB * kDBP + kDB) * sizeof(double);
+constexpr size_t kTrsmSmem = ((size_t)kDB * kDBP + kDB + 2 * (size_t)kDB * 33) * sizeof(double);
 
 // acc(i, j) += sum_{t < kcount} fa(i, t) fb(t, j) for a 32 x 32 warp tile (kcount % 4 == 0)
 template <class FA, class FB>
@@ -588,51 +586,61 @@ __device__ __forceinline__ void zero_acc(double (&acc)[4][4][2]) {
       }
 
 // Warp: unblocked LDL^T of the 32 x 32 lower block at A[c * ld + r] (r >= c) in
-// registers (lane = row), then X = inv(L) (unit lower, lane = column) into
-// Xs[c * 33 + r]; L (strict lower) and d (diagonal) are written back to A.
-__device__ __forceinline__ void warp_ldl32(double* A, int ld, double* Xs, double& d_out) {
+// registers (lane = row); L (strict lower) and d (diagonal) are written back.
+// The pivot steps are template instances (compile-time indices), so the
+// register array never falls back to local memory.
+template <int K>
+__device__ __forceinline__ void ldl32_step(double (&a)[32], int lane, double& dl) {
+  const double dk = __shfl_sync(0xffffffffu, a[K], K);
+  const double lk = a[K] / dk;
+#pragma unroll
+  for (int j = K + 1; j < 32; ++j) {
+    const double ajk = __shfl_sync(0xffffffffu, a[K], j);  // A(j, K), not yet scaled
+    if (lane >= j) a[j] = fma(-lk, ajk, a[j]);
+  }
+  if (lane == K) dl = dk;
+  if (lane > K) a[K] = lk;
+}
+
+// One row of a 32-column block solve by substitution: w[c] <- (w[c] - sum_{t<c} w[t] d(t) L(c, t)) / d(c),
+// i.e. row L(r, kb:kb+32) = A(r, kb:kb+32) L_bb^{-T} D_b^{-1} with compile-time column indices.
+template <int C, class FL, class FD>
+__device__ __forceinline__ void sub32_col(double (&w)[32], FL L, FD d) {
+  double v = w[C];
+#pragma unroll
+  for (int t = 0; t < C; ++t) v = fma(-w[t] * d(t), L(C, t), v);
+  w[C] = v / d(C);
+}
+
+template <class FL, class FD, int... C>
+__device__ __forceinline__ void sub32_all(double (&w)[32], FL L, FD d, std::integer_sequence<int, C...>) {
+  (sub32_col<C>(w, L, d), ...);
+}
+
+template <int... K>
+__device__ __forceinline__ void ldl32_all(double (&a)[32], int lane, double& dl, std::integer_sequence<int, K...>) {
+  (ldl32_step<K>(a, lane, dl), ...);
+}
+
+__device__ __forceinline__ void warp_ldl32(double* A, int ld, double& d_out) {
   const int lane = threadIdx.x & 31;
+  double dl = 0.0;
   double a[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) a[j] = j <= lane ? A[j * ld + lane] : 0.0;
-  double dl = 0.0;
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const double dk = __shfl_sync(0xffffffffu, a[k], k);
-    const double lk = a[k] / dk;
-#pragma unroll
-    for (int j = k + 1; j < 32; ++j) {
-      const double ajk = __shfl_sync(0xffffffffu, a[k], j);  // A(j, k), not yet scaled
-      if (lane >= j) a[j] = fma(-lk, ajk, a[j]);
-    }
-    if (lane == k) dl = dk;
-    if (lane > k) a[k] = lk;
-  }
-  // X = inv(L): lane owns column c = lane: x_r = [r == c] - sum_{t < r} L(r, t) x_t
-  double x[32];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    double v = r == lane ? 1.0 : 0.0;
-#pragma unroll
-    for (int t = 0; t < r; ++t) v = fma(-__shfl_sync(0xffffffffu, a[t], r), x[t], v);
-    x[r] = v;
-  }
+  ldl32_all(a, lane, dl, std::make_integer_sequence<int, 32>{});
 #pragma unroll
   for (int j = 0; j < 32; ++j)
     if (j <= lane) A[j * ld + lane] = j == lane ? dl : a[j];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) Xs[lane * 33 + r] = x[r];
   d_out = dl;
 }
 
 __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
                                                  const double* __restrict__ tol, double* __restrict__ panel,
-                                                 double* __restrict__ D, int64_t* __restrict__ stat,
-                                                 double* __restrict__ xbuf) {
+                                                 double* __restrict__ D, int64_t* __restrict__ stat) {
   extern __shared__ double sm[];
   double* A = sm;               // A[c * kDBP + r], lower triangle
   double* dd = A + kDB * kDBP;  // pivots
-  double* Xs = dd + kDB;        // the four 32 x 32 diagonal inverses
   const int s = nodes[blockIdx.x];
   const int64_t f = S.front[s], np = S.ncol[s];
   if (kbo >= np) return;
@@ -647,26 +655,26 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
   }
   __syncthreads();
   for (int kb = 0; kb < nbp; kb += 32) {
-    double* Xk = Xs + (kb / 32) * kXB;
     if (warp == 0) {
       double dl;
-      warp_ldl32(A + kb * kDBP + kb, kDBP, Xk, dl);
+      warp_ldl32(A + kb * kDBP + kb, kDBP, dl);
       dd[kb + lane] = dl;
     }
     __syncthreads();
-    // rows below the sub-block inside the block: L = A X^T D^{-1}, 32-row tiles on DMMA
+    // rows below the sub-block inside the block: substitution, thread per row
     const int nr = nbp - kb - 32;
-    if (warp < nr / 32) {
-      const int i0 = kb + 32 + 32 * warp;
-      double acc[4][4][2];
-      zero_acc(acc);
-      warp_mma32(acc, [&](int i, int k) { return A[(kb + k) * kDBP + i0 + i]; },
-                 [&](int k, int j) { return Xk[k * 33 + j]; }, 32);  // X(j, k) at [k * 33 + j]
-      __syncwarp();
-      RIGA_ACC_FOR(A[(kb + aj) * kDBP + i0 + ai] = acc[m][q][e] / dd[kb + aj];)
+    if (tid < nr) {
+      const int r = kb + 32 + tid;
+      double w[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) w[c] = A[(kb + c) * kDBP + r];
+      sub32_all(w, [&](int c, int t) { return A[(kb + t) * kDBP + kb + c]; }, [&](int t) { return dd[kb + t]; },
+                std::make_integer_sequence<int, 32>{});
+#pragma unroll
+      for (int c = 0; c < 32; ++c) A[(kb + c) * kDBP + r] = w[c];
     }
     __syncthreads();
-    // the rest of the block -= L D L^T (rank 32): 32 x 32 lower tiles, one per warp
+    // the rest of the block -= L D L^T (rank 32): 32 x 32 lower tiles on DMMA, one per warp
     const int n3 = nr / 32;
     for (int t = warp; t < n3 * (n3 + 1) / 2; t += 8) {
       int ti = 0;
@@ -698,55 +706,57 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
     const int c = idx / nb, r = idx - c * nb;
     if (r >= c) P[(int64_t)c * f + r] = A[c * kDBP + r];
   }
-  double* xb = xbuf + (int64_t)blockIdx.x * 4 * kXB;
-  for (int idx = tid; idx < (nbp / 32) * kXB; idx += blockDim.x) xb[idx] = Xs[idx];
 }
 
-// L21 = A21 L11^{-T} D^{-1} for the rows below the block, by blocked substitution: each warp owns 32
-// rows (independent of the others), its nb columns staged in shared memory.
-__global__ void __launch_bounds__(128) k_trsm128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
-                                                 double* __restrict__ panel, const double* __restrict__ D,
-                                                 const double* __restrict__ xbuf) {
+// L21 = A21 L11^{-T} D^{-1} for the rows below the block, by blocked substitution.  The CTA stages L11 and
+// its pivots in shared memory; each of its 2 warps owns 32 rows (independent of the other): per 32-column
+// step b, T = A_b - sum_{t<b} W_t D_t L_bt^T on DMMA, then W_b = T L_bb^{-T} D_b^{-1} row by row
+// (lane = row, compile-time column indices).
+constexpr int kTrsmWarps = 2;
+__global__ void __launch_bounds__(32 * kTrsmWarps) k_trsm128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
+                                                             double* __restrict__ panel, const double* __restrict__ D) {
   extern __shared__ double sm[];
   const int s = nodes[blockIdx.y];
   const int64_t f = S.front[s], np = S.ncol[s];
   if (kbo >= np) return;
   const int nb = (int)imin(kDB, np - kbo);
   const int nbp = (nb + 31) & ~31;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t r0 = kbo + nb + (int64_t)blockIdx.x * 128 + 32 * warp;
-  if (r0 >= f) return;
-  const int nr = (int)imin(32, f - r0);
+  const int64_t rbase = kbo + nb + (int64_t)blockIdx.x * 32 * kTrsmWarps;
+  if (rbase >= f) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t col0 = S.col0[s];
-  const double* dk = D + col0 + kbo;
-  const double* Lb = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;  // L11(r, c) at Lb[c f + r]
-  double* Pr = panel + S.panel_off[s] + (int64_t)kbo * f + r0;         // A21(row, c) at Pr[c f + row]
-  const double* xb = xbuf + (int64_t)blockIdx.y * 4 * kXB;
-  double* W = sm + warp * kDB * 33;  // W[c * 33 + row], this warp's rows x nbp columns
+  double* Ls = sm;                // L11(r, c) at Ls[c * kDBP + r] (strict lower), pivots after
+  double* ds = Ls + kDB * kDBP;
+  double* W = ds + kDB + warp * kDB * 33;  // W[c * 33 + row]: this warp's rows x nbp columns
+  const double* Lb = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;
+  for (int idx = tid; idx < nbp * nbp; idx += blockDim.x) {
+    const int c = idx / nbp, r = idx - c * nbp;
+    if (r > c) Ls[c * kDBP + r] = (r < nb && c < nb) ? Lb[(int64_t)c * f + r] : 0.0;
+  }
+  for (int c = tid; c < nbp; c += blockDim.x) ds[c] = c < nb ? D[col0 + kbo + c] : 1.0;
+  const int64_t r0 = rbase + 32 * warp;
+  const int nr = (int)imin(32, imin(f - r0, 32));
+  double* Pr = panel + S.panel_off[s] + (int64_t)kbo * f + r0;  // A21(row, c) at Pr[c f + row]
   for (int c = 0; c < nbp; ++c) W[c * 33 + lane] = (c < nb && lane < nr) ? Pr[(int64_t)c * f + lane] : 0.0;
-  __syncwarp();
+  __syncthreads();
+  if (r0 >= f) return;
   for (int kb = 0; kb < nbp; kb += 32) {
-    double acc[4][4][2];
-    RIGA_ACC_FOR(acc[m][q][e] = W[(kb + aj) * 33 + ai];)
-    if (kb > 0) {  // T = A_b - sum_{t < b} W_t D_t L_bt^T
-      double neg[4][4][2];
-      zero_acc(neg);
-      warp_mma32(neg, [&](int i, int k) { return W[k * 33 + i] * dk[k]; },
-                 [&](int k, int j) { return kb + j < nb ? Lb[(int64_t)k * f + kb + j] : 0.0; }, kb);
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[m][q][0] -= neg[m][q][0], acc[m][q][1] -= neg[m][q][1];
+    if (kb > 0) {  // W_b -= sum_{t < b} W_t D_t L_bt^T
+      double acc[4][4][2];
+      zero_acc(acc);
+      warp_mma32(acc, [&](int i, int k) { return W[k * 33 + i] * ds[k]; },
+                 [&](int k, int j) { return Ls[k * kDBP + kb + j]; }, kb);
+      __syncwarp();
+      RIGA_ACC_FOR(W[(kb + aj) * 33 + ai] -= acc[m][q][e];)
+      __syncwarp();
     }
-    __syncwarp();
-    RIGA_ACC_FOR(W[(kb + aj) * 33 + ai] = acc[m][q][e];)
-    __syncwarp();
-    const double* Xk = xb + (kb / 32) * kXB;  // W_b = T X_b^T D_b^{-1}
-    zero_acc(acc);
-    warp_mma32(acc, [&](int i, int k) { return W[(kb + k) * 33 + i]; },
-               [&](int k, int j) { return Xk[k * 33 + j]; }, 32);
-    __syncwarp();
-    RIGA_ACC_FOR(W[(kb + aj) * 33 + ai] = kb + aj < nb ? acc[m][q][e] / dk[kb + aj] : 0.0;)
+    double w[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) w[c] = W[(kb + c) * 33 + lane];
+    sub32_all(w, [&](int c, int t) { return Ls[(kb + t) * kDBP + kb + c]; }, [&](int t) { return ds[kb + t]; },
+              std::make_integer_sequence<int, 32>{});
+#pragma unroll
+    for (int c = 0; c < 32; ++c) W[(kb + c) * 33 + lane] = w[c];
     __syncwarp();
   }
   for (int c = 0; c < nb; ++c)
@@ -929,11 +939,6 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   RIGA_CUDA(cudaGetLastError());
   double* cbuf = nullptr;
   if (h.cb_total) RIGA_CUDA(cudaMallocAsync(&cbuf, h.cb_total * sizeof(double), st));
-  // per large front of a level: X = inv(L11) of its current 128-column block
-  int64_t max_nl = 0;
-  for (const LevelPlan& P : sym->plan) max_nl = std::max<int64_t>(max_nl, P.nlarge);
-  double* xbuf = nullptr;
-  if (max_nl && !g_old_path) RIGA_CUDA(cudaMallocAsync(&xbuf, max_nl * 4 * kXB * sizeof(double), st));
   if (h.panel_large) RIGA_CUDA(cudaMemsetAsync(F->panel.p, 0, h.panel_large * 8, st));
   if (sym->n_large) {
     k_asm_large<<<(unsigned)sym->n_large, 256, 0, st>>>(S, sym->d_large_nodes.p, Kv, Mv, sigma,
@@ -969,9 +974,9 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
       const unsigned nl = (unsigned)P.nlarge;
       for (int64_t kbo = 0; kbo < P.max_np_large; kbo += kDB) {
-        k_diag128<<<nl, 256, kDiag128Smem, st>>>(S, ln, (int)kbo, F->tol.p, F->panel.p, F->D.p, F->stat.p, xbuf);
-        const unsigned nti = (unsigned)((P.max_f_large - kbo + 127) / 128);
-        k_trsm128<<<dim3(nti, nl), 128, kTrsmSmem, st>>>(S, ln, (int)kbo, F->panel.p, F->D.p, xbuf);
+        k_diag128<<<nl, 256, kDiag128Smem, st>>>(S, ln, (int)kbo, F->tol.p, F->panel.p, F->D.p, F->stat.p);
+        const unsigned nti = (unsigned)((P.max_f_large - kbo + 32 * kTrsmWarps - 1) / (32 * kTrsmWarps));
+        k_trsm128<<<dim3(nti, nl), 32 * kTrsmWarps, kTrsmSmem, st>>>(S, ln, (int)kbo, F->panel.p, F->D.p);
         count_launch(2);
         const int64_t m0 = kbo + kDB;
         if (m0 < P.max_np_large) {
@@ -1046,7 +1051,6 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
     }
   }
   if (cbuf) RIGA_CUDA(cudaFreeAsync(cbuf, st));
-  if (xbuf) RIGA_CUDA(cudaFreeAsync(xbuf, st));
   RIGA_CUDA(cudaFreeAsync(scratch, st));
   return build_chain_inverse(F, st);
 }
