@@ -218,15 +218,18 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// EPI 0: C -= acc (the Schur-complement updates); EPI 1: C = acc / dj[j] (the blocked TRSM
-// L21 = A21 X^T D^{-1}; C may alias A: a CTA's rows are read completely before its epilogue writes).
+// EPI 0: C -= acc (the Schur-complement updates); EPI 1: C = acc / dj[j] (C may alias A: a CTA's
+// rows are read completely before its epilogue writes); EPI 2: C -= acc with columns j >= jsplit
+// going to C2 (ld ldc2, rows and columns offset by jsplit): a front's pivot columns and its update
+// block in one trailing update.
 template <int EPI = 0>
 __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64_t lda,
                                              const double* __restrict__ B, int64_t ldb,
                                              const double* __restrict__ d, int64_t k0, int64_t k1,
                                              int64_t i0, int64_t j0, int64_t mend, int64_t nend,
                                              double* C, int64_t ldc, int64_t coff,
-                                             double* __restrict__ smem, const double* __restrict__ dj = nullptr) {
+                                             double* __restrict__ smem, const double* __restrict__ dj = nullptr,
+                                             double* C2 = nullptr, int64_t ldc2 = 0, int64_t jsplit = 0) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;
   double acc[8][4][2];
@@ -309,6 +312,17 @@ __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64
       if (EPI == 0) {
         if (j < nend) C[(j - coff) * ldc + (i - coff)] -= acc[m][q][0];
         if (j + 1 < nend) C[(j + 1 - coff) * ldc + (i - coff)] -= acc[m][q][1];
+      } else if (EPI == 2) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t je = j + e;
+          if (je < nend && je <= i) {
+            if (je < jsplit)
+              C[je * ldc + i] -= acc[m][q][e];
+            else
+              C2[(je - jsplit) * ldc2 + (i - jsplit)] -= acc[m][q][e];
+          }
+        }
       } else {
         if (j < nend) C[(j - coff) * ldc + (i - coff)] = acc[m][q][0] / dj[j];
         if (j + 1 < nend) C[(j + 1 - coff) * ldc + (i - coff)] = acc[m][q][1] / dj[j + 1];

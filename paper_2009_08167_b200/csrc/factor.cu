@@ -763,19 +763,40 @@ __global__ void __launch_bounds__(32 * kTrsmWarps) k_trsm128(SymDev S, const int
     if (lane < nr) Pr[(int64_t)c * f + lane] = W[c * 33 + lane];
 }
 
-// trailing pivot columns [kbo + nb, n_p) -= L21 D L21^T over the block's nb columns (rows to f)
-__global__ void __launch_bounds__(256, 1) k_trail128(SymDev S, const int32_t* __restrict__ nodes, int kbo, int ntj,
-                                                     double* __restrict__ panel, const double* __restrict__ D) {
+// Trailing update of a front over its pivot columns [k0, min(k1, n_p)), lower triangle, rows to f.
+//   narrow (wide = 0): the columns [c0, min(c1, n_p)) -- the rest of the current outer block;
+//   wide   (wide = 1): every column right of min(c0, n_p) -- the remaining pivot columns and the update
+//                      block (columns >= n_p live in the front's update block, so the update block takes
+//                      its Schur complement slice by slice with the pivot columns instead of one long-K
+//                      pass at the end).
+// tri != 0: blockIdx.x enumerates the lower tiles of a triangle of ntj x ntj tiles.
+__global__ void __launch_bounds__(256, 1) k_trail128(SymDev S, const int32_t* __restrict__ nodes, int64_t k0,
+                                                     int64_t k1, int64_t c0, int64_t c1, int wide, int ntj,
+                                                     int tri, double* __restrict__ panel, double* __restrict__ cb,
+                                                     const double* __restrict__ D) {
   extern __shared__ double sm[];
   const int s = nodes[blockIdx.y];
   const int64_t f = S.front[s], np = S.ncol[s];
-  const int64_t m0 = kbo + kDB;
-  if (m0 >= np) return;
-  const int64_t ti = blockIdx.x / ntj, tj = blockIdx.x % ntj;
-  const int64_t i0 = m0 + ti * kT128, j0 = m0 + tj * kT128;
-  if (i0 >= f || j0 >= np || i0 + kT128 - 1 < j0) return;
+  const int64_t kend = imin(k1, np);
+  if (k0 >= kend) return;
+  const int64_t cs = imin(c0, np), ce = wide ? f : imin(c1, np);
+  if (cs >= ce) return;
+  int64_t ti, tj;
+  if (tri) {
+    const int64_t t = blockIdx.x;
+    ti = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (ti * (ti + 1) / 2 > t) --ti;
+    tj = t - ti * (ti + 1) / 2;
+  } else {
+    ti = blockIdx.x / ntj;
+    tj = blockIdx.x % ntj;
+  }
+  const int64_t i0 = cs + ti * kT128, j0 = cs + tj * kT128;
+  if (i0 >= f || j0 >= ce || i0 + kT128 - 1 < j0) return;
   double* L = panel + S.panel_off[s];
-  dmma_tile128<0>(L, f, L, f, D + S.col0[s], kbo, m0, i0, j0, f, np, L, f, 0, sm);
+  dmma_tile128<2>(L, f, L, f, D + S.col0[s], k0, kend, i0, j0, f, ce, L, f, 0, sm, nullptr, cb + S.cb_off[s],
+                  f - np, np);
 }
 
 // ---------------------------------------------------------------------------
@@ -888,6 +909,7 @@ static bool g_block_path = true;  // RIGA_FACTOR_PANEL=32: the 32-column panel c
 static bool g_tile128 = true;      // RIGA_FACTOR_TILE128=0: 64 x 64 tiles for the update blocks
 static bool g_left_looking = false;  // RIGA_PANEL_LL=1: left-looking in-block panel updates (no k_syrk<0>; measured no gain)
 static bool g_old_path = false;  // RIGA_FACTOR_OLD=1: the 32-column panel chain (A/B)
+static int64_t g_nb2 = 256;      // outer block of the trailing updates (multiple of 128; RIGA_FACTOR_NB2)
 static int64_t g_block_max_fronts = 0;  // RIGA_FACTOR_BLOCK_FRONTS=n: block path for levels with <= n large fronts (opt-in: slower today)
 
 static int set_smem_attrs() {
@@ -900,6 +922,8 @@ static int set_smem_attrs() {
     g_tile128 = !(e && std::strcmp(e, "0") == 0);
     e = getenv("RIGA_PANEL_LL");
     g_left_looking = e && std::strcmp(e, "1") == 0;
+    e = getenv("RIGA_FACTOR_NB2");
+    if (e && atoll(e) >= 128) g_nb2 = atoll(e) / 128 * 128;
     e = getenv("RIGA_FACTOR_OLD");
     g_old_path = e && std::strcmp(e, "1") == 0;
     e = getenv("RIGA_FACTOR_BLOCK_FRONTS");
@@ -973,19 +997,32 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
     if (P.nlarge && !g_old_path) {
       const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
       const unsigned nl = (unsigned)P.nlarge;
-      for (int64_t kbo = 0; kbo < P.max_np_large; kbo += kDB) {
-        k_diag128<<<nl, 256, kDiag128Smem, st>>>(S, ln, (int)kbo, F->tol.p, F->panel.p, F->D.p, F->stat.p);
-        const unsigned nti = (unsigned)((P.max_f_large - kbo + 32 * kTrsmWarps - 1) / (32 * kTrsmWarps));
-        k_trsm128<<<dim3(nti, nl), 32 * kTrsmWarps, kTrsmSmem, st>>>(S, ln, (int)kbo, F->panel.p, F->D.p);
-        count_launch(2);
-        const int64_t m0 = kbo + kDB;
-        if (m0 < P.max_np_large) {
-          const int64_t ti = (P.max_f_large - m0 + kT128 - 1) / kT128, tj = (P.max_np_large - m0 + kT128 - 1) / kT128;
-          k_trail128<<<dim3((unsigned)(ti * tj), nl), 256, kT128Smem, st>>>(S, ln, (int)kbo, (int)tj, F->panel.p,
-                                                                            F->D.p);
-          count_launch();
-        }
+      auto trail = [&](int64_t k0, int64_t k1, int64_t c0, int64_t c1, bool wide) -> int {
+        // rows [c0', f) with c0' = min(c0, n_p) per front: tile counts bounded over the level's fronts
+        const int64_t rows = wide ? std::max(P.max_f_large - c0, P.max_nu_large) : P.max_f_large - c0;
+        const int64_t nti = (rows + kT128 - 1) / kT128;
+        if (nti <= 0) return RIGA_OK;
+        const int64_t ntj = wide ? nti : (c1 - c0 + kT128 - 1) / kT128;
+        const int64_t ntiles = wide ? nti * (nti + 1) / 2 : nti * ntj;
+        k_trail128<<<dim3((unsigned)ntiles, nl), 256, kT128Smem, st>>>(S, ln, k0, k1, c0, c1, wide ? 1 : 0, (int)ntj,
+                                                                       wide ? 1 : 0, F->panel.p, cbuf, F->D.p);
+        count_launch();
         RIGA_CUDA(cudaGetLastError());
+        return RIGA_OK;
+      };
+      for (int64_t kbo = 0; kbo < P.max_np_large; kbo += g_nb2) {
+        const int64_t kend = std::min<int64_t>(kbo + g_nb2, P.max_np_large);
+        for (int64_t kb = kbo; kb < kend; kb += kDB) {
+          k_diag128<<<nl, 256, kDiag128Smem, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p, F->D.p, F->stat.p);
+          const unsigned nti = (unsigned)((P.max_f_large - kb + 32 * kTrsmWarps - 1) / (32 * kTrsmWarps));
+          k_trsm128<<<dim3(nti, nl), 32 * kTrsmWarps, kTrsmSmem, st>>>(S, ln, (int)kb, F->panel.p, F->D.p);
+          count_launch(2);
+          RIGA_CUDA(cudaGetLastError());
+          // the block's remaining columns take this 128-column slice now (narrow, K = 128)
+          if (kb + kDB < kend) RIGA_TRY(trail(kb, kb + kDB, kb + kDB, kbo + g_nb2, false));
+        }
+        // everything right of the block -- pivot columns and update block -- in one K = g_nb2 slice
+        RIGA_TRY(trail(kbo, kbo + g_nb2, kbo + g_nb2, 0, true));
       }
     } else if (P.nlarge) {
       const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
@@ -1035,7 +1072,7 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
         }
       }
     }
-    if (P.nlarge) {
+    if (P.nlarge && g_old_path) {
       const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
       const unsigned nl = (unsigned)P.nlarge;
       if (P.max_nu_large > 0 && g_tile128 && P.max_np_large >= 128 && P.max_nu_large >= 256) {
@@ -1266,7 +1303,7 @@ int riga_factor_create(riga_ctx* ctx, riga_symbolic* sym, double sigma, double r
 int riga_factor_solve(riga_factor* f, const double* b, double* x) {
   RIGA_CHECK_ARG(f && b && x, "null arg");
   DeviceGuard g(f->ctx->device);
-  return factor_solve(f, f->ctx->stream, b, x);
+  return factor_solve(f, f->ctx->stream, b, x, false, true);
 }
 
 int riga_factor_time_ms(riga_factor* f, float* ms) {

@@ -152,8 +152,11 @@ int system_spmv(riga_system* sys, cudaStream_t s, int which, double sigma, const
 int kron_mass_apply(riga_system* sys, cudaStream_t s, const double* x, double* y, double* t1, double* t2);
 int csr_spmv(cudaStream_t s, int64_t n, const int64_t* rowptr, const int32_t* colidx,
              const double* val, const double* x, double* y);
-int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x,
-                 bool b_permuted = false);
+// accurate: every chain supernode takes the local refinement step (the API
+// solves); otherwise only those the factor-time probe flagged (the Lanczos
+// steps, whose accuracy the residual gate covers)
+int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x, bool b_permuted = false,
+                 bool accurate = false);
 int build_solve_plan(riga_symbolic* sym);
 int prepare_solve();
 int upload_solve_plan(riga_symbolic* sym, cudaStream_t s);

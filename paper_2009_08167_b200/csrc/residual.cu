@@ -177,7 +177,7 @@ int riga_factor_solve_many(riga_ctx* ctx, riga_factor* f, const double* B_dev, i
     RIGA_CUDA(cudaStreamWaitEvent(s, ev, 0));
     cudaEventDestroy(ev);
   }
-  for (int64_t j = 0; j < nrhs; ++j) RIGA_TRY(factor_solve(f, s, B_dev + j * ldb, X_dev + j * ldx));
+  for (int64_t j = 0; j < nrhs; ++j) RIGA_TRY(factor_solve(f, s, B_dev + j * ldb, X_dev + j * ldx, false, true));
   if (s != f->ctx->stream) {
     // later work on the factor's stream sees these solves' workspace use done
     cudaEvent_t ev;

@@ -1097,7 +1097,10 @@ __global__ void __launch_bounds__(256) k_inv_bwd(SymDev S, const int2* __restric
 // Factor-time accuracy probe of each chain inverse: u = inv~ v for a fixed v, then
 // err[s] = max_i |(L11 u)_i - v_i| / max|v| (the solve's local backward error on
 // this supernode).  Supernodes above RIGA_INV_FIX_TOL (1e-11) get the refinement step.
-__device__ __forceinline__ double chk_v(int k) { return 1.0 + (double)((k * 7919) % 13) / 13.0; }
+__device__ __forceinline__ double chk_v(int k) {  // pseudo-random signs and magnitudes in [0.5, 1)
+  const unsigned h = (unsigned)k * 2654435761u;
+  return ((h >> 31) ? -1.0 : 1.0) * (0.5 + (double)((h >> 8) & 0xffff) / 131072.0);
+}
 
 __global__ void __launch_bounds__(256) k_inv_chk1(SymDev S, const int2* __restrict__ tasks,
                                                   const int64_t* __restrict__ inv_off,
@@ -1150,7 +1153,7 @@ __global__ void __launch_bounds__(256) k_inv_chk2(SymDev S, const int2* __restri
       double t = u[col0 + i];
 #pragma unroll
       for (int q = 0; q < 8; ++q) t += part[q][lane];
-      e = fabs(t - chk_v(i)) / 2.0;  // max|v| < 2
+      e = fabs(t - chk_v(i));  // max|v| < 1
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
@@ -1165,7 +1168,7 @@ __global__ void __launch_bounds__(256) k_inv_fix_fwd_res(SymDev S, SolveDev T, c
   extern __shared__ double zsh[];
   __shared__ double part[8][32];
   pdl_start();
-  if (!flag[tasks[blockIdx.x].x]) return;
+  if (flag && !flag[tasks[blockIdx.x].x]) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = tasks[blockIdx.x].x;
   const int np = (int)S.ncol[s];
@@ -1206,7 +1209,7 @@ __global__ void __launch_bounds__(256) k_inv_fix_fwd_apply(SymDev S, const int2*
   extern __shared__ double y[];
   __shared__ double part[8][32];
   pdl_start();
-  if (!flag[tasks[blockIdx.x].x]) return;
+  if (flag && !flag[tasks[blockIdx.x].x]) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = tasks[blockIdx.x].x;
   const int np = (int)S.ncol[s];
@@ -1240,7 +1243,7 @@ __global__ void __launch_bounds__(256) k_inv_fix_bwd_res(SymDev S, const int2* _
                                                          const double* __restrict__ cvec,
                                                          const double* __restrict__ xp, double* __restrict__ rfix) {
   pdl_start();
-  if (!flag[tasks[blockIdx.x].x]) return;
+  if (flag && !flag[tasks[blockIdx.x].x]) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int s = tasks[blockIdx.x].x;
   const int np = (int)S.ncol[s];
@@ -1264,7 +1267,7 @@ __global__ void __launch_bounds__(256) k_inv_fix_bwd_apply(SymDev S, const int2*
                                                            const double* __restrict__ rfix, double* __restrict__ xp,
                                                            double* __restrict__ x) {
   pdl_start();
-  if (!flag[tasks[blockIdx.x].x]) return;
+  if (flag && !flag[tasks[blockIdx.x].x]) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int s = tasks[blockIdx.x].x;
   const int np = (int)S.ncol[s];
@@ -1632,7 +1635,7 @@ extern "C" int riga_set_solve_sub_levels(int levels) {
 
 namespace riga {
 
-int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bool b_permuted) {
+int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bool b_permuted, bool accurate) {
   riga_symbolic* sym = F->sym;
   const SymbolicHost& h = sym->h;
   const SolvePlanHost& L = sym->sp;
@@ -1665,10 +1668,11 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
       RIGA_CUDA(launch(k_inv_fwd, ni, 256, L.ifwd_smem[l], st, S, T, it, sym->d_inv_off.p, F->linv.p, F->D.p, b,
                        F->xperm.p, F->upd.p, F->cvec.p));
       count_launch();
-      if (L.inv_fix && F->fix_level[l]) {
-        RIGA_CUDA(launch(k_inv_fix_fwd_res, ni, 256, L.ifwd_smem[l], st, S, T, it, F->fix_flag.p, F->panel.p, b,
+      if (L.inv_fix && (accurate || F->fix_level[l])) {
+        const int* fl = accurate ? nullptr : F->fix_flag.p;
+        RIGA_CUDA(launch(k_inv_fix_fwd_res, ni, 256, L.ifwd_smem[l], st, S, T, it, fl, F->panel.p, b,
                          F->xperm.p, F->upd.p, F->rfix.p));
-        RIGA_CUDA(launch(k_inv_fix_fwd_apply, ni, 256, L.ifwd_smem[l], st, S, it, F->fix_flag.p, sym->d_inv_off.p,
+        RIGA_CUDA(launch(k_inv_fix_fwd_apply, ni, 256, L.ifwd_smem[l], st, S, it, fl, sym->d_inv_off.p,
                          F->linv.p, F->D.p, F->rfix.p, F->xperm.p, F->cvec.p));
         count_launch(2);
       }
@@ -1701,10 +1705,11 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
       const int2* it = reinterpret_cast<const int2*>(sym->d_ibwd.p) + L.ibwd_ptr[l];
       RIGA_CUDA(launch(k_inv_bwd, ni, 256, 0, st, S, it, sym->d_inv_off.p, F->linv.p, F->cvec.p, F->xperm.p, x));
       count_launch();
-      if (L.inv_fix && F->fix_level[l]) {
-        RIGA_CUDA(launch(k_inv_fix_bwd_res, ni, 256, 0, st, S, it, F->fix_flag.p, F->panel.p, F->cvec.p, F->xperm.p,
+      if (L.inv_fix && (accurate || F->fix_level[l])) {
+        const int* fl = accurate ? nullptr : F->fix_flag.p;
+        RIGA_CUDA(launch(k_inv_fix_bwd_res, ni, 256, 0, st, S, it, fl, F->panel.p, F->cvec.p, F->xperm.p,
                          F->rfix.p));
-        RIGA_CUDA(launch(k_inv_fix_bwd_apply, ni, 256, 0, st, S, it, F->fix_flag.p, sym->d_inv_off.p, F->linv.p,
+        RIGA_CUDA(launch(k_inv_fix_bwd_apply, ni, 256, 0, st, S, it, fl, sym->d_inv_off.p, F->linv.p,
                          F->rfix.p, F->xperm.p, x));
         count_launch(2);
       }
