@@ -218,25 +218,40 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// EPI 0: C -= acc (the Schur-complement updates); EPI 1: C = acc / dj[j] (C may alias A: a CTA's
-// rows are read completely before its epilogue writes); EPI 2: C -= acc with columns j >= jsplit
-// going to C2 (ld ldc2, rows and columns offset by jsplit): a front's pivot columns and its update
-// block in one trailing update.
+// EPI 0: C(i - coff, j - coff) -= A d B^T; EPI 2: the same with the columns j >= jsplit going to C2
+// (ld ldc2, rows and columns offset by jsplit) and only i >= j touched (a front's pivot columns and its
+// update block in one trailing update).  The C tile is loaded into the accumulators before the K loop
+// (its 64 loads per thread in flight together, overlapping the pipeline prologue) and the MMAs subtract
+// (negated A fragments), so the epilogue is stores only.
 template <int EPI = 0>
 __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64_t lda,
                                              const double* __restrict__ B, int64_t ldb,
                                              const double* __restrict__ d, int64_t k0, int64_t k1,
                                              int64_t i0, int64_t j0, int64_t mend, int64_t nend,
                                              double* C, int64_t ldc, int64_t coff,
-                                             double* __restrict__ smem, const double* __restrict__ dj = nullptr,
-                                             double* C2 = nullptr, int64_t ldc2 = 0, int64_t jsplit = 0) {
+                                             double* __restrict__ smem, double* C2 = nullptr, int64_t ldc2 = 0,
+                                             int64_t jsplit = 0) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;
+  const int r = lane >> 2, cc = (lane & 3) * 2;
+  auto cptr = [&](int64_t i, int64_t j) -> double* {
+    if (i >= mend || j >= nend) return nullptr;
+    if (EPI == 2) {
+      if (j > i) return nullptr;
+      return j < jsplit ? C + j * ldc + i : C2 + (j - jsplit) * ldc2 + (i - jsplit);
+    }
+    return C + (j - coff) * ldc + (i - coff);
+  };
   double acc[8][4][2];
 #pragma unroll
   for (int m = 0; m < 8; ++m)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double* p = cptr(i0 + wm * 64 + m * 8 + r, j0 + wn * 32 + q * 8 + cc + e);
+        acc[m][q][e] = p ? *p : 0.0;
+      }
   const int64_t nk = (k1 - k0 + kT128K - 1) / kT128K;
   auto stage_ptr = [&](int s) { return smem + (int64_t)s * kT128StageDoubles; };
   // thread -> (k row kr0 + 2u, column ci) of a stage; row/column predicates fixed per thread
@@ -287,10 +302,10 @@ __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
       const int kr = k4 * 4 + (lane & 3);
-      const double dk = Ds[kr];
+      const double ndk = -Ds[kr];
       double av[8], bv[4];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) av[m] = As[kr * kT128P + wm * 64 + m * 8 + (lane >> 2)] * dk;
+      for (int m = 0; m < 8; ++m) av[m] = As[kr * kT128P + wm * 64 + m * 8 + (lane >> 2)] * ndk;
 #pragma unroll
       for (int q = 0; q < 4; ++q) bv[q] = Bs[kr * kT128P + wn * 32 + q * 8 + (lane >> 2)];
 #pragma unroll
@@ -300,35 +315,15 @@ __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64
     }
   }
   cp_async_wait<0>();
-  if (EPI == 1) __syncthreads();  // in-place: every warp's operand reads precede the writes
-  const int r = lane >> 2, cc = (lane & 3) * 2;
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const int64_t i = i0 + wm * 64 + m * 8 + r;
-    if (i >= mend) continue;
+  for (int m = 0; m < 8; ++m)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t j = j0 + wn * 32 + q * 8 + cc;
-      if (EPI == 0) {
-        if (j < nend) C[(j - coff) * ldc + (i - coff)] -= acc[m][q][0];
-        if (j + 1 < nend) C[(j + 1 - coff) * ldc + (i - coff)] -= acc[m][q][1];
-      } else if (EPI == 2) {
+    for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t je = j + e;
-          if (je < nend && je <= i) {
-            if (je < jsplit)
-              C[je * ldc + i] -= acc[m][q][e];
-            else
-              C2[(je - jsplit) * ldc2 + (i - jsplit)] -= acc[m][q][e];
-          }
-        }
-      } else {
-        if (j < nend) C[(j - coff) * ldc + (i - coff)] = acc[m][q][0] / dj[j];
-        if (j + 1 < nend) C[(j + 1 - coff) * ldc + (i - coff)] = acc[m][q][1] / dj[j + 1];
+      for (int e = 0; e < 2; ++e) {
+        double* p = cptr(i0 + wm * 64 + m * 8 + r, j0 + wn * 32 + q * 8 + cc + e);
+        if (p) *p = acc[m][q][e];
       }
-    }
-  }
 }
 
 }  // namespace riga

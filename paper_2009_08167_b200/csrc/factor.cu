@@ -795,8 +795,7 @@ __global__ void __launch_bounds__(256, 1) k_trail128(SymDev S, const int32_t* __
   const int64_t i0 = cs + ti * kT128, j0 = cs + tj * kT128;
   if (i0 >= f || j0 >= ce || i0 + kT128 - 1 < j0) return;
   double* L = panel + S.panel_off[s];
-  dmma_tile128<2>(L, f, L, f, D + S.col0[s], k0, kend, i0, j0, f, ce, L, f, 0, sm, nullptr, cb + S.cb_off[s],
-                  f - np, np);
+  dmma_tile128<2>(L, f, L, f, D + S.col0[s], k0, kend, i0, j0, f, ce, L, f, 0, sm, cb + S.cb_off[s], f - np, np);
 }
 
 // ---------------------------------------------------------------------------
