@@ -649,10 +649,16 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
   const int64_t col0 = S.col0[s];
   double* P = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;  // (r, c) of the block at P[c f + r]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // stage the block with cp.async (every load in flight at once; padding rows/columns: zero fill,
+  // identity pivots written after the wait)
   for (int idx = tid; idx < nbp * nbp; idx += blockDim.x) {
     const int c = idx / nbp, r = idx - c * nbp;
-    if (r >= c) A[c * kDBP + r] = (r < nb && c < nb) ? P[(int64_t)c * f + r] : (r == c ? 1.0 : 0.0);
+    const bool in = r >= c && r < nb && c < nb;
+    if (r >= c) cp_async8(A + c * kDBP + r, in ? P + (int64_t)c * f + r : P, in);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
+  for (int c = nb + tid; c < nbp; c += blockDim.x) A[c * kDBP + c] = 1.0;
   __syncthreads();
   for (int kb = 0; kb < nbp; kb += 32) {
     if (warp == 0) {
@@ -729,15 +735,21 @@ __global__ void __launch_bounds__(32 * kTrsmWarps) k_trsm128(SymDev S, const int
   double* ds = Ls + kDB * kDBP;
   double* W = ds + kDB + warp * kDB * 33;  // W[c * 33 + row]: this warp's rows x nbp columns
   const double* Lb = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;
-  for (int idx = tid; idx < nbp * nbp; idx += blockDim.x) {
+  for (int idx = tid; idx < nbp * nbp; idx += blockDim.x) {  // cp.async: all loads in flight at once
     const int c = idx / nbp, r = idx - c * nbp;
-    if (r > c) Ls[c * kDBP + r] = (r < nb && c < nb) ? Lb[(int64_t)c * f + r] : 0.0;
+    const bool in = r < nb && c < nb;
+    if (r > c) cp_async8(Ls + c * kDBP + r, in ? Lb + (int64_t)c * f + r : Lb, in);
   }
   for (int c = tid; c < nbp; c += blockDim.x) ds[c] = c < nb ? D[col0 + kbo + c] : 1.0;
   const int64_t r0 = rbase + 32 * warp;
   const int nr = (int)imin(32, imin(f - r0, 32));
   double* Pr = panel + S.panel_off[s] + (int64_t)kbo * f + r0;  // A21(row, c) at Pr[c f + row]
-  for (int c = 0; c < nbp; ++c) W[c * 33 + lane] = (c < nb && lane < nr) ? Pr[(int64_t)c * f + lane] : 0.0;
+  for (int c = 0; c < nbp; ++c) {
+    const bool in = c < nb && lane < nr;
+    cp_async8(W + c * 33 + lane, in ? Pr + (int64_t)c * f + lane : Lb, in);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   if (r0 >= f) return;
   for (int kb = 0; kb < nbp; kb += 32) {
