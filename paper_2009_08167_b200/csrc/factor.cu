@@ -548,8 +548,7 @@ __global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restric
 // ---------------------------------------------------------------------------
 constexpr int kDB = 128;
 constexpr int kDBP = kDB + 1;
-constexpr size_t kDiag128Smem = ((size_t)kDB * kDBP + kDB) * sizeof(double);
-constexpr size_t kTrsmSmem = ((size_t)kDB * kDBP + kDB + 2 * (size_t)kDB * 33) * sizeof(double);
+constexpr size_t kDiag128Smem = ((size_t)kDB * kDBP + 2 * kDB) * sizeof(double);
 
 // acc(i, j) += sum_{t < kcount} fa(i, t) fb(t, j) for a 32 x 32 warp tile (kcount % 4 == 0)
 template <class FA, class FB>
@@ -592,7 +591,7 @@ __device__ __forceinline__ void zero_acc(double (&acc)[4][4][2]) {
 template <int K>
 __device__ __forceinline__ void ldl32_step(double (&a)[32], int lane, double& dl) {
   const double dk = __shfl_sync(0xffffffffu, a[K], K);
-  const double lk = a[K] / dk;
+  const double lk = a[K] * (1.0 / dk);
 #pragma unroll
   for (int j = K + 1; j < 32; ++j) {
     const double ajk = __shfl_sync(0xffffffffu, a[K], j);  // A(j, K), not yet scaled
@@ -604,17 +603,22 @@ __device__ __forceinline__ void ldl32_step(double (&a)[32], int lane, double& dl
 
 // One row of a 32-column block solve by substitution: w[c] <- (w[c] - sum_{t<c} w[t] d(t) L(c, t)) / d(c),
 // i.e. row L(r, kb:kb+32) = A(r, kb:kb+32) L_bb^{-T} D_b^{-1} with compile-time column indices.
-template <int C, class FL, class FD>
-__device__ __forceinline__ void sub32_col(double (&w)[32], FL L, FD d) {
-  double v = w[C];
+template <int C, class FL>
+__device__ __forceinline__ void sub32_col(double (&w)[32], FL L) {
+  // w[t < C] hold u_t = L(r, t) d_t; u_C = A(r, C) - sum_{t<C} u_t L(C, t) in four independent chains
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int t = 0; t < C; ++t) v = fma(-w[t] * d(t), L(C, t), v);
-  w[C] = v / d(C);
+  for (int t = 0; t < C; ++t) s[t & 3] = fma(w[t], L(C, t), s[t & 3]);
+  w[C] -= (s[0] + s[1]) + (s[2] + s[3]);
 }
 
-template <class FL, class FD, int... C>
-__device__ __forceinline__ void sub32_all(double (&w)[32], FL L, FD d, std::integer_sequence<int, C...>) {
-  (sub32_col<C>(w, L, d), ...);
+// One row of a 32-column block solve by substitution, L(r, kb:kb+32) = A(r, kb:kb+32) L_bb^{-T} D_b^{-1}
+// (compile-time column indices): on return w[c] = L(r, c); rd(c) = 1 / d_c.
+template <class FL, class FR, int... C>
+__device__ __forceinline__ void sub32_all(double (&w)[32], FL L, FR rd, std::integer_sequence<int, C...>) {
+  (sub32_col<C>(w, L), ...);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) w[c] *= rd(c);
 }
 
 template <int... K>
@@ -641,6 +645,7 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
   extern __shared__ double sm[];
   double* A = sm;               // A[c * kDBP + r], lower triangle
   double* dd = A + kDB * kDBP;  // pivots
+  double* rdd = dd + kDB;       // their reciprocals
   const int s = nodes[blockIdx.x];
   const int64_t f = S.front[s], np = S.ncol[s];
   if (kbo >= np) return;
@@ -665,6 +670,7 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
       double dl;
       warp_ldl32(A + kb * kDBP + kb, kDBP, dl);
       dd[kb + lane] = dl;
+      rdd[kb + lane] = 1.0 / dl;
     }
     __syncthreads();
     // rows below the sub-block inside the block: substitution, thread per row
@@ -674,7 +680,7 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
       double w[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) w[c] = A[(kb + c) * kDBP + r];
-      sub32_all(w, [&](int c, int t) { return A[(kb + t) * kDBP + kb + c]; }, [&](int t) { return dd[kb + t]; },
+      sub32_all(w, [&](int c, int t) { return A[(kb + t) * kDBP + kb + c]; }, [&](int c) { return rdd[kb + c]; },
                 std::make_integer_sequence<int, 32>{});
 #pragma unroll
       for (int c = 0; c < 32; ++c) A[(kb + c) * kDBP + r] = w[c];
@@ -714,58 +720,61 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
   }
 }
 
-// L21 = A21 L11^{-T} D^{-1} for the rows below the block, by blocked substitution.  The CTA stages L11 and
-// its pivots in shared memory; each of its 2 warps owns 32 rows (independent of the other): per 32-column
-// step b, T = A_b - sum_{t<b} W_t D_t L_bt^T on DMMA, then W_b = T L_bb^{-T} D_b^{-1} row by row
-// (lane = row, compile-time column indices).
-constexpr int kTrsmWarps = 2;
-__global__ void __launch_bounds__(32 * kTrsmWarps) k_trsm128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
-                                                             double* __restrict__ panel, const double* __restrict__ D) {
+// L21 = A21 L11^{-T} D^{-1} for the rows below the block, by blocked substitution: one warp (CTA) per 32
+// rows, its rows x nb columns staged in shared memory (W); per 32-column step b the L11 row strip
+// L(b rows, 0 : b + 32) is staged, T = A_b - sum_{t<b} W_t D_t L_bt^T runs on DMMA, then W_b = T L_bb^{-T}
+// D_b^{-1} row by row (lane = row).
+constexpr size_t kTrsmSmem = (2 * (size_t)kDB * 33 + 2 * kDB) * sizeof(double);
+__global__ void __launch_bounds__(32) k_trsm128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
+                                                double* __restrict__ panel, const double* __restrict__ D) {
   extern __shared__ double sm[];
   const int s = nodes[blockIdx.y];
   const int64_t f = S.front[s], np = S.ncol[s];
   if (kbo >= np) return;
   const int nb = (int)imin(kDB, np - kbo);
   const int nbp = (nb + 31) & ~31;
-  const int64_t rbase = kbo + nb + (int64_t)blockIdx.x * 32 * kTrsmWarps;
-  if (rbase >= f) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r0 = kbo + nb + (int64_t)blockIdx.x * 32;
+  if (r0 >= f) return;
+  const int lane = threadIdx.x;
+  const int nr = (int)imin(32, f - r0);
   const int64_t col0 = S.col0[s];
-  double* Ls = sm;                // L11(r, c) at Ls[c * kDBP + r] (strict lower), pivots after
-  double* ds = Ls + kDB * kDBP;
-  double* W = ds + kDB + warp * kDB * 33;  // W[c * 33 + row]: this warp's rows x nbp columns
-  const double* Lb = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;
-  for (int idx = tid; idx < nbp * nbp; idx += blockDim.x) {  // cp.async: all loads in flight at once
-    const int c = idx / nbp, r = idx - c * nbp;
-    const bool in = r < nb && c < nb;
-    if (r > c) cp_async8(Ls + c * kDBP + r, in ? Lb + (int64_t)c * f + r : Lb, in);
-  }
-  for (int c = tid; c < nbp; c += blockDim.x) ds[c] = c < nb ? D[col0 + kbo + c] : 1.0;
-  const int64_t r0 = rbase + 32 * warp;
-  const int nr = (int)imin(32, imin(f - r0, 32));
-  double* Pr = panel + S.panel_off[s] + (int64_t)kbo * f + r0;  // A21(row, c) at Pr[c f + row]
+  double* W = sm;               // W[c * 33 + row]
+  double* Ls = W + kDB * 33;    // strip: L(kb + j, t) at Ls[t * 33 + j]
+  double* ds = Ls + kDB * 33;   // pivots
+  double* rds = ds + kDB;       // their reciprocals
+  const double* Lb = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;  // L11(r, c) at Lb[c f + r]
+  double* Pr = panel + S.panel_off[s] + (int64_t)kbo * f + r0;         // A21(row, c) at Pr[c f + row]
   for (int c = 0; c < nbp; ++c) {
     const bool in = c < nb && lane < nr;
     cp_async8(W + c * 33 + lane, in ? Pr + (int64_t)c * f + lane : Lb, in);
   }
   cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  if (r0 >= f) return;
+  for (int c = lane; c < nbp; c += 32) {
+    const double d = c < nb ? D[col0 + kbo + c] : 1.0;
+    ds[c] = d;
+    rds[c] = 1.0 / d;
+  }
   for (int kb = 0; kb < nbp; kb += 32) {
+    const bool rowin = kb + lane < nb;
+    for (int t = 0; t < kb + 32; ++t) {
+      const bool in = rowin && t < nb;
+      cp_async8(Ls + t * 33 + lane, in ? Lb + (int64_t)t * f + kb + lane : Lb, in);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
     if (kb > 0) {  // W_b -= sum_{t < b} W_t D_t L_bt^T
       double acc[4][4][2];
       zero_acc(acc);
-      warp_mma32(acc, [&](int i, int k) { return W[k * 33 + i] * ds[k]; },
-                 [&](int k, int j) { return Ls[k * kDBP + kb + j]; }, kb);
-      __syncwarp();
+      warp_mma32(acc, [&](int i, int k) { return W[k * 33 + i] * ds[k]; }, [&](int k, int j) { return Ls[k * 33 + j]; },
+                 kb);
       RIGA_ACC_FOR(W[(kb + aj) * 33 + ai] -= acc[m][q][e];)
       __syncwarp();
     }
     double w[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) w[c] = W[(kb + c) * 33 + lane];
-    sub32_all(w, [&](int c, int t) { return Ls[(kb + t) * kDBP + kb + c]; }, [&](int t) { return ds[kb + t]; },
+    sub32_all(w, [&](int c, int t) { return Ls[(kb + t) * 33 + c]; }, [&](int c) { return rds[kb + c]; },
               std::make_integer_sequence<int, 32>{});
 #pragma unroll
     for (int c = 0; c < 32; ++c) W[(kb + c) * 33 + lane] = w[c];
@@ -1025,8 +1034,8 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
         const int64_t kend = std::min<int64_t>(kbo + g_nb2, P.max_np_large);
         for (int64_t kb = kbo; kb < kend; kb += kDB) {
           k_diag128<<<nl, 256, kDiag128Smem, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p, F->D.p, F->stat.p);
-          const unsigned nti = (unsigned)((P.max_f_large - kb + 32 * kTrsmWarps - 1) / (32 * kTrsmWarps));
-          k_trsm128<<<dim3(nti, nl), 32 * kTrsmWarps, kTrsmSmem, st>>>(S, ln, (int)kb, F->panel.p, F->D.p);
+          const unsigned nti = (unsigned)((P.max_f_large - kb + 31) / 32);
+          k_trsm128<<<dim3(nti, nl), 32, kTrsmSmem, st>>>(S, ln, (int)kb, F->panel.p, F->D.p);
           count_launch(2);
           RIGA_CUDA(cudaGetLastError());
           // the block's remaining columns take this 128-column slice now (narrow, K = 128)
