@@ -12,14 +12,13 @@
 //     k_small_front  one CTA per front with f <= kSmallFront: the whole front
 //                    (originals + children) in shared memory, dense LDL^T of
 //                    the pivot block, Schur complement written back
-//     large fronts   right-looking blocked LDL^T in HBM, two-level: outer
-//                    blocks of kNBO = 128 pivot columns, each factored 32
-//                    at a time (k_panel: diagonal block + L21 rows;
-//                    k_syrk<0>: rank-32 update inside the outer block), then
-//                    one rank-128 update of the trailing pivot columns
-//                    (k_syrk<2>) and finally update block -= L21 D L21^T
-//                    (k_syrk<1>, K = n_p), all on FP64 tensor cores
-//                    (mma.sync m8n8k4 -> DMMA)
+//     large fronts   right-looking blocked LDL^T in HBM: per 128-column block
+//                    k_diag128 (diagonal block in shared memory), k_trsm128
+//                    (rows below, blocked substitution), narrow k_trail128
+//                    inside the nb2-column outer block and one wide
+//                    k_trail128 per outer block over the remaining pivot
+//                    columns AND the update block (K = nb2, 128 x 128 tiles
+//                    of mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4)
 // Inertia = count of negative pivots (integer atomics, order independent).
 #include <algorithm>
 #include <chrono>
@@ -35,9 +34,6 @@
 
 namespace riga {
 
-constexpr int kNB = 32;         // panel block width of the large-front path
-constexpr int kNBO = 128;       // outer block: trailing updates run as rank-kNBO DMMA GEMMs
-constexpr int kPanelRows = 128;  // rows per CTA in k_panel
 
 // ---------------------------------------------------------------------------
 __global__ void k_tol(int64_t nnz, const double* __restrict__ K, const double* __restrict__ M,
@@ -182,351 +178,6 @@ __global__ void __launch_bounds__(256) k_small_front(SymDev S, const int32_t* __
     for (int b = w; b < nu; b += nw)
       for (int a = b + lane; a < nu; a += 32) C[(int64_t)b * nu + a] = F[(np + b) * ld + np + a];
   }
-}
-
-// ---------------------------------------------------------------------------
-// Large fronts, panel step kb: factor the diagonal block [kb, kb+nbk) (one
-// warp, redundantly per CTA) and turn the rows below it into L.
-// ---------------------------------------------------------------------------
-// Panel step of a large front, in two launches so no CTA reads the diagonal
-// block while another overwrites it with its factor:
-//   ROWS = false: one CTA per front factors the nbk x nbk diagonal block
-//                 (unblocked LDL^T by warp 0, lane = row) and writes L_dd, D
-//                 and the inertia / zero-pivot counters;
-//   ROWS = true:  kPanelRows rows per CTA: L21 = A21 L_dd^{-T} D^{-1} from the
-//                 factored L_dd and D written by the first launch.
-// Left-looking inside the outer block (kbo > 0 <= kb): the panel's columns
-// first take the contributions of the block's previous columns [kbo, kb)
-// (rank <= 96, row-local: no k_syrk<0> launch between panels);
-// kbo = kb disables it (right-looking in-block updates by k_syrk<0>).
-constexpr int kLL = kNBO - kNB;  // previous in-block columns at most
-template <bool ROWS>
-__global__ void __launch_bounds__(kPanelRows) k_panel(SymDev S, const int32_t* __restrict__ nodes,
-                                                      int kb, int kbo, const double* __restrict__ tol,
-                                                      double* __restrict__ panel,
-                                                      double* __restrict__ D,
-                                                      int64_t* __restrict__ stat) {
-  __shared__ double Ld[kNB][kNB + 1];  // Ld[col][row]
-  __shared__ double dd[kNB];
-  __shared__ double Lp[kNB][kLL + 1];  // Lp[c][t] = L(kb + c, kbo + t) d_t (left-looking factor)
-  const int s = nodes[blockIdx.y];
-  const int64_t f = S.front[s], np = S.ncol[s];
-  if (kb >= np) return;
-  const int nbk = (int)imin(kNB, np - kb);
-  const int64_t col0 = S.col0[s];
-  double* P = panel + S.panel_off[s];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int nll = kb - kbo;  // 0, 32, 64 or 96
-  if (nll > 0) {
-    for (int idx = tid; idx < kNB * nll; idx += blockDim.x) {
-      const int t = idx / kNB, c = idx - t * kNB;
-      Lp[c][t] = c < nbk ? P[(int64_t)(kbo + t) * f + kb + c] * D[col0 + kbo + t] : 0.0;
-    }
-    __syncthreads();
-  }
-  if (!ROWS) {
-    for (int idx = tid; idx < kNB * kNB; idx += blockDim.x) {
-      int c = idx / kNB, r = idx % kNB;
-      double v = (c < nbk && r < nbk && r >= c) ? P[(kb + c) * f + kb + r] : 0.0;
-      if (nll > 0 && c < nbk && r < nbk && r >= c) {
-        // A(kb+r, kb+c) -= sum_t L(kb+r, t) d_t L(kb+c, t); L(kb+r, t) d_t = Lp[r][t]
-        double acc = 0.0;
-        for (int t = 0; t < nll; ++t) acc = fma(Lp[r][t], P[(int64_t)(kbo + t) * f + kb + c], acc);
-        v -= acc;
-      }
-      Ld[c][r] = v;
-    }
-    __syncthreads();
-    if (tid < 32) {  // unblocked LDL^T of the diagonal block by warp 0; lane = row
-      for (int k = 0; k < nbk; ++k) {
-        double d = Ld[k][k];
-        double ci = Ld[k][lane];
-        double li = ci / d;
-        __syncwarp();
-        if (lane > k && lane < nbk) {
-          for (int j = k + 1; j <= lane; ++j) Ld[j][lane] -= li * Ld[k][j];
-        }
-        __syncwarp();
-        if (lane > k && lane < nbk) Ld[k][lane] = li;
-        __syncwarp();
-      }
-      if (lane < nbk) dd[lane] = Ld[lane][lane];
-    }
-    __syncthreads();
-    for (int idx = tid; idx < nbk * nbk; idx += blockDim.x) {
-      int c = idx / nbk, r = idx % nbk;
-      if (r >= c) P[(kb + c) * f + kb + r] = Ld[c][r];
-    }
-    if (tid == 0) {
-      int neg = 0;
-      int64_t bad = INT64_MAX;
-      double tv = tol[1];
-      for (int k = 0; k < nbk; ++k) {
-        double d = dd[k];
-        D[col0 + kb + k] = d;
-        if (d < 0.0) neg++;
-        if (fabs(d) < tv && bad == INT64_MAX) bad = col0 + kb + k;
-      }
-      if (neg) atomicAdd((unsigned long long*)&stat[0], (unsigned long long)neg);
-      if (bad != INT64_MAX) atomicMin((long long*)&stat[1], (long long)bad);
-    }
-    return;
-  }
-  const int64_t rbeg = kb + nbk + (int64_t)blockIdx.x * kPanelRows;
-  if (rbeg >= f) return;
-  for (int idx = tid; idx < kNB * kNB; idx += blockDim.x) {
-    int c = idx / kNB, r = idx % kNB;
-    Ld[c][r] = (c < nbk && r < nbk && r > c) ? P[(kb + c) * f + kb + r] : 0.0;
-  }
-  if (tid < kNB) dd[tid] = tid < nbk ? D[col0 + kb + tid] : 1.0;
-  __syncthreads();
-  const int64_t r = rbeg + tid;
-  if (r < f) {
-    double x[kNB];
-#pragma unroll
-    for (int c = 0; c < kNB; ++c) x[c] = c < nbk ? P[(kb + c) * f + r] : 0.0;
-    for (int t = 0; t < nll; ++t) {  // left-looking: x -= L(r, kbo + t) * Lp[:, t]
-      const double a = P[(int64_t)(kbo + t) * f + r];
-#pragma unroll
-      for (int c = 0; c < kNB; ++c) x[c] = fma(-a, Lp[c][t], x[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < kNB; ++c) {
-      if (c < nbk) {
-        double wv = x[c];
-#pragma unroll
-        for (int t = 0; t < c; ++t) wv -= x[t] * dd[t] * Ld[t][c];
-        x[c] = wv / dd[c];
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < kNB; ++c)
-      if (c < nbk) P[(kb + c) * f + r] = x[c];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Outer block of a large front in two launches (replaces 4 x (k_panel<false>,
-// k_panel<true>, k_syrk<0>) per kNBO columns):
-//   k_diag_block  one CTA per front: the nb x nb diagonal block (nb <= kNBO)
-//                 in shared memory, factored 32 columns at a time (warp-0
-//                 unblocked LDL^T of the 32 x 32 block, row TRSM below it,
-//                 rank-32 update of the rest of the block); writes L11, D
-//                 and the inertia / zero-pivot counters
-//   k_l21         row chunks of all fronts: W = A21 L11^{-T} by a row-wise
-//                 forward sweep (warp per 4 rows, lanes over columns, L11 in
-//                 shared memory), L21 = W D^{-1}
-// ---------------------------------------------------------------------------
-constexpr int kL21Rows = 32;
-__host__ __device__ constexpr size_t diag_smem(int nbm) { return ((size_t)nbm * (nbm + 1) + 3 * (size_t)nbm) * sizeof(double); }
-__host__ __device__ constexpr size_t l21_smem(int nbm) {
-  return ((size_t)nbm * (nbm + 1) + (size_t)nbm * (kL21Rows + 1) + nbm) * sizeof(double);
-}
-
-__global__ void __launch_bounds__(256) k_diag_block(SymDev S, const int32_t* __restrict__ nodes, int kb,
-                                                    int kDBP, const double* __restrict__ tol,
-                                                    double* __restrict__ panel, double* __restrict__ D,
-                                                    int64_t* __restrict__ stat) {
-  extern __shared__ double sm[];  // nb x kDBP block + nb pivots (kDBP = level max nb + 1)
-  const int s = nodes[blockIdx.x];
-  const int64_t f = S.front[s], np = S.ncol[s];
-  if (kb >= np) return;
-  const int nb = (int)imin(kNBO, np - kb);
-  const int64_t col0 = S.col0[s];
-  double* P = panel + S.panel_off[s];
-  double* A = sm;  // A[c * kDBP + r], lower triangle
-  double* dd = sm + (kDBP - 1) * kDBP;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-    const int c = idx / nb, r = idx - c * nb;
-    if (r >= c) A[c * kDBP + r] = P[(int64_t)(kb + c) * f + kb + r];
-  }
-  __syncthreads();
-  // right-looking unblocked LDL^T of the block by all threads: per pivot k,
-  // l = A(k+1:, k) / d into a double-buffered vector, rank-1 update of the
-  // trailing lower triangle (warp per column), then column k <- l
-  double* lb0 = dd + (kDBP - 1);
-  double* lb1 = lb0 + (kDBP - 1);
-  for (int k = 0; k < nb; ++k) {
-    double* lb = (k & 1) ? lb1 : lb0;
-    const double d = A[k * kDBP + k];
-    if (tid == 0) dd[k] = d;
-    for (int r = k + 1 + tid; r < nb; r += blockDim.x) lb[r] = A[k * kDBP + r] / d;
-    __syncthreads();
-    for (int c = k + 1 + warp; c < nb; c += 8) {
-      const double ac = A[k * kDBP + c];
-      double* Ac = A + c * kDBP;
-      for (int r = c + lane; r < nb; r += 32) Ac[r] -= lb[r] * ac;
-    }
-    __syncthreads();
-    for (int r = k + 1 + tid; r < nb; r += blockDim.x) A[k * kDBP + r] = lb[r];
-  }
-  __syncthreads();
-  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-    const int c = idx / nb, r = idx - c * nb;
-    if (r >= c) P[(int64_t)(kb + c) * f + kb + r] = A[c * kDBP + r];
-  }
-  if (tid == 0) {
-    int neg = 0;
-    int64_t bad = INT64_MAX;
-    const double tv = tol[1];
-    for (int k = 0; k < nb; ++k) {
-      const double d = dd[k];
-      D[col0 + kb + k] = d;
-      if (d < 0.0) neg++;
-      if (fabs(d) < tv && bad == INT64_MAX) bad = col0 + kb + k;
-    }
-    if (neg) atomicAdd((unsigned long long*)&stat[0], (unsigned long long)neg);
-    if (bad != INT64_MAX) atomicMin((long long*)&stat[1], (long long)bad);
-  }
-}
-
-__global__ void __launch_bounds__(256) k_l21(SymDev S, const int32_t* __restrict__ nodes, int kb, int kDBP,
-                                             int rows_per_cta, double* __restrict__ panel,
-                                             const double* __restrict__ D) {
-  extern __shared__ double sm[];
-  const int s = nodes[blockIdx.y];
-  const int64_t f = S.front[s], np = S.ncol[s];
-  if (kb >= np) return;
-  const int nb = (int)imin(kNBO, np - kb);
-  const int64_t rbeg = kb + nb + (int64_t)blockIdx.x * rows_per_cta;
-  if (rbeg >= f) return;
-  const int64_t rend = imin(f, rbeg + rows_per_cta);
-  double* P = panel + S.panel_off[s];
-  const int nbm = kDBP - 1;
-  double* Ls = sm;                   // Ls[t * kDBP + c] = L11(c, t), c > t
-  double* Wt = sm + nbm * kDBP;      // Wt[c * (kL21Rows + 1) + r]
-  double* dd = Wt + nbm * (kL21Rows + 1);
-  constexpr int WP = kL21Rows + 1;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-    const int t = idx / nb, c = idx - t * nb;
-    Ls[t * kDBP + c] = c > t ? P[(int64_t)(kb + t) * f + kb + c] : 0.0;
-  }
-  for (int c = tid; c < nb; c += blockDim.x) dd[c] = D[S.col0[s] + kb + c];
-  constexpr int RW = kL21Rows / 8;
-  for (int64_t r0 = rbeg; r0 < rend; r0 += kL21Rows) {
-    const int nr = (int)imin(kL21Rows, rend - r0);
-    __syncthreads();
-    for (int idx = tid; idx < nb * kL21Rows; idx += blockDim.x) {
-      const int c = idx / kL21Rows, r = idx - c * kL21Rows;
-      Wt[c * WP + r] = r < nr ? P[(int64_t)(kb + c) * f + r0 + r] : 0.0;
-    }
-    __syncthreads();
-    // W(r, :) L11^T = A21(r, :): forward sweep over the columns; lane owns
-    // columns lane + 32 u, a warp carries RW rows (independent chains)
-    double a[RW][4];
-#pragma unroll
-    for (int q = 0; q < RW; ++q)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = lane + 32 * u;
-        a[q][u] = c < nb ? Wt[c * WP + warp * RW + q] : 0.0;
-      }
-#pragma unroll
-    for (int u0 = 0; u0 < 4; ++u0) {
-      for (int cl = 0; cl < 32; ++cl) {
-        const int c = 32 * u0 + cl;
-        if (c >= nb) break;
-        double w[RW];
-#pragma unroll
-        for (int q = 0; q < RW; ++q) w[q] = __shfl_sync(0xffffffffu, a[q][u0], cl);
-        const double* Lc = Ls + c * kDBP;
-#pragma unroll
-        for (int u = u0; u < 4; ++u) {
-          const int j = lane + 32 * u;
-          if (u == u0 && lane <= cl) continue;
-          const double l = j < nb ? Lc[j] : 0.0;
-#pragma unroll
-          for (int q = 0; q < RW; ++q) a[q][u] = fma(-w[q], l, a[q][u]);
-        }
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < RW; ++q)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = lane + 32 * u;
-        if (c < nb) Wt[c * WP + warp * RW + q] = a[q][u] / dd[c];
-      }
-    __syncthreads();
-    for (int idx = tid; idx < nb * kL21Rows; idx += blockDim.x) {
-      const int c = idx / kL21Rows, r = idx - c * kL21Rows;
-      if (r < nr) P[(int64_t)(kb + c) * f + r0 + r] = Wt[c * WP + r];
-    }
-  }
-}
-
-// update block -= L21 D L21^T on 128 x 128 DMMA tiles (large K = n_p)
-__global__ void __launch_bounds__(256, 1) k_syrk128(SymDev S, const int32_t* __restrict__ nodes,
-                                                    double* __restrict__ panel, double* __restrict__ cb,
-                                                    const double* __restrict__ D) {
-  extern __shared__ double sm[];
-  const int s = nodes[blockIdx.y];
-  const int64_t f = S.front[s], np = S.ncol[s];
-  if (np >= f) return;
-  const int64_t nt = (f - np + kT128 - 1) / kT128;
-  const int64_t ti = blockIdx.x / nt, tj = blockIdx.x % nt;
-  if (ti >= nt || ti < tj) return;
-  const double* L = panel + S.panel_off[s];
-  dmma_tile128(L, f, L, f, D + S.col0[s], 0, np, np + ti * kT128, np + tj * kT128, f, f, cb + S.cb_off[s],
-               f - np, np, sm);
-}
-
-// Trailing updates on FP64 tensor cores (rows always run to f):
-// MODE 0: rank-nbk update of the panel-block columns [kq + nbk, min(kbo + kNBO, np))
-//         by panel columns [kq, kq + nbk)              (inside an outer block)
-// MODE 1: update block -= L21 D L21^T, K = np
-// MODE 2: trailing pivot columns [kbo + kNBO, np) by the outer block's kNBO columns
-template <int MODE>
-__global__ void __launch_bounds__(128) k_syrk(SymDev S, const int32_t* __restrict__ nodes, int kq, int kbo,
-                                              double* __restrict__ panel,
-                                              double* __restrict__ cb,
-                                              const double* __restrict__ D) {
-  const int s = nodes[blockIdx.y];
-  const int64_t f = S.front[s], np = S.ncol[s];
-  int64_t m0, nend, k0, k1;
-  if (MODE == 0) {
-    if (kq >= np) return;
-    int64_t nbk = imin(kNB, np - kq);
-    m0 = kq + nbk;
-    nend = imin((int64_t)kbo + kNBO, np);
-    if (m0 >= nend) return;
-    k0 = kq;
-    k1 = kq + nbk;
-  } else if (MODE == 2) {
-    k0 = kbo;
-    k1 = imin((int64_t)kbo + kNBO, np);
-    m0 = k1;
-    nend = np;
-    if (k0 >= np || m0 >= np) return;
-  } else {
-    if (np >= f) return;
-    m0 = np;
-    nend = f;
-    k0 = 0;
-    k1 = np;
-  }
-  const int64_t ntj = (nend - m0 + 63) / 64, nti = (f - m0 + 63) / 64;
-  const int64_t ti = blockIdx.x / ntj, tj = blockIdx.x % ntj;
-  if (ti >= nti) return;
-  const int64_t i0 = m0 + ti * 64, j0 = m0 + tj * 64;
-  if (i0 + 63 < j0) return;  // strictly above the diagonal
-  const double* L = panel + S.panel_off[s];
-  const double* Dk = D + S.col0[s];
-  double* C;
-  int64_t ldc, coff;
-  if (MODE != 1) {
-    C = panel + S.panel_off[s];
-    ldc = f;
-    coff = 0;
-  } else {
-    C = cb + S.cb_off[s];
-    ldc = f - np;
-    coff = np;
-  }
-  dmma_syrk_tile(L, f, Dk, k0, k1, i0, j0, f, nend, C, ldc, coff);
 }
 
 // ---------------------------------------------------------------------------
@@ -925,33 +576,15 @@ __global__ void k_zero_cb(SymDev S, const int32_t* __restrict__ nodes, double* _
     c[i] = 0.0;
 }
 
-static bool g_block_path = true;  // RIGA_FACTOR_PANEL=32: the 32-column panel chain
-static bool g_tile128 = true;      // RIGA_FACTOR_TILE128=0: 64 x 64 tiles for the update blocks
-static bool g_left_looking = false;  // RIGA_PANEL_LL=1: left-looking in-block panel updates (no k_syrk<0>; measured no gain)
-static bool g_old_path = false;  // RIGA_FACTOR_OLD=1: the 32-column panel chain (A/B)
-static int64_t g_nb2 = 256;      // outer block of the trailing updates (multiple of 128; RIGA_FACTOR_NB2)
-static int64_t g_block_max_fronts = 0;  // RIGA_FACTOR_BLOCK_FRONTS=n: block path for levels with <= n large fronts (opt-in: slower today)
+static int64_t g_nb2 = 512;  // outer block of the trailing updates (multiple of 128; RIGA_FACTOR_NB2)
 
 static int set_smem_attrs() {
   static bool done = false;
   if (done) return RIGA_OK;
   {
-    const char* e = getenv("RIGA_FACTOR_PANEL");
-    g_block_path = !(e && std::strcmp(e, "32") == 0);
-    e = getenv("RIGA_FACTOR_TILE128");
-    g_tile128 = !(e && std::strcmp(e, "0") == 0);
-    e = getenv("RIGA_PANEL_LL");
-    g_left_looking = e && std::strcmp(e, "1") == 0;
-    e = getenv("RIGA_FACTOR_NB2");
+    const char* e = getenv("RIGA_FACTOR_NB2");
     if (e && atoll(e) >= 128) g_nb2 = atoll(e) / 128 * 128;
-    e = getenv("RIGA_FACTOR_OLD");
-    g_old_path = e && std::strcmp(e, "1") == 0;
-    e = getenv("RIGA_FACTOR_BLOCK_FRONTS");
-    if (e) g_block_max_fronts = atoll(e);
   }
-  RIGA_CUDA(cudaFuncSetAttribute(k_diag_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem(kNBO)));
-  RIGA_CUDA(cudaFuncSetAttribute(k_l21, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l21_smem(kNBO)));
-  RIGA_CUDA(cudaFuncSetAttribute(k_syrk128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem));
   RIGA_CUDA(cudaFuncSetAttribute(k_trsm128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem));
   RIGA_CUDA(cudaFuncSetAttribute(k_trail128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem));
   RIGA_CUDA(cudaFuncSetAttribute(k_diag128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiag128Smem));
@@ -1014,7 +647,7 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
                                                        F->D.p, F->stat.p); count_launch();
       RIGA_CUDA(cudaGetLastError());
     }
-    if (P.nlarge && !g_old_path) {
+    if (P.nlarge) {
       const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
       const unsigned nl = (unsigned)P.nlarge;
       auto trail = [&](int64_t k0, int64_t k1, int64_t c0, int64_t c1, bool wide) -> int {
@@ -1043,67 +676,6 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
         }
         // everything right of the block -- pivot columns and update block -- in one K = g_nb2 slice
         RIGA_TRY(trail(kbo, kbo + g_nb2, kbo + g_nb2, 0, true));
-      }
-    } else if (P.nlarge) {
-      const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
-      unsigned nl = (unsigned)P.nlarge;
-      for (int64_t kbo = 0; kbo < P.max_np_large; kbo += kNBO) {
-        const bool blockp = g_block_path && (int64_t)P.nlarge <= g_block_max_fronts;
-        if (blockp) {
-          // diagonal block in one CTA per front, then L21 for every row below it
-          const int nbm = (int)std::min<int64_t>(kNBO, P.max_np_large - kbo);
-          k_diag_block<<<nl, 256, diag_smem(nbm), st>>>(S, ln, (int)kbo, nbm + 1, F->tol.p, F->panel.p, F->D.p,
-                                                        F->stat.p);
-          // rows per CTA: about two waves over all fronts of the level, >= 32
-          const int64_t rows = std::max<int64_t>(1, P.max_f_large - kbo);  // bound over fronts with nb < nbm
-          int64_t rpc = (rows * (int64_t)nl + 2 * 148 - 1) / (2 * 148);
-          rpc = std::max<int64_t>(kL21Rows, (rpc + kL21Rows - 1) / kL21Rows * kL21Rows);
-          const unsigned rchunks = (unsigned)((rows + rpc - 1) / rpc);
-          k_l21<<<dim3(rchunks, nl), 256, l21_smem(nbm), st>>>(S, ln, (int)kbo, nbm + 1, (int)rpc, F->panel.p,
-                                                               F->D.p);
-          count_launch(2);
-          RIGA_CUDA(cudaGetLastError());
-        }
-        // factor the outer block's columns 32 at a time (panel + in-block update)
-        for (int64_t kb = kbo; !blockp && kb < std::min<int64_t>(kbo + kNBO, P.max_np_large); kb += kNB) {
-          unsigned rchunks = (unsigned)std::max<int64_t>(1, (P.max_f_large - kb + kPanelRows - 1) / kPanelRows);
-          const int kll = g_left_looking ? (int)kbo : (int)kb;
-          k_panel<false><<<dim3(1, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, kll, F->tol.p, F->panel.p, F->D.p,
-                                                             F->stat.p);
-          k_panel<true><<<dim3(rchunks, nl), kPanelRows, 0, st>>>(S, ln, (int)kb, kll, F->tol.p, F->panel.p,
-                                                                  F->D.p, F->stat.p);
-          count_launch(2);
-          RIGA_CUDA(cudaGetLastError());
-          int64_t m0 = kb + kNB, nend = std::min<int64_t>(kbo + kNBO, P.max_np_large);
-          if (!g_left_looking && m0 < nend) {
-            int64_t ntj = (nend - m0 + 63) / 64, nti = (P.max_f_large - m0 + 63) / 64;
-            k_syrk<0><<<dim3((unsigned)(ntj * nti), nl), 128, 0, st>>>(S, ln, (int)kb, (int)kbo, F->panel.p,
-                                                                      cbuf, F->D.p); count_launch();
-            RIGA_CUDA(cudaGetLastError());
-          }
-        }
-        // trailing pivot columns: one rank-kNBO update
-        int64_t m0 = kbo + kNBO;
-        if (m0 < P.max_np_large) {
-          int64_t ntj = (P.max_np_large - m0 + 63) / 64, nti = (P.max_f_large - m0 + 63) / 64;
-          k_syrk<2><<<dim3((unsigned)(ntj * nti), nl), 128, 0, st>>>(S, ln, 0, (int)kbo, F->panel.p, cbuf,
-                                                                    F->D.p); count_launch();
-          RIGA_CUDA(cudaGetLastError());
-        }
-      }
-    }
-    if (P.nlarge && g_old_path) {
-      const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
-      const unsigned nl = (unsigned)P.nlarge;
-      if (P.max_nu_large > 0 && g_tile128 && P.max_np_large >= 128 && P.max_nu_large >= 256) {
-        const int64_t t = (P.max_nu_large + kT128 - 1) / kT128;
-        k_syrk128<<<dim3((unsigned)(t * t), nl), 256, kT128Smem, st>>>(S, ln, F->panel.p, cbuf, F->D.p);
-        count_launch();
-        RIGA_CUDA(cudaGetLastError());
-      } else if (P.max_nu_large > 0) {
-        int64_t t = (P.max_nu_large + 63) / 64;
-        k_syrk<1><<<dim3((unsigned)(t * t), nl), 128, 0, st>>>(S, ln, 0, 0, F->panel.p, cbuf, F->D.p); count_launch();
-        RIGA_CUDA(cudaGetLastError());
       }
     }
   }
