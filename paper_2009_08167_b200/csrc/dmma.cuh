@@ -1,10 +1,10 @@
-// FP64 tensor-core tile for the frontal Schur-complement updates.
+// FP64 tensor-core tiles: the frontal Schur-complement updates (dmma_tile128),
+// the chain-inverse doubling GEMMs and the Lanczos lift / locking GEMMs.
 //
 // sm_100a has no tcgen05 kind for f64, so FP64 MMA is the warp-level
-// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  One CTA (4 warps) owns a 64x64
-// tile of C; each warp a 32x32 sub-tile = 4x4 DMMA tiles (32 fp64
-// accumulators per thread).  Operands are staged in shared memory k-major
-// with a 72-double pitch (conflict-free fragment loads).
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  The 64x64 tiles use 4 warps of
+// 32x32 (32 fp64 accumulators per thread) with operands staged in shared
+// memory k-major at a 72-double pitch (conflict-free fragment loads).
 #pragma once
 
 #include <cstdint>
@@ -15,83 +15,6 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
-}
-
-// C(i - coff, j - coff) -= sum_{t in [k0,k1)} L[t*ldl + i] * Dk[t] * L[t*ldl + j]
-// for i in [i0, i0+64) with i < mend, j in [j0, j0+64) with j < nend.
-// C is column-major with leading dimension ldc.  blockDim.x == 128.
-__device__ __forceinline__ void dmma_syrk_tile(const double* __restrict__ L, int64_t ldl,
-                                               const double* __restrict__ Dk, int64_t k0,
-                                               int64_t k1, int64_t i0, int64_t j0, int64_t mend,
-                                               int64_t nend, double* __restrict__ C, int64_t ldc,
-                                               int64_t coff) {
-  __shared__ double As[2][16][72];
-  __shared__ double Bs[2][16][72];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
-  double acc[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-
-  double ra[8], rb[8];
-  auto load = [&](int64_t kt) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      int idx = tid + 128 * u, t = idx >> 6, i = idx & 63;
-      int64_t kk = kt + t;
-      bool kin = kk < k1;
-      ra[u] = (kin && i0 + i < mend) ? L[kk * ldl + i0 + i] * Dk[kk] : 0.0;
-      rb[u] = (kin && j0 + i < nend) ? L[kk * ldl + j0 + i] : 0.0;
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      int idx = tid + 128 * u, t = idx >> 6, i = idx & 63;
-      As[buf][t][i] = ra[u];
-      Bs[buf][t][i] = rb[u];
-    }
-  };
-  int buf = 0;
-  load(k0);
-  store(0);
-  __syncthreads();
-  for (int64_t kt = k0; kt < k1; kt += 16) {
-    const bool more = kt + 16 < k1;
-    if (more) load(kt + 16);  // global loads in flight during the MMAs
-#pragma unroll
-    for (int k4 = 0; k4 < 4; ++k4) {
-      const int kr = k4 * 4 + (lane & 3);
-      double av[4], bv[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) av[m] = As[buf][kr][wm * 32 + m * 8 + (lane >> 2)];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) bv[q] = Bs[buf][kr][wn * 32 + q * 8 + (lane >> 2)];
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[m][q][0], acc[m][q][1], av[m], bv[q]);
-    }
-    if (more) {
-      store(buf ^ 1);
-      __syncthreads();
-      buf ^= 1;
-    }
-  }
-  const int r = lane >> 2, cc = (lane & 3) * 2;
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    const int64_t i = i0 + wm * 32 + m * 8 + r;
-    if (i >= mend) continue;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t j = j0 + wn * 32 + q * 8 + cc;
-      if (j < nend) C[(j - coff) * ldc + (i - coff)] -= acc[m][q][0];
-      if (j + 1 < nend) C[(j + 1 - coff) * ldc + (i - coff)] -= acc[m][q][1];
-    }
-  }
 }
 
 }  // namespace riga
