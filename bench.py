@@ -323,12 +323,37 @@ def ldlt_rate(P, D, cfgname, flush, reps=3):
         del f
     fm = float(np.median(ms[1:]))
     tf = flops / (fm / 1e3) / 1e12
+    # the frontal Schur-complement update kernels in situ (north_star: "LDL^T frontal updates at >= 50 % of
+    # FP64 tensor peak"): CUDA events around each k_trail128 launch of one more factorization, work = their
+    # algorithmic flops (2 K per updated lower-triangle entry)
+    import ctypes
+
+    from paper_2009_08167_b200 import _lib
+
+    L = _lib.lib()
+    L.riga_prof_reset()
+    L.riga_prof_enable(1)
+    flush.zero_()
+    torch.cuda.synchronize()
+    f = numeric_factor(sym, float(sh[1]))
+    torch.cuda.synchronize()
+    L.riga_prof_enable(0)
+    pm, pw, pc = np.zeros(8), np.zeros(8), np.zeros(8, np.int64)
+    L.riga_prof_read(_lib.ptr(pm), _lib.ptr(pw), _lib.ptr(pc), 8)
+    L.riga_prof_reset()
+    del f
+    upd = {"ms": float(pm[6]), "flops": float(pw[6]), "launches": int(pc[6]),
+           "achieved": float(pw[6]) / (pm[6] / 1e3) / 1e12 if pm[6] > 0 else 0.0, "unit": "TFLOP/s",
+           "share_of_factor_flops": float(pw[6]) / flops,
+           "how": "CUDA events around every k_trail128 launch of one factorization (prof scopes on), "
+                  "algorithmic flops of the lower-triangle updates"}
+    upd["frac"] = upd["achieved"] / MEASURED_FP64_TFLOPS
     out = {"config": cfgname, "N": s.dof_count, "ms": fm, "flops_per_launch": flops, "achieved": tf,
            "unit": "TFLOP/s", "peak": MEASURED_FP64_TFLOPS, "frac": tf / MEASURED_FP64_TFLOPS,
            "peak_source": "tools/fp64_peak.cu DMMA loop on this pool's B200",
            "how": f"median of {reps} factorizations (after one warm-up), CUDA events on the factor stream, "
                   "L2 flushed before each; flops = reference sum colcount^2",
-           "setup_s": t_setup}
+           "frontal_updates": upd, "setup_s": t_setup}
     del sym, s
     torch.cuda.synchronize()
     return out

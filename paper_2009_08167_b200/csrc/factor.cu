@@ -657,6 +657,14 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
         if (nti <= 0) return RIGA_OK;
         const int64_t ntj = wide ? nti : (c1 - c0 + kT128 - 1) / kT128;
         const int64_t ntiles = wide ? nti * (nti + 1) / 2 : nti * ntj;
+        double work = 0.0;  // algorithmic flops: 2 K per updated lower entry, over the level's fronts
+        for (int64_t q = P.begin + P.nsmall; q < P.begin + P.nsmall + P.nlarge; ++q) {
+          const int64_t sn = h.level_nodes[q], f = h.front[sn], np = h.ncol[sn];
+          const int64_t kend = std::min(k1, np), cs = std::min(c0, np), ce = wide ? f : std::min(c1, np);
+          if (k0 >= kend || cs >= ce) continue;
+          work += 2.0 * (double)(kend - k0) * ((double)(ce - cs) * f - 0.5 * (double)(ce - 1 + cs) * (ce - cs));
+        }
+        ProfScope prof_t(kProfTrail, st, work);
         k_trail128<<<dim3((unsigned)ntiles, nl), 256, kT128Smem, st>>>(S, ln, k0, k1, c0, c1, wide ? 1 : 0, (int)ntj,
                                                                        wide ? 1 : 0, F->panel.p, cbuf, F->D.p);
         count_launch();

@@ -16,7 +16,8 @@ enum ProfCat {
   kProfCgs = 3,     // one CGS pass (bytes = 2 rows n 8)
   kProfVec = 4,     // dots / residual / normalise
   kProfLift = 5,    // lift / restart skinny GEMMs
-  kProfCount = 6
+  kProfTrail = 6,   // frontal Schur-complement updates (k_trail128; work = their flops)
+  kProfCount = 7
 };
 
 extern std::atomic<long long> g_launches;
