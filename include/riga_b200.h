@@ -252,6 +252,9 @@ int riga_lanczos_dcgs_probe(riga_lanczos* lz, const double* w_dev, int64_t* rows
 /* Gram matrix G = V[:k] MV[:k]^T to host (k x k row-major) for the
  * DEBUG_INVARIANTS checks (ref check_invariants :276-282).                 */
 int riga_lanczos_gram(riga_lanczos* lz, double* G_host);
+/* Device bytes the state holds (basis, locked rows at their current
+ * capacity, scratch): memory planners count pooled idle states with it.   */
+int riga_lanczos_bytes(riga_lanczos* lz, int64_t* bytes);
 /* Device pointers of V and MV (row-major, leading dimension *ld). */
 int riga_lanczos_basis(riga_lanczos* lz, double** V, double** MV, int64_t* ld);
 

@@ -82,6 +82,7 @@ SIGNATURES = {
     "riga_lanczos_append_rows": [_p, _p, _p, _i64, _i64, _p, _p],
     "riga_lanczos_gram": [_p, _p],
     "riga_lanczos_basis": [_p, _p, _p, _p],
+    "riga_lanczos_bytes": [_p, _p],
     "riga_residuals": [_p, _p, _p, _i64, _i64, _p, _p],
     "riga_dot": [_p, _i64, _p, _p, _p],
     "riga_launch_count": [_p],

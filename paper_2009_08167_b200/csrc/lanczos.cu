@@ -1696,6 +1696,17 @@ int riga_lanczos_gram(riga_lanczos* lz, double* G) {
   return RIGA_OK;
 }
 
+int riga_lanczos_bytes(riga_lanczos* lz, int64_t* bytes) {
+  RIGA_CHECK_ARG(lz && bytes, "null arg");
+  const DevBuf<double>* bufs[] = {&lz->V, &lz->MV, &lz->L, &lz->LM, &lz->w, &lz->r, &lz->Mr, &lz->bp, &lz->coef,
+                                  &lz->partial, &lz->upart, &lz->cpl, &lz->Wd, &lz->outs, &lz->dscratch, &lz->vt,
+                                  &lz->mvt, &lz->kt1, &lz->kt2};
+  int64_t b = 0;
+  for (const DevBuf<double>* d : bufs) b += (int64_t)d->n * 8;
+  *bytes = b;
+  return RIGA_OK;
+}
+
 int riga_lanczos_basis(riga_lanczos* lz, double** V, double** MV, int64_t* ld) {
   RIGA_CHECK_ARG(lz, "null arg");
   if (V) *V = lz->V.p;

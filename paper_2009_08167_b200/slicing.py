@@ -317,7 +317,9 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
 
     reuse = ctypes.c_int64(0)
     _L0.check(_L0.lib().riga_device_pool_reusable(base_ctx.device, ctypes.byref(reuse)), "pool")
-    free_b += reuse.value + _E0.pooled_state_bytes(base_ctx.device)
+    # idle Lanczos states of another problem size will never be reused by this call: free them first
+    _E0.trim_state_pool(base_ctx.device, lambda n_, m_: n_ == n)
+    free_b += reuse.value + _E0.pooled_state_bytes(base_ctx.device, n)
     budget = 0.85 * free_b
     keep_factors = (S + 1) * fac_bytes <= 0.35 * budget
 
@@ -388,6 +390,9 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     # --- 2. LPT assignment of slices to ranks -------------------------------
     assign = lpt_assign(list(expected), world)
     my = assign[rank]
+    # pooled states of basis sizes this call does not use are stale: free them before the slices allocate
+    m_used = {max(2, min(m_factor * int(expected[k]), system.dof_count)) for k in my}
+    _E0.trim_state_pool(base_ctx.device, lambda n_, m_: n_ == n and min(m_, n) in m_used)
     # drop factors this rank does not need
     kept = {k: v for k, v in kept.items() if k in my}
 
