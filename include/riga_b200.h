@@ -86,6 +86,19 @@ int riga_system_assemble_kron(riga_ctx* ctx, int dim, const int64_t* n1,
                               const int64_t* const* rowptr1, const int32_t* const* colidx1,
                               const double* const* k1, const double* const* m1,
                               riga_system** out);
+/* Device element-quadrature assembly (ref assembly.py:72-111 integrated in d
+ * dimensions): every element of the tensor mesh with (p+1)^d Gauss points.
+ * Per direction t: ne[t] elements; first[t][e] = global (full) index of the
+ * element's first basis function (span - p); w[t][e][q] scaled Gauss
+ * weights; N[t][e][q][a], dN[t][e][q][a] basis values / derivatives at the
+ * points (host).  n1 / rowptr1 / colidx1 / k1 / m1: the Dirichlet-reduced 1D
+ * matrices as for riga_system_assemble_kron (they define the shared CSR
+ * pattern).  Values equal the Kronecker pencil to roundoff; deterministic
+ * (element colour classes, no atomics).  dim 1-3, degree 1-5 (3D: 1-3).    */
+int riga_system_assemble_quad(riga_ctx* ctx, int dim, int p, const int64_t* ne, const int32_t* const* first,
+                              const double* const* w, const double* const* N, const double* const* dN,
+                              const int64_t* n1, const int64_t* const* rowptr1, const int32_t* const* colidx1,
+                              const double* const* k1, const double* const* m1, riga_system** out);
 /* Attach 1D factors to an uploaded pencil whose M is M_z (x) M_y (x) M_x
  * (arguments as riga_system_assemble_kron; n must equal prod n1): the
  * Lanczos mass products then run axis by axis instead of over the CSR.

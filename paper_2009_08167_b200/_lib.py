@@ -39,6 +39,7 @@ SIGNATURES = {
     "riga_system_upload": [_p, _i64, _i64, _p, _p, _p, _p, _p],
     "riga_system_assemble_kron": [_p, _i32, _p, _p, _p, _p, _p, _p],
     "riga_system_set_kron": [_p, _i32, _p, _p, _p, _p, _p],
+    "riga_system_assemble_quad": [_p, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "riga_system_info": [_p, _p, _p],
     "riga_system_download": [_p, _p, _p, _p, _p],
     "riga_system_device_ptrs": [_p, _p, _p, _p, _p],

@@ -222,8 +222,71 @@ def kron_assemble(spaces, stiffness_only: bool = False, ctx=None) -> DiscreteSys
     return DiscreteSystem(K, M, spaces, d, n, tuple(k1d), tuple(m1d), dev)
 
 
-def build_system(d: int, ne: int, p: int, level: int = 0, **kw) -> DiscreteSystem:
-    return kron_assemble((make_spline_space(ne, p, level),) * d, **kw)
+def quadrature_tables(space: SplineSpace):
+    """Per element of one direction: first global basis index (span - p), the (p+1) Gauss weights scaled to
+    the element, and the (p+1) x (p+1) basis values / derivatives at the points ([e][q][a]).  Host side of
+    the device quadrature assembly (the 1D ingredients of ref assembly.py:72-111)."""
+    p = space.degree
+    first, ws, Ns, dNs = [], [], [], []
+    for mu, a, b in element_spans(space):
+        pts, wts = gauss_points(p + 1, a, b)
+        vals, ders = eval_basis_span(space, mu, pts)
+        first.append(mu - p)
+        ws.append(wts)
+        Ns.append(vals)
+        dNs.append(ders)
+    return (np.ascontiguousarray(first, np.int32), np.ascontiguousarray(np.stack(ws), np.float64),
+            np.ascontiguousarray(np.stack(Ns), np.float64), np.ascontiguousarray(np.stack(dNs), np.float64))
+
+
+def quadrature_assemble(spaces, ctx=None) -> DiscreteSystem:
+    """d-dimensional Dirichlet-reduced system by element quadrature on the device: (p+1)^d Gauss points
+    per d-dimensional element (BASELINE configs), the same CSR pattern and x-fastest numbering as
+    ``kron_assemble``; values equal the Kronecker pencil to roundoff (riga_system_assemble_quad)."""
+    from . import device as _dev
+
+    spaces = tuple(spaces)
+    d = len(spaces)
+    if d not in (1, 2, 3):
+        raise ValueError(f"dimension must be 1, 2 or 3, got {d}")
+    if len({s.degree for s in spaces}) != 1:
+        raise ValueError("per-direction degrees must match")
+    p = spaces[0].degree
+    k1d, m1d, tabs = [], [], []
+    for s in spaces:
+        K1, M1 = apply_dirichlet(*assemble_1d(s))
+        k1d.append(K1.csr); m1d.append(M1.csr)
+        tabs.append(quadrature_tables(s))
+    ctx = ctx or _dev.current()
+    parts_k = [_csr_parts(k) for k in k1d]
+    parts_m = [_csr_parts(m) for m in m1d]
+    n1 = np.array([k.shape[0] for k in k1d], dtype=np.int64)
+    ne = np.array([t[0].size for t in tabs], dtype=np.int64)
+    P = ctypes.c_void_p * d
+    arr = lambda xs: P(*[_lib.ptr(x).value for x in xs])  # noqa: E731
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().riga_system_assemble_quad(
+        ctx.handle, d, p, _lib.ptr(ne), arr([t[0] for t in tabs]), arr([t[1] for t in tabs]),
+        arr([t[2] for t in tabs]), arr([t[3] for t in tabs]), _lib.ptr(n1), arr([q[0] for q in parts_k]),
+        arr([q[1] for q in parts_k]), arr([q[2] for q in parts_k]), arr([q[2] for q in parts_m]),
+        ctypes.byref(h)), "assemble_quad")
+    n = int(np.prod(n1))
+    nnz = int(np.prod([q[0][-1] for q in parts_k]))
+    dev = DeviceSystem(h, ctx, n, nnz)
+    return DiscreteSystem(SymSparseMatrix(device=dev, which=0), SymSparseMatrix(device=dev, which=1), spaces, d, n,
+                          tuple(k1d), tuple(m1d), dev)
+
+
+def build_system(d: int, ne: int, p: int, level: int = 0, assembly: str = "kron", **kw) -> DiscreteSystem:
+    """ref assembly.py:189-192.  ``assembly`` (engine extension): "kron" (default) composes the device CSR
+    from the 1D matrices in the reference's own product and sum order (bit-identical K and M);
+    "quadrature" integrates every d-dimensional element with (p+1)^d Gauss points on the device."""
+    spaces = (make_spline_space(ne, p, level),) * d
+    if assembly == "kron":
+        return kron_assemble(spaces, **kw)
+    if assembly == "quadrature":
+        return quadrature_assemble(spaces, **kw)
+    raise ValueError(f"unknown assembly {assembly!r}")
 
 
 def dof_count(ne: int, p: int, level: int, d: int) -> int:

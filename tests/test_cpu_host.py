@@ -175,3 +175,42 @@ def test_lpt_assignment():
         loads = [sum(counts[k] for k in r) for r in a]
         assert max(loads) - min(loads) <= max(counts)
     assert lpt_assign([96, 17, 31], 2) == [[0], [1, 2]]
+
+
+def test_quadrature_tables_reproduce_kronecker_pencil():
+    """Host side of the device element-quadrature assembly: integrating the 2D elements with the tensor
+    Gauss rule from quadrature_tables (numpy restatement of the device kernel's sums) reproduces the
+    Kronecker-composed K and M to roundoff (ref assembly.py:72-111, :162-177)."""
+    import scipy.sparse as sp
+
+    from paper_2009_08167_b200.assembly import apply_dirichlet, assemble_1d, quadrature_tables
+    from paper_2009_08167_b200.bspline import make_spline_space
+
+    ne, p, lv = 8, 3, 1
+    s = make_spline_space(ne, p, lv)
+    K1, M1 = apply_dirichlet(*assemble_1d(s))
+    n1 = K1.dimension
+    Kk = sp.kron(M1.csr, K1.csr) + sp.kron(K1.csr, M1.csr)
+    Mk = sp.kron(M1.csr, M1.csr)
+    first, w, N, dN = quadrature_tables(s)
+    n = n1 * n1
+    Kq = np.zeros((n, n))
+    Mq = np.zeros((n, n))
+    for ey in range(first.size):
+        for ex in range(first.size):
+            W = np.outer(w[ey], w[ex]).ravel()  # q = (qy, qx), x fastest
+            v = np.einsum("ya,xb->yxab", N[ey], N[ex]).reshape(-1, (p + 1) ** 2)
+            gx = np.einsum("ya,xb->yxab", N[ey], dN[ex]).reshape(-1, (p + 1) ** 2)
+            gy = np.einsum("ya,xb->yxab", dN[ey], N[ex]).reshape(-1, (p + 1) ** 2)
+            ke = gx.T @ (W[:, None] * gx) + gy.T @ (W[:, None] * gy)
+            me = v.T @ (W[:, None] * v)
+            iy = first[ey] + np.arange(p + 1) - 1
+            ix = first[ex] + np.arange(p + 1) - 1
+            g = (iy[:, None] * n1 + ix[None, :]).ravel()
+            ok = ((iy[:, None] >= 0) & (iy[:, None] < n1) & (ix[None, :] >= 0) & (ix[None, :] < n1)).ravel()
+            sel = np.flatnonzero(ok)
+            Kq[np.ix_(g[sel], g[sel])] += ke[np.ix_(sel, sel)]
+            Mq[np.ix_(g[sel], g[sel])] += me[np.ix_(sel, sel)]
+    assert np.abs(Kq - Kk.toarray()).max() <= 1e-13 * np.abs(Kk.toarray()).max()
+    assert np.abs(Mq - Mk.toarray()).max() <= 1e-13 * np.abs(Mk.toarray()).max()
+    assert np.array_equal(Kq != 0, Kk.toarray() != 0)
