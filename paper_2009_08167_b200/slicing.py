@@ -276,9 +276,11 @@ class solve_plan:
 
 def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams: int = 4,
                          rank: int = 0, world: int = 1, vectors_to_host: bool = True,
-                         pencil_symbolic: Symbolic | None = None, perm=None,
+                         pencil_symbolic: Symbolic | None = None, perm=None, m_fixed: int | None = None,
                          **opts) -> SlicesResult:
-    """Solve every slice (shifts[k], shifts[k+1]] (see module docstring)."""
+    """Solve every slice (shifts[k], shifts[k+1]] (see module docstring).  The Lanczos basis of slice k has
+    m = m_factor x count_k vectors (the BASELINE protocol), or m_fixed for every slice (solve_spectrum's
+    SolverOptions.m)."""
     t_all = time.perf_counter()
     shifts = np.asarray(shifts, dtype=np.float64)
     S = shifts.size - 1
@@ -391,7 +393,11 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     assign = lpt_assign(list(expected), world)
     my = assign[rank]
     # pooled states of basis sizes this call does not use are stale: free them before the slices allocate
-    m_used = {max(2, min(m_factor * int(expected[k]), system.dof_count)) for k in my}
+    def slice_m(k):
+        want = m_fixed if m_fixed is not None else m_factor * int(expected[k])
+        return max(2, min(want, system.dof_count))
+
+    m_used = {slice_m(k) for k in my}
     _E0.trim_state_pool(base_ctx.device, lambda n_, m_: n_ == n and min(m_, n) in m_used)
     # drop factors this rank does not need
     kept = {k: v for k, v in kept.items() if k in my}
@@ -405,7 +411,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
     factor_lock = threading.Lock()
     queue = sorted(my, key=lambda k: -expected[k])
     order = list(queue)
-    m_max = max([m_factor * int(expected[k]) for k in my] + [2])
+    m_max = max([slice_m(k) for k in my] + [2])
     # per slice: its factor (unless kept), V + MV and the locked set L + LM
     # (capacity >= m rows each), lifted/locking temporaries and pool vectors
     per_slice = 1.2 * (fac_bytes * (0 if keep_factors else 1) + 16.0 * (m_max + 1) * n * 2
@@ -458,7 +464,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                     count = int(expected[k])
                     pool = _Pool()
                     if count > 0:
-                        m = max(2, min(m_factor * count, system.dof_count))
+                        m = slice_m(k)
                         so = SolverOptions(m=m, **opts)
                         rng = np.random.default_rng(seeds[k])
                         _solve_interval(pen, lob, hib, pool, so, rng, hi - lo)
@@ -538,7 +544,7 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                 if kk != k and (kk, j) not in drop:
                     pool.lams.append(float(lam))
                     pool.vecs.append(torch.as_tensor(x, device=dev))
-            so = SolverOptions(m=max(2, min(m_factor * int(expected[k]), system.dof_count)), **opts)
+            so = SolverOptions(m=slice_m(k), **opts)
             _solve_interval(pen, lob, hib, pool, so, np.random.default_rng(seeds[k] + 104729), hi - lo)
             idx = sorted((i for i, lam in enumerate(pool.lams) if lo < lam <= hi), key=lambda i: pool.lams[i])
             lams = np.array([pool.lams[i] for i in idx])
@@ -621,3 +627,184 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
                    "slice_nfb": {int(k): int(nf) for k, (_, _, nf) in slice_times.items()}}
     res.factor_ms = [allb[k][2] for k in range(S + 1)]
     return res
+
+
+# ---------------------------------------------------------------------------
+# solve_spectrum on concurrent streams
+# ---------------------------------------------------------------------------
+
+
+def factor_inertias(system, sigmas, scale: float, streams: int = 8, sym=None, perm=None):
+    """Inertia nu(sigma) of every shift, the factorizations on concurrent streams (factors discarded).
+    ZeroPivot nudges follow ref _Pencil.factor (sigma += 1e-8 scale, x10, <= 12 tries).  Returns
+    [(sigma_used, nu)] in input order and the CostCounters of the factorizations."""
+    base_ctx = _dev.current()
+    if perm is None:
+        perm = separator_ordering(system)
+    if sym is None:
+        sym = Symbolic.on_device(system.device, perm)
+    sigmas = [float(x) for x in sigmas]
+    out = [None] * len(sigmas)
+    todo = list(range(len(sigmas)))
+    lock = threading.Lock()
+    errs = []
+    total = CostCounters()
+
+    def work(widx):
+        ctx = _take_ctx(base_ctx.device, ("inertia", widx), 0)
+        cnt = CostCounters()
+        pen = _Pencil.__new__(_Pencil)
+        pen.system, pen.ctx, pen.M, pen.n = system, ctx, system.M, system.dof_count
+        pen.perm, pen.counters, pen.symbolic = perm, cnt, sym
+        with ctx:
+            while True:
+                with lock:
+                    if not todo or errs:
+                        break
+                    i = todo.pop(0)
+                try:
+                    sg, f = pen.factor(sigmas[i], scale)
+                    with lock:
+                        out[i] = (sg, f.n_negative)
+                    del f
+                except Exception as e:  # surfaced after join
+                    with lock:
+                        errs.append(e)
+        with lock:
+            total.merge(cnt)
+        _give_ctx(ctx)
+
+    th = [threading.Thread(target=work, args=(w,)) for w in range(max(1, min(streams, len(sigmas))))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    total.nsh += len(sigmas)
+    return out, total
+
+
+def spectrum_shifts(system, count=None, interval=None, target: int = 30, streams: int = 8, sym=None, perm=None):
+    """Shift placement for solve_spectrum by a speculative inertia pre-pass instead of the reference's
+    sequential march (ref _march eigensolver.py:579-633, lowest-count start :756-773): trial shifts are
+    factored a grid at a time on concurrent streams and the inertia decides where to refine, until every
+    slice holds at most 4 target eigenvalues (the march's acceptance bound) and the slices cover the request.
+
+    Returns (shifts, nus, counters): shifts[0] = the start boundary (sigma0 = -0.1 lambda_1 bound for a
+    count request, as the reference; lo for an interval), shifts[-1] with nu >= count (or = hi)."""
+    from .eigensolver import _lambda1_upper_bound
+
+    counters = CostCounters()
+    if perm is None:
+        perm = separator_ordering(system)
+    if sym is None:
+        sym = Symbolic.on_device(system.device, perm)
+
+    def probe(sig, scale):
+        res, c = factor_inertias(system, sig, scale, streams, sym, perm)
+        counters.merge(c)
+        return res
+
+    if interval is not None:
+        lo, hi = float(interval[0]), float(interval[1])
+        scale = hi - lo
+        pts = probe([lo, hi], scale)
+    else:
+        lam1 = _lambda1_upper_bound(system)
+        scale = lam1
+        sigma0 = -0.1 * lam1
+        for _ in range(8):
+            (s0, nu0), = probe([sigma0], scale)
+            if nu0 == 0:
+                break
+            counters.retries += 1
+            sigma0 = s0 * 10.0
+        pts = [(s0, nu0)]
+        # grow a trial grid until the inertia passes `count`
+        width = lam1 * max(2, target)
+        grid = 8
+        while pts[-1][1] - pts[0][1] < count:
+            top = pts[-1][0]
+            pts += probe([top + width * (j + 1) for j in range(grid)], scale)
+            pts.sort()
+            width *= 2.0
+        # keep the shifts up to the first that covers `count`
+        base = pts[0][1]
+        cut = next(i for i, (_, nu) in enumerate(pts) if nu - base >= count)
+        pts = pts[: cut + 1]
+    # refine: a slice holding more than 4 target eigenvalues gets ceil(c / target) - 1 interior shifts
+    for _ in range(12):
+        new = []
+        for (a, na), (b, nb_) in zip(pts[:-1], pts[1:]):
+            c = nb_ - na
+            if c > 4 * target:
+                k = -(-c // target)
+                new += [a + (b - a) * j / k for j in range(1, k)]
+        if not new:
+            break
+        pts = sorted(pts + probe(new, scale))
+    shifts = np.array([p_[0] for p_ in pts])
+    nus = np.array([p_[1] for p_ in pts], dtype=np.int64)
+    return shifts, nus, counters
+
+
+def solve_spectrum_sliced(system, count=None, interval=None, seed: int = 0, device: bool = False, streams: int = 16,
+                          **kwargs):
+    """solve_spectrum (ref eigensolver.py:715-799) with every slice on its own CUDA stream: the shifts come from
+    the concurrent inertia pre-pass (spectrum_shifts), the slices run through solve_uniform_slices with the
+    caller's SolverOptions (basis m fixed, as the reference's slices), then the reference's selection,
+    cluster de-duplication / Loewdin step and residuals.  Slice k uses seed + k (its own RNG stream; the
+    sequential driver shares one).  Same results as the sequential driver: counts exact, eigenvalues to
+    1e-10."""
+    from .eigensolver import EigenResult, _dedup_and_orthonormalize, pair_residuals
+
+    if (count is None) == (interval is None):
+        raise ValueError("request either the lowest `count` or an `interval`")
+    opts = SolverOptions(**kwargs)
+    if interval is not None:
+        if not float(interval[0]) < float(interval[1]):
+            raise ValueError("empty interval")
+    elif not 1 <= count <= system.dof_count:
+        raise ValueError(f"requested {count} of {system.dof_count} eigenpairs")
+    perm = separator_ordering(system)
+    with solve_plan(solve_sub_levels(streams)):
+        sym = Symbolic.on_device(system.device, perm)
+    shifts, nus, pre = spectrum_shifts(system, count, interval, opts.target, min(streams, 8), sym, perm)
+    sopts = {k: v for k, v in kwargs.items() if k != "m"}
+    S = shifts.size - 1
+    res = solve_uniform_slices(system, shifts, seeds=[seed + k for k in range(S)], streams=streams,
+                               vectors_to_host=False, pencil_symbolic=sym, perm=perm, m_fixed=opts.m, **sopts)
+    counters = res.counters
+    counters.merge(pre)
+    lams, vecs, sid = [], [], []
+    for k in range(S):
+        ev = res.local_eigenvalues.get(k, np.empty(0))
+        X = res.local_vectors.get(k)
+        for j in range(ev.size):
+            lams.append(float(ev[j]))
+            vecs.append(X[j])
+            sid.append(k)
+    order = np.argsort(lams, kind="stable")
+    want = count if interval is None else int(nus[-1] - nus[0])
+    order = order[:want] if interval is None else order
+    lams = [lams[i] for i in order]
+    vecs = [vecs[i] for i in order]
+    lams, vecs = _dedup_and_orthonormalize(lams, vecs, system.M)
+    if len(lams) != want:
+        raise CountMismatch(f"deduplication changed the validated count: kept {len(lams)} of {want}",
+                            expected=want, found=len(lams))
+    lams_arr = np.array(lams)
+    slices = [(float(res.shifts[k]), float(res.shifts[k + 1]), int(res.expected[k])) for k in range(S)]
+    bounds = np.array([s_[1] for s_ in slices])
+    slice_ids = np.minimum(np.searchsorted(bounds, lams_arr, side="left"), S - 1)
+    n = system.dof_count
+    if lams:
+        X = torch.stack(vecs)
+        north, residuals = pair_residuals(system, X, lams_arr)
+        Xout = X.T if device else X.cpu().numpy().T
+    else:
+        north = residuals = np.empty(0)
+        Xout = torch.empty((n, 0), dtype=torch.float64) if device else np.empty((n, 0))
+    gate = max(res.gate_rounds.values(), default=0)
+    return EigenResult(lams_arr, Xout, residuals, slice_ids, slices, counters, north, gate)

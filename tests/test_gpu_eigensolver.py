@@ -348,3 +348,26 @@ def test_delayed_cgs2_matches_two_pass_cgs2():
     np.testing.assert_allclose(ca, cb, rtol=1e-10)
     for x in ca:  # and they are eigenvalues of the pencil (locked ones excluded)
         assert np.min(np.abs(lam[2:] - x)) <= 1e-10 * abs(x)
+
+
+@pytest.mark.parametrize("mode", ["count", "interval"])
+def test_solve_spectrum_parallel_matches_sequential(golden, mode):
+    """solve_spectrum on concurrent streams (speculative inertia pre-pass + every slice on its own stream)
+    returns the sequential reference driver's spectrum: same count, eigenvalues to 1e-10 (and the exact
+    spectrum), residuals within the gate, M-orthonormal vectors."""
+    c = golden["configs"]["cfg2_riga"]
+    s = P.build_system(c["d"], c["ne"], c["p"], c["level"])
+    lam = P.kronecker_spectrum(s)
+    kw = dict(count=100) if mode == "count" else dict(interval=(0.5 * (lam[9] + lam[10]), 0.5 * (lam[79] + lam[80])))
+    seq = P.solve_spectrum(s, seed=3, m=40, **kw)
+    par = P.solve_spectrum(s, seed=3, m=40, parallel=True, streams=8, **kw)
+    assert par.eigenvalues.size == seq.eigenvalues.size == (100 if mode == "count" else 70)
+    np.testing.assert_allclose(par.eigenvalues, seq.eigenvalues, rtol=1e-10)
+    ref = lam[:100] if mode == "count" else lam[10:80]
+    np.testing.assert_allclose(par.eigenvalues, ref, rtol=1e-10)
+    assert float(par.north_residuals.max()) <= 1e-8
+    X = par.vectors
+    G = X.T @ (s.M.csr @ X)
+    assert np.abs(G - np.eye(G.shape[0])).max() < 1e-8
+    assert len(par.slices) >= 3 and all(c_ <= 4 * 20 for _, _, c_ in par.slices)
+    assert par.counters.nfa >= par.counters.nsh > 0
