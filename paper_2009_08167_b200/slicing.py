@@ -729,12 +729,17 @@ def spectrum_shifts(system, count=None, interval=None, target: int = 30, streams
             pts += probe([top + width * (j + 1) for j in range(grid)], scale)
             pts.sort()
             width *= 2.0
-        # keep the shifts up to the first that covers `count`
+    def cut(pts):
+        # a count request keeps the shifts up to the first that covers `count`
+        if interval is not None:
+            return pts
         base = pts[0][1]
-        cut = next(i for i, (_, nu) in enumerate(pts) if nu - base >= count)
-        pts = pts[: cut + 1]
+        i = next(i for i, (_, nu) in enumerate(pts) if nu - base >= count)
+        return pts[: i + 1]
+
+    pts = cut(pts)
     # refine: a slice holding more than 4 target eigenvalues gets ceil(c / target) - 1 interior shifts
-    for _ in range(12):
+    for _ in range(40):
         new = []
         for (a, na), (b, nb_) in zip(pts[:-1], pts[1:]):
             c = nb_ - na
@@ -743,7 +748,7 @@ def spectrum_shifts(system, count=None, interval=None, target: int = 30, streams
                 new += [a + (b - a) * j / k for j in range(1, k)]
         if not new:
             break
-        pts = sorted(pts + probe(new, scale))
+        pts = cut(sorted(pts + probe(new, scale)))
     shifts = np.array([p_[0] for p_ in pts])
     nus = np.array([p_[1] for p_ in pts], dtype=np.int64)
     return shifts, nus, counters
