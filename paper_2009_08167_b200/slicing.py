@@ -687,12 +687,13 @@ def factor_inertias(system, sigmas, scale: float, streams: int = 8, sym=None, pe
 
 def spectrum_shifts(system, count=None, interval=None, target: int = 30, streams: int = 8, sym=None, perm=None):
     """Shift placement for solve_spectrum by a speculative inertia pre-pass instead of the reference's
-    sequential march (ref _march eigensolver.py:579-633, lowest-count start :756-773): trial shifts are
-    factored a grid at a time on concurrent streams and the inertia decides where to refine, until every
-    slice holds at most 4 target eigenvalues (the march's acceptance bound) and the slices cover the request.
-
-    Returns (shifts, nus, counters): shifts[0] = the start boundary (sigma0 = -0.1 lambda_1 bound for a
-    count request, as the reference; lo for an interval), shifts[-1] with nu >= count (or = hi)."""
+    sequential march (ref _march eigensolver.py:579-633, lowest-count start :756-773).  Trial shifts are
+    factored a batch at a time on concurrent streams; where they go is predicted from the inertia counts
+    already known with Weyl's law for the d-dimensional Laplacian, nu(sigma) ~ C sigma^(d/2): the first probe
+    calibrates C, every slice is aimed at `target` eigenvalues (the march's width rule), and a slice that
+    still holds more than 4 target (the march's acceptance bound) is split again between its measured
+    endpoints.  Returns (shifts, nus, counters): shifts[0] = sigma0 = -0.1 lambda_1-bound for a count
+    request (as the reference) or lo for an interval; the last shift covers `count` (or is hi)."""
     from .eigensolver import _lambda1_upper_bound
 
     counters = CostCounters()
@@ -700,11 +701,19 @@ def spectrum_shifts(system, count=None, interval=None, target: int = 30, streams
         perm = separator_ordering(system)
     if sym is None:
         sym = Symbolic.on_device(system.device, perm)
+    e = 0.5 * system.dim  # Weyl exponent
 
     def probe(sig, scale):
         res, c = factor_inertias(system, sig, scale, streams, sym, perm)
         counters.merge(c)
         return res
+
+    def split(a, na, b, nb_, k):
+        """k - 1 shifts in (a, b) at equal predicted counts (power law through the two endpoints)."""
+        if a < 0.0 or b <= 0.0:
+            return [a + (b - a) * j / k for j in range(1, k)]
+        ua, ub = a ** e, b ** e
+        return [(ua + (ub - ua) * j / k) ** (1.0 / e) for j in range(1, k)]
 
     if interval is not None:
         lo, hi = float(interval[0]), float(interval[1])
@@ -721,14 +730,21 @@ def spectrum_shifts(system, count=None, interval=None, target: int = 30, streams
             counters.retries += 1
             sigma0 = s0 * 10.0
         pts = [(s0, nu0)]
-        # grow a trial grid until the inertia passes `count`
-        width = lam1 * max(2, target)
-        grid = 8
-        while pts[-1][1] - pts[0][1] < count:
-            top = pts[-1][0]
-            pts += probe([top + width * (j + 1) for j in range(grid)], scale)
-            pts.sort()
-            width *= 2.0
+        # calibrate nu ~ C sigma^e with one probe, then aim a batch at count (+ one beyond) and keep
+        # extending by the fit until count is covered
+        (s1, nu1), = probe([lam1 * max(2, target)], scale)
+        pts.append((s1, nu1))
+        while max(nu for _, nu in pts) - nu0 < count:
+            sa, na = max(pts, key=lambda t: t[1])
+            if na - nu0 <= 0:
+                pts += probe([sa * 4.0], scale)
+                continue
+            c_fit = (na - nu0) / sa ** e
+            want = [((nu0 + count * j / 8.0) / c_fit) ** (1.0 / e) for j in range(1, 9)]
+            want.append((1.05 * (nu0 + count) / c_fit) ** (1.0 / e))
+            pts += probe([w_ for w_ in want if w_ > sa], scale) or probe([2.0 * sa], scale)
+        pts.sort()
+
     def cut(pts):
         # a count request keeps the shifts up to the first that covers `count`
         if interval is not None:
@@ -738,14 +754,15 @@ def spectrum_shifts(system, count=None, interval=None, target: int = 30, streams
         return pts[: i + 1]
 
     pts = cut(pts)
-    # refine: a slice holding more than 4 target eigenvalues gets ceil(c / target) - 1 interior shifts
+    # aim every slice at `target`; split again any slice above 4 target (the march's acceptance bound)
+    first = True
     for _ in range(40):
         new = []
         for (a, na), (b, nb_) in zip(pts[:-1], pts[1:]):
             c = nb_ - na
-            if c > 4 * target:
-                k = -(-c // target)
-                new += [a + (b - a) * j / k for j in range(1, k)]
+            if c > (target if first else 4 * target):
+                new += split(a, na, b, nb_, -(-c // target))
+        first = False
         if not new:
             break
         pts = cut(sorted(pts + probe(new, scale)))
@@ -775,13 +792,18 @@ def solve_spectrum_sliced(system, count=None, interval=None, seed: int = 0, devi
     perm = separator_ordering(system)
     with solve_plan(solve_sub_levels(streams)):
         sym = Symbolic.on_device(system.device, perm)
+    _t0 = time.perf_counter()
     shifts, nus, pre = spectrum_shifts(system, count, interval, opts.target, min(streams, 8), sym, perm)
+    t_shifts = time.perf_counter() - _t0
     sopts = {k: v for k, v in kwargs.items() if k != "m"}
     S = shifts.size - 1
     res = solve_uniform_slices(system, shifts, seeds=[seed + k for k in range(S)], streams=streams,
                                vectors_to_host=False, pencil_symbolic=sym, perm=perm, m_fixed=opts.m, **sopts)
     counters = res.counters
     counters.merge(pre)
+    counters.phase("spectrum_shifts", t_shifts)
+    counters.phase("spectrum_slices", res.timings.get("total_s", 0.0))
+    counters.phase("spectrum_probes", float(pre.nsh))
     lams, vecs, sid = [], [], []
     for k in range(S):
         ev = res.local_eigenvalues.get(k, np.empty(0))

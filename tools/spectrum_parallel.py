@@ -26,6 +26,7 @@ for rep in range(2):  # second run warm
     torch.cuda.synchronize()
     out["parallel_s"] = time.perf_counter() - t0
 out["parallel_slices"] = len(r.slices)
+out["phases"] = {k: round(v, 3) for k, v in r.counters.phase_s.items() if k.startswith("spectrum")}
 out["parallel_err_vs_exact"] = float(np.max(np.abs(r.eigenvalues - lam[:count]) / lam[:count]))
 out["parallel_max_residual"] = float(r.north_residuals.max())
 out["eigenpairs_per_s"] = count / out["parallel_s"]
