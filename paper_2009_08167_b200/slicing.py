@@ -709,11 +709,13 @@ def spectrum_shifts(system, count=None, interval=None, target: int = 30, streams
         return res
 
     def split(a, na, b, nb_, k):
-        """k - 1 shifts in (a, b) at equal predicted counts (power law through the two endpoints)."""
-        if a < 0.0 or b <= 0.0:
+        """k - 1 shifts in (a, b) at equal predicted counts (power law through the endpoints, from 0 for a
+        lower end below the spectrum of the positive definite Laplacian pencil)."""
+        if b <= 0.0:
             return [a + (b - a) * j / k for j in range(1, k)]
-        ua, ub = a ** e, b ** e
-        return [(ua + (ub - ua) * j / k) ** (1.0 / e) for j in range(1, k)]
+        ua, ub = max(a, 0.0) ** e, b ** e
+        out = [(ua + (ub - ua) * j / k) ** (1.0 / e) for j in range(1, k)]
+        return [x for x in out if a < x < b]
 
     if interval is not None:
         lo, hi = float(interval[0]), float(interval[1])
@@ -730,20 +732,17 @@ def spectrum_shifts(system, count=None, interval=None, target: int = 30, streams
             counters.retries += 1
             sigma0 = s0 * 10.0
         pts = [(s0, nu0)]
-        # calibrate nu ~ C sigma^e with one probe, then aim a batch at count (+ one beyond) and keep
-        # extending by the fit until count is covered
-        (s1, nu1), = probe([lam1 * max(2, target)], scale)
-        pts.append((s1, nu1))
-        while max(nu for _, nu in pts) - nu0 < count:
-            sa, na = max(pts, key=lambda t: t[1])
-            if na - nu0 <= 0:
-                pts += probe([sa * 4.0], scale)
-                continue
-            c_fit = (na - nu0) / sa ** e
+        # Weyl's law on [0, 1]^d, nu(sigma) ~ c sigma^e (c = 1/pi, 1/(4 pi), 1/(6 pi^2)), recalibrated from
+        # every batch: a batch aims at count j/8 (j = 1..8) and 1.05 count until count is covered
+        c_fit = {1: 1.0 / math.pi, 2: 1.0 / (4.0 * math.pi), 3: 1.0 / (6.0 * math.pi ** 2)}[system.dim]
+        for _ in range(20):
             want = [((nu0 + count * j / 8.0) / c_fit) ** (1.0 / e) for j in range(1, 9)]
-            want.append((1.05 * (nu0 + count) / c_fit) ** (1.0 / e))
-            pts += probe([w_ for w_ in want if w_ > sa], scale) or probe([2.0 * sa], scale)
-        pts.sort()
+            want.append(((nu0 + 1.05 * count) / c_fit) ** (1.0 / e))
+            pts = sorted(pts + probe(want, scale))
+            if max(nu for _, nu in pts) - nu0 >= count:
+                break
+            sa, na = max(pts, key=lambda t: (t[1], t[0]))
+            c_fit = (na - nu0) / sa ** e if na > nu0 else c_fit / 4.0
 
     def cut(pts):
         # a count request keeps the shifts up to the first that covers `count`

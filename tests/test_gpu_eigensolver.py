@@ -358,12 +358,16 @@ def test_solve_spectrum_parallel_matches_sequential(golden, mode):
     c = golden["configs"]["cfg2_riga"]
     s = P.build_system(c["d"], c["ne"], c["p"], c["level"])
     lam = P.kronecker_spectrum(s)
-    kw = dict(count=100) if mode == "count" else dict(interval=(0.5 * (lam[9] + lam[10]), 0.5 * (lam[79] + lam[80])))
+    # interval endpoints in spectral gaps (2D eigenvalues come in degenerate pairs)
+    gap = lambda i: next(j for j in range(i, lam.size - 1) if lam[j + 1] - lam[j] > 1e-6 * lam[j + 1])  # noqa: E731
+    i0, i1 = gap(9), gap(79)
+    kw = dict(count=100) if mode == "count" else dict(interval=(0.5 * (lam[i0] + lam[i0 + 1]),
+                                                                0.5 * (lam[i1] + lam[i1 + 1])))
     seq = P.solve_spectrum(s, seed=3, m=40, **kw)
     par = P.solve_spectrum(s, seed=3, m=40, parallel=True, streams=8, **kw)
-    assert par.eigenvalues.size == seq.eigenvalues.size == (100 if mode == "count" else 70)
+    assert par.eigenvalues.size == seq.eigenvalues.size == (100 if mode == "count" else i1 - i0)
     np.testing.assert_allclose(par.eigenvalues, seq.eigenvalues, rtol=1e-10)
-    ref = lam[:100] if mode == "count" else lam[10:80]
+    ref = lam[:100] if mode == "count" else lam[i0 + 1: i1 + 1]
     np.testing.assert_allclose(par.eigenvalues, ref, rtol=1e-10)
     assert float(par.north_residuals.max()) <= 1e-8
     X = par.vectors
