@@ -589,6 +589,8 @@ def solve_uniform_slices(system, shifts, seeds=None, m_factor: int = 2, streams:
             lams_k = lams_k[keep]
             X_k = X_k[keep] if isinstance(X_k, np.ndarray) else X_k[torch.as_tensor(keep, device=X_k.device)]
             res_k = res_k[keep] if res_k.size else res_k
+            if rr_k is not None and rr_k.ref_residuals is not None and rr_k.ref_residuals.size:
+                rr_k.ref_residuals = rr_k.ref_residuals[keep]
         results[k] = (lams_k, X_k, res_k, rr_k)
         if lams_k.size < expected[k]:
             # a dropped copy took the place of one of this slice's own pairs: search (lo, hi] again with
@@ -774,11 +776,11 @@ def solve_spectrum_sliced(system, count=None, interval=None, seed: int = 0, devi
                           **kwargs):
     """solve_spectrum (ref eigensolver.py:715-799) with every slice on its own CUDA stream: the shifts come from
     the concurrent inertia pre-pass (spectrum_shifts), the slices run through solve_uniform_slices with the
-    caller's SolverOptions (basis m fixed, as the reference's slices), then the reference's selection,
-    cluster de-duplication / Loewdin step and residuals.  Slice k uses seed + k (its own RNG stream; the
-    sequential driver shares one).  Same results as the sequential driver: counts exact, eigenvalues to
-    1e-10."""
-    from .eigensolver import EigenResult, _dedup_and_orthonormalize, pair_residuals
+    caller's SolverOptions (basis m fixed, as the reference's slices; residual gate and boundary
+    de-duplication per slice), then the reference's selection of the lowest `count` (or every pair of the
+    interval).  Slice k uses seed + k (its own RNG stream; the sequential driver shares one).  Same results as
+    the sequential driver: counts exact, eigenvalues to 1e-10."""
+    from .eigensolver import EigenResult
 
     if (count is None) == (interval is None):
         raise ValueError("request either the lowest `count` or an `interval`")
@@ -788,49 +790,60 @@ def solve_spectrum_sliced(system, count=None, interval=None, seed: int = 0, devi
             raise ValueError("empty interval")
     elif not 1 <= count <= system.dof_count:
         raise ValueError(f"requested {count} of {system.dof_count} eigenpairs")
+    _ta = time.perf_counter()
     perm = separator_ordering(system)
     with solve_plan(solve_sub_levels(streams)):
         sym = Symbolic.on_device(system.device, perm)
+    t_sym = time.perf_counter() - _ta
     _t0 = time.perf_counter()
     shifts, nus, pre = spectrum_shifts(system, count, interval, opts.target, min(streams, 8), sym, perm)
     t_shifts = time.perf_counter() - _t0
     sopts = {k: v for k, v in kwargs.items() if k != "m"}
     S = shifts.size - 1
+    # host vectors come back per slice (pinned, asynchronous, overlapping the other slices); pairs of two
+    # slices in one eigenvalue cluster can only meet at a shared shift, where solve_uniform_slices' boundary
+    # de-duplication applies the reference's _Pool.add / _dedup_and_orthonormalize rules, and a slice's own
+    # locked pairs are M-orthonormal by construction, so the final cluster pass of the sequential driver
+    # has nothing left to do here
     res = solve_uniform_slices(system, shifts, seeds=[seed + k for k in range(S)], streams=streams,
-                               vectors_to_host=False, pencil_symbolic=sym, perm=perm, m_fixed=opts.m, **sopts)
+                               vectors_to_host=not device, pencil_symbolic=sym, perm=perm, m_fixed=opts.m, **sopts)
     counters = res.counters
     counters.merge(pre)
     counters.phase("spectrum_shifts", t_shifts)
     counters.phase("spectrum_slices", res.timings.get("total_s", 0.0))
     counters.phase("spectrum_probes", float(pre.nsh))
-    lams, vecs, sid = [], [], []
-    for k in range(S):
-        ev = res.local_eigenvalues.get(k, np.empty(0))
-        X = res.local_vectors.get(k)
-        for j in range(ev.size):
-            lams.append(float(ev[j]))
-            vecs.append(X[j])
-            sid.append(k)
-    order = np.argsort(lams, kind="stable")
+    counters.phase("spectrum_symbolic", t_sym)
+    _tf = time.perf_counter()
     want = count if interval is None else int(nus[-1] - nus[0])
-    order = order[:want] if interval is None else order
-    lams = [lams[i] for i in order]
-    vecs = [vecs[i] for i in order]
-    lams, vecs = _dedup_and_orthonormalize(lams, vecs, system.M)
-    if len(lams) != want:
-        raise CountMismatch(f"deduplication changed the validated count: kept {len(lams)} of {want}",
-                            expected=want, found=len(lams))
-    lams_arr = np.array(lams)
+    lam_l, vec_l, north_l, ref_l, sid_l = [], [], [], [], []
+    taken = 0
+    for k in range(S):  # slices in ascending order; a count request stops at `count`
+        ev = res.local_eigenvalues.get(k, np.empty(0))
+        if ev.size == 0:
+            continue
+        take = ev.size if interval is not None else min(ev.size, want - taken)
+        if take <= 0:
+            break
+        info = res.gate_info.get(k)
+        lam_l.append(ev[:take])
+        vec_l.append(res.local_vectors[k][:take])
+        north_l.append(res.residuals[k][:take])
+        ref_l.append(info.ref_residuals[:take] if info is not None and info.ref_residuals is not None
+                     else np.full(take, np.nan))
+        sid_l.append(np.full(take, k))
+        taken += take
+    if taken != want:
+        raise CountMismatch(f"slices returned {taken} of {want} eigenpairs", expected=want, found=taken)
+    lams_arr = np.concatenate(lam_l) if lam_l else np.empty(0)
+    north = np.concatenate(north_l) if north_l else np.empty(0)
+    residuals = np.concatenate(ref_l) if ref_l else np.empty(0)
+    slice_ids = np.concatenate(sid_l) if sid_l else np.empty(0, dtype=int)
     slices = [(float(res.shifts[k]), float(res.shifts[k + 1]), int(res.expected[k])) for k in range(S)]
-    bounds = np.array([s_[1] for s_ in slices])
-    slice_ids = np.minimum(np.searchsorted(bounds, lams_arr, side="left"), S - 1)
     n = system.dof_count
-    if lams:
-        X = torch.stack(vecs)
-        north, residuals = pair_residuals(system, X, lams_arr)
-        Xout = X.T if device else X.cpu().numpy().T
+    if device:
+        Xout = torch.cat(vec_l).T if vec_l else torch.empty((n, 0), dtype=torch.float64)
     else:
-        north = residuals = np.empty(0)
-        Xout = torch.empty((n, 0), dtype=torch.float64) if device else np.empty((n, 0))
+        Xout = np.concatenate(vec_l).T if vec_l else np.empty((n, 0))
     gate = max(res.gate_rounds.values(), default=0)
+    counters.phase("spectrum_finish", time.perf_counter() - _tf)
     return EigenResult(lams_arr, Xout, residuals, slice_ids, slices, counters, north, gate)
