@@ -96,6 +96,10 @@ struct riga_ctx {
   double* scratch_host = nullptr;  // pinned scratch for small D2H reads
   double* scratch_dev = nullptr;   // small device scratch (reductions)
   size_t scratch_dev_n = 0;
+  // side streams of the factorization (factor.cu, created on first use): [0] panel chain (high
+  // priority), [1] solve-side companions (low priority); events for the hand-offs
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaEvent_t aux_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 // Device guard: sets the current device for the scope.

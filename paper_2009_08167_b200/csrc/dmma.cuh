@@ -119,21 +119,31 @@ namespace riga {
 // DMMA.8x8x4 tiles (64 fp64 accumulators per thread).  k runs in steps of 16
 // through kT128Stages shared-memory stages filled by 8-byte cp.async (rows
 // of a front are not 16-byte aligned in general) with zero fill outside the
-// ranges; d (the pivots D, or nullptr for 1) multiplies the A fragments in
-// registers.  Pitch 132 doubles (== 4 mod 16): the 16 lanes of a half warp
-// (4 k rows x 4 columns) hit 16 distinct banks pairs.
+// ranges.  The pivots d (or 1 for nullptr) and the sign are folded into the A
+// stage in shared memory one stage ahead of its use, by the thread that copied
+// the element (cp.async.wait_group covers a thread's own copies, so no extra
+// barrier): the k loop is fragment loads and DMMAs only.  (With the scaling
+// in the k loop -- one DMUL per A fragment on the pipe the DMMAs use, in the
+// LDS -> DMUL -> DMMA chain of a single reused fragment register -- ncu showed
+// the DMMA pipe 67 % active on K = 512 frontal updates.)  Pitch 132 doubles
+// (== 4 mod 16): the 16 lanes of a half warp (4 k rows x 4 columns) hit 16
+// distinct bank pairs.
 // ---------------------------------------------------------------------------
 constexpr int kT128 = 128;
 constexpr int kT128K = 16;
 constexpr int kT128P = 132;
-constexpr int kT128Stages = 3;
-constexpr int kT128StageDoubles = 2 * kT128K * kT128P + kT128K;
+constexpr int kT128Stages = 4;
+constexpr int kT128StageDoubles = 2 * kT128K * kT128P;
 constexpr size_t kT128Smem = (size_t)kT128Stages * kT128StageDoubles * sizeof(double);
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   const int n = pred ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async8n(double* smem, const double* gmem, int nbytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(nbytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -143,9 +153,10 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // EPI 0: C(i - coff, j - coff) -= A d B^T; EPI 2: the same with the columns j >= jsplit going to C2
 // (ld ldc2, rows and columns offset by jsplit) and only i >= j touched (a front's pivot columns and its
-// update block in one trailing update).  The C tile is loaded into the accumulators before the K loop
-// (its 64 loads per thread in flight together, overlapping the pipeline prologue) and the MMAs subtract
-// (negated A fragments), so the epilogue is stores only.
+// update block in one trailing update; c2_overwrite: C2 = -A d B^T, nothing read from it).  The C tile
+// is loaded into the accumulators before the K loop (its 64 loads per thread in flight together,
+// overlapping the pipeline prologue) and the MMAs subtract (negated A stage), so the epilogue is
+// stores only.
 template <int EPI = 0>
 __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64_t lda,
                                              const double* __restrict__ B, int64_t ldb,
@@ -153,7 +164,7 @@ __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64
                                              int64_t i0, int64_t j0, int64_t mend, int64_t nend,
                                              double* C, int64_t ldc, int64_t coff,
                                              double* __restrict__ smem, double* C2 = nullptr, int64_t ldc2 = 0,
-                                             int64_t jsplit = 0) {
+                                             int64_t jsplit = 0, bool c2_overwrite = false) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;
   const int r = lane >> 2, cc = (lane & 3) * 2;
@@ -172,69 +183,101 @@ __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const double* p = cptr(i0 + wm * 64 + m * 8 + r, j0 + wn * 32 + q * 8 + cc + e);
-        acc[m][q][e] = p ? *p : 0.0;
+        const int64_t jc = j0 + wn * 32 + q * 8 + cc + e;
+        const double* p = cptr(i0 + wm * 64 + m * 8 + r, jc);
+        // c2_overwrite: the C2 part holds nothing yet (a front's update block at its first update)
+        acc[m][q][e] = p && !(EPI == 2 && c2_overwrite && jc >= jsplit) ? *p : 0.0;
       }
-  const int64_t nk = (k1 - k0 + kT128K - 1) / kT128K;
-  auto stage_ptr = [&](int s) { return smem + (int64_t)s * kT128StageDoubles; };
-  // thread -> (k row kr0 + 2u, column ci) of a stage; row/column predicates fixed per thread
-  const int ci = tid & 127, kr0 = tid >> 7;
-  const bool prow = i0 + ci < mend, pcol = j0 + ci < nend;
-  const double* Ab = A + (prow ? i0 + ci : 0);
-  const double* Bb = B + (pcol ? j0 + ci : 0);
-  auto load = [&](int s, int64_t kt) {
-    double* As = stage_ptr(s) + kr0 * kT128P + ci;
-    double* Bs = As + kT128K * kT128P;
-    const int64_t kb = kt + kr0;
-    const double* pa = Ab + kb * lda;
-    const double* pb = Bb + kb * ldb;
+  const int nk = (int)((k1 - k0 + kT128K - 1) / kT128K);
+  // thread -> k row kr, columns c8 + 16 u (u < 8) of a stage: one pivot per thread and stage, the
+  // 8 copies of an operand at constant offsets from one pointer
+  const int kr = tid >> 4, c8 = tid & 15;
+  unsigned ma = 0, mb = 0;  // column predicates
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const bool kin = kb + 2 * u < k1;
-      cp_async8(As + 2 * u * kT128P, kin && prow ? pa : A, kin && prow);
-      cp_async8(Bs + 2 * u * kT128P, kin && pcol ? pb : B, kin && pcol);
-      pa += 2 * lda;
-      pb += 2 * ldb;
-    }
-    if (tid < kT128K) {
-      double* Ds = stage_ptr(s) + 2 * kT128K * kT128P;
-      const int64_t kk = kt + tid;
-      if (d) {
-        cp_async8(Ds + tid, kk < k1 ? d + kk : d, kk < k1);
-      } else {
-        Ds[tid] = 1.0;
+  for (int u = 0; u < 8; ++u) {
+    ma |= (i0 + c8 + 16 * u < mend ? 1u : 0u) << u;
+    mb |= (j0 + c8 + 16 * u < nend ? 1u : 0u) << u;
+  }
+  const bool full = ma == 0xffu && mb == 0xffu;
+  const double* Ab = A + (k0 + kr) * lda + i0 + c8;
+  const double* Bb = B + (k0 + kr) * ldb + j0 + c8;
+  double* const S0 = smem + kr * kT128P + c8;  // this thread's first A element of stage 0
+  auto load = [&](int it) {
+    double* As = S0 + (it % kT128Stages) * kT128StageDoubles;
+    double* Bs = As + kT128K * kT128P;
+    const double* pa = Ab + (int64_t)it * kT128K * lda;
+    const double* pb = Bb + (int64_t)it * kT128K * ldb;
+    const bool kin = k0 + (int64_t)it * kT128K + kr < k1;
+    if (full && kin) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        cp_async8n(As + 16 * u, pa + 16 * u, 8);
+        cp_async8n(Bs + 16 * u, pb + 16 * u, 8);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool ina = kin && (ma >> u & 1u), inb = kin && (mb >> u & 1u);
+        cp_async8n(As + 16 * u, ina ? pa + 16 * u : A, ina ? 8 : 0);
+        cp_async8n(Bs + 16 * u, inb ? pb + 16 * u : B, inb ? 8 : 0);
       }
     }
   };
+  // d of this thread's k row in stage `it` (zero-filled rows: any finite value); the value is only
+  // consumed by the next iteration's scale(), so the load's latency hides behind a stage of MMAs
+  auto pivot = [&](int it) -> double {
+    const int64_t kk = k0 + (int64_t)it * kT128K + kr;
+    return d ? (it < nk && kk < k1 ? d[kk] : 0.0) : 1.0;
+  };
+  // fold -d into this thread's own A elements of stage `it` (its copies have landed)
+  auto scale = [&](int it, double dk) {
+    double* As = S0 + (it % kT128Stages) * kT128StageDoubles;
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = As[16 * u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) As[16 * u] = v[u] * -dk;
+  };
 #pragma unroll
   for (int s = 0; s < kT128Stages - 1; ++s) {
-    if (s < nk) load(s, k0 + (int64_t)s * kT128K);
+    if (s < nk) load(s);
     cp_async_commit();
   }
-  for (int64_t it = 0; it < nk; ++it) {
+  double dpend = pivot(1);  // pivot of the stage scaled next (loaded one iteration ahead of its use)
+  {
+    const double d0 = pivot(0);
     cp_async_wait<kT128Stages - 2>();
+    if (nk > 0) scale(0, d0);
+  }
+  const double* Af = smem + (lane & 3) * kT128P + wm * 64 + (lane >> 2);
+  const double* Bf = smem + kT128K * kT128P + (lane & 3) * kT128P + wn * 32 + (lane >> 2);
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<kT128Stages - 3>();  // this thread's copies of stage it + 1 have landed
+    if (it + 1 < nk) scale(it + 1, dpend);
     __syncthreads();
-    {
-      const int64_t nx = it + kT128Stages - 1;
-      if (nx < nk) load((int)(nx % kT128Stages), k0 + nx * kT128K);
-      cp_async_commit();
-    }
-    const double* As = stage_ptr((int)(it % kT128Stages));
-    const double* Bs = As + kT128K * kT128P;
-    const double* Ds = Bs + kT128K * kT128P;
+    if (it + kT128Stages - 1 < nk) load(it + kT128Stages - 1);
+    cp_async_commit();
+    dpend = pivot(it + 2);
+    const double* As = Af + (it % kT128Stages) * kT128StageDoubles;
+    const double* Bs = Bf + (it % kT128Stages) * kT128StageDoubles;
+    double av[2][8], bv[2][4];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) av[0][m] = As[m * 8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bv[0][q] = Bs[q * 8];
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
-      const int kr = k4 * 4 + (lane & 3);
-      const double ndk = -Ds[kr];
-      double av[8], bv[4];
+      const int cur = k4 & 1, nxt = cur ^ 1;
+      if (k4 < 3) {
 #pragma unroll
-      for (int m = 0; m < 8; ++m) av[m] = As[kr * kT128P + wm * 64 + m * 8 + (lane >> 2)] * ndk;
+        for (int m = 0; m < 8; ++m) av[nxt][m] = As[(k4 + 1) * 4 * kT128P + m * 8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) bv[q] = Bs[kr * kT128P + wn * 32 + q * 8 + (lane >> 2)];
+        for (int q = 0; q < 4; ++q) bv[nxt][q] = Bs[(k4 + 1) * 4 * kT128P + q * 8];
+      }
 #pragma unroll
       for (int m = 0; m < 8; ++m)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[m][q][0], acc[m][q][1], av[m], bv[q]);
+        for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[m][q][0], acc[m][q][1], av[cur][m], bv[cur][q]);
     }
   }
   cp_async_wait<0>();

@@ -79,8 +79,11 @@ __global__ void k_asm_large(SymDev S, const int32_t* __restrict__ nodes,
   }
 }
 
-// child update block (lower triangle, ld nu_c) scatter-added into the parent
-__global__ void k_extend_add(SymDev S, const int32_t* __restrict__ items,
+// child update block (lower triangle, ld nu_c) scatter-added into the parent:
+// part 0 = the columns that land in the parent's pivot columns (before the
+// parent is factored), part 1 = the columns that land in the parent's update
+// block (after the parent's own Schur complement has been written there)
+__global__ void k_extend_add(SymDev S, const int32_t* __restrict__ items, int part,
                              double* __restrict__ panel, double* __restrict__ cb) {
   int c = items[blockIdx.y];
   int p = S.sparent[c];
@@ -94,13 +97,11 @@ __global__ void k_extend_add(SymDev S, const int32_t* __restrict__ items,
   int64_t b0 = (int64_t)blockIdx.x * 32;
   for (int64_t b = b0 + w; b < min(b0 + 32, nuc); b += nw) {
     int64_t rb = rp[b];
-    for (int64_t a = b + lane; a < nuc; a += 32) {
-      int64_t ra = rp[a];
-      double v = src[b * nuc + a];
-      if (rb < npp)
-        P[rb * fp + ra] += v;
-      else
-        C[(rb - npp) * nup + (ra - npp)] += v;
+    if ((rb < npp) != (part == 0)) continue;
+    if (rb < npp) {
+      for (int64_t a = b + lane; a < nuc; a += 32) P[rb * fp + rp[a]] += src[b * nuc + a];
+    } else {
+      for (int64_t a = b + lane; a < nuc; a += 32) C[(rb - npp) * nup + (rp[a] - npp)] += src[b * nuc + a];
     }
   }
 }
@@ -442,10 +443,12 @@ __global__ void __launch_bounds__(32) k_trsm128(SymDev S, const int32_t* __restr
 //                      its Schur complement slice by slice with the pivot columns instead of one long-K
 //                      pass at the end).
 // tri != 0: blockIdx.x enumerates the lower tiles of a triangle of ntj x ntj tiles.
+// first != 0: the update block holds nothing yet and is written, not accumulated (the children's
+// contributions are extend-added into it afterwards), so it is never zeroed or read here.
 __global__ void __launch_bounds__(256, 1) k_trail128(SymDev S, const int32_t* __restrict__ nodes, int64_t k0,
                                                      int64_t k1, int64_t c0, int64_t c1, int wide, int ntj,
-                                                     int tri, double* __restrict__ panel, double* __restrict__ cb,
-                                                     const double* __restrict__ D) {
+                                                     int tri, int first, double* __restrict__ panel,
+                                                     double* __restrict__ cb, const double* __restrict__ D) {
   extern __shared__ double sm[];
   const int s = nodes[blockIdx.y];
   const int64_t f = S.front[s], np = S.ncol[s];
@@ -467,7 +470,8 @@ __global__ void __launch_bounds__(256, 1) k_trail128(SymDev S, const int32_t* __
   const int64_t i0 = cs + ti * kT128, j0 = cs + tj * kT128;
   if (i0 >= f || j0 >= ce || i0 + kT128 - 1 < j0) return;
   double* L = panel + S.panel_off[s];
-  dmma_tile128<2>(L, f, L, f, D + S.col0[s], k0, kend, i0, j0, f, ce, L, f, 0, sm, cb + S.cb_off[s], f - np, np);
+  dmma_tile128<2>(L, f, L, f, D + S.col0[s], k0, kend, i0, j0, f, ce, L, f, 0, sm, cb + S.cb_off[s], f - np, np,
+                  first != 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -568,14 +572,7 @@ static int upload_symbolic(riga_symbolic* sym) {
   return RIGA_OK;
 }
 
-__global__ void k_zero_cb(SymDev S, const int32_t* __restrict__ nodes, double* __restrict__ cb) {
-  const int s = nodes[blockIdx.y];
-  const int64_t nu = S.front[s] - S.ncol[s], len = nu * nu;
-  double* c = cb + S.cb_off[s];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
-    c[i] = 0.0;
-}
-
+static int g_lookahead = 1;  // RIGA_FACTOR_LOOKAHEAD=0: everything on the factor stream
 static int64_t g_nb2 = 512;  // outer block of the trailing updates (multiple of 128; RIGA_FACTOR_NB2)
 
 static int set_smem_attrs() {
@@ -584,6 +581,8 @@ static int set_smem_attrs() {
   {
     const char* e = getenv("RIGA_FACTOR_NB2");
     if (e && atoll(e) >= 128) g_nb2 = atoll(e) / 128 * 128;
+    const char* la = getenv("RIGA_FACTOR_LOOKAHEAD");
+    if (la && *la) g_lookahead = atoi(la);
   }
   RIGA_CUDA(cudaFuncSetAttribute(k_trsm128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem));
   RIGA_CUDA(cudaFuncSetAttribute(k_trail128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem));
@@ -598,6 +597,21 @@ static int set_smem_attrs() {
   done = true;
   return RIGA_OK;
 }
+
+// Side streams and events of a context (created on first use): aux[0] runs the
+// panel chain of the large fronts one outer block ahead of the trailing
+// updates (high priority), aux[1] builds the solve-side companions (G blocks)
+// of the lower levels while the upper levels are still being factored.
+static int ctx_aux(riga_ctx* ctx) {
+  if (ctx->aux[0]) return RIGA_OK;
+  int lo = 0, hi = 0;
+  RIGA_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  RIGA_CUDA(cudaStreamCreateWithPriority(&ctx->aux[0], cudaStreamNonBlocking, hi));
+  RIGA_CUDA(cudaStreamCreateWithPriority(&ctx->aux[1], cudaStreamNonBlocking, lo));
+  for (auto& e : ctx->aux_ev) RIGA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return RIGA_OK;
+}
+
 
 static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const double* Mv,
                    double sigma, double rel) {
@@ -622,21 +636,35 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
                                                         F->panel.p); count_launch();
     RIGA_CUDA(cudaGetLastError());
   }
+  // does any level have more than one outer block?  then the panel chain runs ahead on aux[0]
+  bool ahead = false;
+  for (int64_t l = 0; l < h.nlevels; ++l) ahead = ahead || (sym->plan[l].nlarge && sym->plan[l].max_np_large > g_nb2);
+  ahead = ahead && g_lookahead;
+  riga_ctx* ctx = F->ctx;
+  if (ahead) RIGA_TRY(ctx_aux(ctx));
+  // G blocks of the small supernodes: on the low-priority side stream as soon as their last level is
+  // factored, beside the upper levels (whose panel chains leave SMs idle); joined at the end
+  const int64_t g_top = small_g_top_level(sym);
+  const SolvePlanHost& SP = sym->sp;
+  if (g_top >= 0 && !F->gsmall.p) RIGA_TRY(F->gsmall.alloc(SP.g_total, st));
+  bool g_forked = false;
+  cudaStream_t sp = ahead ? ctx->aux[0] : st;
+  cudaEvent_t evH = ahead ? ctx->aux_ev[0] : nullptr, evP = ahead ? ctx->aux_ev[1] : nullptr;
   for (int64_t l = 0; l < h.nlevels; ++l) {
     const LevelPlan& P = sym->plan[l];
-    if (P.nlarge && P.max_nu_large > 0) {  // large fronts accumulate into their (reused) update blocks
-      const unsigned gx = (unsigned)std::min<int64_t>(256, (P.max_nu_large * P.max_nu_large + 1023) / 1024);
-      k_zero_cb<<<dim3(gx, (unsigned)P.nlarge), 256, 0, st>>>(S, sym->d_level_nodes.p + P.begin + P.nsmall, cbuf);
-      count_launch();
-    }
-    for (size_t r = 0; r + 1 < P.ea_round_begin.size(); ++r) {
-      int64_t cnt = P.ea_round_begin[r + 1] - P.ea_round_begin[r];
-      if (!cnt) continue;
-      dim3 g((unsigned)((P.ea_round_maxnu[r] + 31) / 32), (unsigned)cnt);
-      if (g.x == 0) continue;
-      k_extend_add<<<g, 256, 0, st>>>(S, sym->d_ea_items.p + P.ea_round_begin[r], F->panel.p, cbuf); count_launch();
-      RIGA_CUDA(cudaGetLastError());
-    }
+    auto extend_add = [&](int part) -> int {
+      for (size_t r = 0; r + 1 < P.ea_round_begin.size(); ++r) {
+        int64_t cnt = P.ea_round_begin[r + 1] - P.ea_round_begin[r];
+        if (!cnt) continue;
+        dim3 g((unsigned)((P.ea_round_maxnu[r] + 31) / 32), (unsigned)cnt);
+        if (g.x == 0) continue;
+        k_extend_add<<<g, 256, 0, st>>>(S, sym->d_ea_items.p + P.ea_round_begin[r], part, F->panel.p, cbuf);
+        count_launch();
+        RIGA_CUDA(cudaGetLastError());
+      }
+      return RIGA_OK;
+    };
+    RIGA_TRY(extend_add(0));  // children -> pivot columns of the large fronts
     for (size_t c = 0; c + 1 < P.cls_begin.size(); ++c) {
       int64_t cnt = P.cls_begin[c + 1] - P.cls_begin[c];
       if (!cnt) continue;
@@ -648,45 +676,88 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       RIGA_CUDA(cudaGetLastError());
     }
     if (P.nlarge) {
-      const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
-      const unsigned nl = (unsigned)P.nlarge;
-      auto trail = [&](int64_t k0, int64_t k1, int64_t c0, int64_t c1, bool wide) -> int {
-        // rows [c0', f) with c0' = min(c0, n_p) per front: tile counts bounded over the level's fronts
-        const int64_t rows = wide ? std::max(P.max_f_large - c0, P.max_nu_large) : P.max_f_large - c0;
-        const int64_t nti = (rows + kT128 - 1) / kT128;
-        if (nti <= 0) return RIGA_OK;
-        const int64_t ntj = wide ? nti : (c1 - c0 + kT128 - 1) / kT128;
-        const int64_t ntiles = wide ? nti * (nti + 1) / 2 : nti * ntj;
-        double work = 0.0;  // algorithmic flops: 2 K per updated lower entry, over the level's fronts
-        for (int64_t q = P.begin + P.nsmall; q < P.begin + P.nsmall + P.nlarge; ++q) {
+    const int32_t* ln = sym->d_level_nodes.p + P.begin + P.nsmall;
+    const unsigned nl = (unsigned)P.nlarge;
+    // trailing update of pivot columns [k0, k1): narrow = the pivot columns [c0, c1); wide = every
+    // column right of c0, update block included (first: the update block is written, not accumulated)
+    auto trail = [&](cudaStream_t ts, int64_t k0, int64_t k1, int64_t c0, int64_t c1, bool wide, bool first) -> int {
+      // rows [c0', f) with c0' = min(c0, n_p) per front: tile counts bounded over the level's fronts
+      const int64_t rows = wide ? std::max(P.max_f_large - c0, P.max_nu_large) : P.max_f_large - c0;
+      const int64_t nti = (rows + kT128 - 1) / kT128;
+      if (nti <= 0) return RIGA_OK;
+      const int64_t ntj = wide ? nti : (std::min(c1, P.max_np_large) - c0 + kT128 - 1) / kT128;
+      if (ntj <= 0) return RIGA_OK;
+      const int64_t ntiles = wide ? nti * (nti + 1) / 2 : nti * ntj;
+      double work = 0.0;  // algorithmic flops: 2 K per updated lower entry, over the level's fronts
+      for (int64_t q = P.begin + P.nsmall; q < P.begin + P.nsmall + P.nlarge; ++q) {
           const int64_t sn = h.level_nodes[q], f = h.front[sn], np = h.ncol[sn];
           const int64_t kend = std::min(k1, np), cs = std::min(c0, np), ce = wide ? f : std::min(c1, np);
           if (k0 >= kend || cs >= ce) continue;
-          work += 2.0 * (double)(kend - k0) * ((double)(ce - cs) * f - 0.5 * (double)(ce - 1 + cs) * (ce - cs));
-        }
-        ProfScope prof_t(kProfTrail, st, work);
-        k_trail128<<<dim3((unsigned)ntiles, nl), 256, kT128Smem, st>>>(S, ln, k0, k1, c0, c1, wide ? 1 : 0, (int)ntj,
-                                                                       wide ? 1 : 0, F->panel.p, cbuf, F->D.p);
-        count_launch();
+        work += 2.0 * (double)(kend - k0) * ((double)(ce - cs) * f - 0.5 * (double)(ce - 1 + cs) * (ce - cs));
+      }
+      ProfScope prof_t(kProfTrail, ts, work);
+      k_trail128<<<dim3((unsigned)ntiles, nl), 256, kT128Smem, ts>>>(S, ln, k0, k1, c0, c1, wide ? 1 : 0, (int)ntj,
+                                                                     wide ? 1 : 0, first ? 1 : 0, F->panel.p, cbuf,
+                                                                     F->D.p);
+      count_launch();
+      RIGA_CUDA(cudaGetLastError());
+      return RIGA_OK;
+    };
+    // panel chain of the outer block [kbo, kbo + nb2): per 128 columns the diagonal block, the rows
+    // below it, and the block's remaining columns (narrow, K = 128)
+    auto panel_block = [&](cudaStream_t ts, int64_t kbo) -> int {
+      const int64_t kend = std::min<int64_t>(kbo + g_nb2, P.max_np_large);
+      for (int64_t kb = kbo; kb < kend; kb += kDB) {
+        k_diag128<<<nl, 256, kDiag128Smem, ts>>>(S, ln, (int)kb, F->tol.p, F->panel.p, F->D.p, F->stat.p);
+        const unsigned nti = (unsigned)((P.max_f_large - kb + 31) / 32);
+        k_trsm128<<<dim3(nti, nl), 32, kTrsmSmem, ts>>>(S, ln, (int)kb, F->panel.p, F->D.p);
+        count_launch(2);
         RIGA_CUDA(cudaGetLastError());
-        return RIGA_OK;
-      };
+        if (kb + kDB < kend) RIGA_TRY(trail(ts, kb, kb + kDB, kb + kDB, kbo + g_nb2, false, false));
+      }
+      return RIGA_OK;
+    };
+    const bool la = ahead && P.max_np_large > g_nb2;
+    if (!la) {
       for (int64_t kbo = 0; kbo < P.max_np_large; kbo += g_nb2) {
-        const int64_t kend = std::min<int64_t>(kbo + g_nb2, P.max_np_large);
-        for (int64_t kb = kbo; kb < kend; kb += kDB) {
-          k_diag128<<<nl, 256, kDiag128Smem, st>>>(S, ln, (int)kb, F->tol.p, F->panel.p, F->D.p, F->stat.p);
-          const unsigned nti = (unsigned)((P.max_f_large - kb + 31) / 32);
-          k_trsm128<<<dim3(nti, nl), 32, kTrsmSmem, st>>>(S, ln, (int)kb, F->panel.p, F->D.p);
-          count_launch(2);
-          RIGA_CUDA(cudaGetLastError());
-          // the block's remaining columns take this 128-column slice now (narrow, K = 128)
-          if (kb + kDB < kend) RIGA_TRY(trail(kb, kb + kDB, kb + kDB, kbo + g_nb2, false));
+        RIGA_TRY(panel_block(st, kbo));
+        // everything right of the block -- pivot columns and update block -- in one K = nb2 slice
+        RIGA_TRY(trail(st, kbo, kbo + g_nb2, kbo + g_nb2, 0, true, kbo == 0));
+      }
+    } else {
+      // look-ahead: the next outer block's pivot columns take the K = nb2 slice first (head), then its
+      // panel chain runs on the high-priority side stream while the factor stream updates the rest
+      RIGA_CUDA(cudaEventRecord(evH, st));
+      RIGA_CUDA(cudaStreamWaitEvent(sp, evH, 0));
+      RIGA_TRY(panel_block(sp, 0));
+      RIGA_CUDA(cudaEventRecord(evP, sp));
+      for (int64_t kbo = 0; kbo < P.max_np_large; kbo += g_nb2) {
+        RIGA_CUDA(cudaStreamWaitEvent(st, evP, 0));
+        const bool more = kbo + g_nb2 < P.max_np_large;
+        if (more) {
+          RIGA_TRY(trail(st, kbo, kbo + g_nb2, kbo + g_nb2, kbo + 2 * g_nb2, false, false));
+          RIGA_CUDA(cudaEventRecord(evH, st));
+          RIGA_CUDA(cudaStreamWaitEvent(sp, evH, 0));
+          RIGA_TRY(panel_block(sp, kbo + g_nb2));
+          RIGA_CUDA(cudaEventRecord(evP, sp));
         }
-        // everything right of the block -- pivot columns and update block -- in one K = g_nb2 slice
-        RIGA_TRY(trail(kbo, kbo + g_nb2, kbo + g_nb2, 0, true));
+        RIGA_TRY(trail(st, kbo, kbo + g_nb2, kbo + (more ? 2 : 1) * g_nb2, 0, true, kbo == 0));
       }
     }
+    RIGA_TRY(extend_add(1));  // children -> update blocks, on top of the fronts' own Schur complements
+    }
+    if (ahead && l == g_top && l + 1 < h.nlevels) {
+      RIGA_CUDA(cudaEventRecord(ctx->aux_ev[2], st));
+      RIGA_CUDA(cudaStreamWaitEvent(ctx->aux[1], ctx->aux_ev[2], 0));
+      RIGA_TRY(build_small_g(F, ctx->aux[1]));
+      RIGA_CUDA(cudaEventRecord(ctx->aux_ev[3], ctx->aux[1]));
+      g_forked = true;
+    }
   }
+  if (g_forked)
+    RIGA_CUDA(cudaStreamWaitEvent(st, ctx->aux_ev[3], 0));
+  else if (g_top >= 0)
+    RIGA_TRY(build_small_g(F, st));
   if (cbuf) RIGA_CUDA(cudaFreeAsync(cbuf, st));
   RIGA_CUDA(cudaFreeAsync(scratch, st));
   return build_chain_inverse(F, st);

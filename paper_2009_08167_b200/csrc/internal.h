@@ -160,7 +160,9 @@ int factor_solve(riga_factor* f, cudaStream_t s, const double* b, double* x, boo
 int build_solve_plan(riga_symbolic* sym);
 int prepare_solve();
 int upload_solve_plan(riga_symbolic* sym, cudaStream_t s);
-int build_chain_inverse(riga_factor* F, cudaStream_t s);
+int build_chain_inverse(riga_factor* F, cudaStream_t s);  // inv(L11) of the chain supernodes + accuracy probe
+int build_small_g(riga_factor* F, cudaStream_t s);        // G blocks of the small supernodes
+int64_t small_g_top_level(const riga_symbolic* sym);
 int flag_inverse_refinement(riga_factor* F, cudaStream_t s);
 inline double __longlong_as_double_host(long long v) {
   double d;

@@ -1572,22 +1572,40 @@ static int set_solve_attrs() {
 
 int prepare_solve() { return set_solve_attrs(); }
 
+// G = [inv(L11); L21 inv(L11)] of every G-mode supernode; needs only those supernodes' finished panels, so
+// the factorization launches it on a side stream once their last tree level is done (gsmall must already
+// be allocated in an order the stream respects)
+int build_small_g(riga_factor* F, cudaStream_t st) {
+  riga_symbolic* sym = F->sym;
+  const SolvePlanHost& L = sym->sp;
+  SymDev S = sym->dev();
+  if (!(L.small_g && L.g_total)) return RIGA_OK;
+  const int nw = (int)L.wholes.size();
+  constexpr int smem = kGMaxNp * (kGMaxNp + 1) * 8;
+  static bool attr = false;
+  if (!attr) {
+    RIGA_CUDA(cudaFuncSetAttribute(k_small_g, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  k_small_g<<<nw, 256, smem, st>>>(S, sym->d_wholes.p, F->panel.p, sym->d_g_off.p, F->gsmall.p);
+  count_launch();
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
+// highest tree level holding a G-mode supernode (-1: none)
+int64_t small_g_top_level(const riga_symbolic* sym) {
+  const SolvePlanHost& L = sym->sp;
+  if (!(L.small_g && L.g_total)) return -1;
+  int64_t top = -1;
+  for (int32_t s : L.wholes) top = std::max<int64_t>(top, sym->h.level[s]);
+  return top;
+}
+
 int build_chain_inverse(riga_factor* F, cudaStream_t st) {
   riga_symbolic* sym = F->sym;
   const SolvePlanHost& L = sym->sp;
   SymDev S = sym->dev();
-  if (L.small_g && L.g_total) {
-    if (!F->gsmall.p) RIGA_TRY(F->gsmall.alloc(L.g_total, st));
-    const int nw = (int)L.wholes.size();
-    constexpr int smem = kGMaxNp * (kGMaxNp + 1) * 8;
-    static bool attr = false;
-    if (!attr) {
-      RIGA_CUDA(cudaFuncSetAttribute(k_small_g, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
-    k_small_g<<<nw, 256, smem, st>>>(S, sym->d_wholes.p, F->panel.p, sym->d_g_off.p, F->gsmall.p);
-    count_launch();
-  }
   if (!L.chain_inv || !L.inv_total) return RIGA_OK;
   if (!F->linv.p) RIGA_TRY(F->linv.alloc(L.inv_total, st));
   if (L.inv_fix && !F->rfix.p) RIGA_TRY(F->rfix.alloc(sym->h.n, st));

@@ -303,6 +303,13 @@ void ctx_release(riga_ctx* c) {
   if (c->refs.fetch_sub(1) != 1) return;
   DeviceGuard g(c->device);
   stream_sync(c->stream);  // this stream only: pending reads into scratch_host
+  for (auto& a : c->aux)
+    if (a) {
+      cudaStreamSynchronize(a);
+      cudaStreamDestroy(a);
+    }
+  for (auto& e : c->aux_ev)
+    if (e) cudaEventDestroy(e);
   if (c->scratch_dev) cudaFreeAsync(c->scratch_dev, c->stream);
   if (c->scratch_host) pinned_put(c->scratch_host);
   if (c->own_stream) cudaStreamDestroy(c->stream);  // released once its work drains

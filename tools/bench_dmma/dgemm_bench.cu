@@ -7,14 +7,6 @@
 
 using namespace riga;
 
-__global__ void __launch_bounds__(128) syrk_tiles(const double* A, int64_t lda, const double* D, int64_t k,
-                                                  double* C, int64_t n) {
-  const int64_t nt = (n + 63) / 64;
-  const int64_t ti = blockIdx.x / nt, tj = blockIdx.x % nt;
-  if (ti < tj) return;
-  dmma_syrk_tile(A, lda, D, 0, k, ti * 64, tj * 64, n, n, C, n, 0);
-}
-
 __global__ void __launch_bounds__(256, 1) syrk_tiles128(const double* A, int64_t lda, const double* D, int64_t k,
                                                         double* C, int64_t n) {
   extern __shared__ double sm[];
@@ -33,21 +25,10 @@ int main(int argc, char** argv) {
   cudaMemset(A, 0, n * k * 8);
   cudaMemset(C, 0, n * n * 8);
   cudaMemset(D, 0, k * 8);
-  const int64_t nt = (n + 63) / 64;
+  cudaFuncSetAttribute(syrk_tiles128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int rep = 0; rep < 3; ++rep) {
-    cudaEventRecord(e0);
-    syrk_tiles<<<(unsigned)(nt * nt), 128>>>(A, n, D, k, C, n);
-    cudaEventRecord(e1);
-    cudaEventSynchronize(e1);
-    float ms;
-    cudaEventElapsedTime(&ms, e0, e1);
-    const double flops = (double)n * (n + 64) * k;  // lower tiles incl. diagonal, 2 flops per mac / 2
-    if (rep) printf("syrk tile n=%lld k=%lld: %.3f ms  %.2f TFLOP/s\n", (long long)n, (long long)k, ms,
-                    flops / ms / 1e9);
-  }
   cudaFuncSetAttribute(syrk_tiles128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT128Smem);
   const int64_t nt2 = (n + 127) / 128;
   for (int rep = 0; rep < 3; ++rep) {

@@ -70,6 +70,18 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* out; cudaMalloc(&out, 4096 * sizeof(double));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  // warps per SM needed to saturate the DMMA pipe: one CTA per SM, 4..32 warps, 8 independent accumulators each
+  for (int warps = 4; warps <= 32; warps *= 2) {
+    int threads = warps * 32, iters = 20000;
+    float ms = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      dmma_loop<<<sms, threads>>>(out, iters);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+    }
+    printf("DMMA one CTA/SM, %d warps/SM: %.2f TFLOP/s\n", warps, 1.0 * sms * warps * iters * 8 * 512.0 / ms / 1e9);
+  }
   for (int warps = 4; warps <= 16; warps *= 2) {
     int threads = warps * 32; int iters = 20000;
     for (int rep = 0; rep < 2; ++rep) {
