@@ -83,26 +83,38 @@ __global__ void k_asm_large(SymDev S, const int32_t* __restrict__ nodes,
 // part 0 = the columns that land in the parent's pivot columns (before the
 // parent is factored), part 1 = the columns that land in the parent's update
 // block (after the parent's own Schur complement has been written there)
-__global__ void k_extend_add(SymDev S, const int32_t* __restrict__ items, int part,
-                             double* __restrict__ panel, double* __restrict__ cb) {
-  int c = items[blockIdx.y];
-  int p = S.sparent[c];
-  int64_t nuc = S.front[c] - S.ncol[c];
-  int64_t fp = S.front[p], npp = S.ncol[p], nup = fp - npp;
+constexpr int kEaRows = 1024;  // rows of a child column handled by one CTA (grid z = row chunks)
+__global__ void __launch_bounds__(256) k_extend_add(SymDev S, const int32_t* __restrict__ items, int part,
+                                                    double* __restrict__ panel, double* __restrict__ cb) {
+  const int c = items[blockIdx.y];
+  const int p = S.sparent[c];
+  const int64_t nuc = S.front[c] - S.ncol[c];
+  const int64_t b0 = (int64_t)blockIdx.x * 32;
+  const int64_t z0 = (int64_t)blockIdx.z * kEaRows, z1 = min(z0 + kEaRows, nuc);
+  if (b0 >= nuc || z1 <= b0) return;  // past the child's columns, or a chunk above the diagonal
+  const int64_t fp = S.front[p], npp = S.ncol[p], nup = fp - npp;
   const double* src = cb + S.cb_off[c];
-  const int32_t* rp = S.relpos + S.upd_off[c];
+  const int32_t* __restrict__ rp = S.relpos + S.upd_off[c];
   double* P = panel + S.panel_off[p];
   double* C = cb + S.cb_off[p];
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int64_t b0 = (int64_t)blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t b = b0 + w; b < min(b0 + 32, nuc); b += nw) {
-    int64_t rb = rp[b];
+    const int64_t rb = rp[b];
     if ((rb < npp) != (part == 0)) continue;
-    if (rb < npp) {
-      for (int64_t a = b + lane; a < nuc; a += 32) P[rb * fp + rp[a]] += src[b * nuc + a];
-    } else {
-      for (int64_t a = b + lane; a < nuc; a += 32) C[(rb - npp) * nup + (rp[a] - npp)] += src[b * nuc + a];
+    // destination column: entry (ra, rb) of the parent front
+    double* dst = rb < npp ? P + rb * fp : C + (rb - npp) * nup - npp;
+    const double* sc = src + b * nuc;
+    int64_t a = max(b, z0) + lane;
+    for (; a + 96 < z1; a += 128) {  // four independent read-modify-writes in flight per lane
+      const int32_t r0 = rp[a], r1 = rp[a + 32], r2 = rp[a + 64], r3 = rp[a + 96];
+      const double v0 = sc[a], v1 = sc[a + 32], v2 = sc[a + 64], v3 = sc[a + 96];
+      const double d0 = dst[r0], d1 = dst[r1], d2 = dst[r2], d3 = dst[r3];
+      dst[r0] = d0 + v0;
+      dst[r1] = d1 + v1;
+      dst[r2] = d2 + v2;
+      dst[r3] = d3 + v3;
     }
+    for (; a < z1; a += 32) dst[rp[a]] += sc[a];
   }
 }
 
@@ -244,10 +256,12 @@ template <int K>
 __device__ __forceinline__ void ldl32_step(double (&a)[32], int lane, double& dl) {
   const double dk = __shfl_sync(0xffffffffu, a[K], K);
   const double lk = a[K] * (1.0 / dk);
+  // every lane updates its whole row: the entries right of the diagonal (lane < j) hold garbage that no
+  // later step reads and the write-back skips, so the update needs no per-element predicate
 #pragma unroll
   for (int j = K + 1; j < 32; ++j) {
     const double ajk = __shfl_sync(0xffffffffu, a[K], j);  // A(j, K), not yet scaled
-    if (lane >= j) a[j] = fma(-lk, ajk, a[j]);
+    a[j] = fma(-lk, ajk, a[j]);
   }
   if (lane == K) dl = dk;
   if (lane > K) a[K] = lk;
@@ -307,12 +321,12 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
   double* P = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;  // (r, c) of the block at P[c f + r]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // stage the block with cp.async (every load in flight at once; padding rows/columns: zero fill,
-  // identity pivots written after the wait)
-  for (int idx = tid; idx < nbp * nbp; idx += blockDim.x) {
-    const int c = idx / nbp, r = idx - c * nbp;
-    const bool in = r >= c && r < nb && c < nb;
-    if (r >= c) cp_async8(A + c * kDBP + r, in ? P + (int64_t)c * f + r : P, in);
-  }
+  // identity pivots written after the wait); warp per column, lanes along the rows
+  for (int c = warp; c < nbp; c += 8)
+    for (int r = (c & ~31) + lane; r < nbp; r += 32) {
+      const bool in = r >= c && r < nb && c < nb;
+      if (r >= c) cp_async8(A + c * kDBP + r, in ? P + (int64_t)c * f + r : P, in);
+    }
   cp_async_commit();
   cp_async_wait<0>();
   for (int c = nb + tid; c < nbp; c += blockDim.x) A[c * kDBP + c] = 1.0;
@@ -366,10 +380,9 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
     if (neg) atomicAdd((unsigned long long*)&stat[0], (unsigned long long)neg);
     if (bad != INT64_MAX) atomicMin((long long*)&stat[1], (long long)bad);
   }
-  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {  // L11, d on the diagonal
-    const int c = idx / nb, r = idx - c * nb;
-    if (r >= c) P[(int64_t)c * f + r] = A[c * kDBP + r];
-  }
+  for (int c = warp; c < nb; c += 8)  // L11, d on the diagonal
+    for (int r = (c & ~31) + lane; r < nb; r += 32)
+      if (r >= c) P[(int64_t)c * f + r] = A[c * kDBP + r];
 }
 
 // L21 = A21 L11^{-T} D^{-1} for the rows below the block, by blocked substitution: one warp (CTA) per 32
@@ -656,7 +669,8 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       for (size_t r = 0; r + 1 < P.ea_round_begin.size(); ++r) {
         int64_t cnt = P.ea_round_begin[r + 1] - P.ea_round_begin[r];
         if (!cnt) continue;
-        dim3 g((unsigned)((P.ea_round_maxnu[r] + 31) / 32), (unsigned)cnt);
+        dim3 g((unsigned)((P.ea_round_maxnu[r] + 31) / 32), (unsigned)cnt,
+               (unsigned)((P.ea_round_maxnu[r] + kEaRows - 1) / kEaRows));
         if (g.x == 0) continue;
         k_extend_add<<<g, 256, 0, st>>>(S, sym->d_ea_items.p + P.ea_round_begin[r], part, F->panel.p, cbuf);
         count_launch();
