@@ -389,7 +389,8 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
 // rows, its rows x nb columns staged in shared memory (W); per 32-column step b the L11 row strip
 // L(b rows, 0 : b + 32) is staged, T = A_b - sum_{t<b} W_t D_t L_bt^T runs on DMMA, then W_b = T L_bb^{-T}
 // D_b^{-1} row by row (lane = row).
-constexpr size_t kTrsmSmem = (2 * (size_t)kDB * 33 + 2 * kDB) * sizeof(double);
+constexpr int kTrsmP = 36;  // pitch == 4 mod 16: conflict-free DMMA fragment loads (33 was 3-way)
+constexpr size_t kTrsmSmem = (2 * (size_t)kDB * kTrsmP + 2 * kDB) * sizeof(double);
 __global__ void __launch_bounds__(32) k_trsm128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
                                                 double* __restrict__ panel, const double* __restrict__ D) {
   extern __shared__ double sm[];
@@ -403,15 +404,15 @@ __global__ void __launch_bounds__(32) k_trsm128(SymDev S, const int32_t* __restr
   const int lane = threadIdx.x;
   const int nr = (int)imin(32, f - r0);
   const int64_t col0 = S.col0[s];
-  double* W = sm;               // W[c * 33 + row]
-  double* Ls = W + kDB * 33;    // strip: L(kb + j, t) at Ls[t * 33 + j]
-  double* ds = Ls + kDB * 33;   // pivots
+  double* W = sm;               // W[c * kTrsmP + row]
+  double* Ls = W + kDB * kTrsmP;    // strip: L(kb + j, t) at Ls[t * kTrsmP + j]
+  double* ds = Ls + kDB * kTrsmP;   // pivots
   double* rds = ds + kDB;       // their reciprocals
   const double* Lb = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;  // L11(r, c) at Lb[c f + r]
   double* Pr = panel + S.panel_off[s] + (int64_t)kbo * f + r0;         // A21(row, c) at Pr[c f + row]
   for (int c = 0; c < nbp; ++c) {
     const bool in = c < nb && lane < nr;
-    cp_async8(W + c * 33 + lane, in ? Pr + (int64_t)c * f + lane : Lb, in);
+    cp_async8(W + c * kTrsmP + lane, in ? Pr + (int64_t)c * f + lane : Lb, in);
   }
   cp_async_commit();
   for (int c = lane; c < nbp; c += 32) {
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(32) k_trsm128(SymDev S, const int32_t* __restr
     const bool rowin = kb + lane < nb;
     for (int t = 0; t < kb + 32; ++t) {
       const bool in = rowin && t < nb;
-      cp_async8(Ls + t * 33 + lane, in ? Lb + (int64_t)t * f + kb + lane : Lb, in);
+      cp_async8(Ls + t * kTrsmP + lane, in ? Lb + (int64_t)t * f + kb + lane : Lb, in);
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -431,22 +432,22 @@ __global__ void __launch_bounds__(32) k_trsm128(SymDev S, const int32_t* __restr
     if (kb > 0) {  // W_b -= sum_{t < b} W_t D_t L_bt^T
       double acc[4][4][2];
       zero_acc(acc);
-      warp_mma32(acc, [&](int i, int k) { return W[k * 33 + i] * ds[k]; }, [&](int k, int j) { return Ls[k * 33 + j]; },
+      warp_mma32(acc, [&](int i, int k) { return W[k * kTrsmP + i] * ds[k]; }, [&](int k, int j) { return Ls[k * kTrsmP + j]; },
                  kb);
-      RIGA_ACC_FOR(W[(kb + aj) * 33 + ai] -= acc[m][q][e];)
+      RIGA_ACC_FOR(W[(kb + aj) * kTrsmP + ai] -= acc[m][q][e];)
       __syncwarp();
     }
     double w[32];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) w[c] = W[(kb + c) * 33 + lane];
-    sub32_all(w, [&](int c, int t) { return Ls[(kb + t) * 33 + c]; }, [&](int c) { return rds[kb + c]; },
+    for (int c = 0; c < 32; ++c) w[c] = W[(kb + c) * kTrsmP + lane];
+    sub32_all(w, [&](int c, int t) { return Ls[(kb + t) * kTrsmP + c]; }, [&](int c) { return rds[kb + c]; },
               std::make_integer_sequence<int, 32>{});
 #pragma unroll
-    for (int c = 0; c < 32; ++c) W[(kb + c) * 33 + lane] = w[c];
+    for (int c = 0; c < 32; ++c) W[(kb + c) * kTrsmP + lane] = w[c];
     __syncwarp();
   }
   for (int c = 0; c < nb; ++c)
-    if (lane < nr) Pr[(int64_t)c * f + lane] = W[c * 33 + lane];
+    if (lane < nr) Pr[(int64_t)c * f + lane] = W[c * kTrsmP + lane];
 }
 
 // Trailing update of a front over its pivot columns [k0, min(k1, n_p)), lower triangle, rows to f.
