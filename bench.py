@@ -345,7 +345,8 @@ def ldlt_rate(P, D, cfgname, flush, reps=3):
     upd = {"ms": float(pm[6]), "flops": float(pw[6]), "launches": int(pc[6]),
            "achieved": float(pw[6]) / (pm[6] / 1e3) / 1e12 if pm[6] > 0 else 0.0, "unit": "TFLOP/s",
            "share_of_factor_flops": float(pw[6]) / flops,
-           "how": "CUDA events around every k_trail128 launch of one factorization (prof scopes on), "
+           "how": "CUDA events around every k_trail128 launch of one factorization (prof scopes on: the "
+                  "factorization then runs on one stream, no look-ahead, so each scope times its kernel alone), "
                   "algorithmic flops of the lower-triangle updates"}
     upd["frac"] = upd["achieved"] / MEASURED_FP64_TFLOPS
     out = {"config": cfgname, "N": s.dof_count, "ms": fm, "flops_per_launch": flops, "achieved": tf,

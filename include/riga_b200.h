@@ -303,6 +303,32 @@ int riga_prof_reset(void);
 int riga_residuals(riga_ctx* ctx, riga_system* sys, const double* X_dev, int64_t ldx, int64_t nvec,
                    const double* lam_host, double* out_host);
 
+/* ---- tensor-product evaluation of the eigen-error study (verify.py) -------
+ * riga_tp_contract replaces one direction of ErrorEvaluator._contract (ref
+ * verify.py:218-225): in is an (outer, n_in, inner) row-major tensor,
+ *   out[o, q, i] = s[o / outer_per_batch] * sum_{j < p1} vals[q p1 + j] * in[o, first[q] + j - off, i]
+ * with rows outside [0, n_in) read as zero (off = 1 embeds the reduced
+ * coefficient tensor between its Dirichlet layers, ref :136-148);
+ * bscale_dev may be NULL.  A collocation matrix has p1 = p + 1 non-zeros per
+ * quadrature point (first[q] = its first basis index), so the contraction is
+ * a banded gather, HBM-bound.
+ * riga_tp_reduce replaces ErrorEvaluator.integrate of (u_h - u)^2 (mode 0) or
+ * u_h u (mode 1) or of the grid itself (mode 2) (ref :227-255) for nbatch grids G (nbatch, q_z, q_y, q_x)
+ * against the exact modes u = prod_t sqrt(2) sin(k_t pi x_t) (ref :105-133;
+ * direction `deriv` >= 0: that factor's derivative), formed on the fly from
+ * kidx_dev[b dim + t]; nq_host, x_dev, w_dev: points and weights per
+ * direction (x first); gsign_dev (may be NULL) multiplies G in mode 0;
+ * out_dev[nbatch].  Fixed-order reductions.
+ * riga_row_dots: out[v] = X[v, :] . Y[v, :] (the c^T M c normalisations).   */
+int riga_tp_contract(riga_ctx* ctx, const double* in_dev, double* out_dev, int64_t outer, int64_t n_in,
+                     int64_t n_out, int64_t inner, int p1, int off, const int32_t* first_dev,
+                     const double* vals_dev, const double* bscale_dev, int64_t outer_per_batch);
+int riga_tp_reduce(riga_ctx* ctx, const double* G_dev, int64_t nbatch, int dim, const int64_t* nq_host,
+                   const double* const* x_dev, const double* const* w_dev, const int32_t* kidx_dev, int deriv,
+                   int mode, const double* gsign_dev, double* out_dev);
+int riga_row_dots(riga_ctx* ctx, const double* X_dev, int64_t ldx, const double* Y_dev, int64_t ldy, int64_t n,
+                  int64_t nvec, double* out_dev);
+
 /* ---- dense vector helpers on the device (stream of ctx) ----------------- */
 int riga_dot(riga_ctx* ctx, int64_t n, const double* x_dev, const double* y_dev, double* out_host);
 

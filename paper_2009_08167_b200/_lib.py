@@ -86,6 +86,9 @@ SIGNATURES = {
     "riga_lanczos_bytes": [_p, _p],
     "riga_residuals": [_p, _p, _p, _i64, _i64, _p, _p],
     "riga_dot": [_p, _i64, _p, _p, _p],
+    "riga_tp_contract": [_p, _p, _p, _i64, _i64, _i64, _i64, _i32, _i32, _p, _p, _p, _i64],
+    "riga_tp_reduce": [_p, _p, _i64, _i32, _p, _p, _p, _p, _i32, _i32, _p, _p],
+    "riga_row_dots": [_p, _p, _i64, _p, _i64, _i64, _i64, _p],
     "riga_launch_count": [_p],
     "riga_set_pdl": [_i32],
     "riga_set_solve_sub_levels": [_i32],

@@ -653,7 +653,8 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   // does any level have more than one outer block?  then the panel chain runs ahead on aux[0]
   bool ahead = false;
   for (int64_t l = 0; l < h.nlevels; ++l) ahead = ahead || (sym->plan[l].nlarge && sym->plan[l].max_np_large > g_nb2);
-  ahead = ahead && g_lookahead;
+  // with the per-kernel timing scopes on, everything stays on one stream so a scope times its kernel alone
+  ahead = ahead && g_lookahead && !prof_on();
   riga_ctx* ctx = F->ctx;
   if (ahead) RIGA_TRY(ctx_aux(ctx));
   // G blocks of the small supernodes: on the low-priority side stream as soon as their last level is

@@ -38,6 +38,11 @@ cudaEvent_t get_event() {
 }
 }  // namespace
 
+bool prof_on() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return g_on;
+}
+
 ProfScope::ProfScope(int c, cudaStream_t st, double w) : cat(c), s(st), work(w) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_on) return;

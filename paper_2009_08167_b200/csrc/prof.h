@@ -29,6 +29,8 @@ inline void count_launch(int n = 1) {
   t_launches += n;
 }
 
+bool prof_on();  // per-category timing enabled (riga_prof_enable)
+
 struct ProfScope {
   int cat;
   cudaStream_t s;

@@ -11,16 +11,20 @@ after sorting (ref :1-17), and
     EFE = EV + EFL
 
 Device side: ``error_table`` evaluates every eigenfunction error of a solve
-at once -- the coefficient tensors of all unique-eigenfunction modes are
-contracted with the per-direction collocation matrices as batched FP64
-GEMMs on the GPU (tensor-product evaluation, ref ErrorEvaluator._contract
-:218-225), the M-normalisations use the engine's mass product, and the
-quadrature sums are batched reductions; the reference loops over modes on
-the host.  The per-mode methods of ``ErrorEvaluator`` are kept for API
-parity and run the same contractions on one mode.
+at once with engine kernels (csrc/verify.cu): the coefficient tensors of all
+unique-eigenfunction modes go through one banded tensor-product contraction
+per direction (``riga_tp_contract``; ref ErrorEvaluator._contract :218-225 --
+a collocation matrix has p + 1 non-zeros per point, so this is HBM-bound
+gather work, not a GEMM), the M-normalisations use the engine's batched mass
+product and row dots, and the quadrature sums against the exact modes, formed
+on the fly, are fixed-order reductions (``riga_tp_reduce``); the reference
+loops over modes on the host.  The per-mode methods of ``ErrorEvaluator`` are
+kept for API parity and run the same kernels on one mode.  There is no host
+path: without a CUDA device the evaluator raises.
 """
 from __future__ import annotations
 
+import ctypes
 import itertools
 import math
 from dataclasses import dataclass
@@ -28,6 +32,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _lib
 from .assembly import DiscreteSystem, gauss_points
 from .bspline import element_spans, eval_basis, eval_basis_span
 
@@ -148,15 +153,20 @@ def evaluate_eigenfunction(system: DiscreteSystem, coeffs, points) -> np.ndarray
 
 class ErrorEvaluator:
     """Per-direction Gauss rules (degree + 2 points per element by default)
-    and dense collocation matrices, built once (ref :181-216); contractions
-    on the device."""
+    and collocation tables, built once on the host (ref :181-216) and kept on
+    the device in banded form: a quadrature point sees p + 1 basis functions,
+    so each direction is ``first`` (their first index) and a (points, p + 1)
+    value table.  Every contraction and quadrature sum is an engine kernel
+    (``riga_tp_contract`` / ``riga_tp_reduce``); there is no host path."""
 
-    def __init__(self, system: DiscreteSystem, n_quad: int | None = None, device=None):
+    def __init__(self, system: DiscreteSystem, n_quad: int | None = None, ctx=None):
+        from . import device as _dev
+
         self.system = system
         self.dim = system.dim
-        self.device = torch.device(device if device is not None else
-                                   ("cuda" if torch.cuda.is_available() else "cpu"))
-        self.axes, self.weights, self.bval, self.bder = [], [], [], []
+        self.ctx = ctx or _dev.current()
+        self.device = torch.device(f"cuda:{self.ctx.device}")
+        self.axes, self.weights, self.first, self.vals, self.ders = [], [], [], [], []
         for space in system.spaces:
             nq = (space.degree + 2) if n_quad is None else n_quad
             pts, wts, rows_v, rows_d, firsts = [], [], [], [], []
@@ -168,91 +178,98 @@ class ErrorEvaluator:
                 rows_v.append(v)
                 rows_d.append(dv)
                 firsts.append(np.full(nq, mu - space.degree))
-            pts = np.concatenate(pts)
-            p1 = space.degree + 1
-            bv = np.zeros((pts.size, space.basis_count))
-            bd = np.zeros_like(bv)
-            f0 = np.concatenate(firsts)
-            rv, rd = np.concatenate(rows_v), np.concatenate(rows_d)
-            rr = np.repeat(np.arange(pts.size), p1)
-            cc = (f0[:, None] + np.arange(p1)[None, :]).ravel()
-            bv[rr, cc] = rv.ravel()
-            bd[rr, cc] = rd.ravel()
-            self.axes.append(pts)
+            self.axes.append(np.concatenate(pts))
             self.weights.append(np.concatenate(wts))
-            self.bval.append(bv)
-            self.bder.append(bd)
-        dev = self.device
-        self._bval = [torch.as_tensor(b, device=dev) for b in self.bval]
-        self._bder = [torch.as_tensor(b, device=dev) for b in self.bder]
-        self._w = [torch.as_tensor(w, device=dev) for w in self.weights]
-        self._ax = [torch.as_tensor(a, device=dev) for a in self.axes]
+            self.first.append(np.concatenate(firsts).astype(np.int32))
+            self.vals.append(np.ascontiguousarray(np.concatenate(rows_v)))
+            self.ders.append(np.ascontiguousarray(np.concatenate(rows_d)))
+        up = lambda a: _dev.to_device(a, self.ctx)  # noqa: E731
+        with torch.cuda.stream(self.ctx.stream):
+            self._first = [torch.from_numpy(f).to(self.device) for f in self.first]
+        self._vals = [up(v) for v in self.vals]
+        self._ders = [up(v) for v in self.ders]
+        self._w = [up(w) for w in self.weights]
+        self._ax = [up(a) for a in self.axes]
+        self._nq = np.array([a.size for a in self.axes], dtype=np.int64)
+        self._red = [s.basis_count - 2 for s in system.spaces]  # x first
+        PP = ctypes.c_void_p * self.dim
+        self._axp = PP(*[a.data_ptr() for a in self._ax])
+        self._wp = PP(*[w.data_ptr() for w in self._w])
 
     # -- batched device kernels (leading batch axis) ---------------------
-    def _contract_b(self, U: torch.Tensor, mats) -> torch.Tensor:
-        """U (B, n_z, n_y, n_x) -> values on the quadrature grid (B, q_z, q_y, q_x)."""
-        out = U
-        for t in range(self.dim):  # x is the last axis
-            ax = out.dim() - 1 - t
-            out = torch.movedim(torch.movedim(out, ax, -1) @ mats[t].T, -1, ax)
-        return out
+    def _contract_b(self, C: torch.Tensor, deriv: int | None = None, scale: torch.Tensor | None = None):
+        """Reduced coefficient rows C (B, dof_count) -> values of u_h (or its partial derivative along
+        ``deriv``) on the quadrature grid, (B, q_z, q_y, q_x); rows optionally scaled by ``scale`` (B,)."""
+        if C.dim() != 2 or C.shape[1] != self.system.dof_count:
+            raise ValueError(f"coefficient block has shape {tuple(C.shape)}, expected (B, {self.system.dof_count})")
+        L = _lib.lib()
+        B = C.shape[0]
+        cur = C if (C.is_contiguous() and C.dtype == torch.float64) else C.to(torch.float64).contiguous()
+        shape = [B] + list(reversed(self._red))  # (B, n_z, n_y, n_x)
+        with torch.cuda.stream(self.ctx.stream):
+            for t in range(self.dim):  # x (the last axis) first
+                ax = len(shape) - 1 - t
+                outer = int(np.prod(shape[:ax]))
+                inner = int(np.prod(shape[ax + 1:]))
+                tab = self._ders[t] if t == deriv else self._vals[t]
+                p1 = tab.shape[1]
+                out = torch.empty(outer * int(self._nq[t]) * inner, dtype=torch.float64, device=self.device)
+                sc = scale if (t == 0 and scale is not None) else None
+                _lib.check(L.riga_tp_contract(self.ctx.handle, _lib.ptr(cur), _lib.ptr(out), outer, shape[ax],
+                                              int(self._nq[t]), inner, p1, 1, _lib.ptr(self._first[t]),
+                                              _lib.ptr(tab), _lib.ptr(sc), outer // B), "tp_contract")
+                shape[ax] = int(self._nq[t])
+                cur = out
+        return cur.reshape(shape)
 
-    def _integrate_b(self, G: torch.Tensor) -> torch.Tensor:
-        out = G
-        for t in range(self.dim):
-            out = out @ self._w[t]  # contracts the current last axis (x, then y, then z)
+    def _reduce_b(self, G: torch.Tensor, modes, kind: int, deriv: int | None = None,
+                  gsign: torch.Tensor | None = None) -> torch.Tensor:
+        """Quadrature sums over the grid per batch member: kind 0 = (g G - u)^2, 1 = G u, 2 = G, with
+        u the exact mode (or its partial derivative along ``deriv``) formed on the device."""
+        B = G.shape[0]
+        G = G if G.is_contiguous() else G.contiguous()
+        ks = np.ascontiguousarray([m.indices for m in modes] if modes else np.ones((B, self.dim)), dtype=np.int32)
+        with torch.cuda.stream(self.ctx.stream):
+            kd = torch.from_numpy(ks).to(self.device)
+            out = torch.empty(B, dtype=torch.float64, device=self.device)
+        _lib.check(_lib.lib().riga_tp_reduce(self.ctx.handle, _lib.ptr(G), B, self.dim, _lib.ptr(self._nq),
+                                             self._axp, self._wp, _lib.ptr(kd), -1 if deriv is None else deriv,
+                                             kind, _lib.ptr(gsign), _lib.ptr(out)), "tp_reduce")
         return out
-
-    def _exact_b(self, modes, deriv: int | None = None) -> torch.Tensor:
-        ks = torch.as_tensor([m.indices for m in modes], dtype=torch.float64, device=self.device)
-        out = None
-        for t in reversed(range(self.dim)):  # z ... x: x fastest
-            arg = math.pi * ks[:, t:t + 1] * self._ax[t][None, :]
-            f = math.sqrt(2.0) * (ks[:, t:t + 1] * math.pi * torch.cos(arg) if t == deriv else torch.sin(arg))
-            out = f if out is None else out[..., None] * f.reshape(f.shape[0], *([1] * (out.dim() - 1)), f.shape[1])
-        return out
-
-    def _embed_b(self, C: torch.Tensor) -> torch.Tensor:
-        red = [s.basis_count - 2 for s in reversed(self.system.spaces)]
-        full = [s.basis_count for s in reversed(self.system.spaces)]
-        U = torch.zeros((C.shape[0], *full), dtype=torch.float64, device=self.device)
-        U[(slice(None),) + tuple(slice(1, n - 1) for n in full)] = C.reshape(C.shape[0], *red)
-        return U
 
     # -- per-mode API (ref :218-255) ---------------------------------------
     def _one(self, coeffs) -> torch.Tensor:
-        c = torch.as_tensor(np.asarray(coeffs, dtype=np.float64), device=self.device)
+        from . import device as _dev
+
+        c = np.asarray(coeffs, dtype=np.float64)
         if c.shape != (self.system.dof_count,):
             raise ValueError(f"coefficient vector has shape {tuple(c.shape)}, expected ({self.system.dof_count},)")
-        return self._embed_b(c[None])
+        return _dev.to_device(c, self.ctx)[None]
 
     def uh_values(self, coeffs) -> np.ndarray:
-        return self._contract_b(self._one(coeffs), self._bval)[0].cpu().numpy()
+        return self._contract_b(self._one(coeffs))[0].cpu().numpy()
 
     def uh_deriv(self, coeffs, t: int) -> np.ndarray:
-        mats = [self._bder[s] if s == t else self._bval[s] for s in range(self.dim)]
-        return self._contract_b(self._one(coeffs), mats)[0].cpu().numpy()
+        return self._contract_b(self._one(coeffs), deriv=t)[0].cpu().numpy()
 
     def integrate(self, grid) -> float:
-        g = torch.as_tensor(np.asarray(grid, dtype=np.float64), device=self.device)
-        return float(self._integrate_b(g[None])[0])
+        from . import device as _dev
+
+        g = _dev.to_device(np.asarray(grid, dtype=np.float64), self.ctx)
+        if tuple(g.shape) != tuple(int(n) for n in reversed(self._nq)):
+            raise ValueError(f"grid has shape {tuple(g.shape)}, expected {tuple(reversed(self._nq.tolist()))}")
+        return float(self._reduce_b(g[None], None, 2)[0])
 
     def l2_error_sq(self, coeffs, mode: ExactMode) -> float:
-        diff = self._contract_b(self._one(coeffs), self._bval) - self._exact_b([mode])
-        return float(self._integrate_b(diff * diff)[0])
+        return float(self._reduce_b(self._contract_b(self._one(coeffs)), [mode], 0)[0])
 
     def energy_error_sq(self, coeffs, mode: ExactMode) -> float:
-        U = self._one(coeffs)
-        tot = 0.0
-        for t in range(self.dim):
-            mats = [self._bder[s] if s == t else self._bval[s] for s in range(self.dim)]
-            diff = self._contract_b(U, mats) - self._exact_b([mode], deriv=t)
-            tot += float(self._integrate_b(diff * diff)[0])
-        return tot
+        C = self._one(coeffs)
+        return sum(float(self._reduce_b(self._contract_b(C, deriv=t), [mode], 0, deriv=t)[0])
+                   for t in range(self.dim))
 
     def inner_with_exact(self, coeffs, mode: ExactMode) -> float:
-        G = self._contract_b(self._one(coeffs), self._bval)
-        return float(self._integrate_b(G * self._exact_b([mode]))[0])
+        return float(self._reduce_b(self._contract_b(self._one(coeffs)), [mode], 1)[0])
 
 
 @dataclass
@@ -277,35 +294,41 @@ class ErrorRecord:
     diagonal: bool
 
 
-def _mass_norms(system: DiscreteSystem, C: torch.Tensor) -> torch.Tensor:
-    """sqrt(c^T M c) of each row of C (device mass product per vector)."""
-    from .sparsela import mass_matvec
+def _mass_norms(system: DiscreteSystem, C: torch.Tensor, ctx) -> torch.Tensor:
+    """sqrt(c^T M c) of each row of the device block C: batched engine mass product + row dots."""
+    from .sparsela import spmv_many
 
-    out = torch.empty(C.shape[0], dtype=torch.float64, device=C.device)
-    for i in range(C.shape[0]):
-        mc = mass_matvec(system.M, C[i])
-        mc = torch.as_tensor(mc, device=C.device) if not isinstance(mc, torch.Tensor) else mc
-        out[i] = torch.dot(C[i], mc)
-    return torch.sqrt(torch.clamp(out, min=0.0))
+    MC = spmv_many(system, 1, C, ctx=ctx)
+    with torch.cuda.stream(ctx.stream):
+        out = torch.empty(C.shape[0], dtype=torch.float64, device=C.device)
+    _lib.check(_lib.lib().riga_row_dots(ctx.handle, _lib.ptr(C), C.stride(0), _lib.ptr(MC), MC.stride(0), C.shape[1],
+                                        C.shape[0], _lib.ptr(out)), "row_dots")
+    with torch.cuda.stream(ctx.stream):
+        return torch.sqrt(torch.clamp(out, min=0.0))
 
 
 def _aligned_batch(lams, vectors, modes, system, evaluator):
-    """Positional match; unique-eigenfunction modes M-normalised and signed
-    to a nonnegative inner product with the exact mode, all at once."""
+    """Positional match; unique-eigenfunction modes M-normalised and signed to a nonnegative inner
+    product with the exact mode, all at once (ref :279-313).  Returns the raw coefficient rows C,
+    their scale (sign / M-norm) and the grid values G of the M-normalised, unsigned functions."""
     n = min(lams.size, len(modes))
     uniq = [i for i in range(n) if modes[i].unique_eigenfunction]
-    C = None
+    C = scale = G = None
     if uniq:
-        V = vectors if isinstance(vectors, torch.Tensor) else torch.as_tensor(np.asarray(vectors, dtype=np.float64))
-        C = V[:, uniq].T.to(device=evaluator.device, dtype=torch.float64).contiguous()
-        nrm = _mass_norms(system, C) if evaluator.device.type == "cuda" else torch.as_tensor(
-            [math.sqrt(max(float(c @ (system.M.csr @ c)), 0.0)) for c in C.cpu().numpy()])
-        C = C / torch.where(nrm > 0, nrm, torch.ones_like(nrm))[:, None].to(C.device)
-        G = evaluator._contract_b(evaluator._embed_b(C), evaluator._bval)
-        E = evaluator._exact_b([modes[i] for i in uniq])
-        sgn = torch.where(evaluator._integrate_b(G * E) < 0, -1.0, 1.0)
-        C = C * sgn[:, None]
-    return n, uniq, C
+        from . import device as _dev
+
+        ctx = evaluator.ctx
+        V = vectors if isinstance(vectors, torch.Tensor) else np.asarray(vectors, dtype=np.float64)
+        C = _dev.to_device(np.ascontiguousarray(V[:, uniq].T) if not isinstance(V, torch.Tensor) else V[:, uniq].T, ctx)
+        nrm = _mass_norms(system, C, ctx)
+        with torch.cuda.stream(ctx.stream):
+            inv = 1.0 / torch.where(nrm > 0, nrm, torch.ones_like(nrm))
+        G = evaluator._contract_b(C, scale=inv)
+        inner = evaluator._reduce_b(G, [modes[i] for i in uniq], 1)
+        with torch.cuda.stream(ctx.stream):
+            sgn = torch.where(inner < 0, -1.0, 1.0).to(torch.float64)
+            scale = inv * sgn
+    return n, uniq, C, scale, G
 
 
 def match_and_normalize(eigenvalues, vectors, modes, system: DiscreteSystem,
@@ -315,8 +338,8 @@ def match_and_normalize(eigenvalues, vectors, modes, system: DiscreteSystem,
     n = min(lams.size, len(modes))
     if evaluator is None and any(modes[i].unique_eigenfunction for i in range(n)):
         evaluator = ErrorEvaluator(system)
-    n, uniq, C = _aligned_batch(lams, vectors, modes, system, evaluator) if evaluator else (n, [], None)
-    Ch = C.cpu().numpy() if C is not None else None
+    n, uniq, C, scale, _ = _aligned_batch(lams, vectors, modes, system, evaluator) if evaluator else (n, [], None, None, None)
+    Ch = (C * scale[:, None]).cpu().numpy() if C is not None else None
     where = {i: q for q, i in enumerate(uniq)}
     return [AlignedMode(modes[i], i, float(lams[i]), Ch[where[i]] if i in where else None) for i in range(n)]
 
@@ -336,15 +359,18 @@ def error_metrics(aligned: AlignedMode, system: DiscreteSystem,
 
 def error_table(result_eigenvalues, result_vectors, system: DiscreteSystem) -> list:
     """Error records of a whole solve against the exact spectrum (ref
-    :332-338); every EFL of the solve in one batched device evaluation."""
+    :332-338); every EFL of the solve in one batched device evaluation: one
+    tensor-product contraction of all unique-eigenfunction modes, the sign
+    and the squared L2 error from the same grid values."""
     lams = np.asarray(result_eigenvalues, dtype=np.float64)
     modes = exact_spectrum(system.dim, count=lams.size)
     ev = ErrorEvaluator(system)
-    n, uniq, C = _aligned_batch(lams, result_vectors, modes, system, ev)
+    n, uniq, C, scale, G = _aligned_batch(lams, result_vectors, modes, system, ev)
     efl = {}
     if uniq:
-        diff = ev._contract_b(ev._embed_b(C), ev._bval) - ev._exact_b([modes[i] for i in uniq])
-        vals = ev._integrate_b(diff * diff).cpu().numpy()
+        with torch.cuda.stream(ev.ctx.stream):
+            sgn = torch.sign(scale)
+        vals = ev._reduce_b(G, [modes[i] for i in uniq], 0, gsign=sgn).cpu().numpy()
         efl = {i: float(v) for i, v in zip(uniq, vals)}
     out = []
     for i in range(n):

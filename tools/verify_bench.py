@@ -1,6 +1,6 @@
 """EV/EFL/EFE table of a whole cfg3 solve (2000 eigenpairs): device
-error_table vs the same contractions on the host (the reference's
-algorithm; its ErrorEvaluator is host numpy, ref verify.py:181-338)."""
+error_table (engine kernels) vs the numpy restatement of the reference's
+algorithm on the host (its ErrorEvaluator is host numpy, ref verify.py:181-338)."""
 import json
 import os
 import sys
@@ -34,16 +34,14 @@ mask = [i for i, rr in enumerate(recs) if not np.isnan(rr.efl)]
 out["unique_modes"] = len(mask)
 out["max_ev"] = float(max(rr.ev for rr in recs))
 out["max_efl"] = float(max(recs[i].efl for i in mask))
-# host evaluation of the same EFLs (reference algorithm on the CPU)
-ev = V.ErrorEvaluator(s, device="cpu")
-modes = V.exact_spectrum(s.dim, count=lams.size)
+# host evaluation of the same EFLs: the numpy restatement of the reference algorithm (oracle/verify_port.py)
+from oracle import rigaeig_port as O  # noqa: E402
+from oracle import verify_port as VP  # noqa: E402
+
+so = O.build_system(c.d, c.ne, c.p, c.level)
 Xh = X.cpu().numpy()
 t0 = time.perf_counter()
-n, uniq, C = V._aligned_batch(lams, Xh, modes, type("S", (), {"M": type("M", (), {"csr": s.M.csr})(), "dim": s.dim,
-                                                               "dof_count": s.dof_count, "spaces": s.spaces})(), ev)
-host = []
-for q, i in enumerate(uniq):
-    host.append(ev.l2_error_sq(C[q].numpy(), modes[i]))
+host = {i: f for i, _, _, f in VP.error_table(lams, Xh, so) if f is not None}
 out["host_s"] = time.perf_counter() - t0
-out["host_vs_device_max_rel"] = float(max(abs(h - recs[i].efl) / recs[i].efl for h, i in zip(host, uniq)))
+out["host_vs_device_max_rel"] = float(max(abs(host[i] - recs[i].efl) / recs[i].efl for i in mask))
 print(json.dumps(out))
