@@ -659,10 +659,24 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
   if (ahead) RIGA_TRY(ctx_aux(ctx));
   // G blocks of the small supernodes: on the low-priority side stream as soon as their last level is
   // factored, beside the upper levels (whose panel chains leave SMs idle); joined at the end
-  const int64_t g_top = small_g_top_level(sym);
+  // (forked no earlier than six levels from the top: lower down every SM is busy with frontal updates and
+  // the G kernels would only take time from them -- measured: forked at level 9 of 19 they doubled level 10)
+  const int64_t g_last = small_g_top_level(sym);
+  const int64_t g_top = g_last < 0 ? -1 : std::max<int64_t>(g_last, h.nlevels - 6);
   const SolvePlanHost& SP = sym->sp;
   if (g_top >= 0 && !F->gsmall.p) RIGA_TRY(F->gsmall.alloc(SP.g_total, st));
   bool g_forked = false;
+  // RIGA_FACTOR_TRACE=1: per-level device time (events on the factor stream), printed after the factorization
+  static const bool trace = getenv("RIGA_FACTOR_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&]() {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
+  mark();
   cudaStream_t sp = ahead ? ctx->aux[0] : st;
   cudaEvent_t evH = ahead ? ctx->aux_ev[0] : nullptr, evP = ahead ? ctx->aux_ev[1] : nullptr;
   for (int64_t l = 0; l < h.nlevels; ++l) {
@@ -762,6 +776,7 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
     }
     RIGA_TRY(extend_add(1));  // children -> update blocks, on top of the fronts' own Schur complements
     }
+    mark();
     if (ahead && l == g_top && l + 1 < h.nlevels) {
       RIGA_CUDA(cudaEventRecord(ctx->aux_ev[2], st));
       RIGA_CUDA(cudaStreamWaitEvent(ctx->aux[1], ctx->aux_ev[2], 0));
@@ -769,6 +784,17 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       RIGA_CUDA(cudaEventRecord(ctx->aux_ev[3], ctx->aux[1]));
       g_forked = true;
     }
+  }
+  if (trace) {
+    cudaStreamSynchronize(st);
+    for (size_t l = 0; l + 1 < tev.size(); ++l) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[l], tev[l + 1]);
+      const LevelPlan& P = sym->plan[l];
+      fprintf(stderr, "[riga] level %2zu: %4lld large fronts, max np %5lld, max f %5lld: %7.3f ms\n", l,
+              (long long)P.nlarge, (long long)P.max_np_large, (long long)P.max_f_large, ms);
+    }
+    for (auto e : tev) cudaEventDestroy(e);
   }
   if (g_forked)
     RIGA_CUDA(cudaStreamWaitEvent(st, ctx->aux_ev[3], 0));

@@ -83,6 +83,8 @@ struct SolvePlanHost {
   std::vector<I2> fwd, bwd;        // light tasks grouped by level
   std::vector<int32_t> chains;     // large supernodes grouped by level
   std::vector<int32_t> wholes;     // small supernodes (warp tasks) grouped by level
+  std::vector<int32_t> gnodes;     // the same sorted by width class (k_small_g<GR>)
+  int64_t gcls_ptr[5] = {0, 0, 0, 0, 0};  // class c (np <= 32 c) is gnodes[gcls_ptr[c-1] .. gcls_ptr[c])
   int sub_levels = 0, nsub = 0;        // bottom subtrees: height bound, count
   int sub_maxsn = 0;                   // most supernodes in one bottom subtree
   std::vector<int32_t> sub_fptr, sub_bptr;  // per subtree (sub_levels + 1) local-level task bounds
@@ -110,7 +112,7 @@ struct riga_symbolic {
   int64_t n_large = 0;
   SolvePlanHost sp;
   riga::DevBuf<I2> d_tfwd, d_tbwd;
-  riga::DevBuf<int32_t> d_chains, d_wholes, d_gsrc, d_sub_fptr, d_sub_bptr;
+  riga::DevBuf<int32_t> d_chains, d_wholes, d_gnodes, d_gsrc, d_sub_fptr, d_sub_bptr;
   riga::DevBuf<int64_t> d_gptr, d_inv_off, d_g_off;
   riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_dbl_tasks, d_gfwd, d_gbwd, d_sub_ftiles, d_sub_btiles;
   riga::DevBuf<int64_t> d_dbl_toff;

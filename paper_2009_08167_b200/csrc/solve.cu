@@ -316,14 +316,17 @@ __device__ __forceinline__ void pf_panel(const double* P, int64_t f, int64_t c0,
   }
 }
 
-// one CTA per G-mode supernode (np <= 128).  inv(L11) by column-oriented
+// one CTA per G-mode supernode (np <= 32 GR).  inv(L11) by column-oriented
 // substitution: warp w owns columns w + 8 j (8 per round), lanes own rows
 // lane + 32 ri; x_k is final at step k and broadcast by shuffle.  Then
-// G_bot = L21 inv(L11) from inv(L11) in shared memory.
+// G_bot = L21 inv(L11) from inv(L11) in shared memory.  Instantiated per
+// width class (GR = 1..4 row strips): shared memory and register work follow
+// the class, so the narrow supernodes -- most of them -- run many CTAs per SM.
+template <int GR>
 __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __restrict__ nodes,
                                                  const double* __restrict__ panel,
                                                  const int64_t* __restrict__ g_off, double* __restrict__ gbuf) {
-  constexpr int LD = kGMaxNp + 1;
+  constexpr int LD = 32 * GR + 1;
   extern __shared__ double Xs[];  // inv(L11) column-major, Xs[c * LD + r]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int s = nodes[blockIdx.x];
@@ -331,16 +334,16 @@ __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __rest
   const double* P = panel + S.panel_off[s];
   double* G = gbuf + g_off[s];
   for (int jb = 0; 64 * jb < np; ++jb) {
-    double x[kGRows][8];
+    double x[GR][8];
 #pragma unroll
-    for (int ri = 0; ri < kGRows; ++ri)
+    for (int ri = 0; ri < GR; ++ri)
 #pragma unroll
       for (int j = 0; j < 8; ++j) x[ri][j] = (lane + 32 * ri == w + 8 * (8 * jb + j)) ? 1.0 : 0.0;
     for (int k = 64 * jb; k + 1 < np; ++k) {
       const int kr = k >> 5, kl = k & 31;
-      double l[kGRows];
+      double l[GR];
 #pragma unroll
-      for (int ri = 0; ri < kGRows; ++ri) {
+      for (int ri = 0; ri < GR; ++ri) {
         const int r = lane + 32 * ri;
         l[ri] = (r > k && r < np) ? P[(int64_t)k * f + r] : 0.0;
       }
@@ -348,11 +351,11 @@ __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __rest
       for (int j = 0; j < 8; ++j) {
         double own = x[0][j];
 #pragma unroll
-        for (int ri = 1; ri < kGRows; ++ri)
+        for (int ri = 1; ri < GR; ++ri)
           if (kr == ri) own = x[ri][j];
         const double xk = __shfl_sync(0xffffffffu, own, kl);
 #pragma unroll
-        for (int ri = 0; ri < kGRows; ++ri) x[ri][j] = fma(-l[ri], xk, x[ri][j]);
+        for (int ri = 0; ri < GR; ++ri) x[ri][j] = fma(-l[ri], xk, x[ri][j]);
       }
     }
 #pragma unroll
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __rest
       const int c = w + 8 * (8 * jb + j);
       if (c < np) {
 #pragma unroll
-        for (int ri = 0; ri < kGRows; ++ri) {
+        for (int ri = 0; ri < GR; ++ri) {
           const int r = lane + 32 * ri;
           if (r < np) {
             Xs[c * LD + r] = x[ri][j];
@@ -374,6 +377,7 @@ __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __rest
   for (int i0 = np; i0 < f; i0 += 32) {
     const int i = i0 + lane;
     for (int jb = 0; 64 * jb < np; ++jb) {
+      if (w + 64 * jb >= np) continue;  // this warp's columns of the round are all past np
       double acc[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = 0.0;
@@ -1456,6 +1460,16 @@ int build_solve_plan(riga_symbolic* sym) {
     L.chf_smem[l] = scf * 8;
     L.chb_smem[l] = scb * 8;
   }
+  // G-mode supernodes by width class for k_small_g<GR> (np <= 32 GR), large fronts first inside a class
+  L.gnodes = L.wholes;
+  std::stable_sort(L.gnodes.begin(), L.gnodes.end(), [&](int32_t a, int32_t b) {
+    const int64_t ca = (h.ncol[a] + 31) / 32, cb = (h.ncol[b] + 31) / 32;
+    return ca != cb ? ca < cb : h.front[a] > h.front[b];
+  });
+  for (int c = 0; c <= 4; ++c)
+    L.gcls_ptr[c] = std::lower_bound(L.gnodes.begin(), L.gnodes.end(), c,
+                                     [&](int32_t a, int cls) { return (h.ncol[a] + 31) / 32 <= cls; }) -
+                    L.gnodes.begin();
   // doubling levels of the pivot-block inversions: level l pairs adjacent
   // diagonal blocks of size 32 << l; T scratch offsets per task
   for (int64_t sz = 32, lev = 0;; sz *= 2, ++lev) {
@@ -1509,6 +1523,7 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
   if (!L.bwd.empty()) RIGA_TRY(sym->d_tbwd.upload(L.bwd.data(), L.bwd.size(), s));
   if (!L.chains.empty()) RIGA_TRY(sym->d_chains.upload(L.chains.data(), L.chains.size(), s));
   if (!L.wholes.empty()) RIGA_TRY(sym->d_wholes.upload(L.wholes.data(), L.wholes.size(), s));
+  if (!L.gnodes.empty()) RIGA_TRY(sym->d_gnodes.upload(L.gnodes.data(), L.gnodes.size(), s));
   if (L.nsub) {
     RIGA_TRY(sym->d_sub_fptr.upload(L.sub_fptr.data(), L.sub_fptr.size(), s));
     RIGA_TRY(sym->d_sub_bptr.upload(L.sub_bptr.data(), L.sub_bptr.size(), s));
@@ -1575,21 +1590,32 @@ int prepare_solve() { return set_solve_attrs(); }
 // G = [inv(L11); L21 inv(L11)] of every G-mode supernode; needs only those supernodes' finished panels, so
 // the factorization launches it on a side stream once their last tree level is done (gsmall must already
 // be allocated in an order the stream respects)
+template <int GR>
+static int launch_small_g(riga_factor* F, cudaStream_t st, const int32_t* nodes, int count) {
+  if (count <= 0) return RIGA_OK;
+  constexpr int smem = 32 * GR * (32 * GR + 1) * 8;
+  static bool attr = false;
+  if (!attr) {
+    RIGA_CUDA(cudaFuncSetAttribute(k_small_g<GR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  riga_symbolic* sym = F->sym;
+  k_small_g<GR><<<count, 256, smem, st>>>(sym->dev(), nodes, F->panel.p, sym->d_g_off.p, F->gsmall.p);
+  count_launch();
+  RIGA_CUDA(cudaGetLastError());
+  return RIGA_OK;
+}
+
 int build_small_g(riga_factor* F, cudaStream_t st) {
   riga_symbolic* sym = F->sym;
   const SolvePlanHost& L = sym->sp;
-  SymDev S = sym->dev();
   if (!(L.small_g && L.g_total)) return RIGA_OK;
-  const int nw = (int)L.wholes.size();
-  constexpr int smem = kGMaxNp * (kGMaxNp + 1) * 8;
-  static bool attr = false;
-  if (!attr) {
-    RIGA_CUDA(cudaFuncSetAttribute(k_small_g, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
-  k_small_g<<<nw, 256, smem, st>>>(S, sym->d_wholes.p, F->panel.p, sym->d_g_off.p, F->gsmall.p);
-  count_launch();
-  RIGA_CUDA(cudaGetLastError());
+  // the G-mode supernodes sorted by width class (np <= 32, 64, 96, 128), widest first
+  const int32_t* nodes = sym->d_gnodes.p;
+  RIGA_TRY(launch_small_g<4>(F, st, nodes + L.gcls_ptr[3], (int)(L.gcls_ptr[4] - L.gcls_ptr[3])));
+  RIGA_TRY(launch_small_g<3>(F, st, nodes + L.gcls_ptr[2], (int)(L.gcls_ptr[3] - L.gcls_ptr[2])));
+  RIGA_TRY(launch_small_g<2>(F, st, nodes + L.gcls_ptr[1], (int)(L.gcls_ptr[2] - L.gcls_ptr[1])));
+  RIGA_TRY(launch_small_g<1>(F, st, nodes + L.gcls_ptr[0], (int)(L.gcls_ptr[1] - L.gcls_ptr[0])));
   return RIGA_OK;
 }
 

@@ -66,6 +66,16 @@ void par_chunks(int nt, int64_t n, int64_t chunk, F&& f) {
   });
 }
 
+// widest supernode kept in one piece (RIGA_SN_MAXCOLS, default 2048; 0 = never split)
+static int64_t max_sn_cols() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("RIGA_SN_MAXCOLS");
+    const int64_t w = e && *e ? std::atoll(e) : 2048;
+    return w <= 0 ? INT64_MAX : std::max<int64_t>(w, 256);
+  }();
+  return v;
+}
+
 struct Relax {
   int64_t nrelax[3] = {4, 16, 48};
   double zrelax[3] = {0.8, 0.1, 0.05};
@@ -300,16 +310,29 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
   for (int64_t s = 0; s < nf; ++s)
     if (find(s) == s) fin.push_back(s);
   std::sort(fin.begin(), fin.end(), [&](int64_t a, int64_t b) { return g_first[a] < g_first[b]; });
-  int64_t ns = (int64_t)fin.size();
-  S.nsuper = ns;
-  S.col0.resize(ns);
-  S.ncol.resize(ns);
-  std::vector<int64_t> c2s(n);
-  for (int64_t s = 0; s < ns; ++s) {
-    S.col0[s] = g_first[fin[s]];
-    S.ncol[s] = g_ncol[fin[s]];
-    for (int64_t j = S.col0[s]; j < S.col0[s] + S.ncol[s]; ++j) c2s[j] = s;
+  // Very wide supernodes (the top separators of a 3D dissection) are cut into a chain of equal pieces of
+  // at most max_sn_cols() columns: piece k's front is the old front minus the earlier pieces' columns and
+  // its parent is piece k + 1, so everything downstream (front structures, extend-add maps, levels) sees
+  // ordinary supernodes.  What it buys: the solve keeps an explicit inv(L11) per chain supernode, and
+  // inverting one 7526-column block (cfg5's root) costs as many flops as factoring its front -- four
+  // 1882-column pieces cost 1/16 of that and the off-diagonal blocks are applied from the panel instead.
+  S.col0.clear();
+  S.ncol.clear();
+  const int64_t wmax = max_sn_cols();
+  for (int64_t q = 0; q < (int64_t)fin.size(); ++q) {
+    const int64_t first = g_first[fin[q]], nc = g_ncol[fin[q]];
+    const int64_t pieces = nc > wmax ? (nc + wmax - 1) / wmax : 1;
+    for (int64_t k = 0; k < pieces; ++k) {
+      const int64_t a = first + nc * k / pieces, b = first + nc * (k + 1) / pieces;
+      S.col0.push_back(a);
+      S.ncol.push_back(b - a);
+    }
   }
+  int64_t ns = (int64_t)S.col0.size();
+  S.nsuper = ns;
+  std::vector<int64_t> c2s(n);
+  for (int64_t s = 0; s < ns; ++s)
+    for (int64_t j = S.col0[s]; j < S.col0[s] + S.ncol[s]; ++j) c2s[j] = s;
   S.sparent.assign(ns, -1);
   for (int64_t s = 0; s < ns; ++s) {
     int64_t last = S.col0[s] + S.ncol[s] - 1;
