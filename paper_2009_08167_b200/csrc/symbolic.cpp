@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <numeric>
@@ -87,6 +89,16 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
             SymbolicHost& S, std::string& err) {
   S = SymbolicHost();
   S.n = n;
+  // RIGA_SYM_TIME=1: wall time of every phase on stderr
+  static const bool timed = std::getenv("RIGA_SYM_TIME") != nullptr;
+  auto tprev = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    if (!timed) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[riga] analyze %-18s %8.2f ms\n", name,
+                 std::chrono::duration<double, std::milli>(now - tprev).count());
+    tprev = now;
+  };
   if (n <= 0) {
     err = "empty matrix";
     return 1;
@@ -143,6 +155,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
       }
     }
   }
+  phase("etree");
   // ---- 2. postorder ------------------------------------------------------
   std::vector<int64_t> head(n, -1), next(n, -1);
   for (int64_t j = n - 1; j >= 0; --j) {
@@ -188,6 +201,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
   for (int64_t k = 0; k < n; ++k) par[k] = parent[post[k]] == -1 ? -1 : ipost[parent[post[k]]];
   const std::vector<int32_t>& io = S.iorder;
 
+  phase("postorder");
   // ---- 3. exact column counts (row subtrees) -----------------------------
   // Row k of L is the union of the tree paths from A's entries (i < k) up to
   // k; rows are independent, so threads take row chunks with private marks
@@ -238,6 +252,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
     for (int64_t j = 0; j < n; ++j) S.tree_height = std::max(S.tree_height, h[j] + 1);
   }
 
+  phase("colcounts");
   // ---- 4a. fundamental supernodes ------------------------------------------
   std::vector<int64_t> nchild(n, 0);
   for (int64_t j = 0; j < n; ++j)
@@ -350,6 +365,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
       if (S.sparent[s] >= 0) S.child_list[fillp[S.sparent[s]]++] = (int32_t)s;
   }
 
+  phase("supernodes");
   // ---- 5a. front structures ---------------------------------------------
   // struct(s) = cols(s) U {rows > last(s) of A's lower columns in s}
   //           U {update rows of children > last(s)}, sorted.
@@ -422,6 +438,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
       for (int64_t s = s0; s < s1; ++s) std::copy(fr[s].begin(), fr[s].end(), S.rows.begin() + S.rows_off[s]);
     });
   }
+  phase("fronts");
   // ---- 5b. storage offsets, statistics -------------------------------------
   S.panel_off.resize(ns);
   S.cb_off.resize(ns);
@@ -450,6 +467,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
     for (int64_t k = 0; k < np; ++k) S.relaxed_flops += (f - k) * (f - k);
   }
   S.upd_off[ns] = S.upd_total;
+  phase("offsets");
   // ---- 5c. extend-add relative positions (update rows -> parent front) ----
   S.relpos.assign(S.upd_total, -1);
   {
@@ -472,6 +490,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
       for (int64_t u = 0; u < S.front[p]; ++u) pos[rp[u]] = -1;
     }
   }
+  phase("relpos");
   // ---- 5d. original-entry scatter map (lower triangle, by supernode) ------
   // Two parallel passes over supernodes: count, then fill at the prefix sums.
   S.asm_ptr.assign(ns + 1, 0);
@@ -523,6 +542,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
     }
   }
   S.nnz_lower = (int64_t)S.asm_slot.size();
+  phase("asm map");
   // ---- 5e. levels (computed in 5a): small fronts first within a level -------
   S.level_nsmall.assign(S.nlevels, 0);
   for (int64_t l = 0; l < S.nlevels; ++l) {
@@ -537,6 +557,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
       if (S.front[*it] <= kSmallFront) cnt++;
     S.level_nsmall[l] = cnt;
   }
+  phase("levels");
   // ---- 5f. update-block memory plan ------------------------------------------
   // A front's update block is written at its own level and consumed (extend-
   // add) at its parent's level, so it is live on [level(s), level(parent)].
@@ -596,6 +617,7 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
     }
     S.cb_large = 0;
   }
+  phase("cb plan");
   return 0;
 }
 
