@@ -970,7 +970,7 @@ int riga_factor_create(riga_ctx* ctx, riga_symbolic* sym, double sigma, double r
   RIGA_TRY(F->panel.alloc(std::max<int64_t>(h.panel_total, 1), st));
   RIGA_TRY(F->D.alloc(h.n, st));
   RIGA_TRY(F->xperm.alloc(h.n, st));
-  RIGA_TRY(F->upd.alloc(std::max<int64_t>(h.upd_total, 1), st));
+  RIGA_TRY(F->upd.alloc(std::max<int64_t>(sym->sp.upd_doubles, 1), st));
   RIGA_TRY(F->stat.alloc(2, st));
   RIGA_TRY(F->tol.alloc(2, st));
   RIGA_TRY(F->cvec.alloc(h.n, st));

@@ -91,8 +91,11 @@ struct SolvePlanHost {
   std::vector<I2> sub_ftiles, sub_btiles;   // their G warp tasks (row tiles / column groups)
   std::vector<int64_t> fwd_ptr, bwd_ptr, chain_ptr;
   std::vector<int64_t> fwd_smem, bwd_smem, chf_smem, chb_smem;  // bytes per level launch
-  std::vector<int32_t> gsrc;
+  std::vector<int32_t> gsrc;            // overflow pull map (children beyond the update-vector slots)
   std::vector<int64_t> gptr;
+  std::vector<uint8_t> cmask;           // per front row: contributing child slots (solve.cu SolveDev)
+  std::vector<int64_t> ubase;           // per supernode: base of its update vector's slot (-1: overflow child)
+  int64_t nfront = 0, otail = 0, upd_doubles = 1;  // slot stride, overflow region start, buffer size
 };
 
 struct riga_symbolic {
@@ -113,7 +116,8 @@ struct riga_symbolic {
   SolvePlanHost sp;
   riga::DevBuf<I2> d_tfwd, d_tbwd;
   riga::DevBuf<int32_t> d_chains, d_wholes, d_gnodes, d_gsrc, d_sub_fptr, d_sub_bptr;
-  riga::DevBuf<int64_t> d_gptr, d_inv_off, d_g_off;
+  riga::DevBuf<int64_t> d_gptr, d_inv_off, d_g_off, d_ubase;
+  riga::DevBuf<uint8_t> d_cmask;
   riga::DevBuf<I2> d_ifwd, d_ibwd, d_idiag, d_dbl_tasks, d_gfwd, d_gbwd, d_sub_ftiles, d_sub_btiles;
   riga::DevBuf<int64_t> d_dbl_toff;
   SymDev dev() const {

@@ -41,37 +41,47 @@ constexpr int64_t kChainSmemMax = 232448 - 4096;  // staged chain panels must fi
 
 enum { kWholeGroup = 1, kUpd = 2, kColdot = 3, kGTiles = 4 };
 
+// Update vectors of the forward sweep.  A supernode's update vector is stored where its parent reads it:
+// child number k (< kUpdSlots) of parent p writes its entry for the parent's front row r to
+// upd[k * nfront + rows_off[p] + r], and a row's gather is one mask byte plus up to kUpdSlots loads at
+// addresses known from the row alone -- no index chain (the earlier pull map cost three dependent loads per
+// row: gptr -> gsrc -> value).  Entries are written before they are read within a solve and only covered
+// entries are read, so the slots are never cleared.  Children beyond kUpdSlots (none in the tensor-product
+// dissections; general patterns can have them) keep the pull map over a tail region of the buffer; mask
+// bit 7 flags a row with such sources.
+constexpr int kUpdSlots = 4;
 struct SolveDev {
-  const int64_t* gptr;  // pull map over front positions (rows_off indexing)
-  const int32_t* gsrc;  // sources in the update-vector buffer
-  int permuted;         // right-hand side already in elimination order
+  const uint8_t* cmask;   // per front row: bit k = child slot k contributes, bit 7 = overflow sources
+  const int64_t* ubase;   // per supernode: k * nfront + rows_off[parent] (slot child), or -1
+  const int64_t* gptr;    // overflow pull map over front positions (rows_off indexing)
+  const int32_t* gsrc;    // its sources in the update-vector buffer
+  int64_t nfront;         // front rows of all supernodes = the stride between slots
+  int64_t otail;          // start of the overflow children's vectors (+ upd_off[c])
+  int permuted;           // right-hand side already in elimination order
 };
+
+// where entry t of supernode s's update vector lives
+__device__ __forceinline__ double* upd_slot(const SymDev& S, const SolveDev& T, int s, int64_t t, double* upd) {
+  const int64_t ub = T.ubase[s];
+  return ub >= 0 ? upd + ub + S.relpos[S.upd_off[s] + t] : upd + T.otail + S.upd_off[s] + t;
+}
 
 __device__ __forceinline__ double gather_row(const SymDev& S, const SolveDev& T, int s, int64_t r,
                                              int64_t np, int64_t col0, const double* __restrict__ b,
                                              const double* upd) {
   double v = r < np ? b[T.permuted ? col0 + r : S.order[col0 + r]] : 0.0;
   const int64_t g = S.rows_off[s] + r;
-  const int64_t q0 = T.gptr[g], q1 = T.gptr[g + 1];
-  int64_t q = q0;
-  // up to 4 contributions per round: their index loads, then their value
-  // loads, issued together (a row of a 2D/3D front has 1-4 child sources)
-  for (; q + 4 <= q1; q += 4) {
-    const int32_t i0 = T.gsrc[q], i1 = T.gsrc[q + 1], i2 = T.gsrc[q + 2], i3 = T.gsrc[q + 3];
-    const double u0 = upd[i0], u1 = upd[i1], u2 = upd[i2], u3 = upd[i3];
-    v += u0;
-    v += u1;
-    v += u2;
-    v += u3;
+  const unsigned m = T.cmask[g];
+  if (m == 0u) return v;
+  const double* y = upd + g;
+  double u[kUpdSlots];
+#pragma unroll
+  for (int k = 0; k < kUpdSlots; ++k) u[k] = (m >> k & 1u) ? y[k * T.nfront] : 0.0;
+#pragma unroll
+  for (int k = 0; k < kUpdSlots; ++k) v += u[k];
+  if (m & 0x80u) {
+    for (int64_t q = T.gptr[g]; q < T.gptr[g + 1]; ++q) v += upd[T.gsrc[q]];
   }
-  if (q + 2 <= q1) {
-    const int32_t i0 = T.gsrc[q], i1 = T.gsrc[q + 1];
-    const double u0 = upd[i0], u1 = upd[i1];
-    v += u0;
-    v += u1;
-    q += 2;
-  }
-  if (q < q1) v += upd[T.gsrc[q]];
   return v;
 }
 
@@ -170,8 +180,7 @@ __device__ __forceinline__ void warp_whole_fwd(const SymDev& S, const SolveDev& 
     __syncwarp();
   }
   for (int r = lane; r < np; r += 32) xp[col0 + r] = yw[r];
-  double* u = upd + S.upd_off[s];
-  for (int r = np + lane; r < f; r += 32) u[r - np] = yw[r];
+  for (int r = np + lane; r < f; r += 32) *upd_slot(S, T, s, r - np, upd) = yw[r];
 }
 
 // one warp: backward sweep of a small supernode
@@ -276,9 +285,7 @@ struct GDev {
 __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 __device__ __forceinline__ void pf_gather(const SymDev& S, const SolveDev& T, int s, int64_t r) {
-  const int64_t g = S.rows_off[s] + r;
-  const int64_t q0 = T.gptr[g], q1 = T.gptr[g + 1];
-  if (q1 > q0) pf_l2(T.gsrc + q0);
+  pf_l2(T.cmask + S.rows_off[s] + r);
 }
 
 // forward G tile (s, t): the G rows of the tile and the gather metadata
@@ -431,7 +438,7 @@ __device__ __forceinline__ void warp_gtile_fwd(const SymDev& S, const SolveDev& 
     xp[col0 + i] = acc;
     GD.wz[col0 + i] = acc / GD.D[col0 + i];
   } else {
-    upd[S.upd_off[s] + i - np] = yi - acc;
+    *upd_slot(S, T, s, i - np, upd) = yi - acc;
   }
 }
 
@@ -610,7 +617,7 @@ __device__ __forceinline__ void k_rest_fwd_body(SymDev S, SolveDev T,
       double v = gather_row(S, T, s, r, np, col0, b, upd);
 #pragma unroll
       for (int q = 0; q < kSolveWarps; ++q) v -= part[q][lane];
-      upd[S.upd_off[s] + r - np] = v;
+      *upd_slot(S, T, s, r - np, upd) = v;
     }
     __syncthreads();  // part[] is reused by the next task of this CTA
   }
@@ -1495,25 +1502,43 @@ int build_solve_plan(riga_symbolic* sym) {
     L.dbl_tmax = std::max(L.dbl_tmax, tt);
   }
   L.dbl_ptr.push_back((int64_t)L.dbl_tasks.size());
-  // pull map: front position -> sources in the update-vector buffer
+  // update-vector slots: child number k < kUpdSlots of a parent writes straight into the parent's front
+  // rows of slot k; later children keep a pull map over a tail region (SolveDev)
   const int64_t nfront = h.rows_off[ns];
+  L.nfront = nfront;
+  L.otail = (int64_t)kUpdSlots * nfront;
+  L.cmask.assign(nfront, 0);
+  L.ubase.assign(ns, -1);
   std::vector<int64_t> cnt(nfront + 1, 0);
+  bool overflow = false;
   for (int64_t p = 0; p < ns; ++p)
     for (int64_t q = h.child_ptr[p]; q < h.child_ptr[p + 1]; ++q) {
-      int64_t c = h.child_list[q];
-      for (int64_t t = 0; t < h.front[c] - h.ncol[c]; ++t)
-        cnt[h.rows_off[p] + h.relpos[h.upd_off[c] + t] + 1]++;
+      const int64_t c = h.child_list[q], k = q - h.child_ptr[p];
+      if (k < kUpdSlots) L.ubase[c] = k * nfront + h.rows_off[p];
+      for (int64_t t = 0; t < h.front[c] - h.ncol[c]; ++t) {
+        const int64_t g = h.rows_off[p] + h.relpos[h.upd_off[c] + t];
+        if (k < kUpdSlots) {
+          L.cmask[g] |= (uint8_t)(1u << k);
+        } else {
+          L.cmask[g] |= 0x80u;
+          cnt[g + 1]++;
+          overflow = true;
+        }
+      }
     }
+  L.upd_doubles = L.otail + (overflow ? h.upd_total : 0);
   for (int64_t i = 0; i < nfront; ++i) cnt[i + 1] += cnt[i];
   L.gptr = cnt;
   L.gsrc.assign(cnt[nfront], 0);
-  std::vector<int64_t> fillp(cnt.begin(), cnt.end() - 1);
-  for (int64_t p = 0; p < ns; ++p)
-    for (int64_t q = h.child_ptr[p]; q < h.child_ptr[p + 1]; ++q) {
-      int64_t c = h.child_list[q];
-      for (int64_t t = 0; t < h.front[c] - h.ncol[c]; ++t)
-        L.gsrc[fillp[h.rows_off[p] + h.relpos[h.upd_off[c] + t]]++] = (int32_t)(h.upd_off[c] + t);
-    }
+  if (overflow) {
+    std::vector<int64_t> fillp(cnt.begin(), cnt.end() - 1);
+    for (int64_t p = 0; p < ns; ++p)
+      for (int64_t q = h.child_ptr[p] + kUpdSlots; q < h.child_ptr[p + 1]; ++q) {
+        const int64_t c = h.child_list[q];
+        for (int64_t t = 0; t < h.front[c] - h.ncol[c]; ++t)
+          L.gsrc[fillp[h.rows_off[p] + h.relpos[h.upd_off[c] + t]]++] = (int32_t)(L.otail + h.upd_off[c] + t);
+      }
+  }
   return RIGA_OK;
 }
 
@@ -1531,6 +1556,8 @@ int upload_solve_plan(riga_symbolic* sym, cudaStream_t s) {
     RIGA_TRY(sym->d_sub_btiles.upload(L.sub_btiles.data(), L.sub_btiles.size(), s));
   }
   RIGA_TRY(sym->d_gptr.upload(L.gptr.data(), L.gptr.size(), s));
+  RIGA_TRY(sym->d_cmask.upload(L.cmask.data(), std::max<size_t>(L.cmask.size(), 1), s));
+  RIGA_TRY(sym->d_ubase.upload(L.ubase.data(), L.ubase.size(), s));
   if (L.small_g && L.g_total) {
     RIGA_TRY(sym->d_g_off.upload(L.g_off.data(), L.g_off.size(), s));
     RIGA_TRY(sym->d_gfwd.upload(L.gfwd.data(), L.gfwd.size(), s));
@@ -1686,7 +1713,7 @@ int factor_solve(riga_factor* F, cudaStream_t st, const double* b, double* x, bo
   ProfScope prof(kProfSolve, st, 16.0 * h.fill_nnz + 32.0 * h.n);
   RIGA_TRY(set_solve_attrs());
   SymDev S = sym->dev();
-  SolveDev T{sym->d_gptr.p, sym->d_gsrc.p, b_permuted ? 1 : 0};
+  SolveDev T{sym->d_cmask.p, sym->d_ubase.p, sym->d_gptr.p, sym->d_gsrc.p, L.nfront, L.otail, b_permuted ? 1 : 0};
   const int gon = L.small_g && L.g_total ? 1 : 0;
   const GDev GDf{F->gsmall.p, sym->d_g_off.p, reinterpret_cast<const int2*>(sym->d_gfwd.p), gon, F->D.p,
                  F->cvec.p};

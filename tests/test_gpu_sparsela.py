@@ -171,6 +171,22 @@ def test_solve_random_spd():
     assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) < 1e-12
 
 
+def test_solve_many_children_per_supernode():
+    """Arrowhead pencil in natural order: the last column's supernode has dozens of children, more than
+    the update-vector slots of the forward sweep (solve.cu kUpdSlots), so the overflow pull map runs."""
+    n = 60
+    rng = np.random.default_rng(5)
+    D = np.diag(4.0 + rng.random(n))
+    D[n - 1, :] = 0.1 * rng.standard_normal(n)
+    D[:, n - 1] = D[n - 1, :]
+    D[n - 1, n - 1] = 10.0
+    A = sp.csr_array(D)
+    f = P.factor_ldl(A, ordering="natural")
+    b = rng.standard_normal(n)
+    x = P.solve_fb(f, b)
+    assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) < 1e-13
+
+
 def test_solve_constructed_rhs():
     s = P.build_system(1, 32, 3, 1)
     A = s.K.csr
