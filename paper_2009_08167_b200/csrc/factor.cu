@@ -385,69 +385,107 @@ __global__ void __launch_bounds__(256) k_diag128(SymDev S, const int32_t* __rest
       if (r >= c) P[(int64_t)c * f + r] = A[c * kDBP + r];
 }
 
-// L21 = A21 L11^{-T} D^{-1} for the rows below the block, by blocked substitution: one warp (CTA) per 32
-// rows, its rows x nb columns staged in shared memory (W); per 32-column step b the L11 row strip
-// L(b rows, 0 : b + 32) is staged, T = A_b - sum_{t<b} W_t D_t L_bt^T runs on DMMA, then W_b = T L_bb^{-T}
-// D_b^{-1} row by row (lane = row).
-constexpr int kTrsmP = 36;  // pitch == 4 mod 16: conflict-free DMMA fragment loads (33 was 3-way)
-constexpr size_t kTrsmSmem = (2 * (size_t)kDB * kTrsmP + 2 * kDB) * sizeof(double);
-__global__ void __launch_bounds__(32) k_trsm128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
-                                                double* __restrict__ panel, const double* __restrict__ D) {
+// L21 = A21 L11^{-T} D^{-1} for the rows below the block, by blocked substitution: a CTA of four warps takes
+// 128 rows, one warp per 32 rows.  Per 32-column step b the CTA stages the L11 row strip L(b rows, 0 : b + 32)
+// once for its four warps; a warp stages its 32 x 32 slice A_b, subtracts sum_{t<b} W_t D_t L_bt^T on DMMA
+// (the earlier slices W_t are read back from the panel, where the warp stored them as final L21 columns --
+// ld.global.cg, one fragment ahead of its use), then W_b = T L_bb^{-T} D_b^{-1} row by row (lane = row) and
+// stores it.  Only the strip and one 32 x 32 tile per warp live in shared memory (74 KB per CTA: twelve
+// warps per SM; the previous one-warp CTAs kept their whole 32 x 128 row block there, three warps per SM).
+constexpr int kTrsmP = 36;  // pitch == 4 mod 16: conflict-free DMMA fragment loads
+constexpr int kTrsmWarps = 4;
+constexpr size_t kTrsmSmem = ((size_t)kDB * kTrsmP + kTrsmWarps * 32 * kTrsmP + 2 * kDB) * sizeof(double);
+
+__device__ __forceinline__ void cp_async8_cg(double* smem, const double* gmem, bool pred) {
+  // 8-byte cp.async has only the .ca form; the slices a warp re-reads after storing them go through
+  // ld.global.cg instead (below), so a stale L1 line is never consulted
+  cp_async8(smem, gmem, pred);
+}
+
+__global__ void __launch_bounds__(32 * kTrsmWarps, 3) k_trsm128(SymDev S, const int32_t* __restrict__ nodes, int kbo,
+                                                             double* __restrict__ panel,
+                                                             const double* __restrict__ D) {
   extern __shared__ double sm[];
   const int s = nodes[blockIdx.y];
   const int64_t f = S.front[s], np = S.ncol[s];
   if (kbo >= np) return;
   const int nb = (int)imin(kDB, np - kbo);
   const int nbp = (nb + 31) & ~31;
-  const int64_t r0 = kbo + nb + (int64_t)blockIdx.x * 32;
-  if (r0 >= f) return;
-  const int lane = threadIdx.x;
-  const int nr = (int)imin(32, f - r0);
+  const int64_t R0 = kbo + nb + (int64_t)blockIdx.x * (32 * kTrsmWarps);
+  if (R0 >= f) return;  // CTA-uniform
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = R0 + 32 * warp;
+  const bool active = r0 < f;
+  const int nr = active ? (int)imin(32, f - r0) : 0;
   const int64_t col0 = S.col0[s];
-  double* W = sm;               // W[c * kTrsmP + row]
-  double* Ls = W + kDB * kTrsmP;    // strip: L(kb + j, t) at Ls[t * kTrsmP + j]
-  double* ds = Ls + kDB * kTrsmP;   // pivots
-  double* rds = ds + kDB;       // their reciprocals
+  double* Ls = sm;                                   // strip: L(kb + j, t) at Ls[t * kTrsmP + j]
+  double* Wt = Ls + kDB * kTrsmP + warp * 32 * kTrsmP;  // this warp's slice: (row, kb + c) at Wt[c * kTrsmP + row]
+  double* ds = sm + kDB * kTrsmP + kTrsmWarps * 32 * kTrsmP;  // pivots
+  double* rds = ds + kDB;                            // their reciprocals
   const double* Lb = panel + S.panel_off[s] + (int64_t)kbo * f + kbo;  // L11(r, c) at Lb[c f + r]
   double* Pr = panel + S.panel_off[s] + (int64_t)kbo * f + r0;         // A21(row, c) at Pr[c f + row]
-  for (int c = 0; c < nbp; ++c) {
-    const bool in = c < nb && lane < nr;
-    cp_async8(W + c * kTrsmP + lane, in ? Pr + (int64_t)c * f + lane : Lb, in);
-  }
-  cp_async_commit();
-  for (int c = lane; c < nbp; c += 32) {
+  for (int c = threadIdx.x; c < nbp; c += blockDim.x) {
     const double d = c < nb ? D[col0 + kbo + c] : 1.0;
     ds[c] = d;
     rds[c] = 1.0 / d;
   }
   for (int kb = 0; kb < nbp; kb += 32) {
     const bool rowin = kb + lane < nb;
-    for (int t = 0; t < kb + 32; ++t) {
+    for (int t = warp; t < kb + 32; t += kTrsmWarps) {
       const bool in = rowin && t < nb;
       cp_async8(Ls + t * kTrsmP + lane, in ? Lb + (int64_t)t * f + kb + lane : Lb, in);
     }
+#pragma unroll 8
+    for (int c = 0; c < 32; ++c) {
+      const bool in = kb + c < nb && lane < nr;
+      cp_async8_cg(Wt + c * kTrsmP + lane, in ? Pr + (int64_t)(kb + c) * f + lane : Lb, in);
+    }
     cp_async_commit();
     cp_async_wait<0>();
-    __syncwarp();
-    if (kb > 0) {  // W_b -= sum_{t < b} W_t D_t L_bt^T
-      double acc[4][4][2];
-      zero_acc(acc);
-      warp_mma32(acc, [&](int i, int k) { return W[k * kTrsmP + i] * ds[k]; }, [&](int k, int j) { return Ls[k * kTrsmP + j]; },
-                 kb);
-      RIGA_ACC_FOR(W[(kb + aj) * kTrsmP + ai] -= acc[m][q][e];)
-      __syncwarp();
+    __syncthreads();  // strip (and ds / rds on the first pass) visible to the four warps
+    if (active) {
+      if (kb > 0) {  // T = A_b - sum_{t < b} W_t D_t L_bt^T, the W_t read back from the panel
+        double acc[4][4][2];
+        zero_acc(acc);
+        const int kq = lane & 3, ir = lane >> 2;
+        auto load_a = [&](double (&av)[4], int k4) {
+          const int kr = k4 + kq;
+          const double dk = ds[kr];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int i = m * 8 + ir;
+            av[m] = i < nr ? __ldcg(Pr + (int64_t)kr * f + i) * dk : 0.0;
+          }
+        };
+        double an[4];
+        load_a(an, 0);
+        for (int k4 = 0; k4 < kb; k4 += 4) {
+          double av[4], bv[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) av[m] = an[m];
+          if (k4 + 4 < kb) load_a(an, k4 + 4);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) bv[q] = Ls[(k4 + kq) * kTrsmP + q * 8 + ir];
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[m][q][0], acc[m][q][1], av[m], bv[q]);
+        }
+        RIGA_ACC_FOR(Wt[aj * kTrsmP + ai] -= acc[m][q][e];)
+        __syncwarp();
+      }
+      double w[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) w[c] = Wt[c * kTrsmP + lane];
+      sub32_all(w, [&](int c, int t) { return Ls[(kb + t) * kTrsmP + c]; }, [&](int c) { return rds[kb + c]; },
+                std::make_integer_sequence<int, 32>{});
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (kb + c < nb && lane < nr) Pr[(int64_t)(kb + c) * f + lane] = w[c];
+      __syncwarp();  // the stores are ordered before the next step's fragment loads of this warp
     }
-    double w[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) w[c] = W[(kb + c) * kTrsmP + lane];
-    sub32_all(w, [&](int c, int t) { return Ls[(kb + t) * kTrsmP + c]; }, [&](int c) { return rds[kb + c]; },
-              std::make_integer_sequence<int, 32>{});
-#pragma unroll
-    for (int c = 0; c < 32; ++c) W[(kb + c) * kTrsmP + lane] = w[c];
-    __syncwarp();
+    __syncthreads();  // every warp is done with the strip before it is restaged
   }
-  for (int c = 0; c < nb; ++c)
-    if (lane < nr) Pr[(int64_t)c * f + lane] = W[c * kTrsmP + lane];
 }
 
 // Trailing update of a front over its pivot columns [k0, min(k1, n_p)), lower triangle, rows to f.
@@ -739,8 +777,8 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       const int64_t kend = std::min<int64_t>(kbo + g_nb2, P.max_np_large);
       for (int64_t kb = kbo; kb < kend; kb += kDB) {
         k_diag128<<<nl, 256, kDiag128Smem, ts>>>(S, ln, (int)kb, F->tol.p, F->panel.p, F->D.p, F->stat.p);
-        const unsigned nti = (unsigned)((P.max_f_large - kb + 31) / 32);
-        k_trsm128<<<dim3(nti, nl), 32, kTrsmSmem, ts>>>(S, ln, (int)kb, F->panel.p, F->D.p);
+        const unsigned nti = (unsigned)((P.max_f_large - kb + 32 * kTrsmWarps - 1) / (32 * kTrsmWarps));
+        k_trsm128<<<dim3(nti, nl), 32 * kTrsmWarps, kTrsmSmem, ts>>>(S, ln, (int)kb, F->panel.p, F->D.p);
         count_launch(2);
         RIGA_CUDA(cudaGetLastError());
         if (kb + kDB < kend) RIGA_TRY(trail(ts, kb, kb + kDB, kb + kDB, kbo + g_nb2, false, false));

@@ -1,6 +1,6 @@
 set -x
-python -m pytest tests/test_gpu_sparsela.py tests/test_gpu_eigensolver.py -x -q 2>&1 | tail -3
-python tools/time_solve.py cfg3 50 2>&1 | tail -1
-python tools/time_solve.py cfg4 50 2>&1 | tail -1
-python tools/time_solve.py cfg5 20 2>&1 | tail -1
-python tools/concurrency_probe.py --steps 300 --what solve 2>&1 | tail -2
+python -m pytest tests/test_gpu_sparsela.py -x -q 2>&1 | tail -3
+RIGA_FACTOR_TRACE=1 python tools/one_factor.py cfg5 2>&1 | tail -23
+python tools/one_factor.py cfg4 2>&1 | tail -1
+python tools/one_factor.py cfg3 2>&1 | tail -1
+ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_tensor_subpipe_dmma.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/r2_factor_launches_cfg5_s4f.csv python tools/one_factor.py cfg5 > /dev/null 2>&1
