@@ -1,6 +1,3 @@
 set -x
-python -m pytest tests/test_gpu_sparsela.py -x -q 2>&1 | tail -3
-RIGA_FACTOR_TRACE=1 python tools/one_factor.py cfg5 2>&1 | tail -23
-python tools/one_factor.py cfg4 2>&1 | tail -1
-python tools/one_factor.py cfg3 2>&1 | tail -1
-ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_tensor_subpipe_dmma.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/r2_factor_launches_cfg5_s4f.csv python tools/one_factor.py cfg5 > /dev/null 2>&1
+for la in 1 0; do RIGA_FACTOR_LOOKAHEAD=$la python tools/one_factor.py cfg5 2>&1 | tail -1; done
+for nb in 384 640 768; do RIGA_FACTOR_NB2=$nb python tools/one_factor.py cfg5 2>&1 | tail -1; done
