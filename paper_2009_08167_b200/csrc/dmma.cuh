@@ -116,7 +116,7 @@ namespace riga {
 //   for i in [i0, i0 + 128), i < mend, and j in [j0, j0 + 128), j < nend.
 //
 // 256 threads = 8 warps as 2 (rows) x 4 (cols), each warp 64 x 32 = 8 x 4
-// DMMA.8x8x4 tiles (64 fp64 accumulators per thread).  k runs in steps of 16
+// DMMA.8x8x4 tiles (64 fp64 accumulators per thread).  k runs in steps of kT128K
 // through kT128Stages shared-memory stages filled by 8-byte cp.async (rows
 // of a front are not 16-byte aligned in general) with zero fill outside the
 // ranges.  The pivots d (or 1 for nullptr) and the sign are folded into the A
@@ -130,11 +130,15 @@ namespace riga {
 // distinct bank pairs.
 // ---------------------------------------------------------------------------
 constexpr int kT128 = 128;
-constexpr int kT128K = 16;
+#ifndef RIGA_T128K
+#define RIGA_T128K 16
+#endif
+constexpr int kT128K = RIGA_T128K;  // k rows per stage (16 or 32)
+constexpr int kT128KG = kT128K / 16;  // k rows of a stage per loader thread
 constexpr int kT128P = 132;
-constexpr int kT128Stages = 4;
+constexpr int kT128Stages = kT128K == 16 ? 4 : 3;
 constexpr int kT128StageDoubles = 2 * kT128K * kT128P;
-constexpr size_t kT128Smem = (size_t)kT128Stages * kT128StageDoubles * sizeof(double);
+constexpr size_t kT128Smem = (size_t)kT128Stages * kT128StageDoubles * sizeof(double) + 2 * kT128Stages * sizeof(uint64_t);
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -149,6 +153,26 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// mbarrier helpers of the tile's stage ring (CTA scope; arrive = release, wait = acquire)
+__device__ __forceinline__ void t128_bar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void t128_bar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void t128_bar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
 }
 
 // EPI 0: C(i - coff, j - coff) -= A d B^T; EPI 2: the same with the columns j >= jsplit going to C2
@@ -203,72 +227,105 @@ __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64
   const double* Bb = B + (k0 + kr) * ldb + j0 + c8;
   double* const S0 = smem + kr * kT128P + c8;  // this thread's first A element of stage 0
   auto load = [&](int it) {
-    double* As = S0 + (it % kT128Stages) * kT128StageDoubles;
-    double* Bs = As + kT128K * kT128P;
-    const double* pa = Ab + (int64_t)it * kT128K * lda;
-    const double* pb = Bb + (int64_t)it * kT128K * ldb;
-    const bool kin = k0 + (int64_t)it * kT128K + kr < k1;
-    if (full && kin) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        cp_async8n(As + 16 * u, pa + 16 * u, 8);
-        cp_async8n(Bs + 16 * u, pb + 16 * u, 8);
-      }
-    } else {
+    for (int g = 0; g < kT128KG; ++g) {
+      double* As = S0 + (it % kT128Stages) * kT128StageDoubles + 16 * g * kT128P;
+      double* Bs = As + kT128K * kT128P;
+      const double* pa = Ab + ((int64_t)it * kT128K + 16 * g) * lda;
+      const double* pb = Bb + ((int64_t)it * kT128K + 16 * g) * ldb;
+      const bool kin = k0 + (int64_t)it * kT128K + 16 * g + kr < k1;
+      if (full && kin) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const bool ina = kin && (ma >> u & 1u), inb = kin && (mb >> u & 1u);
-        cp_async8n(As + 16 * u, ina ? pa + 16 * u : A, ina ? 8 : 0);
-        cp_async8n(Bs + 16 * u, inb ? pb + 16 * u : B, inb ? 8 : 0);
+        for (int u = 0; u < 8; ++u) {
+          cp_async8n(As + 16 * u, pa + 16 * u, 8);
+          cp_async8n(Bs + 16 * u, pb + 16 * u, 8);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const bool ina = kin && (ma >> u & 1u), inb = kin && (mb >> u & 1u);
+          cp_async8n(As + 16 * u, ina ? pa + 16 * u : A, ina ? 8 : 0);
+          cp_async8n(Bs + 16 * u, inb ? pb + 16 * u : B, inb ? 8 : 0);
+        }
       }
     }
   };
-  // d of this thread's k row in stage `it` (zero-filled rows: any finite value); the value is only
-  // consumed by the next iteration's scale(), so the load's latency hides behind a stage of MMAs
-  auto pivot = [&](int it) -> double {
-    const int64_t kk = k0 + (int64_t)it * kT128K + kr;
+  // d of this thread's k rows in stage `it` (zero-filled rows: any finite value); the values are only
+  // consumed by the next iteration's scale(), so the loads' latency hides behind a stage of MMAs
+  auto pivot = [&](int it, int g) -> double {
+    const int64_t kk = k0 + (int64_t)it * kT128K + 16 * g + kr;
     return d ? (it < nk && kk < k1 ? d[kk] : 0.0) : 1.0;
   };
   // fold -d into this thread's own A elements of stage `it` (its copies have landed)
-  auto scale = [&](int it, double dk) {
-    double* As = S0 + (it % kT128Stages) * kT128StageDoubles;
-    double v[8];
+  auto scale = [&](int it, const double (&dk)[kT128KG]) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = As[16 * u];
+    for (int g = 0; g < kT128KG; ++g) {
+      double* As = S0 + (it % kT128Stages) * kT128StageDoubles + 16 * g * kT128P;
+      double v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) As[16 * u] = v[u] * -dk;
+      for (int u = 0; u < 8; ++u) v[u] = As[16 * u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) As[16 * u] = v[u] * -dk[g];
+    }
   };
+  // Stage ring without a CTA-wide barrier per stage: full[b] counts the 256 threads that have copied and
+  // scaled their part of the stage in buffer b, empty[b] the 256 that have finished reading it.  A thread
+  // publishes stage it + 1 before it computes stage it, so by the time any warp wants stage it + 1 the
+  // others published it a whole stage ago; the refill of a buffer waits for empty only after the next
+  // stage's MMAs have been issued.  (A __syncthreads per stage drained the DMMA pipe at every stage.)
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(smem + (size_t)kT128Stages * kT128StageDoubles);
+  uint64_t* bempty = bfull + kT128Stages;
+  if (tid == 0) {
+#pragma unroll
+    for (int b = 0; b < kT128Stages; ++b) {
+      t128_bar_init(bfull + b, 256);
+      t128_bar_init(bempty + b, 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 #pragma unroll
   for (int s = 0; s < kT128Stages - 1; ++s) {
     if (s < nk) load(s);
     cp_async_commit();
   }
-  double dpend = pivot(1);  // pivot of the stage scaled next (loaded one iteration ahead of its use)
+  double dpend[kT128KG];  // pivots of the stage scaled next (loaded one iteration ahead of their use)
   {
-    const double d0 = pivot(0);
+    double d0[kT128KG];
+#pragma unroll
+    for (int g = 0; g < kT128KG; ++g) {
+      d0[g] = pivot(0, g);
+      dpend[g] = pivot(1, g);
+    }
     cp_async_wait<kT128Stages - 2>();
-    if (nk > 0) scale(0, d0);
+    if (nk > 0) {
+      scale(0, d0);
+      t128_bar_arrive(bfull + 0);
+    }
   }
   const double* Af = smem + (lane & 3) * kT128P + wm * 64 + (lane >> 2);
   const double* Bf = smem + kT128K * kT128P + (lane & 3) * kT128P + wn * 32 + (lane >> 2);
   for (int it = 0; it < nk; ++it) {
+    const int buf = it % kT128Stages;
     cp_async_wait<kT128Stages - 3>();  // this thread's copies of stage it + 1 have landed
-    if (it + 1 < nk) scale(it + 1, dpend);
-    __syncthreads();
-    if (it + kT128Stages - 1 < nk) load(it + kT128Stages - 1);
-    cp_async_commit();
-    dpend = pivot(it + 2);
-    const double* As = Af + (it % kT128Stages) * kT128StageDoubles;
-    const double* Bs = Bf + (it % kT128Stages) * kT128StageDoubles;
+    if (it + 1 < nk) {
+      scale(it + 1, dpend);
+      t128_bar_arrive(bfull + (it + 1) % kT128Stages);
+    }
+#pragma unroll
+    for (int g = 0; g < kT128KG; ++g) dpend[g] = pivot(it + 2, g);
+    t128_bar_wait(bfull + buf, (unsigned)(it / kT128Stages) & 1u);
+    const double* As = Af + buf * kT128StageDoubles;
+    const double* Bs = Bf + buf * kT128StageDoubles;
     double av[2][8], bv[2][4];
 #pragma unroll
     for (int m = 0; m < 8; ++m) av[0][m] = As[m * 8];
 #pragma unroll
     for (int q = 0; q < 4; ++q) bv[0][q] = Bs[q * 8];
 #pragma unroll
-    for (int k4 = 0; k4 < 4; ++k4) {
+    for (int k4 = 0; k4 < kT128K / 4; ++k4) {
       const int cur = k4 & 1, nxt = cur ^ 1;
-      if (k4 < 3) {
+      if (k4 < kT128K / 4 - 1) {
 #pragma unroll
         for (int m = 0; m < 8; ++m) av[nxt][m] = As[(k4 + 1) * 4 * kT128P + m * 8];
 #pragma unroll
@@ -278,7 +335,18 @@ __device__ __forceinline__ void dmma_tile128(const double* __restrict__ A, int64
       for (int m = 0; m < 8; ++m)
 #pragma unroll
         for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[m][q][0], acc[m][q][1], av[cur][m], bv[cur][q]);
+      if (k4 == 0) {
+        // refill: stage it + Stages - 1 goes into the buffer stage it - 1 used; every thread has read it once
+        // empty completes (its MMAs of stage it - 1 were issued a stage ago, so this rarely waits)
+        const int nx = it + kT128Stages - 1;
+        if (nx < nk) {
+          if (it >= 1) t128_bar_wait(bempty + nx % kT128Stages, (unsigned)((it - 1) / kT128Stages) & 1u);
+          load(nx);
+        }
+        cp_async_commit();
+      }
     }
+    t128_bar_arrive(bempty + buf);
   }
   cp_async_wait<0>();
 #pragma unroll
