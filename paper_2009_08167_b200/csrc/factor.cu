@@ -105,7 +105,19 @@ __global__ void __launch_bounds__(256) k_extend_add(SymDev S, const int32_t* __r
     double* dst = rb < npp ? P + rb * fp : C + (rb - npp) * nup - npp;
     const double* sc = src + b * nuc;
     int64_t a = max(b, z0) + lane;
-    for (; a + 96 < z1; a += 128) {  // four independent read-modify-writes in flight per lane
+    for (; a + 224 < z1; a += 256) {  // eight independent read-modify-writes in flight per lane (16: no gain)
+      int32_t r[8];
+      double v[8], d[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r[u] = rp[a + 32 * u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = sc[a + 32 * u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) d[u] = dst[r[u]];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dst[r[u]] = d[u] + v[u];
+    }
+    for (; a + 96 < z1; a += 128) {
       const int32_t r0 = rp[a], r1 = rp[a + 32], r2 = rp[a + 64], r3 = rp[a + 96];
       const double v0 = sc[a], v1 = sc[a + 32], v2 = sc[a + 64], v3 = sc[a + 96];
       const double d0 = dst[r0], d1 = dst[r1], d2 = dst[r2], d3 = dst[r3];
