@@ -263,6 +263,11 @@ __device__ __forceinline__ void warp_whole_bwd(const SymDev& S, int s, const dou
 //     backward  x1 = G^T [z ./ d ; -x2]
 // G_top is lower triangular with explicit zeros above the diagonal.
 // ---------------------------------------------------------------------------
+// Layout: 32-row tiles, tile-major -- G(i, k) at g_off + (i / 32) * (32 np) + 32 k + (i % 32).  A forward
+// warp task streams one contiguous np x 256 B block, a backward column group reads 2 KB contiguous per row
+// strip; with the earlier column-major f x np layout every 256 B warp load came from a different DRAM page.
+__host__ __device__ __forceinline__ int64_t g_doubles(int64_t f, int64_t np) { return (f + 31) / 32 * 32 * np; }
+
 struct GDev {
   const double* g;        // all G blocks
   const int64_t* g_off;   // per supernode offset (-1: large supernode)
@@ -293,8 +298,8 @@ __device__ __forceinline__ void pf_gtile_fwd(const SymDev& S, const SolveDev& T,
                                              int lane) {
   const int s = task.x;
   const int f = (int)S.front[s], np = (int)S.ncol[s];
-  const double* G = GD.g + GD.g_off[s] + 32 * task.y;
-  for (int k = lane; k < np; k += 32) pf_l2(G + (int64_t)k * f);
+  const double* G = GD.g + GD.g_off[s] + (int64_t)task.y * 32 * np;  // the tile: np x 32 doubles, contiguous
+  for (int q = lane; q < 2 * np; q += 32) pf_l2(G + 16 * q);
   for (int r = lane; r < np; r += 32) pf_gather(S, T, s, r);
   const int i = 32 * task.y + lane;
   if (i >= np && i < f) pf_gather(S, T, s, i);
@@ -308,7 +313,7 @@ __device__ __forceinline__ void pf_gtile_bwd(const SymDev& S, const GDev& GD, in
   const double* G = GD.g + GD.g_off[s];
   const int nc = min(8, np - c0);
   for (int r = (c0 & ~31) + 32 * (lane >> 3); r < f; r += 128)
-    if ((lane & 7) < nc) pf_l2(G + (int64_t)(c0 + (lane & 7)) * f + r);
+    if ((lane & 7) < nc) pf_l2(G + (int64_t)(r >> 5) * 32 * np + 32 * (c0 + (lane & 7)));
   const int32_t* rows = S.rows + S.rows_off[s];
   for (int r = np + 32 * lane; r < f; r += 32 * 32) pf_l2(rows + r);
 }
@@ -374,7 +379,7 @@ __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __rest
           const int r = lane + 32 * ri;
           if (r < np) {
             Xs[c * LD + r] = x[ri][j];
-            G[(int64_t)c * f + r] = x[ri][j];
+            G[(int64_t)ri * 32 * np + 32 * c + lane] = x[ri][j];
           }
         }
       }
@@ -400,7 +405,7 @@ __global__ void __launch_bounds__(256) k_small_g(SymDev S, const int32_t* __rest
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int c = w + 8 * (8 * jb + j);
-          if (c < np) G[(int64_t)c * f + i] = acc[j];
+          if (c < np) G[(int64_t)(i >> 5) * 32 * np + 32 * c + (i & 31)] = acc[j];
         }
       }
     }
@@ -422,17 +427,17 @@ __device__ __forceinline__ void warp_gtile_fwd(const SymDev& S, const SolveDev& 
   if (i >= f) return;
   // 4 partial sums, 16 independent G loads in flight per lane
   double a4[4] = {0.0, 0.0, 0.0, 0.0};
-  const double* Gi = G + i;
+  const double* Gi = G + (int64_t)task.y * 32 * np + lane;  // the tile's np x 32 block, row `lane`
   int k = 0;
   for (; k + 16 <= np; k += 16) {
     double g[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) g[u] = Gi[(k + u) * f];
+    for (int u = 0; u < 16; ++u) g[u] = Gi[(k + u) * 32];
 #pragma unroll
     for (int u = 0; u < 16; ++u) a4[u & 3] = fma(g[u], yw[k + u], a4[u & 3]);
   }
 #pragma unroll 8
-  for (; k < np; ++k) a4[0] = fma(Gi[k * f], yw[k], a4[0]);
+  for (; k < np; ++k) a4[0] = fma(Gi[k * 32], yw[k], a4[0]);
   const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
   if (i < np) {
     xp[col0 + i] = acc;
@@ -461,10 +466,12 @@ __device__ __forceinline__ void warp_gtile_bwd(const SymDev& S, const GDev& GD, 
     const double v1 = r < np ? GD.wz[col0 + r] : -xp[rows[r]];
     const double v2 = r2 < np ? GD.wz[col0 + r2] : -xp[rows[r2]];
     double g1[8], g2[8];
+    const double* G1 = G + (int64_t)(r >> 5) * 32 * np + 32 * c0 + lane;  // strip r, columns c0 .. c0 + 8
+    const double* G2 = G1 + 32 * np;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      g1[c] = c < nc ? G[(c0 + c) * f + r] : 0.0;
-      g2[c] = c < nc ? G[(c0 + c) * f + r2] : 0.0;
+      g1[c] = c < nc ? G1[32 * c] : 0.0;
+      g2[c] = c < nc ? G2[32 * c] : 0.0;
     }
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[c] = fma(g2[c], v2, fma(g1[c], v1, acc[c]));
@@ -472,7 +479,8 @@ __device__ __forceinline__ void warp_gtile_bwd(const SymDev& S, const GDev& GD, 
   if (r < f) {
     const double v = r < np ? GD.wz[col0 + r] : -xp[rows[r]];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] = fma(c < nc ? G[(c0 + c) * f + r] : 0.0, v, acc[c]);
+    for (int c = 0; c < 8; ++c)
+      acc[c] = fma(c < nc ? G[(int64_t)(r >> 5) * 32 * np + 32 * (c0 + c) + lane] : 0.0, v, acc[c]);
   }
 #pragma unroll
   for (int o = 4; o >= 1; o >>= 1) {
@@ -1363,7 +1371,7 @@ int build_solve_plan(riga_symbolic* sym) {
         byl[h.level[q]].push_back((int32_t)q);
         in_sub[q] = 1;
         L.g_off[q] = L.g_total;
-        L.g_total += h.front[q] * h.ncol[q];
+        L.g_total += g_doubles(h.front[q], h.ncol[q]);
         L.wholes.push_back((int32_t)q);
       }
       for (int j = 0; j < SL; ++j) {
@@ -1421,7 +1429,7 @@ int build_solve_plan(riga_symbolic* sym) {
       } else {
         small.push_back(s);
         L.g_off[s] = L.g_total;
-        L.g_total += h.front[s] * h.ncol[s];
+        L.g_total += g_doubles(h.front[s], h.ncol[s]);
       }
     }
     if (L.small_g) {
