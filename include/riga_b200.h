@@ -126,6 +126,24 @@ int riga_spmv_many(riga_ctx* ctx, riga_system* sys, int which, double sigma, con
 int riga_csr_spmv(riga_ctx* ctx, int64_t n, const int64_t* rowptr_dev, const int32_t* colidx_dev,
                   const double* val_dev, const double* x_dev, double* y_dev);
 
+/* ---- separator ordering (ref sparsela.py:319-392 separator_ordering) -----
+ * Nested dissection aligned with the C0 planes of the tensor-product box of
+ * `d` axes with ext[t] cells (Dirichlet-reduced basis counts) and degree p.
+ * lines: the C0 plane indices of all axes concatenated (ascending per axis),
+ * nlines[t] of them on axis t (ref _direction_c0 :313-316).
+ * riga_separator_boxes builds the dissection tree on the host (a few
+ * thousand boxes) and returns the blocks in elimination order: leaves in
+ * recursion order, then separators deepest level first (ref :386-389).
+ * chunks: cap x 7 int64 (offset, lo[3], extent[3]); with chunks == NULL or
+ * cap too small only *nchunks is set (size query).
+ * riga_separator_emit writes the permutation on the device (one thread per
+ * elimination position; cells of a block in the reference's emit() order,
+ * axis 0 fastest): perm_dev[k] = original index eliminated k-th.           */
+int riga_separator_boxes(int d, const int64_t* ext, int degree, const int64_t* lines, const int64_t* nlines,
+                         int64_t cap, int64_t* nchunks, int64_t* chunks);
+int riga_separator_emit(riga_ctx* ctx, int d, const int64_t* ext, int64_t nchunks, const int64_t* chunks_host,
+                        int64_t n, int64_t* perm_dev);
+
 /* ---- symbolic analysis (host C++, once per pattern + ordering) ----------
  * Replaces the per-call permute/triu/_etree_counts of factor_ldl
  * (ref sparsela.py:239-250, _etree_counts :100-115): elimination tree,

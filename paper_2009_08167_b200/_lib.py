@@ -47,6 +47,8 @@ SIGNATURES = {
     "riga_spmv": [_p, _i32, _d, _p, _p],
     "riga_csr_spmv": [_p, _i64, _p, _p, _p, _p, _p],
     "riga_spmv_many": [_p, _p, _i32, _d, _p, _i64, _i64, _p, _i64],
+    "riga_separator_boxes": [_i32, _p, _i32, _p, _p, _i64, _p, _p],
+    "riga_separator_emit": [_p, _i32, _p, _i64, _p, _i64, _p],
     "riga_symbolic_create": [_p, _p, _p],
     "riga_symbolic_analyze": [_i64, _p, _p, _p, _p],
     "riga_symbolic_stats": [_p, _p],

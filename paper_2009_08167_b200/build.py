@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libriga_b200.so")
-SOURCES = ["system.cu", "factor.cu", "solve.cu", "lanczos.cu", "residual.cu", "quadrature.cu", "verify.cu", "symbolic.cpp", "prof.cpp"]
+SOURCES = ["system.cu", "factor.cu", "solve.cu", "lanczos.cu", "residual.cu", "quadrature.cu", "verify.cu", "ordering.cu", "symbolic.cpp", "prof.cpp"]
 HEADERS = ["common.h", "internal.h", "kernels.cuh", "dmma.cuh", "symbolic.h", "prof.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -478,6 +478,25 @@ def _c0_lines(system: DiscreteSystem):
     return [separator_basis_indices(s) - 1 for s in system.spaces]
 
 
+def separator_blocks(system: DiscreteSystem) -> np.ndarray:
+    """The dissection tree of ``separator_ordering`` as blocks in elimination order: one row
+    (offset, lo[3], extent[3]) per leaf / separator box (engine: riga_separator_boxes, host C++)."""
+    ext = np.array([s.basis_count - 2 for s in system.spaces], dtype=np.int64)
+    lines = [np.ascontiguousarray(l, dtype=np.int64) for l in _c0_lines(system)]
+    nlines = np.array([l.size for l in lines], dtype=np.int64)
+    flat = np.concatenate(lines) if lines else np.zeros(0, np.int64)
+    flat = np.ascontiguousarray(flat if flat.size else np.zeros(1, np.int64))
+    L = _lib.lib()
+    nch = ctypes.c_int64(0)
+    p = int(system.spaces[0].degree)
+    _lib.check(L.riga_separator_boxes(system.dim, _lib.ptr(ext), p, _lib.ptr(flat), _lib.ptr(nlines), 0,
+                                      ctypes.byref(nch), None), "separator_boxes")
+    chunks = np.zeros((nch.value, 7), dtype=np.int64)
+    _lib.check(L.riga_separator_boxes(system.dim, _lib.ptr(ext), p, _lib.ptr(flat), _lib.ptr(nlines), nch.value,
+                                      ctypes.byref(nch), _lib.ptr(chunks)), "separator_boxes")
+    return chunks
+
+
 def separator_ordering(system: DiscreteSystem) -> np.ndarray:
     """Nested dissection aligned with the rIGA C0 planes (ref :319-392).
 
@@ -485,66 +504,33 @@ def separator_ordering(system: DiscreteSystem) -> np.ndarray:
     longest axis with a candidate first); without one, at a width-p slab in
     the middle of its longest axis; boxes no longer than max(2p, 8) are
     leaves.  Order: leaves (recursion order), then separators deepest first.
+
+    The tree (a few thousand boxes) is built by the engine on the host; the
+    permutation itself is written by a device kernel when the system lives on
+    a device (riga_separator_emit), else block by block with numpy.
     """
-    ext = [s.basis_count - 2 for s in system.spaces]
-    p = system.spaces[0].degree
-    d = system.dim
-    lines = _c0_lines(system)
-    strides = [int(np.prod(ext[:t])) for t in range(d)]
-    leaf = max(2 * p, 8)
-    leaves: list = []
-    seps: list = []
-
-    def cells(box):
-        idx = np.zeros(1, dtype=np.int64)
-        for t in range(d):
-            ax = np.arange(box[t][0], box[t][1], dtype=np.int64) * strides[t]
-            idx = (ax[:, None] + idx[None, :]).ravel()
-        return idx
-
-    stack = [(tuple((0, e) for e in ext), 0, False)]
-    # explicit stack: (box, depth, emitted_children) to avoid deep recursion
-    post = []
-    while stack:
-        box, depth, done = stack.pop()
-        if done:
-            post.append((box, depth))
-            continue
-        widths = [b - a for a, b in box]
-        cut = None
-        for t in sorted(range(d), key=lambda t: -widths[t]):
-            a, b = box[t]
-            cand = lines[t][(lines[t] >= a + 1) & (lines[t] <= b - 2)]
-            if cand.size:
-                c = int(cand[np.argmin(np.abs(cand - (a + b - 1) / 2.0))])
-                cut = (t, c, c + 1)
-                break
-        if cut is None:
-            t = int(np.argmax(widths))
-            if widths[t] <= leaf:
-                leaves.append(cells(box))
-                continue
-            a, b = box[t]
-            s0 = min(max(a + (widths[t] - p) // 2, a + 1), b - 1 - p)
-            cut = (t, s0, s0 + p)
-        t, s0, s1 = cut
-        lo = list(box); lo[t] = (box[t][0], s0)
-        hi = list(box); hi[t] = (s1, box[t][1])
-        mid = list(box); mid[t] = (s0, s1)
-        # children are visited left then right; the separator after both
-        stack.append((tuple(mid), depth, True))
-        stack.append((tuple(hi), depth + 1, False))
-        stack.append((tuple(lo), depth + 1, False))
-    for box, depth in post:
-        while len(seps) <= depth:
-            seps.append([])
-        seps[depth].append(cells(box))
-    chunks = leaves
-    for lev in reversed(seps):
-        chunks.extend(lev)
-    order = np.concatenate(chunks)
-    if order.size != system.dof_count:
+    chunks = separator_blocks(system)
+    ext = np.array([s.basis_count - 2 for s in system.spaces], dtype=np.int64)
+    n = system.dof_count
+    if int(chunks[-1, 0] + np.prod(chunks[-1, 4:7])) != n:
         raise AssertionError("dissection did not enumerate every DOF")
+    dev = getattr(system, "device", None)
+    if dev is not None:
+        ctx = dev.ctx
+        with ctx:
+            perm = torch.empty(n, dtype=torch.int64, device=f"cuda:{ctx.device}")
+            _lib.check(_lib.lib().riga_separator_emit(ctx.handle, system.dim, _lib.ptr(ext), chunks.shape[0],
+                                                      _lib.ptr(chunks), n, _lib.ptr(perm)), "separator_emit")
+            return perm.cpu().numpy()
+    strides = np.ones(3, dtype=np.int64)
+    for t in range(1, system.dim):
+        strides[t] = strides[t - 1] * ext[t - 1]
+    order = np.empty(n, dtype=np.int64)
+    for off, l0, l1, l2, e0, e1, e2 in chunks:
+        a0 = (l0 + np.arange(e0, dtype=np.int64)) * strides[0]
+        a1 = (l1 + np.arange(e1, dtype=np.int64)) * strides[1]
+        a2 = (l2 + np.arange(e2, dtype=np.int64)) * strides[2]
+        order[off:off + e0 * e1 * e2] = (a2[:, None, None] + a1[None, :, None] + a0[None, None, :]).ravel()
     return order
 
 

@@ -39,6 +39,23 @@ def test_device_assembly_bit_identical(golden, name):
     assert sha(s.M.csr.data) == g["M_data"]
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_riga", "cfg2_iga", "cfg3_riga", "cfg4_riga", "cfg4_iga", "cfg5_riga"])
+def test_device_separator_ordering_equals_reference(golden, name):
+    """separator_ordering (ref sparsela.py:319-392) with the permutation written by the device kernel
+    (riga_separator_emit over the engine's dissection blocks): identical to the reference's ordering, and
+    to the host emission of the same blocks."""
+    import types
+
+    c = golden["configs"][name]
+    s = P.build_system(c["d"], c["ne"], c["p"], c["level"])
+    assert s.device is not None
+    perm = P.separator_ordering(s)
+    assert perm.dtype == np.int64 and perm.shape == (s.dof_count,)
+    assert sha(perm) == golden["systems"][name]["perm"]
+    host = types.SimpleNamespace(spaces=s.spaces, dim=s.dim, dof_count=s.dof_count, device=None)
+    assert np.array_equal(P.separator_ordering(host), perm)
+
+
 @pytest.mark.parametrize("d,ne,p,lv", [(1, 16, 2, 0), (2, 8, 3, 1), (3, 4, 2, 1), (2, 16, 2, 0)])
 def test_small_assembly_bit_identical(golden, d, ne, p, lv):
     g = golden["systems"][f"s{d}_{ne}_{p}_{lv}"]
