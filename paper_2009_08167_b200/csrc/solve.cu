@@ -1315,10 +1315,10 @@ static int env_flag(const char* name, int dflt) {
 }
 
 // bottom subtrees of G supernodes below this height run as one CTA each
-// (k_sub_fwd/bwd).  cfg3 A/B of the solve: 6 is best for 1-4 concurrent
-// slices (lone solve 0.295 -> 0.253 ms), 8 for 16 (+17 % solves/s, lone
-// +28 % slower); riga_set_solve_sub_levels picks it per run, RIGA_SUB_LEVELS
-// overrides.  Read when a symbolic analysis builds its solve plan.
+// (k_sub_fwd/bwd).  cfg3 A/B of the solve: 6 is best for a few concurrent
+// slices, 7 for 16 (+12 % solves/s, lone solve +1 %; 8: +9 %, lone +23 %);
+// riga_set_solve_sub_levels picks it per run (slicing.solve_sub_levels),
+// RIGA_SUB_LEVELS overrides.  Read when a symbolic analysis builds its solve plan.
 static int g_sub_levels = 6;
 
 int build_solve_plan(riga_symbolic* sym) {

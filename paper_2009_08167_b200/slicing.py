@@ -254,8 +254,12 @@ def _allgather(obj, group_world):
 
 def solve_sub_levels(slices_per_gpu: int) -> int:
     """Subtree height of the solve plan for a run with this many concurrent
-    slices per GPU (riga_set_solve_sub_levels: 8 for many, 6 for few)."""
-    return 8 if slices_per_gpu >= 12 else 6
+    slices per GPU (riga_set_solve_sub_levels).  cfg3 solves/s at 1 / 7 / 10 / 16
+    streams (tools/concurrency_probe.py --what solve): height 6 2.46 k / 11.2 k /
+    13.5 k / 15.0 k, height 7 2.43 k / 10.8 k / 13.8 k / 16.8 k, height 8 2.00 k /
+    9.5 k / 12.4 k / 16.4 k.  7 replaced 8 in session 5: as fast with 16 streams and
+    15 % faster once only 7 slices are still running (the tail of a step)."""
+    return 7 if slices_per_gpu >= 12 else 6
 
 
 class solve_plan:
