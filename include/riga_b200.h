@@ -144,7 +144,8 @@ int riga_separator_boxes(int d, const int64_t* ext, int degree, const int64_t* l
 int riga_separator_emit(riga_ctx* ctx, int d, const int64_t* ext, int64_t nchunks, const int64_t* chunks_host,
                         int64_t n, int64_t* perm_dev);
 
-/* ---- symbolic analysis (host C++, once per pattern + ordering) ----------
+/* ---- symbolic analysis (host C++ and, for the scatter map of the original
+ * entries, device kernels; once per pattern + ordering) ------------------
  * Replaces the per-call permute/triu/_etree_counts of factor_ldl
  * (ref sparsela.py:239-250, _etree_counts :100-115): elimination tree,
  * postorder, column counts, fundamental + relaxed supernodes, frontal row
@@ -164,6 +165,14 @@ int riga_symbolic_stats(riga_symbolic* sym, int64_t* stats16);
 int riga_symbolic_order(riga_symbolic* sym, int64_t* order_host);
 /* Exact column counts of L (diagonal included) in the caller's perm order. */
 int riga_symbolic_colcounts(riga_symbolic* sym, int64_t* counts_host);
+/* Scatter map of the original lower-triangle entries into the fronts, grouped
+ * by supernode: asm_ptr[n_supernodes + 1], then per entry the CSR slot and the
+ * position col_in_front * f + row_pos in the supernode's panel.  A device
+ * analysis (riga_symbolic_create) builds it on the device, a host analysis on
+ * the host; *count = entries (stats nnz_lower); with the three arrays NULL
+ * only *count is set.  For tests.                                            */
+int riga_symbolic_asm_map(riga_symbolic* sym, int64_t* count, int64_t* asm_ptr_host, int32_t* slot_host,
+                          int32_t* local_host);
 /* Supernode table (relaxed supernodes in postorder, n_supernodes entries
  * each): first column, column count, front size, parent (-1 root), tree
  * level (0 = leaf).  For analysis and tests.                              */

@@ -54,6 +54,7 @@ SIGNATURES = {
     "riga_symbolic_stats": [_p, _p],
     "riga_symbolic_order": [_p, _p],
     "riga_symbolic_colcounts": [_p, _p],
+    "riga_symbolic_asm_map": [_p, _p, _p, _p, _p],
     "riga_symbolic_supernodes": [_p, _p, _p, _p, _p, _p],
     "riga_symbolic_destroy": [_p],
     "riga_factor_create": [_p, _p, _d, _d, _p, _p, _p],

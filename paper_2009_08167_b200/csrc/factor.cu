@@ -606,9 +606,122 @@ static int up(DevBuf<T>& d, const std::vector<T>& v, cudaStream_t s) {
   return d.upload(v.data(), v.size(), s);
 }
 
+// ---- scatter map of the original entries, built on the device -----------------------------------------
+// (what symbolic.cpp 5d builds on the host for a host-only analysis: for every supernode the lower-triangle
+// entries of its pivot columns as (CSR slot, position in the panel), columns in elimination order, a column's
+// entries in CSR order.)  One warp per elimination column: count, exclusive scan, fill.
+__global__ void k_asm_count(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
+                            const int32_t* __restrict__ order, const int32_t* __restrict__ io,
+                            int64_t* __restrict__ cnt) {
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const int64_t o = order[j];
+  int c = 0;
+  for (int64_t q = rowptr[o] + lane; q < rowptr[o + 1]; q += 32) c += io[colidx[q]] >= j;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+  if (lane == 0) cnt[j] = c;
+}
+
+__global__ void k_asm_fill(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
+                           const int32_t* __restrict__ order, const int32_t* __restrict__ io,
+                           const int32_t* __restrict__ sn_of, const int64_t* __restrict__ col0,
+                           const int64_t* __restrict__ ncol, const int64_t* __restrict__ front,
+                           const int64_t* __restrict__ rows_off, const int32_t* __restrict__ rows,
+                           const int64_t* __restrict__ colptr, int32_t* __restrict__ slot,
+                           int32_t* __restrict__ local, int* __restrict__ bad) {
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const int64_t o = order[j];
+  const int s = sn_of[j];
+  const int64_t c0 = col0[s], np = ncol[s], f = front[s];
+  const int32_t* upd = rows + rows_off[s] + np;  // the front's update rows, ascending
+  const int64_t nu = f - np;
+  int64_t w = colptr[j];
+  for (int64_t q0 = rowptr[o]; q0 < rowptr[o + 1]; q0 += 32) {
+    const int64_t q = q0 + lane;
+    int64_t i = -1;
+    if (q < rowptr[o + 1]) i = io[colidx[q]];
+    const bool take = i >= j;
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      int64_t r;
+      if (i < c0 + np) {
+        r = i - c0;
+      } else {
+        int64_t a = 0, b = nu;  // lower bound of i in upd
+        while (a < b) {
+          const int64_t h = (a + b) >> 1;
+          if (upd[h] < i) a = h + 1;
+          else b = h;
+        }
+        if (a >= nu || upd[a] != i) *bad = 1;
+        r = np + a;
+      }
+      const int64_t e = w + __popc(m & ((1u << lane) - 1));
+      slot[e] = (int32_t)q;
+      local[e] = (int32_t)((j - c0) * f + r);
+    }
+    w += __popc(m);
+  }
+}
+
+__global__ void k_asm_ptr(int64_t ns, int64_t n, const int64_t* __restrict__ col0, const int64_t* __restrict__ colptr,
+                          int64_t* __restrict__ asm_ptr) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s < ns) asm_ptr[s] = colptr[col0[s]];
+  if (s == ns) asm_ptr[ns] = colptr[n];
+}
+
+// needs d_order, d_col0, d_ncol, d_front, d_rows_off, d_rows on the device
+static int build_asm_map_device(riga_symbolic* sym) {
+  cudaStream_t st = sym->ctx->stream;
+  SymbolicHost& h = sym->h;
+  const int64_t n = h.n, ns = h.nsuper;
+  RIGA_CHECK_ARG(sym->sys && sym->sys->n == n, "device scatter map needs the device pattern");
+  std::vector<int32_t> sn_of(n);
+  for (int64_t s = 0; s < ns; ++s)
+    for (int64_t j = h.col0[s]; j < h.col0[s] + h.ncol[s]; ++j) sn_of[j] = (int32_t)s;
+  DevBuf<int32_t> d_sn, d_io;
+  DevBuf<int64_t> colptr;
+  DevBuf<int> bad;
+  RIGA_TRY(up(d_sn, sn_of, st));
+  RIGA_TRY(up(d_io, h.iorder, st));
+  RIGA_TRY(colptr.alloc(n + 1, st));
+  RIGA_TRY(bad.alloc(1, st));
+  RIGA_CUDA(cudaMemsetAsync(colptr.p, 0, sizeof(int64_t), st));
+  RIGA_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  const unsigned gw = (unsigned)((n * 32 + 255) / 256);
+  k_asm_count<<<gw, 256, 0, st>>>(n, sym->sys->rowptr.p, sym->sys->colidx.p, sym->d_order.p, d_io.p, colptr.p + 1);
+  RIGA_TRY(inclusive_scan_i64(st, colptr.p + 1, n));
+  int64_t total = 0;
+  RIGA_CUDA(cudaMemcpyAsync(&total, colptr.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  RIGA_CUDA(stream_sync(st));
+  RIGA_CHECK_ARG(total > 0 && total < (int64_t)1 << 31, "scatter map size out of range");
+  RIGA_TRY(sym->d_asm_ptr.alloc(ns + 1, st));
+  RIGA_TRY(sym->d_asm_slot.alloc(total, st));
+  RIGA_TRY(sym->d_asm_local.alloc(total, st));
+  k_asm_fill<<<gw, 256, 0, st>>>(n, sym->sys->rowptr.p, sym->sys->colidx.p, sym->d_order.p, d_io.p, d_sn.p,
+                                sym->d_col0.p, sym->d_ncol.p, sym->d_front.p, sym->d_rows_off.p, sym->d_rows.p,
+                                colptr.p, sym->d_asm_slot.p, sym->d_asm_local.p, bad.p);
+  k_asm_ptr<<<(unsigned)((ns + 1 + 255) / 256), 256, 0, st>>>(ns, n, sym->d_col0.p, colptr.p, sym->d_asm_ptr.p);
+  RIGA_CUDA(cudaGetLastError());
+  int hb = 0;
+  RIGA_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RIGA_CUDA(stream_sync(st));
+  if (hb) {
+    set_error("symbolic analysis: original entry outside its front");
+    return RIGA_BAD_ARG;
+  }
+  h.nnz_lower = total;
+  return RIGA_OK;
+}
+
 static int upload_symbolic(riga_symbolic* sym) {
   cudaStream_t s = sym->ctx->stream;
-  const SymbolicHost& h = sym->h;
+  SymbolicHost& h = sym->h;
   RIGA_TRY(up(sym->d_col0, h.col0, s));
   RIGA_TRY(up(sym->d_ncol, h.ncol, s));
   RIGA_TRY(up(sym->d_front, h.front, s));
@@ -617,17 +730,21 @@ static int upload_symbolic(riga_symbolic* sym) {
   RIGA_TRY(up(sym->d_cb_off, h.cb_off, s));
   RIGA_TRY(up(sym->d_upd_off, h.upd_off, s));
   RIGA_TRY(up(sym->d_child_ptr, h.child_ptr, s));
-  RIGA_TRY(up(sym->d_asm_ptr, h.asm_ptr, s));
   RIGA_TRY(up(sym->d_sparent, h.sparent, s));
   RIGA_TRY(up(sym->d_rows, h.rows, s));
   RIGA_TRY(up(sym->d_relpos, h.relpos, s));
   RIGA_TRY(up(sym->d_child_list, h.child_list, s));
-  std::vector<int32_t> slot32(h.asm_slot.begin(), h.asm_slot.end());
-  RIGA_TRY(up(sym->d_asm_slot, slot32, s));
-  RIGA_TRY(up(sym->d_asm_local, h.asm_local, s));
   RIGA_TRY(up(sym->d_level_nodes, h.level_nodes, s));
   std::vector<int32_t> ord32(h.order.begin(), h.order.end());
   RIGA_TRY(up(sym->d_order, ord32, s));
+  if (h.asm_ptr.empty()) {  // device analysis: the scatter map is built here
+    RIGA_TRY(build_asm_map_device(sym));
+  } else {
+    RIGA_TRY(up(sym->d_asm_ptr, h.asm_ptr, s));
+    std::vector<int32_t> slot32(h.asm_slot.begin(), h.asm_slot.end());
+    RIGA_TRY(up(sym->d_asm_slot, slot32, s));
+    RIGA_TRY(up(sym->d_asm_local, h.asm_local, s));
+  }
   RIGA_TRY(up(sym->d_ea_items, sym->ea_items_host, s));
   RIGA_TRY(up(sym->d_large_nodes, sym->large_host, s));
   RIGA_TRY(upload_solve_plan(sym, s));
@@ -933,7 +1050,7 @@ int riga_symbolic_create(riga_system* sys, const int64_t* perm, riga_symbolic** 
   sym->sys = sys;
   std::string err;
   const auto t1 = clk::now();
-  if (analyze(sys->n, rp.data(), ci.data(), perm, sym->h, err)) {
+  if (analyze(sys->n, rp.data(), ci.data(), perm, sym->h, err, /*with_asm_map=*/false)) {
     set_error("symbolic analysis: " + err);
     return RIGA_BAD_ARG;
   }
@@ -968,6 +1085,28 @@ int riga_symbolic_stats(riga_symbolic* sym, int64_t* st) {
 int riga_symbolic_order(riga_symbolic* sym, int64_t* order) {
   RIGA_CHECK_ARG(sym && order, "null arg");
   std::memcpy(order, sym->h.order.data(), sym->h.n * sizeof(int64_t));
+  return RIGA_OK;
+}
+
+int riga_symbolic_asm_map(riga_symbolic* sym, int64_t* count, int64_t* asm_ptr, int32_t* slot, int32_t* local) {
+  RIGA_CHECK_ARG(sym && count, "null arg");
+  const SymbolicHost& h = sym->h;
+  *count = h.nnz_lower;
+  if (!asm_ptr && !slot && !local) return RIGA_OK;
+  RIGA_CHECK_ARG(asm_ptr && slot && local, "null arg");
+  if (!h.asm_ptr.empty()) {  // host analysis
+    std::copy(h.asm_ptr.begin(), h.asm_ptr.end(), asm_ptr);
+    for (size_t e = 0; e < h.asm_slot.size(); ++e) slot[e] = (int32_t)h.asm_slot[e];
+    std::copy(h.asm_local.begin(), h.asm_local.end(), local);
+    return RIGA_OK;
+  }
+  RIGA_CHECK_ARG(sym->on_device, "no scatter map");
+  DeviceGuard g(sym->ctx->device);
+  cudaStream_t st = sym->ctx->stream;
+  RIGA_CUDA(cudaMemcpyAsync(asm_ptr, sym->d_asm_ptr.p, (h.nsuper + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  RIGA_CUDA(cudaMemcpyAsync(slot, sym->d_asm_slot.p, h.nnz_lower * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  RIGA_CUDA(cudaMemcpyAsync(local, sym->d_asm_local.p, h.nnz_lower * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  RIGA_CUDA(stream_sync(st));
   return RIGA_OK;
 }
 

@@ -86,7 +86,7 @@ struct Relax {
 }  // namespace
 
 int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64_t* perm,
-            SymbolicHost& S, std::string& err) {
+            SymbolicHost& S, std::string& err, bool with_asm_map) {
   S = SymbolicHost();
   S.n = n;
   // RIGA_SYM_TIME=1: wall time of every phase on stderr
@@ -493,8 +493,8 @@ int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64
   phase("relpos");
   // ---- 5d. original-entry scatter map (lower triangle, by supernode) ------
   // Two parallel passes over supernodes: count, then fill at the prefix sums.
-  S.asm_ptr.assign(ns + 1, 0);
-  {
+  if (with_asm_map) S.asm_ptr.assign(ns + 1, 0);
+  if (with_asm_map) {
     const int nt = sym_threads(n);
     par_chunks(nt, ns, 32, [&](int, int64_t s0, int64_t s1) {
       for (int64_t s = s0; s < s1; ++s) {

@@ -45,8 +45,10 @@ struct SymbolicHost {
   std::vector<int64_t> level_nsmall;  // count of small fronts at the head of each level
 };
 
-// Returns 0 on success; message in err otherwise.
+// Returns 0 on success; message in err otherwise.  with_asm_map = false leaves the scatter map of the
+// original entries (asm_ptr / asm_slot / asm_local, nnz_lower) empty: a device analysis builds it on the
+// device instead (factor.cu, build_asm_map_device).
 int analyze(int64_t n, const int64_t* rowptr, const int32_t* colidx, const int64_t* perm,
-            SymbolicHost& out, std::string& err);
+            SymbolicHost& out, std::string& err, bool with_asm_map = true);
 
 }  // namespace riga

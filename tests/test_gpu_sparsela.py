@@ -56,6 +56,43 @@ def test_device_separator_ordering_equals_reference(golden, name):
     assert np.array_equal(P.separator_ordering(host), perm)
 
 
+@pytest.mark.parametrize("cfg", [(2, 16, 2, 0), (2, 64, 3, 3), (3, 8, 2, 1), (2, 256, 4, 4), (3, 32, 2, 2)])
+def test_device_scatter_map_equals_host_analysis(cfg):
+    """The scatter map of the original entries into the fronts (symbolic.cpp 5d on the host) is built by device
+    kernels in a device analysis (factor.cu build_asm_map_device: count / scan / fill, one warp per elimination
+    column): identical arrays to the host-only analysis of the same pattern and ordering."""
+    import ctypes
+
+    from paper_2009_08167_b200 import _lib
+
+    s = P.build_system(*cfg)
+    perm = np.ascontiguousarray(P.separator_ordering(s), dtype=np.int64)
+    dev = Symbolic.on_device(s.device, perm)
+    A = s.K.csr
+    rp = np.ascontiguousarray(A.indptr, dtype=np.int64)
+    ci = np.ascontiguousarray(A.indices, dtype=np.int32)
+    L = _lib.lib()
+    hh = ctypes.c_void_p()
+    _lib.check(L.riga_symbolic_analyze(A.shape[0], _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(perm), ctypes.byref(hh)))
+    try:
+        out = []
+        for handle in (dev.handle, hh):
+            cnt = ctypes.c_int64()
+            _lib.check(L.riga_symbolic_asm_map(handle, ctypes.byref(cnt), None, None, None))
+            st = np.zeros(16, dtype=np.int64)
+            _lib.check(L.riga_symbolic_stats(handle, _lib.ptr(st)))
+            ptr = np.zeros(st[2] + 1, dtype=np.int64)
+            slot = np.zeros(cnt.value, dtype=np.int32)
+            loc = np.zeros(cnt.value, dtype=np.int32)
+            _lib.check(L.riga_symbolic_asm_map(handle, ctypes.byref(cnt), _lib.ptr(ptr), _lib.ptr(slot), _lib.ptr(loc)))
+            out.append((cnt.value, ptr, slot, loc))
+        assert out[0][0] == out[1][0] == (A.nnz + A.shape[0]) // 2
+        for a, b in zip(out[0][1:], out[1][1:]):
+            assert np.array_equal(a, b)
+    finally:
+        L.riga_symbolic_destroy(hh)
+
+
 @pytest.mark.parametrize("d,ne,p,lv", [(1, 16, 2, 0), (2, 8, 3, 1), (3, 4, 2, 1), (2, 16, 2, 0)])
 def test_small_assembly_bit_identical(golden, d, ne, p, lv):
     g = golden["systems"][f"s{d}_{ne}_{p}_{lv}"]
