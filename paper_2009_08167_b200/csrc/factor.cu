@@ -133,6 +133,10 @@ __global__ void __launch_bounds__(256) k_extend_add(SymDev S, const int32_t* __r
 // ---------------------------------------------------------------------------
 // Small fronts: whole front in shared memory (column-major, odd ld).
 // ---------------------------------------------------------------------------
+#ifndef RIGA_SF_PANEL
+#define RIGA_SF_PANEL 8
+#endif
+constexpr int kSfPanel = RIGA_SF_PANEL;  // pivots per panel of k_small_front
 __global__ void __launch_bounds__(256) k_small_front(SymDev S, const int32_t* __restrict__ nodes,
                                                      const double* __restrict__ K,
                                                      const double* __restrict__ M, double sigma,
@@ -146,8 +150,7 @@ __global__ void __launch_bounds__(256) k_small_front(SymDev S, const int32_t* __
   const int f = (int)S.front[s], np = (int)S.ncol[s], nu = f - np;
   const int ld = f | 1;
   const int64_t col0 = S.col0[s];
-  double* lb0 = F + f * ld;
-  double* lb1 = lb0 + f;
+  double* lb0 = F + f * ld;  // 2 x kSfPanel x f: the scaled pivot columns of two panels
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
   for (int i = tid; i < f * ld; i += blockDim.x) F[i] = 0.0;
   __syncthreads();
@@ -172,23 +175,56 @@ __global__ void __launch_bounds__(256) k_small_front(SymDev S, const int32_t* __
   const double tv = tol[1];
   int neg = 0;
   int64_t bad = INT64_MAX;
-  for (int k = 0; k < np; ++k) {
-    double* lb = (k & 1) ? lb1 : lb0;
-    const double d = F[k * ld + k];
-    if (tid == 0) {
-      D[col0 + k] = d;
-      if (d < 0.0) neg++;
-      if (fabs(d) < tv && bad == INT64_MAX) bad = col0 + k;
+  // Right-looking LDL^T in panels of kSfPanel pivots: inside a panel each pivot updates only the panel's
+  // remaining columns; the columns to its right then take the panel's kSfPanel rank-1 updates in one pass
+  // (one load and one store of an entry per panel instead of per pivot, the same fused multiply-adds in the
+  // same order: the factor is bitwise that of the pivot-by-pivot loop).  Two panel buffers of scaled columns,
+  // so a panel's write-back overlaps the next panel's first pivot.
+  for (int k0 = 0, pb = 0; k0 < np; k0 += kSfPanel, pb ^= 1) {
+    const int pw = min(kSfPanel, np - k0);
+    double* lbp = lb0 + pb * kSfPanel * f;
+    for (int q = 0; q < pw; ++q) {
+      const int k = k0 + q;
+      double* lb = lbp + q * f;
+      const double d = F[k * ld + k];
+      if (tid == 0) {
+        D[col0 + k] = d;
+        if (d < 0.0) neg++;
+        if (fabs(d) < tv && bad == INT64_MAX) bad = col0 + k;
+      }
+      for (int i = k + 1 + tid; i < f; i += blockDim.x) lb[i] = F[k * ld + i] / d;
+      __syncthreads();
+      const int j = k + 1 + w;  // the panel's remaining columns (at most kSfPanel - 1 warps busy)
+      if (j < k0 + pw) {
+        const double cj = F[k * ld + j];
+        double* Fj = F + j * ld;
+        for (int i = j + lane; i < f; i += 32) Fj[i] -= lb[i] * cj;
+      }
+      if (q + 1 < pw) __syncthreads();
     }
-    for (int i = k + 1 + tid; i < f; i += blockDim.x) lb[i] = F[k * ld + i] / d;
-    __syncthreads();
-    for (int j = k + 1 + w; j < f; j += nw) {
-      const double cj = F[k * ld + j];
+    for (int j = k0 + pw + w; j < f; j += nw) {
+      double c[kSfPanel];
+#pragma unroll
+      for (int q = 0; q < kSfPanel; ++q) c[q] = q < pw ? F[(k0 + q) * ld + j] : 0.0;
       double* Fj = F + j * ld;
-      for (int i = j + lane; i < f; i += 32) Fj[i] -= lb[i] * cj;
+      if (pw == kSfPanel) {
+        for (int i = j + lane; i < f; i += 32) {
+          double x = Fj[i];
+#pragma unroll
+          for (int q = 0; q < kSfPanel; ++q) x -= lbp[q * f + i] * c[q];
+          Fj[i] = x;
+        }
+      } else {
+        for (int i = j + lane; i < f; i += 32) {
+          double x = Fj[i];
+          for (int q = 0; q < pw; ++q) x -= lbp[q * f + i] * c[q];
+          Fj[i] = x;
+        }
+      }
     }
     __syncthreads();
-    for (int i = k + 1 + tid; i < f; i += blockDim.x) F[k * ld + i] = lb[i];
+    for (int q = 0; q < pw; ++q)
+      for (int i = k0 + q + 1 + tid; i < f; i += blockDim.x) F[(k0 + q) * ld + i] = lbp[q * f + i];
   }
   __syncthreads();
   if (tid == 0) {
@@ -866,7 +902,7 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       int64_t cnt = P.cls_begin[c + 1] - P.cls_begin[c];
       if (!cnt) continue;
       int fm = P.cls_f[c];
-      size_t smem = (size_t)fm * (fm | 1) * 8 + 2 * (size_t)fm * 8;
+      size_t smem = (size_t)fm * (fm | 1) * 8 + 2 * kSfPanel * (size_t)fm * 8;
       k_small_front<<<(unsigned)cnt, 256, smem, st>>>(S, sym->d_level_nodes.p + P.cls_begin[c], Kv,
                                                        Mv, sigma, F->tol.p, F->panel.p, cbuf,
                                                        F->D.p, F->stat.p); count_launch();
