@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) k_extend_add(SymDev S, const int32_t* __r
 #define RIGA_SF_PANEL 8
 #endif
 constexpr int kSfPanel = RIGA_SF_PANEL;  // pivots per panel of k_small_front
-__global__ void __launch_bounds__(256) k_small_front(SymDev S, const int32_t* __restrict__ nodes,
+__global__ void __launch_bounds__(512) k_small_front(SymDev S, const int32_t* __restrict__ nodes,
                                                      const double* __restrict__ K,
                                                      const double* __restrict__ M, double sigma,
                                                      const double* __restrict__ tol,
@@ -903,7 +903,10 @@ static int numeric(riga_factor* F, cudaStream_t st, const double* Kv, const doub
       if (!cnt) continue;
       int fm = P.cls_f[c];
       size_t smem = (size_t)fm * (fm | 1) * 8 + 2 * kSfPanel * (size_t)fm * 8;
-      k_small_front<<<(unsigned)cnt, 256, smem, st>>>(S, sym->d_level_nodes.p + P.cls_begin[c], Kv,
+      // a class whose fronts take an SM's shared memory alone (> 113 KB) runs 16 warps per front instead of 8
+      // (cfg3: 17 concurrent factorizations 41.5 -> 35.1 ms; 32 warps: no further gain)
+      const unsigned nthr = fm >= 113 ? 512 : 256;
+      k_small_front<<<(unsigned)cnt, nthr, smem, st>>>(S, sym->d_level_nodes.p + P.cls_begin[c], Kv,
                                                        Mv, sigma, F->tol.p, F->panel.p, cbuf,
                                                        F->D.p, F->stat.p); count_launch();
       RIGA_CUDA(cudaGetLastError());
