@@ -69,8 +69,9 @@ class DeviceSystem:
             bv = np.zeros_like(av)
         else:
             B = B if isinstance(B, sp.csr_array) else sp.csr_array(B)
-            B.sort_indices()
-            same = B.indptr is A.indptr and B.indices is A.indices  # one pattern object
+            same = B.indptr is A.indptr and B.indices is A.indices  # one pattern object (sorted with A)
+            if not same:
+                B.sort_indices()
             if not same and not (np.array_equal(B.indptr, A.indptr) and np.array_equal(B.indices, A.indices)):
                 raise ValueError("K and M must share one sparsity pattern")
             bv = np.ascontiguousarray(B.data, dtype=np.float64)

@@ -1655,11 +1655,20 @@ int riga_lanczos_dcgs_probe(riga_lanczos* lz, const double* w, int64_t* rows) {
   RIGA_TRY(push_state(lz, lz->k, lz->k, 0.0));  // steps = 0: no beta correction
   const int64_t Rmax = lz->max_dim + 1 + lz->cap;
   if (rows) *rows = lz->k + 1 + lz->nlocked;
+  // events around the two sweeps alone (riga_lanczos_last_extend_ms reads them): the state upload above is
+  // not part of the step's sweeps
+  if (!lz->ev0) {
+    RIGA_CUDA(cudaEventCreate(&lz->ev0));
+    RIGA_CUDA(cudaEventCreate(&lz->ev1));
+  }
+  RIGA_CUDA(cudaEventRecord(lz->ev0, s));
   RIGA_CUDA(launch(k_dcgs_dots, dcgs_dot_grid(), 256, 0, s, sel_basis(lz, true, 1), lz->st.p, lz->n, Rmax, lz->V.p, w,
                    lz->partial.p, lz->coef.p, lz->tk_dots.p));
   const dim3 gu((unsigned)((lz->n + kUpdCols - 1) / kUpdCols), kUpdGroups);
   RIGA_CUDA(launch(k_dcgs_upd, gu, 256, 0, s, sel_basis(lz, false, 1), lz->st.p, lz->n, lz->ld, Rmax, lz->coef.p,
                    lz->upart.p, w, lz->vt.p, lz->r.p, lz->tk_upd.p, lz->cpl.p));
+  RIGA_CUDA(cudaEventRecord(lz->ev1, s));
+  lz->ev_valid = true;
   count_launch(2);
   return RIGA_OK;
 }
