@@ -56,6 +56,15 @@ def test_device_separator_ordering_equals_reference(golden, name):
     assert np.array_equal(P.separator_ordering(host), perm)
 
 
+@pytest.mark.parametrize("d,ne,p,lv", [(1, 16, 2, 0), (1, 32, 3, 1), (2, 8, 2, 0), (2, 8, 3, 1), (3, 4, 2, 1), (2, 16, 2, 0)])
+def test_device_separator_ordering_small_systems(golden_arrays, d, ne, p, lv):
+    """Device-written permutation on the small systems of the CPU test (1D, 2D and 3D, with and without C0
+    lines): equal to the reference's recorded ordering."""
+    s = P.build_system(d, ne, p, lv)
+    assert s.device is not None
+    np.testing.assert_array_equal(P.separator_ordering(s), golden_arrays[f"s{d}_{ne}_{p}_{lv}/perm"])
+
+
 @pytest.mark.parametrize("cfg", [(2, 16, 2, 0), (2, 64, 3, 3), (3, 8, 2, 1), (2, 256, 4, 4), (3, 32, 2, 2)])
 def test_device_scatter_map_equals_host_analysis(cfg):
     """The scatter map of the original entries into the fronts (symbolic.cpp 5d on the host) is built by device
