@@ -73,6 +73,11 @@ struct DevBuf {
     n = count;
     return RIGA_OK;
   }
+  // grow-only: keeps the buffer when it already holds `count` elements of this stream
+  int reserve(size_t count, cudaStream_t stream) {
+    if (p && n >= count && s == stream) return RIGA_OK;
+    return alloc(count, stream);
+  }
   int upload(const T* host, size_t count, cudaStream_t st) {
     int rc = alloc(count, st);
     if (rc) return rc;

@@ -924,6 +924,7 @@ struct riga_lanczos {
   int64_t nlocked = 0, cap = 0;
   DevBuf<double> V, MV, L, LM, w, r, Mr, bp, coef, partial, upart, cpl, Wd, outs, dscratch;
   DevBuf<double> vt, mvt;            // finished direction of the delayed pass and its M product
+  DevBuf<double> lk_part, lk_C, lk_G, lk_nrm, lk_Xt, lk_MXt;  // scratch of riga_lanczos_lock_block (grow-only)
   bool delayed = true;               // delayed CGS2 step (RIGA_CGS=classic: two passes per step)
   DevBuf<unsigned> tk_dots, tk_upd;  // last-block tickets of the Gram-Schmidt kernels (self-resetting)
   DevBuf<double> kt1, kt2;           // scratch of the Kronecker mass product
@@ -1435,7 +1436,7 @@ int mdots(riga_lanczos* lz, const double* A, int R, const double* X, int c, doub
   if (R == 0 || c == 0) return RIGA_OK;
   if (g_lift_dmma) {
     const int nz = (int)((lz->n + kMKChunk - 1) / kMKChunk);
-    RIGA_TRY(part.alloc((int64_t)nz * R * c, s));
+    RIGA_TRY(part.reserve((int64_t)nz * R * c, s));
     const dim3 g((unsigned)((R + 63) / 64), (unsigned)((c + 63) / 64), (unsigned)nz);
     k_mdots_dmma<<<g, 128, 0, s>>>(A, lz->ld, R, X, lz->ld, c, lz->n, part.p);
     k_mred<<<(unsigned)(((int64_t)R * c + 255) / 256), 256, 0, s>>>(nz, R, c, part.p, C);
@@ -1444,7 +1445,7 @@ int mdots(riga_lanczos* lz, const double* A, int R, const double* X, int c, doub
     return RIGA_OK;
   }
   const int nchunk = (int)((lz->n + kMChunk - 1) / kMChunk);
-  RIGA_TRY(part.alloc((int64_t)nchunk * R * c, s));
+  RIGA_TRY(part.reserve((int64_t)nchunk * R * c, s));
   const dim3 g(nchunk, (unsigned)((R + 31) / 32), (unsigned)((c + 7) / 8));
   k_mdots<<<g, 256, 8 * 1024 * 8, s>>>(A, lz->ld, R, X, lz->ld, c, lz->n, part.p);
   k_mred<<<(unsigned)(((int64_t)R * c + 255) / 256), 256, 0, s>>>(nchunk, R, c, part.p, C);
@@ -1487,12 +1488,13 @@ int riga_lanczos_lock_block(riga_lanczos* lz, double* X, double* MX, int64_t c, 
     attr = 1;
   }
   const int nl = (int)lz->nlocked, cc = (int)c;
-  DevBuf<double> part, C, G, nrm, Xt, MXt;
-  RIGA_TRY(C.alloc(std::max<int64_t>((int64_t)nl * cc, 1), s));
-  RIGA_TRY(G.alloc((int64_t)cc * cc, s));
-  RIGA_TRY(nrm.alloc(cc, s));
-  RIGA_TRY(Xt.alloc(c * lz->ld, s));
-  RIGA_TRY(MXt.alloc(c * lz->ld, s));
+  // scratch kept on the state (grow-only): no stream-ordered allocations inside a slice's lock phase
+  DevBuf<double>&part = lz->lk_part, &C = lz->lk_C, &G = lz->lk_G, &nrm = lz->lk_nrm, &Xt = lz->lk_Xt, &MXt = lz->lk_MXt;
+  RIGA_TRY(C.reserve(std::max<int64_t>((int64_t)nl * cc, 1), s));
+  RIGA_TRY(G.reserve((int64_t)cc * cc, s));
+  RIGA_TRY(nrm.reserve(cc, s));
+  RIGA_TRY(Xt.reserve(c * lz->ld, s));
+  RIGA_TRY(MXt.reserve(c * lz->ld, s));
   const dim3 gs((unsigned)((lz->n + 255) / 256), (unsigned)cc);
   // M-normalise the lifted vectors (ref: x /= sqrt(x.Mx))
   k_rowdots<<<cc, 256, 0, s>>>(X, MX, lz->ld, lz->n, nrm.p);
@@ -1709,7 +1711,8 @@ int riga_lanczos_bytes(riga_lanczos* lz, int64_t* bytes) {
   RIGA_CHECK_ARG(lz && bytes, "null arg");
   const DevBuf<double>* bufs[] = {&lz->V, &lz->MV, &lz->L, &lz->LM, &lz->w, &lz->r, &lz->Mr, &lz->bp, &lz->coef,
                                   &lz->partial, &lz->upart, &lz->cpl, &lz->Wd, &lz->outs, &lz->dscratch, &lz->vt,
-                                  &lz->mvt, &lz->kt1, &lz->kt2};
+                                  &lz->mvt, &lz->kt1, &lz->kt2, &lz->lk_part, &lz->lk_C, &lz->lk_G, &lz->lk_nrm,
+                                  &lz->lk_Xt, &lz->lk_MXt};
   int64_t b = 0;
   for (const DevBuf<double>* d : bufs) b += (int64_t)d->n * 8;
   *bytes = b;
